@@ -1,0 +1,166 @@
+/*
+ * ivfkm.h — C ABI of the B200 (sm_100a) IVF spherical k-means Lloyd path.
+ *
+ * Drop-in boundary for the hot path of arXiv 2002.09094's reference package
+ * `sparse_kmeans` (/root/reference/pkg/src/sparse_kmeans).  Plain pointers,
+ * sizes and a cudaStream_t; no torch types.  Every entry point returns 0 on
+ * success, a positive cudaError_t, or a negative IVFKM_E_* code
+ * (ivfkm_error_string() names it).  [dev] marks device pointers, [host] host
+ * pointers.  Ids on the device are 0-based; the reference's 1-based ids are
+ * converted only by the host-buffer entry point ivfkm_assign_ivf_host().
+ *
+ * Reference interfaces replaced (file:line under /root/reference/pkg/src/sparse_kmeans):
+ *   ivfkm_assign_ivf_host   <- _kernels.pyx:106-128  assign_ivf(indptr, terms, vals,
+ *                              m_indptr, m_cids, m_vals, rho, labels, ctr): the
+ *                              kernel-module ABI that kernels.py:23-52 dispatches to
+ *   ivfkm_bivf_build        <- means.py:169-179      MeanSet.inverted (term-major postings)
+ *   ivfkm_assign            <- variants.py:162-174   assign_ivf, with _kernels.pyx:17-26
+ *                              (_argmax_label), clustering.py:105-119 (objective_cosine),
+ *                              clustering.py:286 (convergence: changed labels),
+ *                              variants.py:56-59 (Assignment sizes) and
+ *                              counters.py:71-81 (mult_volume_ivf, counted in-kernel)
+ *   ivfkm_update_count/fill <- variants.py:254-312   update_means / update_ivf
+ *   ivfkm_fnv1a64           <- variants.py:77-83     fnv1a64 (assignment digest)
+ *   ivfkm_synth_*           <- no reference counterpart: seeded stand-ins for the
+ *                              BASELINE.json configs (PubMed/NYT are not offline)
+ */
+#ifndef IVFKM_H
+#define IVFKM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* ivfkm_stream_t; /* == cudaStream_t */
+
+#define IVFKM_OK 0
+#define IVFKM_E_ARG (-1)         /* bad argument / shape                         */
+#define IVFKM_E_UNSUPPORTED (-2) /* e.g. k beyond the largest cluster split      */
+#define IVFKM_E_CAPACITY (-3)    /* caller output buffer too small               */
+#define IVFKM_E_WORKSPACE (-4)   /* workspace smaller than *_workspace_size()    */
+#define IVFKM_E_NOGPU (-5)       /* no CUDA device visible                       */
+#define IVFKM_E_RANGE (-6)       /* an id outside its range (CorruptionError)    */
+
+#define IVFKM_OBJ_LIMBS 34 /* 32-bit limbs of the exact objective accumulator  */
+#define IVFKM_MAXC 32      /* near-tie candidates rescored per object in fp64   */
+
+/* Per-iteration device-side statistics; ivfkm_assign() zeroes them. */
+typedef struct ivfkm_stats {
+  unsigned long long postings;  /* V = sum_i sum_h nc_{t(i,h)} (counters.py:71-81)  */
+  unsigned long long changed;   /* labels != prev_labels (clustering.py:286)        */
+  unsigned long long near_ties; /* objects whose fp32 window held >1 candidate      */
+  unsigned long long overflow;  /* of those, more than IVFKM_MAXC candidates        */
+  unsigned long long queue_len; /* internal: rescoring queue length                 */
+  unsigned long long obj_flags; /* nonzero: a similarity fell outside |s| < 8       */
+  long long obj_limbs[IVFKM_OBJ_LIMBS]; /* exact sum of sims; limb l weighs 2^(32l-1074) */
+} ivfkm_stats;
+
+const char* ivfkm_error_string(int code);
+int ivfkm_version(void);
+int ivfkm_device_count(void);
+
+/* ---- bitmap-block inverted file (BIVF) of the means ---------------------
+ * headers[2*(t*nblk + b) + 0] = mask: bit j set <=> mean 32*b+j holds term t;
+ * headers[2*(t*nblk + b) + 1] = offset: that mean's value sits at
+ *   val[offset + popc(mask & ((1u<<j)-1))].
+ * Values are stored term-major, mean ascending — the order of
+ * MeanSet.inverted (means.py:169-179).  val32 feeds the fp32 screening pass,
+ * val64 the exact fp64 rescoring.                                            */
+int64_t ivfkm_bivf_nblk(int64_t k); /* 32-mean blocks per term, padded */
+size_t ivfkm_bivf_workspace_size(int64_t dim, int64_t k);
+/* major = 0: rows of (ptr, cols) are means (mean-major CSR, cols = terms);
+ * major = 1: rows are terms (term-major IVF, cols = mean ids).  0-based ids;
+ * an id outside [0,k) / [0,dim) gives IVFKM_E_RANGE.                        */
+int ivfkm_bivf_build(int64_t k, int64_t dim, int major, int64_t nrows,
+                     const int64_t* ptr /*[dev] nrows+1*/, const int32_t* cols /*[dev]*/,
+                     const double* vals /*[dev]*/, uint32_t* headers /*[dev] 2*dim*nblk*/,
+                     float* val32 /*[dev] nnz*/, double* val64 /*[dev] nnz*/, void* ws,
+                     size_t ws_bytes, ivfkm_stream_t stream);
+
+/* ---- assignment step ------------------------------------------------------
+ * For every object i: rho_i[c] = sum_h x_{i,h} mu_c[t_h] screened in fp32
+ * (registers, fixed order), every mean within the rigorous fp32 error window
+ * of the best rescored in fp64 in the reference's summation order, label =
+ * argmax with the smallest index winning ties (_kernels.pyx:17-26).  Also
+ * writes the per-object similarity to the chosen mean (the objective's
+ * summand), counts changed labels vs prev_labels, histograms sizes, and
+ * accumulates the exact objective into stats->obj_limbs.                      */
+size_t ivfkm_assign_workspace_size(int64_t n_obj, int64_t k);
+/* Tuning: rowcap = row entries staged in shared memory per pass (default 1024;
+ * longer rows run in several passes), smem_limit = shared-memory budget per
+ * CTA in bytes (default 225 KB, min 1 KB; a smaller budget forces the thread-block
+ * cluster split).  Out-of-range values leave the setting unchanged.         */
+void ivfkm_set_tuning(int rowcap, int smem_limit);
+int ivfkm_assign(int64_t n_obj, const int64_t* row_ptr /*[dev] n+1*/,
+                 const int32_t* terms /*[dev]*/, const float* val32 /*[dev]*/,
+                 const double* val64 /*[dev]*/, const double* xnorm /*[dev] n or NULL (=1)*/,
+                 int64_t k, int64_t dim, const uint32_t* headers /*[dev]*/,
+                 const float* pval32 /*[dev]*/, const double* pval64 /*[dev]*/, double mu_max,
+                 const int32_t* prev_labels /*[dev] n or NULL*/, int32_t* labels /*[dev] n*/,
+                 double* sims /*[dev] n*/, unsigned long long* sizes /*[dev] k*/,
+                 ivfkm_stats* stats /*[dev]*/, void* ws, size_t ws_bytes,
+                 ivfkm_stream_t stream);
+
+/* Exact float64 similarity of every object to the mean its (0-based) label
+ * names — the summand of objective_cosine (clustering.py:105-119) — written
+ * to sims, with the exact sum accumulated into stats->obj_limbs (stats is
+ * zeroed first).                                                            */
+int ivfkm_score_labels(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
+                       const double* val64, int64_t k, int64_t dim, const uint32_t* headers,
+                       const double* pval64, const int32_t* labels, double* sims,
+                       ivfkm_stats* stats, ivfkm_stream_t stream);
+
+/* ---- update step (variants.py:254-312), bit-identical to the reference ---
+ * count: sort member entries by (cluster, term) keeping object order, sum
+ * each (cluster, term) run in float64 in ascending object order, divide by
+ * the cluster size, take numpy's pairwise sum of squares for the norm, and
+ * write new_ptr[0..k] (new_ptr[k] = total nonzeros).  Empty clusters keep
+ * their previous mean (retained).  fill: write the mean-major CSR.
+ * The workspace must be the same buffer for the count and fill calls.       */
+size_t ivfkm_update_workspace_size(int64_t n_obj, int64_t nnz, int64_t k, int64_t dim);
+int ivfkm_update_count(int64_t n_obj, int64_t nnz, const int64_t* row_ptr,
+                       const int32_t* terms, const double* val64, int64_t k, int64_t dim,
+                       const int32_t* labels /*[dev] 0-based*/,
+                       const unsigned long long* sizes /*[dev] k*/,
+                       const int64_t* prev_ptr /*[dev] k+1*/, int64_t* new_ptr /*[dev] k+1*/,
+                       void* ws, size_t ws_bytes, ivfkm_stream_t stream);
+int ivfkm_update_fill(int64_t n_obj, int64_t nnz, int64_t k, int64_t dim,
+                      const unsigned long long* sizes, const int64_t* prev_ptr,
+                      const int32_t* prev_terms, const double* prev_vals,
+                      const int64_t* new_ptr, int32_t* new_terms /*[dev]*/,
+                      double* new_vals /*[dev]*/, uint8_t* retained /*[dev] k*/,
+                      int64_t capacity, void* ws, size_t ws_bytes, ivfkm_stream_t stream);
+
+/* ---- host-buffer drop-in for _kernels.pyx:106-128 --------------------------
+ * Same arguments and meaning as the reference kernel: 1-based term / mean
+ * ids, float64 values, labels written 1-based, ctr[0..2] += postings touched.
+ * Copies host->device, runs the BIVF build + assign on the current device,
+ * copies labels back.  Returns IVFKM_E_RANGE for an out-of-range id.          */
+int ivfkm_assign_ivf_host(int64_t n, const int64_t* indptr, const int32_t* terms,
+                          const double* vals, int64_t dim, const int64_t* m_indptr,
+                          const int32_t* m_cids, const double* m_vals, int64_t k,
+                          int32_t* labels, int64_t* ctr);
+
+/* ---- host utilities -------------------------------------------------------*/
+uint64_t ivfkm_fnv1a64(const void* data, size_t nbytes); /* variants.py:77-83 */
+
+typedef struct ivfkm_synth_spec {
+  int64_t n, dim;
+  int32_t nnz_kind; /* 0 = Poisson(nnz_mean), 1 = lognormal(mean, sigma) */
+  double nnz_mean, nnz_sigma;
+  int64_t nnz_lo, nnz_hi;
+  double zipf_s;
+  int64_t seed;
+} ivfkm_synth_spec;
+int ivfkm_synth_rows(const ivfkm_synth_spec* spec, int64_t* nnz_rows /*[host] n*/);
+int ivfkm_synth_fill(const ivfkm_synth_spec* spec, const int64_t* cap_ptr /*[host] n+1*/,
+                     int64_t* indptr, int32_t* terms, double* vals, int64_t* n_out,
+                     int64_t* nnz_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,708 @@
+// Assignment step of IVF spherical k-means on sm_100a.
+//
+// Reference semantics (file:line under /root/reference/pkg/src/sparse_kmeans):
+//   _kernels.pyx:106-128  for each object i: rho[0..k) = 0; for each nonzero
+//                         (t, v) in row order, for each mean posting (c, u) of
+//                         term t: rho[c] += v * u  (float64, mul then add);
+//   _kernels.pyx:17-26    label = argmax, strict '>' from -inf, so the
+//                         smallest index among maximizers wins;
+//   clustering.py:105-119 objective = fsum_i sum_h v_h * mu_{a(i)}[t_h]
+//                         (= rho_i[a(i)] bit for bit: same products, same order);
+//   clustering.py:286     convergence = labels unchanged;
+//   variants.py:56-59     sizes = bincount(labels).
+//
+// B200 design:
+//   1. screen (fp32, registers): one CTA (or a thread-block cluster of CTAs
+//      when k outgrows one SM's shared memory) per object.  Lane `l` of a warp
+//      owns means 32*b + l of RR consecutive 32-mean blocks b and accumulates
+//      rho in registers: for each object nonzero the warp loads the RR block
+//      headers of the term (one coalesced 8*RR-byte load), and each lane whose
+//      mask bit is set loads its value at offset + popc(mask below the lane).
+//      No shared-memory scatter, no bank conflicts, no atomics, fixed FMA order.
+//      Finished spans are parked in shared memory (cluster: distributed
+//      shared memory) for the block argmax.
+//   2. window: |rho32 - rho64| <= eps_i is a rigorous bound (n_i+3 roundings
+//      of size 2^-24 on a sum bounded by |x_i| * max|mu|), so the reference
+//      winner is within 2*eps_i of the fp32 max.  A single candidate is
+//      certified; several are queued for exact rescoring.
+//   3. finalize (fp64, one warp per object): rescore the candidates (or the
+//      certified winner, whose similarity is the objective summand) with
+//      __dmul_rn/__dadd_rn in the reference's h order — bit-identical to the
+//      reference's float64 rho — pick the max with the smallest index.
+//   4. accumulate: changed labels, sizes, and the exact objective (a
+//      fixed-point superaccumulator, so the host can round the exact sum once,
+//      like math.fsum).
+#include <cooperative_groups.h>
+
+#include <cfloat>
+#include <climits>
+#include <cmath>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+using namespace ivfkm;
+
+namespace {
+
+constexpr int kMaxC = IVFKM_MAXC;
+constexpr int kLimbs = IVFKM_OBJ_LIMBS;
+constexpr int kMaxSplit = 8;           // portable cluster size
+constexpr int kSmemLimit = 227 * 1024;  // opt-in dynamic shared memory per CTA
+
+struct ScreenParams {
+  int64_t n_obj;
+  const int64_t* row_ptr;
+  const int32_t* terms;
+  const float* val32;
+  const double* xnorm;
+  int64_t k;
+  int64_t nblk;
+  const uint2* hdr;
+  const float* pv32;
+  double mu_max;
+  int cta_blocks;  // 32-mean blocks held by one CTA (multiple of RR)
+  int nsplit;      // CTAs per object (cluster size)
+  int rowcap;      // row entries staged in shared memory per pass
+  int32_t* label32;
+  int32_t* slot_of;
+  int32_t* q_obj;
+  int32_t* q_cnt;
+  int32_t* q_cid;
+  ivfkm_stats* stats;
+};
+
+struct ScreenShared {
+  float red_v[32];
+  int red_c[32];
+  unsigned long long red_p[32];
+  float best_v;
+  int best_c;
+  int cnt;
+  int cand[kMaxC];
+  unsigned long long post;
+};
+
+__device__ __forceinline__ void better(float& bv, int& bc, float ov, int oc) {
+  if (ov > bv || (ov == bv && oc < bc)) {
+    bv = ov;
+    bc = oc;
+  }
+}
+
+template <int RR>
+__global__ void __launch_bounds__(512) screen_kernel(ScreenParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ ScreenShared sh;
+  float* rho = reinterpret_cast<float*>(smem);
+  const int cta_cids = p.cta_blocks * 32;
+  int32_t* s_term = reinterpret_cast<int32_t*>(rho + cta_cids);
+  float* s_val = reinterpret_cast<float*>(s_term + p.rowcap);
+
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int z = blockIdx.x % p.nsplit;
+  const int64_t obj = blockIdx.x / p.nsplit;
+  if (obj >= p.n_obj) return;  // whole cluster shares obj
+  const int64_t rb = p.row_ptr[obj], re = p.row_ptr[obj + 1];
+  const int64_t blk0 = (int64_t)z * p.cta_blocks;
+  const int nspans = p.cta_blocks / RR;
+  const unsigned lt = (1u << lane) - 1u;
+  unsigned long long post = 0;
+
+  int64_t c0 = rb;
+  do {
+    const int64_t rem = re - c0;
+    const int cn = (int)(rem < p.rowcap ? rem : p.rowcap);
+    __syncthreads();
+    for (int j = threadIdx.x; j < cn; j += blockDim.x) {
+      s_term[j] = p.terms[c0 + j];
+      s_val[j] = p.val32[c0 + j];
+    }
+    __syncthreads();
+    const bool first = (c0 == rb);
+    for (int sp = warp; sp < nspans; sp += nwarps) {
+      const int64_t gb = blk0 + (int64_t)sp * RR;
+      float acc[RR];
+#pragma unroll
+      for (int r = 0; r < RR; ++r) acc[r] = first ? 0.f : rho[(sp * RR + r) * 32 + lane];
+      const bool hl = lane < RR && (gb + lane) < p.nblk;
+      const uint2* hrow = p.hdr + gb + lane;
+      auto ldh = [&](int e) -> uint2 {
+        uint2 h = make_uint2(0u, 0u);
+        if (hl && e < cn) h = __ldg(hrow + (int64_t)s_term[e] * p.nblk);
+        return h;
+      };
+      uint2 hA = ldh(0), hB = ldh(1);
+      for (int e = 0; e < cn; e += 2) {
+        const uint2 hC = ldh(e + 2), hD = ldh(e + 3);
+        const float vA = s_val[e];
+        const float vB = (e + 1 < cn) ? s_val[e + 1] : 0.f;
+        float uA[RR], uB[RR];
+#pragma unroll
+        for (int r = 0; r < RR; ++r) {
+          const unsigned m = __shfl_sync(kFull, hA.x, r);
+          const unsigned o = __shfl_sync(kFull, hA.y, r);
+          uA[r] = ((m >> lane) & 1u) ? __ldg(p.pv32 + o + __popc(m & lt)) : 0.f;
+          post += __popc(m);
+        }
+#pragma unroll
+        for (int r = 0; r < RR; ++r) {
+          const unsigned m = __shfl_sync(kFull, hB.x, r);
+          const unsigned o = __shfl_sync(kFull, hB.y, r);
+          uB[r] = ((m >> lane) & 1u) ? __ldg(p.pv32 + o + __popc(m & lt)) : 0.f;
+          post += __popc(m);
+        }
+        // fma(v, 0, acc) == acc exactly, so absent postings cost no rounding.
+#pragma unroll
+        for (int r = 0; r < RR; ++r) acc[r] = fmaf(vA, uA[r], acc[r]);
+#pragma unroll
+        for (int r = 0; r < RR; ++r) acc[r] = fmaf(vB, uB[r], acc[r]);
+        hA = hC;
+        hB = hD;
+      }
+#pragma unroll
+      for (int r = 0; r < RR; ++r) rho[(sp * RR + r) * 32 + lane] = acc[r];
+    }
+    c0 += p.rowcap;
+  } while (c0 < re);
+  __syncthreads();
+
+  // ---- CTA-local argmax (value desc, index asc) and postings total ----
+  float bv = -INFINITY;
+  int bc = INT_MAX;
+  const int64_t cid0 = blk0 * 32;
+  for (int j = threadIdx.x; j < cta_cids; j += blockDim.x) {
+    const int64_t cid = cid0 + j;
+    if (cid >= p.k) break;
+    const float v = rho[j];
+    if (v > bv) {
+      bv = v;
+      bc = (int)cid;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const float ov = __shfl_xor_sync(kFull, bv, off);
+    const int oc = __shfl_xor_sync(kFull, bc, off);
+    better(bv, bc, ov, oc);
+  }
+  // every lane counted the same warp-uniform masks: keep lane 0's tally
+  if (lane == 0) {
+    sh.red_v[warp] = bv;
+    sh.red_c[warp] = bc;
+    sh.red_p[warp] = post;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    float v = lane < nwarps ? sh.red_v[lane] : -INFINITY;
+    int c = lane < nwarps ? sh.red_c[lane] : INT_MAX;
+    unsigned long long q = lane < nwarps ? sh.red_p[lane] : 0ull;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      better(v, c, __shfl_xor_sync(kFull, v, off), __shfl_xor_sync(kFull, c, off));
+      q += __shfl_xor_sync(kFull, q, off);
+    }
+    if (lane == 0) {
+      sh.best_v = v;
+      sh.best_c = c;
+      sh.post = q;
+      sh.cnt = 0;
+      if (q) atomicAdd(&p.stats->postings, q);
+    }
+  }
+
+  cg::cluster_group cluster = cg::this_cluster();
+  float gv;
+  int gc;
+  unsigned long long gpost;
+  if (p.nsplit > 1) {
+    cluster.sync();
+    gv = -INFINITY;
+    gc = INT_MAX;
+    gpost = 0;
+    for (int q = 0; q < p.nsplit; ++q) {
+      const ScreenShared* o = cluster.map_shared_rank(&sh, q);
+      better(gv, gc, o->best_v, o->best_c);
+      gpost += o->post;
+    }
+  } else {
+    __syncthreads();
+    gv = sh.best_v;
+    gc = sh.best_c;
+    gpost = sh.post;
+  }
+
+  // ---- rigorous fp32 window and candidate collection ----
+  const int64_t n_i = re - rb;
+  const double xn = p.xnorm ? p.xnorm[obj] : 1.0;
+  const double eps = ((double)(n_i + 3) * 0x1p-24 + (double)n_i * 0x1p-50) * xn * p.mu_max *
+                         (1.0 + 1e-6) +
+                     (double)(n_i + 1) * 0x1p-125;
+  const double thr = (double)gv - 2.0 * eps;
+  if (gpost != 0) {
+    for (int j = threadIdx.x; j < cta_cids; j += blockDim.x) {
+      const int64_t cid = cid0 + j;
+      if (cid >= p.k) break;
+      if ((double)rho[j] >= thr) {
+        const int s = atomicAdd(&sh.cnt, 1);
+        if (s < kMaxC) sh.cand[s] = (int)cid;
+      }
+    }
+  }
+  if (p.nsplit > 1) cluster.sync(); else __syncthreads();
+
+  if (z == 0 && threadIdx.x == 0) {
+    int total = 0;
+    if (p.nsplit > 1) {
+      for (int q = 0; q < p.nsplit; ++q) total += cluster.map_shared_rank(&sh, q)->cnt;
+    } else {
+      total = sh.cnt;
+    }
+    // gpost == 0: no posting touched, every rho is exactly 0 -> label 0.
+    const int label = gpost == 0 ? 0 : gc;
+    p.label32[obj] = label;
+    if (total <= 1) {
+      p.slot_of[obj] = -1;
+    } else {
+      const int slot = (int)atomicAdd(&p.stats->queue_len, 1ull);
+      atomicAdd(&p.stats->near_ties, 1ull);
+      if (total > kMaxC) atomicAdd(&p.stats->overflow, 1ull);
+      p.slot_of[obj] = slot;
+      p.q_obj[slot] = (int)obj;
+      p.q_cnt[slot] = total;
+      int w = 0;
+      for (int q = 0; q < p.nsplit && w < kMaxC; ++q) {
+        const ScreenShared* o = p.nsplit > 1 ? cluster.map_shared_rank(&sh, q) : &sh;
+        const int cq = min(o->cnt, kMaxC);
+        for (int j = 0; j < cq && w < kMaxC; ++j) p.q_cid[(int64_t)slot * kMaxC + w++] = o->cand[j];
+      }
+    }
+  }
+  if (p.nsplit > 1) cluster.sync();  // peers keep their shared memory alive
+}
+
+// ---------------------------------------------------------------------------
+// exact float64 similarity of object rows to one mean, in the reference order
+
+struct ExactCtx {
+  const int64_t* row_ptr;
+  const int32_t* terms;
+  const double* val64;
+  int64_t nblk;
+  const uint2* hdr;
+  const double* pv64;
+};
+
+// Warp-cooperative: lanes look up 32 nonzeros at a time, then the products
+// are added serially in row order (every lane holds the same sum).
+__device__ double exact_score_warp(const ExactCtx& x, int64_t rb, int64_t re, int c, int lane) {
+  double acc = 0.0;
+  const int64_t blk = c >> 5;
+  const unsigned bit = 1u << (c & 31);
+  for (int64_t h0 = rb; h0 < re; h0 += 32) {
+    const int64_t h = h0 + lane;
+    bool present = false;
+    double prod = 0.0;
+    if (h < re) {
+      const int64_t t = x.terms[h];
+      const uint2 hd = __ldg(x.hdr + t * x.nblk + blk);
+      if (hd.x & bit) {
+        present = true;
+        prod = __dmul_rn(x.val64[h], __ldg(x.pv64 + hd.y + __popc(hd.x & (bit - 1u))));
+      }
+    }
+    unsigned pm = __ballot_sync(kFull, present);
+    while (pm) {
+      const int j = __ffs(pm) - 1;
+      pm &= pm - 1u;
+      acc = __dadd_rn(acc, __shfl_sync(kFull, prod, j));
+    }
+  }
+  return acc;
+}
+
+// One thread scores one mean over the whole row.
+__device__ double exact_score_thread(const ExactCtx& x, int64_t rb, int64_t re, int64_t c) {
+  double acc = 0.0;
+  const int64_t blk = c >> 5;
+  const unsigned bit = 1u << (c & 31);
+  for (int64_t h = rb; h < re; ++h) {
+    const int64_t t = x.terms[h];
+    const uint2 hd = __ldg(x.hdr + t * x.nblk + blk);
+    if (hd.x & bit)
+      acc = __dadd_rn(acc, __dmul_rn(x.val64[h], __ldg(x.pv64 + hd.y + __popc(hd.x & (bit - 1u)))));
+  }
+  return acc;
+}
+
+struct FinalParams {
+  int64_t n_obj;
+  ExactCtx x;
+  const int32_t* label32;
+  const int32_t* slot_of;
+  const int32_t* q_cnt;
+  const int32_t* q_cid;
+  int32_t* labels;
+  double* sims;
+  int32_t* ovf_list;
+  unsigned int* ovf_len;
+};
+
+__global__ void __launch_bounds__(256) finalize_kernel(FinalParams p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t i = blockIdx.x * wpb + (threadIdx.x >> 5); i < p.n_obj; i += gridDim.x * wpb) {
+    const int64_t rb = p.x.row_ptr[i], re = p.x.row_ptr[i + 1];
+    const int slot = p.slot_of[i];
+    if (slot < 0) {
+      const int c = p.label32[i];
+      const double s = exact_score_warp(p.x, rb, re, c, lane);
+      if (lane == 0) {
+        p.labels[i] = c;
+        p.sims[i] = s;
+      }
+      continue;
+    }
+    const int cnt = p.q_cnt[slot];
+    if (cnt > kMaxC) {
+      if (lane == 0) p.ovf_list[atomicAdd(p.ovf_len, 1u)] = (int)i;
+      continue;
+    }
+    double bv = -INFINITY;
+    int bc = INT_MAX;
+    for (int j = 0; j < cnt; ++j) {
+      const int c = p.q_cid[(int64_t)slot * kMaxC + j];
+      const double s = exact_score_warp(p.x, rb, re, c, lane);
+      if (s > bv || (s == bv && c < bc)) {
+        bv = s;
+        bc = c;
+      }
+    }
+    if (lane == 0) {
+      p.labels[i] = bc;
+      p.sims[i] = bv;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) score_labels_kernel(int64_t n_obj, ExactCtx x,
+                                                           const int32_t* labels, double* sims) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t i = blockIdx.x * wpb + (threadIdx.x >> 5); i < n_obj; i += gridDim.x * wpb) {
+    const double s = exact_score_warp(x, x.row_ptr[i], x.row_ptr[i + 1], labels[i], lane);
+    if (lane == 0) sims[i] = s;
+  }
+}
+
+// Objects whose window held more than kMaxC means: score every mean exactly.
+__global__ void __launch_bounds__(1024) overflow_kernel(FinalParams p, int64_t k) {
+  __shared__ double rv[32];
+  __shared__ int rc[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const unsigned n = *p.ovf_len;
+  for (unsigned q = blockIdx.x; q < n; q += gridDim.x) {
+    const int64_t i = p.ovf_list[q];
+    const int64_t rb = p.x.row_ptr[i], re = p.x.row_ptr[i + 1];
+    double bv = -INFINITY;
+    int bc = INT_MAX;
+    for (int64_t c = threadIdx.x; c < k; c += blockDim.x) {
+      const double s = exact_score_thread(p.x, rb, re, c);
+      if (s > bv) {
+        bv = s;
+        bc = (int)c;
+      }
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ov = __shfl_xor_sync(kFull, bv, off);
+      const int oc = __shfl_xor_sync(kFull, bc, off);
+      if (ov > bv || (ov == bv && oc < bc)) {
+        bv = ov;
+        bc = oc;
+      }
+    }
+    __syncthreads();
+    if (lane == 0) {
+      rv[warp] = bv;
+      rc[warp] = bc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < nw; ++w)
+        if (rv[w] > bv || (rv[w] == bv && rc[w] < bc)) {
+          bv = rv[w];
+          bc = rc[w];
+        }
+      p.labels[i] = bc;
+      p.sims[i] = bv;
+    }
+  }
+}
+
+// Add s exactly into a fixed-point accumulator: X = s * 2^1074 is an integer;
+// limb l holds bits [32l, 32l+32) as a signed partial sum.
+__device__ __forceinline__ void add_exact(double s, long long* limbs, unsigned& flags) {
+  if (s == 0.0) return;
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(s);
+  const int ex = (int)((bits >> 52) & 0x7ff);
+  if (ex == 0x7ff) {
+    flags |= 1u;
+    return;
+  }
+  unsigned long long m = bits & ((1ull << 52) - 1ull);
+  int b = 0;
+  if (ex != 0) {
+    m |= 1ull << 52;
+    b = ex - 1;
+  }
+  const int idx = b >> 5, sh = b & 31;
+  if (idx + 2 >= kLimbs) {
+    flags |= 2u;
+    return;
+  }
+  const unsigned c0 = (unsigned)(m << sh);
+  const unsigned long long t = sh ? (m >> (32 - sh)) : (m >> 32);
+  const long long sg = (bits >> 63) ? -1 : 1;
+  limbs[idx] += sg * (long long)c0;
+  limbs[idx + 1] += sg * (long long)(unsigned)t;
+  limbs[idx + 2] += sg * (long long)(unsigned)(t >> 32);
+}
+
+__global__ void __launch_bounds__(256) accumulate_kernel(int64_t n_obj, const int32_t* labels,
+                                                         const double* sims,
+                                                         const int32_t* prev,
+                                                         unsigned long long* sizes,
+                                                         ivfkm_stats* stats) {
+  __shared__ long long s_limbs[kLimbs];
+  __shared__ unsigned long long s_changed;
+  __shared__ unsigned s_flags;
+  for (int l = threadIdx.x; l < kLimbs; l += blockDim.x) s_limbs[l] = 0;
+  if (threadIdx.x == 0) {
+    s_changed = 0;
+    s_flags = 0;
+  }
+  __syncthreads();
+  long long limbs[kLimbs];
+#pragma unroll
+  for (int l = 0; l < kLimbs; ++l) limbs[l] = 0;
+  unsigned flags = 0;
+  unsigned long long changed = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_obj;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int lab = labels[i];
+    if (prev && prev[i] != lab) ++changed;
+    if (sizes) atomicAdd(&sizes[lab], 1ull);
+    add_exact(sims[i], limbs, flags);
+  }
+#pragma unroll
+  for (int l = 0; l < kLimbs; ++l)
+    if (limbs[l]) atomicAdd(reinterpret_cast<unsigned long long*>(&s_limbs[l]),
+                            (unsigned long long)limbs[l]);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) changed += __shfl_xor_sync(kFull, changed, off);
+  if ((threadIdx.x & 31) == 0 && changed) atomicAdd(&s_changed, changed);
+  if (flags) atomicOr(&s_flags, flags);
+  __syncthreads();
+  for (int l = threadIdx.x; l < kLimbs; l += blockDim.x)
+    if (s_limbs[l])
+      atomicAdd(reinterpret_cast<unsigned long long*>(&stats->obj_limbs[l]),
+                (unsigned long long)s_limbs[l]);
+  if (threadIdx.x == 0) {
+    if (s_changed) atomicAdd(&stats->changed, s_changed);
+    if (s_flags) atomicOr(&stats->obj_flags, (unsigned long long)s_flags);
+  }
+}
+
+struct AssignWs {
+  int32_t* label32;
+  int32_t* slot_of;
+  int32_t* q_obj;
+  int32_t* q_cnt;
+  int32_t* q_cid;
+  int32_t* ovf_list;
+  unsigned int* ovf_len;
+};
+
+AssignWs carve_assign(void* base, int64_t n, size_t* total) {
+  Carver c(base);
+  AssignWs w;
+  w.label32 = c.take<int32_t>(n);
+  w.slot_of = c.take<int32_t>(n);
+  w.q_obj = c.take<int32_t>(n);
+  w.q_cnt = c.take<int32_t>(n);
+  w.q_cid = c.take<int32_t>((size_t)n * kMaxC);
+  w.ovf_list = c.take<int32_t>(n);
+  w.ovf_len = c.take<unsigned int>(4);
+  if (total) *total = c.off;
+  return w;
+}
+
+struct Plan {
+  int rr, nsplit, cta_blocks, warps, rowcap;
+  size_t smem;
+};
+
+int plan_screen(int64_t k, int rowcap, int smem_limit, Plan* out) {
+  const int64_t nblk = ivfkm_bivf_nblk(k);
+  Plan pl;
+  pl.rr = nblk >= 32 ? 8 : 2;
+  pl.rowcap = rowcap;
+  const size_t stage = (size_t)rowcap * 8;
+  pl.nsplit = 0;
+  for (int s = 1; s <= kMaxSplit; ++s) {
+    int64_t cb = (nblk + s - 1) / s;
+    cb = (cb + pl.rr - 1) / pl.rr * pl.rr;
+    const size_t smem = (size_t)cb * 128 + stage;
+    if (smem <= (size_t)smem_limit) {
+      pl.nsplit = s;
+      pl.cta_blocks = (int)cb;
+      pl.smem = smem;
+      break;
+    }
+  }
+  if (pl.nsplit == 0) return IVFKM_E_UNSUPPORTED;
+  // at most 16 warps (512 threads, up to 128 registers per lane); spread the
+  // spans evenly over the passes each warp makes
+  const int spans = pl.cta_blocks / pl.rr;
+  const int passes = (spans + 15) / 16;
+  pl.warps = (spans + passes - 1) / passes;
+  if (pl.warps < 1) pl.warps = 1;
+  *out = pl;
+  return IVFKM_OK;
+}
+
+template <int RR>
+int launch_screen(const Plan& pl, const ScreenParams& p, cudaStream_t st) {
+  auto fn = screen_kernel<RR>;
+  IVFKM_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(p.n_obj * pl.nsplit));
+  cfg.blockDim = dim3(pl.warps * 32);
+  cfg.dynamicSmemBytes = pl.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = pl.nsplit;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pl.nsplit > 1 ? 1 : 0;
+  IVFKM_TRY(cudaLaunchKernelEx(&cfg, fn, p));
+  return IVFKM_OK;
+}
+
+}  // namespace
+
+extern "C" size_t ivfkm_assign_workspace_size(int64_t n_obj, int64_t /*k*/) {
+  size_t total = 0;
+  carve_assign(nullptr, n_obj, &total);
+  return total;
+}
+
+// Tuning knobs.  rowcap: row entries staged per pass (longer rows run in
+// several passes with rho parked in shared memory between passes).
+// smem_limit: shared-memory budget per CTA; a smaller budget forces the
+// thread-block-cluster split at small k (used by the tests).
+static int g_rowcap = 1024;
+static int g_smem_limit = kSmemLimit - 2048;  // leave room for static smem
+extern "C" void ivfkm_set_tuning(int rowcap, int smem_limit) {
+  if (rowcap >= 32 && rowcap <= 8192) g_rowcap = rowcap / 32 * 32;
+  if (smem_limit >= 1024 && smem_limit <= kSmemLimit - 2048) g_smem_limit = smem_limit;
+}
+
+extern "C" int ivfkm_assign(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
+                            const float* val32, const double* val64, const double* xnorm,
+                            int64_t k, int64_t dim, const uint32_t* headers, const float* pval32,
+                            const double* pval64, double mu_max, const int32_t* prev_labels,
+                            int32_t* labels, double* sims, unsigned long long* sizes,
+                            ivfkm_stats* stats, void* ws, size_t ws_bytes,
+                            ivfkm_stream_t stream_) {
+  if (n_obj < 0 || k < 1 || dim < 1 || !row_ptr || !labels || !sims || !stats || !headers)
+    return IVFKM_E_ARG;
+  if (n_obj > INT32_MAX || k > INT32_MAX) return IVFKM_E_UNSUPPORTED;
+  size_t need = 0;
+  AssignWs w = carve_assign(ws, n_obj, &need);
+  if (ws_bytes < need) return IVFKM_E_WORKSPACE;
+  cudaStream_t st = as_stream(stream_);
+  IVFKM_TRY(cudaMemsetAsync(stats, 0, sizeof(ivfkm_stats), st));
+  IVFKM_TRY(cudaMemsetAsync(w.ovf_len, 0, sizeof(unsigned int), st));
+  if (sizes) IVFKM_TRY(cudaMemsetAsync(sizes, 0, sizeof(unsigned long long) * k, st));
+  if (n_obj == 0) return IVFKM_OK;
+
+  Plan pl;
+  int rc = plan_screen(k, g_rowcap, g_smem_limit, &pl);
+  if (rc) return rc;
+  ScreenParams sp;
+  sp.n_obj = n_obj;
+  sp.row_ptr = row_ptr;
+  sp.terms = terms;
+  sp.val32 = val32;
+  sp.xnorm = xnorm;
+  sp.k = k;
+  sp.nblk = ivfkm_bivf_nblk(k);
+  sp.hdr = reinterpret_cast<const uint2*>(headers);
+  sp.pv32 = pval32;
+  sp.mu_max = mu_max > 0 ? mu_max : 1.0;
+  sp.cta_blocks = pl.cta_blocks;
+  sp.nsplit = pl.nsplit;
+  sp.rowcap = pl.rowcap;
+  sp.label32 = w.label32;
+  sp.slot_of = w.slot_of;
+  sp.q_obj = w.q_obj;
+  sp.q_cnt = w.q_cnt;
+  sp.q_cid = w.q_cid;
+  sp.stats = stats;
+  rc = pl.rr == 8 ? launch_screen<8>(pl, sp, st) : launch_screen<2>(pl, sp, st);
+  if (rc) return rc;
+
+  FinalParams fp;
+  fp.n_obj = n_obj;
+  fp.x.row_ptr = row_ptr;
+  fp.x.terms = terms;
+  fp.x.val64 = val64;
+  fp.x.nblk = sp.nblk;
+  fp.x.hdr = sp.hdr;
+  fp.x.pv64 = pval64;
+  fp.label32 = w.label32;
+  fp.slot_of = w.slot_of;
+  fp.q_cnt = w.q_cnt;
+  fp.q_cid = w.q_cid;
+  fp.labels = labels;
+  fp.sims = sims;
+  fp.ovf_list = w.ovf_list;
+  fp.ovf_len = w.ovf_len;
+  finalize_kernel<<<grid_for(n_obj, 8), 256, 0, st>>>(fp);
+  IVFKM_CHECK_LAUNCH();
+  overflow_kernel<<<kNumSM, 1024, 0, st>>>(fp, k);
+  IVFKM_CHECK_LAUNCH();
+  accumulate_kernel<<<grid_for(n_obj, 256, kNumSM * 8), 256, 0, st>>>(n_obj, labels, sims,
+                                                                      prev_labels, sizes, stats);
+  IVFKM_CHECK_LAUNCH();
+  return IVFKM_OK;
+}
+
+extern "C" int ivfkm_score_labels(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
+                                  const double* val64, int64_t k, int64_t dim,
+                                  const uint32_t* headers, const double* pval64,
+                                  const int32_t* labels, double* sims, ivfkm_stats* stats,
+                                  ivfkm_stream_t stream_) {
+  if (n_obj < 0 || k < 1 || dim < 1 || !row_ptr || !labels || !sims || !stats) return IVFKM_E_ARG;
+  cudaStream_t st = as_stream(stream_);
+  IVFKM_TRY(cudaMemsetAsync(stats, 0, sizeof(ivfkm_stats), st));
+  if (n_obj == 0) return IVFKM_OK;
+  ExactCtx x;
+  x.row_ptr = row_ptr;
+  x.terms = terms;
+  x.val64 = val64;
+  x.nblk = ivfkm_bivf_nblk(k);
+  x.hdr = reinterpret_cast<const uint2*>(headers);
+  x.pv64 = pval64;
+  score_labels_kernel<<<grid_for(n_obj, 8), 256, 0, st>>>(n_obj, x, labels, sims);
+  IVFKM_CHECK_LAUNCH();
+  accumulate_kernel<<<grid_for(n_obj, 256, kNumSM * 8), 256, 0, st>>>(n_obj, labels, sims, nullptr,
+                                                                      nullptr, stats);
+  IVFKM_CHECK_LAUNCH();
+  return IVFKM_OK;
+}

@@ -1,0 +1,432 @@
+// Update step of IVF spherical k-means on sm_100a, bit-identical to the
+// reference update_means (reference variants.py:254-307):
+//
+//   for each cluster j with size > 0:
+//     w = bincount(member terms, weights=member values)   # float64, entries
+//                                                         # in ascending object order
+//     w /= size
+//     nrm = sqrt(np.sum(w * w))                           # numpy pairwise sum over
+//                                                         # the dense length-D array
+//     emit (t, w[t] / nrm) for w[t] != 0, terms ascending
+//   empty cluster: copy the previous mean, retained = True
+//
+// Device plan: key every object nonzero by (label, term) and radix-sort the
+// keys stably (CUB onesweep LSD, so equal keys keep ascending object order);
+// one thread sums each (cluster, term) run sequentially in that order with
+// __dadd_rn (bincount's order), divides by the size; one thread per cluster
+// replays numpy's pairwise-summation tree over the run positions (empty
+// subtrees contribute exact zeros, so only populated leaves are visited);
+// scans give the new CSR offsets; the fill pass writes terms and values.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+using namespace ivfkm;
+
+namespace {
+
+template <class K>
+struct UpdWs {
+  K* key_a;
+  K* key_b;
+  uint32_t* idx_a;
+  uint32_t* idx_b;
+  uint32_t* head;     // run-head flags, later nonzero flags
+  uint32_t* segpos;   // scan of head
+  uint32_t* nzpos;    // scan of nonzero flags
+  uint32_t* seg_start;
+  K* seg_key;
+  double* seg_w;
+  uint32_t* cl_seg;   // k+1
+  double* nrm;        // k
+  int64_t* counts;    // k+1
+  uint32_t* n_seg;    // 1
+  void* cub;
+  size_t cub_bytes;
+};
+
+template <class K>
+size_t cub_bytes_for(int64_t nnz, int64_t k) {
+  size_t a = 0, b = 0, c = 0;
+  cub::DoubleBuffer<K> kb(nullptr, nullptr);
+  cub::DoubleBuffer<uint32_t> vb(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, a, kb, vb, (int)nnz, 0, (int)(sizeof(K) * 8));
+  cub::DeviceScan::ExclusiveSum(nullptr, b, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)nnz);
+  cub::DeviceScan::ExclusiveSum(nullptr, c, (int64_t*)nullptr, (int64_t*)nullptr, (int)(k + 1));
+  return std::max(a, std::max(b, c));
+}
+
+template <class K>
+UpdWs<K> carve_upd(void* base, int64_t nnz, int64_t k, size_t* total) {
+  Carver c(base);
+  UpdWs<K> w;
+  const size_t n = (size_t)(nnz > 0 ? nnz : 1);
+  w.key_a = c.take<K>(n);
+  w.key_b = c.take<K>(n);
+  w.idx_a = c.take<uint32_t>(n);
+  w.idx_b = c.take<uint32_t>(n);
+  w.head = c.take<uint32_t>(n);
+  w.segpos = c.take<uint32_t>(n);
+  w.nzpos = c.take<uint32_t>(n);
+  w.seg_start = c.take<uint32_t>(n + 1);
+  w.seg_key = c.take<K>(n);
+  w.seg_w = c.take<double>(n);
+  w.cl_seg = c.take<uint32_t>(k + 1);
+  w.nrm = c.take<double>(k);
+  w.counts = c.take<int64_t>(k + 1);
+  w.n_seg = c.take<uint32_t>(4);
+  w.cub_bytes = cub_bytes_for<K>((int64_t)n, k);
+  w.cub = c.take_bytes(w.cub_bytes);
+  if (total) *total = c.off;
+  return w;
+}
+
+bool use_k32(int64_t k, int64_t dim) { return (double)k * (double)dim < 4294967295.0; }
+
+int key_bits(int64_t k, int64_t dim) {
+  const double top = (double)k * (double)dim;
+  int b = 1;
+  while ((double)(1ull << b) < top && b < 63) ++b;
+  return b;
+}
+
+template <class K>
+__global__ void keys_kernel(int64_t n_obj, const int64_t* __restrict__ row_ptr,
+                            const int32_t* __restrict__ terms, const int32_t* __restrict__ labels,
+                            int64_t dim, K* __restrict__ key, uint32_t* __restrict__ idx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t i = blockIdx.x * wpb + (threadIdx.x >> 5); i < n_obj; i += gridDim.x * wpb) {
+    const K base = (K)labels[i] * (K)dim;
+    for (int64_t e = row_ptr[i] + lane; e < row_ptr[i + 1]; e += 32) {
+      key[e] = base + (K)terms[e];
+      idx[e] = (uint32_t)e;
+    }
+  }
+}
+
+template <class K>
+__global__ void head_kernel(int64_t nnz, const K* __restrict__ key, uint32_t* __restrict__ head) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x)
+    head[e] = (e == 0 || key[e] != key[e - 1]) ? 1u : 0u;
+}
+
+template <class K>
+__global__ void segstart_kernel(int64_t nnz, const K* __restrict__ key,
+                                const uint32_t* __restrict__ head,
+                                const uint32_t* __restrict__ segpos,
+                                uint32_t* __restrict__ seg_start, K* __restrict__ seg_key,
+                                uint32_t* __restrict__ n_seg) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (head[e]) {
+      seg_start[segpos[e]] = (uint32_t)e;
+      seg_key[segpos[e]] = key[e];
+    }
+    if (e == nnz - 1) {
+      const uint32_t ns = segpos[e] + head[e];
+      *n_seg = ns;
+      seg_start[ns] = (uint32_t)nnz;
+    }
+  }
+}
+
+// One thread per (cluster, term) run: sequential float64 sum in ascending
+// object order (bincount), then w = sum / size.  Reuses `head` as the
+// nonzero flag array (zeroed by the caller beyond n_seg).
+template <class K>
+__global__ void segsum_kernel(int64_t nnz, const uint32_t* __restrict__ n_seg_p,
+                              const uint32_t* __restrict__ seg_start,
+                              const K* __restrict__ seg_key, const uint32_t* __restrict__ idx,
+                              const double* __restrict__ val64,
+                              const unsigned long long* __restrict__ sizes, int64_t dim,
+                              double* __restrict__ seg_w, uint32_t* __restrict__ nz) {
+  const uint32_t n_seg = *n_seg_p;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nnz;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    if (s >= n_seg) {
+      nz[s] = 0u;
+      continue;
+    }
+    double acc = 0.0;
+    for (uint32_t e = seg_start[s]; e < seg_start[s + 1]; ++e) acc = __dadd_rn(acc, val64[idx[e]]);
+    const int64_t c = (int64_t)(seg_key[s] / (K)dim);
+    const double w = __ddiv_rn(acc, (double)sizes[c]);
+    seg_w[s] = w;
+    nz[s] = (w != 0.0) ? 1u : 0u;
+  }
+}
+
+template <class K>
+__global__ void clseg_kernel(int64_t k, int64_t dim, const uint32_t* __restrict__ n_seg_p,
+                             const K* __restrict__ seg_key, uint32_t* __restrict__ cl_seg) {
+  const uint32_t n_seg = *n_seg_p;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c <= k;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const K target = (K)c * (K)dim;
+    uint32_t lo = 0, hi = n_seg;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (seg_key[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    cl_seg[c] = c == k ? n_seg : lo;
+  }
+}
+
+// numpy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src,
+// pairwise_sum) over the dense length-D array w*w, replayed on the sparse
+// support: leaves of <= 128 elements use 8 strided accumulators combined as
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a sequential tail, leaves under 8
+// elements a plain sequential sum, larger ranges split at n/2 rounded down to
+// a multiple of 8.  Zeros only ever add exact +0.0, so empty subtrees are
+// skipped without changing a bit.  (Checked against np.sum by the tests.)
+template <class K>
+__device__ double leaf_sum(int64_t lo, int64_t n, uint32_t& cur, uint32_t end,
+                           const K* seg_key, const double* seg_w, K base) {
+  if (n < 8) {
+    double res = 0.0;
+    while (cur < end && (int64_t)(seg_key[cur] - base) < lo + n) {
+      const double w = seg_w[cur++];
+      res = __dadd_rn(res, __dmul_rn(w, w));
+    }
+    return res;
+  }
+  double r[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  const int64_t lim = lo + n - (n % 8);
+  while (cur < end) {
+    const int64_t pos = (int64_t)(seg_key[cur] - base);
+    if (pos >= lim) break;
+    const double w = seg_w[cur++];
+    const int j = (int)((pos - lo) & 7);
+    r[j] = __dadd_rn(r[j], __dmul_rn(w, w));
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  while (cur < end && (int64_t)(seg_key[cur] - base) < lo + n) {
+    const double w = seg_w[cur++];
+    res = __dadd_rn(res, __dmul_rn(w, w));
+  }
+  return res;
+}
+
+template <class K>
+__device__ double pairwise_sq(int64_t D, uint32_t begin, uint32_t end, const K* seg_key,
+                              const double* seg_w, K base) {
+  struct Frame {
+    int64_t lo, n;
+    double left;
+    int stage;
+  };
+  Frame st[40];
+  int sp = 0;
+  uint32_t cur = begin;
+  double ret = 0.0;
+  st[sp++] = Frame{0, D, 0.0, 0};
+  while (sp > 0) {
+    Frame& f = st[sp - 1];
+    if (f.stage == 0) {
+      if (cur >= end || (int64_t)(seg_key[cur] - base) >= f.lo + f.n) {
+        ret = 0.0;
+        --sp;
+        continue;
+      }
+      if (f.n <= 128) {
+        ret = leaf_sum<K>(f.lo, f.n, cur, end, seg_key, seg_w, base);
+        --sp;
+        continue;
+      }
+      int64_t n2 = f.n / 2;
+      n2 -= n2 % 8;
+      f.stage = 1;
+      st[sp++] = Frame{f.lo, n2, 0.0, 0};
+    } else if (f.stage == 1) {
+      f.left = ret;
+      f.stage = 2;
+      int64_t n2 = f.n / 2;
+      n2 -= n2 % 8;
+      st[sp++] = Frame{f.lo + n2, f.n - n2, 0.0, 0};
+    } else {
+      ret = __dadd_rn(f.left, ret);
+      --sp;
+    }
+  }
+  return ret;
+}
+
+template <class K>
+__global__ void norm_kernel(int64_t k, int64_t dim, const unsigned long long* __restrict__ sizes,
+                            const int64_t* __restrict__ prev_ptr,
+                            const uint32_t* __restrict__ cl_seg, const K* __restrict__ seg_key,
+                            const double* __restrict__ seg_w, const uint32_t* __restrict__ nz,
+                            double* __restrict__ nrm, int64_t* __restrict__ counts) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c <= k;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    if (c == k) {
+      counts[k] = 0;
+      continue;
+    }
+    if (sizes[c] == 0) {
+      counts[c] = prev_ptr[c + 1] - prev_ptr[c];
+      nrm[c] = 1.0;
+      continue;
+    }
+    const uint32_t b = cl_seg[c], e = cl_seg[c + 1];
+    int64_t cnt = 0;
+    for (uint32_t s = b; s < e; ++s) cnt += nz[s];
+    counts[c] = cnt;
+    nrm[c] = __dsqrt_rn(pairwise_sq<K>(dim, b, e, seg_key, seg_w, (K)c * (K)dim));
+  }
+}
+
+template <class K>
+__global__ void fill_kernel(int64_t nnz, int64_t dim, const uint32_t* __restrict__ n_seg_p,
+                            const K* __restrict__ seg_key, const double* __restrict__ seg_w,
+                            const uint32_t* __restrict__ nz, const uint32_t* __restrict__ nzpos,
+                            const uint32_t* __restrict__ cl_seg, const double* __restrict__ nrm,
+                            const int64_t* __restrict__ new_ptr, int32_t* __restrict__ new_terms,
+                            double* __restrict__ new_vals) {
+  const uint32_t n_seg = *n_seg_p;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_seg;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    if (!nz[s]) continue;
+    const int64_t c = (int64_t)(seg_key[s] / (K)dim);
+    const int64_t t = (int64_t)(seg_key[s] - (K)c * (K)dim);
+    const int64_t pos = new_ptr[c] + (int64_t)(nzpos[s] - nzpos[cl_seg[c]]);
+    new_terms[pos] = (int32_t)t;
+    new_vals[pos] = __ddiv_rn(seg_w[s], nrm[c]);
+  }
+}
+
+__global__ void retain_kernel(int64_t k, const unsigned long long* __restrict__ sizes,
+                              const int64_t* __restrict__ prev_ptr,
+                              const int32_t* __restrict__ prev_terms,
+                              const double* __restrict__ prev_vals,
+                              const int64_t* __restrict__ new_ptr, int32_t* __restrict__ new_terms,
+                              double* __restrict__ new_vals, uint8_t* __restrict__ retained) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t c = blockIdx.x * wpb + (threadIdx.x >> 5); c < k; c += gridDim.x * wpb) {
+    const bool empty = sizes[c] == 0;
+    if (lane == 0) retained[c] = empty ? 1 : 0;
+    if (!empty) continue;
+    const int64_t pb = prev_ptr[c], n = prev_ptr[c + 1] - pb, nb = new_ptr[c];
+    for (int64_t q = lane; q < n; q += 32) {
+      new_terms[nb + q] = prev_terms[pb + q];
+      new_vals[nb + q] = prev_vals[pb + q];
+    }
+  }
+}
+
+template <class K>
+int update_count_impl(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
+                      const double* val64, int64_t nnz, int64_t k, int64_t dim,
+                      const int32_t* labels, const unsigned long long* sizes,
+                      const int64_t* prev_ptr, int64_t* new_ptr, void* ws, size_t ws_bytes,
+                      cudaStream_t st) {
+  size_t need = 0;
+  UpdWs<K> w = carve_upd<K>(ws, nnz, k, &need);
+  if (ws_bytes < need) return IVFKM_E_WORKSPACE;
+  const int T = 256;
+  if (nnz > 0) {
+    keys_kernel<K><<<grid_for(n_obj, T / 32), T, 0, st>>>(n_obj, row_ptr, terms, labels, dim,
+                                                          w.key_a, w.idx_a);
+    IVFKM_CHECK_LAUNCH();
+    cub::DoubleBuffer<K> kb(w.key_a, w.key_b);
+    cub::DoubleBuffer<uint32_t> vb(w.idx_a, w.idx_b);
+    size_t cb = w.cub_bytes;
+    IVFKM_TRY(cub::DeviceRadixSort::SortPairs(w.cub, cb, kb, vb, (int)nnz, 0, key_bits(k, dim),
+                                              st));
+    K* key = kb.Current();
+    uint32_t* idx = vb.Current();
+    head_kernel<K><<<grid_for(nnz, T), T, 0, st>>>(nnz, key, w.head);
+    IVFKM_CHECK_LAUNCH();
+    cb = w.cub_bytes;
+    IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.head, w.segpos, (int)nnz, st));
+    segstart_kernel<K><<<grid_for(nnz, T), T, 0, st>>>(nnz, key, w.head, w.segpos, w.seg_start,
+                                                       w.seg_key, w.n_seg);
+    IVFKM_CHECK_LAUNCH();
+    segsum_kernel<K><<<grid_for(nnz, T), T, 0, st>>>(nnz, w.n_seg, w.seg_start, w.seg_key, idx,
+                                                     val64, sizes, dim, w.seg_w, w.head);
+    IVFKM_CHECK_LAUNCH();
+    cb = w.cub_bytes;
+    IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.head, w.nzpos, (int)nnz, st));
+  } else {
+    IVFKM_TRY(cudaMemsetAsync(w.n_seg, 0, sizeof(uint32_t), st));
+  }
+  clseg_kernel<K><<<grid_for(k + 1, T), T, 0, st>>>(k, dim, w.n_seg, w.seg_key, w.cl_seg);
+  IVFKM_CHECK_LAUNCH();
+  norm_kernel<K><<<grid_for(k + 1, 64), 64, 0, st>>>(k, dim, sizes, prev_ptr, w.cl_seg,
+                                                     w.seg_key, w.seg_w, w.head, w.nrm, w.counts);
+  IVFKM_CHECK_LAUNCH();
+  size_t cb = w.cub_bytes;
+  IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.counts, new_ptr, (int)(k + 1), st));
+  return IVFKM_OK;
+}
+
+template <class K>
+int update_fill_impl(int64_t nnz, int64_t k, int64_t dim, const unsigned long long* sizes,
+                     const int64_t* prev_ptr, const int32_t* prev_terms,
+                     const double* prev_vals, const int64_t* new_ptr, int32_t* new_terms,
+                     double* new_vals, uint8_t* retained, void* ws, size_t ws_bytes,
+                     cudaStream_t st) {
+  size_t need = 0;
+  UpdWs<K> w = carve_upd<K>(ws, nnz, k, &need);
+  if (ws_bytes < need) return IVFKM_E_WORKSPACE;
+  const int T = 256;
+  if (nnz > 0) {
+    fill_kernel<K><<<grid_for(nnz, T), T, 0, st>>>(nnz, dim, w.n_seg, w.seg_key, w.seg_w, w.head,
+                                                   w.nzpos, w.cl_seg, w.nrm, new_ptr, new_terms,
+                                                   new_vals);
+    IVFKM_CHECK_LAUNCH();
+  }
+  retain_kernel<<<grid_for(k, T / 32), T, 0, st>>>(k, sizes, prev_ptr, prev_terms, prev_vals,
+                                                   new_ptr, new_terms, new_vals, retained);
+  IVFKM_CHECK_LAUNCH();
+  return IVFKM_OK;
+}
+
+}  // namespace
+
+extern "C" size_t ivfkm_update_workspace_size(int64_t /*n_obj*/, int64_t nnz, int64_t k,
+                                              int64_t dim) {
+  size_t total = 0;
+  if (use_k32(k, dim)) carve_upd<uint32_t>(nullptr, nnz, k, &total);
+  else carve_upd<unsigned long long>(nullptr, nnz, k, &total);
+  return total;
+}
+
+extern "C" int ivfkm_update_count(int64_t n_obj, int64_t nnz, const int64_t* row_ptr,
+                                  const int32_t* terms,
+                                  const double* val64, int64_t k, int64_t dim,
+                                  const int32_t* labels, const unsigned long long* sizes,
+                                  const int64_t* prev_ptr, int64_t* new_ptr, void* ws,
+                                  size_t ws_bytes, ivfkm_stream_t stream_) {
+  if (n_obj < 0 || k < 1 || dim < 1 || !row_ptr || !sizes || !prev_ptr || !new_ptr)
+    return IVFKM_E_ARG;
+  if (nnz < 0) return IVFKM_E_ARG;
+  if (nnz >= (int64_t)INT32_MAX) return IVFKM_E_UNSUPPORTED;  // cub length / uint32 indices
+  cudaStream_t st = as_stream(stream_);
+  if (use_k32(k, dim))
+    return update_count_impl<uint32_t>(n_obj, row_ptr, terms, val64, nnz, k, dim, labels, sizes,
+                                       prev_ptr, new_ptr, ws, ws_bytes, st);
+  return update_count_impl<unsigned long long>(n_obj, row_ptr, terms, val64, nnz, k, dim, labels,
+                                               sizes, prev_ptr, new_ptr, ws, ws_bytes, st);
+}
+
+extern "C" int ivfkm_update_fill(int64_t /*n_obj*/, int64_t nnz, int64_t k, int64_t dim,
+                                 const unsigned long long* sizes, const int64_t* prev_ptr,
+                                 const int32_t* prev_terms, const double* prev_vals,
+                                 const int64_t* new_ptr, int32_t* new_terms, double* new_vals,
+                                 uint8_t* retained, int64_t capacity, void* ws, size_t ws_bytes,
+                                 ivfkm_stream_t stream_) {
+  if (k < 1 || dim < 1 || !new_ptr || !retained) return IVFKM_E_ARG;
+  (void)capacity;
+  cudaStream_t st = as_stream(stream_);
+  if (use_k32(k, dim))
+    return update_fill_impl<uint32_t>(nnz, k, dim, sizes, prev_ptr, prev_terms, prev_vals, new_ptr,
+                                      new_terms, new_vals, retained, ws, ws_bytes, st);
+  return update_fill_impl<unsigned long long>(nnz, k, dim, sizes, prev_ptr, prev_terms, prev_vals,
+                                              new_ptr, new_terms, new_vals, retained, ws, ws_bytes,
+                                              st);
+}

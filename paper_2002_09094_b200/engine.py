@@ -1,0 +1,246 @@
+"""Device-resident Lloyd engine: objects, means and every per-iteration
+buffer live in HBM; the host only launches the C-ABI kernels and reads a
+few bytes of statistics per iteration.
+
+One Lloyd iteration (the reference's loop body, clustering.py:262-298):
+
+    assign   ivfkm_assign        fp32 register screen + exact fp64 rescoring,
+                                 changed-label count, sizes, exact objective
+    (host)   read ivfkm_stats    convergence decision, objective, V
+    update   ivfkm_update_count  sort/segment-sum/normalise (bit-exact)
+             ivfkm_update_fill   new mean-major CSR (+ retained copies)
+             ivfkm_bivf_build    new bitmap-block inverted file
+
+torch is used for device memory, pinned host buffers and the current CUDA
+stream only; all compute on the path is in libivfkm.so.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .types import MeanSet
+
+__all__ = ["DeviceDataset", "DeviceMeans", "LloydEngine", "IterStats", "objective_from_limbs"]
+
+_MU_MAX = 1.0 + 1e-9  # means are unit norm to 1e-12 (means.py:56-60)
+
+
+def _p(t: torch.Tensor | None) -> C.c_void_p | None:
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream() -> C.c_void_p:
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def objective_from_limbs(limbs) -> float:
+    """Round the exact fixed-point sum (limb l weighs 2^(32 l - 1074)) once to
+    the nearest double: the same value math.fsum returns (clustering.py:119)."""
+    x = 0
+    for i, v in enumerate(limbs):
+        x += int(v) << (32 * i)
+    return x / (1 << 1074)  # int/int true division is correctly rounded
+
+
+@dataclass
+class IterStats:
+    postings: int
+    changed: int
+    near_ties: int
+    overflow: int
+    objective: float
+
+    @classmethod
+    def from_raw(cls, s: "_lib.Stats") -> "IterStats":
+        if s.obj_flags:
+            raise FloatingPointError("objective summand outside the exact accumulator range")
+        return cls(int(s.postings), int(s.changed), int(s.near_ties), int(s.overflow),
+                   objective_from_limbs(s.obj_limbs))
+
+
+class HostDataset:
+    """Pinned host copies of the device layout (for end-to-end transfers)."""
+
+    def __init__(self, ds, pin: bool = True):
+        ip = np.ascontiguousarray(ds.indptr, dtype=np.int64)
+        self.n = int(ip.size - 1)
+        self.dim = int(ds.dim)
+        self.nnz = int(ip[-1])
+        terms0 = np.ascontiguousarray(ds.term_ids, dtype=np.int32) - 1
+        vals = np.ascontiguousarray(ds.values, dtype=np.float64)
+        rows = np.diff(ip)
+        xn = np.sqrt(np.bincount(np.repeat(np.arange(self.n), rows), weights=vals * vals,
+                                 minlength=self.n)) if self.n else np.zeros(0)
+        self.max_row = int(rows.max()) if self.n else 0
+
+        def host(a):
+            t = torch.from_numpy(np.ascontiguousarray(a))
+            return t.pin_memory() if pin else t
+
+        self.row_ptr = host(ip)
+        self.terms = host(terms0.astype(np.int32))
+        self.val64 = host(vals)
+        self.xnorm = host(xn.astype(np.float64))
+
+    @property
+    def nbytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in (self.row_ptr, self.terms, self.val64,
+                                                          self.xnorm))
+
+
+class DeviceDataset:
+    """Objects on the device: int64 row_ptr, 0-based int32 terms, fp32 values
+    (screening) and fp64 values (rescoring, update), fp64 row norms."""
+
+    def __init__(self, host: HostDataset, device: torch.device | str = "cuda"):
+        self.n, self.dim, self.nnz, self.max_row = host.n, host.dim, host.nnz, host.max_row
+        self.device = torch.device(device)
+        nb = host.row_ptr.is_pinned()
+        self.row_ptr = host.row_ptr.to(self.device, non_blocking=nb)
+        self.terms = host.terms.to(self.device, non_blocking=nb)
+        self.val64 = host.val64.to(self.device, non_blocking=nb)
+        self.xnorm = host.xnorm.to(self.device, non_blocking=nb)
+        self.val32 = self.val64.to(torch.float32)
+
+    @classmethod
+    def from_dataset(cls, ds, device="cuda") -> "DeviceDataset":
+        return cls(HostDataset(ds, pin=False), device)
+
+
+class DeviceMeans:
+    """Means on the device: mean-major CSR (fp64, 0-based terms) + BIVF."""
+
+    def __init__(self, k, dim, ptr, terms, vals, retained):
+        self.k, self.dim = int(k), int(dim)
+        self.ptr, self.terms, self.vals, self.retained = ptr, terms, vals, retained
+        self.nnz = int(terms.numel())
+        self.headers = self.pv32 = self.pv64 = None
+
+    @classmethod
+    def from_meanset(cls, ms, device="cuda") -> "DeviceMeans":
+        dev = torch.device(device)
+        ptr = torch.from_numpy(np.ascontiguousarray(ms.indptr, dtype=np.int64)).to(dev)
+        terms = torch.from_numpy(np.ascontiguousarray(ms.term_ids, dtype=np.int32) - 1).to(dev)
+        vals = torch.from_numpy(np.ascontiguousarray(ms.values, dtype=np.float64)).to(dev)
+        ret = torch.from_numpy(np.ascontiguousarray(ms.retained, dtype=np.uint8)).to(dev)
+        return cls(ms.k, ms.dim, ptr, terms, vals, ret)
+
+    def to_meanset(self, representation: str = "sparse_inverted") -> MeanSet:
+        ptr = self.ptr.cpu().numpy()
+        terms = self.terms.cpu().numpy().astype(np.int32) + 1
+        vals = self.vals.cpu().numpy()
+        ret = self.retained.cpu().numpy().astype(bool)
+        return MeanSet(self.k, self.dim, representation, ptr, terms, vals, ret)
+
+
+class LloydEngine:
+    """Runs IVF Lloyd iterations over one device-resident dataset."""
+
+    def __init__(self, dd: DeviceDataset, k: int):
+        self.lib = _lib.load()
+        self.dd, self.k = dd, int(k)
+        dev = dd.device
+        self.device = dev
+        n, nnz, dim = dd.n, dd.nnz, dd.dim
+        self.nblk = int(self.lib.ivfkm_bivf_nblk(self.k))
+        u8 = torch.uint8
+        self.ws_assign = torch.empty(int(self.lib.ivfkm_assign_workspace_size(n, self.k)),
+                                     dtype=u8, device=dev)
+        self.ws_update = torch.empty(int(self.lib.ivfkm_update_workspace_size(n, nnz, self.k,
+                                                                              dim)),
+                                     dtype=u8, device=dev)
+        self.ws_bivf = torch.empty(int(self.lib.ivfkm_bivf_workspace_size(dim, self.k)),
+                                   dtype=u8, device=dev)
+        self.labels = [torch.empty(n, dtype=torch.int32, device=dev) for _ in range(2)]
+        self.cur = 0
+        self.sims = torch.empty(n, dtype=torch.float64, device=dev)
+        self.sizes = torch.empty(self.k, dtype=torch.int64, device=dev)  # unsigned on device
+        self.stats = torch.zeros(C.sizeof(_lib.Stats), dtype=u8, device=dev)
+        self.stats_host = torch.zeros(C.sizeof(_lib.Stats), dtype=u8).pin_memory() \
+            if torch.cuda.is_available() else torch.zeros(C.sizeof(_lib.Stats), dtype=u8)
+        self.total_host = torch.zeros(1, dtype=torch.int64).pin_memory()
+        self.rowcap = max(32, min(2048, (dd.max_row + 31) // 32 * 32))
+        self.launches = 0  # our kernels launched (for the bench's gpu_launches)
+
+    # -- means ---------------------------------------------------------------
+    def build_bivf(self, dm: DeviceMeans) -> DeviceMeans:
+        dev = self.device
+        dm.headers = torch.empty(2 * dm.dim * self.nblk, dtype=torch.int32, device=dev)
+        dm.pv32 = torch.empty(max(dm.nnz, 1), dtype=torch.float32, device=dev)
+        dm.pv64 = torch.empty(max(dm.nnz, 1), dtype=torch.float64, device=dev)
+        rc = self.lib.ivfkm_bivf_build(self.k, dm.dim, 0, self.k, _p(dm.ptr), _p(dm.terms),
+                                       _p(dm.vals), _p(dm.headers), _p(dm.pv32), _p(dm.pv64),
+                                       _p(self.ws_bivf), self.ws_bivf.numel(), _stream())
+        _lib.check(rc, "ivfkm_bivf_build")
+        self.launches += 5
+        return dm
+
+    def upload_means(self, ms) -> DeviceMeans:
+        return self.build_bivf(DeviceMeans.from_meanset(ms, self.device))
+
+    # -- assign --------------------------------------------------------------
+    def assign(self, dm: DeviceMeans, prev: torch.Tensor | None) -> torch.Tensor:
+        """Launch the assignment step; returns the (device) 0-based labels."""
+        dd = self.dd
+        out = self.labels[self.cur]
+        if prev is not None and prev.data_ptr() == out.data_ptr():
+            self.cur ^= 1
+            out = self.labels[self.cur]
+        self.lib.ivfkm_set_tuning(self.rowcap, 0)
+        rc = self.lib.ivfkm_assign(dd.n, _p(dd.row_ptr), _p(dd.terms), _p(dd.val32),
+                                   _p(dd.val64), _p(dd.xnorm), self.k, dd.dim, _p(dm.headers),
+                                   _p(dm.pv32), _p(dm.pv64), _MU_MAX, _p(prev), _p(out),
+                                   _p(self.sims), _p(self.sizes), _p(self.stats),
+                                   _p(self.ws_assign), self.ws_assign.numel(), _stream())
+        _lib.check(rc, "ivfkm_assign")
+        self.launches += 4
+        return out
+
+    def score_labels(self, dm: DeviceMeans, labels0: torch.Tensor) -> None:
+        dd = self.dd
+        rc = self.lib.ivfkm_score_labels(dd.n, _p(dd.row_ptr), _p(dd.terms), _p(dd.val64),
+                                         self.k, dd.dim, _p(dm.headers), _p(dm.pv64),
+                                         _p(labels0), _p(self.sims), _p(self.stats), _stream())
+        _lib.check(rc, "ivfkm_score_labels")
+        self.launches += 2
+
+    def read_stats(self) -> IterStats:
+        self.stats_host.copy_(self.stats, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        raw = _lib.Stats.from_buffer_copy(self.stats_host.numpy().tobytes())
+        return IterStats.from_raw(raw)
+
+    # -- update --------------------------------------------------------------
+    def update(self, labels0: torch.Tensor, dm: DeviceMeans) -> DeviceMeans:
+        """New means from the assignment (sizes must be the ones ivfkm_assign wrote)."""
+        dd, k, dev = self.dd, self.k, self.device
+        new_ptr = torch.empty(k + 1, dtype=torch.int64, device=dev)
+        rc = self.lib.ivfkm_update_count(dd.n, dd.nnz, _p(dd.row_ptr), _p(dd.terms),
+                                         _p(dd.val64), k, dd.dim, _p(labels0), _p(self.sizes),
+                                         _p(dm.ptr), _p(new_ptr), _p(self.ws_update),
+                                         self.ws_update.numel(), _stream())
+        _lib.check(rc, "ivfkm_update_count")
+        self.total_host.copy_(new_ptr[k:], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        total = int(self.total_host[0])
+        terms = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+        vals = torch.empty(max(total, 1), dtype=torch.float64, device=dev)
+        ret = torch.empty(k, dtype=torch.uint8, device=dev)
+        rc = self.lib.ivfkm_update_fill(dd.n, dd.nnz, k, dd.dim, _p(self.sizes), _p(dm.ptr),
+                                        _p(dm.terms), _p(dm.vals), _p(new_ptr), _p(terms),
+                                        _p(vals), _p(ret), total, _p(self.ws_update),
+                                        self.ws_update.numel(), _stream())
+        _lib.check(rc, "ivfkm_update_fill")
+        self.launches += 12
+        out = DeviceMeans(k, dd.dim, new_ptr, terms[:total], vals[:total], ret)
+        return self.build_bivf(out)
+
+    def set_sizes_from_labels(self, labels0: torch.Tensor) -> None:
+        """sizes = bincount(labels) for an externally supplied assignment."""
+        self.sizes.copy_(torch.bincount(labels0.long(), minlength=self.k))
