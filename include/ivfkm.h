@@ -104,6 +104,20 @@ int ivfkm_assign(int64_t n_obj, const int64_t* row_ptr /*[dev] n+1*/,
                  ivfkm_stats* stats /*[dev]*/, void* ws, size_t ws_bytes,
                  ivfkm_stream_t stream);
 
+/* The two halves of ivfkm_assign, for callers that time the fp32 screen
+ * (the dominant kernel) separately: screen zeroes *stats and fills the
+ * workspace's candidate queue; finish rescores, writes labels/sims/sizes and
+ * the objective.  Use the same workspace for both.                          */
+int ivfkm_assign_screen(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
+                        const float* val32, const double* xnorm, int64_t k, int64_t dim,
+                        const uint32_t* headers, const float* pval32, double mu_max,
+                        ivfkm_stats* stats, void* ws, size_t ws_bytes, ivfkm_stream_t stream);
+int ivfkm_assign_finish(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
+                        const double* val64, int64_t k, int64_t dim, const uint32_t* headers,
+                        const double* pval64, const int32_t* prev_labels, int32_t* labels,
+                        double* sims, unsigned long long* sizes, ivfkm_stats* stats, void* ws,
+                        size_t ws_bytes, ivfkm_stream_t stream);
+
 /* Exact float64 similarity of every object to the mean its (0-based) label
  * names — the summand of objective_cosine (clustering.py:105-119) — written
  * to sims, with the exact sum accumulated into stats->obj_limbs (stats is

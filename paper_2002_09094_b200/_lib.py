@@ -53,6 +53,10 @@ SIGNATURES = {
     "ivfkm_set_tuning": (None, [C.c_int, C.c_int]),
     "ivfkm_assign": (C.c_int, [_i64, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _f64,
                                _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "ivfkm_assign_screen": (C.c_int, [_i64, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _f64, _vp,
+                                      _vp, _sz, _vp]),
+    "ivfkm_assign_finish": (C.c_int, [_i64, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp,
+                                      _vp, _vp, _vp, _sz, _vp]),
     "ivfkm_score_labels": (C.c_int, [_i64, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp,
                                      _vp]),
     "ivfkm_update_workspace_size": (_sz, [_i64, _i64, _i64, _i64]),

@@ -612,39 +612,38 @@ extern "C" void ivfkm_set_tuning(int rowcap, int smem_limit) {
   if (smem_limit >= 1024 && smem_limit <= kSmemLimit - 2048) g_smem_limit = smem_limit;
 }
 
-extern "C" int ivfkm_assign(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
-                            const float* val32, const double* val64, const double* xnorm,
-                            int64_t k, int64_t dim, const uint32_t* headers, const float* pval32,
-                            const double* pval64, double mu_max, const int32_t* prev_labels,
-                            int32_t* labels, double* sims, unsigned long long* sizes,
-                            ivfkm_stats* stats, void* ws, size_t ws_bytes,
-                            ivfkm_stream_t stream_) {
-  if (n_obj < 0 || k < 1 || dim < 1 || !row_ptr || !labels || !sims || !stats || !headers)
-    return IVFKM_E_ARG;
-  if (n_obj > INT32_MAX || k > INT32_MAX) return IVFKM_E_UNSUPPORTED;
-  size_t need = 0;
-  AssignWs w = carve_assign(ws, n_obj, &need);
-  if (ws_bytes < need) return IVFKM_E_WORKSPACE;
-  cudaStream_t st = as_stream(stream_);
-  IVFKM_TRY(cudaMemsetAsync(stats, 0, sizeof(ivfkm_stats), st));
-  IVFKM_TRY(cudaMemsetAsync(w.ovf_len, 0, sizeof(unsigned int), st));
-  if (sizes) IVFKM_TRY(cudaMemsetAsync(sizes, 0, sizeof(unsigned long long) * k, st));
-  if (n_obj == 0) return IVFKM_OK;
+namespace {
 
+struct AssignArgs {
+  int64_t n_obj;
+  const int64_t* row_ptr;
+  const int32_t* terms;
+  const float* val32;
+  const double* val64;
+  const double* xnorm;
+  int64_t k, dim;
+  const uint32_t* headers;
+  const float* pval32;
+  const double* pval64;
+  double mu_max;
+  ivfkm_stats* stats;
+};
+
+int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
   Plan pl;
-  int rc = plan_screen(k, g_rowcap, g_smem_limit, &pl);
+  int rc = plan_screen(a.k, g_rowcap, g_smem_limit, &pl);
   if (rc) return rc;
   ScreenParams sp;
-  sp.n_obj = n_obj;
-  sp.row_ptr = row_ptr;
-  sp.terms = terms;
-  sp.val32 = val32;
-  sp.xnorm = xnorm;
-  sp.k = k;
-  sp.nblk = ivfkm_bivf_nblk(k);
-  sp.hdr = reinterpret_cast<const uint2*>(headers);
-  sp.pv32 = pval32;
-  sp.mu_max = mu_max > 0 ? mu_max : 1.0;
+  sp.n_obj = a.n_obj;
+  sp.row_ptr = a.row_ptr;
+  sp.terms = a.terms;
+  sp.val32 = a.val32;
+  sp.xnorm = a.xnorm;
+  sp.k = a.k;
+  sp.nblk = ivfkm_bivf_nblk(a.k);
+  sp.hdr = reinterpret_cast<const uint2*>(a.headers);
+  sp.pv32 = a.pval32;
+  sp.mu_max = a.mu_max > 0 ? a.mu_max : 1.0;
   sp.cta_blocks = pl.cta_blocks;
   sp.nsplit = pl.nsplit;
   sp.rowcap = pl.rowcap;
@@ -653,18 +652,20 @@ extern "C" int ivfkm_assign(int64_t n_obj, const int64_t* row_ptr, const int32_t
   sp.q_obj = w.q_obj;
   sp.q_cnt = w.q_cnt;
   sp.q_cid = w.q_cid;
-  sp.stats = stats;
-  rc = pl.rr == 8 ? launch_screen<8>(pl, sp, st) : launch_screen<2>(pl, sp, st);
-  if (rc) return rc;
+  sp.stats = a.stats;
+  return pl.rr == 8 ? launch_screen<8>(pl, sp, st) : launch_screen<2>(pl, sp, st);
+}
 
+int finish_impl(const AssignArgs& a, const AssignWs& w, const int32_t* prev_labels,
+                int32_t* labels, double* sims, unsigned long long* sizes, cudaStream_t st) {
   FinalParams fp;
-  fp.n_obj = n_obj;
-  fp.x.row_ptr = row_ptr;
-  fp.x.terms = terms;
-  fp.x.val64 = val64;
-  fp.x.nblk = sp.nblk;
-  fp.x.hdr = sp.hdr;
-  fp.x.pv64 = pval64;
+  fp.n_obj = a.n_obj;
+  fp.x.row_ptr = a.row_ptr;
+  fp.x.terms = a.terms;
+  fp.x.val64 = a.val64;
+  fp.x.nblk = ivfkm_bivf_nblk(a.k);
+  fp.x.hdr = reinterpret_cast<const uint2*>(a.headers);
+  fp.x.pv64 = a.pval64;
   fp.label32 = w.label32;
   fp.slot_of = w.slot_of;
   fp.q_cnt = w.q_cnt;
@@ -673,14 +674,68 @@ extern "C" int ivfkm_assign(int64_t n_obj, const int64_t* row_ptr, const int32_t
   fp.sims = sims;
   fp.ovf_list = w.ovf_list;
   fp.ovf_len = w.ovf_len;
-  finalize_kernel<<<grid_for(n_obj, 8), 256, 0, st>>>(fp);
+  finalize_kernel<<<grid_for(a.n_obj, 8), 256, 0, st>>>(fp);
   IVFKM_CHECK_LAUNCH();
-  overflow_kernel<<<kNumSM, 1024, 0, st>>>(fp, k);
+  overflow_kernel<<<kNumSM, 1024, 0, st>>>(fp, a.k);
   IVFKM_CHECK_LAUNCH();
-  accumulate_kernel<<<grid_for(n_obj, 256, kNumSM * 8), 256, 0, st>>>(n_obj, labels, sims,
-                                                                      prev_labels, sizes, stats);
+  accumulate_kernel<<<grid_for(a.n_obj, 256, kNumSM * 8), 256, 0, st>>>(
+      a.n_obj, labels, sims, prev_labels, sizes, a.stats);
   IVFKM_CHECK_LAUNCH();
   return IVFKM_OK;
+}
+
+}  // namespace
+
+extern "C" int ivfkm_assign_screen(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
+                                   const float* val32, const double* xnorm, int64_t k,
+                                   int64_t dim, const uint32_t* headers, const float* pval32,
+                                   double mu_max, ivfkm_stats* stats, void* ws, size_t ws_bytes,
+                                   ivfkm_stream_t stream_) {
+  if (n_obj < 0 || k < 1 || dim < 1 || !row_ptr || !stats || !headers) return IVFKM_E_ARG;
+  if (n_obj > INT32_MAX || k > INT32_MAX) return IVFKM_E_UNSUPPORTED;
+  size_t need = 0;
+  AssignWs w = carve_assign(ws, n_obj, &need);
+  if (ws_bytes < need) return IVFKM_E_WORKSPACE;
+  cudaStream_t st = as_stream(stream_);
+  IVFKM_TRY(cudaMemsetAsync(stats, 0, sizeof(ivfkm_stats), st));
+  IVFKM_TRY(cudaMemsetAsync(w.ovf_len, 0, sizeof(unsigned int), st));
+  if (n_obj == 0) return IVFKM_OK;
+  AssignArgs a{n_obj, row_ptr, terms, val32, nullptr, xnorm, k, dim, headers, pval32, nullptr,
+               mu_max, stats};
+  return screen_impl(a, w, st);
+}
+
+extern "C" int ivfkm_assign_finish(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
+                                   const double* val64, int64_t k, int64_t dim,
+                                   const uint32_t* headers, const double* pval64,
+                                   const int32_t* prev_labels, int32_t* labels, double* sims,
+                                   unsigned long long* sizes, ivfkm_stats* stats, void* ws,
+                                   size_t ws_bytes, ivfkm_stream_t stream_) {
+  if (n_obj < 0 || k < 1 || dim < 1 || !row_ptr || !labels || !sims || !stats || !headers)
+    return IVFKM_E_ARG;
+  size_t need = 0;
+  AssignWs w = carve_assign(ws, n_obj, &need);
+  if (ws_bytes < need) return IVFKM_E_WORKSPACE;
+  cudaStream_t st = as_stream(stream_);
+  if (sizes) IVFKM_TRY(cudaMemsetAsync(sizes, 0, sizeof(unsigned long long) * k, st));
+  if (n_obj == 0) return IVFKM_OK;
+  AssignArgs a{n_obj, row_ptr, terms, nullptr, val64, nullptr, k, dim, headers, nullptr, pval64,
+               0.0, stats};
+  return finish_impl(a, w, prev_labels, labels, sims, sizes, st);
+}
+
+extern "C" int ivfkm_assign(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
+                            const float* val32, const double* val64, const double* xnorm,
+                            int64_t k, int64_t dim, const uint32_t* headers, const float* pval32,
+                            const double* pval64, double mu_max, const int32_t* prev_labels,
+                            int32_t* labels, double* sims, unsigned long long* sizes,
+                            ivfkm_stats* stats, void* ws, size_t ws_bytes,
+                            ivfkm_stream_t stream_) {
+  int rc = ivfkm_assign_screen(n_obj, row_ptr, terms, val32, xnorm, k, dim, headers, pval32,
+                               mu_max, stats, ws, ws_bytes, stream_);
+  if (rc) return rc;
+  return ivfkm_assign_finish(n_obj, row_ptr, terms, val64, k, dim, headers, pval64, prev_labels,
+                             labels, sims, sizes, stats, ws, ws_bytes, stream_);
 }
 
 extern "C" int ivfkm_score_labels(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,

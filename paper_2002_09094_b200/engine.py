@@ -80,7 +80,7 @@ class HostDataset:
         self.max_row = int(rows.max()) if self.n else 0
 
         def host(a):
-            t = torch.from_numpy(np.ascontiguousarray(a))
+            t = torch.from_numpy(np.array(a, copy=True))
             return t.pin_memory() if pin else t
 
         self.row_ptr = host(ip)
@@ -125,10 +125,10 @@ class DeviceMeans:
     @classmethod
     def from_meanset(cls, ms, device="cuda") -> "DeviceMeans":
         dev = torch.device(device)
-        ptr = torch.from_numpy(np.ascontiguousarray(ms.indptr, dtype=np.int64)).to(dev)
-        terms = torch.from_numpy(np.ascontiguousarray(ms.term_ids, dtype=np.int32) - 1).to(dev)
-        vals = torch.from_numpy(np.ascontiguousarray(ms.values, dtype=np.float64)).to(dev)
-        ret = torch.from_numpy(np.ascontiguousarray(ms.retained, dtype=np.uint8)).to(dev)
+        ptr = torch.from_numpy(np.array(ms.indptr, dtype=np.int64)).to(dev)
+        terms = torch.from_numpy(np.array(ms.term_ids, dtype=np.int32) - 1).to(dev)
+        vals = torch.from_numpy(np.array(ms.values, dtype=np.float64)).to(dev)
+        ret = torch.from_numpy(np.array(ms.retained, dtype=np.uint8)).to(dev)
         return cls(ms.k, ms.dim, ptr, terms, vals, ret)
 
     def to_meanset(self, representation: str = "sparse_inverted") -> MeanSet:
@@ -185,20 +185,33 @@ class LloydEngine:
         return self.build_bivf(DeviceMeans.from_meanset(ms, self.device))
 
     # -- assign --------------------------------------------------------------
-    def assign(self, dm: DeviceMeans, prev: torch.Tensor | None) -> torch.Tensor:
-        """Launch the assignment step; returns the (device) 0-based labels."""
+    def assign(self, dm: DeviceMeans, prev: torch.Tensor | None, events=None) -> torch.Tensor:
+        """Launch the assignment step; returns the (device) 0-based labels.
+
+        ``events``: optional (start, end) torch.cuda.Event pair recorded around
+        the fp32 screen kernel (the dominant kernel) on the current stream.
+        """
         dd = self.dd
         out = self.labels[self.cur]
         if prev is not None and prev.data_ptr() == out.data_ptr():
             self.cur ^= 1
             out = self.labels[self.cur]
         self.lib.ivfkm_set_tuning(self.rowcap, 0)
-        rc = self.lib.ivfkm_assign(dd.n, _p(dd.row_ptr), _p(dd.terms), _p(dd.val32),
-                                   _p(dd.val64), _p(dd.xnorm), self.k, dd.dim, _p(dm.headers),
-                                   _p(dm.pv32), _p(dm.pv64), _MU_MAX, _p(prev), _p(out),
-                                   _p(self.sims), _p(self.sizes), _p(self.stats),
-                                   _p(self.ws_assign), self.ws_assign.numel(), _stream())
-        _lib.check(rc, "ivfkm_assign")
+        st = _stream()
+        if events is not None:
+            events[0].record()
+        rc = self.lib.ivfkm_assign_screen(dd.n, _p(dd.row_ptr), _p(dd.terms), _p(dd.val32),
+                                          _p(dd.xnorm), self.k, dd.dim, _p(dm.headers),
+                                          _p(dm.pv32), _MU_MAX, _p(self.stats),
+                                          _p(self.ws_assign), self.ws_assign.numel(), st)
+        _lib.check(rc, "ivfkm_assign_screen")
+        if events is not None:
+            events[1].record()
+        rc = self.lib.ivfkm_assign_finish(dd.n, _p(dd.row_ptr), _p(dd.terms), _p(dd.val64),
+                                          self.k, dd.dim, _p(dm.headers), _p(dm.pv64), _p(prev),
+                                          _p(out), _p(self.sims), _p(self.sizes), _p(self.stats),
+                                          _p(self.ws_assign), self.ws_assign.numel(), st)
+        _lib.check(rc, "ivfkm_assign_finish")
         self.launches += 4
         return out
 

@@ -195,12 +195,14 @@ def _assign_raw(ds, means, rowcap=None, smem=None):
     return lab.cpu().numpy() + 1, st
 
 
-def _random_case(n=1500, dim=400, k=64, seed=0, signed=False):
+def _random_case(n=1500, dim=400, k=64, seed=0, signed=False, corpus=0):
     from oracle import oracle as O
     from paper_2002_09094_b200 import synth
 
     P = _pkg()
-    spec = synth.CONFIGS[0]["corpus"].scaled(n, dim, seed=100 + seed)
+    if corpus == 1:  # config-1 row lengths (lognormal, mean 230)
+        dim = max(dim, 5000)
+    spec = synth.CONFIGS[corpus]["corpus"].scaled(n, dim, seed=100 + seed)
     ip, t, v, _ = synth.make_corpus(spec)
     if signed:
         v = v * np.where(np.random.default_rng(seed).random(v.size) < 0.4, -1.0, 1.0)
@@ -223,12 +225,12 @@ def test_assign_matches_oracle_exactly(seed, k, signed):
     assert st.objective == O.objective(ds, ol, om)
 
 
-@pytest.mark.parametrize("rowcap", [32, 64])
-def test_multipass_rows(tuning, rowcap):
+@pytest.mark.parametrize("rowcap,corpus", [(32, 0), (64, 1)])
+def test_multipass_rows(tuning, rowcap, corpus):
     """Rows longer than the shared-memory stage run in several passes."""
     from oracle import oracle as O
 
-    ds, om, means = _random_case(seed=5, k=200)
+    ds, om, means = _random_case(seed=5, k=200, corpus=corpus)
     assert int(np.diff(ds.indptr).max()) > rowcap
     labels, st = _assign_raw(ds, means, rowcap=rowcap)
     ol, _, _, post = O.assign(ds, om)
