@@ -53,25 +53,35 @@ BivfWs carve(void* base, int64_t dim, int64_t k, size_t* total) {
   return w;
 }
 
-// One warp per CSR row; lanes stride the row's entries.
+// Row owning entry q of a CSR with nrows rows: the last r with ptr[r] <= q.
+__device__ __forceinline__ int64_t row_of(const int64_t* __restrict__ ptr, int64_t nrows,
+                                          int64_t q) {
+  int64_t lo = 0, hi = nrows;  // ptr[lo] <= q < ptr[hi]
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (__ldg(ptr + mid) <= q) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// One thread per entry (grid-stride), so a few long rows (k means holding
+// ~20k terms each) still spread over the whole GPU.
 __global__ void bivf_mask_kernel(int major, int64_t nrows, const int64_t* __restrict__ ptr,
                                  const int32_t* __restrict__ cols, int64_t k, int64_t dim,
                                  int64_t nblk, unsigned int* __restrict__ hdr,
                                  unsigned int* __restrict__ err) {
-  const int lane = threadIdx.x & 31;
-  const int64_t wpb = blockDim.x >> 5;
-  for (int64_t r = blockIdx.x * wpb + (threadIdx.x >> 5); r < nrows; r += gridDim.x * wpb) {
-    const int64_t b = ptr[r], e = ptr[r + 1];
-    for (int64_t q = b + lane; q < e; q += 32) {
-      const int64_t col = cols[q];
-      const int64_t c = major == 0 ? r : col;
-      const int64_t t = major == 0 ? col : r;
-      if (c < 0 || c >= k || t < 0 || t >= dim) {
-        atomicAdd(err, 1u);
-        continue;
-      }
-      atomicOr(&hdr[2 * (t * nblk + (c >> 5))], 1u << (c & 31));
+  const int64_t nnz = ptr[nrows];
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = row_of(ptr, nrows, q);
+    const int64_t col = cols[q];
+    const int64_t c = major == 0 ? r : col;
+    const int64_t t = major == 0 ? col : r;
+    if (c < 0 || c >= k || t < 0 || t >= dim) {
+      atomicAdd(err, 1u);
+      continue;
     }
+    atomicOr(&hdr[2 * (t * nblk + (c >> 5))], 1u << (c & 31));
   }
 }
 
@@ -94,21 +104,19 @@ __global__ void bivf_scatter_kernel(int major, int64_t nrows, const int64_t* __r
                                     const double* __restrict__ vals, int64_t k, int64_t dim,
                                     int64_t nblk, const unsigned int* __restrict__ hdr,
                                     float* __restrict__ v32, double* __restrict__ v64) {
-  const int lane = threadIdx.x & 31;
-  const int64_t wpb = blockDim.x >> 5;
-  for (int64_t r = blockIdx.x * wpb + (threadIdx.x >> 5); r < nrows; r += gridDim.x * wpb) {
-    const int64_t b = ptr[r], e = ptr[r + 1];
-    for (int64_t q = b + lane; q < e; q += 32) {
-      const int64_t col = cols[q];
-      const int64_t c = major == 0 ? r : col;
-      const int64_t t = major == 0 ? col : r;
-      if (c < 0 || c >= k || t < 0 || t >= dim) continue;
-      const uint2 h = *reinterpret_cast<const uint2*>(&hdr[2 * (t * nblk + (c >> 5))]);
-      const unsigned pos = h.y + __popc(h.x & ((1u << (c & 31)) - 1u));
-      const double v = vals[q];
-      v32[pos] = static_cast<float>(v);
-      v64[pos] = v;
-    }
+  const int64_t nnz = ptr[nrows];
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = row_of(ptr, nrows, q);
+    const int64_t col = cols[q];
+    const int64_t c = major == 0 ? r : col;
+    const int64_t t = major == 0 ? col : r;
+    if (c < 0 || c >= k || t < 0 || t >= dim) continue;
+    const uint2 h = *reinterpret_cast<const uint2*>(&hdr[2 * (t * nblk + (c >> 5))]);
+    const unsigned pos = h.y + __popc(h.x & ((1u << (c & 31)) - 1u));
+    const double v = vals[q];
+    v32[pos] = static_cast<float>(v);
+    v64[pos] = v;
   }
 }
 
@@ -136,7 +144,7 @@ extern "C" int ivfkm_bivf_build(int64_t k, int64_t dim, int major, int64_t nrows
   IVFKM_TRY(cudaMemsetAsync(headers, 0, sizeof(uint32_t) * 2 * nh, st));
   IVFKM_TRY(cudaMemsetAsync(w.err, 0, sizeof(unsigned int), st));
   const int threads = 256;
-  bivf_mask_kernel<<<grid_for(nrows, threads / 32), threads, 0, st>>>(
+  bivf_mask_kernel<<<kNumSM * 8, threads, 0, st>>>(
       major, nrows, ptr, cols, k, dim, nblk, headers, w.err);
   IVFKM_CHECK_LAUNCH();
   bivf_popc_kernel<<<grid_for(nh + 1, threads), threads, 0, st>>>(nh, headers, w.cnt);
@@ -145,7 +153,7 @@ extern "C" int ivfkm_bivf_build(int64_t k, int64_t dim, int major, int64_t nrows
   IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.cnt, w.off, (int)(nh + 1), st));
   bivf_offset_kernel<<<grid_for(nh, threads), threads, 0, st>>>(nh, w.off, headers);
   IVFKM_CHECK_LAUNCH();
-  bivf_scatter_kernel<<<grid_for(nrows, threads / 32), threads, 0, st>>>(
+  bivf_scatter_kernel<<<kNumSM * 8, threads, 0, st>>>(
       major, nrows, ptr, cols, vals, k, dim, nblk, headers, val32, val64);
   IVFKM_CHECK_LAUNCH();
   return IVFKM_OK;

@@ -176,14 +176,47 @@ __global__ void clseg_kernel(int64_t k, int64_t dim, const uint32_t* __restrict_
 
 // numpy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src,
 // pairwise_sum) over the dense length-D array w*w, replayed on the sparse
-// support: leaves of <= 128 elements use 8 strided accumulators combined as
-// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a sequential tail, leaves under 8
-// elements a plain sequential sum, larger ranges split at n/2 rounded down to
-// a multiple of 8.  Zeros only ever add exact +0.0, so empty subtrees are
-// skipped without changing a bit.  (Checked against np.sum by the tests.)
+// support.  The recursion splits a range of n > 128 elements at
+// n2 = n/2 - (n/2)%8, so its leaves (64..128 elements, or the whole array
+// when D <= 128) depend on D only; a leaf of >= 8 elements sums into 8
+// strided accumulators combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a
+// sequential tail, a leaf under 8 elements is a plain sequential sum.  Zeros
+// add exact +0.0, so a leaf only visits the cluster's nonzeros in its range.
+// (tests/test_update_numerics.py checks the replay against np.sum.)
+//
+// One CTA per cluster: threads compute the leaves in parallel, thread 0
+// combines them in the recursion's order.
+
+// leaf boundaries of [0, D) in left-to-right order (host and device)
+__host__ __device__ inline int64_t enum_leaves(int64_t D, int32_t* lo_out) {
+  int64_t stk_lo[64], stk_n[64];
+  int sp = 0;
+  int64_t L = 0;
+  stk_lo[sp] = 0;
+  stk_n[sp++] = D;
+  while (sp > 0) {
+    --sp;
+    const int64_t lo = stk_lo[sp], n = stk_n[sp];
+    if (n <= 128) {
+      if (lo_out) lo_out[L] = (int32_t)lo;
+      ++L;
+      continue;
+    }
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    // push right first so the left subtree is emitted first
+    stk_lo[sp] = lo + n2;
+    stk_n[sp++] = n - n2;
+    stk_lo[sp] = lo;
+    stk_n[sp++] = n2;
+  }
+  if (lo_out) lo_out[L] = (int32_t)D;
+  return L;
+}
+
 template <class K>
-__device__ double leaf_sum(int64_t lo, int64_t n, uint32_t& cur, uint32_t end,
-                           const K* seg_key, const double* seg_w, K base) {
+__device__ double leaf_value(int64_t lo, int64_t n, uint32_t cur, uint32_t end, const K* seg_key,
+                             const double* seg_w, K base) {
   if (n < 8) {
     double res = 0.0;
     while (cur < end && (int64_t)(seg_key[cur] - base) < lo + n) {
@@ -210,42 +243,37 @@ __device__ double leaf_sum(int64_t lo, int64_t n, uint32_t& cur, uint32_t end,
   return res;
 }
 
-template <class K>
-__device__ double pairwise_sq(int64_t D, uint32_t begin, uint32_t end, const K* seg_key,
-                              const double* seg_w, K base) {
+// Combine leaf values in the recursion's order: pw(lo,n) = leaf or
+// pw(left) + pw(right).  Leaves are consumed left to right.
+__device__ double combine_leaves(int64_t D, const double* leaf_val) {
   struct Frame {
-    int64_t lo, n;
+    int64_t n;
     double left;
     int stage;
   };
-  Frame st[40];
+  Frame st[64];
   int sp = 0;
-  uint32_t cur = begin;
+  int64_t next = 0;
   double ret = 0.0;
-  st[sp++] = Frame{0, D, 0.0, 0};
+  st[sp++] = Frame{D, 0.0, 0};
   while (sp > 0) {
     Frame& f = st[sp - 1];
     if (f.stage == 0) {
-      if (cur >= end || (int64_t)(seg_key[cur] - base) >= f.lo + f.n) {
-        ret = 0.0;
-        --sp;
-        continue;
-      }
       if (f.n <= 128) {
-        ret = leaf_sum<K>(f.lo, f.n, cur, end, seg_key, seg_w, base);
+        ret = leaf_val[next++];
         --sp;
         continue;
       }
       int64_t n2 = f.n / 2;
       n2 -= n2 % 8;
       f.stage = 1;
-      st[sp++] = Frame{f.lo, n2, 0.0, 0};
+      st[sp++] = Frame{n2, 0.0, 0};
     } else if (f.stage == 1) {
       f.left = ret;
       f.stage = 2;
       int64_t n2 = f.n / 2;
       n2 -= n2 % 8;
-      st[sp++] = Frame{f.lo + n2, f.n - n2, 0.0, 0};
+      st[sp++] = Frame{f.n - n2, 0.0, 0};
     } else {
       ret = __dadd_rn(f.left, ret);
       --sp;
@@ -255,27 +283,51 @@ __device__ double pairwise_sq(int64_t D, uint32_t begin, uint32_t end, const K* 
 }
 
 template <class K>
-__global__ void norm_kernel(int64_t k, int64_t dim, const unsigned long long* __restrict__ sizes,
-                            const int64_t* __restrict__ prev_ptr,
-                            const uint32_t* __restrict__ cl_seg, const K* __restrict__ seg_key,
-                            const double* __restrict__ seg_w, const uint32_t* __restrict__ nz,
-                            double* __restrict__ nrm, int64_t* __restrict__ counts) {
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c <= k;
-       c += (int64_t)gridDim.x * blockDim.x) {
-    if (c == k) {
-      counts[k] = 0;
-      continue;
-    }
-    if (sizes[c] == 0) {
-      counts[c] = prev_ptr[c + 1] - prev_ptr[c];
-      nrm[c] = 1.0;
+__global__ void __launch_bounds__(256) norm_kernel(
+    int64_t k, int64_t dim, int64_t nleaf, const unsigned long long* __restrict__ sizes,
+    const int64_t* __restrict__ prev_ptr, const uint32_t* __restrict__ cl_seg,
+    const K* __restrict__ seg_key, const double* __restrict__ seg_w,
+    const uint32_t* __restrict__ nz, double* __restrict__ nrm, int64_t* __restrict__ counts) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* leaf_val = reinterpret_cast<double*>(smem);
+  int32_t* leaf_lo = reinterpret_cast<int32_t*>(leaf_val + nleaf);
+  __shared__ int64_t s_cnt;
+  if (threadIdx.x == 0) enum_leaves(dim, leaf_lo);
+  if (blockIdx.x == 0 && threadIdx.x == 0) counts[k] = 0;
+  __syncthreads();
+  for (int64_t c = blockIdx.x; c < k; c += gridDim.x) {
+    if (sizes[c] == 0) {  // retained: previous mean, count only
+      if (threadIdx.x == 0) {
+        counts[c] = prev_ptr[c + 1] - prev_ptr[c];
+        nrm[c] = 1.0;
+      }
       continue;
     }
     const uint32_t b = cl_seg[c], e = cl_seg[c + 1];
+    const K base = (K)c * (K)dim;
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
     int64_t cnt = 0;
-    for (uint32_t s = b; s < e; ++s) cnt += nz[s];
-    counts[c] = cnt;
-    nrm[c] = __dsqrt_rn(pairwise_sq<K>(dim, b, e, seg_key, seg_w, (K)c * (K)dim));
+    for (uint32_t sidx = b + threadIdx.x; sidx < e; sidx += blockDim.x) cnt += nz[sidx];
+    for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd((unsigned long long*)&s_cnt, (unsigned long long)cnt);
+    for (int64_t j = threadIdx.x; j < nleaf; j += blockDim.x) {
+      const int64_t lo = leaf_lo[j], hi = leaf_lo[j + 1];
+      // first run of this cluster at or after position lo
+      uint32_t a = b, z = e;
+      const K target = base + (K)lo;
+      while (a < z) {
+        const uint32_t mid = (a + z) >> 1;
+        if (seg_key[mid] < target) a = mid + 1; else z = mid;
+      }
+      leaf_val[j] = leaf_value<K>(lo, hi - lo, a, e, seg_key, seg_w, base);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      counts[c] = s_cnt;
+      nrm[c] = __dsqrt_rn(combine_leaves(dim, leaf_val));
+    }
+    __syncthreads();
   }
 }
 
@@ -356,8 +408,13 @@ int update_count_impl(int64_t n_obj, const int64_t* row_ptr, const int32_t* term
   }
   clseg_kernel<K><<<grid_for(k + 1, T), T, 0, st>>>(k, dim, w.n_seg, w.seg_key, w.cl_seg);
   IVFKM_CHECK_LAUNCH();
-  norm_kernel<K><<<grid_for(k + 1, 64), 64, 0, st>>>(k, dim, sizes, prev_ptr, w.cl_seg,
-                                                     w.seg_key, w.seg_w, w.head, w.nrm, w.counts);
+  const int64_t nleaf = enum_leaves(dim, nullptr);
+  const size_t nsmem = (size_t)nleaf * 8 + (size_t)(nleaf + 1) * 4;
+  if (nsmem > 200 * 1024) return IVFKM_E_UNSUPPORTED;  // D beyond ~2.4M terms
+  IVFKM_TRY(cudaFuncSetAttribute(norm_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)nsmem));
+  norm_kernel<K><<<(int)std::min<int64_t>(k, kNumSM * 8), 256, nsmem, st>>>(
+      k, dim, nleaf, sizes, prev_ptr, w.cl_seg, w.seg_key, w.seg_w, w.head, w.nrm, w.counts);
   IVFKM_CHECK_LAUNCH();
   size_t cb = w.cub_bytes;
   IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.counts, new_ptr, (int)(k + 1), st));

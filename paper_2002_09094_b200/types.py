@@ -52,9 +52,14 @@ def _rows_strictly_increasing(arr: np.ndarray, indptr: np.ndarray) -> bool:
 
 
 def _row_sq_norms(indptr: np.ndarray, values: np.ndarray) -> np.ndarray:
+    """Per-row sum of squares (validation only: the 1e-12 unit-norm check)."""
     n = indptr.size - 1
-    return np.bincount(np.repeat(np.arange(n), np.diff(indptr)), weights=values * values,
-                       minlength=n)
+    out = np.zeros(n)
+    if values.size == 0 or n == 0:
+        return out
+    nonempty = indptr[1:] > indptr[:-1]
+    out[nonempty] = np.add.reduceat(values * values, indptr[:-1][nonempty])
+    return out
 
 
 @dataclass(frozen=True, eq=False)

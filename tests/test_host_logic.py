@@ -1,0 +1,261 @@
+"""CPU tests: the C-ABI library loads and exports every declared symbol, the
+host-side numerics the kernels implement (pairwise-norm replay, exact
+objective accumulator, error window) are right, the mirrored types validate
+like the reference, and the generator follows its spec."""
+
+import math
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+# ---------------------------------------------------------------- C ABI
+
+def _declared_symbols():
+    text = (ROOT / "include" / "ivfkm.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(ivfkm_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2002_09094_b200 import _lib
+
+    lib = _lib.load()
+    declared = _declared_symbols()
+    assert len(declared) >= 15
+    for name in declared:
+        assert hasattr(lib, name), name
+    # the ctypes table binds exactly the header's entry points
+    assert sorted(_lib.SIGNATURES) == declared
+
+
+def test_abi_constants_and_struct_layout():
+    import ctypes
+
+    from paper_2002_09094_b200 import _lib
+
+    lib = _lib.load()
+    text = (ROOT / "include" / "ivfkm.h").read_text()
+    assert f"#define IVFKM_OBJ_LIMBS {_lib.IVFKM_OBJ_LIMBS}" in text
+    assert f"#define IVFKM_MAXC {_lib.IVFKM_MAXC}" in text
+    assert ctypes.sizeof(_lib.Stats) == 6 * 8 + 8 * _lib.IVFKM_OBJ_LIMBS
+    assert lib.ivfkm_version() >= 1
+    assert lib.ivfkm_error_string(-4) == b"workspace too small"
+    assert lib.ivfkm_bivf_nblk(100) == 8 and lib.ivfkm_bivf_nblk(1000) == 32
+    assert lib.ivfkm_bivf_nblk(60000) == 1880
+    assert lib.ivfkm_assign_workspace_size(1000, 10) > 1000 * 4 * 36
+    assert lib.ivfkm_update_workspace_size(10, 100, 5, 50) > 0
+
+
+def test_host_entry_point_reports_missing_gpu_or_range():
+    """ivfkm_assign_ivf_host validates ids like the reference (data.py:261-262)."""
+    import ctypes
+
+    from paper_2002_09094_b200 import _lib
+
+    lib = _lib.load()
+    ip = np.array([0, 1], np.int64)
+    t = np.array([9], np.int32)  # term 9 > dim 4
+    v = np.array([1.0])
+    mp = np.array([0, 0, 0, 0, 0], np.int64)
+    lab = np.zeros(1, np.int32)
+    ctr = np.zeros(5, np.int64)
+    P = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+    rc = lib.ivfkm_assign_ivf_host(1, P(ip), P(t), P(v), 4, P(mp), None, None, 2, P(lab), P(ctr))
+    assert rc in (-5, -6)  # no GPU here, or the range error when one is present
+
+
+# ---------------------------------------------------------------- numerics replays
+
+def _leaves(D):
+    out = []
+    stack = [(0, D)]
+    while stack:
+        lo, n = stack.pop()
+        if n <= 128:
+            out.append((lo, n))
+            continue
+        n2 = n // 2
+        n2 -= n2 % 8
+        stack.append((lo + n2, n - n2))
+        stack.append((lo, n2))
+    return out
+
+
+def _leaf_value(lo, n, pos, w2):
+    sel = (pos >= lo) & (pos < lo + n)
+    p, x = pos[sel], w2[sel]
+    if n < 8:
+        res = 0.0
+        for val in x:
+            res += val
+        return res
+    lim = lo + n - n % 8
+    r = [0.0] * 8
+    res_tail = []
+    for pi, val in zip(p, x):
+        if pi < lim:
+            r[(pi - lo) & 7] += val
+        else:
+            res_tail.append(val)
+    res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]))
+    for val in res_tail:
+        res += val
+    return res
+
+
+def _combine(D, vals):
+    it = iter(vals)
+
+    def pw(n):
+        if n <= 128:
+            return next(it)
+        n2 = n // 2
+        n2 -= n2 % 8
+        a = pw(n2)
+        b = pw(n - n2)
+        return a + b
+
+    return pw(D)
+
+
+@pytest.mark.parametrize("D", [1, 5, 7, 8, 100, 128, 129, 1000, 10_000, 100_000, 141_000])
+def test_pairwise_norm_replay_matches_numpy(D):
+    """The norm kernel's leaf/combine replay equals np.sum(w*w) bit for bit
+    (variants.py:298 computes nrm = np.sqrt(np.sum(w * w)))."""
+    rng = np.random.default_rng(D)
+    for density in (0.001, 0.05, 0.6):
+        w = np.zeros(D)
+        m = rng.random(D) < density
+        w[m] = rng.random(m.sum()) / 7.0
+        pos = np.flatnonzero(w)
+        w2 = w[pos] * w[pos]
+        vals = [_leaf_value(lo, n, pos, w2) for lo, n in _leaves(D)]
+        assert _combine(D, vals) == float(np.sum(w * w))
+
+
+def _add_exact(s, limbs):
+    """Python replay of add_exact in assign.cu."""
+    if s == 0.0:
+        return
+    bits = np.array([s]).view(np.uint64)[0].item()
+    ex = (bits >> 52) & 0x7FF
+    m = bits & ((1 << 52) - 1)
+    b = 0
+    if ex:
+        m |= 1 << 52
+        b = ex - 1
+    idx, sh = b >> 5, b & 31
+    sg = -1 if bits >> 63 else 1
+    c0 = (m << sh) & 0xFFFFFFFF
+    t = (m >> (32 - sh)) if sh else (m >> 32)
+    limbs[idx] += sg * c0
+    limbs[idx + 1] += sg * (t & 0xFFFFFFFF)
+    limbs[idx + 2] += sg * (t >> 32)
+
+
+def test_exact_objective_accumulator_equals_fsum():
+    """The fixed-point superaccumulator, rounded once on the host, is math.fsum
+    (clustering.py:119)."""
+    from paper_2002_09094_b200.engine import objective_from_limbs
+
+    rng = np.random.default_rng(1)
+    cases = [rng.random(5000), rng.random(2000) ** 9 - 0.3, np.array([1e-300, 1.0, -1.0]),
+             np.array([5e-324, 2.0 ** -1022, 0.75]), np.array([3.9, -3.9, 1e-17])]
+    for x in cases:
+        limbs = [0] * 34
+        for s in x:
+            _add_exact(float(s), limbs)
+        assert objective_from_limbs(limbs) == math.fsum(x.tolist())
+
+
+def test_error_window_is_rigorous():
+    """|rho32 - rho64| stays inside the kernel's eps_i on adversarial-ish rows."""
+    rng = np.random.default_rng(2)
+    for n in (1, 10, 230, 2000):
+        for _ in range(20):
+            v = rng.random(n)
+            v /= np.linalg.norm(v)
+            u = rng.random(n) * (rng.random(n) < 0.7)
+            u /= max(np.linalg.norm(u), 1e-300)
+            acc32 = np.float32(0)
+            for a, b in zip(v.astype(np.float32), u.astype(np.float32)):
+                acc32 = np.float32(np.fma(a, b, acc32)) if hasattr(np, "fma") else \
+                    np.float32(np.float64(a) * np.float64(b) + np.float64(acc32))
+            acc64 = 0.0
+            for a, b in zip(v, u):
+                acc64 = acc64 + a * b
+            eps = ((n + 3) * 2.0 ** -24 + n * 2.0 ** -50) * (1 + 1e-9) * (1 + 1e-6) + \
+                (n + 1) * 2.0 ** -125
+            assert abs(float(acc32) - acc64) <= eps
+
+
+# ---------------------------------------------------------------- types
+
+def test_types_validate_like_reference():
+    from paper_2002_09094_b200 import Assignment, Dataset, MeanSet
+
+    with pytest.raises(ValueError, match="malformed indptr"):
+        Dataset(4, np.array([1, 2]), np.array([1], np.int32), np.array([1.0]))
+    with pytest.raises(ValueError, match="1..dim"):
+        Dataset(4, np.array([0, 1]), np.array([5], np.int32), np.array([1.0]))
+    with pytest.raises(ValueError, match="strictly increasing"):
+        Dataset(4, np.array([0, 2]), np.array([2, 2], np.int32), np.array([0.6, 0.8]))
+    with pytest.raises(ValueError, match="non-unit"):
+        Dataset(4, np.array([0, 1]), np.array([1], np.int32), np.array([0.5]), normalized=True)
+    with pytest.raises(ValueError, match="unit L2"):
+        MeanSet.from_csr(np.array([0, 1]), np.array([1], np.int32), np.array([0.5]), 4)
+    with pytest.raises(ValueError, match="1..k"):
+        Assignment(np.array([0, 1]), np.array([1, 1]))
+    a = Assignment.from_labels(np.array([1, 1, 2]), 3)
+    assert a.sizes.tolist() == [2, 1, 0] and a.n == 3 and a.k == 3
+    assert not a.labels.flags.writeable
+
+
+def test_init_means_matches_oracle(tiny):
+    from oracle import oracle as O
+    from paper_2002_09094_b200.clustering import init_means
+
+    m = init_means(tiny, 2, seed=5, representation="sparse_inverted")
+    o = O.init_means(tiny, 2, 5)
+    assert np.array_equal(m.indptr, o.indptr) and np.array_equal(m.term_ids, o.term_ids)
+    assert np.array_equal(m.values, o.values)
+    with pytest.raises(ValueError):
+        init_means(tiny, 4, seed=1)
+
+
+# ---------------------------------------------------------------- generator
+
+def test_synth_deterministic_and_well_formed():
+    from paper_2002_09094_b200 import Dataset, synth
+
+    spec = synth.CONFIGS[1]["corpus"].scaled(3000, 20000, seed=3)
+    a = synth.make_corpus(spec)
+    b = synth.make_corpus(spec)
+    for x, y in zip(a[:3], b[:3]):
+        assert np.array_equal(x, y)
+    ip, t, v, dropped = a
+    ds = Dataset(spec.dim, ip, t, v, normalized=True)  # validates 1-based, increasing, unit
+    rows = np.diff(ip)
+    assert rows.min() >= 1 and rows.max() <= 2000
+    assert 150 < rows.mean() < 320  # lognormal mean 230, clipped
+    assert np.all(v > 0)
+    df = ds.doc_freq
+    # Zipf: the most frequent kept term is a top-ranked one; a term in every
+    # row has idf 0 and is dropped (df == N never survives, io.py:153-154)
+    assert df.max() < ds.n and int(np.argmax(df)) < 5
+
+
+def test_synth_config_shapes():
+    from paper_2002_09094_b200 import synth
+
+    c = synth.CONFIGS
+    assert (c[0]["corpus"].n, c[0]["corpus"].dim, c[0]["k"]) == (20000, 10000, 100)
+    assert (c[1]["corpus"].n, c[1]["corpus"].dim, c[1]["k"]) == (300000, 100000, 1000)
+    assert c[2]["corpus"] is c[1]["corpus"] and c[2]["k"] == 10000
+    assert (c[3]["corpus"].n, c[3]["corpus"].dim, c[3]["k"]) == (8200000, 141000, 10000)
+    assert c[4]["corpus"] is c[3]["corpus"] and c[4]["k"] == 60000
