@@ -63,9 +63,10 @@ int ivfkm_version(void);
 int ivfkm_device_count(void);
 
 /* ---- bitmap-block inverted file (BIVF) of the means ---------------------
- * headers[2*(t*nblk + b) + 0] = mask: bit j set <=> mean 32*b+j holds term t;
- * headers[2*(t*nblk + b) + 1] = offset: that mean's value sits at
- *   val[offset + popc(mask & ((1u<<j)-1))].
+ * headers is planar, 2*dim*nblk + 1 uint32:
+ * headers[t*nblk + b] = mask: bit j set <=> mean 32*b+j holds term t;
+ * headers[dim*nblk + t*nblk + b] = offset: that mean's value sits at
+ *   val[offset + popc(mask & ((1u<<j)-1))]; headers[2*dim*nblk] = total.
  * Values are stored term-major, mean ascending — the order of
  * MeanSet.inverted (means.py:169-179).  val32 feeds the fp32 screening pass,
  * val64 the exact fp64 rescoring.                                            */
@@ -76,7 +77,7 @@ size_t ivfkm_bivf_workspace_size(int64_t dim, int64_t k);
  * an id outside [0,k) / [0,dim) gives IVFKM_E_RANGE.                        */
 int ivfkm_bivf_build(int64_t k, int64_t dim, int major, int64_t nrows,
                      const int64_t* ptr /*[dev] nrows+1*/, const int32_t* cols /*[dev]*/,
-                     const double* vals /*[dev]*/, uint32_t* headers /*[dev] 2*dim*nblk*/,
+                     const double* vals /*[dev]*/, uint32_t* headers /*[dev] 2*dim*nblk+1*/,
                      float* val32 /*[dev] nnz*/, double* val64 /*[dev] nnz*/, void* ws,
                      size_t ws_bytes, ivfkm_stream_t stream);
 
@@ -92,8 +93,9 @@ size_t ivfkm_assign_workspace_size(int64_t n_obj, int64_t k);
 /* Tuning: rowcap = row entries staged in shared memory per pass (default 1024;
  * longer rows run in several passes), smem_limit = shared-memory budget per
  * CTA in bytes (default 225 KB, min 1 KB; a smaller budget forces the thread-block
- * cluster split).  Out-of-range values leave the setting unchanged.         */
-void ivfkm_set_tuning(int rowcap, int smem_limit);
+ * cluster split), rr = 32-mean blocks per warp span (2, 4 or 8; 0 = automatic).
+ * Out-of-range values leave the setting unchanged.                          */
+void ivfkm_set_tuning(int rowcap, int smem_limit, int rr);
 int ivfkm_assign(int64_t n_obj, const int64_t* row_ptr /*[dev] n+1*/,
                  const int32_t* terms /*[dev]*/, const float* val32 /*[dev]*/,
                  const double* val64 /*[dev]*/, const double* xnorm /*[dev] n or NULL (=1)*/,

@@ -58,7 +58,8 @@ struct ScreenParams {
   const double* xnorm;
   int64_t k;
   int64_t nblk;
-  const uint2* hdr;
+  const uint32_t* masks;  // [dim][nblk]
+  const uint32_t* offs;   // [dim][nblk] (+1: total)
   const float* pv32;
   double mu_max;
   int cta_blocks;  // 32-mean blocks held by one CTA (multiple of RR)
@@ -90,8 +91,53 @@ __device__ __forceinline__ void better(float& bv, int& bc, float ov, int oc) {
   }
 }
 
+// Masks of RR consecutive blocks of one term, loaded with vector loads (every
+// lane reads the same address: one broadcast wavefront).
 template <int RR>
-__global__ void __launch_bounds__(512) screen_kernel(ScreenParams p) {
+struct MaskPack {
+  uint32_t m[RR];
+  __device__ __forceinline__ void load(const uint32_t* __restrict__ src) {
+    if constexpr (RR % 4 == 0) {
+#pragma unroll
+      for (int q = 0; q < RR / 4; ++q) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(src) + q);
+        m[4 * q] = v.x;
+        m[4 * q + 1] = v.y;
+        m[4 * q + 2] = v.z;
+        m[4 * q + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < RR / 2; ++q) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(src) + q);
+        m[2 * q] = v.x;
+        m[2 * q + 1] = v.y;
+      }
+    }
+  }
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int r = 0; r < RR; ++r) m[r] = 0u;
+  }
+};
+
+// One object nonzero (value v) against RR blocks: lane-owned mean 32*b+lane
+// reads its value at o_b + popc(mask_b below the lane); o_{b+1} = o_b + popc(mask_b).
+template <int RR>
+__device__ __forceinline__ void gather_values(const MaskPack<RR>& mk, uint32_t o,
+                                              const float* __restrict__ pv, unsigned lanebit,
+                                              unsigned lt, float (&u)[RR]) {
+#pragma unroll
+  for (int r = 0; r < RR; ++r) {
+    const uint32_t mr = mk.m[r];
+    u[r] = 0.f;
+    if (mr & lanebit) u[r] = __ldg(pv + (o + (uint32_t)__popc(mr & lt)));
+    o += (uint32_t)__popc(mr);
+  }
+}
+
+template <int RR>
+__global__ void __launch_bounds__(512, 1) screen_kernel(ScreenParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ ScreenShared sh;
   float* rho = reinterpret_cast<float*>(smem);
@@ -106,10 +152,26 @@ __global__ void __launch_bounds__(512) screen_kernel(ScreenParams p) {
   const int64_t obj = blockIdx.x / p.nsplit;
   if (obj >= p.n_obj) return;  // whole cluster shares obj
   const int64_t rb = p.row_ptr[obj], re = p.row_ptr[obj + 1];
+  const int64_t nblk = p.nblk;
   const int64_t blk0 = (int64_t)z * p.cta_blocks;
+  const int64_t blk1 = min(blk0 + (int64_t)p.cta_blocks, nblk);
   const int nspans = p.cta_blocks / RR;
-  const unsigned lt = (1u << lane) - 1u;
-  unsigned long long post = 0;
+  const unsigned lanebit = 1u << lane;
+  const unsigned lt = lanebit - 1u;
+  // The bases go through shared memory so they stay in registers: ptxas would
+  // otherwise re-load kernel parameters from the constant bank inside every
+  // predicated gather (one extra LDC per posting block).
+  __shared__ const void* s_base[3];
+  if (threadIdx.x == 0) {
+    s_base[0] = p.masks;
+    s_base[1] = p.offs;
+    s_base[2] = p.pv32;
+  }
+  __syncthreads();
+  const uint32_t* __restrict__ masks = static_cast<const uint32_t*>(s_base[0]);
+  const uint32_t* __restrict__ offs = static_cast<const uint32_t*>(s_base[1]);
+  const float* __restrict__ pv = static_cast<const float*>(s_base[2]);
+  unsigned long long post = 0;  // postings of this CTA's blocks (counters.py:71-81)
 
   int64_t c0 = rb;
   do {
@@ -117,8 +179,11 @@ __global__ void __launch_bounds__(512) screen_kernel(ScreenParams p) {
     const int cn = (int)(rem < p.rowcap ? rem : p.rowcap);
     __syncthreads();
     for (int j = threadIdx.x; j < cn; j += blockDim.x) {
-      s_term[j] = p.terms[c0 + j];
+      const int32_t t = p.terms[c0 + j];
+      s_term[j] = t;
       s_val[j] = p.val32[c0 + j];
+      if (blk1 > blk0)
+        post += __ldg(offs + (int64_t)t * nblk + blk1) - __ldg(offs + (int64_t)t * nblk + blk0);
     }
     __syncthreads();
     const bool first = (c0 == rb);
@@ -127,40 +192,40 @@ __global__ void __launch_bounds__(512) screen_kernel(ScreenParams p) {
       float acc[RR];
 #pragma unroll
       for (int r = 0; r < RR; ++r) acc[r] = first ? 0.f : rho[(sp * RR + r) * 32 + lane];
-      const bool hl = lane < RR && (gb + lane) < p.nblk;
-      const uint2* hrow = p.hdr + gb + lane;
-      auto ldh = [&](int e) -> uint2 {
-        uint2 h = make_uint2(0u, 0u);
-        if (hl && e < cn) h = __ldg(hrow + (int64_t)s_term[e] * p.nblk);
-        return h;
-      };
-      uint2 hA = ldh(0), hB = ldh(1);
-      for (int e = 0; e < cn; e += 2) {
-        const uint2 hC = ldh(e + 2), hD = ldh(e + 3);
-        const float vA = s_val[e];
-        const float vB = (e + 1 < cn) ? s_val[e + 1] : 0.f;
+      if (gb < nblk) {  // nblk is a multiple of RR: a span is all in or all out
+        // 32-bit row arithmetic: dim * nblk < 2^31 is checked at build time
+        const uint32_t nb32 = (uint32_t)nblk, gb32 = (uint32_t)gb;
+        auto ld = [&](int e, MaskPack<RR>& mk, uint32_t& o) {
+          if (e < cn) {
+            const uint32_t row = (uint32_t)s_term[e] * nb32 + gb32;
+            mk.load(masks + row);
+            o = __ldg(offs + row);
+          } else {
+            mk.zero();
+            o = 0u;
+          }
+        };
+        // software pipeline (unrolled by two): values of entries e, e+1 and
+        // masks of e+2 are in flight while entry e accumulates
+        MaskPack<RR> mk;
+        uint32_t o;
         float uA[RR], uB[RR];
+        ld(0, mk, o);
+        gather_values<RR>(mk, o, pv, lanebit, lt, uA);
+        ld(1, mk, o);
+        for (int e = 0; e < cn; e += 2) {
+          gather_values<RR>(mk, o, pv, lanebit, lt, uB);  // entry e+1 (zeros past the end)
+          ld(e + 2, mk, o);
+          const float vA = s_val[e];
+          // fma(v, 0, acc) == acc exactly: absent postings cost no rounding
 #pragma unroll
-        for (int r = 0; r < RR; ++r) {
-          const unsigned m = __shfl_sync(kFull, hA.x, r);
-          const unsigned o = __shfl_sync(kFull, hA.y, r);
-          uA[r] = ((m >> lane) & 1u) ? __ldg(p.pv32 + o + __popc(m & lt)) : 0.f;
-          post += __popc(m);
+          for (int r = 0; r < RR; ++r) acc[r] = fmaf(vA, uA[r], acc[r]);
+          gather_values<RR>(mk, o, pv, lanebit, lt, uA);  // entry e+2
+          ld(e + 3, mk, o);
+          const float vB = (e + 1 < cn) ? s_val[e + 1] : 0.f;
+#pragma unroll
+          for (int r = 0; r < RR; ++r) acc[r] = fmaf(vB, uB[r], acc[r]);
         }
-#pragma unroll
-        for (int r = 0; r < RR; ++r) {
-          const unsigned m = __shfl_sync(kFull, hB.x, r);
-          const unsigned o = __shfl_sync(kFull, hB.y, r);
-          uB[r] = ((m >> lane) & 1u) ? __ldg(p.pv32 + o + __popc(m & lt)) : 0.f;
-          post += __popc(m);
-        }
-        // fma(v, 0, acc) == acc exactly, so absent postings cost no rounding.
-#pragma unroll
-        for (int r = 0; r < RR; ++r) acc[r] = fmaf(vA, uA[r], acc[r]);
-#pragma unroll
-        for (int r = 0; r < RR; ++r) acc[r] = fmaf(vB, uB[r], acc[r]);
-        hA = hC;
-        hB = hD;
       }
 #pragma unroll
       for (int r = 0; r < RR; ++r) rho[(sp * RR + r) * 32 + lane] = acc[r];
@@ -187,8 +252,8 @@ __global__ void __launch_bounds__(512) screen_kernel(ScreenParams p) {
     const float ov = __shfl_xor_sync(kFull, bv, off);
     const int oc = __shfl_xor_sync(kFull, bc, off);
     better(bv, bc, ov, oc);
+    post += __shfl_xor_sync(kFull, post, off);
   }
-  // every lane counted the same warp-uniform masks: keep lane 0's tally
   if (lane == 0) {
     sh.red_v[warp] = bv;
     sh.red_c[warp] = bc;
@@ -291,7 +356,8 @@ struct ExactCtx {
   const int32_t* terms;
   const double* val64;
   int64_t nblk;
-  const uint2* hdr;
+  const uint32_t* masks;
+  const uint32_t* offs;
   const double* pv64;
 };
 
@@ -307,10 +373,11 @@ __device__ double exact_score_warp(const ExactCtx& x, int64_t rb, int64_t re, in
     double prod = 0.0;
     if (h < re) {
       const int64_t t = x.terms[h];
-      const uint2 hd = __ldg(x.hdr + t * x.nblk + blk);
-      if (hd.x & bit) {
+      const uint32_t m = __ldg(x.masks + t * x.nblk + blk);
+      if (m & bit) {
         present = true;
-        prod = __dmul_rn(x.val64[h], __ldg(x.pv64 + hd.y + __popc(hd.x & (bit - 1u))));
+        const uint32_t o = __ldg(x.offs + t * x.nblk + blk);
+        prod = __dmul_rn(x.val64[h], __ldg(x.pv64 + (o + (uint32_t)__popc(m & (bit - 1u)))));
       }
     }
     unsigned pm = __ballot_sync(kFull, present);
@@ -330,9 +397,12 @@ __device__ double exact_score_thread(const ExactCtx& x, int64_t rb, int64_t re, 
   const unsigned bit = 1u << (c & 31);
   for (int64_t h = rb; h < re; ++h) {
     const int64_t t = x.terms[h];
-    const uint2 hd = __ldg(x.hdr + t * x.nblk + blk);
-    if (hd.x & bit)
-      acc = __dadd_rn(acc, __dmul_rn(x.val64[h], __ldg(x.pv64 + hd.y + __popc(hd.x & (bit - 1u)))));
+    const uint32_t m = __ldg(x.masks + t * x.nblk + blk);
+    if (m & bit) {
+      const uint32_t o = __ldg(x.offs + t * x.nblk + blk);
+      acc = __dadd_rn(acc, __dmul_rn(x.val64[h],
+                                     __ldg(x.pv64 + (o + (uint32_t)__popc(m & (bit - 1u))))));
+    }
   }
   return acc;
 }
@@ -544,10 +614,10 @@ struct Plan {
   size_t smem;
 };
 
-int plan_screen(int64_t k, int rowcap, int smem_limit, Plan* out) {
+int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
   const int64_t nblk = ivfkm_bivf_nblk(k);
   Plan pl;
-  pl.rr = nblk >= 32 ? 8 : 2;
+  pl.rr = rr ? rr : (nblk >= 32 ? 8 : 2);
   pl.rowcap = rowcap;
   const size_t stage = (size_t)rowcap * 8;
   pl.nsplit = 0;
@@ -607,9 +677,11 @@ extern "C" size_t ivfkm_assign_workspace_size(int64_t n_obj, int64_t /*k*/) {
 // thread-block-cluster split at small k (used by the tests).
 static int g_rowcap = 1024;
 static int g_smem_limit = kSmemLimit - 2048;  // leave room for static smem
-extern "C" void ivfkm_set_tuning(int rowcap, int smem_limit) {
+static int g_rr = 0;                          // 0: automatic
+extern "C" void ivfkm_set_tuning(int rowcap, int smem_limit, int rr) {
   if (rowcap >= 32 && rowcap <= 8192) g_rowcap = rowcap / 32 * 32;
   if (smem_limit >= 1024 && smem_limit <= kSmemLimit - 2048) g_smem_limit = smem_limit;
+  if (rr == 0 || rr == 2 || rr == 4 || rr == 8) g_rr = rr;
 }
 
 namespace {
@@ -631,7 +703,7 @@ struct AssignArgs {
 
 int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
   Plan pl;
-  int rc = plan_screen(a.k, g_rowcap, g_smem_limit, &pl);
+  int rc = plan_screen(a.k, g_rowcap, g_smem_limit, g_rr, &pl);
   if (rc) return rc;
   ScreenParams sp;
   sp.n_obj = a.n_obj;
@@ -641,7 +713,8 @@ int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
   sp.xnorm = a.xnorm;
   sp.k = a.k;
   sp.nblk = ivfkm_bivf_nblk(a.k);
-  sp.hdr = reinterpret_cast<const uint2*>(a.headers);
+  sp.masks = a.headers;
+  sp.offs = a.headers + a.dim * sp.nblk;
   sp.pv32 = a.pval32;
   sp.mu_max = a.mu_max > 0 ? a.mu_max : 1.0;
   sp.cta_blocks = pl.cta_blocks;
@@ -653,7 +726,11 @@ int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
   sp.q_cnt = w.q_cnt;
   sp.q_cid = w.q_cid;
   sp.stats = a.stats;
-  return pl.rr == 8 ? launch_screen<8>(pl, sp, st) : launch_screen<2>(pl, sp, st);
+  switch (pl.rr) {
+    case 8: return launch_screen<8>(pl, sp, st);
+    case 4: return launch_screen<4>(pl, sp, st);
+    default: return launch_screen<2>(pl, sp, st);
+  }
 }
 
 int finish_impl(const AssignArgs& a, const AssignWs& w, const int32_t* prev_labels,
@@ -664,7 +741,8 @@ int finish_impl(const AssignArgs& a, const AssignWs& w, const int32_t* prev_labe
   fp.x.terms = a.terms;
   fp.x.val64 = a.val64;
   fp.x.nblk = ivfkm_bivf_nblk(a.k);
-  fp.x.hdr = reinterpret_cast<const uint2*>(a.headers);
+  fp.x.masks = a.headers;
+  fp.x.offs = a.headers + a.dim * fp.x.nblk;
   fp.x.pv64 = a.pval64;
   fp.label32 = w.label32;
   fp.slot_of = w.slot_of;
@@ -752,7 +830,8 @@ extern "C" int ivfkm_score_labels(int64_t n_obj, const int64_t* row_ptr, const i
   x.terms = terms;
   x.val64 = val64;
   x.nblk = ivfkm_bivf_nblk(k);
-  x.hdr = reinterpret_cast<const uint2*>(headers);
+  x.masks = headers;
+  x.offs = headers + dim * x.nblk;
   x.pv64 = pval64;
   score_labels_kernel<<<grid_for(n_obj, 8), 256, 0, st>>>(n_obj, x, labels, sims);
   IVFKM_CHECK_LAUNCH();

@@ -64,6 +64,8 @@ __device__ __forceinline__ int64_t row_of(const int64_t* __restrict__ ptr, int64
   return lo;
 }
 
+__device__ __forceinline__ int64_t nh_of(int64_t dim, int64_t nblk) { return dim * nblk; }
+
 // One thread per entry (grid-stride), so a few long rows (k means holding
 // ~20k terms each) still spread over the whole GPU.
 __global__ void bivf_mask_kernel(int major, int64_t nrows, const int64_t* __restrict__ ptr,
@@ -81,7 +83,7 @@ __global__ void bivf_mask_kernel(int major, int64_t nrows, const int64_t* __rest
       atomicAdd(err, 1u);
       continue;
     }
-    atomicOr(&hdr[2 * (t * nblk + (c >> 5))], 1u << (c & 31));
+    atomicOr(&hdr[t * nblk + (c >> 5)], 1u << (c & 31));
   }
 }
 
@@ -89,14 +91,14 @@ __global__ void bivf_popc_kernel(int64_t nh, const unsigned int* __restrict__ hd
                                  unsigned int* __restrict__ cnt) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= nh;
        i += (int64_t)gridDim.x * blockDim.x)
-    cnt[i] = i < nh ? __popc(hdr[2 * i]) : 0u;
+    cnt[i] = i < nh ? __popc(hdr[i]) : 0u;
 }
 
 __global__ void bivf_offset_kernel(int64_t nh, const unsigned int* __restrict__ off,
                                    unsigned int* __restrict__ hdr) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nh;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= nh;
        i += (int64_t)gridDim.x * blockDim.x)
-    hdr[2 * i + 1] = off[i];
+    hdr[nh + i] = off[i];
 }
 
 __global__ void bivf_scatter_kernel(int major, int64_t nrows, const int64_t* __restrict__ ptr,
@@ -112,8 +114,8 @@ __global__ void bivf_scatter_kernel(int major, int64_t nrows, const int64_t* __r
     const int64_t c = major == 0 ? r : col;
     const int64_t t = major == 0 ? col : r;
     if (c < 0 || c >= k || t < 0 || t >= dim) continue;
-    const uint2 h = *reinterpret_cast<const uint2*>(&hdr[2 * (t * nblk + (c >> 5))]);
-    const unsigned pos = h.y + __popc(h.x & ((1u << (c & 31)) - 1u));
+    const int64_t hb = t * nblk + (c >> 5);
+    const unsigned pos = hdr[nh_of(dim, nblk) + hb] + __popc(hdr[hb] & ((1u << (c & 31)) - 1u));
     const double v = vals[q];
     v32[pos] = static_cast<float>(v);
     v64[pos] = v;
@@ -141,7 +143,7 @@ extern "C" int ivfkm_bivf_build(int64_t k, int64_t dim, int major, int64_t nrows
   BivfWs w = carve(ws, dim, k, &need);
   if (ws_bytes < need) return IVFKM_E_WORKSPACE;
   cudaStream_t st = as_stream(stream_);
-  IVFKM_TRY(cudaMemsetAsync(headers, 0, sizeof(uint32_t) * 2 * nh, st));
+  IVFKM_TRY(cudaMemsetAsync(headers, 0, sizeof(uint32_t) * nh, st));
   IVFKM_TRY(cudaMemsetAsync(w.err, 0, sizeof(unsigned int), st));
   const int threads = 256;
   bivf_mask_kernel<<<kNumSM * 8, threads, 0, st>>>(
@@ -151,7 +153,7 @@ extern "C" int ivfkm_bivf_build(int64_t k, int64_t dim, int major, int64_t nrows
   IVFKM_CHECK_LAUNCH();
   size_t cb = w.cub_bytes;
   IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.cnt, w.off, (int)(nh + 1), st));
-  bivf_offset_kernel<<<grid_for(nh, threads), threads, 0, st>>>(nh, w.off, headers);
+  bivf_offset_kernel<<<grid_for(nh + 1, threads), threads, 0, st>>>(nh, w.off, headers);
   IVFKM_CHECK_LAUNCH();
   bivf_scatter_kernel<<<kNumSM * 8, threads, 0, st>>>(
       major, nrows, ptr, cols, vals, k, dim, nblk, headers, val32, val64);

@@ -108,7 +108,7 @@ extern "C" int ivfkm_assign_ivf_host(int64_t n, const int64_t* indptr, const int
   IVFKM_TRY(d_mp.alloc(sizeof(int64_t) * (dim + 1)));
   IVFKM_TRY(d_mc.alloc(sizeof(int32_t) * mnz));
   IVFKM_TRY(d_mv.alloc(sizeof(double) * mnz));
-  IVFKM_TRY(d_hdr.alloc(sizeof(uint32_t) * 2 * dim * nblk));
+  IVFKM_TRY(d_hdr.alloc(sizeof(uint32_t) * (2 * dim * nblk + 1)));
   IVFKM_TRY(d_p32.alloc(sizeof(float) * mnz));
   IVFKM_TRY(d_p64.alloc(sizeof(double) * mnz));
   IVFKM_TRY(d_bws.alloc(bws));

@@ -165,13 +165,13 @@ class LloydEngine:
         self.stats_host = torch.zeros(C.sizeof(_lib.Stats), dtype=u8).pin_memory() \
             if torch.cuda.is_available() else torch.zeros(C.sizeof(_lib.Stats), dtype=u8)
         self.total_host = torch.zeros(1, dtype=torch.int64).pin_memory()
-        self.rowcap = max(32, min(2048, (dd.max_row + 31) // 32 * 32))
+        self.rowcap = max(32, min(512, (dd.max_row + 31) // 32 * 32))
         self.launches = 0  # our kernels launched (for the bench's gpu_launches)
 
     # -- means ---------------------------------------------------------------
     def build_bivf(self, dm: DeviceMeans) -> DeviceMeans:
         dev = self.device
-        dm.headers = torch.empty(2 * dm.dim * self.nblk, dtype=torch.int32, device=dev)
+        dm.headers = torch.empty(2 * dm.dim * self.nblk + 1, dtype=torch.int32, device=dev)
         dm.pv32 = torch.empty(max(dm.nnz, 1), dtype=torch.float32, device=dev)
         dm.pv64 = torch.empty(max(dm.nnz, 1), dtype=torch.float64, device=dev)
         rc = self.lib.ivfkm_bivf_build(self.k, dm.dim, 0, self.k, _p(dm.ptr), _p(dm.terms),
@@ -196,7 +196,7 @@ class LloydEngine:
         if prev is not None and prev.data_ptr() == out.data_ptr():
             self.cur ^= 1
             out = self.labels[self.cur]
-        self.lib.ivfkm_set_tuning(self.rowcap, 0)
+        self.lib.ivfkm_set_tuning(self.rowcap, 0, -1)
         st = _stream()
         if events is not None:
             events[0].record()

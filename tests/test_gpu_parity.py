@@ -175,7 +175,7 @@ def tuning():
 
     lib = _lib.load()
     yield lib.ivfkm_set_tuning
-    lib.ivfkm_set_tuning(1024, 225 * 1024)
+    lib.ivfkm_set_tuning(1024, 225 * 1024, 0)
 
 
 def _assign_raw(ds, means, rowcap=None, smem=None):
@@ -187,11 +187,11 @@ def _assign_raw(ds, means, rowcap=None, smem=None):
     if rowcap:
         eng.rowcap = rowcap
     if smem:
-        eng.lib.ivfkm_set_tuning(eng.rowcap, smem)
+        eng.lib.ivfkm_set_tuning(eng.rowcap, smem, -1)
     dm = eng.upload_means(means)
     lab = eng.assign(dm, None)
     st = eng.read_stats()
-    eng.rowcap = max(32, min(2048, (eng.dd.max_row + 31) // 32 * 32))
+    eng.rowcap = max(32, min(512, (eng.dd.max_row + 31) // 32 * 32))
     return lab.cpu().numpy() + 1, st
 
 

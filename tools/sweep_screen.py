@@ -1,0 +1,66 @@
+"""Sweep the fp32 screen kernel's tuning knobs on one config (GPU).
+
+    python tools/sweep_screen.py --config 1 [--iters 2]
+
+Builds realistic means (after --iters Lloyd iterations), then times
+ivfkm_assign_screen for each (rr, rowcap) with CUDA events and prints
+postings/s and ms per launch.  Results are checked against the default
+plan's labels so a faster variant cannot be a wrong one.
+"""
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import torch  # noqa: E402
+
+from paper_2002_09094_b200 import synth  # noqa: E402
+from paper_2002_09094_b200.clustering import init_means  # noqa: E402
+from paper_2002_09094_b200.engine import DeviceDataset, HostDataset, LloydEngine  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--iters", type=int, default=2)
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--rr", default="2,4,8")
+    ap.add_argument("--rowcap", default="256,512,1024")
+    args = ap.parse_args()
+    c = synth.CONFIGS[args.config]
+    ds = synth.make_dataset(c["corpus"])
+    eng = LloydEngine(DeviceDataset(HostDataset(ds), "cuda"), c["k"])
+    dm = eng.upload_means(init_means(ds, c["k"], c["seed"], "sparse_inverted"))
+    prev = None
+    for _ in range(args.iters):
+        lab = eng.assign(dm, prev)
+        eng.read_stats()
+        dm = eng.update(lab, dm)
+        prev = lab
+    base = eng.assign(dm, None).clone()
+    st = eng.read_stats()
+    out = []
+    for rr in map(int, args.rr.split(",")):
+        for rowcap in map(int, args.rowcap.split(",")):
+            eng.rowcap = rowcap
+            eng.lib.ivfkm_set_tuning(rowcap, 0, rr)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            times = []
+            for _ in range(args.reps):
+                lab = eng.assign(dm, None, events=ev)
+                torch.cuda.synchronize()
+                times.append(ev[0].elapsed_time(ev[1]))
+            ok = bool(torch.equal(lab, base))
+            ms = min(times)
+            rec = {"rr": rr, "rowcap": rowcap, "screen_ms": ms,
+                   "postings_per_s": st.postings / (ms / 1e3), "labels_ok": ok}
+            out.append(rec)
+            print(json.dumps(rec), flush=True)
+    eng.lib.ivfkm_set_tuning(1024, 0, 0)
+
+
+if __name__ == "__main__":
+    main()
