@@ -63,21 +63,28 @@ int ivfkm_version(void);
 int ivfkm_device_count(void);
 
 /* ---- bitmap-block inverted file (BIVF) of the means ---------------------
- * headers is planar, 2*dim*nblk + 1 uint32:
- * headers[t*nblk + b] = mask: bit j set <=> mean 32*b+j holds term t;
- * headers[dim*nblk + t*nblk + b] = offset: that mean's value sits at
- *   val[offset + popc(mask & ((1u<<j)-1))]; headers[2*dim*nblk] = total.
- * Values are stored term-major, mean ascending — the order of
- * MeanSet.inverted (means.py:169-179).  val32 feeds the fp32 screening pass,
- * val64 the exact fp64 rescoring.                                            */
+ * headers is planar uint32 (ivfkm_bivf_headers_size() words):
+ *   masks[t*nblk + b]    bit j set <=> mean 32*b+j holds term t
+ *   offs[t*nblk + b]     at headers[dim*nblk + t*nblk + b]: start of the block's
+ *                        values; bit 31 set = the block's 256-mean span is dense
+ *   total                at headers[2*dim*nblk]: padded value count in use
+ *   nc[t]                at headers[2*dim*nblk + 1 + t]: postings of term t
+ * Values (val32 for the fp32 screen, val64 for the exact fp64 rescoring) are
+ * term-major, mean ascending — the order of MeanSet.inverted
+ * (means.py:169-179) — except that each 256-mean span is padded to a multiple
+ * of 4 values and a fully populated span is stored lane-major (mean
+ * 32*(b0+r)+j at span_base + 8*j + r).  The value arrays need
+ * ivfkm_bivf_values_capacity() elements.                                     */
 int64_t ivfkm_bivf_nblk(int64_t k); /* 32-mean blocks per term, padded */
+int64_t ivfkm_bivf_headers_size(int64_t k, int64_t dim);
+int64_t ivfkm_bivf_values_capacity(int64_t k, int64_t dim, int64_t nnz);
 size_t ivfkm_bivf_workspace_size(int64_t dim, int64_t k);
 /* major = 0: rows of (ptr, cols) are means (mean-major CSR, cols = terms);
  * major = 1: rows are terms (term-major IVF, cols = mean ids).  0-based ids;
  * an id outside [0,k) / [0,dim) gives IVFKM_E_RANGE.                        */
 int ivfkm_bivf_build(int64_t k, int64_t dim, int major, int64_t nrows,
                      const int64_t* ptr /*[dev] nrows+1*/, const int32_t* cols /*[dev]*/,
-                     const double* vals /*[dev]*/, uint32_t* headers /*[dev] 2*dim*nblk+1*/,
+                     const double* vals /*[dev]*/, uint32_t* headers /*[dev]*/,
                      float* val32 /*[dev] nnz*/, double* val64 /*[dev] nnz*/, void* ws,
                      size_t ws_bytes, ivfkm_stream_t stream);
 

@@ -38,6 +38,7 @@
 #include <climits>
 #include <cmath>
 
+#include "bivf.cuh"
 #include "common.cuh"
 
 namespace cg = cooperative_groups;
@@ -60,6 +61,7 @@ struct ScreenParams {
   int64_t nblk;
   const uint32_t* masks;  // [dim][nblk]
   const uint32_t* offs;   // [dim][nblk] (+1: total)
+  const uint32_t* nc;     // [dim] postings per term
   const float* pv32;
   double mu_max;
   int cta_blocks;  // 32-mean blocks held by one CTA (multiple of RR)
@@ -121,12 +123,28 @@ struct MaskPack {
   }
 };
 
-// One object nonzero (value v) against RR blocks: lane-owned mean 32*b+lane
-// reads its value at o_b + popc(mask_b below the lane); o_{b+1} = o_b + popc(mask_b).
+// One object nonzero against RR blocks starting at block gb: lane-owned mean
+// 32*(gb+r)+lane reads its value at o_r + popc(mask_r below the lane), with
+// o_{r+1} = o_r + popc(mask_r); in a dense span (kDense on the offset) the
+// lane's values sit lane-major at span_base + 8*lane + (gb+r)%8.
 template <int RR>
-__device__ __forceinline__ void gather_values(const MaskPack<RR>& mk, uint32_t o,
-                                              const float* __restrict__ pv, unsigned lanebit,
-                                              unsigned lt, float (&u)[RR]) {
+__device__ __forceinline__ void gather_values(const MaskPack<RR>& mk, uint32_t o, uint32_t gb,
+                                              const float* __restrict__ pv, unsigned lane,
+                                              unsigned lanebit, unsigned lt, float (&u)[RR]) {
+  if (o & kDense) {
+    const uint32_t r0 = gb & (kSpan - 1);
+    const uint32_t base = (o & ~kDense) - 32u * r0 + 8u * lane + r0;
+    if constexpr (RR == kSpan) {  // r0 == 0: two aligned 16-B loads
+      const float4 a = __ldg(reinterpret_cast<const float4*>(pv + base));
+      const float4 b = __ldg(reinterpret_cast<const float4*>(pv + base) + 1);
+      u[0] = a.x; u[1] = a.y; u[2] = a.z; u[3] = a.w;
+      u[4] = b.x; u[5] = b.y; u[6] = b.z; u[7] = b.w;
+    } else {
+#pragma unroll
+      for (int r = 0; r < RR; ++r) u[r] = __ldg(pv + base + r);
+    }
+    return;
+  }
 #pragma unroll
   for (int r = 0; r < RR; ++r) {
     const uint32_t mr = mk.m[r];
@@ -137,7 +155,7 @@ __device__ __forceinline__ void gather_values(const MaskPack<RR>& mk, uint32_t o
 }
 
 template <int RR>
-__global__ void __launch_bounds__(512, 1) screen_kernel(ScreenParams p) {
+__global__ void __maxnreg__(72) screen_kernel(ScreenParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ ScreenShared sh;
   float* rho = reinterpret_cast<float*>(smem);
@@ -154,7 +172,6 @@ __global__ void __launch_bounds__(512, 1) screen_kernel(ScreenParams p) {
   const int64_t rb = p.row_ptr[obj], re = p.row_ptr[obj + 1];
   const int64_t nblk = p.nblk;
   const int64_t blk0 = (int64_t)z * p.cta_blocks;
-  const int64_t blk1 = min(blk0 + (int64_t)p.cta_blocks, nblk);
   const int nspans = p.cta_blocks / RR;
   const unsigned lanebit = 1u << lane;
   const unsigned lt = lanebit - 1u;
@@ -182,8 +199,7 @@ __global__ void __launch_bounds__(512, 1) screen_kernel(ScreenParams p) {
       const int32_t t = p.terms[c0 + j];
       s_term[j] = t;
       s_val[j] = p.val32[c0 + j];
-      if (blk1 > blk0)
-        post += __ldg(offs + (int64_t)t * nblk + blk1) - __ldg(offs + (int64_t)t * nblk + blk0);
+      if (z == 0) post += __ldg(p.nc + t);
     }
     __syncthreads();
     const bool first = (c0 == rb);
@@ -211,16 +227,16 @@ __global__ void __launch_bounds__(512, 1) screen_kernel(ScreenParams p) {
         uint32_t o;
         float uA[RR], uB[RR];
         ld(0, mk, o);
-        gather_values<RR>(mk, o, pv, lanebit, lt, uA);
+        gather_values<RR>(mk, o, gb32, pv, lane, lanebit, lt, uA);
         ld(1, mk, o);
         for (int e = 0; e < cn; e += 2) {
-          gather_values<RR>(mk, o, pv, lanebit, lt, uB);  // entry e+1 (zeros past the end)
+          gather_values<RR>(mk, o, gb32, pv, lane, lanebit, lt, uB);  // entry e+1 (zeros past the end)
           ld(e + 2, mk, o);
           const float vA = s_val[e];
           // fma(v, 0, acc) == acc exactly: absent postings cost no rounding
 #pragma unroll
           for (int r = 0; r < RR; ++r) acc[r] = fmaf(vA, uA[r], acc[r]);
-          gather_values<RR>(mk, o, pv, lanebit, lt, uA);  // entry e+2
+          gather_values<RR>(mk, o, gb32, pv, lane, lanebit, lt, uA);  // entry e+2
           ld(e + 3, mk, o);
           const float vB = (e + 1 < cn) ? s_val[e + 1] : 0.f;
 #pragma unroll
@@ -355,9 +371,7 @@ struct ExactCtx {
   const int64_t* row_ptr;
   const int32_t* terms;
   const double* val64;
-  int64_t nblk;
-  const uint32_t* masks;
-  const uint32_t* offs;
+  BivfView bv;
   const double* pv64;
 };
 
@@ -365,19 +379,15 @@ struct ExactCtx {
 // are added serially in row order (every lane holds the same sum).
 __device__ double exact_score_warp(const ExactCtx& x, int64_t rb, int64_t re, int c, int lane) {
   double acc = 0.0;
-  const int64_t blk = c >> 5;
-  const unsigned bit = 1u << (c & 31);
   for (int64_t h0 = rb; h0 < re; h0 += 32) {
     const int64_t h = h0 + lane;
     bool present = false;
     double prod = 0.0;
     if (h < re) {
-      const int64_t t = x.terms[h];
-      const uint32_t m = __ldg(x.masks + t * x.nblk + blk);
-      if (m & bit) {
+      const int64_t pos = bivf_find(x.bv, x.terms[h], c);
+      if (pos >= 0) {
         present = true;
-        const uint32_t o = __ldg(x.offs + t * x.nblk + blk);
-        prod = __dmul_rn(x.val64[h], __ldg(x.pv64 + (o + (uint32_t)__popc(m & (bit - 1u)))));
+        prod = __dmul_rn(x.val64[h], __ldg(x.pv64 + pos));
       }
     }
     unsigned pm = __ballot_sync(kFull, present);
@@ -393,16 +403,9 @@ __device__ double exact_score_warp(const ExactCtx& x, int64_t rb, int64_t re, in
 // One thread scores one mean over the whole row.
 __device__ double exact_score_thread(const ExactCtx& x, int64_t rb, int64_t re, int64_t c) {
   double acc = 0.0;
-  const int64_t blk = c >> 5;
-  const unsigned bit = 1u << (c & 31);
   for (int64_t h = rb; h < re; ++h) {
-    const int64_t t = x.terms[h];
-    const uint32_t m = __ldg(x.masks + t * x.nblk + blk);
-    if (m & bit) {
-      const uint32_t o = __ldg(x.offs + t * x.nblk + blk);
-      acc = __dadd_rn(acc, __dmul_rn(x.val64[h],
-                                     __ldg(x.pv64 + (o + (uint32_t)__popc(m & (bit - 1u))))));
-    }
+    const int64_t pos = bivf_find(x.bv, x.terms[h], c);
+    if (pos >= 0) acc = __dadd_rn(acc, __dmul_rn(x.val64[h], __ldg(x.pv64 + pos)));
   }
   return acc;
 }
@@ -715,6 +718,7 @@ int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
   sp.nblk = ivfkm_bivf_nblk(a.k);
   sp.masks = a.headers;
   sp.offs = a.headers + a.dim * sp.nblk;
+  sp.nc = a.headers + 2 * a.dim * sp.nblk + 1;
   sp.pv32 = a.pval32;
   sp.mu_max = a.mu_max > 0 ? a.mu_max : 1.0;
   sp.cta_blocks = pl.cta_blocks;
@@ -740,9 +744,8 @@ int finish_impl(const AssignArgs& a, const AssignWs& w, const int32_t* prev_labe
   fp.x.row_ptr = a.row_ptr;
   fp.x.terms = a.terms;
   fp.x.val64 = a.val64;
-  fp.x.nblk = ivfkm_bivf_nblk(a.k);
-  fp.x.masks = a.headers;
-  fp.x.offs = a.headers + a.dim * fp.x.nblk;
+  fp.x.bv = BivfView{ivfkm_bivf_nblk(a.k), a.headers,
+                     a.headers + a.dim * ivfkm_bivf_nblk(a.k), nullptr};
   fp.x.pv64 = a.pval64;
   fp.label32 = w.label32;
   fp.slot_of = w.slot_of;
@@ -829,9 +832,7 @@ extern "C" int ivfkm_score_labels(int64_t n_obj, const int64_t* row_ptr, const i
   x.row_ptr = row_ptr;
   x.terms = terms;
   x.val64 = val64;
-  x.nblk = ivfkm_bivf_nblk(k);
-  x.masks = headers;
-  x.offs = headers + dim * x.nblk;
+  x.bv = BivfView{ivfkm_bivf_nblk(k), headers, headers + dim * ivfkm_bivf_nblk(k), nullptr};
   x.pv64 = pval64;
   score_labels_kernel<<<grid_for(n_obj, 8), 256, 0, st>>>(n_obj, x, labels, sims);
   IVFKM_CHECK_LAUNCH();

@@ -1,0 +1,47 @@
+// Bitmap-block inverted file (BIVF): layout constants and the O(1) lookup
+// shared by the build, the fp32 screen and the exact fp64 rescoring.
+//
+// headers (uint32), planar:
+//   masks[t*nblk + b]        bit j <=> mean 32*b+j holds term t
+//   offs [t*nblk + b]        start of block b's values (+ kDense flag)
+//   offs [dim*nblk]          padded total (size of the value arrays in use)
+//   nc   [t]                 postings of term t (= centroid_freq, means.py:144-147)
+// Blocks are grouped in spans of 8 (256 means).  Every span's value segment
+// is padded to a multiple of 4 values (16 B), so a span start is 16-B aligned.
+// A span whose 8 masks are all full is *dense*: its 256 values are stored
+// lane-major (mean 32*(b0+r)+j at span_base + 8*j + r) so a warp lane owning
+// means 32*(b0+r)+lane reads its 8 values with two 16-B loads; every block of
+// a dense span carries kDense in its offset.  Other spans keep the reference
+// order (term-major, mean ascending, means.py:169-179).
+#pragma once
+#include <cstdint>
+
+namespace ivfkm {
+
+constexpr uint32_t kDense = 0x80000000u;
+constexpr int kSpan = 8;
+
+struct BivfView {
+  int64_t nblk;
+  const uint32_t* masks;
+  const uint32_t* offs;
+  const uint32_t* nc;
+};
+
+__host__ __device__ inline int64_t bivf_nh(int64_t dim, int64_t nblk) { return dim * nblk; }
+
+// Position of mean c's value for term t, or -1 when the mean lacks the term.
+__device__ __forceinline__ int64_t bivf_find(const BivfView& v, int64_t t, int64_t c) {
+  const int64_t b = c >> 5;
+  const uint32_t bit = 1u << (c & 31);
+  const uint32_t m = __ldg(v.masks + t * v.nblk + b);
+  if (!(m & bit)) return -1;
+  const uint32_t o = __ldg(v.offs + t * v.nblk + b);
+  if (o & kDense) {
+    const uint32_t r = (uint32_t)(b & (kSpan - 1));
+    return (int64_t)((o & ~kDense) - 32u * r + 8u * (uint32_t)(c & 31) + r);
+  }
+  return (int64_t)(o + (uint32_t)__popc(m & (bit - 1u)));
+}
+
+}  // namespace ivfkm

@@ -95,7 +95,6 @@ extern "C" int ivfkm_assign_ivf_host(int64_t n, const int64_t* indptr, const int
     }
     xn[i] = std::sqrt(s);
   }
-  const int64_t nblk = ivfkm_bivf_nblk(k);
   DevBuf d_ip, d_t, d_v32, d_v64, d_xn, d_mp, d_mc, d_mv, d_hdr, d_p32, d_p64, d_bws, d_lab,
       d_sims, d_sizes, d_stats, d_aws;
   const size_t bws = ivfkm_bivf_workspace_size(dim, k);
@@ -108,9 +107,10 @@ extern "C" int ivfkm_assign_ivf_host(int64_t n, const int64_t* indptr, const int
   IVFKM_TRY(d_mp.alloc(sizeof(int64_t) * (dim + 1)));
   IVFKM_TRY(d_mc.alloc(sizeof(int32_t) * mnz));
   IVFKM_TRY(d_mv.alloc(sizeof(double) * mnz));
-  IVFKM_TRY(d_hdr.alloc(sizeof(uint32_t) * (2 * dim * nblk + 1)));
-  IVFKM_TRY(d_p32.alloc(sizeof(float) * mnz));
-  IVFKM_TRY(d_p64.alloc(sizeof(double) * mnz));
+  const int64_t pcap = ivfkm_bivf_values_capacity(k, dim, mnz);
+  IVFKM_TRY(d_hdr.alloc(sizeof(uint32_t) * ivfkm_bivf_headers_size(k, dim)));
+  IVFKM_TRY(d_p32.alloc(sizeof(float) * pcap));
+  IVFKM_TRY(d_p64.alloc(sizeof(double) * pcap));
   IVFKM_TRY(d_bws.alloc(bws));
   IVFKM_TRY(d_lab.alloc(sizeof(int32_t) * n));
   IVFKM_TRY(d_sims.alloc(sizeof(double) * n));

@@ -171,9 +171,11 @@ class LloydEngine:
     # -- means ---------------------------------------------------------------
     def build_bivf(self, dm: DeviceMeans) -> DeviceMeans:
         dev = self.device
-        dm.headers = torch.empty(2 * dm.dim * self.nblk + 1, dtype=torch.int32, device=dev)
-        dm.pv32 = torch.empty(max(dm.nnz, 1), dtype=torch.float32, device=dev)
-        dm.pv64 = torch.empty(max(dm.nnz, 1), dtype=torch.float64, device=dev)
+        dm.headers = torch.empty(int(self.lib.ivfkm_bivf_headers_size(self.k, dm.dim)),
+                                 dtype=torch.int32, device=dev)
+        cap = int(self.lib.ivfkm_bivf_values_capacity(self.k, dm.dim, dm.nnz))
+        dm.pv32 = torch.empty(cap, dtype=torch.float32, device=dev)
+        dm.pv64 = torch.empty(cap, dtype=torch.float64, device=dev)
         rc = self.lib.ivfkm_bivf_build(self.k, dm.dim, 0, self.k, _p(dm.ptr), _p(dm.terms),
                                        _p(dm.vals), _p(dm.headers), _p(dm.pv32), _p(dm.pv64),
                                        _p(self.ws_bivf), self.ws_bivf.numel(), _stream())
