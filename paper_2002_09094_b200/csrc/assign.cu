@@ -126,22 +126,25 @@ struct MaskPack {
 // One object nonzero against RR blocks starting at block gb: lane-owned mean
 // 32*(gb+r)+lane reads its value at o_r + popc(mask_r below the lane), with
 // o_{r+1} = o_r + popc(mask_r); in a dense span (kDense on the offset) the
-// lane's values sit lane-major at span_base + 8*lane + (gb+r)%8.
+// lane's values sit at span_base + 128*(r/4) + 4*lane + r%4 (bivf.cuh).
 template <int RR>
 __device__ __forceinline__ void gather_values(const MaskPack<RR>& mk, uint32_t o, uint32_t gb,
                                               const float* __restrict__ pv, unsigned lane,
                                               unsigned lanebit, unsigned lt, float (&u)[RR]) {
   if (o & kDense) {
     const uint32_t r0 = gb & (kSpan - 1);
-    const uint32_t base = (o & ~kDense) - 32u * r0 + 8u * lane + r0;
+    const uint32_t sbase = (o & ~kDense) - 32u * r0;
     if constexpr (RR == kSpan) {  // r0 == 0: two aligned 16-B loads
-      const float4 a = __ldg(reinterpret_cast<const float4*>(pv + base));
-      const float4 b = __ldg(reinterpret_cast<const float4*>(pv + base) + 1);
+      const float4 a = __ldg(reinterpret_cast<const float4*>(pv + sbase) + lane);
+      const float4 b = __ldg(reinterpret_cast<const float4*>(pv + sbase) + 32 + lane);
       u[0] = a.x; u[1] = a.y; u[2] = a.z; u[3] = a.w;
       u[4] = b.x; u[5] = b.y; u[6] = b.z; u[7] = b.w;
     } else {
 #pragma unroll
-      for (int r = 0; r < RR; ++r) u[r] = __ldg(pv + base + r);
+      for (int r = 0; r < RR; ++r) {
+        const uint32_t rr = r0 + r;
+        u[r] = __ldg(pv + sbase + 128u * (rr >> 2) + 4u * lane + (rr & 3u));
+      }
     }
     return;
   }
@@ -154,103 +157,17 @@ __device__ __forceinline__ void gather_values(const MaskPack<RR>& mk, uint32_t o
   }
 }
 
-template <int RR>
-__global__ void __maxnreg__(72) screen_kernel(ScreenParams p) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ ScreenShared sh;
-  float* rho = reinterpret_cast<float*>(smem);
-  const int cta_cids = p.cta_blocks * 32;
-  int32_t* s_term = reinterpret_cast<int32_t*>(rho + cta_cids);
-  float* s_val = reinterpret_cast<float*>(s_term + p.rowcap);
-
+// CTA-local argmax (value desc, index asc) over the parked rho, merged over
+// the cluster through DSMEM when k is split; then the rigorous fp32 window and
+// the candidate queue for exact rescoring.  Every thread of the CTA calls it.
+__device__ __forceinline__ void screen_epilogue(const ScreenParams& p, ScreenShared& sh,
+                                                const float* rho, int64_t obj, int z, int64_t rb,
+                                                int64_t re, unsigned long long post) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
-  const int z = blockIdx.x % p.nsplit;
-  const int64_t obj = blockIdx.x / p.nsplit;
-  if (obj >= p.n_obj) return;  // whole cluster shares obj
-  const int64_t rb = p.row_ptr[obj], re = p.row_ptr[obj + 1];
-  const int64_t nblk = p.nblk;
+  const int cta_cids = p.cta_blocks * 32;
   const int64_t blk0 = (int64_t)z * p.cta_blocks;
-  const int nspans = p.cta_blocks / RR;
-  const unsigned lanebit = 1u << lane;
-  const unsigned lt = lanebit - 1u;
-  // The bases go through shared memory so they stay in registers: ptxas would
-  // otherwise re-load kernel parameters from the constant bank inside every
-  // predicated gather (one extra LDC per posting block).
-  __shared__ const void* s_base[3];
-  if (threadIdx.x == 0) {
-    s_base[0] = p.masks;
-    s_base[1] = p.offs;
-    s_base[2] = p.pv32;
-  }
-  __syncthreads();
-  const uint32_t* __restrict__ masks = static_cast<const uint32_t*>(s_base[0]);
-  const uint32_t* __restrict__ offs = static_cast<const uint32_t*>(s_base[1]);
-  const float* __restrict__ pv = static_cast<const float*>(s_base[2]);
-  unsigned long long post = 0;  // postings of this CTA's blocks (counters.py:71-81)
-
-  int64_t c0 = rb;
-  do {
-    const int64_t rem = re - c0;
-    const int cn = (int)(rem < p.rowcap ? rem : p.rowcap);
-    __syncthreads();
-    for (int j = threadIdx.x; j < cn; j += blockDim.x) {
-      const int32_t t = p.terms[c0 + j];
-      s_term[j] = t;
-      s_val[j] = p.val32[c0 + j];
-      if (z == 0) post += __ldg(p.nc + t);
-    }
-    __syncthreads();
-    const bool first = (c0 == rb);
-    for (int sp = warp; sp < nspans; sp += nwarps) {
-      const int64_t gb = blk0 + (int64_t)sp * RR;
-      float acc[RR];
-#pragma unroll
-      for (int r = 0; r < RR; ++r) acc[r] = first ? 0.f : rho[(sp * RR + r) * 32 + lane];
-      if (gb < nblk) {  // nblk is a multiple of RR: a span is all in or all out
-        // 32-bit row arithmetic: dim * nblk < 2^31 is checked at build time
-        const uint32_t nb32 = (uint32_t)nblk, gb32 = (uint32_t)gb;
-        auto ld = [&](int e, MaskPack<RR>& mk, uint32_t& o) {
-          if (e < cn) {
-            const uint32_t row = (uint32_t)s_term[e] * nb32 + gb32;
-            mk.load(masks + row);
-            o = __ldg(offs + row);
-          } else {
-            mk.zero();
-            o = 0u;
-          }
-        };
-        // software pipeline (unrolled by two): values of entries e, e+1 and
-        // masks of e+2 are in flight while entry e accumulates
-        MaskPack<RR> mk;
-        uint32_t o;
-        float uA[RR], uB[RR];
-        ld(0, mk, o);
-        gather_values<RR>(mk, o, gb32, pv, lane, lanebit, lt, uA);
-        ld(1, mk, o);
-        for (int e = 0; e < cn; e += 2) {
-          gather_values<RR>(mk, o, gb32, pv, lane, lanebit, lt, uB);  // entry e+1 (zeros past the end)
-          ld(e + 2, mk, o);
-          const float vA = s_val[e];
-          // fma(v, 0, acc) == acc exactly: absent postings cost no rounding
-#pragma unroll
-          for (int r = 0; r < RR; ++r) acc[r] = fmaf(vA, uA[r], acc[r]);
-          gather_values<RR>(mk, o, gb32, pv, lane, lanebit, lt, uA);  // entry e+2
-          ld(e + 3, mk, o);
-          const float vB = (e + 1 < cn) ? s_val[e + 1] : 0.f;
-#pragma unroll
-          for (int r = 0; r < RR; ++r) acc[r] = fmaf(vB, uB[r], acc[r]);
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < RR; ++r) rho[(sp * RR + r) * 32 + lane] = acc[r];
-    }
-    c0 += p.rowcap;
-  } while (c0 < re);
-  __syncthreads();
-
-  // ---- CTA-local argmax (value desc, index asc) and postings total ----
   float bv = -INFINITY;
   int bc = INT_MAX;
   const int64_t cid0 = blk0 * 32;
@@ -362,6 +279,318 @@ __global__ void __maxnreg__(72) screen_kernel(ScreenParams p) {
     }
   }
   if (p.nsplit > 1) cluster.sync();  // peers keep their shared memory alive
+}
+
+template <int RR>
+__global__ void __maxnreg__(72) screen_kernel(ScreenParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ ScreenShared sh;
+  float* rho = reinterpret_cast<float*>(smem);
+  const int cta_cids = p.cta_blocks * 32;
+  int32_t* s_term = reinterpret_cast<int32_t*>(rho + cta_cids);
+  float* s_val = reinterpret_cast<float*>(s_term + p.rowcap);
+
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int z = blockIdx.x % p.nsplit;
+  const int64_t obj = blockIdx.x / p.nsplit;
+  if (obj >= p.n_obj) return;  // whole cluster shares obj
+  const int64_t rb = p.row_ptr[obj], re = p.row_ptr[obj + 1];
+  const int64_t nblk = p.nblk;
+  const int64_t blk0 = (int64_t)z * p.cta_blocks;
+  const int nspans = p.cta_blocks / RR;
+  const unsigned lanebit = 1u << lane;
+  const unsigned lt = lanebit - 1u;
+  // The bases go through shared memory so they stay in registers: ptxas would
+  // otherwise re-load kernel parameters from the constant bank inside every
+  // predicated gather (one extra LDC per posting block).
+  __shared__ const void* s_base[3];
+  if (threadIdx.x == 0) {
+    s_base[0] = p.masks;
+    s_base[1] = p.offs;
+    s_base[2] = p.pv32;
+  }
+  __syncthreads();
+  const uint32_t* __restrict__ masks = static_cast<const uint32_t*>(s_base[0]);
+  const uint32_t* __restrict__ offs = static_cast<const uint32_t*>(s_base[1]);
+  const float* __restrict__ pv = static_cast<const float*>(s_base[2]);
+  unsigned long long post = 0;  // postings of this CTA's blocks (counters.py:71-81)
+
+  int64_t c0 = rb;
+  do {
+    const int64_t rem = re - c0;
+    const int cn = (int)(rem < p.rowcap ? rem : p.rowcap);
+    __syncthreads();
+    for (int j = threadIdx.x; j < cn; j += blockDim.x) {
+      const int32_t t = p.terms[c0 + j];
+      s_term[j] = t;
+      s_val[j] = p.val32[c0 + j];
+      if (z == 0) post += __ldg(p.nc + t);
+    }
+    __syncthreads();
+    const bool first = (c0 == rb);
+    for (int sp = warp; sp < nspans; sp += nwarps) {
+      const int64_t gb = blk0 + (int64_t)sp * RR;
+      float acc[RR];
+#pragma unroll
+      for (int r = 0; r < RR; ++r) acc[r] = first ? 0.f : rho[(sp * RR + r) * 32 + lane];
+      if (gb < nblk) {  // nblk is a multiple of RR: a span is all in or all out
+        // 32-bit row arithmetic: dim * nblk < 2^31 is checked at build time
+        const uint32_t nb32 = (uint32_t)nblk, gb32 = (uint32_t)gb;
+        auto ld = [&](int e, MaskPack<RR>& mk, uint32_t& o) {
+          if (e < cn) {
+            const uint32_t row = (uint32_t)s_term[e] * nb32 + gb32;
+            mk.load(masks + row);
+            o = __ldg(offs + row);
+          } else {
+            mk.zero();
+            o = 0u;
+          }
+        };
+        // software pipeline (unrolled by two): values of entries e, e+1 and
+        // masks of e+2 are in flight while entry e accumulates
+        MaskPack<RR> mk;
+        uint32_t o;
+        float uA[RR], uB[RR];
+        ld(0, mk, o);
+        gather_values<RR>(mk, o, gb32, pv, lane, lanebit, lt, uA);
+        ld(1, mk, o);
+        for (int e = 0; e < cn; e += 2) {
+          gather_values<RR>(mk, o, gb32, pv, lane, lanebit, lt, uB);  // entry e+1 (zeros past the end)
+          ld(e + 2, mk, o);
+          const float vA = s_val[e];
+          // fma(v, 0, acc) == acc exactly: absent postings cost no rounding
+#pragma unroll
+          for (int r = 0; r < RR; ++r) acc[r] = fmaf(vA, uA[r], acc[r]);
+          gather_values<RR>(mk, o, gb32, pv, lane, lanebit, lt, uA);  // entry e+2
+          ld(e + 3, mk, o);
+          const float vB = (e + 1 < cn) ? s_val[e + 1] : 0.f;
+#pragma unroll
+          for (int r = 0; r < RR; ++r) acc[r] = fmaf(vB, uB[r], acc[r]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RR; ++r) rho[(sp * RR + r) * 32 + lane] = acc[r];
+    }
+    c0 += p.rowcap;
+  } while (c0 < re);
+  __syncthreads();
+
+  screen_epilogue(p, sh, rho, obj, z, rb, re, post);
+}
+
+// ---------------------------------------------------------------------------
+// TMA-pipelined screen.  Same ownership and arithmetic as screen_kernel<8>
+// (lane = mean within a 32-mean block, 8 blocks per warp span, fp32 FMAs in
+// row order), but the posting data of each (object nonzero, span) — the 32-B
+// mask row and the span's contiguous, 16-B-padded value segment — is fetched
+// by cp.async.bulk (TMA) into a per-warp ring of kStages shared-memory stages
+// completed on mbarriers, kStages entries ahead of the FMAs.  Latency is hidden
+// by the copy engine instead of registers, no LSU instruction is spent per
+// posting load, and spans a term does not populate are skipped outright.
+
+constexpr int kStages = 4;
+constexpr int kStageBytes = 32 + 4 * 256;  // masks + the largest span segment
+
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__host__ __device__ inline size_t tma_warp_bytes(int rowcap) {
+  return ((size_t)16 * rowcap + 15) / 16 * 16 + 8 * kStages + (size_t)kStages * kStageBytes;
+}
+
+__global__ void __launch_bounds__(512) screen_tma_kernel(ScreenParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ ScreenShared sh;
+  constexpr int RR = kSpan;
+  float* rho = reinterpret_cast<float*>(smem);
+  const int cta_cids = p.cta_blocks * 32;
+  int32_t* s_term = reinterpret_cast<int32_t*>(rho + cta_cids);
+  float* s_val = reinterpret_cast<float*>(s_term + p.rowcap);
+
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int z = blockIdx.x % p.nsplit;
+  const int64_t obj = blockIdx.x / p.nsplit;
+  if (obj >= p.n_obj) return;  // whole cluster shares obj
+  const int64_t rb = p.row_ptr[obj], re = p.row_ptr[obj + 1];
+  const int64_t nblk = p.nblk;
+  const int64_t blk0 = (int64_t)z * p.cta_blocks;
+  const int nspans = p.cta_blocks / RR;
+  const unsigned lanebit = 1u << lane;
+  const unsigned lt = lanebit - 1u;
+
+  // per-warp region: active list, mbarriers, stage ring
+  unsigned char* wbase = reinterpret_cast<unsigned char*>(s_val + p.rowcap);
+  wbase = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(wbase) + 127) & ~(uintptr_t)127);
+  wbase += (size_t)warp * tma_warp_bytes(p.rowcap);
+  uint32_t* act_row = reinterpret_cast<uint32_t*>(wbase);
+  uint32_t* act_os = act_row + p.rowcap;
+  uint32_t* act_nv = act_os + p.rowcap;
+  float* act_v = reinterpret_cast<float*>(act_nv + p.rowcap);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(wbase + ((size_t)16 * p.rowcap + 15) / 16 * 16);
+  unsigned char* ring = reinterpret_cast<unsigned char*>(mbar + kStages);
+
+  __shared__ const void* s_base[4];
+  if (threadIdx.x == 0) {
+    s_base[0] = p.masks;
+    s_base[1] = p.offs;
+    s_base[2] = p.pv32;
+    s_base[3] = p.nc;
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < kStages; ++q) mbar_init(&mbar[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t* __restrict__ masks = static_cast<const uint32_t*>(s_base[0]);
+  const uint32_t* __restrict__ offs = static_cast<const uint32_t*>(s_base[1]);
+  const float* __restrict__ pv = static_cast<const float*>(s_base[2]);
+  const uint32_t* __restrict__ ncp = static_cast<const uint32_t*>(s_base[3]);
+  unsigned long long post = 0;
+  uint32_t used = 0;  // stage uses so far (ring position and mbarrier parity)
+
+  int64_t c0 = rb;
+  do {
+    const int64_t rem = re - c0;
+    const int cn = (int)(rem < p.rowcap ? rem : p.rowcap);
+    __syncthreads();
+    for (int j = threadIdx.x; j < cn; j += blockDim.x) {
+      const int32_t t = p.terms[c0 + j];
+      s_term[j] = t;
+      s_val[j] = p.val32[c0 + j];
+      if (z == 0) post += __ldg(ncp + t);
+    }
+    __syncthreads();
+    const bool first = (c0 == rb);
+    for (int sp = warp; sp < nspans; sp += nwarps) {
+      const int64_t gb = blk0 + (int64_t)sp * RR;
+      float acc[RR];
+#pragma unroll
+      for (int r = 0; r < RR; ++r) acc[r] = first ? 0.f : rho[(sp * RR + r) * 32 + lane];
+      if (gb < nblk) {
+        const uint32_t nb32 = (uint32_t)nblk, gb32 = (uint32_t)gb;
+        // ---- active list: entries whose term populates this span
+        int n_act = 0;
+        for (int j0 = 0; j0 < cn; j0 += 128) {
+          uint32_t os[4], oe[4], row[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int e = j0 + 32 * q + lane;
+            os[q] = 0u;
+            oe[q] = 0u;
+            row[q] = 0u;
+            if (e < cn) {
+              row[q] = (uint32_t)s_term[e] * nb32 + gb32;
+              os[q] = __ldg(offs + row[q]);
+              oe[q] = __ldg(offs + row[q] + RR);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int e = j0 + 32 * q + lane;
+            const uint32_t start = os[q] & ~kDense;
+            const uint32_t nv = (oe[q] & ~kDense) - start;
+            const bool on = e < cn && nv != 0u;
+            const unsigned bal = __ballot_sync(kFull, on);
+            if (on) {
+              const int at = n_act + __popc(bal & lt);
+              act_row[at] = row[q];
+              act_os[at] = os[q];
+              act_nv[at] = nv;
+              act_v[at] = s_val[e];
+            }
+            n_act += __popc(bal);
+          }
+        }
+        __syncwarp();
+        // ---- pipeline: kStages bulk copies in flight ahead of the FMAs
+        auto issue = [&](int i) {
+          const uint32_t st = (used + (uint32_t)i) % kStages;
+          unsigned char* dst = ring + (size_t)st * kStageBytes;
+          const uint32_t nv = act_nv[i];
+          mbar_expect_tx(&mbar[st], 32u + 4u * nv);
+          bulk_g2s(dst, masks + act_row[i], 32u, &mbar[st]);
+          bulk_g2s(dst + 32, pv + (act_os[i] & ~kDense), 4u * nv, &mbar[st]);
+        };
+        if (lane == 0)
+          for (int i = 0; i < n_act && i < kStages; ++i) issue(i);
+        for (int i = 0; i < n_act; ++i) {
+          const uint32_t g = used + (uint32_t)i;
+          const uint32_t st = g % kStages;
+          while (!mbar_try_wait(&mbar[st], (g / kStages) & 1u)) {
+          }
+          const unsigned char* src = ring + (size_t)st * kStageBytes;
+          const float v = act_v[i];
+          float u[RR];
+          if (act_os[i] & kDense) {
+            const float4 a = reinterpret_cast<const float4*>(src + 32)[lane];
+            const float4 b = reinterpret_cast<const float4*>(src + 32)[32 + lane];
+            u[0] = a.x; u[1] = a.y; u[2] = a.z; u[3] = a.w;
+            u[4] = b.x; u[5] = b.y; u[6] = b.z; u[7] = b.w;
+          } else {
+            const uint4 ma = reinterpret_cast<const uint4*>(src)[0];
+            const uint4 mb = reinterpret_cast<const uint4*>(src)[1];
+            const uint32_t m[RR] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
+            const float* vals = reinterpret_cast<const float*>(src + 32);
+            uint32_t o = 0;
+#pragma unroll
+            for (int r = 0; r < RR; ++r) {
+              u[r] = 0.f;
+              if (m[r] & lanebit) u[r] = vals[o + (uint32_t)__popc(m[r] & lt)];
+              o += (uint32_t)__popc(m[r]);
+            }
+          }
+          // fma(v, 0, acc) == acc exactly: absent postings cost no rounding
+#pragma unroll
+          for (int r = 0; r < RR; ++r) acc[r] = fmaf(v, u[r], acc[r]);
+          __syncwarp();  // every lane is done with this stage
+          if (lane == 0 && i + kStages < n_act) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(i + kStages);
+          }
+        }
+        used += (uint32_t)n_act;
+        __syncwarp();
+      }
+#pragma unroll
+      for (int r = 0; r < RR; ++r) rho[(sp * RR + r) * 32 + lane] = acc[r];
+    }
+    c0 += p.rowcap;
+  } while (c0 < re);
+  __syncthreads();
+  screen_epilogue(p, sh, rho, obj, z, rb, re, post);
 }
 
 // ---------------------------------------------------------------------------
@@ -612,15 +841,43 @@ AssignWs carve_assign(void* base, int64_t n, size_t* total) {
   return w;
 }
 
+static int g_tma_warps = 8;
+
 struct Plan {
   int rr, nsplit, cta_blocks, warps, rowcap;
+  bool tma;
   size_t smem;
 };
 
 int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
   const int64_t nblk = ivfkm_bivf_nblk(k);
   Plan pl;
-  pl.rr = rr ? rr : (nblk >= 32 ? 8 : 2);
+  if (rr == 0 || rr == -8) {  // default: the TMA-pipelined screen (8-block spans)
+    pl.tma = true;
+    pl.rr = kSpan;
+    pl.rowcap = rowcap < 256 ? rowcap : 256;
+    const int64_t spans_total = nblk / kSpan;
+    for (int s = 1; s <= kMaxSplit; ++s) {
+      int64_t cb = (nblk + s - 1) / s;
+      cb = (cb + kSpan - 1) / kSpan * kSpan;
+      const int spans = (int)(cb / kSpan);
+      const int warps = spans < g_tma_warps ? spans : g_tma_warps;
+      const size_t smem = (size_t)cb * 128 + (size_t)pl.rowcap * 8 + 128 +
+                          (size_t)warps * tma_warp_bytes(pl.rowcap);
+      if (smem <= (size_t)smem_limit) {
+        pl.nsplit = s;
+        pl.cta_blocks = (int)cb;
+        pl.warps = warps;
+        pl.smem = smem;
+        *out = pl;
+        (void)spans_total;
+        return IVFKM_OK;
+      }
+    }
+    return IVFKM_E_UNSUPPORTED;
+  }
+  pl.tma = false;
+  pl.rr = rr > 0 ? rr : (nblk >= 32 ? 8 : 2);
   pl.rowcap = rowcap;
   const size_t stage = (size_t)rowcap * 8;
   pl.nsplit = 0;
@@ -648,7 +905,7 @@ int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
 
 template <int RR>
 int launch_screen(const Plan& pl, const ScreenParams& p, cudaStream_t st) {
-  auto fn = screen_kernel<RR>;
+  auto fn = pl.tma ? screen_tma_kernel : screen_kernel<RR>;
   IVFKM_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(p.n_obj * pl.nsplit));
@@ -680,11 +937,12 @@ extern "C" size_t ivfkm_assign_workspace_size(int64_t n_obj, int64_t /*k*/) {
 // thread-block-cluster split at small k (used by the tests).
 static int g_rowcap = 1024;
 static int g_smem_limit = kSmemLimit - 2048;  // leave room for static smem
-static int g_rr = 0;                          // 0: automatic
+static int g_rr = 0;                          // 0: TMA screen; 2/4/8: LDG screen
 extern "C" void ivfkm_set_tuning(int rowcap, int smem_limit, int rr) {
   if (rowcap >= 32 && rowcap <= 8192) g_rowcap = rowcap / 32 * 32;
   if (smem_limit >= 1024 && smem_limit <= kSmemLimit - 2048) g_smem_limit = smem_limit;
   if (rr == 0 || rr == 2 || rr == 4 || rr == 8) g_rr = rr;
+  if (rr <= -16 && rr >= -16 * 16) g_tma_warps = -rr / 16;  // -16*w: TMA warps per CTA
 }
 
 namespace {
@@ -730,6 +988,7 @@ int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
   sp.q_cnt = w.q_cnt;
   sp.q_cid = w.q_cid;
   sp.stats = a.stats;
+  if (pl.tma) return launch_screen<8>(pl, sp, st);
   switch (pl.rr) {
     case 8: return launch_screen<8>(pl, sp, st);
     case 4: return launch_screen<4>(pl, sp, st);

@@ -9,9 +9,10 @@
 // Blocks are grouped in spans of 8 (256 means).  Every span's value segment
 // is padded to a multiple of 4 values (16 B), so a span start is 16-B aligned.
 // A span whose 8 masks are all full is *dense*: its 256 values are stored
-// lane-major (mean 32*(b0+r)+j at span_base + 8*j + r) so a warp lane owning
-// means 32*(b0+r)+lane reads its 8 values with two 16-B loads; every block of
-// a dense span carries kDense in its offset.  Other spans keep the reference
+// lane-major in two halves (mean 32*(b0+r)+j at span_base + 128*(r/4) + 4*j +
+// r%4), so a warp lane owning means 32*(b0+r)+lane reads its 8 values with two
+// 16-B loads that are coalesced in global memory and conflict-free in shared
+// memory; every block of a dense span carries kDense in its offset.  Other spans keep the reference
 // order (term-major, mean ascending, means.py:169-179).
 #pragma once
 #include <cstdint>
@@ -39,7 +40,8 @@ __device__ __forceinline__ int64_t bivf_find(const BivfView& v, int64_t t, int64
   const uint32_t o = __ldg(v.offs + t * v.nblk + b);
   if (o & kDense) {
     const uint32_t r = (uint32_t)(b & (kSpan - 1));
-    return (int64_t)((o & ~kDense) - 32u * r + 8u * (uint32_t)(c & 31) + r);
+    return (int64_t)((o & ~kDense) - 32u * r + 128u * (r >> 2) + 4u * (uint32_t)(c & 31) +
+                     (r & 3u));
   }
   return (int64_t)(o + (uint32_t)__popc(m & (bit - 1u)));
 }

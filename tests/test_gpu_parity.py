@@ -178,16 +178,15 @@ def tuning():
     lib.ivfkm_set_tuning(1024, 225 * 1024, 0)
 
 
-def _assign_raw(ds, means, rowcap=None, smem=None):
-    """Assign through the engine with explicit tuning (rowcap applies per call)."""
+def _assign_raw(ds, means, rowcap=None, smem=None, rr=-1):
+    """Assign through the engine with explicit tuning (rowcap applies per call;
+    rr = 0 selects the TMA-pipelined screen, 2/4/8 the LDG screen)."""
     from paper_2002_09094_b200.variants import engine_for
 
-    P = _pkg()
     eng = engine_for(ds, means.k)
     if rowcap:
         eng.rowcap = rowcap
-    if smem:
-        eng.lib.ivfkm_set_tuning(eng.rowcap, smem, -1)
+    eng.lib.ivfkm_set_tuning(eng.rowcap, smem or 0, rr)
     dm = eng.upload_means(means)
     lab = eng.assign(dm, None)
     st = eng.read_stats()
@@ -212,39 +211,42 @@ def _random_case(n=1500, dim=400, k=64, seed=0, signed=False, corpus=0):
     return ds, om, means
 
 
+@pytest.mark.parametrize("rr", [0, 8, 2])
 @pytest.mark.parametrize("seed,k,signed", [(0, 64, False), (1, 300, False), (2, 1000, True),
                                            (3, 5, False), (4, 1, False)])
-def test_assign_matches_oracle_exactly(seed, k, signed):
+def test_assign_matches_oracle_exactly(tuning, seed, k, signed, rr):
     from oracle import oracle as O
 
     ds, om, means = _random_case(k=max(k, 1), seed=seed, signed=signed)
-    labels, st = _assign_raw(ds, means)
+    labels, st = _assign_raw(ds, means, rr=rr)
     ol, _, _, post = O.assign(ds, om)
     assert np.array_equal(labels, ol)
     assert st.postings == post == O.volume_ivf(ds, om)
     assert st.objective == O.objective(ds, ol, om)
 
 
+@pytest.mark.parametrize("rr", [0, 8])
 @pytest.mark.parametrize("rowcap,corpus", [(32, 0), (64, 1)])
-def test_multipass_rows(tuning, rowcap, corpus):
+def test_multipass_rows(tuning, rowcap, corpus, rr):
     """Rows longer than the shared-memory stage run in several passes."""
     from oracle import oracle as O
 
     ds, om, means = _random_case(seed=5, k=200, corpus=corpus)
     assert int(np.diff(ds.indptr).max()) > rowcap
-    labels, st = _assign_raw(ds, means, rowcap=rowcap)
+    labels, st = _assign_raw(ds, means, rowcap=rowcap, rr=rr)
     ol, _, _, post = O.assign(ds, om)
     assert np.array_equal(labels, ol) and st.postings == post
 
 
-@pytest.mark.parametrize("k,smem", [(1000, 3 * 1024), (1500, 2 * 1024)])
-def test_cluster_split_dsmem(tuning, k, smem):
+@pytest.mark.parametrize("k,smem,rr", [(1000, 25 * 1024, 0), (1500, 12 * 1024, 0),
+                                       (1000, 3 * 1024, 8), (1500, 2 * 1024, 8)])
+def test_cluster_split_dsmem(tuning, k, smem, rr):
     """Force the thread-block-cluster split (rho spread over 2-8 CTAs' shared
     memory, argmax and candidate window merged over DSMEM)."""
     from oracle import oracle as O
 
     ds, om, means = _random_case(seed=6, k=k, n=2500)
-    labels, st = _assign_raw(ds, means, rowcap=64, smem=smem)
+    labels, st = _assign_raw(ds, means, rowcap=64, smem=smem, rr=rr)
     ol, _, _, post = O.assign(ds, om)
     assert np.array_equal(labels, ol) and st.postings == post
     assert st.objective == O.objective(ds, ol, om)

@@ -27,7 +27,8 @@ def main():
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--iters", type=int, default=2)
     ap.add_argument("--reps", type=int, default=3)
-    ap.add_argument("--rr", default="2,4,8")
+    ap.add_argument("--rr", default="0,8", help="0 = TMA screen, 2/4/8 = LDG screen, "
+                    "-16*w = TMA screen with w warps per CTA")
     ap.add_argument("--rowcap", default="256,512,1024")
     args = ap.parse_args()
     c = synth.CONFIGS[args.config]
@@ -60,6 +61,7 @@ def main():
             out.append(rec)
             print(json.dumps(rec), flush=True)
     eng.lib.ivfkm_set_tuning(1024, 0, 0)
+    eng.lib.ivfkm_set_tuning(1024, 0, -128)
 
 
 if __name__ == "__main__":
