@@ -100,7 +100,9 @@ size_t ivfkm_assign_workspace_size(int64_t n_obj, int64_t k);
 /* Tuning: rowcap = row entries staged in shared memory per pass (default 1024;
  * longer rows run in several passes), smem_limit = shared-memory budget per
  * CTA in bytes (default 225 KB, min 1 KB; a smaller budget forces the thread-block
- * cluster split), rr = 32-mean blocks per warp span (2, 4 or 8; 0 = automatic).
+ * cluster split), rr = 32-mean blocks per warp span of the register screen
+ * (2, 4 or 8; 0 = automatic) or -8 for the TMA-pipelined screen; rr = -16*w
+ * sets w warps per CTA for the TMA screen.
  * Out-of-range values leave the setting unchanged.                          */
 void ivfkm_set_tuning(int rowcap, int smem_limit, int rr);
 int ivfkm_assign(int64_t n_obj, const int64_t* row_ptr /*[dev] n+1*/,

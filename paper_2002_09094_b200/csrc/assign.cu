@@ -852,7 +852,7 @@ struct Plan {
 int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
   const int64_t nblk = ivfkm_bivf_nblk(k);
   Plan pl;
-  if (rr == 0 || rr == -8) {  // default: the TMA-pipelined screen (8-block spans)
+  if (rr == -8) {  // the TMA-pipelined screen (8-block spans); opt-in for now
     pl.tma = true;
     pl.rr = kSpan;
     pl.rowcap = rowcap < 256 ? rowcap : 256;
@@ -937,11 +937,11 @@ extern "C" size_t ivfkm_assign_workspace_size(int64_t n_obj, int64_t /*k*/) {
 // thread-block-cluster split at small k (used by the tests).
 static int g_rowcap = 1024;
 static int g_smem_limit = kSmemLimit - 2048;  // leave room for static smem
-static int g_rr = 0;                          // 0: TMA screen; 2/4/8: LDG screen
+static int g_rr = 0;  // 0: automatic LDG screen; 2/4/8: LDG screen span; -8: TMA screen
 extern "C" void ivfkm_set_tuning(int rowcap, int smem_limit, int rr) {
   if (rowcap >= 32 && rowcap <= 8192) g_rowcap = rowcap / 32 * 32;
   if (smem_limit >= 1024 && smem_limit <= kSmemLimit - 2048) g_smem_limit = smem_limit;
-  if (rr == 0 || rr == 2 || rr == 4 || rr == 8) g_rr = rr;
+  if (rr == 0 || rr == 2 || rr == 4 || rr == 8 || rr == -8) g_rr = rr;
   if (rr <= -16 && rr >= -16 * 16) g_tma_warps = -rr / 16;  // -16*w: TMA warps per CTA
 }
 

@@ -139,6 +139,32 @@ class DeviceMeans:
         return MeanSet(self.k, self.dim, representation, ptr, terms, vals, ret)
 
 
+def update_rows(lib, n_obj, nnz, row_ptr, terms, val64, labels0, sizes, prev: DeviceMeans, k,
+                dim, ws, total_host=None) -> DeviceMeans:
+    """Bit-exact update (variants.py:254-307) of k means from n_obj device rows
+    whose 0-based labels lie in [0, k): ivfkm_update_count, one 8-byte
+    device->host read of the new size, ivfkm_update_fill.  No BIVF."""
+    dev = row_ptr.device
+    new_ptr = torch.empty(k + 1, dtype=torch.int64, device=dev)
+    rc = lib.ivfkm_update_count(n_obj, nnz, _p(row_ptr), _p(terms), _p(val64), k, dim,
+                                _p(labels0), _p(sizes), _p(prev.ptr), _p(new_ptr), _p(ws),
+                                ws.numel(), _stream())
+    _lib.check(rc, "ivfkm_update_count")
+    if total_host is None:
+        total_host = torch.zeros(1, dtype=torch.int64)
+    total_host.copy_(new_ptr[k:], non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    total = int(total_host[0])
+    t = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+    v = torch.empty(max(total, 1), dtype=torch.float64, device=dev)
+    ret = torch.empty(k, dtype=torch.uint8, device=dev)
+    rc = lib.ivfkm_update_fill(n_obj, nnz, k, dim, _p(sizes), _p(prev.ptr), _p(prev.terms),
+                               _p(prev.vals), _p(new_ptr), _p(t), _p(v), _p(ret), total, _p(ws),
+                               ws.numel(), _stream())
+    _lib.check(rc, "ivfkm_update_fill")
+    return DeviceMeans(k, dim, new_ptr, t[:total], v[:total], ret)
+
+
 class LloydEngine:
     """Runs IVF Lloyd iterations over one device-resident dataset."""
 
@@ -234,26 +260,10 @@ class LloydEngine:
     # -- update --------------------------------------------------------------
     def update(self, labels0: torch.Tensor, dm: DeviceMeans) -> DeviceMeans:
         """New means from the assignment (sizes must be the ones ivfkm_assign wrote)."""
-        dd, k, dev = self.dd, self.k, self.device
-        new_ptr = torch.empty(k + 1, dtype=torch.int64, device=dev)
-        rc = self.lib.ivfkm_update_count(dd.n, dd.nnz, _p(dd.row_ptr), _p(dd.terms),
-                                         _p(dd.val64), k, dd.dim, _p(labels0), _p(self.sizes),
-                                         _p(dm.ptr), _p(new_ptr), _p(self.ws_update),
-                                         self.ws_update.numel(), _stream())
-        _lib.check(rc, "ivfkm_update_count")
-        self.total_host.copy_(new_ptr[k:], non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        total = int(self.total_host[0])
-        terms = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
-        vals = torch.empty(max(total, 1), dtype=torch.float64, device=dev)
-        ret = torch.empty(k, dtype=torch.uint8, device=dev)
-        rc = self.lib.ivfkm_update_fill(dd.n, dd.nnz, k, dd.dim, _p(self.sizes), _p(dm.ptr),
-                                        _p(dm.terms), _p(dm.vals), _p(new_ptr), _p(terms),
-                                        _p(vals), _p(ret), total, _p(self.ws_update),
-                                        self.ws_update.numel(), _stream())
-        _lib.check(rc, "ivfkm_update_fill")
+        dd = self.dd
+        out = update_rows(self.lib, dd.n, dd.nnz, dd.row_ptr, dd.terms, dd.val64, labels0,
+                          self.sizes, dm, self.k, dd.dim, self.ws_update, self.total_host)
         self.launches += 12
-        out = DeviceMeans(k, dd.dim, new_ptr, terms[:total], vals[:total], ret)
         return self.build_bivf(out)
 
     def set_sizes_from_labels(self, labels0: torch.Tensor) -> None:

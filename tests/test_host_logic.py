@@ -138,24 +138,7 @@ def test_pairwise_norm_replay_matches_numpy(D):
         assert _combine(D, vals) == float(np.sum(w * w))
 
 
-def _add_exact(s, limbs):
-    """Python replay of add_exact in assign.cu."""
-    if s == 0.0:
-        return
-    bits = np.array([s]).view(np.uint64)[0].item()
-    ex = (bits >> 52) & 0x7FF
-    m = bits & ((1 << 52) - 1)
-    b = 0
-    if ex:
-        m |= 1 << 52
-        b = ex - 1
-    idx, sh = b >> 5, b & 31
-    sg = -1 if bits >> 63 else 1
-    c0 = (m << sh) & 0xFFFFFFFF
-    t = (m >> (32 - sh)) if sh else (m >> 32)
-    limbs[idx] += sg * c0
-    limbs[idx + 1] += sg * (t & 0xFFFFFFFF)
-    limbs[idx + 2] += sg * (t >> 32)
+from exact_sum import add_exact as _add_exact  # noqa: E402
 
 
 def test_exact_objective_accumulator_equals_fsum():
