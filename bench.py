@@ -191,38 +191,51 @@ def cpu_sample_assign(ds, inv, k, rows, threads):
     return time.perf_counter() - t0
 
 
-def cpu_baseline_measure(ds, k, seed, budget_s, steps=1, labels=None):
-    """Time the reference CPU path: sampled all-core assign (extrapolated to N)
-    + full numpy update + objective.  Returns dict and per-step seconds."""
+def cpu_baseline_measure(ds, k, seed, budget_s, steps=1, labels=None, means=None):
+    """Time the reference CPU path on this host: all-core sampled assign with
+    the reference's own compiled kernel (oracle/_ref; the C restatement when
+    it was not built), extrapolated to N, plus the numpy update
+    (variants.py:254-307) and objective on the full corpus.
+
+    ``means``/``labels``: the state the GPU arm is timing (same iteration);
+    without them the means are warmed by one update from seeded random labels
+    (untimed) so the postings per object resemble a steady-state iteration
+    rather than the sparse initial means."""
     import numpy as np
 
     from oracle import oracle as O
 
     threads = O.host_threads()
-    m = O.init_means(ds, k, seed)
+    rng = np.random.default_rng(0)
+    if means is None:
+        m0 = O.init_means(ds, k, seed)
+        warm = rng.integers(1, k + 1, size=ds.n).astype(np.int32)
+        m = O.update(ds, warm, m0)
+    else:
+        m = O.Means(means.k, means.dim, np.asarray(means.indptr), np.asarray(means.term_ids),
+                    np.asarray(means.values), np.asarray(means.retained))
+    if labels is None:
+        labels = rng.integers(1, k + 1, size=ds.n).astype(np.int32)
     inv = O.inverted(m)
-    # size the sample from a short probe
     probe = min(ds.n, max(threads * 4, 64))
     tp = cpu_sample_assign(ds, inv, k, probe, threads)
     rows = int(min(ds.n, max(probe, probe * budget_s / max(tp, 1e-6))))
-    per_step = []
-    if labels is None:
-        rng = np.random.default_rng(0)
-        labels = rng.integers(1, k + 1, size=ds.n).astype(np.int32)
     t0 = time.perf_counter()
     O.update(ds, labels, m)
     t_upd = time.perf_counter() - t0
     t0 = time.perf_counter()
     O.objective(ds, labels, m)
     t_obj = time.perf_counter() - t0
+    per_step = []
     for _ in range(steps):
         ta = cpu_sample_assign(ds, inv, k, rows, threads) * ds.n / rows
         per_step.append(ta + t_upd + t_obj)
     _, kind = cpu_assign_kernel()
     sample = (f"assign: {rows} of {ds.n} rows on {threads} threads "
-              f"({'reference _kernels.assign_ivf' if kind == 'reference' else 'C oracle'}), "
-              f"scaled to N; update (numpy restatement of variants.py:254-307, 1 thread) "
-              f"{t_upd:.2f}s and objective {t_obj:.2f}s on the full corpus")
+              f"({'reference _kernels.assign_ivf (oracle/_ref)' if kind == 'reference' else 'C oracle'}), "
+              f"scaled to N, means {'= the GPU run state' if means is not None else 'warmed by one update'}; "
+              f"update (numpy restatement of variants.py:254-307, 1 thread) {t_upd:.2f}s and "
+              f"objective {t_obj:.2f}s on the full corpus")
     return {"threads": threads, "kind": kind, "sample": sample, "t_update": t_upd,
             "t_objective": t_obj}, per_step
 
@@ -384,7 +397,7 @@ def ours_arm(args, rank, world):
         try:
             labels = (lab.cpu().numpy() + 1).astype(np.int32)
             info, per = cpu_baseline_measure(ds, k, c["seed"], args.cpu_seconds, steps=1,
-                                             labels=labels)
+                                             labels=labels, means=dm.to_meanset())
             line["cpu_baseline"] = {"value": 1.0 / per[0], "unit": UNIT, "cores": info["threads"],
                                     "kind": info["kind"], "sample": info["sample"]}
         except Exception as exc:  # baseline must not sink the GPU number

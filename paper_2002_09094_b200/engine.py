@@ -139,6 +139,13 @@ class DeviceMeans:
         return MeanSet(self.k, self.dim, representation, ptr, terms, vals, ret)
 
 
+def update_launches(k: int, dim: int) -> int:
+    """Kernels one update launches: keys, CUB onesweep radix sort (histogram,
+    exclusive sum, one pass per 8 key bits), head, 3 CUB scans (init + sweep
+    each), segstart, segsum, clseg, norm, fill, retain."""
+    bits = max(1, int(np.ceil(np.log2(max(2.0, float(k) * float(dim))))))
+    return 1 + 2 + (bits + 7) // 8 + 1 + 6 + 6
+
 def update_rows(lib, n_obj, nnz, row_ptr, terms, val64, labels0, sizes, prev: DeviceMeans, k,
                 dim, ws, total_host=None) -> DeviceMeans:
     """Bit-exact update (variants.py:254-307) of k means from n_obj device rows
@@ -206,7 +213,7 @@ class LloydEngine:
                                        _p(dm.vals), _p(dm.headers), _p(dm.pv32), _p(dm.pv64),
                                        _p(self.ws_bivf), self.ws_bivf.numel(), _stream())
         _lib.check(rc, "ivfkm_bivf_build")
-        self.launches += 5
+        self.launches += 7  # mask, count, scan (init + sweep), offset, scatter, nc
         return dm
 
     def upload_means(self, ms) -> DeviceMeans:
@@ -263,7 +270,7 @@ class LloydEngine:
         dd = self.dd
         out = update_rows(self.lib, dd.n, dd.nnz, dd.row_ptr, dd.terms, dd.val64, labels0,
                           self.sizes, dm, self.k, dd.dim, self.ws_update, self.total_host)
-        self.launches += 12
+        self.launches += update_launches(self.k, dd.dim)
         return self.build_bivf(out)
 
     def set_sizes_from_labels(self, labels0: torch.Tensor) -> None:
