@@ -594,6 +594,186 @@ __global__ void __launch_bounds__(512) screen_tma_kernel(ScreenParams p) {
 }
 
 // ---------------------------------------------------------------------------
+// cp.async-pipelined screen.  Same ownership and arithmetic as
+// screen_kernel<8>, but each (object nonzero, span) segment — the span's
+// contiguous, 16-B-padded values and, for a sparse span, its 32-B mask row —
+// is copied global -> shared with 16-B cp.async (LDGSTS) into a per-warp ring
+// of kAsyncStages stages, kAsyncStages-1 entries ahead of the FMAs.  The
+// segment bounds come from a per-span prepass (all lanes load offsets for the
+// whole staged row at once), so only one dependent global latency remains
+// per row chunk, and the in-flight data occupies shared memory, not registers.
+
+constexpr int kAsyncStages = 6;
+constexpr int kAsyncStageBytes = 32 + 4 * 256;
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__host__ __device__ inline size_t async_warp_bytes(int rowcap) {
+  return (size_t)8 * rowcap + (size_t)kAsyncStages * kAsyncStageBytes;
+}
+
+__global__ void __launch_bounds__(512) screen_async_kernel(ScreenParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ ScreenShared sh;
+  constexpr int RR = kSpan;
+  float* rho = reinterpret_cast<float*>(smem);
+  const int cta_cids = p.cta_blocks * 32;
+  int32_t* s_term = reinterpret_cast<int32_t*>(rho + cta_cids);
+  float* s_val = reinterpret_cast<float*>(s_term + p.rowcap);
+
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int z = blockIdx.x % p.nsplit;
+  const int64_t obj = blockIdx.x / p.nsplit;
+  if (obj >= p.n_obj) return;
+  const int64_t rb = p.row_ptr[obj], re = p.row_ptr[obj + 1];
+  const int64_t nblk = p.nblk;
+  const int64_t blk0 = (int64_t)z * p.cta_blocks;
+  const int nspans = p.cta_blocks / RR;
+  const unsigned lanebit = 1u << lane;
+  const unsigned lt = lanebit - 1u;
+
+  unsigned char* wbase = reinterpret_cast<unsigned char*>(s_val + p.rowcap);
+  wbase = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(wbase) + 127) &
+                                           ~(uintptr_t)127);
+  wbase += (size_t)warp * async_warp_bytes(p.rowcap);
+  unsigned char* ring = wbase;  // kAsyncStages stages, 16-B aligned
+  uint32_t* m_os = reinterpret_cast<uint32_t*>(wbase + (size_t)kAsyncStages * kAsyncStageBytes);
+  uint32_t* m_nv = m_os + p.rowcap;
+
+  __shared__ const void* s_base[4];
+  if (threadIdx.x == 0) {
+    s_base[0] = p.masks;
+    s_base[1] = p.offs;
+    s_base[2] = p.pv32;
+    s_base[3] = p.nc;
+  }
+  __syncthreads();
+  const uint32_t* __restrict__ masks = static_cast<const uint32_t*>(s_base[0]);
+  const uint32_t* __restrict__ offs = static_cast<const uint32_t*>(s_base[1]);
+  const float* __restrict__ pv = static_cast<const float*>(s_base[2]);
+  const uint32_t* __restrict__ ncp = static_cast<const uint32_t*>(s_base[3]);
+  unsigned long long post = 0;
+
+  int64_t c0 = rb;
+  do {
+    const int64_t rem = re - c0;
+    const int cn = (int)(rem < p.rowcap ? rem : p.rowcap);
+    __syncthreads();
+    for (int j = threadIdx.x; j < cn; j += blockDim.x) {
+      const int32_t t = p.terms[c0 + j];
+      s_term[j] = t;
+      s_val[j] = p.val32[c0 + j];
+      if (z == 0) post += __ldg(ncp + t);
+    }
+    __syncthreads();
+    const bool first = (c0 == rb);
+    for (int sp = warp; sp < nspans; sp += nwarps) {
+      const int64_t gb = blk0 + (int64_t)sp * RR;
+      float acc[RR];
+#pragma unroll
+      for (int r = 0; r < RR; ++r) acc[r] = first ? 0.f : rho[(sp * RR + r) * 32 + lane];
+      if (gb < nblk) {
+        const uint32_t nb32 = (uint32_t)nblk, gb32 = (uint32_t)gb;
+        // ---- prepass: segment bounds of every staged entry for this span
+        for (int j0 = 0; j0 < cn; j0 += 128) {
+          uint32_t os[4], oe[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int e = j0 + 32 * q + lane;
+            os[q] = 0u;
+            oe[q] = 0u;
+            if (e < cn) {
+              const uint32_t row = (uint32_t)s_term[e] * nb32 + gb32;
+              os[q] = __ldg(offs + row);
+              oe[q] = __ldg(offs + row + RR);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int e = j0 + 32 * q + lane;
+            if (e < cn) {
+              m_os[e] = os[q];
+              m_nv[e] = (oe[q] & ~kDense) - (os[q] & ~kDense);
+            }
+          }
+        }
+        __syncwarp();
+        auto issue = [&](int e) {
+          if (e < cn) {
+            unsigned char* dst = ring + (size_t)(e % kAsyncStages) * kAsyncStageBytes;
+            const uint32_t os = m_os[e];
+            const uint32_t nv = m_nv[e];
+            if (nv) {
+              if (!(os & kDense) && lane < 2)
+                cp_async16(dst + 16 * lane,
+                           masks + (uint32_t)s_term[e] * nb32 + gb32 + 4u * (uint32_t)lane);
+              const float* src = pv + (os & ~kDense);
+              for (uint32_t q = (uint32_t)lane; 4u * q < nv; q += 32u)
+                cp_async16(dst + 32 + 16 * q, src + 4u * q);
+            }
+          }
+          cp_async_commit();
+        };
+#pragma unroll
+        for (int e = 0; e < kAsyncStages - 1; ++e) issue(e);
+        for (int e = 0; e < cn; ++e) {
+          issue(e + kAsyncStages - 1);
+          cp_async_wait<kAsyncStages - 1>();
+          __syncwarp();
+          const uint32_t os = m_os[e];
+          const uint32_t nv = m_nv[e];
+          if (nv) {
+            const unsigned char* src = ring + (size_t)(e % kAsyncStages) * kAsyncStageBytes;
+            const float v = s_val[e];
+            float u[RR];
+            if (os & kDense) {
+              const float4 a = reinterpret_cast<const float4*>(src + 32)[lane];
+              const float4 b = reinterpret_cast<const float4*>(src + 32)[32 + lane];
+              u[0] = a.x; u[1] = a.y; u[2] = a.z; u[3] = a.w;
+              u[4] = b.x; u[5] = b.y; u[6] = b.z; u[7] = b.w;
+            } else {
+              const uint4 ma = reinterpret_cast<const uint4*>(src)[0];
+              const uint4 mb = reinterpret_cast<const uint4*>(src)[1];
+              const uint32_t m[RR] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
+              const float* vals = reinterpret_cast<const float*>(src + 32);
+              uint32_t o = 0;
+#pragma unroll
+              for (int r = 0; r < RR; ++r) {
+                u[r] = 0.f;
+                if (m[r] & lanebit) u[r] = vals[o + (uint32_t)__popc(m[r] & lt)];
+                o += (uint32_t)__popc(m[r]);
+              }
+            }
+#pragma unroll
+            for (int r = 0; r < RR; ++r) acc[r] = fmaf(v, u[r], acc[r]);
+          }
+          __syncwarp();  // the stage is re-filled by issue(e + kAsyncStages)
+        }
+        cp_async_wait<0>();
+        __syncwarp();
+      }
+#pragma unroll
+      for (int r = 0; r < RR; ++r) rho[(sp * RR + r) * 32 + lane] = acc[r];
+    }
+    c0 += p.rowcap;
+  } while (c0 < re);
+  __syncthreads();
+  screen_epilogue(p, sh, rho, obj, z, rb, re, post);
+}
+
+// ---------------------------------------------------------------------------
 // exact float64 similarity of object rows to one mean, in the reference order
 
 struct ExactCtx {
@@ -846,14 +1026,16 @@ static int g_tma_warps = 8;
 struct Plan {
   int rr, nsplit, cta_blocks, warps, rowcap;
   bool tma;
+  int mode;  // 0 LDG register screen, 1 TMA ring, 2 cp.async ring
   size_t smem;
 };
 
 int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
   const int64_t nblk = ivfkm_bivf_nblk(k);
   Plan pl;
-  if (rr == -8) {  // the TMA-pipelined screen (8-block spans); opt-in for now
+  if (rr == -8 || rr == -4) {  // TMA (-8) / cp.async (-4) pipelined screens, 8-block spans
     pl.tma = true;
+    pl.mode = rr == -8 ? 1 : 2;
     pl.rr = kSpan;
     pl.rowcap = rowcap < 256 ? rowcap : 256;
     const int64_t spans_total = nblk / kSpan;
@@ -863,7 +1045,8 @@ int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
       const int spans = (int)(cb / kSpan);
       const int warps = spans < g_tma_warps ? spans : g_tma_warps;
       const size_t smem = (size_t)cb * 128 + (size_t)pl.rowcap * 8 + 128 +
-                          (size_t)warps * tma_warp_bytes(pl.rowcap);
+                          (size_t)warps * (pl.mode == 1 ? tma_warp_bytes(pl.rowcap)
+                                                        : async_warp_bytes(pl.rowcap));
       if (smem <= (size_t)smem_limit) {
         pl.nsplit = s;
         pl.cta_blocks = (int)cb;
@@ -877,6 +1060,7 @@ int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
     return IVFKM_E_UNSUPPORTED;
   }
   pl.tma = false;
+  pl.mode = 0;
   pl.rr = rr > 0 ? rr : (nblk >= 32 ? 8 : 2);
   pl.rowcap = rowcap;
   const size_t stage = (size_t)rowcap * 8;
@@ -905,7 +1089,8 @@ int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
 
 template <int RR>
 int launch_screen(const Plan& pl, const ScreenParams& p, cudaStream_t st) {
-  auto fn = pl.tma ? screen_tma_kernel : screen_kernel<RR>;
+  auto fn = pl.mode == 1 ? screen_tma_kernel
+                         : (pl.mode == 2 ? screen_async_kernel : screen_kernel<RR>);
   IVFKM_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(p.n_obj * pl.nsplit));
@@ -941,7 +1126,7 @@ static int g_rr = 0;  // 0: automatic LDG screen; 2/4/8: LDG screen span; -8: TM
 extern "C" void ivfkm_set_tuning(int rowcap, int smem_limit, int rr) {
   if (rowcap >= 32 && rowcap <= 8192) g_rowcap = rowcap / 32 * 32;
   if (smem_limit >= 1024 && smem_limit <= kSmemLimit - 2048) g_smem_limit = smem_limit;
-  if (rr == 0 || rr == 2 || rr == 4 || rr == 8 || rr == -8) g_rr = rr;
+  if (rr == 0 || rr == 2 || rr == 4 || rr == 8 || rr == -8 || rr == -4) g_rr = rr;
   if (rr <= -16 && rr >= -16 * 16) g_tma_warps = -rr / 16;  // -16*w: TMA warps per CTA
 }
 

@@ -211,7 +211,7 @@ def _random_case(n=1500, dim=400, k=64, seed=0, signed=False, corpus=0):
     return ds, om, means
 
 
-@pytest.mark.parametrize("rr", [0, -8, 2])
+@pytest.mark.parametrize("rr", [0, -8, -4, 2])
 @pytest.mark.parametrize("seed,k,signed", [(0, 64, False), (1, 300, False), (2, 1000, True),
                                            (3, 5, False), (4, 1, False)])
 def test_assign_matches_oracle_exactly(tuning, seed, k, signed, rr):
@@ -225,7 +225,7 @@ def test_assign_matches_oracle_exactly(tuning, seed, k, signed, rr):
     assert st.objective == O.objective(ds, ol, om)
 
 
-@pytest.mark.parametrize("rr", [0, -8])
+@pytest.mark.parametrize("rr", [0, -8, -4])
 @pytest.mark.parametrize("rowcap,corpus", [(32, 0), (64, 1)])
 def test_multipass_rows(tuning, rowcap, corpus, rr):
     """Rows longer than the shared-memory stage run in several passes."""
@@ -239,6 +239,7 @@ def test_multipass_rows(tuning, rowcap, corpus, rr):
 
 
 @pytest.mark.parametrize("k,smem,rr", [(1000, 25 * 1024, -8), (1500, 12 * 1024, -8),
+                                       (1000, 25 * 1024, -4), (1500, 12 * 1024, -4),
                                        (1000, 3 * 1024, 0), (1500, 2 * 1024, 0)])
 def test_cluster_split_dsmem(tuning, k, smem, rr):
     """Force the thread-block-cluster split (rho spread over 2-8 CTAs' shared
