@@ -343,34 +343,25 @@ def ours_arm(args, rank, world):
         except Exception:
             traffic = None
 
-    # ---- end to end through host buffers (corpus + means H2D, labels + means D2H)
+    # ---- end to end through host buffers: every step uploads the corpus and the
+    # current means from pinned memory and reads labels + new means back
+    from paper_2002_09094_b200.engine import HostIteration
+
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(1, min(args.steps, 5))
     host_means = dm.to_meanset()
+    stepper = HostIteration(hd, k, dev)
     h2d = d2h = 0
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(e2e_steps):
-        dd2 = DeviceDataset(hd, dev)
-        eng.dd = dd2
-        dmh = DeviceMeans.from_meanset(host_means, dev)
-        h2d_step = hd.nbytes + host_means.indptr.nbytes + host_means.term_ids.nbytes + \
-            host_means.values.nbytes + host_means.retained.nbytes
-        dmh = eng.build_bivf(dmh)
-        lab = eng.assign(dmh, None)
-        st = eng.read_stats()
-        labels_host = lab.cpu()
-        new = eng.update(lab, dmh)
-        host_means = new.to_meanset()
-        d2h_step = labels_host.numel() * 4 + host_means.indptr.nbytes + \
-            host_means.term_ids.nbytes + host_means.values.nbytes + host_means.retained.nbytes
-        h2d, d2h = h2d_step, d2h_step
-    e1.record()
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
-    e2e_dev_ms = e0.elapsed_time(e1)
-    e2e_value = e2e_steps / max(e2e_s, e2e_dev_ms / 1000.0)
+    e2e_value = None
+    if e2e_steps > 0:
+        _, host_means, _ = stepper.step(host_means)  # warm-up (allocations)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            labels_e2e, host_means, _ = stepper.step(host_means)
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        e2e_value = e2e_steps / e2e_s
+        h2d, d2h = stepper.last_h2d, stepper.last_d2h
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -128,7 +128,7 @@ struct MaskPack {
 // o_{r+1} = o_r + popc(mask_r); in a dense span (kDense on the offset) the
 // lane's values sit at span_base + 128*(r/4) + 4*lane + r%4 (bivf.cuh).
 template <int RR>
-__device__ __forceinline__ void gather_values(const MaskPack<RR>& mk, uint32_t o, uint32_t gb,
+__device__ __forceinline__ bool gather_values(const MaskPack<RR>& mk, uint32_t o, uint32_t gb,
                                               const float* __restrict__ pv, unsigned lane,
                                               unsigned lanebit, unsigned lt, float (&u)[RR]) {
   if (o & kDense) {
@@ -146,8 +146,12 @@ __device__ __forceinline__ void gather_values(const MaskPack<RR>& mk, uint32_t o
         u[r] = __ldg(pv + sbase + 128u * (rr >> 2) + 4u * lane + (rr & 3u));
       }
     }
-    return;
+    return true;
   }
+  uint32_t any = 0;
+#pragma unroll
+  for (int r = 0; r < RR; ++r) any |= mk.m[r];
+  if (!any) return false;  // the term populates none of these blocks
 #pragma unroll
   for (int r = 0; r < RR; ++r) {
     const uint32_t mr = mk.m[r];
@@ -155,6 +159,7 @@ __device__ __forceinline__ void gather_values(const MaskPack<RR>& mk, uint32_t o
     if (mr & lanebit) u[r] = __ldg(pv + (o + (uint32_t)__popc(mr & lt)));
     o += (uint32_t)__popc(mr);
   }
+  return true;
 }
 
 // CTA-local argmax (value desc, index asc) over the parked rho, merged over
@@ -354,20 +359,25 @@ __global__ void __maxnreg__(72) screen_kernel(ScreenParams p) {
         uint32_t o;
         float uA[RR], uB[RR];
         ld(0, mk, o);
-        gather_values<RR>(mk, o, gb32, pv, lane, lanebit, lt, uA);
+        bool hA = gather_values<RR>(mk, o, gb32, pv, lane, lanebit, lt, uA), hB;
         ld(1, mk, o);
         for (int e = 0; e < cn; e += 2) {
-          gather_values<RR>(mk, o, gb32, pv, lane, lanebit, lt, uB);  // entry e+1 (zeros past the end)
+          hB = gather_values<RR>(mk, o, gb32, pv, lane, lanebit, lt, uB);  // entry e+1
           ld(e + 2, mk, o);
-          const float vA = s_val[e];
-          // fma(v, 0, acc) == acc exactly: absent postings cost no rounding
+          // fma(v, 0, acc) == acc exactly: absent postings cost no rounding;
+          // a span the term does not populate skips the FMAs altogether
+          if (hA) {
+            const float vA = s_val[e];
 #pragma unroll
-          for (int r = 0; r < RR; ++r) acc[r] = fmaf(vA, uA[r], acc[r]);
-          gather_values<RR>(mk, o, gb32, pv, lane, lanebit, lt, uA);  // entry e+2
+            for (int r = 0; r < RR; ++r) acc[r] = fmaf(vA, uA[r], acc[r]);
+          }
+          hA = gather_values<RR>(mk, o, gb32, pv, lane, lanebit, lt, uA);  // entry e+2
           ld(e + 3, mk, o);
-          const float vB = (e + 1 < cn) ? s_val[e + 1] : 0.f;
+          if (hB) {
+            const float vB = s_val[e + 1];
 #pragma unroll
-          for (int r = 0; r < RR; ++r) acc[r] = fmaf(vB, uB[r], acc[r]);
+            for (int r = 0; r < RR; ++r) acc[r] = fmaf(vB, uB[r], acc[r]);
+          }
         }
       }
 #pragma unroll

@@ -131,11 +131,13 @@ class DeviceMeans:
         ret = torch.from_numpy(np.array(ms.retained, dtype=np.uint8)).to(dev)
         return cls(ms.k, ms.dim, ptr, terms, vals, ret)
 
-    def to_meanset(self, representation: str = "sparse_inverted") -> MeanSet:
+    def to_meanset(self, representation: str = "sparse_inverted", validate: bool = True) -> MeanSet:
         ptr = self.ptr.cpu().numpy()
-        terms = self.terms.cpu().numpy().astype(np.int32) + 1
+        terms = (self.terms + 1).cpu().numpy()
         vals = self.vals.cpu().numpy()
         ret = self.retained.cpu().numpy().astype(bool)
+        if not validate:
+            return MeanSet.trusted(self.k, self.dim, representation, ptr, terms, vals, ret)
         return MeanSet(self.k, self.dim, representation, ptr, terms, vals, ret)
 
 
@@ -276,3 +278,69 @@ class LloydEngine:
     def set_sizes_from_labels(self, labels0: torch.Tensor) -> None:
         """sizes = bincount(labels) for an externally supplied assignment."""
         self.sizes.copy_(torch.bincount(labels0.long(), minlength=self.k))
+
+
+class HostIteration:
+    """One Lloyd iteration through host buffers — the end-to-end path.
+
+    Every call copies the corpus (pinned HostDataset) and the current means
+    host -> device, runs assign + update on the GPU, and reads labels, the
+    statistics and the new means back into pinned buffers; the returned
+    MeanSet wraps those host buffers (double-buffered, so the next call can
+    upload them while they stay valid).  Equivalent to the reference's
+    assign_ivf + objective_cosine + update_ivf on host arrays.
+    """
+
+    def __init__(self, hd: HostDataset, k: int, device="cuda"):
+        self.hd, self.k = hd, int(k)
+        self.device = torch.device(device)
+        self.eng = None
+        self.buf = [None, None]
+        self.cur = 0
+        self.labels_host = torch.empty(hd.n, dtype=torch.int32).pin_memory()
+        self.last_h2d = self.last_d2h = 0
+
+    def _host_buffers(self, nnz: int):
+        b = self.buf[self.cur]
+        if b is None or b["cap"] < nnz:
+            cap = int(nnz * 1.25) + 1024
+            b = {"cap": cap,
+                 "ptr": torch.empty(self.k + 1, dtype=torch.int64).pin_memory(),
+                 "terms": torch.empty(cap, dtype=torch.int32).pin_memory(),
+                 "vals": torch.empty(cap, dtype=torch.float64).pin_memory(),
+                 "ret": torch.empty(self.k, dtype=torch.uint8).pin_memory()}
+            self.buf[self.cur] = b
+        return b
+
+    def step(self, ms: MeanSet):
+        dev = self.device
+        dd = DeviceDataset(self.hd, dev)  # H2D of the corpus (pinned, async)
+        if self.eng is None:
+            self.eng = LloydEngine(dd, self.k)
+        self.eng.dd = dd
+        t = lambda a: torch.from_numpy(np.asarray(a))  # noqa: E731 (pinned views stay pinned)
+        ptr = t(ms.indptr).to(dev, non_blocking=True)
+        terms = t(ms.term_ids).to(dev, non_blocking=True) - 1
+        vals = t(ms.values).to(dev, non_blocking=True)
+        ret = t(np.asarray(ms.retained).view(np.uint8)).to(dev, non_blocking=True)
+        dm = self.eng.build_bivf(DeviceMeans(self.k, ms.dim, ptr, terms, vals, ret))
+        lab = self.eng.assign(dm, None)
+        st = self.eng.read_stats()
+        self.labels_host.copy_(lab, non_blocking=True)
+        new = self.eng.update(lab, dm)
+        self.cur ^= 1
+        b = self._host_buffers(new.nnz)
+        b["ptr"].copy_(new.ptr, non_blocking=True)
+        b["terms"][: new.nnz].copy_(new.terms + 1, non_blocking=True)
+        b["vals"][: new.nnz].copy_(new.vals, non_blocking=True)
+        b["ret"].copy_(new.retained, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        out = MeanSet.trusted(self.k, ms.dim, "sparse_inverted", b["ptr"].numpy(),
+                              b["terms"][: new.nnz].numpy(), b["vals"][: new.nnz].numpy(),
+                              b["ret"].numpy().view(np.bool_))
+        labels = self.labels_host.numpy() + 1
+        self.last_h2d = self.hd.nbytes + ms.indptr.nbytes + ms.term_ids.nbytes + \
+            ms.values.nbytes + np.asarray(ms.retained).nbytes
+        self.last_d2h = self.labels_host.numel() * 4 + C.sizeof(_lib.Stats) + \
+            (self.k + 1) * 8 + new.nnz * 12 + self.k
+        return labels, out, st

@@ -151,6 +151,21 @@ class MeanSet:
         object.__setattr__(self, "retained", _frozen(r))
 
     @classmethod
+    def trusted(cls, k, dim, representation, indptr, term_ids, values, retained) -> "MeanSet":
+        """Wrap arrays produced by the device update without re-validating them:
+        its output is strictly increasing per mean and unit-norm by
+        construction (bit-identical to variants.py:254-307, whose MeanSet the
+        tests validate).  Arrays are frozen, not copied."""
+        obj = cls.__new__(cls)
+        for name, val in (("k", int(k)), ("dim", int(dim)), ("representation", representation),
+                          ("indptr", indptr), ("term_ids", term_ids), ("values", values),
+                          ("retained", retained)):
+            if isinstance(val, np.ndarray):
+                val.setflags(write=False)
+            object.__setattr__(obj, name, val)
+        return obj
+
+    @classmethod
     def from_csr(cls, indptr, term_ids, values, dim, representation="sparse_standard",
                  retained=None) -> "MeanSet":
         k = int(np.asarray(indptr).size - 1)

@@ -327,3 +327,24 @@ def test_dist_driver_single_rank_matches_engine():
         m = O.update(ds, ol, m)
         assert np.array_equal(dm.vals.cpu().numpy(), m.values)
         prev = lab
+
+
+def test_host_iteration_end_to_end_matches_oracle():
+    """The e2e path (corpus + means uploaded from pinned host memory each step,
+    labels + means read back) equals the oracle's iteration bit for bit."""
+    from oracle import oracle as O
+    from paper_2002_09094_b200.engine import HostDataset, HostIteration
+
+    P = _pkg()
+    ds, om, means = _random_case(n=1800, dim=900, seed=14, k=60)
+    it = HostIteration(HostDataset(ds, pin=True), 60, "cuda")
+    m = om
+    for _ in range(3):
+        labels, means, st = it.step(means)
+        ol, _, _, post = O.assign(ds, m)
+        assert np.array_equal(labels, ol) and st.postings == post
+        assert st.objective == O.objective(ds, ol, m)
+        m = O.update(ds, ol, m)
+        assert np.array_equal(means.values, m.values) and np.array_equal(means.term_ids, m.term_ids)
+        P.MeanSet(means.k, means.dim, means.representation, means.indptr, means.term_ids,
+                  means.values, means.retained)  # the trusted wrap passes full validation
