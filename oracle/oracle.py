@@ -9,8 +9,9 @@ reference file:line it follows (paths under /root/reference/pkg/src/sparse_kmean
                  here (oracle/build_ref.sh), loaded by ``ref_kernels()``
 * inverted    -> means.py:169-179   MeanSet.inverted
 * update      -> variants.py:240-307 _member_entry_order + update_means
-* objective   -> clustering.py:105-119 objective_cosine (sparse gather instead of the
-                 k x D dense matrix; same products, same per-object order, fsum)
+* objective   -> clustering.py:105-119 objective_cosine (the reference's dense k x D
+                 gather when it fits in memory, else the same products gathered
+                 from the sparse CSR; same per-object order, fsum)
 * volume      -> counters.py:71-81  mult_volume_ivf
 * seeding     -> clustering.py:41-102 SplitMix64 / sample_without_replacement / init_means
 * run         -> clustering.py:229-315 (IVF branch)
@@ -205,13 +206,20 @@ def update(ds, labels, prev: Means) -> Means:
     return Means(k, ds.dim, indptr, terms.astype(np.int32), vals, retained)
 
 
-def objective(ds, labels, m: Means) -> float:
-    """clustering.py:105-119 without the dense k x D matrix: each entry's
-    product v * mu_{label}[t] (0 where the mean lacks t), per-object bincount
-    in entry order, then math.fsum."""
+def objective(ds, labels, m: Means, dense_limit: int = 600_000_000) -> float:
+    """clustering.py:105-119: each entry's product v * mu_{label}[t] (0 where
+    the mean lacks t), per-object bincount in entry order, then math.fsum.
+    Uses the reference's dense k x D gather when it fits (k*D <= dense_limit
+    float64s), else the same products gathered from the sparse CSR."""
     n = ds.indptr.size - 1
     owners = np.repeat(np.arange(n), np.diff(ds.indptr))
     rows = (np.asarray(labels, np.int64) - 1)[owners]
+    if m.k * m.dim <= dense_limit:  # literally clustering.py:115-119 (means.py:156-162)
+        dense = np.zeros((m.k, m.dim), dtype=np.float64)
+        dense[np.repeat(np.arange(m.k), np.diff(m.indptr)), m.term_ids - 1] = m.values
+        contrib = np.asarray(ds.values) * dense[rows, np.asarray(ds.term_ids) - 1]
+        sims = np.bincount(owners, weights=contrib, minlength=n)
+        return math.fsum(sims.tolist())
     mkeys = np.repeat(np.arange(m.k, dtype=np.int64), np.diff(m.indptr)) * (m.dim + 1) + \
         m.term_ids.astype(np.int64)
     ekeys = rows * (m.dim + 1) + np.asarray(ds.term_ids, np.int64)

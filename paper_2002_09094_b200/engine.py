@@ -291,7 +291,7 @@ class HostIteration:
     assign_ivf + objective_cosine + update_ivf on host arrays.
     """
 
-    def __init__(self, hd: HostDataset, k: int, device="cuda"):
+    def __init__(self, hd: HostDataset, k: int, device="cuda", prefetch: bool = True):
         self.hd, self.k = hd, int(k)
         self.device = torch.device(device)
         self.eng = None
@@ -299,6 +299,18 @@ class HostIteration:
         self.cur = 0
         self.labels_host = torch.empty(hd.n, dtype=torch.int32).pin_memory()
         self.last_h2d = self.last_d2h = 0
+        # the next step's corpus upload overlaps this step's kernels on a copy stream
+        self.prefetch = prefetch
+        self.copy_stream = torch.cuda.Stream(device=self.device) if prefetch else None
+        self.next_dd = None
+        self.next_ready = None
+
+    def _upload(self):
+        with torch.cuda.stream(self.copy_stream):
+            dd = DeviceDataset(self.hd, self.device)
+            ev = torch.cuda.Event()
+            ev.record(self.copy_stream)
+        return dd, ev
 
     def _host_buffers(self, nnz: int):
         b = self.buf[self.cur]
@@ -314,7 +326,16 @@ class HostIteration:
 
     def step(self, ms: MeanSet):
         dev = self.device
-        dd = DeviceDataset(self.hd, dev)  # H2D of the corpus (pinned, async)
+        if self.prefetch:
+            if self.next_dd is None:
+                self.next_dd, self.next_ready = self._upload()
+            dd, ready = self.next_dd, self.next_ready
+            torch.cuda.current_stream().wait_event(ready)
+            for t_ in (dd.row_ptr, dd.terms, dd.val64, dd.xnorm, dd.val32):
+                t_.record_stream(torch.cuda.current_stream())
+            self.next_dd, self.next_ready = self._upload()  # the next step's corpus
+        else:
+            dd = DeviceDataset(self.hd, dev)  # H2D of the corpus (pinned, async)
         if self.eng is None:
             self.eng = LloydEngine(dd, self.k)
         self.eng.dd = dd
