@@ -330,10 +330,6 @@ class HostIteration:
             if self.next_dd is None:
                 self.next_dd, self.next_ready = self._upload()
             dd, ready = self.next_dd, self.next_ready
-            torch.cuda.current_stream().wait_event(ready)
-            for t_ in (dd.row_ptr, dd.terms, dd.val64, dd.xnorm, dd.val32):
-                t_.record_stream(torch.cuda.current_stream())
-            self.next_dd, self.next_ready = self._upload()  # the next step's corpus
         else:
             dd = DeviceDataset(self.hd, dev)  # H2D of the corpus (pinned, async)
         if self.eng is None:
@@ -344,6 +340,16 @@ class HostIteration:
         terms = t(ms.term_ids).to(dev, non_blocking=True) - 1
         vals = t(ms.values).to(dev, non_blocking=True)
         ret = t(np.asarray(ms.retained).view(np.uint8)).to(dev, non_blocking=True)
+        if self.prefetch:
+            # the means go first on the H2D engine; then the next step's corpus
+            # streams in on the copy stream while this step computes
+            torch.cuda.current_stream().wait_event(ready)
+            for t_ in (dd.row_ptr, dd.terms, dd.val64, dd.xnorm, dd.val32):
+                t_.record_stream(torch.cuda.current_stream())
+            go = torch.cuda.Event()
+            go.record()
+            self.copy_stream.wait_event(go)
+            self.next_dd, self.next_ready = self._upload()
         dm = self.eng.build_bivf(DeviceMeans(self.k, ms.dim, ptr, terms, vals, ret))
         lab = self.eng.assign(dm, None)
         st = self.eng.read_stats()
