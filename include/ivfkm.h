@@ -63,21 +63,30 @@ int ivfkm_version(void);
 int ivfkm_device_count(void);
 
 /* ---- bitmap-block inverted file (BIVF) of the means ---------------------
- * headers is planar uint32 (ivfkm_bivf_headers_size() words):
- *   masks[t*nblk + b]    bit j set <=> mean 32*b+j holds term t
+ * Means occupy *slots*: slot = perm[mean], means ordered by term count
+ * (descending), so mid-frequency postings crowd into whole spans; results
+ * are mapped back before any tie is broken.  headers is planar uint32
+ * (ivfkm_bivf_headers_size() words):
+ *   masks[t*nblk + b]    bit j set <=> slot 32*b+j holds term t
  *   offs[t*nblk + b]     at headers[dim*nblk + t*nblk + b]: start of the block's
- *                        values; bit 31 set = the block's 256-mean span is dense
+ *                        values; bit 31 set = the block's 256-slot span is dense
  *   total                at headers[2*dim*nblk]: padded value count in use
  *   nc[t]                at headers[2*dim*nblk + 1 + t]: postings of term t
+ *   perm[k], inv[k]      (int32) after nc: mean -> slot, slot -> mean
  * Values (val32 for the fp32 screen, val64 for the exact fp64 rescoring) are
- * term-major, mean ascending — the order of MeanSet.inverted
- * (means.py:169-179) — except that each 256-mean span is padded to a multiple
- * of 4 values and a fully populated span is stored lane-major (mean
- * 32*(b0+r)+j at span_base + 8*j + r).  The value arrays need
+ * term-major, slot ascending — the order of MeanSet.inverted
+ * (means.py:169-179) — except that each 256-slot span is padded to a multiple
+ * of 4 values and a span holding >= dense_fill*256 postings is stored dense
+ * and lane-major (slot 32*(b0+r)+j at span_base + 128*(r/4) + 4*j + r%4,
+ * exact zeros for absent slots).  The value arrays need
  * ivfkm_bivf_values_capacity() elements.                                     */
 int64_t ivfkm_bivf_nblk(int64_t k); /* 32-mean blocks per term, padded */
 int64_t ivfkm_bivf_headers_size(int64_t k, int64_t dim);
 int64_t ivfkm_bivf_values_capacity(int64_t k, int64_t dim, int64_t nnz);
+/* Build options: dense_fill in [0.25, 1] (> 1: never dense; default 0.5),
+ * permute = 1 orders slots by mean term count (default), 0 keeps mean ids.
+ * Out-of-range values leave the setting unchanged.                          */
+void ivfkm_set_bivf_options(float dense_fill, int permute);
 size_t ivfkm_bivf_workspace_size(int64_t dim, int64_t k);
 /* major = 0: rows of (ptr, cols) are means (mean-major CSR, cols = terms);
  * major = 1: rows are terms (term-major IVF, cols = mean ids).  0-based ids;

@@ -48,6 +48,7 @@ SIGNATURES = {
     "ivfkm_bivf_nblk": (_i64, [_i64]),
     "ivfkm_bivf_headers_size": (_i64, [_i64, _i64]),
     "ivfkm_bivf_values_capacity": (_i64, [_i64, _i64, _i64]),
+    "ivfkm_set_bivf_options": (None, [C.c_float, C.c_int]),
     "ivfkm_bivf_workspace_size": (_sz, [_i64, _i64]),
     "ivfkm_bivf_build": (C.c_int, [_i64, _i64, C.c_int, _i64, _vp, _vp, _vp, _vp, _vp, _vp,
                                    _vp, _sz, _vp]),

@@ -62,6 +62,7 @@ struct ScreenParams {
   const uint32_t* masks;  // [dim][nblk]
   const uint32_t* offs;   // [dim][nblk] (+1: total)
   const uint32_t* nc;     // [dim] postings per term
+  const int32_t* inv;     // [k] slot -> mean
   const float* pv32;
   double mu_max;
   int cta_blocks;  // 32-mean blocks held by one CTA (multiple of RR)
@@ -264,7 +265,8 @@ __device__ __forceinline__ void screen_epilogue(const ScreenParams& p, ScreenSha
       total = sh.cnt;
     }
     // gpost == 0: no posting touched, every rho is exactly 0 -> label 0.
-    const int label = gpost == 0 ? 0 : gc;
+    // (slots map back to mean ids here; exact ties are always in the window)
+    const int label = gpost == 0 ? 0 : __ldg(p.inv + gc);
     p.label32[obj] = label;
     if (total <= 1) {
       p.slot_of[obj] = -1;
@@ -279,7 +281,8 @@ __device__ __forceinline__ void screen_epilogue(const ScreenParams& p, ScreenSha
       for (int q = 0; q < p.nsplit && w < kMaxC; ++q) {
         const ScreenShared* o = p.nsplit > 1 ? cluster.map_shared_rank(&sh, q) : &sh;
         const int cq = min(o->cnt, kMaxC);
-        for (int j = 0; j < cq && w < kMaxC; ++j) p.q_cid[(int64_t)slot * kMaxC + w++] = o->cand[j];
+        for (int j = 0; j < cq && w < kMaxC; ++j)
+          p.q_cid[(int64_t)slot * kMaxC + w++] = __ldg(p.inv + o->cand[j]);
       }
     }
   }
@@ -1172,6 +1175,7 @@ int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
   sp.masks = a.headers;
   sp.offs = a.headers + a.dim * sp.nblk;
   sp.nc = a.headers + 2 * a.dim * sp.nblk + 1;
+  sp.inv = reinterpret_cast<const int32_t*>(sp.nc + a.dim) + a.k;
   sp.pv32 = a.pval32;
   sp.mu_max = a.mu_max > 0 ? a.mu_max : 1.0;
   sp.cta_blocks = pl.cta_blocks;
@@ -1198,8 +1202,11 @@ int finish_impl(const AssignArgs& a, const AssignWs& w, const int32_t* prev_labe
   fp.x.row_ptr = a.row_ptr;
   fp.x.terms = a.terms;
   fp.x.val64 = a.val64;
-  fp.x.bv = BivfView{ivfkm_bivf_nblk(a.k), a.headers,
-                     a.headers + a.dim * ivfkm_bivf_nblk(a.k), nullptr};
+  {
+    const int64_t nb = ivfkm_bivf_nblk(a.k);
+    fp.x.bv = BivfView{nb, a.headers, a.headers + a.dim * nb,
+                       reinterpret_cast<const int32_t*>(a.headers + 2 * a.dim * nb + 1 + a.dim)};
+  }
   fp.x.pv64 = a.pval64;
   fp.label32 = w.label32;
   fp.slot_of = w.slot_of;
@@ -1286,7 +1293,11 @@ extern "C" int ivfkm_score_labels(int64_t n_obj, const int64_t* row_ptr, const i
   x.row_ptr = row_ptr;
   x.terms = terms;
   x.val64 = val64;
-  x.bv = BivfView{ivfkm_bivf_nblk(k), headers, headers + dim * ivfkm_bivf_nblk(k), nullptr};
+  {
+    const int64_t nb = ivfkm_bivf_nblk(k);
+    x.bv = BivfView{nb, headers, headers + dim * nb,
+                    reinterpret_cast<const int32_t*>(headers + 2 * dim * nb + 1 + dim)};
+  }
   x.pv64 = pval64;
   score_labels_kernel<<<grid_for(n_obj, 8), 256, 0, st>>>(n_obj, x, labels, sims);
   IVFKM_CHECK_LAUNCH();

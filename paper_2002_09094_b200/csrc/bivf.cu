@@ -32,9 +32,23 @@ struct BivfWs {
   unsigned int* err;
   unsigned int* cnt;
   unsigned int* off;
+  unsigned int* key_a;  // k: descending-size keys
+  unsigned int* key_b;
+  int32_t* id_a;        // k: mean ids
+  int32_t* id_b;
   void* cub;
   size_t cub_bytes;
 };
+
+// build options (ivfkm_set_bivf_options)
+float g_dense_fill = 0.5f;  // spans with >= fill*256 postings are stored dense
+int g_permute = 1;          // slots ordered by mean size
+
+uint32_t dense_threshold() {
+  if (g_dense_fill > 1.0f) return 1u << 30;  // never
+  uint32_t th = (uint32_t)(g_dense_fill * 256.0f + 0.999f);
+  return th < 1 ? 1 : th;
+}
 
 size_t cub_scan_bytes(int64_t n) {
   size_t b = 0;
@@ -50,7 +64,15 @@ BivfWs carve(void* base, int64_t dim, int64_t k, size_t* total) {
   w.err = c.take<unsigned int>(4);
   w.cnt = c.take<unsigned int>(nh + 1);
   w.off = c.take<unsigned int>(nh + 1);
-  w.cub_bytes = cub_scan_bytes(nh + 1);
+  w.key_a = c.take<unsigned int>(k);
+  w.key_b = c.take<unsigned int>(k);
+  w.id_a = c.take<int32_t>(k);
+  w.id_b = c.take<int32_t>(k);
+  size_t sb = 0;
+  cub::DoubleBuffer<unsigned int> kb(nullptr, nullptr);
+  cub::DoubleBuffer<int32_t> vb(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, sb, kb, vb, (int)k);
+  w.cub_bytes = std::max(cub_scan_bytes(nh + 1), sb);
   w.cub = c.take_bytes(w.cub_bytes);
   if (total) *total = c.off;
   return w;
@@ -71,8 +93,8 @@ __device__ __forceinline__ int64_t row_of(const int64_t* __restrict__ ptr, int64
 // ~20k terms each) still spread over the whole GPU.
 __global__ void bivf_mask_kernel(int major, int64_t nrows, const int64_t* __restrict__ ptr,
                                  const int32_t* __restrict__ cols, int64_t k, int64_t dim,
-                                 int64_t nblk, unsigned int* __restrict__ hdr,
-                                 unsigned int* __restrict__ err) {
+                                 int64_t nblk, const int32_t* __restrict__ perm,
+                                 unsigned int* __restrict__ hdr, unsigned int* __restrict__ err) {
   const int64_t nnz = ptr[nrows];
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz;
        q += (int64_t)gridDim.x * blockDim.x) {
@@ -84,14 +106,15 @@ __global__ void bivf_mask_kernel(int major, int64_t nrows, const int64_t* __rest
       atomicAdd(err, 1u);
       continue;
     }
-    atomicOr(&hdr[t * nblk + (c >> 5)], 1u << (c & 31));
+    const int64_t sl = perm[c];
+    atomicOr(&hdr[t * nblk + (sl >> 5)], 1u << (sl & 31));
   }
 }
 
 // One thread per (term, span): popcounts of its 8 blocks, the span total
 // padded to a multiple of 4 values on the last block.
 __global__ void bivf_count_kernel(int64_t nh, const unsigned int* __restrict__ masks,
-                                  unsigned int* __restrict__ cnt) {
+                                  unsigned int dense_th, unsigned int* __restrict__ cnt) {
   const int64_t nspan = nh / kSpan;
   for (int64_t sp = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sp <= nspan;
        sp += (int64_t)gridDim.x * blockDim.x) {
@@ -99,19 +122,21 @@ __global__ void bivf_count_kernel(int64_t nh, const unsigned int* __restrict__ m
       cnt[nh] = 0u;
       continue;
     }
-    unsigned tot = 0;
+    unsigned c[kSpan], tot = 0;
 #pragma unroll
     for (int r = 0; r < kSpan; ++r) {
-      const unsigned c = __popc(masks[sp * kSpan + r]);
-      cnt[sp * kSpan + r] = c;
-      tot += c;
+      c[r] = __popc(masks[sp * kSpan + r]);
+      tot += c[r];
     }
-    cnt[sp * kSpan + kSpan - 1] += (4u - (tot & 3u)) & 3u;
+    const bool dense = tot >= dense_th;
+#pragma unroll
+    for (int r = 0; r < kSpan; ++r) cnt[sp * kSpan + r] = dense ? 32u : c[r];
+    if (!dense) cnt[sp * kSpan + kSpan - 1] += (4u - (tot & 3u)) & 3u;
   }
 }
 
 __global__ void bivf_offset_kernel(int64_t nh, const unsigned int* __restrict__ off,
-                                   unsigned int* __restrict__ hdr) {
+                                   unsigned int dense_th, unsigned int* __restrict__ hdr) {
   const int64_t nspan = nh / kSpan;
   for (int64_t sp = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sp <= nspan;
        sp += (int64_t)gridDim.x * blockDim.x) {
@@ -119,12 +144,14 @@ __global__ void bivf_offset_kernel(int64_t nh, const unsigned int* __restrict__ 
       hdr[nh + nh] = off[nh];
       continue;
     }
-    bool dense = true;
+    unsigned tot = 0;
 #pragma unroll
-    for (int r = 0; r < kSpan; ++r) dense &= hdr[sp * kSpan + r] == 0xffffffffu;
+    for (int r = 0; r < kSpan; ++r) tot += __popc(hdr[sp * kSpan + r]);
+    const bool dense = tot >= dense_th;
 #pragma unroll
     for (int r = 0; r < kSpan; ++r)
       hdr[nh + sp * kSpan + r] = off[sp * kSpan + r] | (dense ? kDense : 0u);
+
   }
 }
 
@@ -132,10 +159,11 @@ __global__ void bivf_scatter_kernel(int major, int64_t nrows, const int64_t* __r
                                     const int32_t* __restrict__ cols,
                                     const double* __restrict__ vals, int64_t k, int64_t dim,
                                     int64_t nblk, const unsigned int* __restrict__ hdr,
+                                    const int32_t* __restrict__ perm,
                                     float* __restrict__ v32, double* __restrict__ v64) {
   const int64_t nnz = ptr[nrows];
   const int64_t nh = bivf_nh(dim, nblk);
-  BivfView view{nblk, hdr, hdr + nh, nullptr};
+  BivfView view{nblk, hdr, hdr + nh, perm};
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz;
        q += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = row_of(ptr, nrows, q);
@@ -147,6 +175,56 @@ __global__ void bivf_scatter_kernel(int major, int64_t nrows, const int64_t* __r
     const double v = vals[q];
     v32[pos] = static_cast<float>(v);
     v64[pos] = v;
+  }
+}
+
+// absent slots of dense spans (and padding) hold exact zeros: clear [0, total)
+__global__ void bivf_zero_kernel(const unsigned int* __restrict__ total, float* __restrict__ v32,
+                                 double* __restrict__ v64) {
+  const int64_t n = *total;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    v32[i] = 0.f;
+    v64[i] = 0.0;
+  }
+}
+
+// descending-size sort keys: ~terms_of_mean (stable sort => ties by mean id)
+__global__ void bivf_sizes_kernel(int major, int64_t nrows, const int64_t* __restrict__ ptr,
+                                  const int32_t* __restrict__ cols, int64_t k,
+                                  unsigned int* __restrict__ key, int32_t* __restrict__ id) {
+  if (major == 0) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < k;
+         c += (int64_t)gridDim.x * blockDim.x) {
+      key[c] = ~(unsigned)(ptr[c + 1] - ptr[c]);
+      id[c] = (int32_t)c;
+    }
+    return;
+  }
+  // term-major input: count each mean's postings (keys were set to ~0u)
+  const int64_t nnz = ptr[nrows];
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = cols[q];
+    if (c >= 0 && c < k) atomicSub(&key[c], 1u);
+  }
+}
+
+__global__ void bivf_ids_kernel(int64_t k, int32_t* __restrict__ id) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < k;
+       c += (int64_t)gridDim.x * blockDim.x)
+    id[c] = (int32_t)c;
+}
+
+// inv[slot] = sorted id; perm[id] = slot
+__global__ void bivf_perm_kernel(int64_t k, const int32_t* __restrict__ sorted,
+                                 int32_t* __restrict__ perm, int32_t* __restrict__ inv,
+                                 int identity) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < k;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = identity ? (int32_t)s : sorted[s];
+    inv[s] = c;
+    perm[c] = (int32_t)s;
   }
 }
 
@@ -172,12 +250,18 @@ extern "C" size_t ivfkm_bivf_workspace_size(int64_t dim, int64_t k) {
   return total;
 }
 
+extern "C" void ivfkm_set_bivf_options(float dense_fill, int permute) {
+  if ((dense_fill >= 0.25f && dense_fill <= 1.0f) || dense_fill > 1.0f) g_dense_fill = dense_fill;
+  if (permute == 0 || permute == 1) g_permute = permute;
+}
+
 extern "C" int64_t ivfkm_bivf_headers_size(int64_t k, int64_t dim) {
-  return 2 * bivf_nh(dim, ivfkm_bivf_nblk(k)) + 1 + dim;
+  return 2 * bivf_nh(dim, ivfkm_bivf_nblk(k)) + 1 + dim + 2 * k;
 }
 
 extern "C" int64_t ivfkm_bivf_values_capacity(int64_t k, int64_t dim, int64_t nnz) {
-  return nnz + 3 * dim * (ivfkm_bivf_nblk(k) / kSpan) + 4;
+  const double f = g_dense_fill > 1.0f ? 1.0 : (double)g_dense_fill;
+  return (int64_t)((double)nnz / f) + 3 * dim * (ivfkm_bivf_nblk(k) / kSpan) + 256 + 4;
 }
 
 extern "C" int ivfkm_bivf_build(int64_t k, int64_t dim, int major, int64_t nrows,
@@ -186,6 +270,7 @@ extern "C" int ivfkm_bivf_build(int64_t k, int64_t dim, int major, int64_t nrows
                                 size_t ws_bytes, ivfkm_stream_t stream_) {
   if (k < 1 || dim < 1 || nrows < 0 || (major != 0 && major != 1) || !ptr || !headers)
     return IVFKM_E_ARG;
+  if (k > INT32_MAX) return IVFKM_E_UNSUPPORTED;
   const int64_t nblk = ivfkm_bivf_nblk(k);
   const int64_t nh = bivf_nh(dim, nblk);
   if (nh + 1 > INT32_MAX) return IVFKM_E_UNSUPPORTED;  // cub scan length, 32-bit rows
@@ -193,23 +278,49 @@ extern "C" int ivfkm_bivf_build(int64_t k, int64_t dim, int major, int64_t nrows
   BivfWs w = carve(ws, dim, k, &need);
   if (ws_bytes < need) return IVFKM_E_WORKSPACE;
   cudaStream_t st = as_stream(stream_);
+  uint32_t* nc = headers + 2 * nh + 1;
+  int32_t* perm = reinterpret_cast<int32_t*>(nc + dim);
+  int32_t* inv = perm + k;
+  const unsigned th = dense_threshold();
+  const int threads = 256;
+  // ---- slot order: means by term count, descending (stable)
+  if (g_permute) {
+    if (major == 1) {
+      IVFKM_TRY(cudaMemsetAsync(w.key_a, 0xff, sizeof(unsigned) * k, st));
+      bivf_ids_kernel<<<grid_for(k, threads), threads, 0, st>>>(k, w.id_a);
+      IVFKM_CHECK_LAUNCH();
+    }
+    bivf_sizes_kernel<<<major == 0 ? grid_for(k, threads) : kNumSM * 8, threads, 0, st>>>(
+        major, nrows, ptr, cols, k, w.key_a, w.id_a);
+    IVFKM_CHECK_LAUNCH();
+    cub::DoubleBuffer<unsigned int> kb(w.key_a, w.key_b);
+    cub::DoubleBuffer<int32_t> vb(w.id_a, w.id_b);
+    size_t cb = w.cub_bytes;
+    IVFKM_TRY(cub::DeviceRadixSort::SortPairs(w.cub, cb, kb, vb, (int)k, 0, 32, st));
+    bivf_perm_kernel<<<grid_for(k, threads), threads, 0, st>>>(k, vb.Current(), perm, inv, 0);
+  } else {
+    bivf_perm_kernel<<<grid_for(k, threads), threads, 0, st>>>(k, nullptr, perm, inv, 1);
+  }
+  IVFKM_CHECK_LAUNCH();
   IVFKM_TRY(cudaMemsetAsync(headers, 0, sizeof(uint32_t) * nh, st));
   IVFKM_TRY(cudaMemsetAsync(w.err, 0, sizeof(unsigned int), st));
-  const int threads = 256;
-  bivf_mask_kernel<<<kNumSM * 8, threads, 0, st>>>(major, nrows, ptr, cols, k, dim, nblk,
+  bivf_mask_kernel<<<kNumSM * 8, threads, 0, st>>>(major, nrows, ptr, cols, k, dim, nblk, perm,
                                                    headers, w.err);
   IVFKM_CHECK_LAUNCH();
-  bivf_count_kernel<<<grid_for(nh / kSpan + 1, threads), threads, 0, st>>>(nh, headers, w.cnt);
+  bivf_count_kernel<<<grid_for(nh / kSpan + 1, threads), threads, 0, st>>>(nh, headers, th,
+                                                                          w.cnt);
   IVFKM_CHECK_LAUNCH();
   size_t cb = w.cub_bytes;
   IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.cnt, w.off, (int)(nh + 1), st));
-  bivf_offset_kernel<<<grid_for(nh / kSpan + 1, threads), threads, 0, st>>>(nh, w.off, headers);
+  bivf_offset_kernel<<<grid_for(nh / kSpan + 1, threads), threads, 0, st>>>(nh, w.off, th,
+                                                                           headers);
+  IVFKM_CHECK_LAUNCH();
+  bivf_zero_kernel<<<kNumSM * 16, threads, 0, st>>>(w.off + nh, val32, val64);
   IVFKM_CHECK_LAUNCH();
   bivf_scatter_kernel<<<kNumSM * 8, threads, 0, st>>>(major, nrows, ptr, cols, vals, k, dim,
-                                                      nblk, headers, val32, val64);
+                                                      nblk, headers, perm, val32, val64);
   IVFKM_CHECK_LAUNCH();
-  bivf_nc_kernel<<<grid_for(dim, threads / 32), threads, 0, st>>>(dim, nblk, headers,
-                                                                  headers + 2 * nh + 1);
+  bivf_nc_kernel<<<grid_for(dim, threads / 32), threads, 0, st>>>(dim, nblk, headers, nc);
   IVFKM_CHECK_LAUNCH();
   return IVFKM_OK;
 }

@@ -1,19 +1,29 @@
 // Bitmap-block inverted file (BIVF): layout constants and the O(1) lookup
 // shared by the build, the fp32 screen and the exact fp64 rescoring.
 //
+// Mean ids inside the BIVF are *slots*: slot = perm[mean], means sorted by
+// their number of terms (descending) so that the postings of mid-frequency
+// terms crowd into the low slots and fill whole spans.  Results are mapped
+// back (inv[slot] = mean) before any tie is broken, so the order is invisible
+// outside (ties are always rescored exactly, see assign.cu).
+//
 // headers (uint32), planar:
-//   masks[t*nblk + b]        bit j <=> mean 32*b+j holds term t
+//   masks[t*nblk + b]        bit j <=> slot 32*b+j holds term t
 //   offs [t*nblk + b]        start of block b's values (+ kDense flag)
 //   offs [dim*nblk]          padded total (size of the value arrays in use)
 //   nc   [t]                 postings of term t (= centroid_freq, means.py:144-147)
-// Blocks are grouped in spans of 8 (256 means).  Every span's value segment
+//   perm [k], inv [k]        mean -> slot, slot -> mean
+// Blocks are grouped in spans of 8 (256 slots).  Every span's value segment
 // is padded to a multiple of 4 values (16 B), so a span start is 16-B aligned.
-// A span whose 8 masks are all full is *dense*: its 256 values are stored
-// lane-major in two halves (mean 32*(b0+r)+j at span_base + 128*(r/4) + 4*j +
-// r%4), so a warp lane owning means 32*(b0+r)+lane reads its 8 values with two
-// 16-B loads that are coalesced in global memory and conflict-free in shared
-// memory; every block of a dense span carries kDense in its offset.  Other spans keep the reference
-// order (term-major, mean ascending, means.py:169-179).
+// A span holding at least dense_fill*256 postings is stored *dense*: all 256
+// values (0.0 for absent slots) lane-major in two halves (slot 32*(b0+r)+j at
+// span_base + 128*(r/4) + 4*j + r%4), so a warp lane owning slots
+// 32*(b0+r)+lane reads its 8 values with two 16-B loads, coalesced in global
+// memory and conflict-free in shared memory; every block of a dense span
+// carries kDense in its offset.  The zeros are exact no-ops for both the fp32
+// FMAs and the fp64 rescoring (which still consults the true masks).  Other
+// spans keep the reference order (term-major, mean ascending,
+// means.py:169-179, in slot order).
 #pragma once
 #include <cstdint>
 
@@ -26,24 +36,29 @@ struct BivfView {
   int64_t nblk;
   const uint32_t* masks;
   const uint32_t* offs;
-  const uint32_t* nc;
+  const int32_t* perm;  // mean -> slot (nullptr: identity)
 };
 
 __host__ __device__ inline int64_t bivf_nh(int64_t dim, int64_t nblk) { return dim * nblk; }
 
-// Position of mean c's value for term t, or -1 when the mean lacks the term.
-__device__ __forceinline__ int64_t bivf_find(const BivfView& v, int64_t t, int64_t c) {
-  const int64_t b = c >> 5;
-  const uint32_t bit = 1u << (c & 31);
+// Position of slot s's value for term t, or -1 when the slot lacks the term.
+__device__ __forceinline__ int64_t bivf_find_slot(const BivfView& v, int64_t t, int64_t s) {
+  const int64_t b = s >> 5;
+  const uint32_t bit = 1u << (s & 31);
   const uint32_t m = __ldg(v.masks + t * v.nblk + b);
   if (!(m & bit)) return -1;
   const uint32_t o = __ldg(v.offs + t * v.nblk + b);
   if (o & kDense) {
     const uint32_t r = (uint32_t)(b & (kSpan - 1));
-    return (int64_t)((o & ~kDense) - 32u * r + 128u * (r >> 2) + 4u * (uint32_t)(c & 31) +
+    return (int64_t)((o & ~kDense) - 32u * r + 128u * (r >> 2) + 4u * (uint32_t)(s & 31) +
                      (r & 3u));
   }
   return (int64_t)(o + (uint32_t)__popc(m & (bit - 1u)));
+}
+
+// Position of mean c's value for term t, or -1.
+__device__ __forceinline__ int64_t bivf_find(const BivfView& v, int64_t t, int64_t c) {
+  return bivf_find_slot(v, t, v.perm ? (int64_t)__ldg(v.perm + c) : c);
 }
 
 }  // namespace ivfkm
