@@ -41,7 +41,7 @@ struct BivfWs {
 };
 
 // build options (ivfkm_set_bivf_options)
-float g_dense_fill = 0.5f;  // spans with >= fill*256 postings are stored dense
+float g_dense_fill = 0.25f;  // spans with >= fill*256 postings are stored dense
 int g_permute = 1;          // slots ordered by mean size
 
 uint32_t dense_threshold() {

@@ -30,6 +30,8 @@ def main():
     ap.add_argument("--rr", default="0,8", help="0 = TMA screen, 2/4/8 = LDG screen, "
                     "-16*w = TMA screen with w warps per CTA")
     ap.add_argument("--rowcap", default="256,512,1024")
+    ap.add_argument("--fill", default="0.5", help="BIVF dense_fill values (>1: never dense)")
+    ap.add_argument("--permute", default="1")
     args = ap.parse_args()
     c = synth.CONFIGS[args.config]
     ds = synth.make_dataset(c["corpus"])
@@ -44,8 +46,14 @@ def main():
     base = eng.assign(dm, None).clone()
     st = eng.read_stats()
     out = []
-    for rr in map(int, args.rr.split(",")):
-        for rowcap in map(int, args.rowcap.split(",")):
+    import itertools
+    for fill, perm, rr, rowcap in itertools.product(map(float, args.fill.split(",")),
+                                                    map(int, args.permute.split(",")),
+                                                    map(int, args.rr.split(",")),
+                                                    map(int, args.rowcap.split(","))):
+        if True:
+            eng.lib.ivfkm_set_bivf_options(fill, perm)
+            eng.build_bivf(dm)
             eng.rowcap = rowcap
             eng.lib.ivfkm_set_tuning(rowcap, 0, rr)
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -56,12 +64,13 @@ def main():
                 times.append(ev[0].elapsed_time(ev[1]))
             ok = bool(torch.equal(lab, base))
             ms = min(times)
-            rec = {"rr": rr, "rowcap": rowcap, "screen_ms": ms,
+            rec = {"fill": fill, "permute": perm, "rr": rr, "rowcap": rowcap, "screen_ms": ms,
                    "postings_per_s": st.postings / (ms / 1e3), "labels_ok": ok}
             out.append(rec)
             print(json.dumps(rec), flush=True)
     eng.lib.ivfkm_set_tuning(1024, 0, 0)
     eng.lib.ivfkm_set_tuning(1024, 0, -128)
+    eng.lib.ivfkm_set_bivf_options(0.25, 1)
 
 
 if __name__ == "__main__":
