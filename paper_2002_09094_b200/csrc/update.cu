@@ -29,8 +29,8 @@ template <class K>
 struct UpdWs {
   K* key_a;
   K* key_b;
-  uint32_t* idx_a;
-  uint32_t* idx_b;
+  double* val_a;  // float64 values travel with their keys through the sort
+  double* val_b;
   uint32_t* head;     // run-head flags, later nonzero flags
   uint32_t* segpos;   // scan of head
   uint32_t* nzpos;    // scan of nonzero flags
@@ -49,7 +49,7 @@ template <class K>
 size_t cub_bytes_for(int64_t nnz, int64_t k) {
   size_t a = 0, b = 0, c = 0;
   cub::DoubleBuffer<K> kb(nullptr, nullptr);
-  cub::DoubleBuffer<uint32_t> vb(nullptr, nullptr);
+  cub::DoubleBuffer<double> vb(nullptr, nullptr);
   cub::DeviceRadixSort::SortPairs(nullptr, a, kb, vb, (int)nnz, 0, (int)(sizeof(K) * 8));
   cub::DeviceScan::ExclusiveSum(nullptr, b, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)nnz);
   cub::DeviceScan::ExclusiveSum(nullptr, c, (int64_t*)nullptr, (int64_t*)nullptr, (int)(k + 1));
@@ -63,8 +63,8 @@ UpdWs<K> carve_upd(void* base, int64_t nnz, int64_t k, size_t* total) {
   const size_t n = (size_t)(nnz > 0 ? nnz : 1);
   w.key_a = c.take<K>(n);
   w.key_b = c.take<K>(n);
-  w.idx_a = c.take<uint32_t>(n);
-  w.idx_b = c.take<uint32_t>(n);
+  w.val_a = c.take<double>(n);
+  w.val_b = c.take<double>(n);
   w.head = c.take<uint32_t>(n);
   w.segpos = c.take<uint32_t>(n);
   w.nzpos = c.take<uint32_t>(n);
@@ -92,15 +92,16 @@ int key_bits(int64_t k, int64_t dim) {
 
 template <class K>
 __global__ void keys_kernel(int64_t n_obj, const int64_t* __restrict__ row_ptr,
-                            const int32_t* __restrict__ terms, const int32_t* __restrict__ labels,
-                            int64_t dim, K* __restrict__ key, uint32_t* __restrict__ idx) {
+                            const int32_t* __restrict__ terms, const double* __restrict__ val64,
+                            const int32_t* __restrict__ labels, int64_t dim,
+                            K* __restrict__ key, double* __restrict__ val) {
   const int lane = threadIdx.x & 31;
   const int64_t wpb = blockDim.x >> 5;
   for (int64_t i = blockIdx.x * wpb + (threadIdx.x >> 5); i < n_obj; i += gridDim.x * wpb) {
     const K base = (K)labels[i] * (K)dim;
     for (int64_t e = row_ptr[i] + lane; e < row_ptr[i + 1]; e += 32) {
       key[e] = base + (K)terms[e];
-      idx[e] = (uint32_t)e;
+      val[e] = val64[e];
     }
   }
 }
@@ -138,8 +139,7 @@ __global__ void segstart_kernel(int64_t nnz, const K* __restrict__ key,
 template <class K>
 __global__ void segsum_kernel(int64_t nnz, const uint32_t* __restrict__ n_seg_p,
                               const uint32_t* __restrict__ seg_start,
-                              const K* __restrict__ seg_key, const uint32_t* __restrict__ idx,
-                              const double* __restrict__ val64,
+                              const K* __restrict__ seg_key, const double* __restrict__ sval,
                               const unsigned long long* __restrict__ sizes, int64_t dim,
                               double* __restrict__ seg_w, uint32_t* __restrict__ nz) {
   const uint32_t n_seg = *n_seg_p;
@@ -150,7 +150,7 @@ __global__ void segsum_kernel(int64_t nnz, const uint32_t* __restrict__ n_seg_p,
       continue;
     }
     double acc = 0.0;
-    for (uint32_t e = seg_start[s]; e < seg_start[s + 1]; ++e) acc = __dadd_rn(acc, val64[idx[e]]);
+    for (uint32_t e = seg_start[s]; e < seg_start[s + 1]; ++e) acc = __dadd_rn(acc, sval[e]);
     const int64_t c = (int64_t)(seg_key[s] / (K)dim);
     const double w = __ddiv_rn(acc, (double)sizes[c]);
     seg_w[s] = w;
@@ -243,43 +243,82 @@ __device__ double leaf_value(int64_t lo, int64_t n, uint32_t cur, uint32_t end, 
   return res;
 }
 
-// Combine leaf values in the recursion's order: pw(lo,n) = leaf or
-// pw(left) + pw(right).  Leaves are consumed left to right.
-__device__ double combine_leaves(int64_t D, const double* leaf_val) {
-  struct Frame {
-    int64_t n;
-    double left;
+// The recursion's combine tree, built once per CTA in shared memory: leaves
+// are nodes 0..L-1 (left to right), internal nodes L..2L-2 in post-order with
+// their children; internal nodes are then listed by height so a cluster's
+// tree is evaluated level by level (node = left + right, exactly the
+// recursion's association), all threads in parallel.
+struct NormPlan {
+  int32_t* leaf_lo;  // L+1
+  int32_t* left;     // L-1 (indexed by internal id - L)
+  int32_t* right;    // L-1
+  int32_t* order;    // L-1 internal ids by height
+  int32_t* lvl;      // level starts into order, H+1 entries (H <= 63)
+  double* val;       // 2L-1
+  int nlevels;
+};
+
+__host__ __device__ inline size_t norm_plan_bytes(int64_t L) {
+  return (size_t)(2 * L - 1) * 8 + (size_t)(L + 1) * 4 + (size_t)(L - 1) * 12 + 64 * 4 + 64;
+}
+
+__device__ void build_norm_plan(int64_t D, int64_t L, NormPlan& pl, unsigned char* hbuf) {
+  // iterative post-order over (lo, n); hbuf[i] = height of internal node L+i
+  struct F {
+    int64_t lo, n;
+    int32_t lch;
     int stage;
   };
-  Frame st[64];
+  F st[64];
   int sp = 0;
-  int64_t next = 0;
-  double ret = 0.0;
-  st[sp++] = Frame{D, 0.0, 0};
+  int32_t next_leaf = 0, next_int = 0, ret = 0;
+  st[sp++] = F{0, D, 0, 0};
   while (sp > 0) {
-    Frame& f = st[sp - 1];
+    F& f = st[sp - 1];
     if (f.stage == 0) {
       if (f.n <= 128) {
-        ret = leaf_val[next++];
+        pl.leaf_lo[next_leaf] = (int32_t)f.lo;
+        ret = next_leaf++;
         --sp;
         continue;
       }
       int64_t n2 = f.n / 2;
       n2 -= n2 % 8;
       f.stage = 1;
-      st[sp++] = Frame{n2, 0.0, 0};
+      st[sp++] = F{f.lo, n2, 0, 0};
     } else if (f.stage == 1) {
-      f.left = ret;
+      f.lch = ret;
       f.stage = 2;
       int64_t n2 = f.n / 2;
       n2 -= n2 % 8;
-      st[sp++] = Frame{f.n - n2, 0.0, 0};
+      st[sp++] = F{f.lo + n2, f.n - n2, 0, 0};
     } else {
-      ret = __dadd_rn(f.left, ret);
+      const int32_t id = (int32_t)L + next_int;
+      pl.left[next_int] = f.lch;
+      pl.right[next_int] = ret;
+      const int hl = f.lch < L ? 0 : hbuf[f.lch - L];
+      const int hr = ret < L ? 0 : hbuf[ret - L];
+      hbuf[next_int] = (unsigned char)(1 + (hl > hr ? hl : hr));
+      ++next_int;
+      ret = id;
       --sp;
     }
   }
-  return ret;
+  pl.leaf_lo[L] = (int32_t)D;
+  // bucket internal nodes by height
+  int cnt[64];
+  for (int h = 0; h < 64; ++h) cnt[h] = 0;
+  int H = 0;
+  for (int64_t i = 0; i < L - 1; ++i) {
+    ++cnt[hbuf[i]];
+    if (hbuf[i] > H) H = hbuf[i];
+  }
+  pl.lvl[0] = 0;
+  for (int h = 1; h <= H; ++h) pl.lvl[h] = pl.lvl[h - 1] + cnt[h];
+  int fill[64];
+  for (int h = 1; h <= H; ++h) fill[h] = h == 1 ? 0 : pl.lvl[h - 1];
+  for (int64_t i = 0; i < L - 1; ++i) pl.order[fill[hbuf[i]]++] = (int32_t)(L + i);
+  pl.nlevels = H;
 }
 
 template <class K>
@@ -289,12 +328,24 @@ __global__ void __launch_bounds__(256) norm_kernel(
     const K* __restrict__ seg_key, const double* __restrict__ seg_w,
     const uint32_t* __restrict__ nz, double* __restrict__ nrm, int64_t* __restrict__ counts) {
   extern __shared__ __align__(16) unsigned char smem[];
-  double* leaf_val = reinterpret_cast<double*>(smem);
-  int32_t* leaf_lo = reinterpret_cast<int32_t*>(leaf_val + nleaf);
+  const int64_t L = nleaf;
+  NormPlan pl;
+  pl.val = reinterpret_cast<double*>(smem);
+  pl.leaf_lo = reinterpret_cast<int32_t*>(pl.val + (2 * L - 1));
+  pl.left = pl.leaf_lo + (L + 1);
+  pl.right = pl.left + (L - 1);
+  pl.order = pl.right + (L - 1);
+  pl.lvl = pl.order + (L - 1);
+  unsigned char* hbuf = reinterpret_cast<unsigned char*>(pl.val);  // scratch before use
   __shared__ int64_t s_cnt;
-  if (threadIdx.x == 0) enum_leaves(dim, leaf_lo);
+  __shared__ int s_levels;
+  if (threadIdx.x == 0) {
+    build_norm_plan(dim, L, pl, hbuf);
+    s_levels = pl.nlevels;
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) counts[k] = 0;
   __syncthreads();
+  const int H = s_levels;
   for (int64_t c = blockIdx.x; c < k; c += gridDim.x) {
     if (sizes[c] == 0) {  // retained: previous mean, count only
       if (threadIdx.x == 0) {
@@ -311,8 +362,8 @@ __global__ void __launch_bounds__(256) norm_kernel(
     for (uint32_t sidx = b + threadIdx.x; sidx < e; sidx += blockDim.x) cnt += nz[sidx];
     for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
     if ((threadIdx.x & 31) == 0 && cnt) atomicAdd((unsigned long long*)&s_cnt, (unsigned long long)cnt);
-    for (int64_t j = threadIdx.x; j < nleaf; j += blockDim.x) {
-      const int64_t lo = leaf_lo[j], hi = leaf_lo[j + 1];
+    for (int64_t j = threadIdx.x; j < L; j += blockDim.x) {
+      const int64_t lo = pl.leaf_lo[j], hi = pl.leaf_lo[j + 1];
       // first run of this cluster at or after position lo
       uint32_t a = b, z = e;
       const K target = base + (K)lo;
@@ -320,12 +371,19 @@ __global__ void __launch_bounds__(256) norm_kernel(
         const uint32_t mid = (a + z) >> 1;
         if (seg_key[mid] < target) a = mid + 1; else z = mid;
       }
-      leaf_val[j] = leaf_value<K>(lo, hi - lo, a, e, seg_key, seg_w, base);
+      pl.val[j] = leaf_value<K>(lo, hi - lo, a, e, seg_key, seg_w, base);
     }
     __syncthreads();
+    for (int h = 1; h <= H; ++h) {
+      for (int q = pl.lvl[h - 1] + threadIdx.x; q < pl.lvl[h]; q += blockDim.x) {
+        const int32_t id = pl.order[q];
+        pl.val[id] = __dadd_rn(pl.val[pl.left[id - L]], pl.val[pl.right[id - L]]);
+      }
+      __syncthreads();
+    }
     if (threadIdx.x == 0) {
       counts[c] = s_cnt;
-      nrm[c] = __dsqrt_rn(combine_leaves(dim, leaf_val));
+      nrm[c] = __dsqrt_rn(pl.val[2 * L - 2]);
     }
     __syncthreads();
   }
@@ -381,16 +439,16 @@ int update_count_impl(int64_t n_obj, const int64_t* row_ptr, const int32_t* term
   if (ws_bytes < need) return IVFKM_E_WORKSPACE;
   const int T = 256;
   if (nnz > 0) {
-    keys_kernel<K><<<grid_for(n_obj, T / 32), T, 0, st>>>(n_obj, row_ptr, terms, labels, dim,
-                                                          w.key_a, w.idx_a);
+    keys_kernel<K><<<grid_for(n_obj, T / 32), T, 0, st>>>(n_obj, row_ptr, terms, val64, labels,
+                                                          dim, w.key_a, w.val_a);
     IVFKM_CHECK_LAUNCH();
     cub::DoubleBuffer<K> kb(w.key_a, w.key_b);
-    cub::DoubleBuffer<uint32_t> vb(w.idx_a, w.idx_b);
+    cub::DoubleBuffer<double> vb(w.val_a, w.val_b);
     size_t cb = w.cub_bytes;
     IVFKM_TRY(cub::DeviceRadixSort::SortPairs(w.cub, cb, kb, vb, (int)nnz, 0, key_bits(k, dim),
                                               st));
     K* key = kb.Current();
-    uint32_t* idx = vb.Current();
+    double* sval = vb.Current();
     head_kernel<K><<<grid_for(nnz, T), T, 0, st>>>(nnz, key, w.head);
     IVFKM_CHECK_LAUNCH();
     cb = w.cub_bytes;
@@ -398,8 +456,8 @@ int update_count_impl(int64_t n_obj, const int64_t* row_ptr, const int32_t* term
     segstart_kernel<K><<<grid_for(nnz, T), T, 0, st>>>(nnz, key, w.head, w.segpos, w.seg_start,
                                                        w.seg_key, w.n_seg);
     IVFKM_CHECK_LAUNCH();
-    segsum_kernel<K><<<grid_for(nnz, T), T, 0, st>>>(nnz, w.n_seg, w.seg_start, w.seg_key, idx,
-                                                     val64, sizes, dim, w.seg_w, w.head);
+    segsum_kernel<K><<<grid_for(nnz, T), T, 0, st>>>(nnz, w.n_seg, w.seg_start, w.seg_key, sval,
+                                                     sizes, dim, w.seg_w, w.head);
     IVFKM_CHECK_LAUNCH();
     cb = w.cub_bytes;
     IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.head, w.nzpos, (int)nnz, st));
@@ -409,8 +467,8 @@ int update_count_impl(int64_t n_obj, const int64_t* row_ptr, const int32_t* term
   clseg_kernel<K><<<grid_for(k + 1, T), T, 0, st>>>(k, dim, w.n_seg, w.seg_key, w.cl_seg);
   IVFKM_CHECK_LAUNCH();
   const int64_t nleaf = enum_leaves(dim, nullptr);
-  const size_t nsmem = (size_t)nleaf * 8 + (size_t)(nleaf + 1) * 4;
-  if (nsmem > 200 * 1024) return IVFKM_E_UNSUPPORTED;  // D beyond ~2.4M terms
+  const size_t nsmem = norm_plan_bytes(nleaf);
+  if (nsmem > 200 * 1024) return IVFKM_E_UNSUPPORTED;  // D beyond ~1M terms
   IVFKM_TRY(cudaFuncSetAttribute(norm_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)nsmem));
   norm_kernel<K><<<(int)std::min<int64_t>(k, kNumSM * 8), 256, nsmem, st>>>(
