@@ -41,6 +41,8 @@ struct UpdWs {
   double* nrm;        // k
   int64_t* counts;    // k+1
   uint32_t* n_seg;    // 1
+  int32_t* plan;      // pairwise-norm combine plan
+  unsigned char* plan_h;
   void* cub;
   size_t cub_bytes;
 };
@@ -75,6 +77,8 @@ UpdWs<K> carve_upd(void* base, int64_t nnz, int64_t k, size_t* total) {
   w.nrm = c.take<double>(k);
   w.counts = c.take<int64_t>(k + 1);
   w.n_seg = c.take<uint32_t>(4);
+  w.plan = c.take<int32_t>(64 * 1024);      // norm plan (L up to ~16k leaves)
+  w.plan_h = c.take<unsigned char>(64 * 1024);
   w.cub_bytes = cub_bytes_for<K>((int64_t)n, k);
   w.cub = c.take_bytes(w.cub_bytes);
   if (total) *total = c.off;
@@ -259,7 +263,7 @@ struct NormPlan {
 };
 
 __host__ __device__ inline size_t norm_plan_bytes(int64_t L) {
-  return (size_t)(2 * L - 1) * 8 + (size_t)(L + 1) * 4 + (size_t)(L - 1) * 12 + 64 * 4 + 64;
+  return (size_t)(2 * L - 1) * 8 + (size_t)(L + 1) * 4 + (size_t)(L - 1) * 12 + 65 * 4 + 64;
 }
 
 __device__ void build_norm_plan(int64_t D, int64_t L, NormPlan& pl, unsigned char* hbuf) {
@@ -321,9 +325,25 @@ __device__ void build_norm_plan(int64_t D, int64_t L, NormPlan& pl, unsigned cha
   pl.nlevels = H;
 }
 
+// plan words: leaf_lo[L+1], left[L-1], right[L-1], order[L-1], lvl[64], H
+__host__ __device__ inline int64_t norm_plan_words(int64_t L) { return (L + 1) + 3 * (L - 1) + 65; }
+
+__global__ void norm_plan_kernel(int64_t dim, int64_t L, int32_t* __restrict__ g,
+                                 unsigned char* __restrict__ hbuf) {
+  NormPlan pl;
+  pl.leaf_lo = g;
+  pl.left = g + (L + 1);
+  pl.right = pl.left + (L - 1);
+  pl.order = pl.right + (L - 1);
+  pl.lvl = pl.order + (L - 1);
+  build_norm_plan(dim, L, pl, hbuf);
+  pl.lvl[64] = pl.nlevels;
+}
+
 template <class K>
 __global__ void __launch_bounds__(256) norm_kernel(
-    int64_t k, int64_t dim, int64_t nleaf, const unsigned long long* __restrict__ sizes,
+    int64_t k, int64_t dim, int64_t nleaf, const int32_t* __restrict__ gplan,
+    const unsigned long long* __restrict__ sizes,
     const int64_t* __restrict__ prev_ptr, const uint32_t* __restrict__ cl_seg,
     const K* __restrict__ seg_key, const double* __restrict__ seg_w,
     const uint32_t* __restrict__ nz, double* __restrict__ nrm, int64_t* __restrict__ counts) {
@@ -336,16 +356,12 @@ __global__ void __launch_bounds__(256) norm_kernel(
   pl.right = pl.left + (L - 1);
   pl.order = pl.right + (L - 1);
   pl.lvl = pl.order + (L - 1);
-  unsigned char* hbuf = reinterpret_cast<unsigned char*>(pl.val);  // scratch before use
   __shared__ int64_t s_cnt;
-  __shared__ int s_levels;
-  if (threadIdx.x == 0) {
-    build_norm_plan(dim, L, pl, hbuf);
-    s_levels = pl.nlevels;
-  }
+  const int64_t words = norm_plan_words(L);
+  for (int64_t i = threadIdx.x; i < words; i += blockDim.x) pl.leaf_lo[i] = gplan[i];
   if (blockIdx.x == 0 && threadIdx.x == 0) counts[k] = 0;
   __syncthreads();
-  const int H = s_levels;
+  const int H = pl.lvl[64];
   for (int64_t c = blockIdx.x; c < k; c += gridDim.x) {
     if (sizes[c] == 0) {  // retained: previous mean, count only
       if (threadIdx.x == 0) {
@@ -471,8 +487,12 @@ int update_count_impl(int64_t n_obj, const int64_t* row_ptr, const int32_t* term
   if (nsmem > 200 * 1024) return IVFKM_E_UNSUPPORTED;  // D beyond ~1M terms
   IVFKM_TRY(cudaFuncSetAttribute(norm_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)nsmem));
+  if (norm_plan_words(nleaf) > 64 * 1024) return IVFKM_E_UNSUPPORTED;
+  norm_plan_kernel<<<1, 1, 0, st>>>(dim, nleaf, w.plan, w.plan_h);
+  IVFKM_CHECK_LAUNCH();
   norm_kernel<K><<<(int)std::min<int64_t>(k, kNumSM * 8), 256, nsmem, st>>>(
-      k, dim, nleaf, sizes, prev_ptr, w.cl_seg, w.seg_key, w.seg_w, w.head, w.nrm, w.counts);
+      k, dim, nleaf, w.plan, sizes, prev_ptr, w.cl_seg, w.seg_key, w.seg_w, w.head, w.nrm,
+      w.counts);
   IVFKM_CHECK_LAUNCH();
   size_t cb = w.cub_bytes;
   IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.counts, new_ptr, (int)(k + 1), st));

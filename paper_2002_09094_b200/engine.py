@@ -144,9 +144,9 @@ class DeviceMeans:
 def update_launches(k: int, dim: int) -> int:
     """Kernels one update launches: keys, CUB onesweep radix sort (histogram,
     exclusive sum, one pass per 8 key bits), head, 3 CUB scans (init + sweep
-    each), segstart, segsum, clseg, norm, fill, retain."""
+    each), segstart, segsum, clseg, norm plan, norm, fill, retain."""
     bits = max(1, int(np.ceil(np.log2(max(2.0, float(k) * float(dim))))))
-    return 1 + 2 + (bits + 7) // 8 + 1 + 6 + 6
+    return 17 + (bits + 7) // 8
 
 def update_rows(lib, n_obj, nnz, row_ptr, terms, val64, labels0, sizes, prev: DeviceMeans, k,
                 dim, ws, total_host=None) -> DeviceMeans:
@@ -215,7 +215,9 @@ class LloydEngine:
                                        _p(dm.vals), _p(dm.headers), _p(dm.pv32), _p(dm.pv64),
                                        _p(self.ws_bivf), self.ws_bivf.numel(), _stream())
         _lib.check(rc, "ivfkm_bivf_build")
-        self.launches += 7  # mask, count, scan (init + sweep), offset, scatter, nc
+        # sizes, CUB sort of the k slot keys (single tile / onesweep), perm, mask,
+        # count, scan (init + sweep), offset, zero, scatter, nc
+        self.launches += 11 + (1 if self.k <= 4096 else 6)
         return dm
 
     def upload_means(self, ms) -> DeviceMeans:
