@@ -41,8 +41,6 @@ struct UpdWs {
   double* nrm;        // k
   int64_t* counts;    // k+1
   uint32_t* n_seg;    // 1
-  int32_t* plan;      // pairwise-norm combine plan
-  unsigned char* plan_h;
   void* cub;
   size_t cub_bytes;
 };
@@ -77,8 +75,6 @@ UpdWs<K> carve_upd(void* base, int64_t nnz, int64_t k, size_t* total) {
   w.nrm = c.take<double>(k);
   w.counts = c.take<int64_t>(k + 1);
   w.n_seg = c.take<uint32_t>(4);
-  w.plan = c.take<int32_t>(64 * 1024);      // norm plan (L up to ~16k leaves)
-  w.plan_h = c.take<unsigned char>(64 * 1024);
   w.cub_bytes = cub_bytes_for<K>((int64_t)n, k);
   w.cub = c.take_bytes(w.cub_bytes);
   if (total) *total = c.off;
@@ -247,121 +243,58 @@ __device__ double leaf_value(int64_t lo, int64_t n, uint32_t cur, uint32_t end, 
   return res;
 }
 
-// The recursion's combine tree, built once per CTA in shared memory: leaves
-// are nodes 0..L-1 (left to right), internal nodes L..2L-2 in post-order with
-// their children; internal nodes are then listed by height so a cluster's
-// tree is evaluated level by level (node = left + right, exactly the
-// recursion's association), all threads in parallel.
-struct NormPlan {
-  int32_t* leaf_lo;  // L+1
-  int32_t* left;     // L-1 (indexed by internal id - L)
-  int32_t* right;    // L-1
-  int32_t* order;    // L-1 internal ids by height
-  int32_t* lvl;      // level starts into order, H+1 entries (H <= 63)
-  double* val;       // 2L-1
-  int nlevels;
-};
-
-__host__ __device__ inline size_t norm_plan_bytes(int64_t L) {
-  return (size_t)(2 * L - 1) * 8 + (size_t)(L + 1) * 4 + (size_t)(L - 1) * 12 + 65 * 4 + 64;
-}
-
-__device__ void build_norm_plan(int64_t D, int64_t L, NormPlan& pl, unsigned char* hbuf) {
-  // iterative post-order over (lo, n); hbuf[i] = height of internal node L+i
-  struct F {
-    int64_t lo, n;
-    int32_t lch;
+// Combine leaf values in the recursion's order: pw(lo,n) = leaf or
+// pw(left) + pw(right).  Leaves are consumed left to right.
+__device__ double combine_leaves(int64_t D, const double* leaf_val) {
+  struct Frame {
+    int64_t n;
+    double left;
     int stage;
   };
-  F st[64];
+  Frame st[64];
   int sp = 0;
-  int32_t next_leaf = 0, next_int = 0, ret = 0;
-  st[sp++] = F{0, D, 0, 0};
+  int64_t next = 0;
+  double ret = 0.0;
+  st[sp++] = Frame{D, 0.0, 0};
   while (sp > 0) {
-    F& f = st[sp - 1];
+    Frame& f = st[sp - 1];
     if (f.stage == 0) {
       if (f.n <= 128) {
-        pl.leaf_lo[next_leaf] = (int32_t)f.lo;
-        ret = next_leaf++;
+        ret = leaf_val[next++];
         --sp;
         continue;
       }
       int64_t n2 = f.n / 2;
       n2 -= n2 % 8;
       f.stage = 1;
-      st[sp++] = F{f.lo, n2, 0, 0};
+      st[sp++] = Frame{n2, 0.0, 0};
     } else if (f.stage == 1) {
-      f.lch = ret;
+      f.left = ret;
       f.stage = 2;
       int64_t n2 = f.n / 2;
       n2 -= n2 % 8;
-      st[sp++] = F{f.lo + n2, f.n - n2, 0, 0};
+      st[sp++] = Frame{f.n - n2, 0.0, 0};
     } else {
-      const int32_t id = (int32_t)L + next_int;
-      pl.left[next_int] = f.lch;
-      pl.right[next_int] = ret;
-      const int hl = f.lch < L ? 0 : hbuf[f.lch - L];
-      const int hr = ret < L ? 0 : hbuf[ret - L];
-      hbuf[next_int] = (unsigned char)(1 + (hl > hr ? hl : hr));
-      ++next_int;
-      ret = id;
+      ret = __dadd_rn(f.left, ret);
       --sp;
     }
   }
-  pl.leaf_lo[L] = (int32_t)D;
-  // bucket internal nodes by height
-  int cnt[64];
-  for (int h = 0; h < 64; ++h) cnt[h] = 0;
-  int H = 0;
-  for (int64_t i = 0; i < L - 1; ++i) {
-    ++cnt[hbuf[i]];
-    if (hbuf[i] > H) H = hbuf[i];
-  }
-  pl.lvl[0] = 0;
-  for (int h = 1; h <= H; ++h) pl.lvl[h] = pl.lvl[h - 1] + cnt[h];
-  int fill[64];
-  for (int h = 1; h <= H; ++h) fill[h] = h == 1 ? 0 : pl.lvl[h - 1];
-  for (int64_t i = 0; i < L - 1; ++i) pl.order[fill[hbuf[i]]++] = (int32_t)(L + i);
-  pl.nlevels = H;
-}
-
-// plan words: leaf_lo[L+1], left[L-1], right[L-1], order[L-1], lvl[64], H
-__host__ __device__ inline int64_t norm_plan_words(int64_t L) { return (L + 1) + 3 * (L - 1) + 65; }
-
-__global__ void norm_plan_kernel(int64_t dim, int64_t L, int32_t* __restrict__ g,
-                                 unsigned char* __restrict__ hbuf) {
-  NormPlan pl;
-  pl.leaf_lo = g;
-  pl.left = g + (L + 1);
-  pl.right = pl.left + (L - 1);
-  pl.order = pl.right + (L - 1);
-  pl.lvl = pl.order + (L - 1);
-  build_norm_plan(dim, L, pl, hbuf);
-  pl.lvl[64] = pl.nlevels;
+  return ret;
 }
 
 template <class K>
 __global__ void __launch_bounds__(256) norm_kernel(
-    int64_t k, int64_t dim, int64_t nleaf, const int32_t* __restrict__ gplan,
-    const unsigned long long* __restrict__ sizes,
+    int64_t k, int64_t dim, int64_t nleaf, const unsigned long long* __restrict__ sizes,
     const int64_t* __restrict__ prev_ptr, const uint32_t* __restrict__ cl_seg,
     const K* __restrict__ seg_key, const double* __restrict__ seg_w,
     const uint32_t* __restrict__ nz, double* __restrict__ nrm, int64_t* __restrict__ counts) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int64_t L = nleaf;
-  NormPlan pl;
-  pl.val = reinterpret_cast<double*>(smem);
-  pl.leaf_lo = reinterpret_cast<int32_t*>(pl.val + (2 * L - 1));
-  pl.left = pl.leaf_lo + (L + 1);
-  pl.right = pl.left + (L - 1);
-  pl.order = pl.right + (L - 1);
-  pl.lvl = pl.order + (L - 1);
+  double* leaf_val = reinterpret_cast<double*>(smem);
+  int32_t* leaf_lo = reinterpret_cast<int32_t*>(leaf_val + nleaf);
   __shared__ int64_t s_cnt;
-  const int64_t words = norm_plan_words(L);
-  for (int64_t i = threadIdx.x; i < words; i += blockDim.x) pl.leaf_lo[i] = gplan[i];
+  if (threadIdx.x == 0) enum_leaves(dim, leaf_lo);
   if (blockIdx.x == 0 && threadIdx.x == 0) counts[k] = 0;
   __syncthreads();
-  const int H = pl.lvl[64];
   for (int64_t c = blockIdx.x; c < k; c += gridDim.x) {
     if (sizes[c] == 0) {  // retained: previous mean, count only
       if (threadIdx.x == 0) {
@@ -378,8 +311,8 @@ __global__ void __launch_bounds__(256) norm_kernel(
     for (uint32_t sidx = b + threadIdx.x; sidx < e; sidx += blockDim.x) cnt += nz[sidx];
     for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
     if ((threadIdx.x & 31) == 0 && cnt) atomicAdd((unsigned long long*)&s_cnt, (unsigned long long)cnt);
-    for (int64_t j = threadIdx.x; j < L; j += blockDim.x) {
-      const int64_t lo = pl.leaf_lo[j], hi = pl.leaf_lo[j + 1];
+    for (int64_t j = threadIdx.x; j < nleaf; j += blockDim.x) {
+      const int64_t lo = leaf_lo[j], hi = leaf_lo[j + 1];
       // first run of this cluster at or after position lo
       uint32_t a = b, z = e;
       const K target = base + (K)lo;
@@ -387,19 +320,12 @@ __global__ void __launch_bounds__(256) norm_kernel(
         const uint32_t mid = (a + z) >> 1;
         if (seg_key[mid] < target) a = mid + 1; else z = mid;
       }
-      pl.val[j] = leaf_value<K>(lo, hi - lo, a, e, seg_key, seg_w, base);
+      leaf_val[j] = leaf_value<K>(lo, hi - lo, a, e, seg_key, seg_w, base);
     }
     __syncthreads();
-    for (int h = 1; h <= H; ++h) {
-      for (int q = pl.lvl[h - 1] + threadIdx.x; q < pl.lvl[h]; q += blockDim.x) {
-        const int32_t id = pl.order[q];
-        pl.val[id] = __dadd_rn(pl.val[pl.left[id - L]], pl.val[pl.right[id - L]]);
-      }
-      __syncthreads();
-    }
     if (threadIdx.x == 0) {
       counts[c] = s_cnt;
-      nrm[c] = __dsqrt_rn(pl.val[2 * L - 2]);
+      nrm[c] = __dsqrt_rn(combine_leaves(dim, leaf_val));
     }
     __syncthreads();
   }
@@ -483,16 +409,12 @@ int update_count_impl(int64_t n_obj, const int64_t* row_ptr, const int32_t* term
   clseg_kernel<K><<<grid_for(k + 1, T), T, 0, st>>>(k, dim, w.n_seg, w.seg_key, w.cl_seg);
   IVFKM_CHECK_LAUNCH();
   const int64_t nleaf = enum_leaves(dim, nullptr);
-  const size_t nsmem = norm_plan_bytes(nleaf);
-  if (nsmem > 200 * 1024) return IVFKM_E_UNSUPPORTED;  // D beyond ~1M terms
+  const size_t nsmem = (size_t)nleaf * 8 + (size_t)(nleaf + 1) * 4;
+  if (nsmem > 200 * 1024) return IVFKM_E_UNSUPPORTED;  // D beyond ~2.4M terms
   IVFKM_TRY(cudaFuncSetAttribute(norm_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)nsmem));
-  if (norm_plan_words(nleaf) > 64 * 1024) return IVFKM_E_UNSUPPORTED;
-  norm_plan_kernel<<<1, 1, 0, st>>>(dim, nleaf, w.plan, w.plan_h);
-  IVFKM_CHECK_LAUNCH();
   norm_kernel<K><<<(int)std::min<int64_t>(k, kNumSM * 8), 256, nsmem, st>>>(
-      k, dim, nleaf, w.plan, sizes, prev_ptr, w.cl_seg, w.seg_key, w.seg_w, w.head, w.nrm,
-      w.counts);
+      k, dim, nleaf, sizes, prev_ptr, w.cl_seg, w.seg_key, w.seg_w, w.head, w.nrm, w.counts);
   IVFKM_CHECK_LAUNCH();
   size_t cb = w.cub_bytes;
   IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.counts, new_ptr, (int)(k + 1), st));

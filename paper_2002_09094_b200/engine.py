@@ -144,9 +144,9 @@ class DeviceMeans:
 def update_launches(k: int, dim: int) -> int:
     """Kernels one update launches: keys, CUB onesweep radix sort (histogram,
     exclusive sum, one pass per 8 key bits), head, 3 CUB scans (init + sweep
-    each), segstart, segsum, clseg, norm plan, norm, fill, retain."""
+    each), segstart, segsum, clseg, norm, fill, retain."""
     bits = max(1, int(np.ceil(np.log2(max(2.0, float(k) * float(dim))))))
-    return 17 + (bits + 7) // 8
+    return 16 + (bits + 7) // 8
 
 def update_rows(lib, n_obj, nnz, row_ptr, terms, val64, labels0, sizes, prev: DeviceMeans, k,
                 dim, ws, total_host=None) -> DeviceMeans:
