@@ -108,7 +108,8 @@ int ivfkm_bivf_build(int64_t k, int64_t dim, int major, int64_t nrows,
 size_t ivfkm_assign_workspace_size(int64_t n_obj, int64_t k);
 /* Tuning: rowcap = row entries staged in shared memory per pass (default 1024;
  * longer rows run in several passes), smem_limit = shared-memory budget per
- * CTA in bytes (default 225 KB, min 1 KB; a smaller budget forces the thread-block
+ * CTA in bytes (min 1 KB; -1 = adaptive default: rho is split over a
+ * thread-block cluster once it passes ~24 KB; a smaller budget forces the thread-block
  * cluster split), rr = 32-mean blocks per warp span of the register screen
  * (2, 4 or 8; 0 = automatic) or -8 for the TMA-pipelined screen; rr = -16*w
  * sets w warps per CTA for the TMA screen.

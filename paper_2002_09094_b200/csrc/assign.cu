@@ -1046,6 +1046,17 @@ struct Plan {
 int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
   const int64_t nblk = ivfkm_bivf_nblk(k);
   Plan pl;
+  if (smem_limit <= 0) {
+    // Adaptive budget (measured on configs 1-4): split rho over a thread-block
+    // cluster once it passes ~24 KB, so at least two CTAs stay resident per
+    // SM, but never below 24 KB per CTA nor above 100 KB.
+    const int64_t rho = nblk * 128;
+    int64_t b = rho / 2 + 8 * 1024;
+    if (b < 24 * 1024) b = 24 * 1024;
+    if (b > 100 * 1024) b = 100 * 1024;
+    if (rho + (int64_t)rowcap * 8 <= 24 * 1024) b = kSmemLimit - 2048;
+    smem_limit = (int)b;
+  }
   if (rr == -8 || rr == -4) {  // TMA (-8) / cp.async (-4) pipelined screens, 8-block spans
     pl.tma = true;
     pl.mode = rr == -8 ? 1 : 2;
@@ -1134,11 +1145,12 @@ extern "C" size_t ivfkm_assign_workspace_size(int64_t n_obj, int64_t /*k*/) {
 // smem_limit: shared-memory budget per CTA; a smaller budget forces the
 // thread-block-cluster split at small k (used by the tests).
 static int g_rowcap = 1024;
-static int g_smem_limit = kSmemLimit - 2048;  // leave room for static smem
+static int g_smem_limit = 0;  // 0: adaptive (see plan_screen)
 static int g_rr = 0;  // 0: automatic LDG screen; 2/4/8: LDG screen span; -8: TMA screen
 extern "C" void ivfkm_set_tuning(int rowcap, int smem_limit, int rr) {
   if (rowcap >= 32 && rowcap <= 8192) g_rowcap = rowcap / 32 * 32;
   if (smem_limit >= 1024 && smem_limit <= kSmemLimit - 2048) g_smem_limit = smem_limit;
+  if (smem_limit == -1) g_smem_limit = 0;  // back to adaptive
   if (rr == 0 || rr == 2 || rr == 4 || rr == 8 || rr == -8 || rr == -4) g_rr = rr;
   if (rr <= -16 && rr >= -16 * 16) g_tma_warps = -rr / 16;  // -16*w: TMA warps per CTA
 }

@@ -175,7 +175,7 @@ def tuning():
 
     lib = _lib.load()
     yield lib.ivfkm_set_tuning
-    lib.ivfkm_set_tuning(1024, 225 * 1024, 0)
+    lib.ivfkm_set_tuning(1024, -1, 0)
 
 
 def _assign_raw(ds, means, rowcap=None, smem=None, rr=-1):

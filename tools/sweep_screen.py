@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--rowcap", default="256,512,1024")
     ap.add_argument("--fill", default="0.5", help="BIVF dense_fill values (>1: never dense)")
     ap.add_argument("--permute", default="1")
+    ap.add_argument("--smem", default="0", help="shared-memory budgets per CTA (0 = default)")
     args = ap.parse_args()
     c = synth.CONFIGS[args.config]
     ds = synth.make_dataset(c["corpus"])
@@ -47,15 +48,19 @@ def main():
     st = eng.read_stats()
     out = []
     import itertools
-    for fill, perm, rr, rowcap in itertools.product(map(float, args.fill.split(",")),
-                                                    map(int, args.permute.split(",")),
-                                                    map(int, args.rr.split(",")),
-                                                    map(int, args.rowcap.split(","))):
+    last_bivf = None
+    for fill, perm, smem, rr, rowcap in itertools.product(map(float, args.fill.split(",")),
+                                                          map(int, args.permute.split(",")),
+                                                          map(int, args.smem.split(",")),
+                                                          map(int, args.rr.split(",")),
+                                                          map(int, args.rowcap.split(","))):
         if True:
-            eng.lib.ivfkm_set_bivf_options(fill, perm)
-            eng.build_bivf(dm)
+            if last_bivf != (fill, perm):
+                eng.lib.ivfkm_set_bivf_options(fill, perm)
+                eng.build_bivf(dm)
+                last_bivf = (fill, perm)
+            eng.lib.ivfkm_set_tuning(rowcap, smem if smem else -1, rr)
             eng.rowcap = rowcap
-            eng.lib.ivfkm_set_tuning(rowcap, 0, rr)
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
             times = []
             for _ in range(args.reps):
@@ -64,7 +69,7 @@ def main():
                 times.append(ev[0].elapsed_time(ev[1]))
             ok = bool(torch.equal(lab, base))
             ms = min(times)
-            rec = {"fill": fill, "permute": perm, "rr": rr, "rowcap": rowcap, "screen_ms": ms,
+            rec = {"fill": fill, "permute": perm, "smem": smem, "rr": rr, "rowcap": rowcap, "screen_ms": ms,
                    "postings_per_s": st.postings / (ms / 1e3), "labels_ok": ok}
             out.append(rec)
             print(json.dumps(rec), flush=True)
