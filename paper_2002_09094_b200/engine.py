@@ -18,6 +18,7 @@ stream only; all compute on the path is in libivfkm.so.
 from __future__ import annotations
 
 import ctypes as C
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -337,11 +338,13 @@ class HostIteration:
         if self.eng is None:
             self.eng = LloydEngine(dd, self.k)
         self.eng.dd = dd
-        t = lambda a: torch.from_numpy(np.asarray(a))  # noqa: E731 (pinned views stay pinned)
-        ptr = t(ms.indptr).to(dev, non_blocking=True)
-        terms = t(ms.term_ids).to(dev, non_blocking=True) - 1
-        vals = t(ms.values).to(dev, non_blocking=True)
-        ret = t(np.asarray(ms.retained).view(np.uint8)).to(dev, non_blocking=True)
+        with warnings.catch_warnings():  # read-only views of pinned buffers: only read here
+            warnings.simplefilter("ignore", UserWarning)
+            t = lambda a: torch.from_numpy(np.asarray(a))  # noqa: E731
+            ptr = t(ms.indptr).to(dev, non_blocking=True)
+            terms = t(ms.term_ids).to(dev, non_blocking=True) - 1
+            vals = t(ms.values).to(dev, non_blocking=True)
+            ret = t(np.asarray(ms.retained).view(np.uint8)).to(dev, non_blocking=True)
         if self.prefetch:
             # the means go first on the H2D engine; then the next step's corpus
             # streams in on the copy stream while this step computes

@@ -91,7 +91,7 @@ def update_ivf(ds, asg, prev) -> MeanSet:
     eng = engine_for(ds, k)
     dm = DeviceMeans.from_meanset(prev, eng.device)
     lab = torch.from_numpy(np.ascontiguousarray(asg.labels, dtype=np.int32) - 1).to(eng.device)
-    eng.sizes.copy_(torch.from_numpy(np.ascontiguousarray(asg.sizes, dtype=np.int64)))
+    eng.sizes.copy_(torch.from_numpy(np.array(asg.sizes, dtype=np.int64)))
     new = eng.update(lab, dm)
     return new.to_meanset("sparse_inverted")
 
