@@ -15,6 +15,7 @@ config 0 stores a SHA-256 of the regenerated inputs instead.
 from __future__ import annotations
 
 import hashlib
+import json
 import sys
 from pathlib import Path
 
@@ -76,6 +77,9 @@ def dump(name, ds, k, seed, max_iter, store_inputs=True, extra=None):
         final_indptr=fm.indptr, final_terms=fm.term_ids, final_values=fm.values,
         final_retained=fm.retained, final_sizes=res.final_assignment.sizes,
         inputs_sha=sha(ds.indptr, ds.term_ids, ds.values),
+        # the reference's own JSON record of the run (clustering.py:206-226),
+        # minus the backend name, for a byte-level comparison
+        run_json=np.array(json.dumps(_strip_backend(res.to_json_dict()), sort_keys=True)),
     )
     if store_inputs:
         payload.update(indptr=ds.indptr, term_ids=ds.term_ids, values=ds.values)
@@ -89,6 +93,12 @@ def dump(name, ds, k, seed, max_iter, store_inputs=True, extra=None):
     np.savez_compressed(OUT / f"{name}.npz", **payload)
     print(f"{name}: iters={res.iterations} converged={res.converged} "
           f"min_gap={min(g.min() for g in gaps):.3g} obj={res.objectives[-1]:.12g}")
+
+
+def _strip_backend(d):
+    d = dict(d)
+    d["meta"] = {k: v for k, v in d["meta"].items() if k != "backend"}
+    return d
 
 
 def ref_dataset(indptr, terms, vals, dim):

@@ -143,6 +143,13 @@ def test_run_matches_reference_golden(name):
     ds = golden_dataset(g)
     res = P.run("IVF", ds, int(g["k"]), seed=int(g["seed"]), max_iter=int(g["max_iter"]))
     _check_run_against_golden(res, g)
+    # the RunResult JSON record (clustering.py:206-226) equals the reference's,
+    # byte for byte once serialised (backend name aside)
+    import json
+
+    d = res.to_json_dict()
+    d["meta"] = {k: v for k, v in d["meta"].items() if k != "backend"}
+    assert json.dumps(d, sort_keys=True) == str(g["run_json"])
 
 
 def test_run_config0_matches_reference_golden():
