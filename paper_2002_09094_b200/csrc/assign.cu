@@ -157,10 +157,8 @@ __device__ __forceinline__ bool gather_values(const MaskPack<RR>& mk, uint32_t o
   for (int r = 0; r < RR; ++r) {
     const uint32_t mr = mk.m[r];
     u[r] = 0.f;
-    if (mr) {  // warp-uniform: empty blocks cost one test
-      if (mr & lanebit) u[r] = __ldg(pv + (o + (uint32_t)__popc(mr & lt)));
-      o += (uint32_t)__popc(mr);
-    }
+    if (mr & lanebit) u[r] = __ldg(pv + (o + (uint32_t)__popc(mr & lt)));
+    o += (uint32_t)__popc(mr);
   }
   return true;
 }
