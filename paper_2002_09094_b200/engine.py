@@ -318,13 +318,20 @@ class HostIteration:
     def _host_buffers(self, nnz: int):
         b = self.buf[self.cur]
         if b is None or b["cap"] < nnz:
-            cap = int(nnz * 1.25) + 1024
-            b = {"cap": cap,
-                 "ptr": torch.empty(self.k + 1, dtype=torch.int64).pin_memory(),
-                 "terms": torch.empty(cap, dtype=torch.int32).pin_memory(),
-                 "vals": torch.empty(cap, dtype=torch.float64).pin_memory(),
-                 "ret": torch.empty(self.k, dtype=torch.uint8).pin_memory()}
-            self.buf[self.cur] = b
+            # (re)allocate both halves of the double buffer together, with headroom,
+            # so steady-state steps never pin memory
+            cap = int(nnz * 1.5) + 1024
+            for i in (0, 1):
+                if self.buf[i] is None or self.buf[i]["cap"] < nnz:
+                    if i != self.cur and self.buf[i] is not None:
+                        continue  # still referenced by the MeanSet returned last step
+                    self.buf[i] = {
+                        "cap": cap,
+                        "ptr": torch.empty(self.k + 1, dtype=torch.int64).pin_memory(),
+                        "terms": torch.empty(cap, dtype=torch.int32).pin_memory(),
+                        "vals": torch.empty(cap, dtype=torch.float64).pin_memory(),
+                        "ret": torch.empty(self.k, dtype=torch.uint8).pin_memory()}
+            b = self.buf[self.cur]
         return b
 
     def step(self, ms: MeanSet):
