@@ -115,6 +115,10 @@ size_t ivfkm_assign_workspace_size(int64_t n_obj, int64_t k);
  * sets w warps per CTA for the TMA screen.
  * Out-of-range values leave the setting unchanged.                          */
 void ivfkm_set_tuning(int rowcap, int smem_limit, int rr);
+/* Order in which the screen visits objects ([dev] permutation of 0..n_obj-1
+ * used by subsequent ivfkm_assign/_screen calls; NULL = natural order).
+ * Results do not depend on it; it only changes cache locality.              */
+void ivfkm_set_object_order(const int32_t* order);
 int ivfkm_assign(int64_t n_obj, const int64_t* row_ptr /*[dev] n+1*/,
                  const int32_t* terms /*[dev]*/, const float* val32 /*[dev]*/,
                  const double* val64 /*[dev]*/, const double* xnorm /*[dev] n or NULL (=1)*/,

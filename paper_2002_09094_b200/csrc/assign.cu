@@ -63,6 +63,7 @@ struct ScreenParams {
   const uint32_t* offs;   // [dim][nblk] (+1: total)
   const uint32_t* nc;     // [dim] postings per term
   const int32_t* inv;     // [k] slot -> mean
+  const int32_t* order;   // [n] processing order of objects, or nullptr
   const float* pv32;
   double mu_max;
   int cta_blocks;  // 32-mean blocks held by one CTA (multiple of RR)
@@ -302,7 +303,8 @@ __global__ void __maxnreg__(72) screen_kernel(ScreenParams p) {
   const int warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
   const int z = blockIdx.x % p.nsplit;
-  const int64_t obj = blockIdx.x / p.nsplit;
+  const int64_t obj = p.order ? (int64_t)__ldg(p.order + blockIdx.x / p.nsplit)
+                              : (int64_t)(blockIdx.x / p.nsplit);
   if (obj >= p.n_obj) return;  // whole cluster shares obj
   const int64_t rb = p.row_ptr[obj], re = p.row_ptr[obj + 1];
   const int64_t nblk = p.nblk;
@@ -454,7 +456,8 @@ __global__ void __launch_bounds__(512) screen_tma_kernel(ScreenParams p) {
   const int warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
   const int z = blockIdx.x % p.nsplit;
-  const int64_t obj = blockIdx.x / p.nsplit;
+  const int64_t obj = p.order ? (int64_t)__ldg(p.order + blockIdx.x / p.nsplit)
+                              : (int64_t)(blockIdx.x / p.nsplit);
   if (obj >= p.n_obj) return;  // whole cluster shares obj
   const int64_t rb = p.row_ptr[obj], re = p.row_ptr[obj + 1];
   const int64_t nblk = p.nblk;
@@ -648,7 +651,8 @@ __global__ void __launch_bounds__(512) screen_async_kernel(ScreenParams p) {
   const int warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
   const int z = blockIdx.x % p.nsplit;
-  const int64_t obj = blockIdx.x / p.nsplit;
+  const int64_t obj = p.order ? (int64_t)__ldg(p.order + blockIdx.x / p.nsplit)
+                              : (int64_t)(blockIdx.x / p.nsplit);
   if (obj >= p.n_obj) return;
   const int64_t rb = p.row_ptr[obj], re = p.row_ptr[obj + 1];
   const int64_t nblk = p.nblk;
@@ -1147,6 +1151,8 @@ extern "C" size_t ivfkm_assign_workspace_size(int64_t n_obj, int64_t /*k*/) {
 static int g_rowcap = 1024;
 static int g_smem_limit = 0;  // 0: adaptive (see plan_screen)
 static int g_rr = 0;  // 0: automatic LDG screen; 2/4/8: LDG screen span; -8: TMA screen
+static const int32_t* g_order = nullptr;  // object processing order (device), or null
+extern "C" void ivfkm_set_object_order(const int32_t* order) { g_order = order; }
 extern "C" void ivfkm_set_tuning(int rowcap, int smem_limit, int rr) {
   if (rowcap >= 32 && rowcap <= 8192) g_rowcap = rowcap / 32 * 32;
   if (smem_limit >= 1024 && smem_limit <= kSmemLimit - 2048) g_smem_limit = smem_limit;
@@ -1188,6 +1194,7 @@ int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
   sp.offs = a.headers + a.dim * sp.nblk;
   sp.nc = a.headers + 2 * a.dim * sp.nblk + 1;
   sp.inv = reinterpret_cast<const int32_t*>(sp.nc + a.dim) + a.k;
+  sp.order = g_order;
   sp.pv32 = a.pval32;
   sp.mu_max = a.mu_max > 0 ? a.mu_max : 1.0;
   sp.cta_blocks = pl.cta_blocks;

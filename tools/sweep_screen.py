@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--fill", default="0.5", help="BIVF dense_fill values (>1: never dense)")
     ap.add_argument("--permute", default="1")
     ap.add_argument("--smem", default="0", help="shared-memory budgets per CTA (0 = default)")
+    ap.add_argument("--order", default="none", help="none,label: object processing order")
     args = ap.parse_args()
     c = synth.CONFIGS[args.config]
     ds = synth.make_dataset(c["corpus"])
@@ -49,7 +50,14 @@ def main():
     out = []
     import itertools
     last_bivf = None
-    for fill, perm, smem, rr, rowcap in itertools.product(map(float, args.fill.split(",")),
+    import ctypes
+    orders = {"none": None, "label": torch.argsort(base.long(), stable=True).to(torch.int32),
+              "rowlen": torch.argsort(-(eng.dd.row_ptr[1:] - eng.dd.row_ptr[:-1]),
+                                      stable=True).to(torch.int32)}
+    for oname in args.order.split(","):
+      o = orders[oname]
+      eng.lib.ivfkm_set_object_order(None if o is None else ctypes.c_void_p(o.data_ptr()))
+      for fill, perm, smem, rr, rowcap in itertools.product(map(float, args.fill.split(",")),
                                                           map(int, args.permute.split(",")),
                                                           map(int, args.smem.split(",")),
                                                           map(int, args.rr.split(",")),
@@ -69,13 +77,14 @@ def main():
                 times.append(ev[0].elapsed_time(ev[1]))
             ok = bool(torch.equal(lab, base))
             ms = min(times)
-            rec = {"fill": fill, "permute": perm, "smem": smem, "rr": rr, "rowcap": rowcap, "screen_ms": ms,
+            rec = {"order": oname, "fill": fill, "permute": perm, "smem": smem, "rr": rr, "rowcap": rowcap, "screen_ms": ms,
                    "postings_per_s": st.postings / (ms / 1e3), "labels_ok": ok}
             out.append(rec)
             print(json.dumps(rec), flush=True)
     eng.lib.ivfkm_set_tuning(1024, 0, 0)
     eng.lib.ivfkm_set_tuning(1024, 0, -128)
     eng.lib.ivfkm_set_bivf_options(0.25, 1)
+    eng.lib.ivfkm_set_object_order(None)
 
 
 if __name__ == "__main__":
