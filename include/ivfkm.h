@@ -119,6 +119,11 @@ void ivfkm_set_tuning(int rowcap, int smem_limit, int rr);
  * used by subsequent ivfkm_assign/_screen calls; NULL = natural order).
  * Results do not depend on it; it only changes cache locality.              */
 void ivfkm_set_object_order(const int32_t* order);
+/* The default order the engine uses: objects by row length, longest first
+ * (static longest-processing-time scheduling of the one-CTA-per-object grid). */
+size_t ivfkm_row_order_workspace_size(int64_t n_obj);
+int ivfkm_row_order(int64_t n_obj, const int64_t* row_ptr /*[dev]*/, int32_t* order /*[dev]*/,
+                    void* ws, size_t ws_bytes, ivfkm_stream_t stream);
 int ivfkm_assign(int64_t n_obj, const int64_t* row_ptr /*[dev] n+1*/,
                  const int32_t* terms /*[dev]*/, const float* val32 /*[dev]*/,
                  const double* val64 /*[dev]*/, const double* xnorm /*[dev] n or NULL (=1)*/,

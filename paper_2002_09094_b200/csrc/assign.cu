@@ -33,6 +33,7 @@
 //      fixed-point superaccumulator, so the host can round the exact sum once,
 //      like math.fsum).
 #include <cooperative_groups.h>
+#include <cub/cub.cuh>
 
 #include <cfloat>
 #include <climits>
@@ -1137,6 +1138,61 @@ int launch_screen(const Plan& pl, const ScreenParams& p, cudaStream_t st) {
 }
 
 }  // namespace
+
+// Longest rows first: a static LPT order for the one-CTA-per-object screen,
+// so the long rows do not trail at the end of the grid.
+namespace {
+__global__ void rowlen_keys_kernel(int64_t n, const int64_t* __restrict__ row_ptr,
+                                   unsigned int* __restrict__ key, int32_t* __restrict__ id) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t len = row_ptr[i + 1] - row_ptr[i];
+    key[i] = ~(unsigned)(len < 0xffffffffll ? len : 0xffffffffll);
+    id[i] = (int32_t)i;
+  }
+}
+}  // namespace
+
+extern "C" size_t ivfkm_row_order_workspace_size(int64_t n_obj) {
+  size_t sb = 0;
+  cub::DoubleBuffer<unsigned int> kb(nullptr, nullptr);
+  cub::DoubleBuffer<int32_t> vb(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, sb, kb, vb, (int)n_obj);
+  Carver c(nullptr);
+  c.take<unsigned int>(n_obj);
+  c.take<unsigned int>(n_obj);
+  c.take<int32_t>(n_obj);
+  c.take_bytes(sb);
+  return c.off;
+}
+
+extern "C" int ivfkm_row_order(int64_t n_obj, const int64_t* row_ptr, int32_t* order, void* ws,
+                               size_t ws_bytes, ivfkm_stream_t stream_) {
+  if (n_obj < 0 || n_obj > INT32_MAX || !row_ptr || !order) return IVFKM_E_ARG;
+  if (ws_bytes < ivfkm_row_order_workspace_size(n_obj)) return IVFKM_E_WORKSPACE;
+  if (n_obj == 0) return IVFKM_OK;
+  size_t sb = 0;
+  {
+    cub::DoubleBuffer<unsigned int> kb(nullptr, nullptr);
+    cub::DoubleBuffer<int32_t> vb(nullptr, nullptr);
+    cub::DeviceRadixSort::SortPairs(nullptr, sb, kb, vb, (int)n_obj);
+  }
+  Carver c(ws);
+  unsigned int* ka = c.take<unsigned int>(n_obj);
+  unsigned int* kb2 = c.take<unsigned int>(n_obj);
+  int32_t* ib = c.take<int32_t>(n_obj);
+  void* tmp = c.take_bytes(sb);
+  cudaStream_t st = as_stream(stream_);
+  rowlen_keys_kernel<<<grid_for(n_obj, 256), 256, 0, st>>>(n_obj, row_ptr, ka, order);
+  IVFKM_CHECK_LAUNCH();
+  cub::DoubleBuffer<unsigned int> kbuf(ka, kb2);
+  cub::DoubleBuffer<int32_t> vbuf(order, ib);
+  IVFKM_TRY(cub::DeviceRadixSort::SortPairs(tmp, sb, kbuf, vbuf, (int)n_obj, 0, 32, st));
+  if (vbuf.Current() != order)
+    IVFKM_TRY(cudaMemcpyAsync(order, vbuf.Current(), sizeof(int32_t) * n_obj,
+                              cudaMemcpyDeviceToDevice, st));
+  return IVFKM_OK;
+}
 
 extern "C" size_t ivfkm_assign_workspace_size(int64_t n_obj, int64_t /*k*/) {
   size_t total = 0;

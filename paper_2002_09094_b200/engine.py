@@ -202,7 +202,17 @@ class LloydEngine:
             if torch.cuda.is_available() else torch.zeros(C.sizeof(_lib.Stats), dtype=u8)
         self.total_host = torch.zeros(1, dtype=torch.int64).pin_memory()
         self.rowcap = max(32, min(512, (dd.max_row + 31) // 32 * 32))
+        self.order = self._row_order(dd)
         self.launches = 0  # our kernels launched (for the bench's gpu_launches)
+
+    def _row_order(self, dd):
+        """Longest rows first (computed once per dataset, on the device)."""
+        order = torch.empty(max(dd.n, 1), dtype=torch.int32, device=self.device)
+        ws = torch.empty(int(self.lib.ivfkm_row_order_workspace_size(dd.n)), dtype=torch.uint8,
+                         device=self.device)
+        _lib.check(self.lib.ivfkm_row_order(dd.n, _p(dd.row_ptr), _p(order), _p(ws), ws.numel(),
+                                            _stream()), "ivfkm_row_order")
+        return order
 
     # -- means ---------------------------------------------------------------
     def build_bivf(self, dm: DeviceMeans) -> DeviceMeans:
@@ -237,6 +247,10 @@ class LloydEngine:
             self.cur ^= 1
             out = self.labels[self.cur]
         self.lib.ivfkm_set_tuning(self.rowcap, 0, -1)
+        if self.order is not None and self.dd.n == self.order.numel():
+            self.lib.ivfkm_set_object_order(_p(self.order))
+        else:
+            self.lib.ivfkm_set_object_order(None)
         st = _stream()
         if events is not None:
             events[0].record()

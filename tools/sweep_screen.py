@@ -56,7 +56,7 @@ def main():
                                       stable=True).to(torch.int32)}
     for oname in args.order.split(","):
       o = orders[oname]
-      eng.lib.ivfkm_set_object_order(None if o is None else ctypes.c_void_p(o.data_ptr()))
+      eng.order = o
       for fill, perm, smem, rr, rowcap in itertools.product(map(float, args.fill.split(",")),
                                                           map(int, args.permute.split(",")),
                                                           map(int, args.smem.split(",")),
@@ -84,7 +84,7 @@ def main():
     eng.lib.ivfkm_set_tuning(1024, 0, 0)
     eng.lib.ivfkm_set_tuning(1024, 0, -128)
     eng.lib.ivfkm_set_bivf_options(0.25, 1)
-    eng.lib.ivfkm_set_object_order(None)
+    eng.lib.ivfkm_set_object_order(None)  # (the engine sets its own order per call)
 
 
 if __name__ == "__main__":
