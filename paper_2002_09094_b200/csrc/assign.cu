@@ -126,65 +126,43 @@ struct MaskPack {
   }
 };
 
-// One object nonzero against RR blocks starting at block gb (RR = 2, 4, 8 or
-// 16; groups of 8 blocks = one span each carry their own offset): lane-owned
-// slot 32*(gb+r)+lane reads its value at o_r + popc(mask_r below the lane),
-// with o_{r+1} = o_r + popc(mask_r); in a dense span (kDense on the offset)
-// the lane's values sit at span_base + 128*(r/4) + 4*lane + r%4 (bivf.cuh).
+// One object nonzero against RR blocks starting at block gb: lane-owned mean
+// 32*(gb+r)+lane reads its value at o_r + popc(mask_r below the lane), with
+// o_{r+1} = o_r + popc(mask_r); in a dense span (kDense on the offset) the
+// lane's values sit at span_base + 128*(r/4) + 4*lane + r%4 (bivf.cuh).
 template <int RR>
-struct OffPack {
-  static constexpr int G = (RR + kSpan - 1) / kSpan;
-  uint32_t o[G];
-};
-
-template <int RR>
-__device__ __forceinline__ bool gather_values(const MaskPack<RR>& mk, const OffPack<RR>& op,
-                                              uint32_t gb, const float* __restrict__ pv,
-                                              unsigned lane, unsigned lanebit, unsigned lt,
-                                              float (&u)[RR]) {
-  constexpr int G = OffPack<RR>::G;
-  constexpr int W = RR < kSpan ? RR : kSpan;  // blocks per group
-  bool work = false;
+__device__ __forceinline__ bool gather_values(const MaskPack<RR>& mk, uint32_t o, uint32_t gb,
+                                              const float* __restrict__ pv, unsigned lane,
+                                              unsigned lanebit, unsigned lt, float (&u)[RR]) {
+  if (o & kDense) {
+    const uint32_t r0 = gb & (kSpan - 1);
+    const uint32_t sbase = (o & ~kDense) - 32u * r0;
+    if constexpr (RR == kSpan) {  // r0 == 0: two aligned 16-B loads
+      const float4 a = __ldg(reinterpret_cast<const float4*>(pv + sbase) + lane);
+      const float4 b = __ldg(reinterpret_cast<const float4*>(pv + sbase) + 32 + lane);
+      u[0] = a.x; u[1] = a.y; u[2] = a.z; u[3] = a.w;
+      u[4] = b.x; u[5] = b.y; u[6] = b.z; u[7] = b.w;
+    } else {
 #pragma unroll
-  for (int h = 0; h < G; ++h) {
-    uint32_t o = op.o[h];
-    if (o & kDense) {
-      if constexpr (RR >= kSpan) {  // span-aligned: two aligned 16-B loads
-        const uint32_t sbase = o & ~kDense;
-        const float4 a = __ldg(reinterpret_cast<const float4*>(pv + sbase) + lane);
-        const float4 b = __ldg(reinterpret_cast<const float4*>(pv + sbase) + 32 + lane);
-        u[W * h + 0] = a.x; u[W * h + 1] = a.y; u[W * h + 2] = a.z; u[W * h + 3] = a.w;
-        u[W * h + 4] = b.x; u[W * h + 5] = b.y; u[W * h + 6] = b.z; u[W * h + 7] = b.w;
-      } else {
-        const uint32_t r0 = gb & (kSpan - 1);
-        const uint32_t sbase = (o & ~kDense) - 32u * r0;
-#pragma unroll
-        for (int r = 0; r < W; ++r) {
-          const uint32_t rr = r0 + r;
-          u[r] = __ldg(pv + sbase + 128u * (rr >> 2) + 4u * lane + (rr & 3u));
-        }
+      for (int r = 0; r < RR; ++r) {
+        const uint32_t rr = r0 + r;
+        u[r] = __ldg(pv + sbase + 128u * (rr >> 2) + 4u * lane + (rr & 3u));
       }
-      work = true;
-      continue;
     }
-    uint32_t any = 0;
-#pragma unroll
-    for (int r = 0; r < W; ++r) any |= mk.m[W * h + r];
-    if (!any) {  // the term populates none of these blocks
-#pragma unroll
-      for (int r = 0; r < W; ++r) u[W * h + r] = 0.f;
-      continue;
-    }
-    work = true;
-#pragma unroll
-    for (int r = 0; r < W; ++r) {
-      const uint32_t mr = mk.m[W * h + r];
-      u[W * h + r] = 0.f;
-      if (mr & lanebit) u[W * h + r] = __ldg(pv + (o + (uint32_t)__popc(mr & lt)));
-      o += (uint32_t)__popc(mr);
-    }
+    return true;
   }
-  return work;
+  uint32_t any = 0;
+#pragma unroll
+  for (int r = 0; r < RR; ++r) any |= mk.m[r];
+  if (!any) return false;  // the term populates none of these blocks
+#pragma unroll
+  for (int r = 0; r < RR; ++r) {
+    const uint32_t mr = mk.m[r];
+    u[r] = 0.f;
+    if (mr & lanebit) u[r] = __ldg(pv + (o + (uint32_t)__popc(mr & lt)));
+    o += (uint32_t)__popc(mr);
+  }
+  return true;
 }
 
 // CTA-local argmax (value desc, index asc) over the parked rho, merged over
@@ -371,22 +349,20 @@ __global__ void __maxnreg__(72) screen_kernel(ScreenParams p) {
       if (gb < nblk) {  // nblk is a multiple of RR: a span is all in or all out
         // 32-bit row arithmetic: dim * nblk < 2^31 is checked at build time
         const uint32_t nb32 = (uint32_t)nblk, gb32 = (uint32_t)gb;
-        auto ld = [&](int e, MaskPack<RR>& mk, OffPack<RR>& o) {
+        auto ld = [&](int e, MaskPack<RR>& mk, uint32_t& o) {
           if (e < cn) {
             const uint32_t row = (uint32_t)s_term[e] * nb32 + gb32;
             mk.load(masks + row);
-#pragma unroll
-            for (int h = 0; h < OffPack<RR>::G; ++h) o.o[h] = __ldg(offs + row + kSpan * h);
+            o = __ldg(offs + row);
           } else {
             mk.zero();
-#pragma unroll
-            for (int h = 0; h < OffPack<RR>::G; ++h) o.o[h] = 0u;
+            o = 0u;
           }
         };
         // software pipeline (unrolled by two): values of entries e, e+1 and
         // masks of e+2 are in flight while entry e accumulates
         MaskPack<RR> mk;
-        OffPack<RR> o;
+        uint32_t o;
         float uA[RR], uB[RR];
         ld(0, mk, o);
         bool hA = gather_values<RR>(mk, o, gb32, pv, lane, lanebit, lt, uA), hB;
@@ -1115,7 +1091,6 @@ int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
   pl.tma = false;
   pl.mode = 0;
   pl.rr = rr > 0 ? rr : (nblk >= 32 ? 8 : 2);
-  if (pl.rr == 16 && nblk % 16 != 0) pl.rr = 8;  // 16-block spans need nblk % 16 == 0
   pl.rowcap = rowcap;
   const size_t stage = (size_t)rowcap * 8;
   pl.nsplit = 0;
@@ -1238,7 +1213,7 @@ extern "C" void ivfkm_set_tuning(int rowcap, int smem_limit, int rr) {
   if (rowcap >= 32 && rowcap <= 8192) g_rowcap = rowcap / 32 * 32;
   if (smem_limit >= 1024 && smem_limit <= kSmemLimit - 2048) g_smem_limit = smem_limit;
   if (smem_limit == -1) g_smem_limit = 0;  // back to adaptive
-  if (rr == 0 || rr == 2 || rr == 4 || rr == 8 || rr == 16 || rr == -8 || rr == -4) g_rr = rr;
+  if (rr == 0 || rr == 2 || rr == 4 || rr == 8 || rr == -8 || rr == -4) g_rr = rr;
   if (rr <= -16 && rr >= -16 * 16) g_tma_warps = -rr / 16;  // -16*w: TMA warps per CTA
 }
 
@@ -1289,7 +1264,6 @@ int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
   sp.stats = a.stats;
   if (pl.tma) return launch_screen<8>(pl, sp, st);
   switch (pl.rr) {
-    case 16: return launch_screen<16>(pl, sp, st);
     case 8: return launch_screen<8>(pl, sp, st);
     case 4: return launch_screen<4>(pl, sp, st);
     default: return launch_screen<2>(pl, sp, st);
