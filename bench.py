@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist", action="store_true",
+                    help="use the sharded multi-GPU driver even at one rank (torchrun)")
     ap.add_argument("--cpu-seconds", type=float, default=8.0,
                     help="target CPU time of the sampled assign in the baseline")
     return ap.parse_args()
@@ -275,7 +277,7 @@ def ours_arm(args, rank, world):
     from paper_2002_09094_b200.engine import (DeviceDataset, DeviceMeans, HostDataset,
                                               LloydEngine)
 
-    if world > 1:
+    if world > 1 or args.dist:
         from paper_2002_09094_b200 import dist as D
 
         return D.bench_multi(args, rank, world)

@@ -245,14 +245,21 @@ class DistLloyd:
 
 
 def bench_multi(args, rank: int, world: int) -> None:
-    """bench.py --gpus N under torchrun: strong scaling of one Lloyd run."""
+    """bench.py --gpus N under torchrun: strong scaling of one Lloyd run over N
+    ranks (objects sharded, means replicated), plus the same metric end to end
+    (every step re-uploads each rank's shard and the means from pinned host
+    memory and reads labels + means back)."""
     from . import synth
     from .clustering import init_means
+    from .engine import DeviceDataset, DeviceMeans
 
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    if os.environ.get("MASTER_ADDR") is None:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29513")
+    dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
     comm = ShardComm(rank, world)
     c = synth.CONFIGS[args.config]
     spec = c["corpus"]
@@ -279,6 +286,32 @@ def bench_multi(args, rank: int, world: int) -> None:
     torch.cuda.synchronize()
     ms = torch.tensor([s.elapsed_time(e)], dtype=torch.float64, device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    # ---- end to end: host buffers in and out every step
+    e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(1, min(args.steps, 3))
+    host = {name: getattr(dm, name).cpu().pin_memory() for name in ("ptr", "terms", "vals",
+                                                                     "retained")}
+    lab_host = torch.empty(run.dd.n, dtype=torch.int32).pin_memory()
+    h2d = d2h = 0
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        run.dd = DeviceDataset(run.host, dev)
+        run.eng.dd = run.dd
+        dmh = DeviceMeans(k, ds.dim, host["ptr"].to(dev, non_blocking=True),
+                          host["terms"].to(dev, non_blocking=True),
+                          host["vals"].to(dev, non_blocking=True),
+                          host["retained"].to(dev, non_blocking=True))
+        dmh = run.eng.build_bivf(dmh)
+        lab, _ = run.assign(dmh, None)
+        lab_host.copy_(lab, non_blocking=True)
+        new = run.update(lab, dmh)
+        host = {name: getattr(new, name).cpu() for name in ("ptr", "terms", "vals", "retained")}
+        h2d = run.host.nbytes + sum(v.numel() * v.element_size() for v in host.values())
+        d2h = lab_host.numel() * 4 + sum(v.numel() * v.element_size() for v in host.values())
+    torch.cuda.synchronize()
+    e2e_t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     dist.barrier()
     if rank == 0:
         t = float(ms.item())
@@ -293,6 +326,9 @@ def bench_multi(args, rank: int, world: int) -> None:
                        "parallelism": f"objects sharded over {world} GPUs, means replicated",
                        "l2": "inputs larger than L2"},
             "postings_per_sec": sum(posts) / (t / 1000.0),
+            "e2e": {"value": e2e_steps / float(e2e_t.item()), "unit": "iter/s",
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "steps": e2e_steps, "per_rank_bytes": True},
             "time": time.strftime("%Y-%m-%dT%H:%M:%S"),
         }), flush=True)
     dist.destroy_process_group()
