@@ -115,11 +115,10 @@ size_t ivfkm_assign_workspace_size(int64_t n_obj, int64_t k);
  * sets w warps per CTA for the TMA screen.
  * Out-of-range values leave the setting unchanged.                          */
 void ivfkm_set_tuning(int rowcap, int smem_limit, int rr);
-/* Order in which the screen visits objects ([dev] permutation of 0..n_obj-1
- * used by subsequent ivfkm_assign/_screen calls; NULL = natural order).
- * Results do not depend on it; it only changes cache locality.              */
-void ivfkm_set_object_order(const int32_t* order);
-/* The default order the engine uses: objects by row length, longest first
+/* Object order: ivfkm_assign/_screen take `order`, the order in which the
+ * screen visits objects ([dev] permutation of 0..n_obj-1; NULL = natural
+ * order).  Results do not depend on it; it only changes load balance and
+ * cache locality.  The default order the engine uses: objects by row length, longest first
  * (static longest-processing-time scheduling of the one-CTA-per-object grid). */
 size_t ivfkm_row_order_workspace_size(int64_t n_obj);
 int ivfkm_row_order(int64_t n_obj, const int64_t* row_ptr /*[dev]*/, int32_t* order /*[dev]*/,
@@ -131,8 +130,8 @@ int ivfkm_assign(int64_t n_obj, const int64_t* row_ptr /*[dev] n+1*/,
                  const float* pval32 /*[dev]*/, const double* pval64 /*[dev]*/, double mu_max,
                  const int32_t* prev_labels /*[dev] n or NULL*/, int32_t* labels /*[dev] n*/,
                  double* sims /*[dev] n*/, unsigned long long* sizes /*[dev] k*/,
-                 ivfkm_stats* stats /*[dev]*/, void* ws, size_t ws_bytes,
-                 ivfkm_stream_t stream);
+                 ivfkm_stats* stats /*[dev]*/, const int32_t* order /*[dev] n or NULL*/,
+                 void* ws, size_t ws_bytes, ivfkm_stream_t stream);
 
 /* The two halves of ivfkm_assign, for callers that time the fp32 screen
  * (the dominant kernel) separately: screen zeroes *stats and fills the
@@ -141,7 +140,8 @@ int ivfkm_assign(int64_t n_obj, const int64_t* row_ptr /*[dev] n+1*/,
 int ivfkm_assign_screen(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
                         const float* val32, const double* xnorm, int64_t k, int64_t dim,
                         const uint32_t* headers, const float* pval32, double mu_max,
-                        ivfkm_stats* stats, void* ws, size_t ws_bytes, ivfkm_stream_t stream);
+                        ivfkm_stats* stats, const int32_t* order, void* ws, size_t ws_bytes,
+                        ivfkm_stream_t stream);
 int ivfkm_assign_finish(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
                         const double* val64, int64_t k, int64_t dim, const uint32_t* headers,
                         const double* pval64, const int32_t* prev_labels, int32_t* labels,

@@ -54,13 +54,12 @@ SIGNATURES = {
                                    _vp, _sz, _vp]),
     "ivfkm_assign_workspace_size": (_sz, [_i64, _i64]),
     "ivfkm_set_tuning": (None, [C.c_int, C.c_int, C.c_int]),
-    "ivfkm_set_object_order": (None, [_vp]),
     "ivfkm_row_order_workspace_size": (_sz, [_i64]),
     "ivfkm_row_order": (C.c_int, [_i64, _vp, _vp, _vp, _sz, _vp]),
     "ivfkm_assign": (C.c_int, [_i64, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _f64,
-                               _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+                               _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "ivfkm_assign_screen": (C.c_int, [_i64, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _f64, _vp,
-                                      _vp, _sz, _vp]),
+                                      _vp, _vp, _sz, _vp]),
     "ivfkm_assign_finish": (C.c_int, [_i64, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp,
                                       _vp, _vp, _vp, _sz, _vp]),
     "ivfkm_score_labels": (C.c_int, [_i64, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp,

@@ -1207,8 +1207,6 @@ extern "C" size_t ivfkm_assign_workspace_size(int64_t n_obj, int64_t /*k*/) {
 static int g_rowcap = 1024;
 static int g_smem_limit = 0;  // 0: adaptive (see plan_screen)
 static int g_rr = 0;  // 0: automatic LDG screen; 2/4/8: LDG screen span; -8: TMA screen
-static const int32_t* g_order = nullptr;  // object processing order (device), or null
-extern "C" void ivfkm_set_object_order(const int32_t* order) { g_order = order; }
 extern "C" void ivfkm_set_tuning(int rowcap, int smem_limit, int rr) {
   if (rowcap >= 32 && rowcap <= 8192) g_rowcap = rowcap / 32 * 32;
   if (smem_limit >= 1024 && smem_limit <= kSmemLimit - 2048) g_smem_limit = smem_limit;
@@ -1232,6 +1230,7 @@ struct AssignArgs {
   const double* pval64;
   double mu_max;
   ivfkm_stats* stats;
+  const int32_t* order;
 };
 
 int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
@@ -1250,7 +1249,7 @@ int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
   sp.offs = a.headers + a.dim * sp.nblk;
   sp.nc = a.headers + 2 * a.dim * sp.nblk + 1;
   sp.inv = reinterpret_cast<const int32_t*>(sp.nc + a.dim) + a.k;
-  sp.order = g_order;
+  sp.order = a.order;
   sp.pv32 = a.pval32;
   sp.mu_max = a.mu_max > 0 ? a.mu_max : 1.0;
   sp.cta_blocks = pl.cta_blocks;
@@ -1306,8 +1305,8 @@ int finish_impl(const AssignArgs& a, const AssignWs& w, const int32_t* prev_labe
 extern "C" int ivfkm_assign_screen(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
                                    const float* val32, const double* xnorm, int64_t k,
                                    int64_t dim, const uint32_t* headers, const float* pval32,
-                                   double mu_max, ivfkm_stats* stats, void* ws, size_t ws_bytes,
-                                   ivfkm_stream_t stream_) {
+                                   double mu_max, ivfkm_stats* stats, const int32_t* order,
+                                   void* ws, size_t ws_bytes, ivfkm_stream_t stream_) {
   if (n_obj < 0 || k < 1 || dim < 1 || !row_ptr || !stats || !headers) return IVFKM_E_ARG;
   if (n_obj > INT32_MAX || k > INT32_MAX) return IVFKM_E_UNSUPPORTED;
   size_t need = 0;
@@ -1318,7 +1317,7 @@ extern "C" int ivfkm_assign_screen(int64_t n_obj, const int64_t* row_ptr, const 
   IVFKM_TRY(cudaMemsetAsync(w.ovf_len, 0, sizeof(unsigned int), st));
   if (n_obj == 0) return IVFKM_OK;
   AssignArgs a{n_obj, row_ptr, terms, val32, nullptr, xnorm, k, dim, headers, pval32, nullptr,
-               mu_max, stats};
+               mu_max, stats, order};
   return screen_impl(a, w, st);
 }
 
@@ -1337,7 +1336,7 @@ extern "C" int ivfkm_assign_finish(int64_t n_obj, const int64_t* row_ptr, const 
   if (sizes) IVFKM_TRY(cudaMemsetAsync(sizes, 0, sizeof(unsigned long long) * k, st));
   if (n_obj == 0) return IVFKM_OK;
   AssignArgs a{n_obj, row_ptr, terms, nullptr, val64, nullptr, k, dim, headers, nullptr, pval64,
-               0.0, stats};
+               0.0, stats, nullptr};
   return finish_impl(a, w, prev_labels, labels, sims, sizes, st);
 }
 
@@ -1346,10 +1345,10 @@ extern "C" int ivfkm_assign(int64_t n_obj, const int64_t* row_ptr, const int32_t
                             int64_t k, int64_t dim, const uint32_t* headers, const float* pval32,
                             const double* pval64, double mu_max, const int32_t* prev_labels,
                             int32_t* labels, double* sims, unsigned long long* sizes,
-                            ivfkm_stats* stats, void* ws, size_t ws_bytes,
+                            ivfkm_stats* stats, const int32_t* order, void* ws, size_t ws_bytes,
                             ivfkm_stream_t stream_) {
   int rc = ivfkm_assign_screen(n_obj, row_ptr, terms, val32, xnorm, k, dim, headers, pval32,
-                               mu_max, stats, ws, ws_bytes, stream_);
+                               mu_max, stats, order, ws, ws_bytes, stream_);
   if (rc) return rc;
   return ivfkm_assign_finish(n_obj, row_ptr, terms, val64, k, dim, headers, pval64, prev_labels,
                              labels, sims, sizes, stats, ws, ws_bytes, stream_);

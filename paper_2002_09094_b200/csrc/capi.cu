@@ -134,7 +134,7 @@ extern "C" int ivfkm_assign_ivf_host(int64_t n, const int64_t* indptr, const int
                     d_v64.as<double>(), d_xn.as<double>(), k, dim, d_hdr.as<uint32_t>(),
                     d_p32.as<float>(), d_p64.as<double>(), mu_max, nullptr, d_lab.as<int32_t>(),
                     d_sims.as<double>(), d_sizes.as<unsigned long long>(),
-                    d_stats.as<ivfkm_stats>(), d_aws.p, aws, nullptr);
+                    d_stats.as<ivfkm_stats>(), nullptr, d_aws.p, aws, nullptr);
   if (rc) return rc;
   ivfkm_stats stats;
   IVFKM_TRY(cudaMemcpyAsync(labels, d_lab.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));

@@ -247,16 +247,13 @@ class LloydEngine:
             self.cur ^= 1
             out = self.labels[self.cur]
         self.lib.ivfkm_set_tuning(self.rowcap, 0, -1)
-        if self.order is not None and self.dd.n == self.order.numel():
-            self.lib.ivfkm_set_object_order(_p(self.order))
-        else:
-            self.lib.ivfkm_set_object_order(None)
+        order = self.order if self.order is not None and dd.n == self.order.numel() else None
         st = _stream()
         if events is not None:
             events[0].record()
         rc = self.lib.ivfkm_assign_screen(dd.n, _p(dd.row_ptr), _p(dd.terms), _p(dd.val32),
                                           _p(dd.xnorm), self.k, dd.dim, _p(dm.headers),
-                                          _p(dm.pv32), _MU_MAX, _p(self.stats),
+                                          _p(dm.pv32), _MU_MAX, _p(self.stats), _p(order),
                                           _p(self.ws_assign), self.ws_assign.numel(), st)
         _lib.check(rc, "ivfkm_assign_screen")
         if events is not None:

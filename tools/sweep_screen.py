@@ -84,7 +84,6 @@ def main():
     eng.lib.ivfkm_set_tuning(1024, 0, 0)
     eng.lib.ivfkm_set_tuning(1024, 0, -128)
     eng.lib.ivfkm_set_bivf_options(0.25, 1)
-    eng.lib.ivfkm_set_object_order(None)  # (the engine sets its own order per call)
 
 
 if __name__ == "__main__":
