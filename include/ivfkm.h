@@ -83,7 +83,7 @@ int ivfkm_device_count(void);
 int64_t ivfkm_bivf_nblk(int64_t k); /* 32-mean blocks per term, padded */
 int64_t ivfkm_bivf_headers_size(int64_t k, int64_t dim);
 int64_t ivfkm_bivf_values_capacity(int64_t k, int64_t dim, int64_t nnz);
-/* Build options: dense_fill in [0.25, 1] (> 1: never dense; default 0.25),
+/* Build options: dense_fill in [1/32, 1] (> 1: never dense; default 0.25),
  * permute = 1 orders slots by mean term count (default), 0 keeps mean ids.
  * Out-of-range values leave the setting unchanged.                          */
 void ivfkm_set_bivf_options(float dense_fill, int permute);
@@ -91,11 +91,14 @@ size_t ivfkm_bivf_workspace_size(int64_t dim, int64_t k);
 /* major = 0: rows of (ptr, cols) are means (mean-major CSR, cols = terms);
  * major = 1: rows are terms (term-major IVF, cols = mean ids).  0-based ids;
  * an id outside [0,k) / [0,dim) gives IVFKM_E_RANGE.                        */
+/* Screen values: screen_bits = 32 stores them as fp32, 16 as fp16 (half the
+ * bytes; the screen's error window widens accordingly, labels stay exact).
+ * val_screen and val64 hold ivfkm_bivf_values_capacity() values each.       */
 int ivfkm_bivf_build(int64_t k, int64_t dim, int major, int64_t nrows,
                      const int64_t* ptr /*[dev] nrows+1*/, const int32_t* cols /*[dev]*/,
                      const double* vals /*[dev]*/, uint32_t* headers /*[dev]*/,
-                     float* val32 /*[dev] nnz*/, double* val64 /*[dev] nnz*/, void* ws,
-                     size_t ws_bytes, ivfkm_stream_t stream);
+                     void* val_screen /*[dev]*/, int screen_bits /*32 or 16*/,
+                     double* val64 /*[dev]*/, void* ws, size_t ws_bytes, ivfkm_stream_t stream);
 
 /* ---- assignment step ------------------------------------------------------
  * For every object i: rho_i[c] = sum_h x_{i,h} mu_c[t_h] screened in fp32
@@ -127,7 +130,8 @@ int ivfkm_assign(int64_t n_obj, const int64_t* row_ptr /*[dev] n+1*/,
                  const int32_t* terms /*[dev]*/, const float* val32 /*[dev]*/,
                  const double* val64 /*[dev]*/, const double* xnorm /*[dev] n or NULL (=1)*/,
                  int64_t k, int64_t dim, const uint32_t* headers /*[dev]*/,
-                 const float* pval32 /*[dev]*/, const double* pval64 /*[dev]*/, double mu_max,
+                 const void* pval_screen /*[dev]*/, int screen_bits /*as built*/,
+                 const double* pval64 /*[dev]*/, double mu_max,
                  const int32_t* prev_labels /*[dev] n or NULL*/, int32_t* labels /*[dev] n*/,
                  double* sims /*[dev] n*/, unsigned long long* sizes /*[dev] k*/,
                  ivfkm_stats* stats /*[dev]*/, const int32_t* order /*[dev] n or NULL*/,
@@ -139,7 +143,8 @@ int ivfkm_assign(int64_t n_obj, const int64_t* row_ptr /*[dev] n+1*/,
  * the objective.  Use the same workspace for both.                          */
 int ivfkm_assign_screen(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
                         const float* val32, const double* xnorm, int64_t k, int64_t dim,
-                        const uint32_t* headers, const float* pval32, double mu_max,
+                        const uint32_t* headers, const void* pval_screen, int screen_bits,
+                        double mu_max,
                         ivfkm_stats* stats, const int32_t* order, void* ws, size_t ws_bytes,
                         ivfkm_stream_t stream);
 int ivfkm_assign_finish(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,

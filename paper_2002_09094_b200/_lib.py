@@ -50,15 +50,17 @@ SIGNATURES = {
     "ivfkm_bivf_values_capacity": (_i64, [_i64, _i64, _i64]),
     "ivfkm_set_bivf_options": (None, [C.c_float, C.c_int]),
     "ivfkm_bivf_workspace_size": (_sz, [_i64, _i64]),
-    "ivfkm_bivf_build": (C.c_int, [_i64, _i64, C.c_int, _i64, _vp, _vp, _vp, _vp, _vp, _vp,
-                                   _vp, _sz, _vp]),
+    "ivfkm_bivf_build": (C.c_int, [_i64, _i64, C.c_int, _i64, _vp, _vp, _vp, _vp, _vp, C.c_int,
+                                   _vp, _vp, _sz, _vp]),
     "ivfkm_assign_workspace_size": (_sz, [_i64, _i64]),
     "ivfkm_set_tuning": (None, [C.c_int, C.c_int, C.c_int]),
     "ivfkm_row_order_workspace_size": (_sz, [_i64]),
     "ivfkm_row_order": (C.c_int, [_i64, _vp, _vp, _vp, _sz, _vp]),
-    "ivfkm_assign": (C.c_int, [_i64, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _f64,
+    "ivfkm_assign": (C.c_int, [_i64, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, C.c_int, _vp,
+                               _f64,
                                _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
-    "ivfkm_assign_screen": (C.c_int, [_i64, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _f64, _vp,
+    "ivfkm_assign_screen": (C.c_int, [_i64, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, C.c_int,
+                                      _f64, _vp,
                                       _vp, _vp, _sz, _vp]),
     "ivfkm_assign_finish": (C.c_int, [_i64, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp,
                                       _vp, _vp, _vp, _sz, _vp]),

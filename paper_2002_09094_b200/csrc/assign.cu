@@ -33,6 +33,8 @@
 //      fixed-point superaccumulator, so the host can round the exact sum once,
 //      like math.fsum).
 #include <cooperative_groups.h>
+#include <cuda_fp16.h>
+
 #include <cub/cub.cuh>
 
 #include <cfloat>
@@ -51,6 +53,8 @@ constexpr int kMaxC = IVFKM_MAXC;
 constexpr int kLimbs = IVFKM_OBJ_LIMBS;
 constexpr int kMaxSplit = 8;           // portable cluster size
 constexpr int kSmemLimit = 227 * 1024;  // opt-in dynamic shared memory per CTA
+constexpr int kMaxLocalSpans = 255;     // dense-prefix buckets per CTA (screen_kernel)
+constexpr int kEntryBytes = 20;         // screen_kernel staging per row entry
 
 struct ScreenParams {
   int64_t n_obj;
@@ -63,9 +67,11 @@ struct ScreenParams {
   const uint32_t* masks;  // [dim][nblk]
   const uint32_t* offs;   // [dim][nblk] (+1: total)
   const uint32_t* nc;     // [dim] postings per term
+  const uint32_t* dpre;   // [dim] dense prefix spans per term
   const int32_t* inv;     // [k] slot -> mean
   const int32_t* order;   // [n] processing order of objects, or nullptr
-  const float* pv32;
+  const float* pv32;  // fp32 screen values, or fp16 ones when half
+  int half;
   double mu_max;
   int cta_blocks;  // 32-mean blocks held by one CTA (multiple of RR)
   int nsplit;      // CTAs per object (cluster size)
@@ -165,6 +171,144 @@ __device__ __forceinline__ bool gather_values(const MaskPack<RR>& mk, uint32_t o
   return true;
 }
 
+// fp16 screen values (bivf.cuh, bivf_find16_slot): a dense span holds each
+// lane's 8 values contiguously, so one 16-B load serves the whole span.  The
+// raw bits stay packed in registers until the FMAs: converting right after
+// the load would make the warp wait for it and defeat the software pipeline.
+// Returns 0 (term absent from these blocks), 1 (w[r] = one value's bits per
+// block) or 2 (w[0..RR/2) = packed pairs).
+template <int RR>
+__device__ __forceinline__ int gather_values16(const MaskPack<RR>& mk, uint32_t o, uint32_t gb,
+                                               const __half* __restrict__ pv, unsigned lane,
+                                               unsigned lanebit, unsigned lt, uint32_t (&w)[RR]) {
+  const unsigned short* __restrict__ p16 = reinterpret_cast<const unsigned short*>(pv);
+  if (o & kDense) {
+    const uint32_t r0 = gb & (kSpan - 1);
+    const uint32_t sbase = (o & ~kDense) - 32u * r0;
+    if constexpr (RR == kSpan) {
+      const uint4 a = __ldg(reinterpret_cast<const uint4*>(pv + sbase) + lane);
+      w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+      return 2;
+    } else {
+#pragma unroll
+      for (int r = 0; r < RR; ++r) w[r] = __ldg(p16 + sbase + 8u * lane + r0 + r);
+      return 1;
+    }
+  }
+  uint32_t any = 0;
+#pragma unroll
+  for (int r = 0; r < RR; ++r) any |= mk.m[r];
+  if (!any) return 0;
+#pragma unroll
+  for (int r = 0; r < RR; ++r) {
+    const uint32_t mr = mk.m[r];
+    w[r] = 0u;
+    if (mr & lanebit) w[r] = __ldg(p16 + (o + (uint32_t)__popc(mr & lt)));
+    o += (uint32_t)__popc(mr);
+  }
+  return 1;
+}
+
+// The screen's in-flight values of one (entry, span): fp32 values, or fp16 bits.
+template <int RR, bool HALF>
+struct SpanVals;
+
+template <int RR>
+struct SpanVals<RR, false> {
+  float u[RR];
+  bool has;
+  __device__ __forceinline__ void gather(const MaskPack<RR>& mk, uint32_t o, uint32_t gb,
+                                         const void* pv, unsigned lane, unsigned lanebit,
+                                         unsigned lt) {
+    has = gather_values<RR>(mk, o, gb, static_cast<const float*>(pv), lane, lanebit, lt, u);
+  }
+  // Lane's first dense value of a span in bytes from the array start, given the
+  // span's first value index sbase: slot 32*(b0+r)+lane at sbase + 128*(r/4) +
+  // 4*lane + r%4 for blocks r = r0 .. r0+RR-1 (bivf.cuh).
+  static __device__ __forceinline__ uint32_t lane_bytes(uint32_t sbase, uint32_t r0,
+                                                        unsigned lane) {
+    return 4u * (sbase + 128u * (r0 >> 2) + 4u * lane + (r0 & 3u));
+  }
+  __device__ __forceinline__ void load_dense(const char* at) {
+    has = true;
+    if constexpr (RR == 8) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(at));
+      const float4 b = __ldg(reinterpret_cast<const float4*>(at + 512));
+      u[0] = a.x; u[1] = a.y; u[2] = a.z; u[3] = a.w;
+      u[4] = b.x; u[5] = b.y; u[6] = b.z; u[7] = b.w;
+    } else if constexpr (RR == 4) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(at));
+      u[0] = a.x; u[1] = a.y; u[2] = a.z; u[3] = a.w;
+    } else {
+      const float2 a = __ldg(reinterpret_cast<const float2*>(at));
+      u[0] = a.x; u[1] = a.y;
+    }
+  }
+  static constexpr uint32_t kElem = 4;
+  __device__ __forceinline__ void fma(float v, float (&acc)[RR]) const {
+    // fma(v, 0, acc) == acc exactly: absent postings cost no rounding;
+    // a span the term does not populate skips the FMAs altogether
+    if (has) {
+#pragma unroll
+      for (int r = 0; r < RR; ++r) acc[r] = fmaf(v, u[r], acc[r]);
+    }
+  }
+  // the entry's value is read only when the span holds postings
+  __device__ __forceinline__ void fma(const int* vbits, float (&acc)[RR]) const {
+    if (has) {
+      const float v = __int_as_float(*vbits);
+#pragma unroll
+      for (int r = 0; r < RR; ++r) acc[r] = fmaf(v, u[r], acc[r]);
+    }
+  }
+};
+
+template <int RR>
+struct SpanVals<RR, true> {
+  uint32_t w[RR];
+  int code;
+  __device__ __forceinline__ void gather(const MaskPack<RR>& mk, uint32_t o, uint32_t gb,
+                                         const void* pv, unsigned lane, unsigned lanebit,
+                                         unsigned lt) {
+    code = gather_values16<RR>(mk, o, gb, static_cast<const __half*>(pv), lane, lanebit, lt, w);
+  }
+  // lane's RR contiguous halves of a dense span: sbase + 8*lane + r0 (bivf.cuh)
+  static __device__ __forceinline__ uint32_t lane_bytes(uint32_t sbase, uint32_t r0,
+                                                        unsigned lane) {
+    return 2u * (sbase + 8u * lane + r0);
+  }
+  __device__ __forceinline__ void load_dense(const char* at) {
+    code = 2;
+    if constexpr (RR == 8) {
+      const uint4 a = __ldg(reinterpret_cast<const uint4*>(at));
+      w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+    } else if constexpr (RR == 4) {
+      const uint2 a = __ldg(reinterpret_cast<const uint2*>(at));
+      w[0] = a.x; w[1] = a.y;
+    } else {
+      w[0] = __ldg(reinterpret_cast<const unsigned int*>(at));
+    }
+  }
+  static constexpr uint32_t kElem = 2;
+  __device__ __forceinline__ void fma(const int* vbits, float (&acc)[RR]) const {
+    if (code != 0) fma(__int_as_float(*vbits), acc);
+  }
+  __device__ __forceinline__ void fma(float v, float (&acc)[RR]) const {
+    if (code == 2) {
+#pragma unroll
+      for (int q = 0; q < RR / 2; ++q) {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[q]));
+        acc[2 * q] = fmaf(v, f.x, acc[2 * q]);
+        acc[2 * q + 1] = fmaf(v, f.y, acc[2 * q + 1]);
+      }
+    } else if (code == 1) {
+#pragma unroll
+      for (int r = 0; r < RR; ++r)
+        acc[r] = fmaf(v, __half2float(__ushort_as_half((unsigned short)w[r])), acc[r]);
+    }
+  }
+};
+
 // CTA-local argmax (value desc, index asc) over the parked rho, merged over
 // the cluster through DSMEM when k is split; then the rigorous fp32 window and
 // the candidate queue for exact rescoring.  Every thread of the CTA calls it.
@@ -243,9 +387,14 @@ __device__ __forceinline__ void screen_epilogue(const ScreenParams& p, ScreenSha
   // ---- rigorous fp32 window and candidate collection ----
   const int64_t n_i = re - rb;
   const double xn = p.xnorm ? p.xnorm[obj] : 1.0;
-  const double eps = ((double)(n_i + 3) * 0x1p-24 + (double)n_i * 0x1p-50) * xn * p.mu_max *
-                         (1.0 + 1e-6) +
-                     (double)(n_i + 1) * 0x1p-125;
+  // fp16 screen values add a relative 2^-11 rounding per mean value plus an
+  // absolute 2^-25 below fp16's normal range (sum over h of |x_h| <= n*|x|)
+  const double eps =
+      p.half ? (0x1p-11 + (double)(n_i + 4) * 0x1p-24) * xn * p.mu_max * (1.0 + 0x1p-9) +
+                   (double)n_i * xn * 0x1p-25 * (1.0 + 0x1p-9) + (double)(n_i + 1) * 0x1p-125
+             : ((double)(n_i + 3) * 0x1p-24 + (double)n_i * 0x1p-50) * xn * p.mu_max *
+                       (1.0 + 1e-6) +
+                   (double)(n_i + 1) * 0x1p-125;
   const double thr = (double)gv - 2.0 * eps;
   if (gpost != 0) {
     for (int j = threadIdx.x; j < cta_cids; j += blockDim.x) {
@@ -291,14 +440,17 @@ __device__ __forceinline__ void screen_epilogue(const ScreenParams& p, ScreenSha
   if (p.nsplit > 1) cluster.sync();  // peers keep their shared memory alive
 }
 
-template <int RR>
-__global__ void __maxnreg__(72) screen_kernel(ScreenParams p) {
+template <int RR, bool HALF>
+__global__ void __maxnreg__(64) screen_kernel(ScreenParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ ScreenShared sh;
   float* rho = reinterpret_cast<float*>(smem);
   const int cta_cids = p.cta_blocks * 32;
-  int32_t* s_term = reinterpret_cast<int32_t*>(rho + cta_cids);
-  float* s_val = reinterpret_cast<float*>(s_term + p.rowcap);
+  // staged row entries {header row t*nblk, value, dense-run start, value},
+  // sorted by dense prefix; then each entry's position and local prefix
+  int4* s_ent = reinterpret_cast<int4*>(rho + cta_cids);
+  uint16_t* s_pos = reinterpret_cast<uint16_t*>(s_ent + p.rowcap);
+  uint8_t* s_lp = reinterpret_cast<uint8_t*>(s_pos + p.rowcap);
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -325,19 +477,74 @@ __global__ void __maxnreg__(72) screen_kernel(ScreenParams p) {
   __syncthreads();
   const uint32_t* __restrict__ masks = static_cast<const uint32_t*>(s_base[0]);
   const uint32_t* __restrict__ offs = static_cast<const uint32_t*>(s_base[1]);
-  const float* __restrict__ pv = static_cast<const float*>(s_base[2]);
+  const void* pv = s_base[2];
   unsigned long long post = 0;  // postings of this CTA's blocks (counters.py:71-81)
 
+  // BIVF spans this CTA touches: gs0 .. gs0+nls-1 (bivf.cuh: 8 blocks each)
+  const int gs0 = (int)(blk0 >> 3);
+  int nls = (int)(((blk0 + p.cta_blocks - 1) >> 3) - gs0 + 1);
+  if (nls > kMaxLocalSpans) nls = kMaxLocalSpans;
+  __shared__ int s_start[kMaxLocalSpans + 1];  // bucket starts (then cursors)
+  __shared__ int s_cntd[kMaxLocalSpans + 1];   // entries whose prefix covers local span s
   int64_t c0 = rb;
   do {
     const int64_t rem = re - c0;
     const int cn = (int)(rem < p.rowcap ? rem : p.rowcap);
     __syncthreads();
+    // Stage the row chunk sorted by the terms' dense prefix (bivf.cuh, dpre),
+    // longest first, stable: for local span s the entries [0, cntd[s]) read
+    // span s as one contiguous 256-value run (no masks, no offsets), the rest
+    // [cntd[s], cn) go through masks + offsets.  (The screen's fp32 sum may run
+    // in any order — its error bound does not depend on it — and the sort is
+    // stable, so the sums are deterministic; the exact rescoring keeps the
+    // reference order.)
+    for (int b = threadIdx.x; b <= nls; b += blockDim.x) s_start[b] = 0;
+    __syncthreads();
     for (int j = threadIdx.x; j < cn; j += blockDim.x) {
-      const int32_t t = p.terms[c0 + j];
-      s_term[j] = t;
-      s_val[j] = p.val32[c0 + j];
+      const uint32_t t = (uint32_t)p.terms[c0 + j];
+      int lp = (int)__ldg(p.dpre + t) - gs0;
+      lp = lp < 0 ? 0 : (lp > nls ? nls : lp);
+      s_lp[j] = (uint8_t)lp;
+      atomicAdd(&s_start[lp], 1);
       if (z == 0) post += __ldg(p.nc + t);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      // bucket starts in descending prefix order (warp scan, 32 buckets a step)
+      int run = 0;
+      for (int b0 = nls; b0 >= 0; b0 -= 32) {
+        const int b = b0 - lane;
+        const int c = b >= 0 ? s_start[b] : 0;
+        int x = c;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int y = __shfl_up_sync(kFull, x, off);
+          if (lane >= off) x += y;
+        }
+        if (b >= 0) {
+          s_start[b] = run + x - c;
+          s_cntd[b] = run + x - c;  // = entries with a longer prefix than b
+        }
+        run += __shfl_sync(kFull, x, 31);
+      }
+      __syncwarp();
+      // stable placement, 32 entries at a time
+      for (int j0 = 0; j0 < cn; j0 += 32) {
+        const int j = j0 + lane;
+        const int lp = j < cn ? (int)s_lp[j] : -1;
+        const unsigned peers = __match_any_sync(kFull, lp);
+        if (j < cn) s_pos[j] = (uint16_t)(s_start[lp] + __popc(peers & lt));
+        __syncwarp();
+        if (j < cn && lane == __ffs(peers) - 1) s_start[lp] += __popc(peers);
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < cn; j += blockDim.x) {
+      const uint32_t row = (uint32_t)p.terms[c0 + j] * (uint32_t)nblk;
+      const int v = __float_as_int(p.val32[c0 + j]);
+      const uint32_t base = s_lp[j] ? (__ldg(offs + row) & ~kDense) : 0u;
+      s_ent[s_pos[j]] = make_int4((int)row, v, (int)base, v);
     }
     __syncthreads();
     const bool first = (c0 == rb);
@@ -348,10 +555,42 @@ __global__ void __maxnreg__(72) screen_kernel(ScreenParams p) {
       for (int r = 0; r < RR; ++r) acc[r] = first ? 0.f : rho[(sp * RR + r) * 32 + lane];
       if (gb < nblk) {  // nblk is a multiple of RR: a span is all in or all out
         // 32-bit row arithmetic: dim * nblk < 2^31 is checked at build time
-        const uint32_t nb32 = (uint32_t)nblk, gb32 = (uint32_t)gb;
+        const uint32_t gb32 = (uint32_t)gb;
+        const int ls = (int)(gb32 >> 3) - gs0;
+        const int nd = ls < nls ? s_cntd[ls] : 0;
+        {
+          // dense-prefix entries: span gb>>3 starts 256*(gb>>3) values into the
+          // term's run; kDepth entries' values in flight, then their FMAs
+          using SV = SpanVals<RR, HALF>;
+          const uint32_t r0 = gb32 & (kSpan - 1);
+          const char* pl =
+              static_cast<const char*>(pv) + SV::lane_bytes(32u * (gb32 - r0), r0, lane);
+          const int2* dl = reinterpret_cast<const int2*>(s_ent) + 1;  // {base, value}
+          constexpr int kDepth = HALF ? 4 : 2;
+          int e = 0;
+          for (; e + kDepth <= nd; e += kDepth) {
+            SV q[kDepth];
+            int2 en[kDepth];
+#pragma unroll
+            for (int u = 0; u < kDepth; ++u) {
+              en[u] = dl[2 * (e + u)];
+              q[u].load_dense(pl + SV::kElem * (uint32_t)en[u].x);
+            }
+#pragma unroll
+            for (int u = 0; u < kDepth; ++u) q[u].fma(__int_as_float(en[u].y), acc);
+          }
+          for (; e < nd; ++e) {
+            SV q;
+            const int2 en = dl[2 * e];
+            q.load_dense(pl + SV::kElem * (uint32_t)en.x);
+            q.fma(__int_as_float(en.y), acc);
+          }
+        }
+        // other terms: masks + offsets, software pipeline (unrolled by two):
+        // values of entries e, e+1 and masks of e+2 in flight while e accumulates
         auto ld = [&](int e, MaskPack<RR>& mk, uint32_t& o) {
           if (e < cn) {
-            const uint32_t row = (uint32_t)s_term[e] * nb32 + gb32;
+            const uint32_t row = (uint32_t)s_ent[e].x + gb32;
             mk.load(masks + row);
             o = __ldg(offs + row);
           } else {
@@ -359,30 +598,20 @@ __global__ void __maxnreg__(72) screen_kernel(ScreenParams p) {
             o = 0u;
           }
         };
-        // software pipeline (unrolled by two): values of entries e, e+1 and
-        // masks of e+2 are in flight while entry e accumulates
-        MaskPack<RR> mk;
-        uint32_t o;
-        float uA[RR], uB[RR];
-        ld(0, mk, o);
-        bool hA = gather_values<RR>(mk, o, gb32, pv, lane, lanebit, lt, uA), hB;
-        ld(1, mk, o);
-        for (int e = 0; e < cn; e += 2) {
-          hB = gather_values<RR>(mk, o, gb32, pv, lane, lanebit, lt, uB);  // entry e+1
-          ld(e + 2, mk, o);
-          // fma(v, 0, acc) == acc exactly: absent postings cost no rounding;
-          // a span the term does not populate skips the FMAs altogether
-          if (hA) {
-            const float vA = s_val[e];
-#pragma unroll
-            for (int r = 0; r < RR; ++r) acc[r] = fmaf(vA, uA[r], acc[r]);
-          }
-          hA = gather_values<RR>(mk, o, gb32, pv, lane, lanebit, lt, uA);  // entry e+2
-          ld(e + 3, mk, o);
-          if (hB) {
-            const float vB = s_val[e + 1];
-#pragma unroll
-            for (int r = 0; r < RR; ++r) acc[r] = fmaf(vB, uB[r], acc[r]);
+        if (nd < cn) {
+          MaskPack<RR> mk;
+          uint32_t o;
+          ld(nd, mk, o);
+          SpanVals<RR, HALF> A, B;
+          A.gather(mk, o, gb32, pv, lane, lanebit, lt);
+          ld(nd + 1, mk, o);
+          for (int e = nd; e < cn; e += 2) {
+            B.gather(mk, o, gb32, pv, lane, lanebit, lt);  // entry e+1
+            ld(e + 2, mk, o);
+            A.fma(&s_ent[e].y, acc);
+            A.gather(mk, o, gb32, pv, lane, lanebit, lt);  // entry e+2
+            ld(e + 3, mk, o);
+            B.fma(&s_ent[e + 1].y, acc);  // e+1 may be cn: read only if present
           }
         }
       }
@@ -1056,10 +1285,11 @@ int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
     // cluster once it passes ~24 KB, so at least two CTAs stay resident per
     // SM, but never below 24 KB per CTA nor above 100 KB.
     const int64_t rho = nblk * 128;
-    int64_t b = rho / 2 + 8 * 1024;
+    const int64_t stg = (int64_t)rowcap * (rr < 0 ? 8 : kEntryBytes);
+    int64_t b = rho / 2 + (stg > 8 * 1024 ? stg : 8 * 1024);
     if (b < 24 * 1024) b = 24 * 1024;
     if (b > 100 * 1024) b = 100 * 1024;
-    if (rho + (int64_t)rowcap * 8 <= 24 * 1024) b = kSmemLimit - 2048;
+    if (rho + stg <= 24 * 1024) b = kSmemLimit - 2048;
     smem_limit = (int)b;
   }
   if (rr == -8 || rr == -4) {  // TMA (-8) / cp.async (-4) pipelined screens, 8-block spans
@@ -1092,7 +1322,7 @@ int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
   pl.mode = 0;
   pl.rr = rr > 0 ? rr : (nblk >= 32 ? 8 : 2);
   pl.rowcap = rowcap;
-  const size_t stage = (size_t)rowcap * 8;
+  const size_t stage = (size_t)rowcap * kEntryBytes;
   pl.nsplit = 0;
   for (int s = 1; s <= kMaxSplit; ++s) {
     int64_t cb = (nblk + s - 1) / s;
@@ -1119,7 +1349,9 @@ int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
 template <int RR>
 int launch_screen(const Plan& pl, const ScreenParams& p, cudaStream_t st) {
   auto fn = pl.mode == 1 ? screen_tma_kernel
-                         : (pl.mode == 2 ? screen_async_kernel : screen_kernel<RR>);
+                         : (pl.mode == 2 ? screen_async_kernel
+                                         : (p.half ? screen_kernel<RR, true>
+                                                   : screen_kernel<RR, false>));
   IVFKM_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(p.n_obj * pl.nsplit));
@@ -1226,7 +1458,8 @@ struct AssignArgs {
   const double* xnorm;
   int64_t k, dim;
   const uint32_t* headers;
-  const float* pval32;
+  const void* pval_screen;
+  int screen_bits;
   const double* pval64;
   double mu_max;
   ivfkm_stats* stats;
@@ -1237,6 +1470,7 @@ int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
   Plan pl;
   int rc = plan_screen(a.k, g_rowcap, g_smem_limit, g_rr, &pl);
   if (rc) return rc;
+  if (pl.tma && a.screen_bits != 32) return IVFKM_E_UNSUPPORTED;  // staged screens: fp32 only
   ScreenParams sp;
   sp.n_obj = a.n_obj;
   sp.row_ptr = a.row_ptr;
@@ -1249,8 +1483,10 @@ int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
   sp.offs = a.headers + a.dim * sp.nblk;
   sp.nc = a.headers + 2 * a.dim * sp.nblk + 1;
   sp.inv = reinterpret_cast<const int32_t*>(sp.nc + a.dim) + a.k;
+  sp.dpre = reinterpret_cast<const uint32_t*>(sp.inv + a.k);
   sp.order = a.order;
-  sp.pv32 = a.pval32;
+  sp.pv32 = static_cast<const float*>(a.pval_screen);
+  sp.half = a.screen_bits == 16;
   sp.mu_max = a.mu_max > 0 ? a.mu_max : 1.0;
   sp.cta_blocks = pl.cta_blocks;
   sp.nsplit = pl.nsplit;
@@ -1304,10 +1540,14 @@ int finish_impl(const AssignArgs& a, const AssignWs& w, const int32_t* prev_labe
 
 extern "C" int ivfkm_assign_screen(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
                                    const float* val32, const double* xnorm, int64_t k,
-                                   int64_t dim, const uint32_t* headers, const float* pval32,
-                                   double mu_max, ivfkm_stats* stats, const int32_t* order,
-                                   void* ws, size_t ws_bytes, ivfkm_stream_t stream_) {
+                                   int64_t dim, const uint32_t* headers, const void* pval_screen,
+                                   int screen_bits, double mu_max, ivfkm_stats* stats,
+                                   const int32_t* order, void* ws, size_t ws_bytes,
+                                   ivfkm_stream_t stream_) {
   if (n_obj < 0 || k < 1 || dim < 1 || !row_ptr || !stats || !headers) return IVFKM_E_ARG;
+  if (screen_bits != 32 && screen_bits != 16) return IVFKM_E_ARG;
+  // fp16 holds mean values up to 65504; unit-norm means are far inside
+  if (screen_bits == 16 && !(mu_max <= 32768.0)) return IVFKM_E_UNSUPPORTED;
   if (n_obj > INT32_MAX || k > INT32_MAX) return IVFKM_E_UNSUPPORTED;
   size_t need = 0;
   AssignWs w = carve_assign(ws, n_obj, &need);
@@ -1316,8 +1556,8 @@ extern "C" int ivfkm_assign_screen(int64_t n_obj, const int64_t* row_ptr, const 
   IVFKM_TRY(cudaMemsetAsync(stats, 0, sizeof(ivfkm_stats), st));
   IVFKM_TRY(cudaMemsetAsync(w.ovf_len, 0, sizeof(unsigned int), st));
   if (n_obj == 0) return IVFKM_OK;
-  AssignArgs a{n_obj, row_ptr, terms, val32, nullptr, xnorm, k, dim, headers, pval32, nullptr,
-               mu_max, stats, order};
+  AssignArgs a{n_obj,   row_ptr,     terms,       val32,   nullptr, xnorm, k, dim,
+               headers, pval_screen, screen_bits, nullptr, mu_max,  stats, order};
   return screen_impl(a, w, st);
 }
 
@@ -1335,20 +1575,22 @@ extern "C" int ivfkm_assign_finish(int64_t n_obj, const int64_t* row_ptr, const 
   cudaStream_t st = as_stream(stream_);
   if (sizes) IVFKM_TRY(cudaMemsetAsync(sizes, 0, sizeof(unsigned long long) * k, st));
   if (n_obj == 0) return IVFKM_OK;
-  AssignArgs a{n_obj, row_ptr, terms, nullptr, val64, nullptr, k, dim, headers, nullptr, pval64,
-               0.0, stats, nullptr};
+  AssignArgs a{n_obj,   row_ptr, terms, nullptr, val64, nullptr, k,      dim,
+               headers, nullptr, 32,    pval64,  0.0,   stats,   nullptr};
   return finish_impl(a, w, prev_labels, labels, sims, sizes, st);
 }
 
 extern "C" int ivfkm_assign(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
                             const float* val32, const double* val64, const double* xnorm,
-                            int64_t k, int64_t dim, const uint32_t* headers, const float* pval32,
-                            const double* pval64, double mu_max, const int32_t* prev_labels,
+                            int64_t k, int64_t dim, const uint32_t* headers,
+                            const void* pval_screen, int screen_bits, const double* pval64,
+                            double mu_max, const int32_t* prev_labels,
                             int32_t* labels, double* sims, unsigned long long* sizes,
                             ivfkm_stats* stats, const int32_t* order, void* ws, size_t ws_bytes,
                             ivfkm_stream_t stream_) {
-  int rc = ivfkm_assign_screen(n_obj, row_ptr, terms, val32, xnorm, k, dim, headers, pval32,
-                               mu_max, stats, order, ws, ws_bytes, stream_);
+  int rc = ivfkm_assign_screen(n_obj, row_ptr, terms, val32, xnorm, k, dim, headers,
+                               pval_screen, screen_bits, mu_max, stats, order, ws, ws_bytes,
+                               stream_);
   if (rc) return rc;
   return ivfkm_assign_finish(n_obj, row_ptr, terms, val64, k, dim, headers, pval64, prev_labels,
                              labels, sims, sizes, stats, ws, ws_bytes, stream_);

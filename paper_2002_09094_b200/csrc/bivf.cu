@@ -14,6 +14,8 @@
 // Build (no sort needed): atomicOr the masks; count each span (padded to a
 // multiple of 4 values); exclusive-scan into offsets, flag dense spans;
 // scatter each value to its slot; per-term posting counts.
+#include <cuda_fp16.h>
+
 #include <cub/cub.cuh>
 
 #include "bivf.cuh"
@@ -43,6 +45,7 @@ struct BivfWs {
 // build options (ivfkm_set_bivf_options)
 float g_dense_fill = 0.25f;  // spans with >= fill*256 postings are stored dense
 int g_permute = 1;          // slots ordered by mean size
+int g_use_dpre = 1;  // (experiment switch, permute bit 1)
 
 uint32_t dense_threshold() {
   if (g_dense_fill > 1.0f) return 1u << 30;  // never
@@ -112,7 +115,7 @@ __global__ void bivf_mask_kernel(int major, int64_t nrows, const int64_t* __rest
 }
 
 // One thread per (term, span): popcounts of its 8 blocks, the span total
-// padded to a multiple of 4 values on the last block.
+// padded to a multiple of 8 values on the last block (16 B of fp16 values).
 __global__ void bivf_count_kernel(int64_t nh, const unsigned int* __restrict__ masks,
                                   unsigned int dense_th, unsigned int* __restrict__ cnt) {
   const int64_t nspan = nh / kSpan;
@@ -131,7 +134,7 @@ __global__ void bivf_count_kernel(int64_t nh, const unsigned int* __restrict__ m
     const bool dense = tot >= dense_th;
 #pragma unroll
     for (int r = 0; r < kSpan; ++r) cnt[sp * kSpan + r] = dense ? 32u : c[r];
-    if (!dense) cnt[sp * kSpan + kSpan - 1] += (4u - (tot & 3u)) & 3u;
+    if (!dense) cnt[sp * kSpan + kSpan - 1] += (8u - (tot & 7u)) & 7u;
   }
 }
 
@@ -160,7 +163,7 @@ __global__ void bivf_scatter_kernel(int major, int64_t nrows, const int64_t* __r
                                     const double* __restrict__ vals, int64_t k, int64_t dim,
                                     int64_t nblk, const unsigned int* __restrict__ hdr,
                                     const int32_t* __restrict__ perm,
-                                    float* __restrict__ v32, double* __restrict__ v64) {
+                                    float* __restrict__ v32, double* __restrict__ v64, int half) {
   const int64_t nnz = ptr[nrows];
   const int64_t nh = bivf_nh(dim, nblk);
   BivfView view{nblk, hdr, hdr + nh, perm};
@@ -173,18 +176,24 @@ __global__ void bivf_scatter_kernel(int major, int64_t nrows, const int64_t* __r
     if (c < 0 || c >= k || t < 0 || t >= dim) continue;
     const int64_t pos = bivf_find(view, t, c);
     const double v = vals[q];
-    v32[pos] = static_cast<float>(v);
+    if (half) {
+      reinterpret_cast<__half*>(v32)[bivf_find16(view, t, c)] = __double2half(v);
+    } else {
+      v32[pos] = static_cast<float>(v);
+    }
     v64[pos] = v;
   }
 }
 
 // absent slots of dense spans (and padding) hold exact zeros: clear [0, total)
-__global__ void bivf_zero_kernel(const unsigned int* __restrict__ total, float* __restrict__ v32,
-                                 double* __restrict__ v64) {
+// (the total is a multiple of 8, so the fp16 array is n/2 whole 32-bit words)
+__global__ void bivf_zero_kernel(const unsigned int* __restrict__ total, float* __restrict__ vs,
+                                 int half, double* __restrict__ v64) {
   const int64_t n = *total;
+  const int64_t ns = half ? n / 2 : n;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    v32[i] = 0.f;
+    if (i < ns) vs[i] = 0.f;
     v64[i] = 0.0;
   }
 }
@@ -229,16 +238,33 @@ __global__ void bivf_perm_kernel(int64_t k, const int32_t* __restrict__ sorted,
 }
 
 // postings per term: nc[t] = sum_b popc(masks[t][b])
+// One warp per term: postings (nc) and the dense prefix (dpre, bivf.cuh).
 __global__ void bivf_nc_kernel(int64_t dim, int64_t nblk, const unsigned int* __restrict__ masks,
-                               unsigned int* __restrict__ nc) {
+                               const unsigned int* __restrict__ offs,
+                               unsigned int* __restrict__ nc, unsigned int* __restrict__ dpre,
+                               int use_dpre) {
   const int lane = threadIdx.x & 31;
   const int64_t wpb = blockDim.x >> 5;
+  const int64_t nspan = nblk / kSpan;
   for (int64_t t = blockIdx.x * wpb + (threadIdx.x >> 5); t < dim; t += gridDim.x * wpb) {
     unsigned c = 0;
     for (int64_t b = lane; b < nblk; b += 32) c += __popc(masks[t * nblk + b]);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
-    if (lane == 0) nc[t] = c;
+    int64_t pre = nspan;
+    for (int64_t s0 = 0; s0 < nspan; s0 += 32) {
+      const int64_t s = s0 + lane;
+      const bool sparse = s < nspan && !(offs[t * nblk + s * kSpan] & kDense);
+      const unsigned m = __ballot_sync(0xffffffffu, sparse);
+      if (m) {
+        pre = s0 + __ffs(m) - 1;
+        break;
+      }
+    }
+    if (lane == 0) {
+      nc[t] = c;
+      dpre[t] = use_dpre ? (unsigned)pre : 0u;
+    }
   }
 }
 
@@ -251,25 +277,32 @@ extern "C" size_t ivfkm_bivf_workspace_size(int64_t dim, int64_t k) {
 }
 
 extern "C" void ivfkm_set_bivf_options(float dense_fill, int permute) {
-  if ((dense_fill >= 0.25f && dense_fill <= 1.0f) || dense_fill > 1.0f) g_dense_fill = dense_fill;
-  if (permute == 0 || permute == 1) g_permute = permute;
+  if (dense_fill >= 1.0f / 32.0f) g_dense_fill = dense_fill;
+  if (permute >= 0 && permute <= 3) { g_permute = permute & 1; g_use_dpre = !(permute & 2); }
 }
 
 extern "C" int64_t ivfkm_bivf_headers_size(int64_t k, int64_t dim) {
-  return 2 * bivf_nh(dim, ivfkm_bivf_nblk(k)) + 1 + dim + 2 * k;
+  return 2 * bivf_nh(dim, ivfkm_bivf_nblk(k)) + 1 + dim + 2 * k + dim;
 }
 
 extern "C" int64_t ivfkm_bivf_values_capacity(int64_t k, int64_t dim, int64_t nnz) {
   const double f = g_dense_fill > 1.0f ? 1.0 : (double)g_dense_fill;
-  return (int64_t)((double)nnz / f) + 3 * dim * (ivfkm_bivf_nblk(k) / kSpan) + 256 + 4;
+  const int64_t nblk = ivfkm_bivf_nblk(k);
+  // dense spans hold 256 values each; no layout exceeds every span dense
+  const int64_t by_fill = (int64_t)((double)nnz / f) + 7 * dim * (nblk / kSpan);
+  const int64_t all_dense = dim * nblk * 32;
+  return (by_fill < all_dense ? by_fill : all_dense) + 256 + 8;
 }
 
 extern "C" int ivfkm_bivf_build(int64_t k, int64_t dim, int major, int64_t nrows,
                                 const int64_t* ptr, const int32_t* cols, const double* vals,
-                                uint32_t* headers, float* val32, double* val64, void* ws,
-                                size_t ws_bytes, ivfkm_stream_t stream_) {
+                                uint32_t* headers, void* val_screen, int screen_bits,
+                                double* val64, void* ws, size_t ws_bytes,
+                                ivfkm_stream_t stream_) {
   if (k < 1 || dim < 1 || nrows < 0 || (major != 0 && major != 1) || !ptr || !headers)
     return IVFKM_E_ARG;
+  if (screen_bits != 32 && screen_bits != 16) return IVFKM_E_ARG;
+  float* val32 = static_cast<float*>(val_screen);  // or fp16 values (screen_bits 16)
   if (k > INT32_MAX) return IVFKM_E_UNSUPPORTED;
   const int64_t nblk = ivfkm_bivf_nblk(k);
   const int64_t nh = bivf_nh(dim, nblk);
@@ -281,6 +314,7 @@ extern "C" int ivfkm_bivf_build(int64_t k, int64_t dim, int major, int64_t nrows
   uint32_t* nc = headers + 2 * nh + 1;
   int32_t* perm = reinterpret_cast<int32_t*>(nc + dim);
   int32_t* inv = perm + k;
+  uint32_t* dpre = reinterpret_cast<uint32_t*>(inv + k);
   const unsigned th = dense_threshold();
   const int threads = 256;
   // ---- slot order: means by term count, descending (stable)
@@ -315,12 +349,16 @@ extern "C" int ivfkm_bivf_build(int64_t k, int64_t dim, int major, int64_t nrows
   bivf_offset_kernel<<<grid_for(nh / kSpan + 1, threads), threads, 0, st>>>(nh, w.off, th,
                                                                            headers);
   IVFKM_CHECK_LAUNCH();
-  bivf_zero_kernel<<<kNumSM * 16, threads, 0, st>>>(w.off + nh, val32, val64);
+  bivf_zero_kernel<<<kNumSM * 16, threads, 0, st>>>(w.off + nh, val32, screen_bits == 16,
+                                                     val64);
   IVFKM_CHECK_LAUNCH();
   bivf_scatter_kernel<<<kNumSM * 8, threads, 0, st>>>(major, nrows, ptr, cols, vals, k, dim,
-                                                      nblk, headers, perm, val32, val64);
+                                                      nblk, headers, perm, val32, val64,
+                                                      screen_bits == 16);
   IVFKM_CHECK_LAUNCH();
-  bivf_nc_kernel<<<grid_for(dim, threads / 32), threads, 0, st>>>(dim, nblk, headers, nc);
+  bivf_nc_kernel<<<grid_for(dim, threads / 32), threads, 0, st>>>(dim, nblk, headers,
+                                                                 headers + nh, nc, dpre,
+                                                                 g_use_dpre);
   IVFKM_CHECK_LAUNCH();
   return IVFKM_OK;
 }

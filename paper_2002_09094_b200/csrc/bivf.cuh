@@ -13,8 +13,13 @@
 //   offs [dim*nblk]          padded total (size of the value arrays in use)
 //   nc   [t]                 postings of term t (= centroid_freq, means.py:144-147)
 //   perm [k], inv [k]        mean -> slot, slot -> mean
+//   dpre [t]                 dense prefix: t's first dpre[t] spans are all dense,
+//                            so their values are one contiguous run — span s at
+//                            (offs[t*nblk] & ~kDense) + 256*s — and the screen
+//                            reads them without masks or offsets
 // Blocks are grouped in spans of 8 (256 slots).  Every span's value segment
-// is padded to a multiple of 4 values (16 B), so a span start is 16-B aligned.
+// is padded to a multiple of 8 values, so a span start is 16-B aligned in
+// both the fp32 and the fp16 screen arrays.
 // A span holding at least dense_fill*256 postings is stored *dense*: all 256
 // values (0.0 for absent slots) lane-major in two halves (slot 32*(b0+r)+j at
 // span_base + 128*(r/4) + 4*j + r%4), so a warp lane owning slots
@@ -24,6 +29,9 @@
 // FMAs and the fp64 rescoring (which still consults the true masks).  Other
 // spans keep the reference order (term-major, mean ascending,
 // means.py:169-179, in slot order).
+// The fp16 screen array (screen_bits = 16) uses the same positions except
+// inside dense spans, where each lane's 8 values are contiguous (slot
+// 32*(b0+r)+j at span_base + 8*j + r: one 16-B load per lane and span).
 #pragma once
 #include <cstdint>
 
@@ -54,6 +62,26 @@ __device__ __forceinline__ int64_t bivf_find_slot(const BivfView& v, int64_t t, 
                      (r & 3u));
   }
   return (int64_t)(o + (uint32_t)__popc(m & (bit - 1u)));
+}
+
+// Position of slot s's value in the 16-bit screen array: sparse spans as
+// above; a dense span keeps each lane's 8 values contiguous (one 16-B load):
+// slot 32*(b0+r)+j at span_base + 8*j + r.
+__device__ __forceinline__ int64_t bivf_find16_slot(const BivfView& v, int64_t t, int64_t s) {
+  const int64_t b = s >> 5;
+  const uint32_t bit = 1u << (s & 31);
+  const uint32_t m = __ldg(v.masks + t * v.nblk + b);
+  if (!(m & bit)) return -1;
+  const uint32_t o = __ldg(v.offs + t * v.nblk + b);
+  if (o & kDense) {
+    const uint32_t r = (uint32_t)(b & (kSpan - 1));
+    return (int64_t)((o & ~kDense) - 32u * r + 8u * (uint32_t)(s & 31) + r);
+  }
+  return (int64_t)(o + (uint32_t)__popc(m & (bit - 1u)));
+}
+
+__device__ __forceinline__ int64_t bivf_find16(const BivfView& v, int64_t t, int64_t c) {
+  return bivf_find16_slot(v, t, v.perm ? (int64_t)__ldg(v.perm + c) : c);
 }
 
 // Position of mean c's value for term t, or -1.

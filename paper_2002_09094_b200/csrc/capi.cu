@@ -126,13 +126,16 @@ extern "C" int ivfkm_assign_ivf_host(int64_t n, const int64_t* indptr, const int
   IVFKM_TRY(cudaMemcpyAsync(d_mp.p, m_indptr, sizeof(int64_t) * (dim + 1), cudaMemcpyHostToDevice, st));
   IVFKM_TRY(cudaMemcpyAsync(d_mc.p, c0.data(), sizeof(int32_t) * mnz, cudaMemcpyHostToDevice, st));
   IVFKM_TRY(cudaMemcpyAsync(d_mv.p, m_vals, sizeof(double) * mnz, cudaMemcpyHostToDevice, st));
+  // fp16 screen values (half the posting bytes) unless the means are not
+  // normalised far beyond unit norm (fp16 range)
+  const int bits = mu_max <= 32768.0 ? 16 : 32;
   int rc = ivfkm_bivf_build(k, dim, 1, dim, d_mp.as<int64_t>(), d_mc.as<int32_t>(),
-                            d_mv.as<double>(), d_hdr.as<uint32_t>(), d_p32.as<float>(),
+                            d_mv.as<double>(), d_hdr.as<uint32_t>(), d_p32.p, bits,
                             d_p64.as<double>(), d_bws.p, bws, nullptr);
   if (rc) return rc;
   rc = ivfkm_assign(n, d_ip.as<int64_t>(), d_t.as<int32_t>(), d_v32.as<float>(),
                     d_v64.as<double>(), d_xn.as<double>(), k, dim, d_hdr.as<uint32_t>(),
-                    d_p32.as<float>(), d_p64.as<double>(), mu_max, nullptr, d_lab.as<int32_t>(),
+                    d_p32.p, bits, d_p64.as<double>(), mu_max, nullptr, d_lab.as<int32_t>(),
                     d_sims.as<double>(), d_sizes.as<unsigned long long>(),
                     d_stats.as<ivfkm_stats>(), nullptr, d_aws.p, aws, nullptr);
   if (rc) return rc;

@@ -121,7 +121,8 @@ class DeviceMeans:
         self.k, self.dim = int(k), int(dim)
         self.ptr, self.terms, self.vals, self.retained = ptr, terms, vals, retained
         self.nnz = int(terms.numel())
-        self.headers = self.pv32 = self.pv64 = None
+        self.headers = self.pvs = self.pv64 = None
+        self.screen_bits = 32  # precision of pvs (the screen's values), set by build_bivf
 
     @classmethod
     def from_meanset(cls, ms, device="cuda") -> "DeviceMeans":
@@ -178,9 +179,12 @@ def update_rows(lib, n_obj, nnz, row_ptr, terms, val64, labels0, sizes, prev: De
 class LloydEngine:
     """Runs IVF Lloyd iterations over one device-resident dataset."""
 
-    def __init__(self, dd: DeviceDataset, k: int):
+    def __init__(self, dd: DeviceDataset, k: int, screen_bits: int = 16):
         self.lib = _lib.load()
         self.dd, self.k = dd, int(k)
+        # fp16 screen values: half the posting bytes, a wider (still rigorous)
+        # error window, labels unchanged (DESIGN.md §3); 32 = fp32 screen
+        self.screen_bits = screen_bits
         dev = dd.device
         self.device = dev
         n, nnz, dim = dd.n, dd.nnz, dd.dim
@@ -220,11 +224,15 @@ class LloydEngine:
         dm.headers = torch.empty(int(self.lib.ivfkm_bivf_headers_size(self.k, dm.dim)),
                                  dtype=torch.int32, device=dev)
         cap = int(self.lib.ivfkm_bivf_values_capacity(self.k, dm.dim, dm.nnz))
-        dm.pv32 = torch.empty(cap, dtype=torch.float32, device=dev)
+        bits = self.screen_bits
+        dm.pvs = torch.empty(cap, dtype=torch.float16 if bits == 16 else torch.float32,
+                             device=dev)
         dm.pv64 = torch.empty(cap, dtype=torch.float64, device=dev)
         rc = self.lib.ivfkm_bivf_build(self.k, dm.dim, 0, self.k, _p(dm.ptr), _p(dm.terms),
-                                       _p(dm.vals), _p(dm.headers), _p(dm.pv32), _p(dm.pv64),
-                                       _p(self.ws_bivf), self.ws_bivf.numel(), _stream())
+                                       _p(dm.vals), _p(dm.headers), _p(dm.pvs), bits,
+                                       _p(dm.pv64), _p(self.ws_bivf), self.ws_bivf.numel(),
+                                       _stream())
+        dm.screen_bits = bits
         _lib.check(rc, "ivfkm_bivf_build")
         # sizes, CUB sort of the k slot keys (single tile / onesweep), perm, mask,
         # count, scan (init + sweep), offset, zero, scatter, nc
@@ -253,7 +261,8 @@ class LloydEngine:
             events[0].record()
         rc = self.lib.ivfkm_assign_screen(dd.n, _p(dd.row_ptr), _p(dd.terms), _p(dd.val32),
                                           _p(dd.xnorm), self.k, dd.dim, _p(dm.headers),
-                                          _p(dm.pv32), _MU_MAX, _p(self.stats), _p(order),
+                                          _p(dm.pvs), dm.screen_bits, _MU_MAX, _p(self.stats),
+                                          _p(order),
                                           _p(self.ws_assign), self.ws_assign.numel(), st)
         _lib.check(rc, "ivfkm_assign_screen")
         if events is not None:

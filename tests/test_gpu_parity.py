@@ -185,19 +185,24 @@ def tuning():
     lib.ivfkm_set_tuning(1024, -1, 0)
 
 
-def _assign_raw(ds, means, rowcap=None, smem=None, rr=-1):
+def _assign_raw(ds, means, rowcap=None, smem=None, rr=-1, bits=None):
     """Assign through the engine with explicit tuning (rowcap applies per call;
-    rr = 0 selects the TMA-pipelined screen, 2/4/8 the LDG screen)."""
+    rr = 0 automatic LDG screen, 2/4/8 LDG screen with that span, -8 / -4 the
+    TMA / cp.async staged screens, which take fp32 screen values only)."""
     from paper_2002_09094_b200.variants import engine_for
 
     eng = engine_for(ds, means.k)
     if rowcap:
         eng.rowcap = rowcap
+    eng.screen_bits = bits or (32 if rr < 0 else 16)
     eng.lib.ivfkm_set_tuning(eng.rowcap, smem or 0, rr)
-    dm = eng.upload_means(means)
-    lab = eng.assign(dm, None)
-    st = eng.read_stats()
-    eng.rowcap = max(32, min(512, (eng.dd.max_row + 31) // 32 * 32))
+    try:
+        dm = eng.upload_means(means)
+        lab = eng.assign(dm, None)
+        st = eng.read_stats()
+    finally:
+        eng.rowcap = max(32, min(512, (eng.dd.max_row + 31) // 32 * 32))
+        eng.screen_bits = 16
     return lab.cpu().numpy() + 1, st
 
 
@@ -218,46 +223,80 @@ def _random_case(n=1500, dim=400, k=64, seed=0, signed=False, corpus=0):
     return ds, om, means
 
 
-@pytest.mark.parametrize("rr", [0, -8, -4, 2])
+SCREENS = [(0, 16), (0, 32), (-8, 32), (-4, 32), (2, 16), (2, 32)]
+
+
+@pytest.mark.parametrize("rr,bits", SCREENS)
 @pytest.mark.parametrize("seed,k,signed", [(0, 64, False), (1, 300, False), (2, 1000, True),
                                            (3, 5, False), (4, 1, False)])
-def test_assign_matches_oracle_exactly(tuning, seed, k, signed, rr):
+def test_assign_matches_oracle_exactly(tuning, seed, k, signed, rr, bits):
     from oracle import oracle as O
 
     ds, om, means = _random_case(k=max(k, 1), seed=seed, signed=signed)
-    labels, st = _assign_raw(ds, means, rr=rr)
+    labels, st = _assign_raw(ds, means, rr=rr, bits=bits)
     ol, _, _, post = O.assign(ds, om)
     assert np.array_equal(labels, ol)
     assert st.postings == post == O.volume_ivf(ds, om)
     assert st.objective == O.objective(ds, ol, om)
 
 
-@pytest.mark.parametrize("rr", [0, -8, -4])
+@pytest.mark.parametrize("rr,bits", SCREENS[:4])
 @pytest.mark.parametrize("rowcap,corpus", [(32, 0), (64, 1)])
-def test_multipass_rows(tuning, rowcap, corpus, rr):
+def test_multipass_rows(tuning, rowcap, corpus, rr, bits):
     """Rows longer than the shared-memory stage run in several passes."""
     from oracle import oracle as O
 
     ds, om, means = _random_case(seed=5, k=200, corpus=corpus)
     assert int(np.diff(ds.indptr).max()) > rowcap
-    labels, st = _assign_raw(ds, means, rowcap=rowcap, rr=rr)
+    labels, st = _assign_raw(ds, means, rowcap=rowcap, rr=rr, bits=bits)
     ol, _, _, post = O.assign(ds, om)
     assert np.array_equal(labels, ol) and st.postings == post
 
 
 @pytest.mark.parametrize("k,smem,rr", [(1000, 25 * 1024, -8), (1500, 12 * 1024, -8),
                                        (1000, 25 * 1024, -4), (1500, 12 * 1024, -4),
-                                       (1000, 3 * 1024, 0), (1500, 2 * 1024, 0)])
-def test_cluster_split_dsmem(tuning, k, smem, rr):
+                                       (1000, 3 * 1024, 0), (1500, 2560, 0)])
+@pytest.mark.parametrize("bits", [16, 32])
+def test_cluster_split_dsmem(tuning, k, smem, rr, bits):
     """Force the thread-block-cluster split (rho spread over 2-8 CTAs' shared
     memory, argmax and candidate window merged over DSMEM)."""
     from oracle import oracle as O
 
     ds, om, means = _random_case(seed=6, k=k, n=2500)
-    labels, st = _assign_raw(ds, means, rowcap=64, smem=smem, rr=rr)
+    if rr < 0 and bits == 16:
+        pytest.skip("the staged screens take fp32 screen values only")
+    labels, st = _assign_raw(ds, means, rowcap=64, smem=smem, rr=rr, bits=bits)
     ol, _, _, post = O.assign(ds, om)
     assert np.array_equal(labels, ol) and st.postings == post
     assert st.objective == O.objective(ds, ol, om)
+
+
+@pytest.mark.parametrize("signed", [False, True])
+def test_fp16_screen_tiny_and_wide_values(tuning, signed):
+    """fp16 screen values over six decades of magnitude (many below fp16's
+    normal range, 6.1e-5): the window's absolute term must still cover them."""
+    from oracle import oracle as O
+
+    P = _pkg()
+    rng = np.random.default_rng(11 + signed)
+    n, dim, k = 3000, 600, 300
+    lens = rng.integers(1, 120, n)
+    ip = np.zeros(n + 1, np.int64)
+    np.cumsum(lens, out=ip[1:])
+    t = np.concatenate([np.sort(rng.choice(dim, m, replace=False)) + 1 for m in lens])
+    v = 10.0 ** rng.uniform(-7, 0, ip[-1])
+    if signed:
+        v *= np.where(rng.random(v.size) < 0.5, -1.0, 1.0)
+    for i in range(n):
+        v[ip[i]:ip[i + 1]] /= np.sqrt(np.sum(v[ip[i]:ip[i + 1]] ** 2))
+    ds = P.Dataset(dim, ip, t.astype(np.int32), v, normalized=True)
+    om = O.init_means(ds, k, 3)
+    means = P.MeanSet.from_csr(om.indptr, om.term_ids, om.values, dim, "sparse_inverted")
+    ol, _, _, post = O.assign(ds, om)
+    for bits in (16, 32):
+        labels, st = _assign_raw(ds, means, bits=bits)
+        assert np.array_equal(labels, ol) and st.postings == post
+        assert st.objective == O.objective(ds, ol, om)
 
 
 def test_exact_ties_overflow_path():
@@ -355,3 +394,45 @@ def test_host_iteration_end_to_end_matches_oracle():
         assert np.array_equal(means.values, m.values) and np.array_equal(means.term_ids, m.term_ids)
         P.MeanSet(means.k, means.dim, means.representation, means.indptr, means.term_ids,
                   means.values, means.retained)  # the trusted wrap passes full validation
+
+
+@pytest.mark.parametrize("bits", [16, 32])
+@pytest.mark.parametrize("fill", [0.25, 1.0 / 32])
+def test_bivf_build_stays_within_capacity(bits, fill):
+    """The build writes only [0, total) of each value array, total <=
+    ivfkm_bivf_values_capacity: guard bytes past the capacity stay intact."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2002_09094_b200 import _lib
+    from paper_2002_09094_b200.engine import _p
+
+    ds, om, means = _random_case(seed=7, k=700, n=3000)
+    lib = _lib.load()
+    lib.ivfkm_set_bivf_options(fill, 1)
+    try:
+        dev = torch.device("cuda")
+        k, dim = means.k, ds.dim
+        ptr = torch.from_numpy(np.asarray(means.indptr, np.int64)).to(dev)
+        terms = torch.from_numpy(np.asarray(means.term_ids, np.int32) - 1).to(dev)
+        vals = torch.from_numpy(np.asarray(means.values, np.float64)).to(dev)
+        cap = int(lib.ivfkm_bivf_values_capacity(k, dim, terms.numel()))
+        guard = 4096
+        esz = bits // 8
+        vs = torch.full(((cap + guard) * esz,), 0x5A, dtype=torch.uint8, device=dev)
+        v64 = torch.full(((cap + guard) * 8,), 0x5A, dtype=torch.uint8, device=dev)
+        hdr = torch.empty(int(lib.ivfkm_bivf_headers_size(k, dim)), dtype=torch.int32,
+                          device=dev)
+        ws = torch.empty(int(lib.ivfkm_bivf_workspace_size(dim, k)), dtype=torch.uint8,
+                         device=dev)
+        rc = lib.ivfkm_bivf_build(k, dim, 0, k, _p(ptr), _p(terms), _p(vals), _p(hdr), _p(vs),
+                                  bits, _p(v64), _p(ws), ws.numel(), C.c_void_p(0))
+        _lib.check(rc, "ivfkm_bivf_build")
+        torch.cuda.synchronize()
+        nh = dim * int(lib.ivfkm_bivf_nblk(k))
+        total = int(hdr[2 * nh].item()) & 0xFFFFFFFF
+        assert total <= cap
+        assert bool((vs[cap * esz:] == 0x5A).all()) and bool((v64[cap * 8:] == 0x5A).all())
+    finally:
+        lib.ivfkm_set_bivf_options(0.25, 1)

@@ -34,10 +34,11 @@ def main():
     ap.add_argument("--permute", default="1")
     ap.add_argument("--smem", default="0", help="shared-memory budgets per CTA (0 = default)")
     ap.add_argument("--order", default="none", help="none,label: object processing order")
+    ap.add_argument("--bits", type=int, default=16, help="screen value precision (16 or 32)")
     args = ap.parse_args()
     c = synth.CONFIGS[args.config]
     ds = synth.make_dataset(c["corpus"])
-    eng = LloydEngine(DeviceDataset(HostDataset(ds), "cuda"), c["k"])
+    eng = LloydEngine(DeviceDataset(HostDataset(ds), "cuda"), c["k"], screen_bits=args.bits)
     dm = eng.upload_means(init_means(ds, c["k"], c["seed"], "sparse_inverted"))
     prev = None
     for _ in range(args.iters):
@@ -76,9 +77,11 @@ def main():
                 torch.cuda.synchronize()
                 times.append(ev[0].elapsed_time(ev[1]))
             ok = bool(torch.equal(lab, base))
+            st2 = eng.read_stats()
             ms = min(times)
-            rec = {"order": oname, "fill": fill, "permute": perm, "smem": smem, "rr": rr, "rowcap": rowcap, "screen_ms": ms,
-                   "postings_per_s": st.postings / (ms / 1e3), "labels_ok": ok}
+            rec = {"bits": args.bits, "order": oname, "fill": fill, "permute": perm, "smem": smem, "rr": rr, "rowcap": rowcap, "screen_ms": ms,
+                   "postings_per_s": st.postings / (ms / 1e3), "labels_ok": ok,
+                   "near_ties": st2.near_ties, "overflow": st2.overflow}
             out.append(rec)
             print(json.dumps(rec), flush=True)
     eng.lib.ivfkm_set_tuning(1024, 0, 0)
