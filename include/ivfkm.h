@@ -83,17 +83,32 @@ int ivfkm_device_count(void);
 int64_t ivfkm_bivf_nblk(int64_t k); /* 32-mean blocks per term, padded */
 int64_t ivfkm_bivf_headers_size(int64_t k, int64_t dim);
 int64_t ivfkm_bivf_values_capacity(int64_t k, int64_t dim, int64_t nnz);
-/* Build options: dense_fill in [1/32, 1] (> 1: never dense; default 0.25),
+/* Build options: dense_fill in [1/32, 1] (> 1: never dense; default 1/32),
  * permute = 1 orders slots by mean term count (default), 0 keeps mean ids.
  * Out-of-range values leave the setting unchanged.                          */
 void ivfkm_set_bivf_options(float dense_fill, int permute);
 size_t ivfkm_bivf_workspace_size(int64_t dim, int64_t k);
 /* major = 0: rows of (ptr, cols) are means (mean-major CSR, cols = terms);
- * major = 1: rows are terms (term-major IVF, cols = mean ids).  0-based ids;
- * an id outside [0,k) / [0,dim) gives IVFKM_E_RANGE.                        */
-/* Screen values: screen_bits = 32 stores them as fp32, 16 as fp16 (half the
+ * major = 1: rows are terms (term-major IVF, cols = mean ids).  0-based ids.
+ * Screen values: screen_bits = 32 stores them as fp32, 16 as fp16 (half the
  * bytes; the screen's error window widens accordingly, labels stay exact).
- * val_screen and val64 hold ivfkm_bivf_values_capacity() values each.       */
+ *
+ * Two-step build (exact allocation): ivfkm_bivf_plan writes the headers,
+ * synchronises the stream and returns in *total the number of values the
+ * layout uses (raising the dense threshold itself if the 31-bit value offsets
+ * would overflow; IVFKM_E_RANGE on an out-of-range id); ivfkm_bivf_fill then
+ * writes val_screen and val64 (total values each).
+ * One-step build: ivfkm_bivf_build = plan + fill without a host round trip,
+ * into buffers of ivfkm_bivf_values_capacity() values (ids not checked).    */
+int ivfkm_bivf_plan(int64_t k, int64_t dim, int major, int64_t nrows,
+                    const int64_t* ptr /*[dev] nrows+1*/, const int32_t* cols /*[dev]*/,
+                    uint32_t* headers /*[dev]*/, int64_t* total /*[host] out*/, void* ws,
+                    size_t ws_bytes, ivfkm_stream_t stream);
+int ivfkm_bivf_fill(int64_t k, int64_t dim, int major, int64_t nrows,
+                    const int64_t* ptr /*[dev]*/, const int32_t* cols /*[dev]*/,
+                    const double* vals /*[dev]*/, const uint32_t* headers /*[dev], planned*/,
+                    void* val_screen /*[dev]*/, int screen_bits, double* val64 /*[dev]*/,
+                    ivfkm_stream_t stream);
 int ivfkm_bivf_build(int64_t k, int64_t dim, int major, int64_t nrows,
                      const int64_t* ptr /*[dev] nrows+1*/, const int32_t* cols /*[dev]*/,
                      const double* vals /*[dev]*/, uint32_t* headers /*[dev]*/,

@@ -32,6 +32,7 @@ namespace {
 
 struct BivfWs {
   unsigned int* err;
+  unsigned long long* tot64;  // total values, 64-bit (overflow check of the 32-bit offsets)
   unsigned int* cnt;
   unsigned int* off;
   unsigned int* key_a;  // k: descending-size keys
@@ -43,7 +44,7 @@ struct BivfWs {
 };
 
 // build options (ivfkm_set_bivf_options)
-float g_dense_fill = 0.25f;  // spans with >= fill*256 postings are stored dense
+float g_dense_fill = 1.0f / 32.0f;  // spans with >= fill*256 postings are stored dense
 int g_permute = 1;          // slots ordered by mean size
 int g_use_dpre = 1;  // (experiment switch, permute bit 1)
 
@@ -65,6 +66,7 @@ BivfWs carve(void* base, int64_t dim, int64_t k, size_t* total) {
   Carver c(base);
   BivfWs w;
   w.err = c.take<unsigned int>(4);
+  w.tot64 = c.take<unsigned long long>(1);
   w.cnt = c.take<unsigned int>(nh + 1);
   w.off = c.take<unsigned int>(nh + 1);
   w.key_a = c.take<unsigned int>(k);
@@ -117,8 +119,10 @@ __global__ void bivf_mask_kernel(int major, int64_t nrows, const int64_t* __rest
 // One thread per (term, span): popcounts of its 8 blocks, the span total
 // padded to a multiple of 8 values on the last block (16 B of fp16 values).
 __global__ void bivf_count_kernel(int64_t nh, const unsigned int* __restrict__ masks,
-                                  unsigned int dense_th, unsigned int* __restrict__ cnt) {
+                                  unsigned int dense_th, unsigned int* __restrict__ cnt,
+                                  unsigned long long* __restrict__ tot64) {
   const int64_t nspan = nh / kSpan;
+  unsigned long long mine = 0;
   for (int64_t sp = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sp <= nspan;
        sp += (int64_t)gridDim.x * blockDim.x) {
     if (sp == nspan) {
@@ -135,7 +139,11 @@ __global__ void bivf_count_kernel(int64_t nh, const unsigned int* __restrict__ m
 #pragma unroll
     for (int r = 0; r < kSpan; ++r) cnt[sp * kSpan + r] = dense ? 32u : c[r];
     if (!dense) cnt[sp * kSpan + kSpan - 1] += (8u - (tot & 7u)) & 7u;
+    mine += dense ? 256u : tot + ((8u - (tot & 7u)) & 7u);
   }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, off);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(tot64, mine);
 }
 
 __global__ void bivf_offset_kernel(int64_t nh, const unsigned int* __restrict__ off,
@@ -294,28 +302,16 @@ extern "C" int64_t ivfkm_bivf_values_capacity(int64_t k, int64_t dim, int64_t nn
   return (by_fill < all_dense ? by_fill : all_dense) + 256 + 8;
 }
 
-extern "C" int ivfkm_bivf_build(int64_t k, int64_t dim, int major, int64_t nrows,
-                                const int64_t* ptr, const int32_t* cols, const double* vals,
-                                uint32_t* headers, void* val_screen, int screen_bits,
-                                double* val64, void* ws, size_t ws_bytes,
-                                ivfkm_stream_t stream_) {
-  if (k < 1 || dim < 1 || nrows < 0 || (major != 0 && major != 1) || !ptr || !headers)
-    return IVFKM_E_ARG;
-  if (screen_bits != 32 && screen_bits != 16) return IVFKM_E_ARG;
-  float* val32 = static_cast<float*>(val_screen);  // or fp16 values (screen_bits 16)
-  if (k > INT32_MAX) return IVFKM_E_UNSUPPORTED;
+namespace {
+
+// Headers, part 1: slot order and masks.
+int plan_masks(int64_t k, int64_t dim, int major, int64_t nrows, const int64_t* ptr,
+               const int32_t* cols, uint32_t* headers, const BivfWs& w, cudaStream_t st) {
   const int64_t nblk = ivfkm_bivf_nblk(k);
   const int64_t nh = bivf_nh(dim, nblk);
-  if (nh + 1 > INT32_MAX) return IVFKM_E_UNSUPPORTED;  // cub scan length, 32-bit rows
-  size_t need = 0;
-  BivfWs w = carve(ws, dim, k, &need);
-  if (ws_bytes < need) return IVFKM_E_WORKSPACE;
-  cudaStream_t st = as_stream(stream_);
   uint32_t* nc = headers + 2 * nh + 1;
   int32_t* perm = reinterpret_cast<int32_t*>(nc + dim);
   int32_t* inv = perm + k;
-  uint32_t* dpre = reinterpret_cast<uint32_t*>(inv + k);
-  const unsigned th = dense_threshold();
   const int threads = 256;
   // ---- slot order: means by term count, descending (stable)
   if (g_permute) {
@@ -341,24 +337,128 @@ extern "C" int ivfkm_bivf_build(int64_t k, int64_t dim, int major, int64_t nrows
   bivf_mask_kernel<<<kNumSM * 8, threads, 0, st>>>(major, nrows, ptr, cols, k, dim, nblk, perm,
                                                    headers, w.err);
   IVFKM_CHECK_LAUNCH();
+  return IVFKM_OK;
+}
+
+// Span counts under dense threshold th (+ the 64-bit total in w.tot64).
+int plan_count(int64_t k, int64_t dim, const uint32_t* headers, unsigned th, const BivfWs& w,
+               cudaStream_t st) {
+  const int64_t nh = bivf_nh(dim, ivfkm_bivf_nblk(k));
+  const int threads = 256;
+  IVFKM_TRY(cudaMemsetAsync(w.tot64, 0, sizeof(unsigned long long), st));
   bivf_count_kernel<<<grid_for(nh / kSpan + 1, threads), threads, 0, st>>>(nh, headers, th,
-                                                                          w.cnt);
+                                                                          w.cnt, w.tot64);
   IVFKM_CHECK_LAUNCH();
+  return IVFKM_OK;
+}
+
+// Headers, part 2: offsets (total at offs[nh]), nc, dense prefixes.
+int plan_layout(int64_t k, int64_t dim, uint32_t* headers, unsigned th, const BivfWs& w,
+                cudaStream_t st) {
+  const int64_t nblk = ivfkm_bivf_nblk(k);
+  const int64_t nh = bivf_nh(dim, nblk);
+  uint32_t* nc = headers + 2 * nh + 1;
+  uint32_t* dpre = reinterpret_cast<uint32_t*>(nc + dim + 2 * k);
+  const int threads = 256;
   size_t cb = w.cub_bytes;
   IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.cnt, w.off, (int)(nh + 1), st));
   bivf_offset_kernel<<<grid_for(nh / kSpan + 1, threads), threads, 0, st>>>(nh, w.off, th,
                                                                            headers);
-  IVFKM_CHECK_LAUNCH();
-  bivf_zero_kernel<<<kNumSM * 16, threads, 0, st>>>(w.off + nh, val32, screen_bits == 16,
-                                                     val64);
-  IVFKM_CHECK_LAUNCH();
-  bivf_scatter_kernel<<<kNumSM * 8, threads, 0, st>>>(major, nrows, ptr, cols, vals, k, dim,
-                                                      nblk, headers, perm, val32, val64,
-                                                      screen_bits == 16);
   IVFKM_CHECK_LAUNCH();
   bivf_nc_kernel<<<grid_for(dim, threads / 32), threads, 0, st>>>(dim, nblk, headers,
                                                                  headers + nh, nc, dpre,
                                                                  g_use_dpre);
   IVFKM_CHECK_LAUNCH();
   return IVFKM_OK;
+}
+
+// Values: zero [0, total) (absent slots of dense spans), scatter the postings.
+int fill_impl(int64_t k, int64_t dim, int major, int64_t nrows, const int64_t* ptr,
+              const int32_t* cols, const double* vals, const uint32_t* headers,
+              void* val_screen, int screen_bits, double* val64, cudaStream_t st) {
+  const int64_t nblk = ivfkm_bivf_nblk(k);
+  const int64_t nh = bivf_nh(dim, nblk);
+  const int32_t* perm = reinterpret_cast<const int32_t*>(headers + 2 * nh + 1 + dim);
+  float* val32 = static_cast<float*>(val_screen);  // or fp16 values (screen_bits 16)
+  const int threads = 256;
+  bivf_zero_kernel<<<kNumSM * 16, threads, 0, st>>>(headers + 2 * nh, val32, screen_bits == 16,
+                                                     val64);
+  IVFKM_CHECK_LAUNCH();
+  bivf_scatter_kernel<<<kNumSM * 8, threads, 0, st>>>(major, nrows, ptr, cols, vals, k, dim,
+                                                      nblk, headers, perm, val32, val64,
+                                                      screen_bits == 16);
+  IVFKM_CHECK_LAUNCH();
+  return IVFKM_OK;
+}
+
+int check_build_args(int64_t k, int64_t dim, int major, int64_t nrows, const int64_t* ptr,
+                     const void* headers) {
+  if (k < 1 || dim < 1 || nrows < 0 || (major != 0 && major != 1) || !ptr || !headers)
+    return IVFKM_E_ARG;
+  if (k > INT32_MAX) return IVFKM_E_UNSUPPORTED;
+  if (bivf_nh(dim, ivfkm_bivf_nblk(k)) + 1 > INT32_MAX)
+    return IVFKM_E_UNSUPPORTED;  // cub scan length, 32-bit rows
+  return IVFKM_OK;
+}
+
+}  // namespace
+
+extern "C" int ivfkm_bivf_plan(int64_t k, int64_t dim, int major, int64_t nrows,
+                               const int64_t* ptr, const int32_t* cols, uint32_t* headers,
+                               int64_t* total, void* ws, size_t ws_bytes,
+                               ivfkm_stream_t stream_) {
+  if (int rc = check_build_args(k, dim, major, nrows, ptr, headers)) return rc;
+  if (!total) return IVFKM_E_ARG;
+  size_t need = 0;
+  BivfWs w = carve(ws, dim, k, &need);
+  if (ws_bytes < need) return IVFKM_E_WORKSPACE;
+  cudaStream_t st = as_stream(stream_);
+  if (int rc = plan_masks(k, dim, major, nrows, ptr, cols, headers, w, st)) return rc;
+  // Value offsets are 31 bits (bit 31 flags dense blocks): while the layout
+  // would not fit, raise the dense threshold (fewer, fuller dense spans).
+  unsigned th = dense_threshold();
+  unsigned int err = 0;
+  unsigned long long tot = 0;
+  for (;;) {
+    if (int rc = plan_count(k, dim, headers, th, w, st)) return rc;
+    IVFKM_TRY(cudaMemcpyAsync(&tot, w.tot64, sizeof(tot), cudaMemcpyDeviceToHost, st));
+    IVFKM_TRY(cudaMemcpyAsync(&err, w.err, sizeof(err), cudaMemcpyDeviceToHost, st));
+    IVFKM_TRY(cudaStreamSynchronize(st));
+    if (err) return IVFKM_E_RANGE;
+    if (tot < (1ull << 31) - 256) break;
+    if (th > 256) return IVFKM_E_UNSUPPORTED;  // even all-sparse does not fit
+    th = th * 2 > 256 ? (1u << 30) : th * 2;
+  }
+  if (int rc = plan_layout(k, dim, headers, th, w, st)) return rc;
+  *total = (int64_t)tot;
+  return IVFKM_OK;
+}
+
+extern "C" int ivfkm_bivf_fill(int64_t k, int64_t dim, int major, int64_t nrows,
+                               const int64_t* ptr, const int32_t* cols, const double* vals,
+                               const uint32_t* headers, void* val_screen, int screen_bits,
+                               double* val64, ivfkm_stream_t stream_) {
+  if (int rc = check_build_args(k, dim, major, nrows, ptr, headers)) return rc;
+  if (screen_bits != 32 && screen_bits != 16) return IVFKM_E_ARG;
+  return fill_impl(k, dim, major, nrows, ptr, cols, vals, headers, val_screen, screen_bits,
+                   val64, as_stream(stream_));
+}
+
+extern "C" int ivfkm_bivf_build(int64_t k, int64_t dim, int major, int64_t nrows,
+                                const int64_t* ptr, const int32_t* cols, const double* vals,
+                                uint32_t* headers, void* val_screen, int screen_bits,
+                                double* val64, void* ws, size_t ws_bytes,
+                                ivfkm_stream_t stream_) {
+  if (int rc = check_build_args(k, dim, major, nrows, ptr, headers)) return rc;
+  if (screen_bits != 32 && screen_bits != 16) return IVFKM_E_ARG;
+  size_t need = 0;
+  BivfWs w = carve(ws, dim, k, &need);
+  if (ws_bytes < need) return IVFKM_E_WORKSPACE;
+  cudaStream_t st = as_stream(stream_);
+  const unsigned th = dense_threshold();
+  if (int rc = plan_masks(k, dim, major, nrows, ptr, cols, headers, w, st)) return rc;
+  if (int rc = plan_count(k, dim, headers, th, w, st)) return rc;
+  if (int rc = plan_layout(k, dim, headers, th, w, st)) return rc;
+  return fill_impl(k, dim, major, nrows, ptr, cols, vals, headers, val_screen, screen_bits,
+                   val64, st);
 }

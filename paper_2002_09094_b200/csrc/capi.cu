@@ -107,10 +107,7 @@ extern "C" int ivfkm_assign_ivf_host(int64_t n, const int64_t* indptr, const int
   IVFKM_TRY(d_mp.alloc(sizeof(int64_t) * (dim + 1)));
   IVFKM_TRY(d_mc.alloc(sizeof(int32_t) * mnz));
   IVFKM_TRY(d_mv.alloc(sizeof(double) * mnz));
-  const int64_t pcap = ivfkm_bivf_values_capacity(k, dim, mnz);
   IVFKM_TRY(d_hdr.alloc(sizeof(uint32_t) * ivfkm_bivf_headers_size(k, dim)));
-  IVFKM_TRY(d_p32.alloc(sizeof(float) * pcap));
-  IVFKM_TRY(d_p64.alloc(sizeof(double) * pcap));
   IVFKM_TRY(d_bws.alloc(bws));
   IVFKM_TRY(d_lab.alloc(sizeof(int32_t) * n));
   IVFKM_TRY(d_sims.alloc(sizeof(double) * n));
@@ -129,9 +126,14 @@ extern "C" int ivfkm_assign_ivf_host(int64_t n, const int64_t* indptr, const int
   // fp16 screen values (half the posting bytes) unless the means are not
   // normalised far beyond unit norm (fp16 range)
   const int bits = mu_max <= 32768.0 ? 16 : 32;
-  int rc = ivfkm_bivf_build(k, dim, 1, dim, d_mp.as<int64_t>(), d_mc.as<int32_t>(),
-                            d_mv.as<double>(), d_hdr.as<uint32_t>(), d_p32.p, bits,
-                            d_p64.as<double>(), d_bws.p, bws, nullptr);
+  int64_t total = 0;
+  int rc = ivfkm_bivf_plan(k, dim, 1, dim, d_mp.as<int64_t>(), d_mc.as<int32_t>(),
+                           d_hdr.as<uint32_t>(), &total, d_bws.p, bws, nullptr);
+  if (rc) return rc;
+  IVFKM_TRY(d_p32.alloc(sizeof(float) * (total + 1)));
+  IVFKM_TRY(d_p64.alloc(sizeof(double) * (total + 1)));
+  rc = ivfkm_bivf_fill(k, dim, 1, dim, d_mp.as<int64_t>(), d_mc.as<int32_t>(), d_mv.as<double>(),
+                       d_hdr.as<uint32_t>(), d_p32.p, bits, d_p64.as<double>(), nullptr);
   if (rc) return rc;
   rc = ivfkm_assign(n, d_ip.as<int64_t>(), d_t.as<int32_t>(), d_v32.as<float>(),
                     d_v64.as<double>(), d_xn.as<double>(), k, dim, d_hdr.as<uint32_t>(),

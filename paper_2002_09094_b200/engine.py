@@ -223,17 +223,21 @@ class LloydEngine:
         dev = self.device
         dm.headers = torch.empty(int(self.lib.ivfkm_bivf_headers_size(self.k, dm.dim)),
                                  dtype=torch.int32, device=dev)
-        cap = int(self.lib.ivfkm_bivf_values_capacity(self.k, dm.dim, dm.nnz))
+        # plan (headers; the host learns the exact value count), then fill
+        total = C.c_int64(0)
+        rc = self.lib.ivfkm_bivf_plan(self.k, dm.dim, 0, self.k, _p(dm.ptr), _p(dm.terms),
+                                      _p(dm.headers), C.byref(total), _p(self.ws_bivf),
+                                      self.ws_bivf.numel(), _stream())
+        _lib.check(rc, "ivfkm_bivf_plan")
+        n = max(int(total.value), 1)
         bits = self.screen_bits
-        dm.pvs = torch.empty(cap, dtype=torch.float16 if bits == 16 else torch.float32,
-                             device=dev)
-        dm.pv64 = torch.empty(cap, dtype=torch.float64, device=dev)
-        rc = self.lib.ivfkm_bivf_build(self.k, dm.dim, 0, self.k, _p(dm.ptr), _p(dm.terms),
-                                       _p(dm.vals), _p(dm.headers), _p(dm.pvs), bits,
-                                       _p(dm.pv64), _p(self.ws_bivf), self.ws_bivf.numel(),
-                                       _stream())
+        dm.pvs = torch.empty(n, dtype=torch.float16 if bits == 16 else torch.float32, device=dev)
+        dm.pv64 = torch.empty(n, dtype=torch.float64, device=dev)
+        rc = self.lib.ivfkm_bivf_fill(self.k, dm.dim, 0, self.k, _p(dm.ptr), _p(dm.terms),
+                                      _p(dm.vals), _p(dm.headers), _p(dm.pvs), bits,
+                                      _p(dm.pv64), _stream())
         dm.screen_bits = bits
-        _lib.check(rc, "ivfkm_bivf_build")
+        _lib.check(rc, "ivfkm_bivf_fill")
         # sizes, CUB sort of the k slot keys (single tile / onesweep), perm, mask,
         # count, scan (init + sweep), offset, zero, scatter, nc
         self.launches += 11 + (1 if self.k <= 4096 else 6)

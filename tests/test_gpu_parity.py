@@ -436,3 +436,31 @@ def test_bivf_build_stays_within_capacity(bits, fill):
         assert bool((vs[cap * esz:] == 0x5A).all()) and bool((v64[cap * 8:] == 0x5A).all())
     finally:
         lib.ivfkm_set_bivf_options(0.25, 1)
+
+
+def test_bivf_plan_reports_out_of_range_ids():
+    """ivfkm_bivf_plan synchronises and reports a posting id outside [0, dim)
+    (the reference raises CorruptionError for it, data.py:261-262)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2002_09094_b200 import _lib
+    from paper_2002_09094_b200.engine import _p
+
+    lib = _lib.load()
+    dev = torch.device("cuda")
+    k, dim = 3, 5
+    ptr = torch.tensor([0, 2, 3, 5], dtype=torch.int64, device=dev)
+    for bad, want in ((4, 0), (5, -6)):  # IVFKM_E_RANGE
+        terms = torch.tensor([0, 1, 2, 3, bad], dtype=torch.int32, device=dev)
+        hdr = torch.empty(int(lib.ivfkm_bivf_headers_size(k, dim)), dtype=torch.int32,
+                          device=dev)
+        ws = torch.empty(int(lib.ivfkm_bivf_workspace_size(dim, k)), dtype=torch.uint8,
+                         device=dev)
+        total = C.c_int64(-1)
+        rc = lib.ivfkm_bivf_plan(k, dim, 0, k, _p(ptr), _p(terms), _p(hdr), C.byref(total),
+                                 _p(ws), ws.numel(), C.c_void_p(0))
+        assert rc == want
+        if rc == 0:
+            assert total.value % 8 == 0 and total.value >= 5
