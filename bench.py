@@ -16,10 +16,13 @@ another.  Prints ONE JSON line (rank 0).
 ``e2e``    = the same metric through host buffers: every step copies the
              corpus and the current means host->device from pinned memory and
              reads labels + new means back;
-``roofline`` = the fp32 screen kernel (dominant) against measured HBM: the
-             algorithmic bytes of an assign pass, 8 B/posting * V + 16 B *
-             sum_nnz + 4 B * (N+1) + 8 B * N, over its average
-             launch time (CUDA events);
+``roofline`` = the screen kernel (dominant) against measured HBM: the
+             algorithmic bytes of an assign pass in this layout (SURVEY.md §8(d)
+             with b_p = the screen's value bytes): b_p * V +
+             20 B * sum_nnz + 8 B * (N+1) + 8 B * N, over its average launch time
+             (CUDA events); ``roofline.l2`` sets the L2->SM bytes ncu measured
+             for the kernel (profiles/traffic.json) against the measured L2
+             read bandwidth (profiles/l2_peak.json);
 ``cpu_baseline`` = the reference's own compiled kernel (oracle/_ref, or the
              C oracle restatement when it was not built) on this host's cores,
              on a bounded row sample, plus the numpy update; test
@@ -143,9 +146,30 @@ class Clocks:
                 "samples": len(sm)}
 
 
-def algorithmic_bytes(postings, sum_nnz, n):
-    """B_assign = V*8 + sum_nnz*(4+4) + sum_nnz*8 + (N+1)*4 + N*(4+4)."""
-    return 8 * postings + 16 * sum_nnz + 4 * (n + 1) + 8 * n
+def algorithmic_bytes(postings, sum_nnz, n, value_bytes):
+    """SURVEY.md §8(d) for this layout: every posting's screen value once
+    (b_p = value_bytes: 2 for fp16, 4 for fp32; the bitmap costs 1 bit per
+    slot and is not charged), the object entries (int32 term + fp32 value) and
+    their three per-term lookups (nc, dense prefix, run start: 12 B), row
+    offsets (int64) and the per-object outputs (label + queue slot)."""
+    return value_bytes * postings + 20 * sum_nnz + 8 * (n + 1) + 8 * n
+
+
+def l2_model(cfg_index, screen_s):
+    """roofline.l2: ncu's L2->SM read bytes per screen launch (profiles/
+    traffic.json, same config) over the live launch time, against the L2 read
+    bandwidth measured by tools/l2_peak.cu (profiles/l2_peak.json)."""
+    try:
+        tr = json.loads((ROOT / "profiles" / "traffic.json").read_text()).get(f"config{cfg_index}")
+        pk = json.loads((ROOT / "profiles" / "l2_peak.json").read_text())
+        peak = max(r["GB_per_s"] for r in pk["results"] if r["buffer_mb"] * 2**20 < pk["l2_bytes"])
+    except Exception:
+        return None
+    if not isinstance(tr, dict) or not tr.get("l2_read_bytes"):
+        return None
+    ach = tr["l2_read_bytes"] / screen_s / 1e9
+    return {"achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "l2_read_bytes": tr["l2_read_bytes"], "source": "ncu lts__t_sectors_srcunit_tex_op_read"}
 
 
 # ----------------------------------------------------------------- CPU baseline
@@ -332,7 +356,7 @@ def ours_arm(args, rank, world):
     assign_ms = [a.elapsed_time(b) for a, b in evs]
     value = args.steps / (total_ms / 1000.0)
     n = ds.n
-    bytes_alg = [algorithmic_bytes(p, ds.sum_nnz, n) for p in posts]
+    bytes_alg = [algorithmic_bytes(p, ds.sum_nnz, n, eng.screen_bits // 8) for p in posts]
     avg_b = sum(bytes_alg) / len(bytes_alg)
     avg_screen_s = sum(screen_ms) / len(screen_ms) / 1000.0
     achieved = avg_b / avg_screen_s / 1e9
@@ -341,7 +365,8 @@ def ours_arm(args, rank, world):
     tp = ROOT / "profiles" / "traffic.json"
     if tp.exists():
         try:
-            traffic = json.loads(tp.read_text()).get(f"config{args.config}")
+            tr = json.loads(tp.read_text()).get(f"config{args.config}")
+            traffic = tr.get("dram_bytes") if isinstance(tr, dict) else tr
         except Exception:
             traffic = None
 
@@ -369,7 +394,8 @@ def ours_arm(args, rank, world):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "fp32 screen + fp64 exact",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "screen": f"fp{eng.screen_bits} values, fp32 FMA, rigorous window -> exact f64 rescoring",
         "data": "synthetic", "config": config_dict(args.config, c, spec, ds, world),
         "postings_per_sec": sum(posts) / (sum(assign_ms) / 1000.0),
         "screen_postings_per_sec": sum(posts) / (sum(screen_ms) / 1000.0),
@@ -379,8 +405,8 @@ def ours_arm(args, rank, world):
         "near_ties_per_step": sum(near) / len(near), "changed_per_step": sum(changed) / len(changed),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                     "kernel": "screen_kernel (fp32 BIVF register screen)",
-                     "bytes_per_launch": avg_b},
+                     "kernel": f"screen_kernel (BIVF register screen, fp{eng.screen_bits} values)",
+                     "bytes_per_launch": avg_b, "l2": l2_model(args.config, avg_screen_s)},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "steps": e2e_steps},
         "gpu_launches": launches,

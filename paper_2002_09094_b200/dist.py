@@ -35,8 +35,10 @@ from __future__ import annotations
 
 import json
 import os
+import sys
 import time
 from dataclasses import dataclass
+from pathlib import Path
 
 import numpy as np
 import torch
@@ -211,6 +213,7 @@ class DistLloyd:
         v[38:] = self.eng.sizes
         self.comm.allreduce_sum_(v)
         h = v.cpu()
+        self.local_postings = int(raw[0].item())  # this rank's share (roofline)
         self.eng.sizes.copy_(v[38:])  # global sizes for the update
         return lab, dict(postings=int(h[0]), changed=int(h[1]), near_ties=int(h[2]),
                          overflow=int(h[3]), objective=objective_from_limbs(h[4:38].tolist()))
@@ -275,17 +278,38 @@ def bench_multi(args, rank: int, world: int) -> None:
     torch.cuda.synchronize()
     dist.barrier()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    posts = []
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    posts, local_posts = [], []
+    launches0 = run.eng.launches
+    clk = None
+    if rank == 0:
+        sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+        from bench import Clocks  # the driver's nvidia-smi sampler (bench.py)
+
+        clk = Clocks(local)
     s.record()
-    for _ in range(args.steps):
-        lab, st = run.assign(dm, prev)
+    for i in range(args.steps):
+        lab, st = run.assign(dm, prev, events=ev[i])
         posts.append(st["postings"])
+        local_posts.append(run.local_postings)
         dm = run.update(lab, dm)
         prev = lab
     e.record()
     torch.cuda.synchronize()
+    clocks = clk.stop() if clk is not None else None
+    launches = run.eng.launches - launches0
     ms = torch.tensor([s.elapsed_time(e)], dtype=torch.float64, device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    screen_s = sum(a.elapsed_time(b) for a, b in ev) / len(ev) / 1000.0
+    # roofline of the screen on the slowest rank: its own shard's bytes / time
+    from bench import algorithmic_bytes, measured_peak_hbm
+
+    mine = algorithmic_bytes(sum(local_posts) / len(local_posts), run.dd.nnz, run.dd.n,
+                             run.eng.screen_bits // 8)
+    rl = torch.tensor([mine / screen_s / 1e9, screen_s], dtype=torch.float64, device=dev)
+    slow = rl.clone()
+    dist.all_reduce(slow, op=dist.ReduceOp.MIN)  # lowest achieved GB/s over ranks
     # ---- end to end: host buffers in and out every step
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(1, min(args.steps, 3))
     host = {name: getattr(dm, name).cpu().pin_memory() for name in ("ptr", "terms", "vals",
@@ -315,17 +339,25 @@ def bench_multi(args, rank: int, world: int) -> None:
     dist.barrier()
     if rank == 0:
         t = float(ms.item())
+        peak, peak_kind = measured_peak_hbm()
         print(json.dumps({
             "metric": "Lloyd iterations/sec and assign-step postings/sec (% roofline), 1/2/4/8 B200",
             "value": args.steps / (t / 1000.0), "unit": "iter/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "fp32 screen + fp64 exact", "data": "synthetic",
+            "dtype": "f64", "data": "synthetic",
+            "screen": f"fp{run.eng.screen_bits} values, fp32 FMA, rigorous window -> exact f64 rescoring",
             "config": {"workload": f"config{args.config}", "N": ds.n, "D": ds.dim, "k": k,
                        "sum_nnz": int(ds.sum_nnz),
                        "parallelism": f"objects sharded over {world} GPUs, means replicated",
                        "l2": "inputs larger than L2"},
             "postings_per_sec": sum(posts) / (t / 1000.0),
+            "roofline": {"bound": "hbm", "achieved": float(slow[0].item()), "peak": peak,
+                         "unit": "GB/s", "frac": float(slow[0].item()) / peak, "traffic": None,
+                         "peak_source": peak_kind, "per": "slowest rank's screen over its shard",
+                         "kernel": f"screen_kernel (BIVF register screen, fp{run.eng.screen_bits} values)"},
+            "gpu_launches": launches * world,
+            "clocks": clocks,
             "e2e": {"value": e2e_steps / float(e2e_t.item()), "unit": "iter/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "steps": e2e_steps, "per_rank_bytes": True},
