@@ -566,7 +566,7 @@ __global__ void __maxnreg__(64) screen_kernel(ScreenParams p) {
           const char* pl =
               static_cast<const char*>(pv) + SV::lane_bytes(32u * (gb32 - r0), r0, lane);
           const int2* dl = reinterpret_cast<const int2*>(s_ent) + 1;  // {base, value}
-          constexpr int kDepth = HALF ? 4 : 2;
+          constexpr int kDepth = HALF ? 8 : 2;
           int e = 0;
           for (; e + kDepth <= nd; e += kDepth) {
             SV q[kDepth];
@@ -1281,15 +1281,16 @@ int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
   const int64_t nblk = ivfkm_bivf_nblk(k);
   Plan pl;
   if (smem_limit <= 0) {
-    // Adaptive budget (measured on configs 1-4): split rho over a thread-block
-    // cluster once it passes ~24 KB, so at least two CTAs stay resident per
-    // SM, but never below 24 KB per CTA nor above 100 KB.
+    // Adaptive budget (measured on configs 1-4): one CTA per object while rho
+    // and the staged row fit in 64 KB (k <= ~13,000: every split CTA would
+    // stage the whole row again); beyond, split rho over a thread-block
+    // cluster at about half of it per CTA, between 24 KB and 100 KB.
     const int64_t rho = nblk * 128;
     const int64_t stg = (int64_t)rowcap * (rr < 0 ? 8 : kEntryBytes);
     int64_t b = rho / 2 + (stg > 8 * 1024 ? stg : 8 * 1024);
     if (b < 24 * 1024) b = 24 * 1024;
     if (b > 100 * 1024) b = 100 * 1024;
-    if (rho + stg <= 24 * 1024) b = kSmemLimit - 2048;
+    if (rho + stg <= (rr < 0 ? 24 : 64) * 1024) b = kSmemLimit - 2048;
     smem_limit = (int)b;
   }
   if (rr == -8 || rr == -4) {  // TMA (-8) / cp.async (-4) pipelined screens, 8-block spans
