@@ -53,7 +53,8 @@ constexpr int kMaxC = IVFKM_MAXC;
 constexpr int kLimbs = IVFKM_OBJ_LIMBS;
 constexpr int kMaxSplit = 8;           // portable cluster size
 constexpr int kSmemLimit = 227 * 1024;  // opt-in dynamic shared memory per CTA
-constexpr int kMaxLocalSpans = 255;     // dense-prefix buckets per CTA (screen_kernel)
+constexpr int kMaxLocalSpans = 63;      // dense-prefix buckets per CTA (screen_kernel)
+constexpr int kMaxChunks = 32;          // 32-entry chunks per staged row piece (rowcap 1024)
 constexpr int kEntryBytes = 20;         // screen_kernel staging per row entry
 
 struct ScreenParams {
@@ -483,13 +484,16 @@ __global__ void __maxnreg__(64) screen_kernel(ScreenParams p) {
   // BIVF spans this CTA touches: gs0 .. gs0+nls-1 (bivf.cuh: 8 blocks each)
   const int gs0 = (int)(blk0 >> 3);
   int nls = (int)(((blk0 + p.cta_blocks - 1) >> 3) - gs0 + 1);
-  if (nls > kMaxLocalSpans) nls = kMaxLocalSpans;
-  __shared__ int s_start[kMaxLocalSpans + 1];  // bucket starts (then cursors)
-  __shared__ int s_cntd[kMaxLocalSpans + 1];   // entries whose prefix covers local span s
+  if (nls > kMaxLocalSpans) nls = kMaxLocalSpans;  // later local spans: masked path
+  const int nb = nls + 1;                           // prefix buckets 0..nls
+  __shared__ uint16_t s_cc[kMaxChunks * (kMaxLocalSpans + 1)];  // [chunk][bucket]
+  __shared__ int s_cntd[kMaxLocalSpans + 1];  // entries whose prefix covers local span s
+  __shared__ int s_next;                      // next span to process (dynamic)
   int64_t c0 = rb;
   do {
     const int64_t rem = re - c0;
     const int cn = (int)(rem < p.rowcap ? rem : p.rowcap);
+    const int nch = (cn + 31) >> 5;
     __syncthreads();
     // Stage the row chunk sorted by the terms' dense prefix (bivf.cuh, dpre),
     // longest first, stable: for local span s the entries [0, cntd[s]) read
@@ -497,58 +501,70 @@ __global__ void __maxnreg__(64) screen_kernel(ScreenParams p) {
     // [cntd[s], cn) go through masks + offsets.  (The screen's fp32 sum may run
     // in any order — its error bound does not depend on it — and the sort is
     // stable, so the sums are deterministic; the exact rescoring keeps the
-    // reference order.)
-    for (int b = threadIdx.x; b <= nls; b += blockDim.x) s_start[b] = 0;
+    // reference order.)  Counting sort over 32-entry chunks: rank within the
+    // chunk by __match_any_sync, per-(chunk, bucket) counts, offsets.
+    for (int q = threadIdx.x; q < nch * nb; q += blockDim.x) s_cc[q] = 0;
+    if (threadIdx.x == 0) s_next = 0;
     __syncthreads();
-    for (int j = threadIdx.x; j < cn; j += blockDim.x) {
-      const uint32_t t = (uint32_t)p.terms[c0 + j];
-      int lp = (int)__ldg(p.dpre + t) - gs0;
-      lp = lp < 0 ? 0 : (lp > nls ? nls : lp);
-      s_lp[j] = (uint8_t)lp;
-      atomicAdd(&s_start[lp], 1);
-      if (z == 0) post += __ldg(p.nc + t);
+    for (int j0 = warp * 32; j0 < cn; j0 += nwarps * 32) {
+      const int j = j0 + lane;
+      int lp = -1;
+      if (j < cn) {
+        const uint32_t t = (uint32_t)p.terms[c0 + j];
+        lp = (int)__ldg(p.dpre + t) - gs0;
+        lp = lp < 0 ? 0 : (lp > nls ? nls : lp);
+        if (z == 0) post += __ldg(p.nc + t);
+      }
+      const unsigned peers = __match_any_sync(kFull, lp);
+      if (j < cn) {
+        s_lp[j] = (uint8_t)lp;
+        s_pos[j] = (uint16_t)__popc(peers & lt);  // rank among the chunk's equals
+        if (lane == __ffs(peers) - 1) s_cc[(j0 >> 5) * nb + lp] = (uint16_t)__popc(peers);
+      }
     }
     __syncthreads();
-    if (warp == 0) {
-      // bucket starts in descending prefix order (warp scan, 32 buckets a step)
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {  // per bucket: chunk offsets
+      int run = 0;
+      for (int c = 0; c < nch; ++c) {
+        const int x = s_cc[c * nb + b];
+        s_cc[c * nb + b] = (uint16_t)run;
+        run += x;
+      }
+      s_cntd[b] = run;
+    }
+    __syncthreads();
+    if (warp == 0) {  // bucket starts in descending prefix order
       int run = 0;
       for (int b0 = nls; b0 >= 0; b0 -= 32) {
         const int b = b0 - lane;
-        const int c = b >= 0 ? s_start[b] : 0;
+        const int c = b >= 0 ? s_cntd[b] : 0;
         int x = c;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
           const int y = __shfl_up_sync(kFull, x, off);
           if (lane >= off) x += y;
         }
-        if (b >= 0) {
-          s_start[b] = run + x - c;
-          s_cntd[b] = run + x - c;  // = entries with a longer prefix than b
-        }
+        if (b >= 0) s_cntd[b] = run + x - c;  // = entries with a longer prefix than b
         run += __shfl_sync(kFull, x, 31);
-      }
-      __syncwarp();
-      // stable placement, 32 entries at a time
-      for (int j0 = 0; j0 < cn; j0 += 32) {
-        const int j = j0 + lane;
-        const int lp = j < cn ? (int)s_lp[j] : -1;
-        const unsigned peers = __match_any_sync(kFull, lp);
-        if (j < cn) s_pos[j] = (uint16_t)(s_start[lp] + __popc(peers & lt));
-        __syncwarp();
-        if (j < cn && lane == __ffs(peers) - 1) s_start[lp] += __popc(peers);
-        __syncwarp();
       }
     }
     __syncthreads();
     for (int j = threadIdx.x; j < cn; j += blockDim.x) {
+      const int lp = s_lp[j];
       const uint32_t row = (uint32_t)p.terms[c0 + j] * (uint32_t)nblk;
       const int v = __float_as_int(p.val32[c0 + j]);
-      const uint32_t base = s_lp[j] ? (__ldg(offs + row) & ~kDense) : 0u;
-      s_ent[s_pos[j]] = make_int4((int)row, v, (int)base, v);
+      const uint32_t base = lp ? (__ldg(offs + row) & ~kDense) : 0u;
+      s_ent[s_cntd[lp] + s_cc[(j >> 5) * nb + lp] + s_pos[j]] =
+          make_int4((int)row, v, (int)base, v);
     }
     __syncthreads();
     const bool first = (c0 == rb);
-    for (int sp = warp; sp < nspans; sp += nwarps) {
+    for (;;) {  // spans handed out dynamically: dense low spans and sparse high
+                // ones cost very differently
+      int sp = 0;
+      if (lane == 0) sp = atomicAdd(&s_next, 1);
+      sp = __shfl_sync(kFull, sp, 0);
+      if (sp >= nspans) break;
       const int64_t gb = blk0 + (int64_t)sp * RR;
       float acc[RR];
 #pragma unroll
@@ -1031,26 +1047,31 @@ struct ExactCtx {
   const double* pv64;
 };
 
-// Warp-cooperative: lanes look up 32 nonzeros at a time, then the products
-// are added serially in row order (every lane holds the same sum).
+// Warp-cooperative: lanes look up 64 nonzeros at a time (two independent
+// lookup chains in flight), then the products are added serially in row
+// order (every lane holds the same sum).
 __device__ double exact_score_warp(const ExactCtx& x, int64_t rb, int64_t re, int c, int lane) {
   double acc = 0.0;
-  for (int64_t h0 = rb; h0 < re; h0 += 32) {
-    const int64_t h = h0 + lane;
-    bool present = false;
-    double prod = 0.0;
-    if (h < re) {
-      const int64_t pos = bivf_find(x.bv, x.terms[h], c);
-      if (pos >= 0) {
-        present = true;
-        prod = __dmul_rn(x.val64[h], __ldg(x.pv64 + pos));
-      }
-    }
-    unsigned pm = __ballot_sync(kFull, present);
+  const int64_t slot = x.bv.perm ? (int64_t)__ldg(x.bv.perm + c) : c;
+  for (int64_t h0 = rb; h0 < re; h0 += 64) {
+    const int64_t ha = h0 + lane, hb = h0 + 32 + lane;
+    const int32_t ta = ha < re ? x.terms[ha] : -1;
+    const int32_t tb = hb < re ? x.terms[hb] : -1;
+    const int64_t pa = ta >= 0 ? bivf_find_slot(x.bv, ta, slot) : -1;
+    const int64_t pb = tb >= 0 ? bivf_find_slot(x.bv, tb, slot) : -1;
+    const double va = pa >= 0 ? __dmul_rn(x.val64[ha], __ldg(x.pv64 + pa)) : 0.0;
+    const double vb = pb >= 0 ? __dmul_rn(x.val64[hb], __ldg(x.pv64 + pb)) : 0.0;
+    unsigned pm = __ballot_sync(kFull, pa >= 0);
     while (pm) {
       const int j = __ffs(pm) - 1;
       pm &= pm - 1u;
-      acc = __dadd_rn(acc, __shfl_sync(kFull, prod, j));
+      acc = __dadd_rn(acc, __shfl_sync(kFull, va, j));
+    }
+    pm = __ballot_sync(kFull, pb >= 0);
+    while (pm) {
+      const int j = __ffs(pm) - 1;
+      pm &= pm - 1u;
+      acc = __dadd_rn(acc, __shfl_sync(kFull, vb, j));
     }
   }
   return acc;
@@ -1322,8 +1343,8 @@ int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
   pl.tma = false;
   pl.mode = 0;
   pl.rr = rr > 0 ? rr : (nblk >= 32 ? 8 : 2);
-  pl.rowcap = rowcap;
-  const size_t stage = (size_t)rowcap * kEntryBytes;
+  pl.rowcap = rowcap < kMaxChunks * 32 ? rowcap : kMaxChunks * 32;  // staging counts cap
+  const size_t stage = (size_t)pl.rowcap * kEntryBytes;
   pl.nsplit = 0;
   for (int s = 1; s <= kMaxSplit; ++s) {
     int64_t cb = (nblk + s - 1) / s;

@@ -94,26 +94,48 @@ __device__ __forceinline__ int64_t row_of(const int64_t* __restrict__ ptr, int64
   return lo;
 }
 
-// One thread per entry (grid-stride), so a few long rows (k means holding
-// ~20k terms each) still spread over the whole GPU.
+// Entries of a CSR in contiguous per-warp chunks (so a few long rows — k
+// means holding ~20k terms each — still spread over the whole GPU): one
+// binary search per warp, then each lane walks the row pointer forward.
+template <class F>
+__device__ __forceinline__ void for_each_entry(int64_t nrows, const int64_t* __restrict__ ptr,
+                                               F&& f) {
+  const int64_t nnz = ptr[nrows];
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  int64_t chunk = (nnz + nwarps - 1) / nwarps;
+  chunk = (chunk + 31) / 32 * 32;
+  const int64_t q0 = wid * chunk;
+  const int64_t q1 = q0 + chunk < nnz ? q0 + chunk : nnz;
+  if (q0 >= q1) return;
+  int64_t r = row_of(ptr, nrows, q0);
+  for (int64_t qb = q0; qb < q1; qb += 32) {
+    const int64_t q = qb + lane;
+    int64_t rl = r;
+    if (q < q1) {
+      while (__ldg(ptr + rl + 1) <= q) ++rl;
+      f(rl, q);
+    }
+    r = __shfl_sync(0xffffffffu, rl, 31);  // lane 31 holds the furthest row
+  }
+}
+
 __global__ void bivf_mask_kernel(int major, int64_t nrows, const int64_t* __restrict__ ptr,
                                  const int32_t* __restrict__ cols, int64_t k, int64_t dim,
                                  int64_t nblk, const int32_t* __restrict__ perm,
                                  unsigned int* __restrict__ hdr, unsigned int* __restrict__ err) {
-  const int64_t nnz = ptr[nrows];
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = row_of(ptr, nrows, q);
+  for_each_entry(nrows, ptr, [&](int64_t r, int64_t q) {
     const int64_t col = cols[q];
     const int64_t c = major == 0 ? r : col;
     const int64_t t = major == 0 ? col : r;
     if (c < 0 || c >= k || t < 0 || t >= dim) {
       atomicAdd(err, 1u);
-      continue;
+      return;
     }
     const int64_t sl = perm[c];
     atomicOr(&hdr[t * nblk + (sl >> 5)], 1u << (sl & 31));
-  }
+  });
 }
 
 // One thread per (term, span): popcounts of its 8 blocks, the span total
@@ -172,25 +194,35 @@ __global__ void bivf_scatter_kernel(int major, int64_t nrows, const int64_t* __r
                                     int64_t nblk, const unsigned int* __restrict__ hdr,
                                     const int32_t* __restrict__ perm,
                                     float* __restrict__ v32, double* __restrict__ v64, int half) {
-  const int64_t nnz = ptr[nrows];
   const int64_t nh = bivf_nh(dim, nblk);
-  BivfView view{nblk, hdr, hdr + nh, perm};
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = row_of(ptr, nrows, q);
+  for_each_entry(nrows, ptr, [&](int64_t r, int64_t q) {
     const int64_t col = cols[q];
     const int64_t c = major == 0 ? r : col;
     const int64_t t = major == 0 ? col : r;
-    if (c < 0 || c >= k || t < 0 || t >= dim) continue;
-    const int64_t pos = bivf_find(view, t, c);
+    if (c < 0 || c >= k || t < 0 || t >= dim) return;
+    // bivf_find / bivf_find16 in one: the positions differ only in dense spans
+    const int64_t s = perm[c];
+    const int64_t b = s >> 5;
+    const uint32_t j = (uint32_t)(s & 31);
+    const uint32_t m = hdr[t * nblk + b];
+    const uint32_t o = hdr[nh + t * nblk + b];
+    int64_t pos, pos16;
+    if (o & kDense) {
+      const uint32_t rr = (uint32_t)(b & (kSpan - 1));
+      const uint32_t sb = (o & ~kDense) - 32u * rr;
+      pos = sb + 128u * (rr >> 2) + 4u * j + (rr & 3u);
+      pos16 = sb + 8u * j + rr;
+    } else {
+      pos = pos16 = o + (uint32_t)__popc(m & ((1u << j) - 1u));
+    }
     const double v = vals[q];
     if (half) {
-      reinterpret_cast<__half*>(v32)[bivf_find16(view, t, c)] = __double2half(v);
+      reinterpret_cast<__half*>(v32)[pos16] = __double2half(v);
     } else {
       v32[pos] = static_cast<float>(v);
     }
     v64[pos] = v;
-  }
+  });
 }
 
 // absent slots of dense spans (and padding) hold exact zeros: clear [0, total)

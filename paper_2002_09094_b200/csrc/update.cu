@@ -150,7 +150,13 @@ __global__ void segsum_kernel(int64_t nnz, const uint32_t* __restrict__ n_seg_p,
       continue;
     }
     double acc = 0.0;
-    for (uint32_t e = seg_start[s]; e < seg_start[s + 1]; ++e) acc = __dadd_rn(acc, sval[e]);
+    uint32_t e = seg_start[s];
+    const uint32_t end = seg_start[s + 1];
+    for (; e + 4 <= end; e += 4) {  // four loads in flight, adds in order
+      const double a = sval[e], b = sval[e + 1], c2 = sval[e + 2], d = sval[e + 3];
+      acc = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(acc, a), b), c2), d);
+    }
+    for (; e < end; ++e) acc = __dadd_rn(acc, sval[e]);
     const int64_t c = (int64_t)(seg_key[s] / (K)dim);
     const double w = __ddiv_rn(acc, (double)sizes[c]);
     seg_w[s] = w;
