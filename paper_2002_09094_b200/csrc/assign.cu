@@ -1048,9 +1048,13 @@ struct ExactCtx {
 };
 
 // Warp-cooperative: lanes look up 64 nonzeros at a time (two independent
-// lookup chains in flight), then the products are added serially in row
-// order (every lane holds the same sum).
-__device__ double exact_score_warp(const ExactCtx& x, int64_t rb, int64_t re, int c, int lane) {
+// lookup chains in flight) and park the products in the warp's shared
+// scratch (64 doubles); lane 0 then adds them in row order.  An absent
+// posting parks +0.0: adding it is exact (x + 0.0 == x; at most the sign of
+// an all-zero sum differs, which no comparison or sum can see), so the sum
+// equals the reference's sum over present postings.
+__device__ double exact_score_warp(const ExactCtx& x, int64_t rb, int64_t re, int c, int lane,
+                                   double* scratch) {
   double acc = 0.0;
   const int64_t slot = x.bv.perm ? (int64_t)__ldg(x.bv.perm + c) : c;
   for (int64_t h0 = rb; h0 < re; h0 += 64) {
@@ -1059,22 +1063,22 @@ __device__ double exact_score_warp(const ExactCtx& x, int64_t rb, int64_t re, in
     const int32_t tb = hb < re ? x.terms[hb] : -1;
     const int64_t pa = ta >= 0 ? bivf_find_slot(x.bv, ta, slot) : -1;
     const int64_t pb = tb >= 0 ? bivf_find_slot(x.bv, tb, slot) : -1;
-    const double va = pa >= 0 ? __dmul_rn(x.val64[ha], __ldg(x.pv64 + pa)) : 0.0;
-    const double vb = pb >= 0 ? __dmul_rn(x.val64[hb], __ldg(x.pv64 + pb)) : 0.0;
-    unsigned pm = __ballot_sync(kFull, pa >= 0);
-    while (pm) {
-      const int j = __ffs(pm) - 1;
-      pm &= pm - 1u;
-      acc = __dadd_rn(acc, __shfl_sync(kFull, va, j));
+    scratch[lane] = pa >= 0 ? __dmul_rn(x.val64[ha], __ldg(x.pv64 + pa)) : 0.0;
+    scratch[32 + lane] = pb >= 0 ? __dmul_rn(x.val64[hb], __ldg(x.pv64 + pb)) : 0.0;
+    __syncwarp();
+    if (lane == 0) {
+      const int m = re - h0 < 64 ? (int)(re - h0) : 64;
+      int j = 0;
+      for (; j + 4 <= m; j += 4) {
+        const double2 u = reinterpret_cast<const double2*>(scratch)[j >> 1];
+        const double2 v = reinterpret_cast<const double2*>(scratch)[(j >> 1) + 1];
+        acc = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(acc, u.x), u.y), v.x), v.y);
+      }
+      for (; j < m; ++j) acc = __dadd_rn(acc, scratch[j]);
     }
-    pm = __ballot_sync(kFull, pb >= 0);
-    while (pm) {
-      const int j = __ffs(pm) - 1;
-      pm &= pm - 1u;
-      acc = __dadd_rn(acc, __shfl_sync(kFull, vb, j));
-    }
+    __syncwarp();
   }
-  return acc;
+  return __shfl_sync(kFull, acc, 0);
 }
 
 // One thread scores one mean over the whole row.
@@ -1101,14 +1105,16 @@ struct FinalParams {
 };
 
 __global__ void __launch_bounds__(256) finalize_kernel(FinalParams p) {
+  __shared__ __align__(16) double s_scr[8][64];
   const int lane = threadIdx.x & 31;
+  double* scratch = s_scr[threadIdx.x >> 5];
   const int64_t wpb = blockDim.x >> 5;
   for (int64_t i = blockIdx.x * wpb + (threadIdx.x >> 5); i < p.n_obj; i += gridDim.x * wpb) {
     const int64_t rb = p.x.row_ptr[i], re = p.x.row_ptr[i + 1];
     const int slot = p.slot_of[i];
     if (slot < 0) {
       const int c = p.label32[i];
-      const double s = exact_score_warp(p.x, rb, re, c, lane);
+      const double s = exact_score_warp(p.x, rb, re, c, lane, scratch);
       if (lane == 0) {
         p.labels[i] = c;
         p.sims[i] = s;
@@ -1124,7 +1130,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalParams p) {
     int bc = INT_MAX;
     for (int j = 0; j < cnt; ++j) {
       const int c = p.q_cid[(int64_t)slot * kMaxC + j];
-      const double s = exact_score_warp(p.x, rb, re, c, lane);
+      const double s = exact_score_warp(p.x, rb, re, c, lane, scratch);
       if (s > bv || (s == bv && c < bc)) {
         bv = s;
         bc = c;
@@ -1139,10 +1145,13 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalParams p) {
 
 __global__ void __launch_bounds__(256) score_labels_kernel(int64_t n_obj, ExactCtx x,
                                                            const int32_t* labels, double* sims) {
+  __shared__ __align__(16) double s_scr[8][64];
   const int lane = threadIdx.x & 31;
+  double* scratch = s_scr[threadIdx.x >> 5];
   const int64_t wpb = blockDim.x >> 5;
   for (int64_t i = blockIdx.x * wpb + (threadIdx.x >> 5); i < n_obj; i += gridDim.x * wpb) {
-    const double s = exact_score_warp(x, x.row_ptr[i], x.row_ptr[i + 1], labels[i], lane);
+    const double s =
+        exact_score_warp(x, x.row_ptr[i], x.row_ptr[i + 1], labels[i], lane, scratch);
     if (lane == 0) sims[i] = s;
   }
 }
