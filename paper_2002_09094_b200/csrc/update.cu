@@ -19,6 +19,12 @@
 // scans give the new CSR offsets; the fill pass writes terms and values.
 #include <cub/cub.cuh>
 
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <utility>
+#include <vector>
+
 #include "common.cuh"
 
 using namespace ivfkm;
@@ -41,6 +47,7 @@ struct UpdWs {
   double* nrm;        // k
   int64_t* counts;    // k+1
   uint32_t* n_seg;    // 1
+  int32_t* plan;      // pairwise-sum tree of [0, dim) (NormPlan::buf)
   void* cub;
   size_t cub_bytes;
 };
@@ -56,8 +63,82 @@ size_t cub_bytes_for(int64_t nnz, int64_t k) {
   return std::max(a, std::max(b, c));
 }
 
+// numpy's pairwise-summation tree over [0, D) (see norm_kernel), built once
+// per D on the host: leaves left to right, internal nodes ordered by height
+// so that one level can be evaluated in parallel once the lower ones are.
+//   buf = leaf_lo[nleaf+1] | lv_off[nlevels+1] | node_l[nint] | node_r[nint]
+// node_l/node_r index the value array: leaf j -> j, the q-th internal node
+// (level order) -> nleaf + q; the root is the last value.
+struct NormPlan {
+  int64_t nleaf = 0, nint = 0, nlevels = 0;
+  std::vector<int32_t> buf;
+};
+
+int64_t norm_plan_ints_max(int64_t dim) { return 4 * (dim / 64 + 2) + 130; }
+
+const NormPlan& norm_plan(int64_t D) {
+  static std::mutex mu;
+  static std::map<int64_t, NormPlan> cache;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(D);
+  if (it != cache.end()) return it->second;
+  std::vector<int32_t> lo;
+  struct Node {
+    int64_t l, r;  // >= 0: leaf index; < 0: -(internal id) - 1
+    int h;
+  };
+  std::vector<Node> nodes;
+  struct Rec {
+    std::vector<int32_t>& lo;
+    std::vector<Node>& nodes;
+    std::pair<int64_t, int> go(int64_t l, int64_t n) {
+      if (n <= 128) {
+        lo.push_back((int32_t)l);
+        return {(int64_t)lo.size() - 1, 0};
+      }
+      int64_t n2 = n / 2;
+      n2 -= n2 % 8;
+      const auto a = go(l, n2);
+      const auto b = go(l + n2, n - n2);
+      const int h = std::max(a.second, b.second) + 1;
+      nodes.push_back(Node{a.first, b.first, h});
+      return {-(int64_t)nodes.size(), h};
+    }
+  } rec{lo, nodes};
+  rec.go(0, D);
+  NormPlan P;
+  P.nleaf = (int64_t)lo.size();
+  P.nint = (int64_t)nodes.size();
+  int H = 0;
+  for (const Node& n : nodes) H = std::max(H, n.h);
+  P.nlevels = H;
+  std::vector<int64_t> order(nodes.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = (int64_t)i;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int64_t a, int64_t b) { return nodes[a].h < nodes[b].h; });
+  std::vector<int64_t> pos(nodes.size());
+  for (size_t q = 0; q < order.size(); ++q) pos[order[q]] = (int64_t)q;
+  auto ref = [&](int64_t r) -> int32_t {
+    return (int32_t)(r >= 0 ? r : P.nleaf + pos[-r - 1]);
+  };
+  P.buf.reserve(P.nleaf + 1 + H + 1 + 2 * P.nint);
+  for (int32_t x : lo) P.buf.push_back(x);
+  P.buf.push_back((int32_t)D);
+  std::vector<int32_t> off(H + 1, 0);
+  for (const Node& n : nodes) off[n.h]++;  // heights 1..H -> levels 0..H-1
+  int32_t run = 0;
+  for (int h = 1; h <= H; ++h) {
+    P.buf.push_back(run);
+    run += off[h];
+  }
+  P.buf.push_back(run);
+  for (size_t q = 0; q < order.size(); ++q) P.buf.push_back(ref(nodes[order[q]].l));
+  for (size_t q = 0; q < order.size(); ++q) P.buf.push_back(ref(nodes[order[q]].r));
+  return cache.emplace(D, std::move(P)).first->second;
+}
+
 template <class K>
-UpdWs<K> carve_upd(void* base, int64_t nnz, int64_t k, size_t* total) {
+UpdWs<K> carve_upd(void* base, int64_t nnz, int64_t k, int64_t dim, size_t* total) {
   Carver c(base);
   UpdWs<K> w;
   const size_t n = (size_t)(nnz > 0 ? nnz : 1);
@@ -75,6 +156,7 @@ UpdWs<K> carve_upd(void* base, int64_t nnz, int64_t k, size_t* total) {
   w.nrm = c.take<double>(k);
   w.counts = c.take<int64_t>(k + 1);
   w.n_seg = c.take<uint32_t>(4);
+  w.plan = c.take<int32_t>((size_t)norm_plan_ints_max(dim));
   w.cub_bytes = cub_bytes_for<K>((int64_t)n, k);
   w.cub = c.take_bytes(w.cub_bytes);
   if (total) *total = c.off;
@@ -193,33 +275,6 @@ __global__ void clseg_kernel(int64_t k, int64_t dim, const uint32_t* __restrict_
 // One CTA per cluster: threads compute the leaves in parallel, thread 0
 // combines them in the recursion's order.
 
-// leaf boundaries of [0, D) in left-to-right order (host and device)
-__host__ __device__ inline int64_t enum_leaves(int64_t D, int32_t* lo_out) {
-  int64_t stk_lo[64], stk_n[64];
-  int sp = 0;
-  int64_t L = 0;
-  stk_lo[sp] = 0;
-  stk_n[sp++] = D;
-  while (sp > 0) {
-    --sp;
-    const int64_t lo = stk_lo[sp], n = stk_n[sp];
-    if (n <= 128) {
-      if (lo_out) lo_out[L] = (int32_t)lo;
-      ++L;
-      continue;
-    }
-    int64_t n2 = n / 2;
-    n2 -= n2 % 8;
-    // push right first so the left subtree is emitted first
-    stk_lo[sp] = lo + n2;
-    stk_n[sp++] = n - n2;
-    stk_lo[sp] = lo;
-    stk_n[sp++] = n2;
-  }
-  if (lo_out) lo_out[L] = (int32_t)D;
-  return L;
-}
-
 template <class K>
 __device__ double leaf_value(int64_t lo, int64_t n, uint32_t cur, uint32_t end, const K* seg_key,
                              const double* seg_w, K base) {
@@ -249,56 +304,21 @@ __device__ double leaf_value(int64_t lo, int64_t n, uint32_t cur, uint32_t end, 
   return res;
 }
 
-// Combine leaf values in the recursion's order: pw(lo,n) = leaf or
-// pw(left) + pw(right).  Leaves are consumed left to right.
-__device__ double combine_leaves(int64_t D, const double* leaf_val) {
-  struct Frame {
-    int64_t n;
-    double left;
-    int stage;
-  };
-  Frame st[64];
-  int sp = 0;
-  int64_t next = 0;
-  double ret = 0.0;
-  st[sp++] = Frame{D, 0.0, 0};
-  while (sp > 0) {
-    Frame& f = st[sp - 1];
-    if (f.stage == 0) {
-      if (f.n <= 128) {
-        ret = leaf_val[next++];
-        --sp;
-        continue;
-      }
-      int64_t n2 = f.n / 2;
-      n2 -= n2 % 8;
-      f.stage = 1;
-      st[sp++] = Frame{n2, 0.0, 0};
-    } else if (f.stage == 1) {
-      f.left = ret;
-      f.stage = 2;
-      int64_t n2 = f.n / 2;
-      n2 -= n2 % 8;
-      st[sp++] = Frame{f.n - n2, 0.0, 0};
-    } else {
-      ret = __dadd_rn(f.left, ret);
-      --sp;
-    }
-  }
-  return ret;
-}
-
 template <class K>
 __global__ void __launch_bounds__(256) norm_kernel(
-    int64_t k, int64_t dim, int64_t nleaf, const unsigned long long* __restrict__ sizes,
+    int64_t k, int64_t dim, int64_t nleaf, int64_t nint, int64_t nlevels,
+    const int32_t* __restrict__ plan, const unsigned long long* __restrict__ sizes,
     const int64_t* __restrict__ prev_ptr, const uint32_t* __restrict__ cl_seg,
     const K* __restrict__ seg_key, const double* __restrict__ seg_w,
     const uint32_t* __restrict__ nz, double* __restrict__ nrm, int64_t* __restrict__ counts) {
   extern __shared__ __align__(16) unsigned char smem[];
-  double* leaf_val = reinterpret_cast<double*>(smem);
-  int32_t* leaf_lo = reinterpret_cast<int32_t*>(leaf_val + nleaf);
+  double* val = reinterpret_cast<double*>(smem);                  // nleaf + nint
+  int32_t* leaf_lo = reinterpret_cast<int32_t*>(val + nleaf + nint);  // nleaf + 1
+  const int32_t* lv_off = plan + nleaf + 1;
+  const int32_t* node_l = lv_off + nlevels + 1;
+  const int32_t* node_r = node_l + nint;
   __shared__ int64_t s_cnt;
-  if (threadIdx.x == 0) enum_leaves(dim, leaf_lo);
+  for (int64_t j = threadIdx.x; j <= nleaf; j += blockDim.x) leaf_lo[j] = plan[j];
   if (blockIdx.x == 0 && threadIdx.x == 0) counts[k] = 0;
   __syncthreads();
   for (int64_t c = blockIdx.x; c < k; c += gridDim.x) {
@@ -326,12 +346,18 @@ __global__ void __launch_bounds__(256) norm_kernel(
         const uint32_t mid = (a + z) >> 1;
         if (seg_key[mid] < target) a = mid + 1; else z = mid;
       }
-      leaf_val[j] = leaf_value<K>(lo, hi - lo, a, e, seg_key, seg_w, base);
+      val[j] = leaf_value<K>(lo, hi - lo, a, e, seg_key, seg_w, base);
     }
     __syncthreads();
+    // internal nodes level by level: pw(node) = pw(left) + pw(right)
+    for (int64_t l = 0; l < nlevels; ++l) {
+      for (int64_t q = lv_off[l] + threadIdx.x; q < lv_off[l + 1]; q += blockDim.x)
+        val[nleaf + q] = __dadd_rn(val[node_l[q]], val[node_r[q]]);
+      __syncthreads();
+    }
     if (threadIdx.x == 0) {
       counts[c] = s_cnt;
-      nrm[c] = __dsqrt_rn(combine_leaves(dim, leaf_val));
+      nrm[c] = __dsqrt_rn(val[nleaf + nint - 1]);
     }
     __syncthreads();
   }
@@ -383,7 +409,7 @@ int update_count_impl(int64_t n_obj, const int64_t* row_ptr, const int32_t* term
                       const int64_t* prev_ptr, int64_t* new_ptr, void* ws, size_t ws_bytes,
                       cudaStream_t st) {
   size_t need = 0;
-  UpdWs<K> w = carve_upd<K>(ws, nnz, k, &need);
+  UpdWs<K> w = carve_upd<K>(ws, nnz, k, dim, &need);
   if (ws_bytes < need) return IVFKM_E_WORKSPACE;
   const int T = 256;
   if (nnz > 0) {
@@ -414,13 +440,18 @@ int update_count_impl(int64_t n_obj, const int64_t* row_ptr, const int32_t* term
   }
   clseg_kernel<K><<<grid_for(k + 1, T), T, 0, st>>>(k, dim, w.n_seg, w.seg_key, w.cl_seg);
   IVFKM_CHECK_LAUNCH();
-  const int64_t nleaf = enum_leaves(dim, nullptr);
-  const size_t nsmem = (size_t)nleaf * 8 + (size_t)(nleaf + 1) * 4;
-  if (nsmem > 200 * 1024) return IVFKM_E_UNSUPPORTED;  // D beyond ~2.4M terms
+  const NormPlan& P = norm_plan(dim);
+  const int64_t nleaf = P.nleaf, nint = P.nint;
+  const size_t nsmem = (size_t)(nleaf + nint) * 8 + (size_t)(nleaf + 1) * 4;
+  if (nsmem > 200 * 1024) return IVFKM_E_UNSUPPORTED;  // D beyond ~1.1M terms
+  // the plan lives in a process-lifetime cache, so an async copy is safe
+  IVFKM_TRY(cudaMemcpyAsync(w.plan, P.buf.data(), P.buf.size() * sizeof(int32_t),
+                            cudaMemcpyHostToDevice, st));
   IVFKM_TRY(cudaFuncSetAttribute(norm_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)nsmem));
   norm_kernel<K><<<(int)std::min<int64_t>(k, kNumSM * 8), 256, nsmem, st>>>(
-      k, dim, nleaf, sizes, prev_ptr, w.cl_seg, w.seg_key, w.seg_w, w.head, w.nrm, w.counts);
+      k, dim, nleaf, nint, P.nlevels, w.plan, sizes, prev_ptr, w.cl_seg, w.seg_key, w.seg_w,
+      w.head, w.nrm, w.counts);
   IVFKM_CHECK_LAUNCH();
   size_t cb = w.cub_bytes;
   IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.counts, new_ptr, (int)(k + 1), st));
@@ -434,7 +465,7 @@ int update_fill_impl(int64_t nnz, int64_t k, int64_t dim, const unsigned long lo
                      double* new_vals, uint8_t* retained, void* ws, size_t ws_bytes,
                      cudaStream_t st) {
   size_t need = 0;
-  UpdWs<K> w = carve_upd<K>(ws, nnz, k, &need);
+  UpdWs<K> w = carve_upd<K>(ws, nnz, k, dim, &need);
   if (ws_bytes < need) return IVFKM_E_WORKSPACE;
   const int T = 256;
   if (nnz > 0) {
@@ -454,8 +485,8 @@ int update_fill_impl(int64_t nnz, int64_t k, int64_t dim, const unsigned long lo
 extern "C" size_t ivfkm_update_workspace_size(int64_t /*n_obj*/, int64_t nnz, int64_t k,
                                               int64_t dim) {
   size_t total = 0;
-  if (use_k32(k, dim)) carve_upd<uint32_t>(nullptr, nnz, k, &total);
-  else carve_upd<unsigned long long>(nullptr, nnz, k, &total);
+  if (use_k32(k, dim)) carve_upd<uint32_t>(nullptr, nnz, k, dim, &total);
+  else carve_upd<unsigned long long>(nullptr, nnz, k, dim, &total);
   return total;
 }
 
