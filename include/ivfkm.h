@@ -208,6 +208,32 @@ int ivfkm_assign_ivf_host(int64_t n, const int64_t* indptr, const int32_t* terms
                           const int32_t* m_cids, const double* m_vals, int64_t k,
                           int32_t* labels, int64_t* ctr);
 
+/* ---- ingestion: the step before the path ---------
+ *   ivfkm_uci_parse   <- io.py:72-121   parse_uci_bow (host, multi-threaded)
+ *   ivfkm_bow_sort    <- io.py:120      triples.sort() + duplicate-pair check
+ *   ivfkm_bow_df      <- io.py:138      df = bincount(terms)
+ *   ivfkm_tfidf       <- io.py:141-174  weights, drops, L2 normalisation
+ * Parse errors are returned as data (line, code, values); the Python layer
+ * raises ParseError with the reference's wording.                          */
+int ivfkm_uci_parse(const char* text, size_t len, int threads, int64_t* header /*[3]*/,
+                    int64_t cap, int32_t* docs, int32_t* terms, int32_t* counts,
+                    int64_t* lines, int64_t* n_read, int64_t* n_lines, int64_t* err_line,
+                    int* err_code, int64_t* err_val /*[3]*/);
+size_t ivfkm_bow_workspace_size(int64_t n);
+int ivfkm_bow_sort(int64_t n, int64_t n_docs, int64_t dim, int32_t* docs /*[dev]*/,
+                   int32_t* terms /*[dev]*/, int32_t* counts /*[dev]*/, int64_t* lines /*[dev]*/,
+                   unsigned long long* dup_line /*[dev] 1*/, void* ws, size_t ws_bytes,
+                   ivfkm_stream_t stream);
+int ivfkm_bow_df(int64_t n, int64_t dim, const int32_t* terms /*[dev]*/,
+                 unsigned long long* df /*[dev] dim*/, ivfkm_stream_t stream);
+size_t ivfkm_tfidf_workspace_size(int64_t n, int64_t n_docs);
+int ivfkm_tfidf(int64_t n, int64_t n_docs, int64_t dim, const int32_t* docs /*[dev]*/,
+                const int32_t* terms /*[dev]*/, const int32_t* counts /*[dev]*/,
+                const double* idf /*[dev] dim*/, int64_t* out_ptr /*[dev] n_docs+1*/,
+                int32_t* out_terms /*[dev] n*/, double* out_vals /*[dev] n*/,
+                int32_t* dropped /*[dev] n_docs*/, int64_t* counts_out /*[host] 2*/, void* ws,
+                size_t ws_bytes, ivfkm_stream_t stream);
+
 /* ---- host utilities -------------------------------------------------------*/
 uint64_t ivfkm_fnv1a64(const void* data, size_t nbytes); /* variants.py:77-83 */
 

@@ -77,6 +77,14 @@ SIGNATURES = {
                                     _vp, _i64, _vp, _sz, _vp]),
     "ivfkm_assign_ivf_host": (C.c_int, [_i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp,
                                         _vp]),
+    "ivfkm_uci_parse": (C.c_int, [_vp, _sz, C.c_int, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp,
+                                  _vp, _vp, _vp]),
+    "ivfkm_bow_workspace_size": (_sz, [_i64]),
+    "ivfkm_bow_sort": (C.c_int, [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "ivfkm_bow_df": (C.c_int, [_i64, _i64, _vp, _vp, _vp]),
+    "ivfkm_tfidf_workspace_size": (_sz, [_i64, _i64]),
+    "ivfkm_tfidf": (C.c_int, [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                              _vp, _sz, _vp]),
     "ivfkm_fnv1a64": (_u64, [_vp, _sz]),
     "ivfkm_synth_rows": (C.c_int, [C.POINTER(SynthSpec), _vp]),
     "ivfkm_synth_fill": (C.c_int, [C.POINTER(SynthSpec), _vp, _vp, _vp, _vp,
