@@ -109,6 +109,8 @@ class ShardComm:
     def route_rows(self, rows: Rows, k: int) -> Rows:
         """Send each row to the owner of its label's cluster range; the result
         holds the owner's rows in ascending global object order."""
+        if self.world == 1:  # the only rank owns every cluster: nothing moves
+            return rows
         dev = rows.row_ptr.device
         bounds = cluster_owner_bounds(k, self.world).to(dev)
         lab = rows.labels.to(torch.int64)
