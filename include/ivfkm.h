@@ -150,7 +150,12 @@ int ivfkm_assign(int64_t n_obj, const int64_t* row_ptr /*[dev] n+1*/,
                  const int32_t* prev_labels /*[dev] n or NULL*/, int32_t* labels /*[dev] n*/,
                  double* sims /*[dev] n*/, unsigned long long* sizes /*[dev] k*/,
                  ivfkm_stats* stats /*[dev]*/, const int32_t* order /*[dev] n or NULL*/,
-                 void* ws, size_t ws_bytes, ivfkm_stream_t stream);
+                 int label_rule, void* ws, size_t ws_bytes, ivfkm_stream_t stream);
+/* label_rule 0: IVF — argmax from -inf, smallest index among maximizers
+ * (_kernels.pyx:17-26); 1: IVFD — the argmax only if its similarity beats
+ * 0.0, else mean 0 (_kernels.pyx:178-207, rho_max starts at 0.0).  The
+ * similarities (and so the objective) are the same float64 values for both
+ * variants: both add the products in ascending term order.                */
 
 /* The two halves of ivfkm_assign, for callers that time the fp32 screen
  * (the dominant kernel) separately: screen zeroes *stats and fills the
@@ -165,8 +170,8 @@ int ivfkm_assign_screen(int64_t n_obj, const int64_t* row_ptr, const int32_t* te
 int ivfkm_assign_finish(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
                         const double* val64, int64_t k, int64_t dim, const uint32_t* headers,
                         const double* pval64, const int32_t* prev_labels, int32_t* labels,
-                        double* sims, unsigned long long* sizes, ivfkm_stats* stats, void* ws,
-                        size_t ws_bytes, ivfkm_stream_t stream);
+                        double* sims, unsigned long long* sizes, ivfkm_stats* stats,
+                        int label_rule, void* ws, size_t ws_bytes, ivfkm_stream_t stream);
 
 /* Exact float64 similarity of every object to the mean its (0-based) label
  * names — the summand of objective_cosine (clustering.py:105-119) — written
@@ -207,6 +212,15 @@ int ivfkm_assign_ivf_host(int64_t n, const int64_t* indptr, const int32_t* terms
                           const double* vals, int64_t dim, const int64_t* m_indptr,
                           const int32_t* m_cids, const double* m_vals, int64_t k,
                           int32_t* labels, int64_t* ctr);
+/* The IVFD entry of the same kernel-module ABI (_kernels.pyx:178-207):
+ * objects as their inverted file (x_indptr[dim+1], 1-based object ids),
+ * means mean-major (m_indptr[k+1], 1-based terms); labels by the IVFD rule
+ * (include note at ivfkm_assign).  The reference's rho / rho_max scratch
+ * arrays are not needed.                                                    */
+int ivfkm_assign_ivfd_host(int64_t n, const int64_t* x_indptr, const int32_t* x_oids,
+                           const double* x_vals, int64_t dim, const int64_t* m_indptr,
+                           const int32_t* m_terms, const double* m_vals, int64_t k,
+                           int32_t* labels, int64_t* ctr);
 
 /* ---- ingestion: the step before the path ---------
  *   ivfkm_uci_parse   <- io.py:72-121   parse_uci_bow (host, multi-threaded)

@@ -312,9 +312,13 @@ class OracleRun:
     final_labels: np.ndarray
 
 
-def run_ivf(ds, k, seed, max_iter=50, epsilon=None, threads=1, means=None) -> OracleRun:
+def run_ivf(ds, k, seed, max_iter=50, epsilon=None, threads=1, means=None,
+            variant="IVF") -> OracleRun:
     """clustering.py:229-315 for variant IVF (records hold the means that
-    produced each assignment; convergence is tested before the update)."""
+    produced each assignment; convergence is tested before the update).
+    variant="IVFD": the same similarities (IVFD adds the products in the
+    same ascending term order), labels by _kernels.pyx:178-207 — the argmax
+    only when it beats 0.0 (rho_max starts at 0.0), else mean 1."""
     m = means if means is not None else init_means(ds, k, seed)
     iters = []
     prev = None
@@ -322,6 +326,8 @@ def run_ivf(ds, k, seed, max_iter=50, epsilon=None, threads=1, means=None) -> Or
     converged = False
     for r in range(1, max_iter + 1):
         labels, top1, top2, post = assign(ds, m, threads)
+        if variant == "IVFD":
+            labels = np.where(top1 > 0.0, labels, 1).astype(np.int32)
         obj = objective(ds, labels, m)
         iters.append(OracleIter(r, obj, fnv1a64(labels), post, m.sum_terms, labels, top1, top2, m))
         if prev is not None and np.array_equal(labels, prev):

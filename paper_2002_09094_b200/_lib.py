@@ -61,13 +61,12 @@ SIGNATURES = {
     "ivfkm_row_order_workspace_size": (_sz, [_i64]),
     "ivfkm_row_order": (C.c_int, [_i64, _vp, _vp, _vp, _sz, _vp]),
     "ivfkm_assign": (C.c_int, [_i64, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, C.c_int, _vp,
-                               _f64,
-                               _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+                               _f64, _vp, _vp, _vp, _vp, _vp, _vp, C.c_int, _vp, _sz, _vp]),
     "ivfkm_assign_screen": (C.c_int, [_i64, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, C.c_int,
                                       _f64, _vp,
                                       _vp, _vp, _sz, _vp]),
     "ivfkm_assign_finish": (C.c_int, [_i64, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp,
-                                      _vp, _vp, _vp, _sz, _vp]),
+                                      _vp, _vp, C.c_int, _vp, _sz, _vp]),
     "ivfkm_score_labels": (C.c_int, [_i64, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp,
                                      _vp]),
     "ivfkm_update_workspace_size": (_sz, [_i64, _i64, _i64, _i64]),
@@ -85,6 +84,8 @@ SIGNATURES = {
     "ivfkm_tfidf_workspace_size": (_sz, [_i64, _i64]),
     "ivfkm_tfidf": (C.c_int, [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                               _vp, _sz, _vp]),
+    "ivfkm_assign_ivfd_host": (C.c_int, [_i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp,
+                                         _vp]),
     "ivfkm_fnv1a64": (_u64, [_vp, _sz]),
     "ivfkm_synth_rows": (C.c_int, [C.POINTER(SynthSpec), _vp]),
     "ivfkm_synth_fill": (C.c_int, [C.POINTER(SynthSpec), _vp, _vp, _vp, _vp,

@@ -58,6 +58,33 @@ def assign_ivf(indptr, terms, vals, m_indptr, m_cids, m_vals, rho, labels, ctr) 
     ctr[:3] += c[:3]
 
 
+def assign_ivfd(x_indptr, x_oids, x_vals, m_indptr, m_terms, m_vals, rho, rho_max, labels,
+                ctr) -> None:
+    """_kernels.pyx:178-207: objects given as their inverted file, means
+    mean-major; ``rho`` / ``rho_max`` scratch accepted and left untouched."""
+    lib = _lib.load()
+    xp, p_xp = _arr(x_indptr, np.int64)
+    xo, p_xo = _arr(x_oids, np.int32)
+    xv, p_xv = _arr(x_vals, np.float64)
+    mp, p_mp = _arr(m_indptr, np.int64)
+    mt, p_mt = _arr(m_terms, np.int32)
+    mv, p_mv = _arr(m_vals, np.float64)
+    n = int(np.asarray(rho).shape[0])
+    dim = xp.size - 1
+    k = mp.size - 1
+    out = np.empty(n, dtype=np.int32)
+    c = np.zeros(5, dtype=np.int64)
+    rc = lib.ivfkm_assign_ivfd_host(n, p_xp, p_xo, p_xv, dim, p_mp, p_mt, p_mv, k,
+                                    C.c_void_p(out.ctypes.data), C.c_void_p(c.ctypes.data))
+    if rc == -6:
+        from .types import CorruptionError
+
+        raise CorruptionError("posting id outside its owner range")
+    _lib.check(rc, "ivfkm_assign_ivfd_host")
+    labels[:] = out
+    ctr[:3] += c[:3]
+
+
 def register(kernels_module) -> None:
     """Add this backend to a reference ``sparse_kmeans.kernels`` registry."""
     kernels_module._MODULES[BACKEND_NAME] = __import__(__name__, fromlist=["x"])

@@ -1102,7 +1102,15 @@ struct FinalParams {
   double* sims;
   int32_t* ovf_list;
   unsigned int* ovf_len;
+  int rule;  // 0: IVF argmax (_kernels.pyx:17-26); 1: IVFD (_kernels.pyx:178-207)
 };
+
+// IVFD keeps a label only when its similarity beats 0.0 (rho_max starts at
+// 0.0 and label at 1, strict '>', _kernels.pyx:190-205): otherwise mean 0,
+// whose exact similarity is then the objective summand.
+__device__ __forceinline__ bool ivfd_falls_back(const FinalParams& p, double best, int c) {
+  return p.rule == 1 && !(best > 0.0) && c != 0;
+}
 
 __global__ void __launch_bounds__(256) finalize_kernel(FinalParams p) {
   __shared__ __align__(16) double s_scr[8][64];
@@ -1113,8 +1121,12 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalParams p) {
     const int64_t rb = p.x.row_ptr[i], re = p.x.row_ptr[i + 1];
     const int slot = p.slot_of[i];
     if (slot < 0) {
-      const int c = p.label32[i];
-      const double s = exact_score_warp(p.x, rb, re, c, lane, scratch);
+      int c = p.label32[i];
+      double s = exact_score_warp(p.x, rb, re, c, lane, scratch);
+      if (ivfd_falls_back(p, s, c)) {
+        c = 0;
+        s = exact_score_warp(p.x, rb, re, 0, lane, scratch);
+      }
       if (lane == 0) {
         p.labels[i] = c;
         p.sims[i] = s;
@@ -1135,6 +1147,10 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalParams p) {
         bv = s;
         bc = c;
       }
+    }
+    if (ivfd_falls_back(p, bv, bc)) {
+      bc = 0;
+      bv = exact_score_warp(p.x, rb, re, 0, lane, scratch);
     }
     if (lane == 0) {
       p.labels[i] = bc;
@@ -1194,6 +1210,10 @@ __global__ void __launch_bounds__(1024) overflow_kernel(FinalParams p, int64_t k
           bv = rv[w];
           bc = rc[w];
         }
+      if (ivfd_falls_back(p, bv, bc)) {
+        bc = 0;
+        bv = exact_score_thread(p.x, rb, re, 0);
+      }
       p.labels[i] = bc;
       p.sims[i] = bv;
     }
@@ -1537,9 +1557,11 @@ int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
 }
 
 int finish_impl(const AssignArgs& a, const AssignWs& w, const int32_t* prev_labels,
-                int32_t* labels, double* sims, unsigned long long* sizes, cudaStream_t st) {
+                int32_t* labels, double* sims, unsigned long long* sizes, int rule,
+                cudaStream_t st) {
   FinalParams fp;
   fp.n_obj = a.n_obj;
+  fp.rule = rule;
   fp.x.row_ptr = a.row_ptr;
   fp.x.terms = a.terms;
   fp.x.val64 = a.val64;
@@ -1596,10 +1618,11 @@ extern "C" int ivfkm_assign_finish(int64_t n_obj, const int64_t* row_ptr, const 
                                    const double* val64, int64_t k, int64_t dim,
                                    const uint32_t* headers, const double* pval64,
                                    const int32_t* prev_labels, int32_t* labels, double* sims,
-                                   unsigned long long* sizes, ivfkm_stats* stats, void* ws,
-                                   size_t ws_bytes, ivfkm_stream_t stream_) {
+                                   unsigned long long* sizes, ivfkm_stats* stats, int label_rule,
+                                   void* ws, size_t ws_bytes, ivfkm_stream_t stream_) {
   if (n_obj < 0 || k < 1 || dim < 1 || !row_ptr || !labels || !sims || !stats || !headers)
     return IVFKM_E_ARG;
+  if (label_rule != 0 && label_rule != 1) return IVFKM_E_ARG;
   size_t need = 0;
   AssignWs w = carve_assign(ws, n_obj, &need);
   if (ws_bytes < need) return IVFKM_E_WORKSPACE;
@@ -1608,7 +1631,7 @@ extern "C" int ivfkm_assign_finish(int64_t n_obj, const int64_t* row_ptr, const 
   if (n_obj == 0) return IVFKM_OK;
   AssignArgs a{n_obj,   row_ptr, terms, nullptr, val64, nullptr, k,      dim,
                headers, nullptr, 32,    pval64,  0.0,   stats,   nullptr};
-  return finish_impl(a, w, prev_labels, labels, sims, sizes, st);
+  return finish_impl(a, w, prev_labels, labels, sims, sizes, label_rule, st);
 }
 
 extern "C" int ivfkm_assign(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
@@ -1617,14 +1640,14 @@ extern "C" int ivfkm_assign(int64_t n_obj, const int64_t* row_ptr, const int32_t
                             const void* pval_screen, int screen_bits, const double* pval64,
                             double mu_max, const int32_t* prev_labels,
                             int32_t* labels, double* sims, unsigned long long* sizes,
-                            ivfkm_stats* stats, const int32_t* order, void* ws, size_t ws_bytes,
-                            ivfkm_stream_t stream_) {
+                            ivfkm_stats* stats, const int32_t* order, int label_rule, void* ws,
+                            size_t ws_bytes, ivfkm_stream_t stream_) {
   int rc = ivfkm_assign_screen(n_obj, row_ptr, terms, val32, xnorm, k, dim, headers,
                                pval_screen, screen_bits, mu_max, stats, order, ws, ws_bytes,
                                stream_);
   if (rc) return rc;
   return ivfkm_assign_finish(n_obj, row_ptr, terms, val64, k, dim, headers, pval64, prev_labels,
-                             labels, sims, sizes, stats, ws, ws_bytes, stream_);
+                             labels, sims, sizes, stats, label_rule, ws, ws_bytes, stream_);
 }
 
 extern "C" int ivfkm_score_labels(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,

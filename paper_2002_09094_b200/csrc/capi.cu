@@ -59,17 +59,19 @@ struct DevBuf {
 
 }  // namespace
 
-// Same arguments and meaning as the reference kernel (1-based ids, float64
-// values, labels written 1-based, ctr[0..2] += postings).  The reference's
-// rho scratch argument is not needed: rho lives in registers on the device.
-extern "C" int ivfkm_assign_ivf_host(int64_t n, const int64_t* indptr, const int32_t* terms,
-                                     const double* vals, int64_t dim, const int64_t* m_indptr,
-                                     const int32_t* m_cids, const double* m_vals, int64_t k,
-                                     int32_t* labels, int64_t* ctr) {
+namespace {
+
+// Host buffers -> device -> labels: objects as a CSR (1-based terms), means
+// as term-major postings (major 1: rows = terms, cols = 1-based mean ids) or
+// mean-major rows (major 0: rows = means, cols = 1-based terms).
+int assign_host(int64_t n, const int64_t* indptr, const int32_t* terms, const double* vals,
+                int64_t dim, int major, const int64_t* m_indptr, const int32_t* m_cids,
+                const double* m_vals, int64_t k, int rule, int32_t* labels, int64_t* ctr) {
   if (n < 0 || dim < 1 || k < 1 || !indptr || !m_indptr || !labels) return IVFKM_E_ARG;
+  const int64_t m_rows = major == 1 ? dim : k;
   if (ivfkm_device_count() < 1) return IVFKM_E_NOGPU;
   const int64_t nnz = indptr[n];
-  const int64_t mnz = m_indptr[dim];
+  const int64_t mnz = m_indptr[m_rows];
   // validation the reference performs before its kernel (data.py:148-175,
   // data.py:261-262 CorruptionError), restated on the host buffers
   std::vector<int32_t> t0((size_t)nnz), c0((size_t)mnz);
@@ -79,9 +81,15 @@ extern "C" int ivfkm_assign_ivf_host(int64_t n, const int64_t* indptr, const int
   }
   std::vector<double> mnorm2((size_t)k, 0.0);
   for (int64_t q = 0; q < mnz; ++q) {
-    if (m_cids[q] < 1 || m_cids[q] > k) return IVFKM_E_RANGE;
+    const int64_t lim = major == 1 ? k : dim;  // cols: mean ids or terms
+    if (m_cids[q] < 1 || m_cids[q] > lim) return IVFKM_E_RANGE;
     c0[q] = m_cids[q] - 1;
-    mnorm2[c0[q]] += m_vals[q] * m_vals[q];
+  }
+  for (int64_t r = 0; r < m_rows; ++r) {
+    for (int64_t q = m_indptr[r]; q < m_indptr[r + 1]; ++q) {
+      const int64_t c = major == 1 ? c0[q] : r;
+      mnorm2[c] += m_vals[q] * m_vals[q];
+    }
   }
   double mu_max = 0.0;
   for (double v : mnorm2) mu_max = std::fmax(mu_max, std::sqrt(v));
@@ -104,7 +112,7 @@ extern "C" int ivfkm_assign_ivf_host(int64_t n, const int64_t* indptr, const int
   IVFKM_TRY(d_v32.alloc(sizeof(float) * nnz));
   IVFKM_TRY(d_v64.alloc(sizeof(double) * nnz));
   IVFKM_TRY(d_xn.alloc(sizeof(double) * n));
-  IVFKM_TRY(d_mp.alloc(sizeof(int64_t) * (dim + 1)));
+  IVFKM_TRY(d_mp.alloc(sizeof(int64_t) * (m_rows + 1)));
   IVFKM_TRY(d_mc.alloc(sizeof(int32_t) * mnz));
   IVFKM_TRY(d_mv.alloc(sizeof(double) * mnz));
   IVFKM_TRY(d_hdr.alloc(sizeof(uint32_t) * ivfkm_bivf_headers_size(k, dim)));
@@ -120,26 +128,26 @@ extern "C" int ivfkm_assign_ivf_host(int64_t n, const int64_t* indptr, const int
   IVFKM_TRY(cudaMemcpyAsync(d_v32.p, v32.data(), sizeof(float) * nnz, cudaMemcpyHostToDevice, st));
   IVFKM_TRY(cudaMemcpyAsync(d_v64.p, vals, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
   IVFKM_TRY(cudaMemcpyAsync(d_xn.p, xn.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
-  IVFKM_TRY(cudaMemcpyAsync(d_mp.p, m_indptr, sizeof(int64_t) * (dim + 1), cudaMemcpyHostToDevice, st));
+  IVFKM_TRY(cudaMemcpyAsync(d_mp.p, m_indptr, sizeof(int64_t) * (m_rows + 1), cudaMemcpyHostToDevice, st));
   IVFKM_TRY(cudaMemcpyAsync(d_mc.p, c0.data(), sizeof(int32_t) * mnz, cudaMemcpyHostToDevice, st));
   IVFKM_TRY(cudaMemcpyAsync(d_mv.p, m_vals, sizeof(double) * mnz, cudaMemcpyHostToDevice, st));
   // fp16 screen values (half the posting bytes) unless the means are not
   // normalised far beyond unit norm (fp16 range)
   const int bits = mu_max <= 32768.0 ? 16 : 32;
   int64_t total = 0;
-  int rc = ivfkm_bivf_plan(k, dim, 1, dim, d_mp.as<int64_t>(), d_mc.as<int32_t>(),
+  int rc = ivfkm_bivf_plan(k, dim, major, m_rows, d_mp.as<int64_t>(), d_mc.as<int32_t>(),
                            d_hdr.as<uint32_t>(), &total, d_bws.p, bws, nullptr);
   if (rc) return rc;
   IVFKM_TRY(d_p32.alloc(sizeof(float) * (total + 1)));
   IVFKM_TRY(d_p64.alloc(sizeof(double) * (total + 1)));
-  rc = ivfkm_bivf_fill(k, dim, 1, dim, d_mp.as<int64_t>(), d_mc.as<int32_t>(), d_mv.as<double>(),
+  rc = ivfkm_bivf_fill(k, dim, major, m_rows, d_mp.as<int64_t>(), d_mc.as<int32_t>(), d_mv.as<double>(),
                        d_hdr.as<uint32_t>(), d_p32.p, bits, d_p64.as<double>(), nullptr);
   if (rc) return rc;
   rc = ivfkm_assign(n, d_ip.as<int64_t>(), d_t.as<int32_t>(), d_v32.as<float>(),
                     d_v64.as<double>(), d_xn.as<double>(), k, dim, d_hdr.as<uint32_t>(),
                     d_p32.p, bits, d_p64.as<double>(), mu_max, nullptr, d_lab.as<int32_t>(),
                     d_sims.as<double>(), d_sizes.as<unsigned long long>(),
-                    d_stats.as<ivfkm_stats>(), nullptr, d_aws.p, aws, nullptr);
+                    d_stats.as<ivfkm_stats>(), nullptr, rule, d_aws.p, aws, nullptr);
   if (rc) return rc;
   ivfkm_stats stats;
   IVFKM_TRY(cudaMemcpyAsync(labels, d_lab.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
@@ -152,4 +160,46 @@ extern "C" int ivfkm_assign_ivf_host(int64_t n, const int64_t* indptr, const int
     ctr[2] += (int64_t)stats.postings;
   }
   return IVFKM_OK;
+}
+
+}  // namespace
+
+// Same arguments and meaning as the reference kernel (1-based ids, float64
+// values, labels written 1-based, ctr[0..2] += postings).  The reference's
+// rho scratch argument is not needed: rho lives in registers on the device.
+extern "C" int ivfkm_assign_ivf_host(int64_t n, const int64_t* indptr, const int32_t* terms,
+                                     const double* vals, int64_t dim, const int64_t* m_indptr,
+                                     const int32_t* m_cids, const double* m_vals, int64_t k,
+                                     int32_t* labels, int64_t* ctr) {
+  return assign_host(n, indptr, terms, vals, dim, 1, m_indptr, m_cids, m_vals, k, 0, labels, ctr);
+}
+
+// IVFD (_kernels.pyx:178-207): objects arrive as their inverted file
+// (x_indptr over terms, 1-based object ids), means mean-major.  The object
+// postings are transposed back to rows on the host (terms ascending per row,
+// as the reference's per-object sums run), then the IVF kernels run with the
+// IVFD label rule.
+extern "C" int ivfkm_assign_ivfd_host(int64_t n, const int64_t* x_indptr, const int32_t* x_oids,
+                                      const double* x_vals, int64_t dim, const int64_t* m_indptr,
+                                      const int32_t* m_terms, const double* m_vals, int64_t k,
+                                      int32_t* labels, int64_t* ctr) {
+  if (n < 0 || dim < 1 || k < 1 || !x_indptr || !m_indptr || !labels) return IVFKM_E_ARG;
+  const int64_t nnz = x_indptr[dim];
+  std::vector<int64_t> ip((size_t)n + 1, 0);
+  for (int64_t q = 0; q < nnz; ++q) {
+    if (x_oids[q] < 1 || x_oids[q] > n) return IVFKM_E_RANGE;
+    ++ip[(size_t)x_oids[q]];
+  }
+  for (int64_t i = 0; i < n; ++i) ip[i + 1] += ip[i];
+  std::vector<int64_t> cur(ip.begin(), ip.end() - 1);
+  std::vector<int32_t> t((size_t)nnz);
+  std::vector<double> v((size_t)nnz);
+  for (int64_t term = 0; term < dim; ++term)
+    for (int64_t q = x_indptr[term]; q < x_indptr[term + 1]; ++q) {
+      const int64_t o = cur[x_oids[q] - 1]++;
+      t[o] = (int32_t)(term + 1);
+      v[o] = x_vals[q];
+    }
+  return assign_host(n, ip.data(), t.data(), v.data(), dim, 0, m_indptr, m_terms, m_vals, k, 1,
+                     labels, ctr);
 }

@@ -247,11 +247,14 @@ class LloydEngine:
         return self.build_bivf(DeviceMeans.from_meanset(ms, self.device))
 
     # -- assign --------------------------------------------------------------
-    def assign(self, dm: DeviceMeans, prev: torch.Tensor | None, events=None) -> torch.Tensor:
+    def assign(self, dm: DeviceMeans, prev: torch.Tensor | None, events=None,
+               rule: int = 0) -> torch.Tensor:
         """Launch the assignment step; returns the (device) 0-based labels.
 
         ``events``: optional (start, end) torch.cuda.Event pair recorded around
-        the fp32 screen kernel (the dominant kernel) on the current stream.
+        the screen kernel (the dominant kernel) on the current stream.
+        ``rule``: 0 = IVF argmax, 1 = IVFD (argmax only above 0.0, else mean 0;
+        see include/ivfkm.h).
         """
         dd = self.dd
         out = self.labels[self.cur]
@@ -274,7 +277,7 @@ class LloydEngine:
         rc = self.lib.ivfkm_assign_finish(dd.n, _p(dd.row_ptr), _p(dd.terms), _p(dd.val64),
                                           self.k, dd.dim, _p(dm.headers), _p(dm.pv64), _p(prev),
                                           _p(out), _p(self.sims), _p(self.sizes), _p(self.stats),
-                                          _p(self.ws_assign), self.ws_assign.numel(), st)
+                                          rule, _p(self.ws_assign), self.ws_assign.numel(), st)
         _lib.check(rc, "ivfkm_assign_finish")
         self.launches += 4
         return out

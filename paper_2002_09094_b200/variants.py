@@ -6,7 +6,13 @@
   touched in mults/adds/inner_entries exactly like _kernels.pyx:126-128.
 * ``update_ivf(ds, asg, prev)`` <- variants.py:310-312 (update_means
   :254-307): bit-identical means, empty clusters retained.
-* ``assign_step`` / ``update_step`` <- variants.py:219-234, 340-345 (IVF only).
+* ``assign_ivfd(ds, means, ...)`` <- variants.py:188-206 (IVFD): the same
+  exact similarities (both variants add the products in ascending term
+  order), the IVFD label rule (an argmax must beat 0.0, else mean 1,
+  _kernels.pyx:178-207); the object inverted file is not needed on the
+  device (accepted and checked like the reference).
+* ``update_sparse_standard`` <- variants.py:315-317 (IVFD's update).
+* ``assign_step`` / ``update_step`` <- variants.py:219-234, 340-345 (IVF, IVFD).
 
 The dataset is uploaded once and cached on the device by object identity
 (the reference arrays are immutable), so repeated calls on the same Dataset
@@ -23,7 +29,8 @@ import torch
 from .engine import DeviceDataset, DeviceMeans, LloydEngine
 from .types import Assignment, CorruptionError, MeanSet, OpCounters
 
-__all__ = ["assign_ivf", "update_ivf", "assign_step", "update_step", "Workspace", "engine_for"]
+__all__ = ["assign_ivf", "assign_ivfd", "update_ivf", "update_sparse_standard", "assign_step",
+           "update_step", "Workspace", "engine_for"]
 
 _ENGINES: dict[int, tuple[LloydEngine, object]] = {}
 
@@ -64,6 +71,21 @@ def assign_ivf(ds, means, counters: OpCounters | None = None, backend: str | Non
                workspace: Workspace | None = None) -> Assignment:
     """Scan of the means' per-term postings (variants.py:162-174) on the GPU."""
     _require(means, "sparse_inverted", "IVF")
+    return _assign(ds, means, counters, backend, rule=0)
+
+
+def assign_ivfd(ds, means, counters: OpCounters | None = None, backend: str | None = None,
+                workspace: Workspace | None = None, obj_inverted=None) -> Assignment:
+    """IVFD assignment (variants.py:188-206) on the GPU: same similarities as
+    IVF, the IVFD label rule (argmax only above 0.0, else mean 1)."""
+    _require(means, "sparse_standard", "IVFD")
+    if obj_inverted is not None and (obj_inverted.n_owners != ds.n
+                                     or obj_inverted.dim != ds.dim):
+        raise CorruptionError("object postings do not match the dataset")
+    return _assign(ds, means, counters, backend, rule=1)
+
+
+def _assign(ds, means, counters, backend, rule: int) -> Assignment:
     if ds.dim != means.dim:
         raise ValueError("dataset and means disagree on dim")
     if means.k < 1:
@@ -75,7 +97,7 @@ def assign_ivf(ds, means, counters: OpCounters | None = None, backend: str | Non
         raise CorruptionError("mean postings reference terms beyond dim")
     eng = engine_for(ds, means.k)
     dm = eng.upload_means(means)
-    lab = eng.assign(dm, None)
+    lab = eng.assign(dm, None, rule=rule)
     st = eng.read_stats()
     if counters is not None:
         counters.add_array([st.postings, st.postings, st.postings, 0, 0])
@@ -85,6 +107,15 @@ def assign_ivf(ds, means, counters: OpCounters | None = None, backend: str | Non
 
 def update_ivf(ds, asg, prev) -> MeanSet:
     """Update step emitting the means as per-term postings (variants.py:310-312)."""
+    return _update(ds, asg, prev, "sparse_inverted")
+
+
+def update_sparse_standard(ds, asg, prev) -> MeanSet:
+    """Update step emitting per-mean sorted sparse vectors (variants.py:315-317)."""
+    return _update(ds, asg, prev, "sparse_standard")
+
+
+def _update(ds, asg, prev, representation: str) -> MeanSet:
     k = prev.k
     if asg.k != k or asg.n != ds.n:
         raise ValueError("assignment does not match dataset and means")
@@ -93,17 +124,21 @@ def update_ivf(ds, asg, prev) -> MeanSet:
     lab = torch.from_numpy(np.ascontiguousarray(asg.labels, dtype=np.int32) - 1).to(eng.device)
     eng.sizes.copy_(torch.from_numpy(np.array(asg.sizes, dtype=np.int64)))
     new = eng.update(lab, dm)
-    return new.to_meanset("sparse_inverted")
+    return new.to_meanset(representation)
 
 
 def assign_step(variant, ds, means, counters=None, backend=None, workspace=None,
                 obj_inverted=None) -> Assignment:
+    if variant == "IVFD":
+        return assign_ivfd(ds, means, counters, backend, workspace, obj_inverted)
     if variant != "IVF":
         raise ValueError(f"unknown variant {variant!r} on the B200 path")
     return assign_ivf(ds, means, counters, backend, workspace)
 
 
 def update_step(variant, ds, asg, prev) -> MeanSet:
+    if variant == "IVFD":
+        return update_sparse_standard(ds, asg, prev)
     if variant != "IVF":
         raise ValueError(f"unknown variant {variant!r} on the B200 path")
     return update_ivf(ds, asg, prev)

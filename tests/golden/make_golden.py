@@ -46,14 +46,15 @@ def sha(*arrays) -> str:
     return h.hexdigest()
 
 
-def run_ref(ds, k, seed, max_iter, backend="compiled"):
-    res = sk.run("IVF", ds, k, seed=seed, max_iter=max_iter, backend=backend, keep_history=True)
+def run_ref(ds, k, seed, max_iter, backend="compiled", variant="IVF"):
+    res = sk.run(variant, ds, k, seed=seed, max_iter=max_iter, backend=backend,
+                 keep_history=True)
     return res
 
 
-def dump(name, ds, k, seed, max_iter, store_inputs=True, extra=None):
-    res = run_ref(ds, k, seed, max_iter)
-    res_py = run_ref(ds, k, seed, max_iter, backend="python")
+def dump(name, ds, k, seed, max_iter, store_inputs=True, extra=None, variant="IVF"):
+    res = run_ref(ds, k, seed, max_iter, variant=variant)
+    res_py = run_ref(ds, k, seed, max_iter, backend="python", variant=variant)
     assert [r.assignment_digest for r in res.records] == \
         [r.assignment_digest for r in res_py.records], "reference backends disagree"
     labels = np.stack([r.labels for r in res.records]).astype(np.int32)
@@ -66,7 +67,7 @@ def dump(name, ds, k, seed, max_iter, store_inputs=True, extra=None):
         gaps.append(t1 - t2)
     fm = res.final_means
     payload = dict(
-        k=k, seed=seed, max_iter=max_iter, dim=ds.dim,
+        variant=np.array(variant), k=k, seed=seed, max_iter=max_iter, dim=ds.dim,
         converged=res.converged, iterations=res.iterations,
         objectives=np.array(res.objectives, dtype=np.float64),
         digests=np.array([r.assignment_digest for r in res.records], dtype=np.uint64),
@@ -105,17 +106,28 @@ def ref_dataset(indptr, terms, vals, dim):
     return sk.Dataset(dim, indptr, terms, vals, normalized=True)
 
 
-def main():
+def main(only_ivfd=False):
     # 1) small synthetic with the config-0 distributions, several k
     spec = synth.CONFIGS[0]["corpus"].scaled(2000, 500, seed=7)
     ip, t, v, _ = synth.make_corpus(spec)
     ds = ref_dataset(ip, t, v, spec.dim)
-    for k in (8, 32, 128):
-        dump(f"small_k{k}", ds, k, seed=23, max_iter=30)
-    # 2) signed values (the reference allows any finite nonzero value)
     rng = np.random.default_rng(5)
     v2 = v * np.where(rng.random(v.size) < 0.3, -1.0, 1.0)
     ds2 = ref_dataset(ip, t, v2, spec.dim)
+    # IVFD (variants.py:188-206): same similarities, its own label rule; signed
+    # data makes the rule visible (objects whose best similarity is <= 0)
+    dump("small_k32_ivfd", ds, 32, seed=23, max_iter=30, variant="IVFD")
+    dump("signed_k16_ivfd", ds2, 16, seed=3, max_iter=20, variant="IVFD")
+    # half the values negative and few means: many objects have no positive
+    # similarity, so IVFD's "beat 0.0, else mean 1" rule decides their labels
+    v3 = v * np.where(np.random.default_rng(9).random(v.size) < 0.5, -1.0, 1.0)
+    dump("signed_k4_ivfd", ref_dataset(ip, t, v3, spec.dim), 4, seed=5, max_iter=15,
+         variant="IVFD")
+    if only_ivfd:
+        return
+    for k in (8, 32, 128):
+        dump(f"small_k{k}", ds, k, seed=23, max_iter=30)
+    # 2) signed values (the reference allows any finite nonzero value)
     dump("signed_k16", ds2, 16, seed=3, max_iter=20)
     # 3) duplicated rows -> duplicated means -> exact ties, empty (retained) clusters
     n0 = 300
@@ -137,4 +149,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    main(only_ivfd="--ivfd" in sys.argv)

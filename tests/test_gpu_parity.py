@@ -16,7 +16,8 @@ from conftest import R, golden_dataset, load_golden
 
 pytestmark = pytest.mark.gpu
 
-SMALL = ["small_k8", "small_k32", "small_k128", "signed_k16", "dups_k40"]
+SMALL = ["small_k8", "small_k32", "small_k128", "signed_k16", "dups_k40",
+         "small_k32_ivfd", "signed_k16_ivfd", "signed_k4_ivfd"]
 
 
 def _pkg():
@@ -109,6 +110,33 @@ def test_backend_shim_tiny(tiny, tiny_means):
     assert ctr.tolist() == [8, 8, 8, 0, 0]
 
 
+def test_backend_shim_ivfd_matches_oracle():
+    """The IVFD entry of the kernel-module ABI (_kernels.pyx:178-207): objects
+    as their inverted file, means mean-major; signed data so that the
+    "beat 0.0, else mean 1" rule decides some labels."""
+    from oracle import oracle as O
+    from paper_2002_09094_b200 import backend
+
+    g = load_golden("signed_k4_ivfd")
+    ds = golden_dataset(g)
+    om = O.init_means(ds, int(g["k"]), int(g["seed"]))
+    ol, top1, _, post = O.assign(ds, om)
+    want = np.where(top1 > 0.0, ol, 1)
+    assert (want != ol).sum() > 0  # the rule is exercised
+    # the object inverted file (term-major postings of the objects)
+    n = ds.n
+    owner = np.repeat(np.arange(1, n + 1, dtype=np.int32), np.diff(ds.indptr))
+    order = np.argsort(ds.term_ids, kind="stable")
+    x_ip = np.zeros(ds.dim + 1, np.int64)
+    np.cumsum(np.bincount(ds.term_ids, minlength=ds.dim + 1)[1:], out=x_ip[1:])
+    labels = np.zeros(n, np.int32)
+    ctr = np.zeros(5, np.int64)
+    backend.assign_ivfd(x_ip, owner[order], np.asarray(ds.values)[order], om.indptr,
+                        om.term_ids, om.values, np.zeros(n), np.zeros(n), labels, ctr)
+    assert np.array_equal(labels, want)
+    assert ctr[0] == post
+
+
 # ---------------------------------------------------------------- golden runs
 
 def _check_run_against_golden(res, g, final_by_sha=False):
@@ -141,8 +169,11 @@ def test_run_matches_reference_golden(name):
     P = _pkg()
     g = load_golden(name)
     ds = golden_dataset(g)
-    res = P.run("IVF", ds, int(g["k"]), seed=int(g["seed"]), max_iter=int(g["max_iter"]))
+    variant = str(g["variant"]) if "variant" in g else "IVF"
+    res = P.run(variant, ds, int(g["k"]), seed=int(g["seed"]), max_iter=int(g["max_iter"]))
     _check_run_against_golden(res, g)
+    assert res.final_means.representation == (
+        "sparse_standard" if variant == "IVFD" else "sparse_inverted")
     # the RunResult JSON record (clustering.py:206-226) equals the reference's,
     # byte for byte once serialised (backend name aside)
     import json

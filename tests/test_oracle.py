@@ -10,7 +10,8 @@ import pytest
 from conftest import R, golden_dataset, load_golden
 from oracle import oracle as O
 
-SMALL = ["small_k8", "small_k32", "small_k128", "signed_k16", "dups_k40"]
+SMALL = ["small_k8", "small_k32", "small_k128", "signed_k16", "dups_k40",
+         "small_k32_ivfd", "signed_k16_ivfd", "signed_k4_ivfd"]
 
 
 def _tiny():
@@ -86,7 +87,9 @@ def test_fnv1a64_known_answers():
 def test_oracle_run_matches_reference_golden(name):
     g = load_golden(name)
     ds = golden_dataset(g)
-    res = O.run_ivf(ds, int(g["k"]), int(g["seed"]), max_iter=int(g["max_iter"]))
+    variant = str(g["variant"]) if "variant" in g else "IVF"
+    res = O.run_ivf(ds, int(g["k"]), int(g["seed"]), max_iter=int(g["max_iter"]),
+                    variant=variant)
     assert len(res.iters) == int(g["iterations"])
     assert res.converged == bool(g["converged"])
     for i, it in enumerate(res.iters):
