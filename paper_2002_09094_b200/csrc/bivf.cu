@@ -46,7 +46,6 @@ struct BivfWs {
 // build options (ivfkm_set_bivf_options)
 float g_dense_fill = 1.0f / 32.0f;  // spans with >= fill*256 postings are stored dense
 int g_permute = 1;          // slots ordered by mean size
-int g_use_dpre = 1;  // (experiment switch, permute bit 1)
 
 uint32_t dense_threshold() {
   if (g_dense_fill > 1.0f) return 1u << 30;  // never
@@ -281,8 +280,7 @@ __global__ void bivf_perm_kernel(int64_t k, const int32_t* __restrict__ sorted,
 // One warp per term: postings (nc) and the dense prefix (dpre, bivf.cuh).
 __global__ void bivf_nc_kernel(int64_t dim, int64_t nblk, const unsigned int* __restrict__ masks,
                                const unsigned int* __restrict__ offs,
-                               unsigned int* __restrict__ nc, unsigned int* __restrict__ dpre,
-                               int use_dpre) {
+                               unsigned int* __restrict__ nc, unsigned int* __restrict__ dpre) {
   const int lane = threadIdx.x & 31;
   const int64_t wpb = blockDim.x >> 5;
   const int64_t nspan = nblk / kSpan;
@@ -303,7 +301,7 @@ __global__ void bivf_nc_kernel(int64_t dim, int64_t nblk, const unsigned int* __
     }
     if (lane == 0) {
       nc[t] = c;
-      dpre[t] = use_dpre ? (unsigned)pre : 0u;
+      dpre[t] = (unsigned)pre;
     }
   }
 }
@@ -318,7 +316,7 @@ extern "C" size_t ivfkm_bivf_workspace_size(int64_t dim, int64_t k) {
 
 extern "C" void ivfkm_set_bivf_options(float dense_fill, int permute) {
   if (dense_fill >= 1.0f / 32.0f) g_dense_fill = dense_fill;
-  if (permute >= 0 && permute <= 3) { g_permute = permute & 1; g_use_dpre = !(permute & 2); }
+  if (permute == 0 || permute == 1) g_permute = permute;
 }
 
 extern "C" int64_t ivfkm_bivf_headers_size(int64_t k, int64_t dim) {
@@ -398,8 +396,7 @@ int plan_layout(int64_t k, int64_t dim, uint32_t* headers, unsigned th, const Bi
                                                                            headers);
   IVFKM_CHECK_LAUNCH();
   bivf_nc_kernel<<<grid_for(dim, threads / 32), threads, 0, st>>>(dim, nblk, headers,
-                                                                 headers + nh, nc, dpre,
-                                                                 g_use_dpre);
+                                                                 headers + nh, nc, dpre);
   IVFKM_CHECK_LAUNCH();
   return IVFKM_OK;
 }
