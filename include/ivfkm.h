@@ -93,16 +93,19 @@ size_t ivfkm_bivf_workspace_size(int64_t dim, int64_t k);
  * Screen values: screen_bits = 32 stores them as fp32, 16 as fp16 (half the
  * bytes; the screen's error window widens accordingly, labels stay exact).
  *
+ * The exact (fp64) values are stored compactly — postings only, term-major,
+ * slot ascending — so val64 holds one value per input entry.
  * Two-step build (exact allocation): ivfkm_bivf_plan writes the headers,
- * synchronises the stream and returns in *total the number of values the
- * layout uses (raising the dense threshold itself if the 31-bit value offsets
+ * synchronises the stream and returns totals = (screen values, exact values)
+ * (raising the dense threshold itself if the 31-bit screen-value offsets
  * would overflow; IVFKM_E_RANGE on an out-of-range id); ivfkm_bivf_fill then
- * writes val_screen and val64 (total values each).
+ * writes val_screen (totals[0]) and val64 (totals[1]).
  * One-step build: ivfkm_bivf_build = plan + fill without a host round trip,
- * into buffers of ivfkm_bivf_values_capacity() values (ids not checked).    */
+ * into val_screen of ivfkm_bivf_values_capacity() values and val64 of one
+ * value per input entry (ids not checked).                                  */
 int ivfkm_bivf_plan(int64_t k, int64_t dim, int major, int64_t nrows,
                     const int64_t* ptr /*[dev] nrows+1*/, const int32_t* cols /*[dev]*/,
-                    uint32_t* headers /*[dev]*/, int64_t* total /*[host] out*/, void* ws,
+                    uint32_t* headers /*[dev]*/, int64_t* totals /*[host] out, 2*/, void* ws,
                     size_t ws_bytes, ivfkm_stream_t stream);
 int ivfkm_bivf_fill(int64_t k, int64_t dim, int major, int64_t nrows,
                     const int64_t* ptr /*[dev]*/, const int32_t* cols /*[dev]*/,

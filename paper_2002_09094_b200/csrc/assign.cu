@@ -1039,6 +1039,15 @@ __global__ void __launch_bounds__(512) screen_async_kernel(ScreenParams p) {
 // ---------------------------------------------------------------------------
 // exact float64 similarity of object rows to one mean, in the reference order
 
+// headers -> the exact-value lookup view (bivf.cuh: masks, perm, off64)
+BivfView exact_view(const uint32_t* headers, int64_t k, int64_t dim) {
+  const int64_t nb = ivfkm_bivf_nblk(k);
+  const int64_t nh = dim * nb;
+  const uint32_t* nc = headers + 2 * nh + 1;
+  return BivfView{nb, headers, nc + dim + 2 * k + dim,
+                  reinterpret_cast<const int32_t*>(nc + dim)};
+}
+
 struct ExactCtx {
   const int64_t* row_ptr;
   const int32_t* terms;
@@ -1565,11 +1574,7 @@ int finish_impl(const AssignArgs& a, const AssignWs& w, const int32_t* prev_labe
   fp.x.row_ptr = a.row_ptr;
   fp.x.terms = a.terms;
   fp.x.val64 = a.val64;
-  {
-    const int64_t nb = ivfkm_bivf_nblk(a.k);
-    fp.x.bv = BivfView{nb, a.headers, a.headers + a.dim * nb,
-                       reinterpret_cast<const int32_t*>(a.headers + 2 * a.dim * nb + 1 + a.dim)};
-  }
+  fp.x.bv = exact_view(a.headers, a.k, a.dim);
   fp.x.pv64 = a.pval64;
   fp.label32 = w.label32;
   fp.slot_of = w.slot_of;
@@ -1663,11 +1668,7 @@ extern "C" int ivfkm_score_labels(int64_t n_obj, const int64_t* row_ptr, const i
   x.row_ptr = row_ptr;
   x.terms = terms;
   x.val64 = val64;
-  {
-    const int64_t nb = ivfkm_bivf_nblk(k);
-    x.bv = BivfView{nb, headers, headers + dim * nb,
-                    reinterpret_cast<const int32_t*>(headers + 2 * dim * nb + 1 + dim)};
-  }
+  x.bv = exact_view(headers, k, dim);
   x.pv64 = pval64;
   score_labels_kernel<<<grid_for(n_obj, 8), 256, 0, st>>>(n_obj, x, labels, sims);
   IVFKM_CHECK_LAUNCH();

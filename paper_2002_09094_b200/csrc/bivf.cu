@@ -35,6 +35,7 @@ struct BivfWs {
   unsigned long long* tot64;  // total values, 64-bit (overflow check of the 32-bit offsets)
   unsigned int* cnt;
   unsigned int* off;
+  unsigned int* cnt64;  // postings per block (compact exact-value layout)
   unsigned int* key_a;  // k: descending-size keys
   unsigned int* key_b;
   int32_t* id_a;        // k: mean ids
@@ -68,6 +69,7 @@ BivfWs carve(void* base, int64_t dim, int64_t k, size_t* total) {
   w.tot64 = c.take<unsigned long long>(1);
   w.cnt = c.take<unsigned int>(nh + 1);
   w.off = c.take<unsigned int>(nh + 1);
+  w.cnt64 = c.take<unsigned int>(nh + 1);
   w.key_a = c.take<unsigned int>(k);
   w.key_b = c.take<unsigned int>(k);
   w.id_a = c.take<int32_t>(k);
@@ -141,6 +143,7 @@ __global__ void bivf_mask_kernel(int major, int64_t nrows, const int64_t* __rest
 // padded to a multiple of 8 values on the last block (16 B of fp16 values).
 __global__ void bivf_count_kernel(int64_t nh, const unsigned int* __restrict__ masks,
                                   unsigned int dense_th, unsigned int* __restrict__ cnt,
+                                  unsigned int* __restrict__ cnt64,
                                   unsigned long long* __restrict__ tot64) {
   const int64_t nspan = nh / kSpan;
   unsigned long long mine = 0;
@@ -148,12 +151,14 @@ __global__ void bivf_count_kernel(int64_t nh, const unsigned int* __restrict__ m
        sp += (int64_t)gridDim.x * blockDim.x) {
     if (sp == nspan) {
       cnt[nh] = 0u;
+      cnt64[nh] = 0u;
       continue;
     }
     unsigned c[kSpan], tot = 0;
 #pragma unroll
     for (int r = 0; r < kSpan; ++r) {
       c[r] = __popc(masks[sp * kSpan + r]);
+      cnt64[sp * kSpan + r] = c[r];
       tot += c[r];
     }
     const bool dense = tot >= dense_th;
@@ -194,17 +199,19 @@ __global__ void bivf_scatter_kernel(int major, int64_t nrows, const int64_t* __r
                                     const int32_t* __restrict__ perm,
                                     float* __restrict__ v32, double* __restrict__ v64, int half) {
   const int64_t nh = bivf_nh(dim, nblk);
+  const unsigned int* off64 = hdr + 2 * nh + 1 + dim + 2 * k + dim;
   for_each_entry(nrows, ptr, [&](int64_t r, int64_t q) {
     const int64_t col = cols[q];
     const int64_t c = major == 0 ? r : col;
     const int64_t t = major == 0 ? col : r;
     if (c < 0 || c >= k || t < 0 || t >= dim) return;
-    // bivf_find / bivf_find16 in one: the positions differ only in dense spans
     const int64_t s = perm[c];
     const int64_t b = s >> 5;
     const uint32_t j = (uint32_t)(s & 31);
     const uint32_t m = hdr[t * nblk + b];
     const uint32_t o = hdr[nh + t * nblk + b];
+    const uint32_t below = (uint32_t)__popc(m & ((1u << j) - 1u));
+    // screen positions (fp32 and fp16 differ only inside dense spans)
     int64_t pos, pos16;
     if (o & kDense) {
       const uint32_t rr = (uint32_t)(b & (kSpan - 1));
@@ -212,7 +219,7 @@ __global__ void bivf_scatter_kernel(int major, int64_t nrows, const int64_t* __r
       pos = sb + 128u * (rr >> 2) + 4u * j + (rr & 3u);
       pos16 = sb + 8u * j + rr;
     } else {
-      pos = pos16 = o + (uint32_t)__popc(m & ((1u << j) - 1u));
+      pos = pos16 = o + below;
     }
     const double v = vals[q];
     if (half) {
@@ -220,21 +227,20 @@ __global__ void bivf_scatter_kernel(int major, int64_t nrows, const int64_t* __r
     } else {
       v32[pos] = static_cast<float>(v);
     }
-    v64[pos] = v;
+    v64[(int64_t)off64[t * nblk + b] + below] = v;  // compact exact-value array
   });
 }
 
-// absent slots of dense spans (and padding) hold exact zeros: clear [0, total)
-// (the total is a multiple of 8, so the fp16 array is n/2 whole 32-bit words)
+// absent slots of dense spans (and padding) hold exact zeros: clear the
+// screen array's [0, total) (the total is a multiple of 8, so the fp16 array
+// is n/2 whole 32-bit words); the compact exact-value array has no holes
 __global__ void bivf_zero_kernel(const unsigned int* __restrict__ total, float* __restrict__ vs,
-                                 int half, double* __restrict__ v64) {
+                                 int half) {
   const int64_t n = *total;
   const int64_t ns = half ? n / 2 : n;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    if (i < ns) vs[i] = 0.f;
-    v64[i] = 0.0;
-  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ns;
+       i += (int64_t)gridDim.x * blockDim.x)
+    vs[i] = 0.f;
 }
 
 // descending-size sort keys: ~terms_of_mean (stable sort => ties by mean id)
@@ -320,7 +326,8 @@ extern "C" void ivfkm_set_bivf_options(float dense_fill, int permute) {
 }
 
 extern "C" int64_t ivfkm_bivf_headers_size(int64_t k, int64_t dim) {
-  return 2 * bivf_nh(dim, ivfkm_bivf_nblk(k)) + 1 + dim + 2 * k + dim;
+  const int64_t nh = bivf_nh(dim, ivfkm_bivf_nblk(k));
+  return 2 * nh + 1 + dim + 2 * k + dim + nh + 1;
 }
 
 extern "C" int64_t ivfkm_bivf_values_capacity(int64_t k, int64_t dim, int64_t nnz) {
@@ -377,7 +384,7 @@ int plan_count(int64_t k, int64_t dim, const uint32_t* headers, unsigned th, con
   const int threads = 256;
   IVFKM_TRY(cudaMemsetAsync(w.tot64, 0, sizeof(unsigned long long), st));
   bivf_count_kernel<<<grid_for(nh / kSpan + 1, threads), threads, 0, st>>>(nh, headers, th,
-                                                                          w.cnt, w.tot64);
+                                                                          w.cnt, w.cnt64, w.tot64);
   IVFKM_CHECK_LAUNCH();
   return IVFKM_OK;
 }
@@ -389,8 +396,11 @@ int plan_layout(int64_t k, int64_t dim, uint32_t* headers, unsigned th, const Bi
   const int64_t nh = bivf_nh(dim, nblk);
   uint32_t* nc = headers + 2 * nh + 1;
   uint32_t* dpre = reinterpret_cast<uint32_t*>(nc + dim + 2 * k);
+  uint32_t* off64 = dpre + dim;
   const int threads = 256;
   size_t cb = w.cub_bytes;
+  IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.cnt64, off64, (int)(nh + 1), st));
+  cb = w.cub_bytes;
   IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.cnt, w.off, (int)(nh + 1), st));
   bivf_offset_kernel<<<grid_for(nh / kSpan + 1, threads), threads, 0, st>>>(nh, w.off, th,
                                                                            headers);
@@ -410,8 +420,7 @@ int fill_impl(int64_t k, int64_t dim, int major, int64_t nrows, const int64_t* p
   const int32_t* perm = reinterpret_cast<const int32_t*>(headers + 2 * nh + 1 + dim);
   float* val32 = static_cast<float*>(val_screen);  // or fp16 values (screen_bits 16)
   const int threads = 256;
-  bivf_zero_kernel<<<kNumSM * 16, threads, 0, st>>>(headers + 2 * nh, val32, screen_bits == 16,
-                                                     val64);
+  bivf_zero_kernel<<<kNumSM * 16, threads, 0, st>>>(headers + 2 * nh, val32, screen_bits == 16);
   IVFKM_CHECK_LAUNCH();
   bivf_scatter_kernel<<<kNumSM * 8, threads, 0, st>>>(major, nrows, ptr, cols, vals, k, dim,
                                                       nblk, headers, perm, val32, val64,
@@ -434,10 +443,10 @@ int check_build_args(int64_t k, int64_t dim, int major, int64_t nrows, const int
 
 extern "C" int ivfkm_bivf_plan(int64_t k, int64_t dim, int major, int64_t nrows,
                                const int64_t* ptr, const int32_t* cols, uint32_t* headers,
-                               int64_t* total, void* ws, size_t ws_bytes,
+                               int64_t* totals, void* ws, size_t ws_bytes,
                                ivfkm_stream_t stream_) {
   if (int rc = check_build_args(k, dim, major, nrows, ptr, headers)) return rc;
-  if (!total) return IVFKM_E_ARG;
+  if (!totals) return IVFKM_E_ARG;
   size_t need = 0;
   BivfWs w = carve(ws, dim, k, &need);
   if (ws_bytes < need) return IVFKM_E_WORKSPACE;
@@ -459,7 +468,13 @@ extern "C" int ivfkm_bivf_plan(int64_t k, int64_t dim, int major, int64_t nrows,
     th = th * 2 > 256 ? (1u << 30) : th * 2;
   }
   if (int rc = plan_layout(k, dim, headers, th, w, st)) return rc;
-  *total = (int64_t)tot;
+  const int64_t nh = bivf_nh(dim, ivfkm_bivf_nblk(k));
+  unsigned int n64 = 0;  // postings (off64[nh])
+  IVFKM_TRY(cudaMemcpyAsync(&n64, headers + 2 * nh + 1 + dim + 2 * k + dim + nh, sizeof(n64),
+                            cudaMemcpyDeviceToHost, st));
+  IVFKM_TRY(cudaStreamSynchronize(st));
+  totals[0] = (int64_t)tot;
+  totals[1] = (int64_t)n64;
   return IVFKM_OK;
 }
 

@@ -10,24 +10,26 @@
 // headers (uint32), planar:
 //   masks[t*nblk + b]        bit j <=> slot 32*b+j holds term t
 //   offs [t*nblk + b]        start of block b's values (+ kDense flag)
-//   offs [dim*nblk]          padded total (size of the value arrays in use)
+//   offs [dim*nblk]          padded total (size of the screen-value array)
 //   nc   [t]                 postings of term t (= centroid_freq, means.py:144-147)
 //   perm [k], inv [k]        mean -> slot, slot -> mean
 //   dpre [t]                 dense prefix: t's first dpre[t] spans are all dense,
 //                            so their values are one contiguous run — span s at
 //                            (offs[t*nblk] & ~kDense) + 256*s — and the screen
 //                            reads them without masks or offsets
-// Blocks are grouped in spans of 8 (256 slots).  Every span's value segment
-// is padded to a multiple of 8 values, so a span start is 16-B aligned in
-// both the fp32 and the fp16 screen arrays.
+//   off64[t*nblk + b]        start of block b in the compact exact-value (fp64)
+//                            array: postings only, term-major, slot ascending;
+//   off64[dim*nblk]          their number
+// Screen values: blocks are grouped in spans of 8 (256 slots); every span's
+// value segment is padded to a multiple of 8 values, so a span start is 16-B
+// aligned in both the fp32 and the fp16 screen arrays.
 // A span holding at least dense_fill*256 postings is stored *dense*: all 256
 // values (0.0 for absent slots) lane-major in two halves (slot 32*(b0+r)+j at
 // span_base + 128*(r/4) + 4*j + r%4), so a warp lane owning slots
 // 32*(b0+r)+lane reads its 8 values with two 16-B loads, coalesced in global
 // memory and conflict-free in shared memory; every block of a dense span
-// carries kDense in its offset.  The zeros are exact no-ops for both the fp32
-// FMAs and the fp64 rescoring (which still consults the true masks).  Other
-// spans keep the reference order (term-major, mean ascending,
+// carries kDense in its offset.  The zeros are exact no-ops for the FMAs.
+// Other spans keep the reference order (term-major, mean ascending,
 // means.py:169-179, in slot order).
 // The fp16 screen array (screen_bits = 16) uses the same positions except
 // inside dense spans, where each lane's 8 values are contiguous (slot
@@ -40,51 +42,28 @@ namespace ivfkm {
 constexpr uint32_t kDense = 0x80000000u;
 constexpr int kSpan = 8;
 
+// Lookup view for the exact (fp64) values: the compact array holds only the
+// postings, term-major and slot-ascending (the reference's order,
+// means.py:169-179), so block b of term t starts at off64[t*nblk + b].
 struct BivfView {
   int64_t nblk;
   const uint32_t* masks;
-  const uint32_t* offs;
+  const uint32_t* off64;
   const int32_t* perm;  // mean -> slot (nullptr: identity)
 };
 
 __host__ __device__ inline int64_t bivf_nh(int64_t dim, int64_t nblk) { return dim * nblk; }
 
-// Position of slot s's value for term t, or -1 when the slot lacks the term.
+// Position of slot s's exact value for term t, or -1 when the slot lacks it.
 __device__ __forceinline__ int64_t bivf_find_slot(const BivfView& v, int64_t t, int64_t s) {
   const int64_t b = s >> 5;
   const uint32_t bit = 1u << (s & 31);
   const uint32_t m = __ldg(v.masks + t * v.nblk + b);
   if (!(m & bit)) return -1;
-  const uint32_t o = __ldg(v.offs + t * v.nblk + b);
-  if (o & kDense) {
-    const uint32_t r = (uint32_t)(b & (kSpan - 1));
-    return (int64_t)((o & ~kDense) - 32u * r + 128u * (r >> 2) + 4u * (uint32_t)(s & 31) +
-                     (r & 3u));
-  }
-  return (int64_t)(o + (uint32_t)__popc(m & (bit - 1u)));
+  return (int64_t)__ldg(v.off64 + t * v.nblk + b) + __popc(m & (bit - 1u));
 }
 
-// Position of slot s's value in the 16-bit screen array: sparse spans as
-// above; a dense span keeps each lane's 8 values contiguous (one 16-B load):
-// slot 32*(b0+r)+j at span_base + 8*j + r.
-__device__ __forceinline__ int64_t bivf_find16_slot(const BivfView& v, int64_t t, int64_t s) {
-  const int64_t b = s >> 5;
-  const uint32_t bit = 1u << (s & 31);
-  const uint32_t m = __ldg(v.masks + t * v.nblk + b);
-  if (!(m & bit)) return -1;
-  const uint32_t o = __ldg(v.offs + t * v.nblk + b);
-  if (o & kDense) {
-    const uint32_t r = (uint32_t)(b & (kSpan - 1));
-    return (int64_t)((o & ~kDense) - 32u * r + 8u * (uint32_t)(s & 31) + r);
-  }
-  return (int64_t)(o + (uint32_t)__popc(m & (bit - 1u)));
-}
-
-__device__ __forceinline__ int64_t bivf_find16(const BivfView& v, int64_t t, int64_t c) {
-  return bivf_find16_slot(v, t, v.perm ? (int64_t)__ldg(v.perm + c) : c);
-}
-
-// Position of mean c's value for term t, or -1.
+// Position of mean c's exact value for term t, or -1.
 __device__ __forceinline__ int64_t bivf_find(const BivfView& v, int64_t t, int64_t c) {
   return bivf_find_slot(v, t, v.perm ? (int64_t)__ldg(v.perm + c) : c);
 }

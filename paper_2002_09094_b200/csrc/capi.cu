@@ -134,12 +134,12 @@ int assign_host(int64_t n, const int64_t* indptr, const int32_t* terms, const do
   // fp16 screen values (half the posting bytes) unless the means are not
   // normalised far beyond unit norm (fp16 range)
   const int bits = mu_max <= 32768.0 ? 16 : 32;
-  int64_t total = 0;
+  int64_t totals[2] = {0, 0};
   int rc = ivfkm_bivf_plan(k, dim, major, m_rows, d_mp.as<int64_t>(), d_mc.as<int32_t>(),
-                           d_hdr.as<uint32_t>(), &total, d_bws.p, bws, nullptr);
+                           d_hdr.as<uint32_t>(), totals, d_bws.p, bws, nullptr);
   if (rc) return rc;
-  IVFKM_TRY(d_p32.alloc(sizeof(float) * (total + 1)));
-  IVFKM_TRY(d_p64.alloc(sizeof(double) * (total + 1)));
+  IVFKM_TRY(d_p32.alloc(sizeof(float) * (totals[0] + 1)));
+  IVFKM_TRY(d_p64.alloc(sizeof(double) * (totals[1] + 1)));
   rc = ivfkm_bivf_fill(k, dim, major, m_rows, d_mp.as<int64_t>(), d_mc.as<int32_t>(), d_mv.as<double>(),
                        d_hdr.as<uint32_t>(), d_p32.p, bits, d_p64.as<double>(), nullptr);
   if (rc) return rc;

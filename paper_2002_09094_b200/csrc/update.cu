@@ -58,7 +58,8 @@ size_t cub_bytes_for(int64_t nnz, int64_t k) {
   cub::DoubleBuffer<K> kb(nullptr, nullptr);
   cub::DoubleBuffer<double> vb(nullptr, nullptr);
   cub::DeviceRadixSort::SortPairs(nullptr, a, kb, vb, (int)nnz, 0, (int)(sizeof(K) * 8));
-  cub::DeviceScan::ExclusiveSum(nullptr, b, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)nnz);
+  cub::DeviceScan::ExclusiveSum(nullptr, b, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                (int)nnz + 1);
   cub::DeviceScan::ExclusiveSum(nullptr, c, (int64_t*)nullptr, (int64_t*)nullptr, (int)(k + 1));
   return std::max(a, std::max(b, c));
 }
@@ -146,9 +147,9 @@ UpdWs<K> carve_upd(void* base, int64_t nnz, int64_t k, int64_t dim, size_t* tota
   w.key_b = c.take<K>(n);
   w.val_a = c.take<double>(n);
   w.val_b = c.take<double>(n);
-  w.head = c.take<uint32_t>(n);
+  w.head = c.take<uint32_t>(n + 1);  // + the closing flag of the nonzero scan
   w.segpos = c.take<uint32_t>(n);
-  w.nzpos = c.take<uint32_t>(n);
+  w.nzpos = c.take<uint32_t>(n + 1);
   w.seg_start = c.take<uint32_t>(n + 1);
   w.seg_key = c.take<K>(n);
   w.seg_w = c.take<double>(n);
@@ -217,17 +218,15 @@ __global__ void segstart_kernel(int64_t nnz, const K* __restrict__ key,
 
 // One thread per (cluster, term) run: sequential float64 sum in ascending
 // object order (bincount), then w = sum / size.  Reuses `head` as the
-// nonzero flag array (zeroed by the caller beyond n_seg).
+// nonzero flag array, [0, n_seg] (nz[n_seg] = 0 closes the scan).
 template <class K>
-__global__ void segsum_kernel(int64_t nnz, const uint32_t* __restrict__ n_seg_p,
-                              const uint32_t* __restrict__ seg_start,
+__global__ void segsum_kernel(int64_t n_seg, const uint32_t* __restrict__ seg_start,
                               const K* __restrict__ seg_key, const double* __restrict__ sval,
                               const unsigned long long* __restrict__ sizes, int64_t dim,
                               double* __restrict__ seg_w, uint32_t* __restrict__ nz) {
-  const uint32_t n_seg = *n_seg_p;
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nnz;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s <= n_seg;
        s += (int64_t)gridDim.x * blockDim.x) {
-    if (s >= n_seg) {
+    if (s == n_seg) {
       nz[s] = 0u;
       continue;
     }
@@ -430,11 +429,15 @@ int update_count_impl(int64_t n_obj, const int64_t* row_ptr, const int32_t* term
     segstart_kernel<K><<<grid_for(nnz, T), T, 0, st>>>(nnz, key, w.head, w.segpos, w.seg_start,
                                                        w.seg_key, w.n_seg);
     IVFKM_CHECK_LAUNCH();
-    segsum_kernel<K><<<grid_for(nnz, T), T, 0, st>>>(nnz, w.n_seg, w.seg_start, w.seg_key, sval,
-                                                     sizes, dim, w.seg_w, w.head);
+    // the run count sizes the rest of the update (one 4-byte read-back)
+    uint32_t n_seg = 0;
+    IVFKM_TRY(cudaMemcpyAsync(&n_seg, w.n_seg, sizeof(n_seg), cudaMemcpyDeviceToHost, st));
+    IVFKM_TRY(cudaStreamSynchronize(st));
+    segsum_kernel<K><<<grid_for((int64_t)n_seg + 1, T), T, 0, st>>>(
+        n_seg, w.seg_start, w.seg_key, sval, sizes, dim, w.seg_w, w.head);
     IVFKM_CHECK_LAUNCH();
     cb = w.cub_bytes;
-    IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.head, w.nzpos, (int)nnz, st));
+    IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.head, w.nzpos, (int)n_seg + 1, st));
   } else {
     IVFKM_TRY(cudaMemsetAsync(w.n_seg, 0, sizeof(uint32_t), st));
   }

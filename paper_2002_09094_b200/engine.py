@@ -224,15 +224,15 @@ class LloydEngine:
         dm.headers = torch.empty(int(self.lib.ivfkm_bivf_headers_size(self.k, dm.dim)),
                                  dtype=torch.int32, device=dev)
         # plan (headers; the host learns the exact value count), then fill
-        total = C.c_int64(0)
+        totals = np.zeros(2, np.int64)  # (screen values, exact values)
         rc = self.lib.ivfkm_bivf_plan(self.k, dm.dim, 0, self.k, _p(dm.ptr), _p(dm.terms),
-                                      _p(dm.headers), C.byref(total), _p(self.ws_bivf),
-                                      self.ws_bivf.numel(), _stream())
+                                      _p(dm.headers), C.c_void_p(totals.ctypes.data),
+                                      _p(self.ws_bivf), self.ws_bivf.numel(), _stream())
         _lib.check(rc, "ivfkm_bivf_plan")
-        n = max(int(total.value), 1)
         bits = self.screen_bits
-        dm.pvs = torch.empty(n, dtype=torch.float16 if bits == 16 else torch.float32, device=dev)
-        dm.pv64 = torch.empty(n, dtype=torch.float64, device=dev)
+        dm.pvs = torch.empty(max(int(totals[0]), 1),
+                             dtype=torch.float16 if bits == 16 else torch.float32, device=dev)
+        dm.pv64 = torch.empty(max(int(totals[1]), 1), dtype=torch.float64, device=dev)
         rc = self.lib.ivfkm_bivf_fill(self.k, dm.dim, 0, self.k, _p(dm.ptr), _p(dm.terms),
                                       _p(dm.vals), _p(dm.headers), _p(dm.pvs), bits,
                                       _p(dm.pv64), _stream())
