@@ -177,6 +177,35 @@ def test_error_window_is_rigorous():
             assert abs(float(acc32) - acc64) <= eps
 
 
+def test_fp16_error_window_is_rigorous():
+    """The fp16 screen (mean values rounded to fp16, object values to fp32,
+    fp32 FMAs in any order) stays inside its eps_i (csrc/assign.cu,
+    screen_epilogue) — including values below fp16's normal
+    range, signed data, and the worst accumulation order (largest first)."""
+    rng = np.random.default_rng(3)
+    for n in (1, 10, 230, 2000):
+        for trial in range(24):
+            v = 10.0 ** rng.uniform(-7 if trial % 3 == 0 else -2, 0, n)
+            u = 10.0 ** rng.uniform(-7 if trial % 2 == 0 else -2, 0, n) * (rng.random(n) < 0.7)
+            if trial % 4 == 1:  # signed
+                v *= np.where(rng.random(n) < 0.5, -1.0, 1.0)
+                u *= np.where(rng.random(n) < 0.5, -1.0, 1.0)
+            v /= np.linalg.norm(v)
+            u /= max(np.linalg.norm(u), 1e-300)
+            order = np.argsort(-np.abs(v * u)) if trial % 2 else rng.permutation(n)
+            acc32 = np.float32(0)
+            v32, u16 = v.astype(np.float32), u.astype(np.float16).astype(np.float32)
+            for h in order:
+                acc32 = np.float32(np.float64(v32[h]) * np.float64(u16[h]) + np.float64(acc32))
+            acc64 = 0.0
+            for a, b in zip(v, u):
+                acc64 = acc64 + a * b
+            xn, mu = float(np.linalg.norm(v)), 1.0
+            eps = (2.0 ** -11 + (n + 4) * 2.0 ** -24) * xn * mu * (1 + 2.0 ** -9) + \
+                n * xn * 2.0 ** -25 * (1 + 2.0 ** -9) + (n + 1) * 2.0 ** -125
+            assert abs(float(acc32) - acc64) <= eps, (n, trial, abs(float(acc32) - acc64), eps)
+
+
 # ---------------------------------------------------------------- types
 
 def test_types_validate_like_reference():
