@@ -83,7 +83,7 @@ int ivfkm_device_count(void);
 int64_t ivfkm_bivf_nblk(int64_t k); /* 32-mean blocks per term, padded */
 int64_t ivfkm_bivf_headers_size(int64_t k, int64_t dim);
 int64_t ivfkm_bivf_values_capacity(int64_t k, int64_t dim, int64_t nnz);
-/* Build options: dense_fill in [1/32, 1] (> 1: never dense; default 1/32),
+/* Build options: dense_fill in [1/256, 1] (> 1: never dense; default 1/64),
  * permute = 1 orders slots by mean term count (default), 0 keeps mean ids.
  * Out-of-range values leave the setting unchanged.                          */
 void ivfkm_set_bivf_options(float dense_fill, int permute);

@@ -45,7 +45,7 @@ struct BivfWs {
 };
 
 // build options (ivfkm_set_bivf_options)
-float g_dense_fill = 1.0f / 32.0f;  // spans with >= fill*256 postings are stored dense
+float g_dense_fill = 1.0f / 64.0f;  // spans with >= fill*256 postings are stored dense
 int g_permute = 1;          // slots ordered by mean size
 
 uint32_t dense_threshold() {
@@ -321,7 +321,7 @@ extern "C" size_t ivfkm_bivf_workspace_size(int64_t dim, int64_t k) {
 }
 
 extern "C" void ivfkm_set_bivf_options(float dense_fill, int permute) {
-  if (dense_fill >= 1.0f / 32.0f) g_dense_fill = dense_fill;
+  if (dense_fill >= 1.0f / 256.0f) g_dense_fill = dense_fill;
   if (permute == 0 || permute == 1) g_permute = permute;
 }
 
