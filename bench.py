@@ -103,13 +103,44 @@ def config_dict(cfg_index, c, spec, ds, world):
 
 
 class Clocks:
-    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+    """Clock / throttle sampler for the timed region (B200_PROFILING.md clocks
+    line): NVML every 5 ms from a thread (so even a 0.2 s region gets dozens
+    of samples), nvidia-smi -lms 200 when NVML is unavailable."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index=0):
+        self.p = self.thread = None
+        self.sm, self.mx, self.reasons = [], 0.0, set()
+        try:
+            import threading
+
+            import pynvml as N
+
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(index)
+            bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap}
+            self.mx = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+            self.stop_flag = threading.Event()
+
+            def run():
+                while not self.stop_flag.is_set():
+                    self.sm.append(float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)))
+                    r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.reasons.update(nm for nm, b in bits.items() if r & b)
+                    self.stop_flag.wait(0.005)
+
+            self.thread = threading.Thread(target=run, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.thread = None
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.p = subprocess.Popen(
@@ -119,6 +150,13 @@ class Clocks:
             self.p = None
 
     def stop(self):
+        if self.thread is not None:
+            self.stop_flag.set()
+            self.thread.join(timeout=5)
+            if not self.sm:
+                return None
+            return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.mx,
+                    "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml"}
         if self.p is None:
             return None
         self.p.terminate()
@@ -130,12 +168,11 @@ class Clocks:
         rows = [r.split(",") for r in Path(self.f.name).read_text().strip().splitlines() if r]
         os.unlink(self.f.name)
         sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for r in rows:
             try:
                 sm.append(float(r[1]))
                 mx = max(mx, float(r[2]))
-                for nm, val in zip(names, r[5:9]):
+                for nm, val in zip(self.NAMES, r[5:9]):
                     if val.strip().lower() == "active":
                         reasons.add(nm)
             except (ValueError, IndexError):
@@ -143,7 +180,7 @@ class Clocks:
         if not sm:
             return None
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvidia-smi"}
 
 
 def algorithmic_bytes(postings, sum_nnz, n, value_bytes):
