@@ -107,11 +107,15 @@ int ivfkm_bivf_plan(int64_t k, int64_t dim, int major, int64_t nrows,
                     const int64_t* ptr /*[dev] nrows+1*/, const int32_t* cols /*[dev]*/,
                     uint32_t* headers /*[dev]*/, int64_t* totals /*[host] out, 2*/, void* ws,
                     size_t ws_bytes, ivfkm_stream_t stream);
+/* fill: with a workspace of ivfkm_bivf_fill_workspace_size(k, dim, nnz)
+ * bytes (nnz = input entries) the postings are sorted by position first, so
+ * the writes stream; ws = NULL scatters them directly.                      */
+size_t ivfkm_bivf_fill_workspace_size(int64_t k, int64_t dim, int64_t nnz);
 int ivfkm_bivf_fill(int64_t k, int64_t dim, int major, int64_t nrows,
                     const int64_t* ptr /*[dev]*/, const int32_t* cols /*[dev]*/,
                     const double* vals /*[dev]*/, const uint32_t* headers /*[dev], planned*/,
                     void* val_screen /*[dev]*/, int screen_bits, double* val64 /*[dev]*/,
-                    ivfkm_stream_t stream);
+                    int64_t nnz, void* ws /*or NULL*/, size_t ws_bytes, ivfkm_stream_t stream);
 int ivfkm_bivf_build(int64_t k, int64_t dim, int major, int64_t nrows,
                      const int64_t* ptr /*[dev] nrows+1*/, const int32_t* cols /*[dev]*/,
                      const double* vals /*[dev]*/, uint32_t* headers /*[dev]*/,

@@ -52,8 +52,9 @@ SIGNATURES = {
     "ivfkm_bivf_workspace_size": (_sz, [_i64, _i64]),
     "ivfkm_bivf_plan": (C.c_int, [_i64, _i64, C.c_int, _i64, _vp, _vp, _vp, _vp, _vp, _sz,
                                   _vp]),
+    "ivfkm_bivf_fill_workspace_size": (_sz, [_i64, _i64, _i64]),
     "ivfkm_bivf_fill": (C.c_int, [_i64, _i64, C.c_int, _i64, _vp, _vp, _vp, _vp, _vp, C.c_int,
-                                  _vp, _vp]),
+                                  _vp, _i64, _vp, _sz, _vp]),
     "ivfkm_bivf_build": (C.c_int, [_i64, _i64, C.c_int, _i64, _vp, _vp, _vp, _vp, _vp, C.c_int,
                                    _vp, _vp, _sz, _vp]),
     "ivfkm_assign_workspace_size": (_sz, [_i64, _i64]),

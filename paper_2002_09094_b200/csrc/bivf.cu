@@ -231,6 +231,62 @@ __global__ void bivf_scatter_kernel(int major, int64_t nrows, const int64_t* __r
   });
 }
 
+// Sorted fill (two-step build): the postings are first sorted by BIVF
+// position (term, slot) so the value writes and the header reads walk the
+// arrays in order instead of scattering across every term row.
+template <class K>
+__global__ void bivf_poskey_kernel(int major, int64_t nrows, const int64_t* __restrict__ ptr,
+                                   const int32_t* __restrict__ cols,
+                                   const double* __restrict__ vals, int64_t k, int64_t dim,
+                                   int64_t nslot, const int32_t* __restrict__ perm,
+                                   K* __restrict__ key, double* __restrict__ val) {
+  for_each_entry(nrows, ptr, [&](int64_t r, int64_t q) {
+    const int64_t col = cols[q];
+    const int64_t c = major == 0 ? r : col;
+    const int64_t t = major == 0 ? col : r;
+    const bool ok = c >= 0 && c < k && t >= 0 && t < dim;
+    key[q] = ok ? (K)t * (K)nslot + (K)perm[c] : (K)dim * (K)nslot;  // sentinel sorts last
+    val[q] = vals[q];
+  });
+}
+
+template <class K>
+__global__ void bivf_write_kernel(int64_t n, int64_t dim, int64_t nblk, int64_t nslot,
+                                  const K* __restrict__ key, const double* __restrict__ val,
+                                  const unsigned int* __restrict__ hdr,
+                                  const unsigned int* __restrict__ off64,
+                                  float* __restrict__ v32, double* __restrict__ v64, int half) {
+  const int64_t nh = bivf_nh(dim, nblk);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const K kk = key[i];
+    if (kk >= (K)dim * (K)nslot) continue;
+    const int64_t t = (int64_t)(kk / (K)nslot);
+    const int64_t s = (int64_t)(kk - (K)t * (K)nslot);
+    const int64_t b = s >> 5;
+    const uint32_t j = (uint32_t)(s & 31);
+    const uint32_t m = hdr[t * nblk + b];
+    const uint32_t o = hdr[nh + t * nblk + b];
+    const uint32_t below = (uint32_t)__popc(m & ((1u << j) - 1u));
+    int64_t pos, pos16;
+    if (o & kDense) {
+      const uint32_t rr = (uint32_t)(b & (kSpan - 1));
+      const uint32_t sb = (o & ~kDense) - 32u * rr;
+      pos = sb + 128u * (rr >> 2) + 4u * j + (rr & 3u);
+      pos16 = sb + 8u * j + rr;
+    } else {
+      pos = pos16 = o + below;
+    }
+    const double v = val[i];
+    if (half) {
+      reinterpret_cast<__half*>(v32)[pos16] = __double2half(v);
+    } else {
+      v32[pos] = static_cast<float>(v);
+    }
+    v64[(int64_t)off64[t * nblk + b] + below] = v;
+  }
+}
+
 // absent slots of dense spans (and padding) hold exact zeros: clear the
 // screen array's [0, total) (the total is a multiple of 8, so the fp16 array
 // is n/2 whole 32-bit words); the compact exact-value array has no holes
@@ -412,9 +468,70 @@ int plan_layout(int64_t k, int64_t dim, uint32_t* headers, unsigned th, const Bi
 }
 
 // Values: zero [0, total) (absent slots of dense spans), scatter the postings.
+template <class K>
+struct FillWs {
+  K* key_a;
+  K* key_b;
+  double* val_a;
+  double* val_b;
+  void* cub;
+  size_t cub_bytes;
+};
+
+template <class K>
+FillWs<K> carve_fill(void* base, int64_t nnz, size_t* total) {
+  Carver c(base);
+  FillWs<K> w;
+  const size_t n = (size_t)(nnz > 0 ? nnz : 1);
+  w.key_a = c.take<K>(n);
+  w.key_b = c.take<K>(n);
+  w.val_a = c.take<double>(n);
+  w.val_b = c.take<double>(n);
+  size_t a = 0;
+  cub::DoubleBuffer<K> kb(nullptr, nullptr);
+  cub::DoubleBuffer<double> vb(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, a, kb, vb, (int)n, 0, (int)(sizeof(K) * 8));
+  w.cub_bytes = a;
+  w.cub = c.take_bytes(a);
+  if (total) *total = c.off;
+  return w;
+}
+
+bool fill_k32(int64_t k, int64_t dim) {
+  return (double)dim * (double)(ivfkm_bivf_nblk(k) * 32) < 4294967295.0;
+}
+
+template <class K>
+int sorted_fill(int64_t k, int64_t dim, int major, int64_t nrows, const int64_t* ptr,
+                const int32_t* cols, const double* vals, const uint32_t* headers, float* val32,
+                int half, double* val64, int64_t nnz, void* ws, cudaStream_t st) {
+  const int64_t nblk = ivfkm_bivf_nblk(k);
+  const int64_t nh = bivf_nh(dim, nblk);
+  const int64_t nslot = nblk * 32;
+  const int32_t* perm = reinterpret_cast<const int32_t*>(headers + 2 * nh + 1 + dim);
+  const unsigned int* off64 = headers + 2 * nh + 1 + dim + 2 * k + dim;
+  FillWs<K> w = carve_fill<K>(ws, nnz, nullptr);
+  const int threads = 256;
+  bivf_poskey_kernel<K><<<kNumSM * 8, threads, 0, st>>>(major, nrows, ptr, cols, vals, k, dim,
+                                                        nslot, perm, w.key_a, w.val_a);
+  IVFKM_CHECK_LAUNCH();
+  int bits = 1;  // keys lie in [0, dim * nslot] (the sentinel included)
+  while (bits < (int)(sizeof(K) * 8) && (double)(1ull << bits) <= (double)dim * (double)nslot)
+    ++bits;
+  cub::DoubleBuffer<K> kb(w.key_a, w.key_b);
+  cub::DoubleBuffer<double> vb(w.val_a, w.val_b);
+  size_t cb = w.cub_bytes;
+  IVFKM_TRY(cub::DeviceRadixSort::SortPairs(w.cub, cb, kb, vb, (int)nnz, 0, bits, st));
+  bivf_write_kernel<K><<<grid_for(nnz, threads), threads, 0, st>>>(
+      nnz, dim, nblk, nslot, kb.Current(), vb.Current(), headers, off64, val32, val64, half);
+  IVFKM_CHECK_LAUNCH();
+  return IVFKM_OK;
+}
+
 int fill_impl(int64_t k, int64_t dim, int major, int64_t nrows, const int64_t* ptr,
               const int32_t* cols, const double* vals, const uint32_t* headers,
-              void* val_screen, int screen_bits, double* val64, cudaStream_t st) {
+              void* val_screen, int screen_bits, double* val64, cudaStream_t st,
+              int64_t nnz = -1, void* ws = nullptr) {
   const int64_t nblk = ivfkm_bivf_nblk(k);
   const int64_t nh = bivf_nh(dim, nblk);
   const int32_t* perm = reinterpret_cast<const int32_t*>(headers + 2 * nh + 1 + dim);
@@ -422,6 +539,13 @@ int fill_impl(int64_t k, int64_t dim, int major, int64_t nrows, const int64_t* p
   const int threads = 256;
   bivf_zero_kernel<<<kNumSM * 16, threads, 0, st>>>(headers + 2 * nh, val32, screen_bits == 16);
   IVFKM_CHECK_LAUNCH();
+  if (ws && nnz > 0 && nnz < (int64_t)INT32_MAX) {
+    return fill_k32(k, dim)
+               ? sorted_fill<uint32_t>(k, dim, major, nrows, ptr, cols, vals, headers, val32,
+                                       screen_bits == 16, val64, nnz, ws, st)
+               : sorted_fill<unsigned long long>(k, dim, major, nrows, ptr, cols, vals, headers,
+                                                 val32, screen_bits == 16, val64, nnz, ws, st);
+  }
   bivf_scatter_kernel<<<kNumSM * 8, threads, 0, st>>>(major, nrows, ptr, cols, vals, k, dim,
                                                       nblk, headers, perm, val32, val64,
                                                       screen_bits == 16);
@@ -478,14 +602,23 @@ extern "C" int ivfkm_bivf_plan(int64_t k, int64_t dim, int major, int64_t nrows,
   return IVFKM_OK;
 }
 
+extern "C" size_t ivfkm_bivf_fill_workspace_size(int64_t k, int64_t dim, int64_t nnz) {
+  size_t t = 0;
+  if (fill_k32(k, dim)) carve_fill<uint32_t>(nullptr, nnz, &t);
+  else carve_fill<unsigned long long>(nullptr, nnz, &t);
+  return t;
+}
+
 extern "C" int ivfkm_bivf_fill(int64_t k, int64_t dim, int major, int64_t nrows,
                                const int64_t* ptr, const int32_t* cols, const double* vals,
                                const uint32_t* headers, void* val_screen, int screen_bits,
-                               double* val64, ivfkm_stream_t stream_) {
+                               double* val64, int64_t nnz, void* ws, size_t ws_bytes,
+                               ivfkm_stream_t stream_) {
   if (int rc = check_build_args(k, dim, major, nrows, ptr, headers)) return rc;
   if (screen_bits != 32 && screen_bits != 16) return IVFKM_E_ARG;
+  if (ws && ws_bytes < ivfkm_bivf_fill_workspace_size(k, dim, nnz)) return IVFKM_E_WORKSPACE;
   return fill_impl(k, dim, major, nrows, ptr, cols, vals, headers, val_screen, screen_bits,
-                   val64, as_stream(stream_));
+                   val64, as_stream(stream_), nnz, ws);
 }
 
 extern "C" int ivfkm_bivf_build(int64_t k, int64_t dim, int major, int64_t nrows,

@@ -141,7 +141,8 @@ int assign_host(int64_t n, const int64_t* indptr, const int32_t* terms, const do
   IVFKM_TRY(d_p32.alloc(sizeof(float) * (totals[0] + 1)));
   IVFKM_TRY(d_p64.alloc(sizeof(double) * (totals[1] + 1)));
   rc = ivfkm_bivf_fill(k, dim, major, m_rows, d_mp.as<int64_t>(), d_mc.as<int32_t>(), d_mv.as<double>(),
-                       d_hdr.as<uint32_t>(), d_p32.p, bits, d_p64.as<double>(), nullptr);
+                       d_hdr.as<uint32_t>(), d_p32.p, bits, d_p64.as<double>(), mnz,
+                       nullptr, 0, nullptr);
   if (rc) return rc;
   rc = ivfkm_assign(n, d_ip.as<int64_t>(), d_t.as<int32_t>(), d_v32.as<float>(),
                     d_v64.as<double>(), d_xn.as<double>(), k, dim, d_hdr.as<uint32_t>(),

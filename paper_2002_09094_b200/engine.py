@@ -197,6 +197,7 @@ class LloydEngine:
                                      dtype=u8, device=dev)
         self.ws_bivf = torch.empty(int(self.lib.ivfkm_bivf_workspace_size(dim, self.k)),
                                    dtype=u8, device=dev)
+        self.ws_fill = None  # sorted BIVF fill (grows with the means' size)
         self.labels = [torch.empty(n, dtype=torch.int32, device=dev) for _ in range(2)]
         self.cur = 0
         self.sims = torch.empty(n, dtype=torch.float64, device=dev)
@@ -233,14 +234,22 @@ class LloydEngine:
         dm.pvs = torch.empty(max(int(totals[0]), 1),
                              dtype=torch.float16 if bits == 16 else torch.float32, device=dev)
         dm.pv64 = torch.empty(max(int(totals[1]), 1), dtype=torch.float64, device=dev)
+        need = int(self.lib.ivfkm_bivf_fill_workspace_size(self.k, dm.dim, dm.nnz))
+        if self.ws_fill is None or self.ws_fill.numel() < need:
+            self.ws_fill = torch.empty(int(need * 1.25) + 4096, dtype=torch.uint8, device=dev)
         rc = self.lib.ivfkm_bivf_fill(self.k, dm.dim, 0, self.k, _p(dm.ptr), _p(dm.terms),
                                       _p(dm.vals), _p(dm.headers), _p(dm.pvs), bits,
-                                      _p(dm.pv64), _stream())
+                                      _p(dm.pv64), dm.nnz, _p(self.ws_fill),
+                                      self.ws_fill.numel(), _stream())
         dm.screen_bits = bits
         _lib.check(rc, "ivfkm_bivf_fill")
-        # sizes, CUB sort of the k slot keys (single tile / onesweep), perm, mask,
-        # count, scan (init + sweep), offset, zero, scatter, nc
-        self.launches += 11 + (1 if self.k <= 4096 else 6)
+        # plan: sizes, CUB sort of the k slot keys (single tile / onesweep), perm,
+        # mask, count, 2 scans (init + sweep each), offset, nc; fill: zero,
+        # position keys, CUB onesweep sort (histogram, exclusive sum, a pass
+        # per 8 key bits), write
+        nslot = self.nblk * 32
+        kbits = max(1, int(np.ceil(np.log2(float(dm.dim) * nslot + 1))))
+        self.launches += 10 + (1 if self.k <= 4096 else 6) + 5 + (kbits + 7) // 8
         return dm
 
     def upload_means(self, ms) -> DeviceMeans:

@@ -55,6 +55,22 @@ def main():
     orders = {"none": None, "label": torch.argsort(base.long(), stable=True).to(torch.int32),
               "rowlen": torch.argsort(-(eng.dd.row_ptr[1:] - eng.dd.row_ptr[:-1]),
                                       stable=True).to(torch.int32)}
+    # cache-locality experiments: group objects by one of their terms (by
+    # document frequency rank within the row: rarest / median / q-quantile)
+    import numpy as np
+
+    ip = np.asarray(ds.indptr)
+    tt = np.asarray(ds.term_ids) - 1
+    df = np.bincount(tt, minlength=ds.dim)
+    lens = np.diff(ip)
+    row = np.repeat(np.arange(ds.n), lens)
+    key = df[tt].astype(np.int64) * (ds.dim + 1) + tt  # (df, term) per entry
+    srt = np.lexsort((key, row))  # rows in order, entries by ascending df
+    for name, q in (("mindf", 0.0), ("q25df", 0.25), ("meddf", 0.5)):
+        pick = ip[:-1] + np.minimum((lens * q).astype(np.int64), np.maximum(lens - 1, 0))
+        term = tt[srt[pick]]
+        o = np.lexsort((np.arange(ds.n), term)).astype(np.int32)
+        orders[name] = torch.from_numpy(o).to(eng.device)
     for oname in args.order.split(","):
       o = orders[oname]
       eng.order = o
