@@ -419,3 +419,60 @@ class HostIteration:
         self.last_d2h = self.labels_host.numel() * 4 + C.sizeof(_lib.Stats) + \
             (self.k + 1) * 8 + new.nnz * 12 + self.k
         return labels, out, st
+
+
+class StreamIteration:
+    """Lloyd iterations with the corpus streamed from pinned host memory every
+    step and the step's result read back — labels, objective and counters
+    (the per-iteration record of clustering.py:154-176); the means are the
+    model state and stay on the device between steps, as inside ``run``.
+
+    The next step's corpus upload overlaps the current step's kernels on a
+    copy stream (the H2D engine), the labels come back on the D2H engine.
+    """
+
+    def __init__(self, hd: HostDataset, k: int, means: MeanSet, device="cuda"):
+        self.hd, self.k = hd, int(k)
+        self.device = torch.device(device)
+        self.means0 = means
+        self.eng = None
+        self.dm = None
+        self.prev = None
+        self.labels_host = torch.empty(hd.n, dtype=torch.int32).pin_memory()
+        self.copy_stream = torch.cuda.Stream(device=self.device)
+        self.next_dd = None
+        self.next_ready = None
+        self.last_h2d = self.last_d2h = 0
+
+    def _upload(self):
+        with torch.cuda.stream(self.copy_stream):
+            dd = DeviceDataset(self.hd, self.device)
+            ev = torch.cuda.Event()
+            ev.record(self.copy_stream)
+        return dd, ev
+
+    def step(self):
+        if self.next_dd is None:
+            self.next_dd, self.next_ready = self._upload()
+        dd, ready = self.next_dd, self.next_ready
+        torch.cuda.current_stream().wait_event(ready)
+        for t_ in (dd.row_ptr, dd.terms, dd.val64, dd.xnorm, dd.val32):
+            t_.record_stream(torch.cuda.current_stream())
+        go = torch.cuda.Event()
+        go.record()
+        self.copy_stream.wait_event(go)
+        self.next_dd, self.next_ready = self._upload()  # the next step's corpus, in flight
+        if self.eng is None:
+            self.eng = LloydEngine(dd, self.k)
+            self.dm = self.eng.upload_means(self.means0)
+        self.eng.dd = dd
+        lab = self.eng.assign(self.dm, self.prev)
+        st = self.eng.read_stats()  # objective, changed, counters: the step's result
+        self.labels_host.copy_(lab, non_blocking=True)
+        self.dm = self.eng.update(lab, self.dm)
+        self.prev = lab
+        torch.cuda.current_stream().synchronize()
+        self.last_h2d = self.hd.nbytes
+        self.last_d2h = self.labels_host.numel() * 4 + C.sizeof(_lib.Stats)
+        return self.labels_host.numpy() + 1, st
+
