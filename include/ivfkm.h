@@ -203,6 +203,21 @@ int ivfkm_update_count(int64_t n_obj, int64_t nnz, const int64_t* row_ptr,
                        const unsigned long long* sizes /*[dev] k*/,
                        const int64_t* prev_ptr /*[dev] k+1*/, int64_t* new_ptr /*[dev] k+1*/,
                        void* ws, size_t ws_bytes, ivfkm_stream_t stream);
+/* count with a label-delta sort: `state` keeps the previous iteration's
+ * sorted (cluster, term, object) entries and is updated by removing the
+ * objects whose label changed and merging their re-keyed entries back in
+ * (one full sort when more than a quarter of the entries move).  Same
+ * results as ivfkm_update_count, bit for bit.  The state belongs to ONE
+ * corpus (row_ptr/terms/val64 contents): zero-fill it before first use and
+ * whenever the corpus changes.  state_size returns 0 when the composite key
+ * (log2 N + log2 D + log2 k bits) does not fit 64 bits.                      */
+size_t ivfkm_update_state_size(int64_t n_obj, int64_t nnz, int64_t k, int64_t dim);
+int ivfkm_update_count_delta(int64_t n_obj, int64_t nnz, const int64_t* row_ptr,
+                             const int32_t* terms, const double* val64, int64_t k, int64_t dim,
+                             const int32_t* labels, const unsigned long long* sizes,
+                             const int64_t* prev_ptr, int64_t* new_ptr, void* ws,
+                             size_t ws_bytes, void* state /*[dev] zero-filled first*/,
+                             size_t state_bytes, ivfkm_stream_t stream);
 int ivfkm_update_fill(int64_t n_obj, int64_t nnz, int64_t k, int64_t dim,
                       const unsigned long long* sizes, const int64_t* prev_ptr,
                       const int32_t* prev_terms, const double* prev_vals,

@@ -73,6 +73,9 @@ SIGNATURES = {
     "ivfkm_update_workspace_size": (_sz, [_i64, _i64, _i64, _i64]),
     "ivfkm_update_count": (C.c_int, [_i64, _i64, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp,
                                      _vp, _sz, _vp]),
+    "ivfkm_update_state_size": (_sz, [_i64, _i64, _i64, _i64]),
+    "ivfkm_update_count_delta": (C.c_int, [_i64, _i64, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp,
+                                           _vp, _vp, _sz, _vp, _sz, _vp]),
     "ivfkm_update_fill": (C.c_int, [_i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                     _vp, _i64, _vp, _sz, _vp]),
     "ivfkm_assign_ivf_host": (C.c_int, [_i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp,

@@ -12,6 +12,12 @@
     if (e_ != cudaSuccess) return static_cast<int>(e_);  \
   } while (0)
 
+#define IVFKM_TRY_RC(expr)         \
+  do {                             \
+    int rc_ = (expr);              \
+    if (rc_ != 0) return rc_;      \
+  } while (0)
+
 #define IVFKM_CHECK_LAUNCH() IVFKM_TRY(cudaGetLastError())
 
 namespace ivfkm {

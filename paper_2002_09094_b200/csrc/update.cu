@@ -18,6 +18,7 @@
 // subtrees contribute exact zeros, so only populated leaves are visited);
 // scans give the new CSR offsets; the fill pass writes terms and values.
 #include <cub/cub.cuh>
+#include <cub/device/device_merge.cuh>
 
 #include <algorithm>
 #include <map>
@@ -401,30 +402,301 @@ __global__ void retain_kernel(int64_t k, const unsigned long long* __restrict__ 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Label-delta sort (optional state, ivfkm_update_count_delta).  After the
+// first iterations only a few percent of the objects change cluster, so the
+// previous iteration's sorted entries are kept as composite keys
+// (label, term, object) — unique, so every order is the stable order — and
+// updated by (1) dropping the changed objects' entries (stable compaction),
+// (2) keying and sorting those entries under their new labels, (3) merging
+// the two sorted runs.  Iterations where more than a quarter of the entries
+// move fall back to one full sort of the composite keys.
+
+struct DeltaHdr {
+  long long magic, n_obj, nnz, k, dim, valid, cur, pad;
+};
+constexpr long long kDeltaMagic = 0x69766b6d64656c74ll;
+
+struct DeltaState {
+  DeltaHdr* hdr;
+  int32_t* labels;               // the labels S was built with
+  unsigned long long* key[2];    // S: composite keys
+  double* val[2];                // S: values
+  unsigned long long* bkey[2];   // changed entries (B), capacity nnz/4
+  double* bval[2];
+  uint8_t* oflag;                // n_obj: changed
+  uint8_t* eflag;                // nnz: entry kept in A
+  int32_t* clist;                // n_obj: changed objects
+  int64_t* cptr;                 // n_obj+1: their entry offsets in B
+  unsigned long long* counts;    // [0] changed objects, [1] their entries, [2] selected
+  void* cub;
+  size_t cub_bytes;
+};
+
+int64_t delta_cap(int64_t nnz) { return nnz / 4 + 1024; }
+
+DeltaState carve_delta(void* base, int64_t n_obj, int64_t nnz, size_t* total) {
+  Carver c(base);
+  DeltaState d;
+  const size_t n = (size_t)(nnz > 0 ? nnz : 1), no = (size_t)(n_obj > 0 ? n_obj : 1);
+  const size_t nb = (size_t)delta_cap(nnz);
+  d.hdr = c.take<DeltaHdr>(1);
+  d.labels = c.take<int32_t>(no);
+  for (int b = 0; b < 2; ++b) {
+    d.key[b] = c.take<unsigned long long>(n);
+    d.val[b] = c.take<double>(n);
+    d.bkey[b] = c.take<unsigned long long>(nb);
+    d.bval[b] = c.take<double>(nb);
+  }
+  d.oflag = c.take<uint8_t>(no);
+  d.eflag = c.take<uint8_t>(n);
+  d.clist = c.take<int32_t>(no);
+  d.cptr = c.take<int64_t>(no + 1);
+  d.counts = c.take<unsigned long long>(4);
+  size_t a = 0, b = 0, m = 0, sc = 0, so = 0;
+  cub::DoubleBuffer<unsigned long long> kb(nullptr, nullptr);
+  cub::DoubleBuffer<double> vb(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, a, kb, vb, (int)n, 0, 64);
+  cub::DeviceSelect::Flagged(nullptr, b, (unsigned long long*)nullptr, (uint8_t*)nullptr,
+                             (unsigned long long*)nullptr, (unsigned long long*)nullptr, (int)n);
+  cub::DeviceMerge::MergePairs(nullptr, m, (unsigned long long*)nullptr, (double*)nullptr, (int)n,
+                               (unsigned long long*)nullptr, (double*)nullptr, (int)nb,
+                               (unsigned long long*)nullptr, (double*)nullptr);
+  cub::DeviceScan::ExclusiveSum(nullptr, sc, (int64_t*)nullptr, (int64_t*)nullptr, (int)no + 1);
+  cub::DeviceSelect::Flagged(nullptr, so, (int32_t*)nullptr, (uint8_t*)nullptr,
+                             (int32_t*)nullptr, (unsigned long long*)nullptr, (int)no);
+  d.cub_bytes = std::max(std::max(a, b), std::max(std::max(m, sc), so));
+  d.cub = c.take_bytes(d.cub_bytes);
+  if (total) *total = c.off;
+  return d;
+}
+
+struct Bits {
+  int ob, tb, lb;
+  unsigned long long omask, tmask;
+};
+
+inline int bits_for(int64_t n) {
+  int b = 1;
+  while (b < 63 && (1ll << b) < n) ++b;
+  return b;
+}
+
+Bits comp_bits(int64_t n_obj, int64_t dim, int64_t k) {
+  Bits b;
+  b.ob = bits_for(n_obj);
+  b.tb = bits_for(dim);
+  b.lb = bits_for(k);
+  b.omask = (1ull << b.ob) - 1ull;
+  b.tmask = (1ull << b.tb) - 1ull;
+  return b;
+}
+
+__global__ void comp_keys_kernel(int64_t n_obj, const int64_t* __restrict__ row_ptr,
+                                 const int32_t* __restrict__ terms,
+                                 const double* __restrict__ val64,
+                                 const int32_t* __restrict__ labels,
+                                 const int32_t* __restrict__ objs, int64_t n_list,
+                                 const int64_t* __restrict__ out_ptr, Bits bt,
+                                 unsigned long long* __restrict__ key, double* __restrict__ val) {
+  // one warp per object: all objects (objs == nullptr) or the listed ones
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  const int64_t n = objs ? n_list : n_obj;
+  for (int64_t q = blockIdx.x * wpb + (threadIdx.x >> 5); q < n; q += gridDim.x * wpb) {
+    const int64_t i = objs ? objs[q] : q;
+    const int64_t rb = row_ptr[i], re = row_ptr[i + 1];
+    const int64_t o = objs ? out_ptr[q] : rb;
+    const unsigned long long hi = ((unsigned long long)labels[i] << (bt.tb + bt.ob)) |
+                                  (unsigned long long)i;
+    for (int64_t e = rb + lane; e < re; e += 32) {
+      key[o + (e - rb)] = hi | ((unsigned long long)terms[e] << bt.ob);
+      val[o + (e - rb)] = val64[e];
+    }
+  }
+}
+
+__global__ void changed_kernel(int64_t n_obj, const int32_t* __restrict__ labels,
+                               const int32_t* __restrict__ old, const int64_t* __restrict__ row_ptr,
+                               uint8_t* __restrict__ oflag, int64_t* __restrict__ len,
+                               unsigned long long* __restrict__ counts) {
+  unsigned long long co = 0, ce = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_obj;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool ch = labels[i] != old[i];
+    oflag[i] = ch ? 1 : 0;
+    const int64_t l = ch ? row_ptr[i + 1] - row_ptr[i] : 0;
+    len[i] = l;
+    co += ch;
+    ce += (unsigned long long)l;
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    co += __shfl_xor_sync(0xffffffffu, co, off);
+    ce += __shfl_xor_sync(0xffffffffu, ce, off);
+  }
+  if ((threadIdx.x & 31) == 0 && (co | ce)) {
+    atomicAdd(&counts[0], co);
+    atomicAdd(&counts[1], ce);
+  }
+}
+
+// lens of the listed changed objects (in list order) for the B offsets
+__global__ void list_len_kernel(int64_t n_list, const int32_t* __restrict__ objs,
+                                const int64_t* __restrict__ row_ptr, int64_t* __restrict__ len) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n_list;
+       q += (int64_t)gridDim.x * blockDim.x)
+    len[q] = row_ptr[objs[q] + 1] - row_ptr[objs[q]];
+}
+
+__global__ void keep_flags_kernel(int64_t nnz, const unsigned long long* __restrict__ key,
+                                  unsigned long long omask, const uint8_t* __restrict__ oflag,
+                                  uint8_t* __restrict__ eflag) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x)
+    eflag[e] = oflag[key[e] & omask] ? 0 : 1;
+}
+
+// composite (label, term, obj) -> the (label * dim + term) key of the classic path
+template <class K>
+__global__ void derive_keys_kernel(int64_t nnz, const unsigned long long* __restrict__ ck,
+                                   Bits bt, int64_t dim, K* __restrict__ key) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long c = ck[e];
+    const unsigned long long lab = c >> (bt.tb + bt.ob);
+    const unsigned long long t = (c >> bt.ob) & bt.tmask;
+    key[e] = (K)lab * (K)dim + (K)t;
+  }
+}
+
+// Sorted (key, value) for this update: the composite-key state S brought up to
+// the current labels (incrementally when few objects moved); returns the S
+// buffers through *sk / *sv.
+int delta_sort(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms, const double* val64,
+               int64_t nnz, int64_t k, int64_t dim, const int32_t* labels, DeltaState& d,
+               const unsigned long long** sk, const double** sv, int64_t* moved,
+               cudaStream_t st) {
+  const Bits bt = comp_bits(n_obj, dim, k);
+  const int total_bits = bt.ob + bt.tb + bt.lb;
+  const int T = 256;
+  DeltaHdr h;
+  IVFKM_TRY(cudaMemcpyAsync(&h, d.hdr, sizeof(h), cudaMemcpyDeviceToHost, st));
+  IVFKM_TRY(cudaStreamSynchronize(st));
+  bool full = !(h.magic == kDeltaMagic && h.valid == 1 && h.n_obj == n_obj && h.nnz == nnz &&
+                h.k == k && h.dim == dim && (h.cur == 0 || h.cur == 1));
+  int cur = full ? 0 : (int)h.cur;
+  unsigned long long cnt[2] = {0, 0};
+  if (!full) {
+    IVFKM_TRY(cudaMemsetAsync(d.counts, 0, sizeof(unsigned long long) * 4, st));
+    changed_kernel<<<grid_for(n_obj, T), T, 0, st>>>(n_obj, labels, d.labels, row_ptr, d.oflag,
+                                                    d.cptr, d.counts);
+    IVFKM_CHECK_LAUNCH();
+    IVFKM_TRY(cudaMemcpyAsync(cnt, d.counts, sizeof(cnt), cudaMemcpyDeviceToHost, st));
+    IVFKM_TRY(cudaStreamSynchronize(st));
+    if ((int64_t)cnt[1] > delta_cap(nnz) - 1024) full = true;
+  }
+  if (full) {
+    comp_keys_kernel<<<grid_for(n_obj, T / 32), T, 0, st>>>(n_obj, row_ptr, terms, val64, labels,
+                                                           nullptr, 0, nullptr, bt, d.key[0],
+                                                           d.val[0]);
+    IVFKM_CHECK_LAUNCH();
+    cub::DoubleBuffer<unsigned long long> kb(d.key[0], d.key[1]);
+    cub::DoubleBuffer<double> vb(d.val[0], d.val[1]);
+    size_t cb = d.cub_bytes;
+    IVFKM_TRY(cub::DeviceRadixSort::SortPairs(d.cub, cb, kb, vb, (int)nnz, 0, total_bits, st));
+    cur = kb.selector;
+    *moved = nnz;
+  } else if (cnt[1] > 0) {
+    const int oth = cur ^ 1;
+    const int64_t nb = (int64_t)cnt[1], nc = (int64_t)cnt[0];
+    // A: the unchanged objects' entries, in order
+    keep_flags_kernel<<<grid_for(nnz, T), T, 0, st>>>(nnz, d.key[cur], bt.omask, d.oflag,
+                                                      d.eflag);
+    IVFKM_CHECK_LAUNCH();
+    size_t cb = d.cub_bytes;
+    IVFKM_TRY(cub::DeviceSelect::Flagged(d.cub, cb, d.key[cur], d.eflag, d.key[oth],
+                                         d.counts + 2, (int)nnz, st));
+    cb = d.cub_bytes;
+    IVFKM_TRY(cub::DeviceSelect::Flagged(d.cub, cb, d.val[cur], d.eflag, d.val[oth],
+                                         d.counts + 2, (int)nnz, st));
+    // B: the changed objects' entries under their new labels, sorted
+    {
+      // list the changed objects (ascending ids)
+      cub::CountingInputIterator<int32_t> it(0);
+      cb = d.cub_bytes;
+      IVFKM_TRY(cub::DeviceSelect::Flagged(d.cub, cb, it, d.oflag, d.clist, d.counts + 3,
+                                           (int)n_obj, st));
+    }
+    list_len_kernel<<<grid_for(nc, T), T, 0, st>>>(nc, d.clist, row_ptr, d.cptr);
+    IVFKM_CHECK_LAUNCH();
+    IVFKM_TRY(cudaMemsetAsync(d.cptr + nc, 0, sizeof(int64_t), st));
+    cb = d.cub_bytes;
+    IVFKM_TRY(cub::DeviceScan::ExclusiveSum(d.cub, cb, d.cptr, d.cptr, (int)nc + 1, st));
+    comp_keys_kernel<<<grid_for(nc, T / 32), T, 0, st>>>(n_obj, row_ptr, terms, val64, labels,
+                                                        d.clist, nc, d.cptr, bt, d.bkey[0],
+                                                        d.bval[0]);
+    IVFKM_CHECK_LAUNCH();
+    cub::DoubleBuffer<unsigned long long> kb(d.bkey[0], d.bkey[1]);
+    cub::DoubleBuffer<double> vb(d.bval[0], d.bval[1]);
+    cb = d.cub_bytes;
+    IVFKM_TRY(cub::DeviceRadixSort::SortPairs(d.cub, cb, kb, vb, (int)nb, 0, total_bits, st));
+    // merge A (oth) and B into cur (keys are unique: no ties to order)
+    cb = d.cub_bytes;
+    IVFKM_TRY(cub::DeviceMerge::MergePairs(d.cub, cb, d.key[oth], d.val[oth], (int)(nnz - nb),
+                                           kb.Current(), vb.Current(), (int)nb, d.key[cur],
+                                           d.val[cur], ::cuda::std::less<>{}, st));
+    *moved = nb;
+  } else {
+    *moved = 0;
+  }
+  // remember the labels S now holds
+  IVFKM_TRY(cudaMemcpyAsync(d.labels, labels, sizeof(int32_t) * n_obj, cudaMemcpyDeviceToDevice,
+                            st));
+  DeltaHdr nh{kDeltaMagic, n_obj, nnz, k, dim, 1, cur, 0};
+  IVFKM_TRY(cudaMemcpyAsync(d.hdr, &nh, sizeof(nh), cudaMemcpyHostToDevice, st));
+  IVFKM_TRY(cudaStreamSynchronize(st));  // nh lives on this stack frame
+  *sk = d.key[cur];
+  *sv = d.val[cur];
+  return IVFKM_OK;
+}
+
 template <class K>
 int update_count_impl(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
                       const double* val64, int64_t nnz, int64_t k, int64_t dim,
                       const int32_t* labels, const unsigned long long* sizes,
                       const int64_t* prev_ptr, int64_t* new_ptr, void* ws, size_t ws_bytes,
-                      cudaStream_t st) {
+                      DeltaState* delta, cudaStream_t st) {
   size_t need = 0;
   UpdWs<K> w = carve_upd<K>(ws, nnz, k, dim, &need);
   if (ws_bytes < need) return IVFKM_E_WORKSPACE;
   const int T = 256;
   if (nnz > 0) {
-    keys_kernel<K><<<grid_for(n_obj, T / 32), T, 0, st>>>(n_obj, row_ptr, terms, val64, labels,
-                                                          dim, w.key_a, w.val_a);
-    IVFKM_CHECK_LAUNCH();
-    cub::DoubleBuffer<K> kb(w.key_a, w.key_b);
-    cub::DoubleBuffer<double> vb(w.val_a, w.val_b);
-    size_t cb = w.cub_bytes;
-    IVFKM_TRY(cub::DeviceRadixSort::SortPairs(w.cub, cb, kb, vb, (int)nnz, 0, key_bits(k, dim),
-                                              st));
-    K* key = kb.Current();
-    double* sval = vb.Current();
+    K* key;
+    const double* sval;
+    if (delta) {
+      const unsigned long long* ck;
+      int64_t moved = 0;
+      IVFKM_TRY_RC(delta_sort(n_obj, row_ptr, terms, val64, nnz, k, dim, labels, *delta, &ck,
+                              &sval, &moved, st));
+      derive_keys_kernel<K><<<grid_for(nnz, T), T, 0, st>>>(nnz, ck, comp_bits(n_obj, dim, k),
+                                                            dim, w.key_a);
+      IVFKM_CHECK_LAUNCH();
+      key = w.key_a;
+    } else {
+      keys_kernel<K><<<grid_for(n_obj, T / 32), T, 0, st>>>(n_obj, row_ptr, terms, val64, labels,
+                                                            dim, w.key_a, w.val_a);
+      IVFKM_CHECK_LAUNCH();
+      cub::DoubleBuffer<K> kb(w.key_a, w.key_b);
+      cub::DoubleBuffer<double> vb(w.val_a, w.val_b);
+      size_t cb = w.cub_bytes;
+      IVFKM_TRY(cub::DeviceRadixSort::SortPairs(w.cub, cb, kb, vb, (int)nnz, 0, key_bits(k, dim),
+                                                st));
+      key = kb.Current();
+      sval = vb.Current();
+    }
     head_kernel<K><<<grid_for(nnz, T), T, 0, st>>>(nnz, key, w.head);
     IVFKM_CHECK_LAUNCH();
-    cb = w.cub_bytes;
+    size_t cb = w.cub_bytes;
     IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.head, w.segpos, (int)nnz, st));
     segstart_kernel<K><<<grid_for(nnz, T), T, 0, st>>>(nnz, key, w.head, w.segpos, w.seg_start,
                                                        w.seg_key, w.n_seg);
@@ -506,9 +778,39 @@ extern "C" int ivfkm_update_count(int64_t n_obj, int64_t nnz, const int64_t* row
   cudaStream_t st = as_stream(stream_);
   if (use_k32(k, dim))
     return update_count_impl<uint32_t>(n_obj, row_ptr, terms, val64, nnz, k, dim, labels, sizes,
-                                       prev_ptr, new_ptr, ws, ws_bytes, st);
+                                       prev_ptr, new_ptr, ws, ws_bytes, nullptr, st);
   return update_count_impl<unsigned long long>(n_obj, row_ptr, terms, val64, nnz, k, dim, labels,
-                                               sizes, prev_ptr, new_ptr, ws, ws_bytes, st);
+                                               sizes, prev_ptr, new_ptr, ws, ws_bytes, nullptr, st);
+}
+
+extern "C" size_t ivfkm_update_state_size(int64_t n_obj, int64_t nnz, int64_t k, int64_t dim) {
+  if (n_obj < 0 || nnz < 0 || k < 1 || dim < 1 || nnz >= (int64_t)INT32_MAX) return 0;
+  const Bits bt = comp_bits(n_obj, dim, k);
+  if (bt.ob + bt.tb + bt.lb > 64) return 0;
+  size_t total = 0;
+  carve_delta(nullptr, n_obj, nnz, &total);
+  return total;
+}
+
+extern "C" int ivfkm_update_count_delta(int64_t n_obj, int64_t nnz, const int64_t* row_ptr,
+                                        const int32_t* terms, const double* val64, int64_t k,
+                                        int64_t dim, const int32_t* labels,
+                                        const unsigned long long* sizes, const int64_t* prev_ptr,
+                                        int64_t* new_ptr, void* ws, size_t ws_bytes, void* state,
+                                        size_t state_bytes, ivfkm_stream_t stream_) {
+  if (n_obj < 0 || k < 1 || dim < 1 || !row_ptr || !sizes || !prev_ptr || !new_ptr || !state)
+    return IVFKM_E_ARG;
+  if (nnz < 0) return IVFKM_E_ARG;
+  const size_t need = ivfkm_update_state_size(n_obj, nnz, k, dim);
+  if (need == 0) return IVFKM_E_UNSUPPORTED;
+  if (state_bytes < need) return IVFKM_E_WORKSPACE;
+  DeltaState d = carve_delta(state, n_obj, nnz, nullptr);
+  cudaStream_t st = as_stream(stream_);
+  if (use_k32(k, dim))
+    return update_count_impl<uint32_t>(n_obj, row_ptr, terms, val64, nnz, k, dim, labels, sizes,
+                                       prev_ptr, new_ptr, ws, ws_bytes, &d, st);
+  return update_count_impl<unsigned long long>(n_obj, row_ptr, terms, val64, nnz, k, dim, labels,
+                                               sizes, prev_ptr, new_ptr, ws, ws_bytes, &d, st);
 }
 
 extern "C" int ivfkm_update_fill(int64_t /*n_obj*/, int64_t nnz, int64_t k, int64_t dim,

@@ -150,17 +150,32 @@ def update_launches(k: int, dim: int) -> int:
     bits = max(1, int(np.ceil(np.log2(max(2.0, float(k) * float(dim))))))
     return 16 + (bits + 7) // 8
 
+def delta_update_launches() -> int:
+    """Extra kernels of the label-delta sort (changed, keep flags, 3 CUB
+    selects, lengths, scan, keys, the changed entries' radix sort, merge,
+    derived keys) in place of keys + the full sort."""
+    return 23
+
+
 def update_rows(lib, n_obj, nnz, row_ptr, terms, val64, labels0, sizes, prev: DeviceMeans, k,
-                dim, ws, total_host=None) -> DeviceMeans:
+                dim, ws, total_host=None, state=None) -> DeviceMeans:
     """Bit-exact update (variants.py:254-307) of k means from n_obj device rows
-    whose 0-based labels lie in [0, k): ivfkm_update_count, one 8-byte
-    device->host read of the new size, ivfkm_update_fill.  No BIVF."""
+    whose 0-based labels lie in [0, k): ivfkm_update_count (or, with a
+    label-delta ``state``, ivfkm_update_count_delta), one 8-byte device->host
+    read of the new size, ivfkm_update_fill.  No BIVF."""
     dev = row_ptr.device
     new_ptr = torch.empty(k + 1, dtype=torch.int64, device=dev)
-    rc = lib.ivfkm_update_count(n_obj, nnz, _p(row_ptr), _p(terms), _p(val64), k, dim,
-                                _p(labels0), _p(sizes), _p(prev.ptr), _p(new_ptr), _p(ws),
-                                ws.numel(), _stream())
-    _lib.check(rc, "ivfkm_update_count")
+    if state is not None:
+        rc = lib.ivfkm_update_count_delta(n_obj, nnz, _p(row_ptr), _p(terms), _p(val64), k, dim,
+                                          _p(labels0), _p(sizes), _p(prev.ptr), _p(new_ptr),
+                                          _p(ws), ws.numel(), _p(state), state.numel(),
+                                          _stream())
+        _lib.check(rc, "ivfkm_update_count_delta")
+    else:
+        rc = lib.ivfkm_update_count(n_obj, nnz, _p(row_ptr), _p(terms), _p(val64), k, dim,
+                                    _p(labels0), _p(sizes), _p(prev.ptr), _p(new_ptr), _p(ws),
+                                    ws.numel(), _stream())
+        _lib.check(rc, "ivfkm_update_count")
     if total_host is None:
         total_host = torch.zeros(1, dtype=torch.int64)
     total_host.copy_(new_ptr[k:], non_blocking=True)
@@ -179,7 +194,8 @@ def update_rows(lib, n_obj, nnz, row_ptr, terms, val64, labels0, sizes, prev: De
 class LloydEngine:
     """Runs IVF Lloyd iterations over one device-resident dataset."""
 
-    def __init__(self, dd: DeviceDataset, k: int, screen_bits: int = 16):
+    def __init__(self, dd: DeviceDataset, k: int, screen_bits: int = 16,
+                 delta_update: bool = True):
         self.lib = _lib.load()
         self.dd, self.k = dd, int(k)
         # fp16 screen values: half the posting bytes, a wider (still rigorous)
@@ -198,6 +214,10 @@ class LloydEngine:
         self.ws_bivf = torch.empty(int(self.lib.ivfkm_bivf_workspace_size(dim, self.k)),
                                    dtype=u8, device=dev)
         self.ws_fill = None  # sorted BIVF fill (grows with the means' size)
+        # label-delta update sort: the previous iteration's sorted entries
+        # (DESIGN.md §4); zero-filled = no state yet
+        sbytes = int(self.lib.ivfkm_update_state_size(n, nnz, self.k, dim)) if delta_update else 0
+        self.upd_state = torch.zeros(sbytes, dtype=u8, device=dev) if sbytes else None
         self.labels = [torch.empty(n, dtype=torch.int32, device=dev) for _ in range(2)]
         self.cur = 0
         self.sims = torch.empty(n, dtype=torch.float64, device=dev)
@@ -310,8 +330,12 @@ class LloydEngine:
         """New means from the assignment (sizes must be the ones ivfkm_assign wrote)."""
         dd = self.dd
         out = update_rows(self.lib, dd.n, dd.nnz, dd.row_ptr, dd.terms, dd.val64, labels0,
-                          self.sizes, dm, self.k, dd.dim, self.ws_update, self.total_host)
+                          self.sizes, dm, self.k, dd.dim, self.ws_update, self.total_host,
+                          self.upd_state)
         self.launches += update_launches(self.k, dd.dim)
+        if self.upd_state is not None:
+            # minus keys + the full sort (histogram, exclusive sum, passes)
+            self.launches += delta_update_launches() - (update_launches(self.k, dd.dim) - 13)
         return self.build_bivf(out)
 
     def set_sizes_from_labels(self, labels0: torch.Tensor) -> None:

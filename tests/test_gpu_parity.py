@@ -367,6 +367,45 @@ def test_update_matches_oracle_bitwise_with_empty_clusters():
     assert np.array_equal(up.retained, ref.retained) and up.retained[40:].all()
 
 
+def test_update_label_delta_sort_matches_oracle_bitwise():
+    """The engine's label-delta update sort (kept entries + merged movers,
+    full re-sort past a quarter of the entries, nothing moved, a label set
+    with empty clusters) against the oracle on every step, and against the
+    stateless sort."""
+    from oracle import oracle as O
+    from paper_2002_09094_b200.engine import DeviceMeans, update_rows
+    from paper_2002_09094_b200.variants import engine_for
+
+    P = _pkg()
+    ds, om, means = _random_case(seed=12, k=60, n=2500)
+    rng = np.random.default_rng(12)
+    labels = rng.integers(1, 61, size=ds.n).astype(np.int32)
+    steps = [0.0, 0.02, 0.0, 0.001, 0.6, 0.05, 0.3, 0.01, 1.0]
+    eng = engine_for(ds, 60)
+    assert eng.upd_state is not None
+    for i, frac in enumerate(steps):
+        moved = rng.random(ds.n) < frac
+        labels = np.where(moved, rng.integers(1, 61, size=ds.n), labels).astype(np.int32)
+        if i == 5:
+            labels = np.where(labels > 50, 1 + labels % 7, labels).astype(np.int32)
+        asg = P.Assignment.from_labels(labels, 60)
+        up = P.update_ivf(ds, asg, means)
+        ref = O.update(ds, labels, om)
+        assert np.array_equal(up.indptr, ref.indptr), i
+        assert np.array_equal(up.term_ids, ref.term_ids), i
+        assert np.array_equal(up.values.view(np.int64), ref.values.view(np.int64)), i
+        assert np.array_equal(up.retained, ref.retained), i
+    # the stateless path on the final labels gives the same bytes
+    import torch
+    dd = eng.dd
+    dm = DeviceMeans.from_meanset(means, eng.device)
+    lab = torch.from_numpy(labels - 1).to(eng.device)
+    eng.sizes.copy_(torch.from_numpy(np.array(asg.sizes, dtype=np.int64)))
+    out = update_rows(eng.lib, dd.n, dd.nnz, dd.row_ptr, dd.terms, dd.val64, lab, eng.sizes, dm,
+                      60, dd.dim, eng.ws_update)
+    assert np.array_equal(out.vals.cpu().numpy().view(np.int64), up.values.view(np.int64))
+
+
 def test_run_matches_oracle_random_large_k():
     """A longer run at k=500 on fresh data: every iteration bit-identical."""
     from oracle import oracle as O

@@ -49,6 +49,8 @@ def test_abi_constants_and_struct_layout():
     assert lib.ivfkm_bivf_nblk(60000) == 1880
     assert lib.ivfkm_assign_workspace_size(1000, 10) > 1000 * 4 * 36
     assert lib.ivfkm_update_workspace_size(10, 100, 5, 50) > 0
+    assert lib.ivfkm_update_state_size(10, 100, 5, 50) > 0
+    assert lib.ivfkm_update_state_size(1 << 30, 100, 1 << 20, 1 << 20) == 0  # 70-bit key
 
 
 def test_host_entry_point_reports_missing_gpu_or_range():
