@@ -1059,34 +1059,54 @@ struct ExactCtx {
   const double* pv64;
 };
 
-// Warp-cooperative: lanes look up 64 nonzeros at a time (two independent
-// lookup chains in flight) and park the products in the warp's shared
-// scratch (64 doubles); lane 0 then adds them in row order.  An absent
-// posting parks +0.0: adding it is exact (x + 0.0 == x; at most the sign of
-// an all-zero sum differs, which no comparison or sum can see), so the sum
-// equals the reference's sum over present postings.
+// Warp-cooperative: lanes look up kExactU*32 nonzeros at a time (every
+// lookup chain of the chunk in flight: term -> mask + block offset -> value)
+// and park the products in the warp's shared scratch; lane 0 then adds them
+// in row order.  An absent posting parks +0.0: adding it is exact
+// (x + 0.0 == x; at most the sign of an all-zero sum differs, which no
+// comparison or sum can see), so the sum equals the reference's sum over
+// present postings.
+constexpr int kExactU = 4;
+
 __device__ double exact_score_warp(const ExactCtx& x, int64_t rb, int64_t re, int c, int lane,
                                    double* scratch) {
   double acc = 0.0;
   const int64_t slot = x.bv.perm ? (int64_t)__ldg(x.bv.perm + c) : c;
-  for (int64_t h0 = rb; h0 < re; h0 += 64) {
-    const int64_t ha = h0 + lane, hb = h0 + 32 + lane;
-    const int32_t ta = ha < re ? x.terms[ha] : -1;
-    const int32_t tb = hb < re ? x.terms[hb] : -1;
-    const int64_t pa = ta >= 0 ? bivf_find_slot(x.bv, ta, slot) : -1;
-    const int64_t pb = tb >= 0 ? bivf_find_slot(x.bv, tb, slot) : -1;
-    scratch[lane] = pa >= 0 ? __dmul_rn(x.val64[ha], __ldg(x.pv64 + pa)) : 0.0;
-    scratch[32 + lane] = pb >= 0 ? __dmul_rn(x.val64[hb], __ldg(x.pv64 + pb)) : 0.0;
+  const int64_t sb = slot >> 5;
+  const uint32_t bit = 1u << (slot & 31);
+  for (int64_t h0 = rb; h0 < re; h0 += 32 * kExactU) {
+    int32_t t[kExactU];
+    uint32_t m[kExactU];
+    int64_t o[kExactU];
+#pragma unroll
+    for (int u = 0; u < kExactU; ++u) {
+      const int64_t h = h0 + 32 * u + lane;
+      t[u] = h < re ? __ldg(x.terms + h) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kExactU; ++u) {
+      const int64_t q = (int64_t)t[u] * x.bv.nblk + sb;
+      m[u] = t[u] >= 0 ? __ldg(x.bv.masks + q) : 0u;
+      o[u] = t[u] >= 0 ? (int64_t)__ldg(x.bv.off64 + q) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kExactU; ++u) {
+      const int64_t h = h0 + 32 * u + lane;
+      scratch[32 * u + lane] =
+          (m[u] & bit) ? __dmul_rn(__ldg(x.val64 + h),
+                                   __ldg(x.pv64 + o[u] + __popc(m[u] & (bit - 1u))))
+                       : 0.0;
+    }
     __syncwarp();
     if (lane == 0) {
-      const int m = re - h0 < 64 ? (int)(re - h0) : 64;
+      const int n = re - h0 < 32 * kExactU ? (int)(re - h0) : 32 * kExactU;
       int j = 0;
-      for (; j + 4 <= m; j += 4) {
+      for (; j + 4 <= n; j += 4) {
         const double2 u = reinterpret_cast<const double2*>(scratch)[j >> 1];
         const double2 v = reinterpret_cast<const double2*>(scratch)[(j >> 1) + 1];
         acc = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(acc, u.x), u.y), v.x), v.y);
       }
-      for (; j < m; ++j) acc = __dadd_rn(acc, scratch[j]);
+      for (; j < n; ++j) acc = __dadd_rn(acc, scratch[j]);
     }
     __syncwarp();
   }
@@ -1125,7 +1145,7 @@ __device__ __forceinline__ bool ivfd_falls_back(const FinalParams& p, double bes
 }
 
 __global__ void __launch_bounds__(256) finalize_kernel(FinalParams p) {
-  __shared__ __align__(16) double s_scr[8][64];
+  __shared__ __align__(16) double s_scr[8][32 * kExactU];
   const int lane = threadIdx.x & 31;
   double* scratch = s_scr[threadIdx.x >> 5];
   const int64_t wpb = blockDim.x >> 5;
@@ -1173,7 +1193,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalParams p) {
 
 __global__ void __launch_bounds__(256) score_labels_kernel(int64_t n_obj, ExactCtx x,
                                                            const int32_t* labels, double* sims) {
-  __shared__ __align__(16) double s_scr[8][64];
+  __shared__ __align__(16) double s_scr[8][32 * kExactU];
   const int lane = threadIdx.x & 31;
   double* scratch = s_scr[threadIdx.x >> 5];
   const int64_t wpb = blockDim.x >> 5;

@@ -45,6 +45,7 @@ struct UpdWs {
   K* seg_key;
   double* seg_w;
   uint32_t* cl_seg;   // k+1
+  uint32_t* gstart;   // k * (leaf groups + 1): first run of each (cluster, leaf group)
   double* nrm;        // k
   int64_t* counts;    // k+1
   uint32_t* n_seg;    // 1
@@ -77,6 +78,11 @@ struct NormPlan {
 };
 
 int64_t norm_plan_ints_max(int64_t dim) { return 4 * (dim / 64 + 2) + 130; }
+
+// The norm kernel takes leaves in groups of kLeafG (one warp, one dense
+// shared window of <= kLeafG * 128 positions).
+constexpr int kLeafG = 4;
+inline int64_t leaf_groups_max(int64_t dim) { return (dim / 64 + 2) / kLeafG + 2; }
 
 const NormPlan& norm_plan(int64_t D) {
   static std::mutex mu;
@@ -155,6 +161,7 @@ UpdWs<K> carve_upd(void* base, int64_t nnz, int64_t k, int64_t dim, size_t* tota
   w.seg_key = c.take<K>(n);
   w.seg_w = c.take<double>(n);
   w.cl_seg = c.take<uint32_t>(k + 1);
+  w.gstart = c.take<uint32_t>((size_t)k * (size_t)(leaf_groups_max(dim) + 1));
   w.nrm = c.take<double>(k);
   w.counts = c.take<int64_t>(k + 1);
   w.n_seg = c.take<uint32_t>(4);
@@ -219,12 +226,18 @@ __global__ void segstart_kernel(int64_t nnz, const K* __restrict__ key,
 
 // One thread per (cluster, term) run: sequential float64 sum in ascending
 // object order (bincount), then w = sum / size.  Reuses `head` as the
-// nonzero flag array, [0, n_seg] (nz[n_seg] = 0 closes the scan).
+// nonzero flag array, [0, n_seg] (nz[n_seg] = 0 closes the scan).  Runs
+// longer than kLongRun (the hot terms: hundreds of members each) go to a
+// list summed a warp per run (segsum_long_kernel), so no thread walks a
+// long run four loads at a time.
+constexpr uint32_t kLongRun = 40;
+
 template <class K>
 __global__ void segsum_kernel(int64_t n_seg, const uint32_t* __restrict__ seg_start,
                               const K* __restrict__ seg_key, const double* __restrict__ sval,
                               const unsigned long long* __restrict__ sizes, int64_t dim,
-                              double* __restrict__ seg_w, uint32_t* __restrict__ nz) {
+                              double* __restrict__ seg_w, uint32_t* __restrict__ nz,
+                              uint32_t* __restrict__ long_list, uint32_t* __restrict__ n_long) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s <= n_seg;
        s += (int64_t)gridDim.x * blockDim.x) {
     if (s == n_seg) {
@@ -234,6 +247,10 @@ __global__ void segsum_kernel(int64_t n_seg, const uint32_t* __restrict__ seg_st
     double acc = 0.0;
     uint32_t e = seg_start[s];
     const uint32_t end = seg_start[s + 1];
+    if (end - e > kLongRun) {
+      long_list[atomicAdd(n_long, 1u)] = (uint32_t)s;
+      continue;
+    }
     for (; e + 4 <= end; e += 4) {  // four loads in flight, adds in order
       const double a = sval[e], b = sval[e + 1], c2 = sval[e + 2], d = sval[e + 3];
       acc = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(acc, a), b), c2), d);
@@ -243,6 +260,56 @@ __global__ void segsum_kernel(int64_t n_seg, const uint32_t* __restrict__ seg_st
     const double w = __ddiv_rn(acc, (double)sizes[c]);
     seg_w[s] = w;
     nz[s] = (w != 0.0) ? 1u : 0u;
+  }
+}
+
+// A warp per long run: lanes stage 64 values at a time in shared memory
+// (the next 64 already in flight) and lane 0 adds them in order.
+template <class K>
+__global__ void __launch_bounds__(256) segsum_long_kernel(
+    const uint32_t* __restrict__ seg_start, const K* __restrict__ seg_key,
+    const double* __restrict__ sval, const unsigned long long* __restrict__ sizes, int64_t dim,
+    double* __restrict__ seg_w, uint32_t* __restrict__ nz, const uint32_t* __restrict__ long_list,
+    const uint32_t* __restrict__ n_long) {
+  __shared__ __align__(16) double s_buf[8][64];
+  const int lane = threadIdx.x & 31;
+  double* buf = s_buf[threadIdx.x >> 5];
+  const double2* buf2 = reinterpret_cast<const double2*>(buf);
+  const uint32_t n = *n_long;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t q = blockIdx.x * wpb + (threadIdx.x >> 5); q < n; q += gridDim.x * wpb) {
+    const uint32_t s = long_list[q];
+    const uint32_t b = seg_start[s], end = seg_start[s + 1];
+    double acc = 0.0;
+    double x0 = b + lane < end ? sval[b + lane] : 0.0;
+    double x1 = b + 32 + lane < end ? sval[b + 32 + lane] : 0.0;
+    for (uint32_t e0 = b; e0 < end; e0 += 64) {
+      buf[lane] = x0;
+      buf[32 + lane] = x1;
+      __syncwarp();
+      const uint32_t e1 = e0 + 64;
+      x0 = e1 + lane < end ? sval[e1 + lane] : 0.0;
+      x1 = e1 + 32 + lane < end ? sval[e1 + 32 + lane] : 0.0;
+      if (lane == 0) {
+        const uint32_t m = end - e0 < 64 ? end - e0 : 64;
+        if (m == 64) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const double2 v = buf2[j];
+            acc = __dadd_rn(__dadd_rn(acc, v.x), v.y);
+          }
+        } else {
+          for (uint32_t j = 0; j < m; ++j) acc = __dadd_rn(acc, buf[j]);
+        }
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      const int64_t c = (int64_t)(seg_key[s] / (K)dim);
+      const double w = __ddiv_rn(acc, (double)sizes[c]);
+      seg_w[s] = w;
+      nz[s] = (w != 0.0) ? 1u : 0u;
+    }
   }
 }
 
@@ -269,55 +336,78 @@ __global__ void clseg_kernel(int64_t k, int64_t dim, const uint32_t* __restrict_
 // when D <= 128) depend on D only; a leaf of >= 8 elements sums into 8
 // strided accumulators combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a
 // sequential tail, a leaf under 8 elements is a plain sequential sum.  Zeros
-// add exact +0.0, so a leaf only visits the cluster's nonzeros in its range.
-// (tests/test_update_numerics.py checks the replay against np.sum.)
-//
-// One CTA per cluster: threads compute the leaves in parallel, thread 0
-// combines them in the recursion's order.
+// add exact +0.0, so only the cluster's nonzeros need visiting (scattered
+// into a zeroed window by norm_kernel).
+// (test_gpu_parity.py::test_update_norm_across_dims checks it at many D.)
 
-template <class K>
-__device__ double leaf_value(int64_t lo, int64_t n, uint32_t cur, uint32_t end, const K* seg_key,
-                             const double* seg_w, K base) {
-  if (n < 8) {
-    double res = 0.0;
-    while (cur < end && (int64_t)(seg_key[cur] - base) < lo + n) {
-      const double w = seg_w[cur++];
-      res = __dadd_rn(res, __dmul_rn(w, w));
-    }
-    return res;
+// First run of every (cluster, leaf group): runs are sorted by (cluster,
+// term), so group boundaries are where the group of consecutive runs'
+// positions changes; groups holding no run point at the next run.
+__device__ __forceinline__ int group_of(int64_t pos, const int32_t* glo, int ng) {
+  int lo = 0, hi = ng - 1;  // last g with glo[g] <= pos
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (glo[mid] <= pos) lo = mid; else hi = mid - 1;
   }
-  double r[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-  const int64_t lim = lo + n - (n % 8);
-  while (cur < end) {
-    const int64_t pos = (int64_t)(seg_key[cur] - base);
-    if (pos >= lim) break;
-    const double w = seg_w[cur++];
-    const int j = (int)((pos - lo) & 7);
-    r[j] = __dadd_rn(r[j], __dmul_rn(w, w));
-  }
-  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-  while (cur < end && (int64_t)(seg_key[cur] - base) < lo + n) {
-    const double w = seg_w[cur++];
-    res = __dadd_rn(res, __dmul_rn(w, w));
-  }
-  return res;
+  return lo;
 }
 
 template <class K>
-__global__ void __launch_bounds__(256) norm_kernel(
+__global__ void __launch_bounds__(256) gstart_kernel(const uint32_t* __restrict__ n_seg_p,
+                                                     const K* __restrict__ seg_key, int64_t dim,
+                                                     const int32_t* __restrict__ plan,
+                                                     int64_t nleaf, uint32_t* __restrict__ gstart) {
+  extern __shared__ int32_t glo[];  // group start positions
+  const int ng = (int)((nleaf + kLeafG - 1) / kLeafG);
+  for (int g = threadIdx.x; g < ng; g += blockDim.x) glo[g] = plan[(int64_t)g * kLeafG];
+  __syncthreads();
+  const int64_t n_seg = *n_seg_p;
+  const int64_t stride = ng + 1;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_seg;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const K key = seg_key[s];
+    const int64_t c = (int64_t)(key / (K)dim);
+    const int g = group_of((int64_t)(key - (K)c * (K)dim), glo, ng);
+    uint32_t* gs = gstart + c * stride;
+    int from = 0;
+    if (s > 0) {
+      const K pk = seg_key[s - 1];
+      const int64_t pc = (int64_t)(pk / (K)dim);
+      if (pc == c) from = group_of((int64_t)(pk - (K)pc * (K)dim), glo, ng) + 1;
+    }
+    for (int q = from; q <= g; ++q) gs[q] = (uint32_t)s;
+    bool last = s + 1 == n_seg;
+    if (!last) last = (int64_t)(seg_key[s + 1] / (K)dim) != c;
+    if (last)
+      for (int q = g + 1; q <= ng; ++q) gs[q] = (uint32_t)(s + 1);
+  }
+}
+
+// One CTA per cluster, one warp per group of kLeafG leaves: the group's runs
+// (a contiguous range, gstart) put w*w into the warp's zeroed dense window
+// (absent terms stay 0.0); lane 8i+j sums leaf i's strided accumulator j,
+// shuffles combine them in numpy's order, lane 8i adds the tail.  The
+// internal nodes are then evaluated level by level.
+constexpr int kNormWarps = 16;
+
+template <class K>
+__global__ void __launch_bounds__(kNormWarps * 32) norm_kernel(
     int64_t k, int64_t dim, int64_t nleaf, int64_t nint, int64_t nlevels,
     const int32_t* __restrict__ plan, const unsigned long long* __restrict__ sizes,
     const int64_t* __restrict__ prev_ptr, const uint32_t* __restrict__ cl_seg,
-    const K* __restrict__ seg_key, const double* __restrict__ seg_w,
-    const uint32_t* __restrict__ nz, double* __restrict__ nrm, int64_t* __restrict__ counts) {
+    const uint32_t* __restrict__ gstart, const K* __restrict__ seg_key,
+    const double* __restrict__ seg_w, const uint32_t* __restrict__ nzpos,
+    double* __restrict__ nrm, int64_t* __restrict__ counts) {
   extern __shared__ __align__(16) unsigned char smem[];
-  double* val = reinterpret_cast<double*>(smem);                  // nleaf + nint
+  double* win_all = reinterpret_cast<double*>(smem);              // warps * kLeafG * 128
+  double* val = win_all + kNormWarps * kLeafG * 128;               // nleaf + nint
   int32_t* leaf_lo = reinterpret_cast<int32_t*>(val + nleaf + nint);  // nleaf + 1
   const int32_t* lv_off = plan + nleaf + 1;
   const int32_t* node_l = lv_off + nlevels + 1;
   const int32_t* node_r = node_l + nint;
-  __shared__ int64_t s_cnt;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* win = win_all + warp * kLeafG * 128;
+  const int ng = (int)((nleaf + kLeafG - 1) / kLeafG);
   for (int64_t j = threadIdx.x; j <= nleaf; j += blockDim.x) leaf_lo[j] = plan[j];
   if (blockIdx.x == 0 && threadIdx.x == 0) counts[k] = 0;
   __syncthreads();
@@ -329,24 +419,51 @@ __global__ void __launch_bounds__(256) norm_kernel(
       }
       continue;
     }
-    const uint32_t b = cl_seg[c], e = cl_seg[c + 1];
+    const uint32_t* gs = gstart + c * (int64_t)(ng + 1);
     const K base = (K)c * (K)dim;
-    if (threadIdx.x == 0) s_cnt = 0;
-    __syncthreads();
-    int64_t cnt = 0;
-    for (uint32_t sidx = b + threadIdx.x; sidx < e; sidx += blockDim.x) cnt += nz[sidx];
-    for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
-    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd((unsigned long long*)&s_cnt, (unsigned long long)cnt);
-    for (int64_t j = threadIdx.x; j < nleaf; j += blockDim.x) {
-      const int64_t lo = leaf_lo[j], hi = leaf_lo[j + 1];
-      // first run of this cluster at or after position lo
-      uint32_t a = b, z = e;
-      const K target = base + (K)lo;
-      while (a < z) {
-        const uint32_t mid = (a + z) >> 1;
-        if (seg_key[mid] < target) a = mid + 1; else z = mid;
+    const bool no_runs = cl_seg[c] == cl_seg[c + 1];  // members with empty rows only
+    for (int g = warp; g < ng; g += kNormWarps) {
+      const uint32_t s0 = no_runs ? 0u : gs[g], s1 = no_runs ? 0u : gs[g + 1];
+      const int l0 = g * kLeafG;
+      const int nl = (int)(nleaf - l0 < kLeafG ? nleaf - l0 : kLeafG);
+      const int p0 = leaf_lo[l0], np = leaf_lo[l0 + nl] - p0;
+      for (int i = lane; i < np; i += 32) win[i] = 0.0;
+      __syncwarp();
+      for (uint32_t sidx = s0 + lane; sidx < s1; sidx += 32) {
+        const double w = seg_w[sidx];
+        win[(int64_t)(seg_key[sidx] - base) - p0] = __dmul_rn(w, w);
       }
-      val[j] = leaf_value<K>(lo, hi - lo, a, e, seg_key, seg_w, base);
+      __syncwarp();
+      const int li = lane >> 3, j = lane & 7;
+      const bool has = li < nl;
+      const int lo = has ? leaf_lo[l0 + li] - p0 : 0;
+      const int n = has ? leaf_lo[l0 + li + 1] - leaf_lo[l0 + li] : 0;
+      double r = 0.0;
+      if (n < 8) {
+        if (j == 0)
+          for (int i = 0; i < n; ++i) r = __dadd_rn(r, win[lo + i]);
+      } else {
+        const int lim = n - (n & 7);
+        for (int i = j; i < lim; i += 8) r = __dadd_rn(r, win[lo + i]);
+      }
+      // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))
+      const double r1 = __shfl_down_sync(kFull, r, 1);
+      const double a = __dadd_rn(r, r1);
+      const double a2 = __shfl_down_sync(kFull, a, 2);
+      const double b2 = __dadd_rn(a, a2);
+      const double b4 = __shfl_down_sync(kFull, b2, 4);
+      const double c8 = __dadd_rn(b2, b4);
+      if (has && j == 0) {
+        double res;
+        if (n < 8) {
+          res = r;
+        } else {
+          res = c8;
+          for (int i = n - (n & 7); i < n; ++i) res = __dadd_rn(res, win[lo + i]);
+        }
+        val[l0 + li] = res;
+      }
+      __syncwarp();
     }
     __syncthreads();
     // internal nodes level by level: pw(node) = pw(left) + pw(right)
@@ -356,7 +473,8 @@ __global__ void __launch_bounds__(256) norm_kernel(
       __syncthreads();
     }
     if (threadIdx.x == 0) {
-      counts[c] = s_cnt;
+      const uint32_t b = cl_seg[c], e = cl_seg[c + 1];
+      counts[c] = (int64_t)nzpos[e] - (int64_t)nzpos[b];
       nrm[c] = __dsqrt_rn(val[nleaf + nint - 1]);
     }
     __syncthreads();
@@ -569,6 +687,8 @@ __global__ void derive_keys_kernel(int64_t nnz, const unsigned long long* __rest
   }
 }
 
+__global__ void set_hdr_kernel(DeltaHdr* hdr, DeltaHdr v) { *hdr = v; }
+
 // Sorted (key, value) for this update: the composite-key state S brought up to
 // the current labels (incrementally when few objects moved); returns the S
 // buffers through *sk / *sv.
@@ -579,22 +699,21 @@ int delta_sort(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms, cons
   const Bits bt = comp_bits(n_obj, dim, k);
   const int total_bits = bt.ob + bt.tb + bt.lb;
   const int T = 256;
+  // the header and the movers' counts come back in one read (on a fresh
+  // state the counts are computed against zeros and ignored)
   DeltaHdr h;
+  unsigned long long cnt[2] = {0, 0};
+  IVFKM_TRY(cudaMemsetAsync(d.counts, 0, sizeof(unsigned long long) * 4, st));
+  changed_kernel<<<grid_for(n_obj, T), T, 0, st>>>(n_obj, labels, d.labels, row_ptr, d.oflag,
+                                                  d.cptr, d.counts);
+  IVFKM_CHECK_LAUNCH();
   IVFKM_TRY(cudaMemcpyAsync(&h, d.hdr, sizeof(h), cudaMemcpyDeviceToHost, st));
+  IVFKM_TRY(cudaMemcpyAsync(cnt, d.counts, sizeof(cnt), cudaMemcpyDeviceToHost, st));
   IVFKM_TRY(cudaStreamSynchronize(st));
   bool full = !(h.magic == kDeltaMagic && h.valid == 1 && h.n_obj == n_obj && h.nnz == nnz &&
                 h.k == k && h.dim == dim && (h.cur == 0 || h.cur == 1));
   int cur = full ? 0 : (int)h.cur;
-  unsigned long long cnt[2] = {0, 0};
-  if (!full) {
-    IVFKM_TRY(cudaMemsetAsync(d.counts, 0, sizeof(unsigned long long) * 4, st));
-    changed_kernel<<<grid_for(n_obj, T), T, 0, st>>>(n_obj, labels, d.labels, row_ptr, d.oflag,
-                                                    d.cptr, d.counts);
-    IVFKM_CHECK_LAUNCH();
-    IVFKM_TRY(cudaMemcpyAsync(cnt, d.counts, sizeof(cnt), cudaMemcpyDeviceToHost, st));
-    IVFKM_TRY(cudaStreamSynchronize(st));
-    if ((int64_t)cnt[1] > delta_cap(nnz) - 1024) full = true;
-  }
+  if (!full && (int64_t)cnt[1] > delta_cap(nnz) - 1024) full = true;
   if (full) {
     comp_keys_kernel<<<grid_for(n_obj, T / 32), T, 0, st>>>(n_obj, row_ptr, terms, val64, labels,
                                                            nullptr, 0, nullptr, bt, d.key[0],
@@ -652,9 +771,8 @@ int delta_sort(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms, cons
   // remember the labels S now holds
   IVFKM_TRY(cudaMemcpyAsync(d.labels, labels, sizeof(int32_t) * n_obj, cudaMemcpyDeviceToDevice,
                             st));
-  DeltaHdr nh{kDeltaMagic, n_obj, nnz, k, dim, 1, cur, 0};
-  IVFKM_TRY(cudaMemcpyAsync(d.hdr, &nh, sizeof(nh), cudaMemcpyHostToDevice, st));
-  IVFKM_TRY(cudaStreamSynchronize(st));  // nh lives on this stack frame
+  set_hdr_kernel<<<1, 1, 0, st>>>(d.hdr, DeltaHdr{kDeltaMagic, n_obj, nnz, k, dim, 1, cur, 0});
+  IVFKM_CHECK_LAUNCH();
   *sk = d.key[cur];
   *sv = d.val[cur];
   return IVFKM_OK;
@@ -705,8 +823,13 @@ int update_count_impl(int64_t n_obj, const int64_t* row_ptr, const int32_t* term
     uint32_t n_seg = 0;
     IVFKM_TRY(cudaMemcpyAsync(&n_seg, w.n_seg, sizeof(n_seg), cudaMemcpyDeviceToHost, st));
     IVFKM_TRY(cudaStreamSynchronize(st));
+    IVFKM_TRY(cudaMemsetAsync(w.n_seg + 1, 0, sizeof(uint32_t), st));
+    // segpos is free again: it holds the long-run list
     segsum_kernel<K><<<grid_for((int64_t)n_seg + 1, T), T, 0, st>>>(
-        n_seg, w.seg_start, w.seg_key, sval, sizes, dim, w.seg_w, w.head);
+        n_seg, w.seg_start, w.seg_key, sval, sizes, dim, w.seg_w, w.head, w.segpos, w.n_seg + 1);
+    IVFKM_CHECK_LAUNCH();
+    segsum_long_kernel<K><<<kNumSM * 8, 256, 0, st>>>(w.seg_start, w.seg_key, sval, sizes, dim,
+                                                      w.seg_w, w.head, w.segpos, w.n_seg + 1);
     IVFKM_CHECK_LAUNCH();
     cb = w.cub_bytes;
     IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.head, w.nzpos, (int)n_seg + 1, st));
@@ -717,16 +840,23 @@ int update_count_impl(int64_t n_obj, const int64_t* row_ptr, const int32_t* term
   IVFKM_CHECK_LAUNCH();
   const NormPlan& P = norm_plan(dim);
   const int64_t nleaf = P.nleaf, nint = P.nint;
-  const size_t nsmem = (size_t)(nleaf + nint) * 8 + (size_t)(nleaf + 1) * 4;
-  if (nsmem > 200 * 1024) return IVFKM_E_UNSUPPORTED;  // D beyond ~1.1M terms
+  const size_t nsmem = (size_t)kNormWarps * kLeafG * 128 * 8 + (size_t)(nleaf + nint) * 8 +
+                       (size_t)(nleaf + 1) * 4;
+  if (nsmem > 200 * 1024) return IVFKM_E_UNSUPPORTED;  // D beyond ~1M terms
   // the plan lives in a process-lifetime cache, so an async copy is safe
   IVFKM_TRY(cudaMemcpyAsync(w.plan, P.buf.data(), P.buf.size() * sizeof(int32_t),
                             cudaMemcpyHostToDevice, st));
+  const int ng = (int)((nleaf + kLeafG - 1) / kLeafG);
+  if (nnz > 0) {
+    gstart_kernel<K><<<grid_for(nnz / 4 + 1, T), T, (size_t)ng * 4, st>>>(w.n_seg, w.seg_key, dim,
+                                                                          w.plan, nleaf, w.gstart);
+    IVFKM_CHECK_LAUNCH();
+  }
   IVFKM_TRY(cudaFuncSetAttribute(norm_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)nsmem));
-  norm_kernel<K><<<(int)std::min<int64_t>(k, kNumSM * 8), 256, nsmem, st>>>(
-      k, dim, nleaf, nint, P.nlevels, w.plan, sizes, prev_ptr, w.cl_seg, w.seg_key, w.seg_w,
-      w.head, w.nrm, w.counts);
+  norm_kernel<K><<<(int)std::min<int64_t>(k, kNumSM * 4), kNormWarps * 32, nsmem, st>>>(
+      k, dim, nleaf, nint, P.nlevels, w.plan, sizes, prev_ptr, w.cl_seg, w.gstart, w.seg_key,
+      w.seg_w, w.nzpos, w.nrm, w.counts);
   IVFKM_CHECK_LAUNCH();
   size_t cb = w.cub_bytes;
   IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.counts, new_ptr, (int)(k + 1), st));

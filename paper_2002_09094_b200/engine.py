@@ -146,15 +146,16 @@ class DeviceMeans:
 def update_launches(k: int, dim: int) -> int:
     """Kernels one update launches: keys, CUB onesweep radix sort (histogram,
     exclusive sum, one pass per 8 key bits), head, 3 CUB scans (init + sweep
-    each), segstart, segsum, clseg, norm, fill, retain."""
+    each), segstart, segsum (short + long runs), clseg, group starts, norm,
+    fill, retain."""
     bits = max(1, int(np.ceil(np.log2(max(2.0, float(k) * float(dim))))))
-    return 16 + (bits + 7) // 8
+    return 18 + (bits + 7) // 8
 
 def delta_update_launches() -> int:
     """Extra kernels of the label-delta sort (changed, keep flags, 3 CUB
     selects, lengths, scan, keys, the changed entries' radix sort, merge,
-    derived keys) in place of keys + the full sort."""
-    return 23
+    derived keys, header) in place of keys + the full sort."""
+    return 24
 
 
 def update_rows(lib, n_obj, nnz, row_ptr, terms, val64, labels0, sizes, prev: DeviceMeans, k,
@@ -335,7 +336,7 @@ class LloydEngine:
         self.launches += update_launches(self.k, dd.dim)
         if self.upd_state is not None:
             # minus keys + the full sort (histogram, exclusive sum, passes)
-            self.launches += delta_update_launches() - (update_launches(self.k, dd.dim) - 13)
+            self.launches += delta_update_launches() - (update_launches(self.k, dd.dim) - 15)
         return self.build_bivf(out)
 
     def set_sizes_from_labels(self, labels0: torch.Tensor) -> None:

@@ -406,6 +406,32 @@ def test_update_label_delta_sort_matches_oracle_bitwise():
     assert np.array_equal(out.vals.cpu().numpy().view(np.int64), up.values.view(np.int64))
 
 
+@pytest.mark.parametrize("dim", [5, 8, 100, 128, 129, 257, 4095, 4096, 4097, 4200, 8193, 30011])
+def test_update_norm_across_dims(dim):
+    """The norm's pairwise-sum replay (leaves, leaf batches of the dense
+    window, tails) against numpy's own sum at dims around every boundary."""
+    from oracle import oracle as O
+
+    P = _pkg()
+    rng = np.random.default_rng(dim)
+    n, k = 400, 7
+    lens = rng.integers(1, min(dim, 300) + 1, n)
+    ip = np.zeros(n + 1, np.int64)
+    np.cumsum(lens, out=ip[1:])
+    t = np.concatenate([np.sort(rng.choice(dim, m, replace=False)) + 1 for m in lens])
+    v = rng.random(ip[-1]) + 1e-3
+    for i in range(n):
+        v[ip[i]:ip[i + 1]] /= np.sqrt(np.sum(v[ip[i]:ip[i + 1]] ** 2))
+    ds = P.Dataset(dim, ip, t.astype(np.int32), v, normalized=True)
+    om = O.init_means(ds, k, 1)
+    means = P.MeanSet.from_csr(om.indptr, om.term_ids, om.values, dim, "sparse_inverted")
+    labels = rng.integers(1, k + 1, size=n).astype(np.int32)
+    up = P.update_ivf(ds, P.Assignment.from_labels(labels, k), means)
+    ref = O.update(ds, labels, om)
+    assert np.array_equal(up.indptr, ref.indptr)
+    assert np.array_equal(up.values.view(np.int64), ref.values.view(np.int64))
+
+
 def test_run_matches_oracle_random_large_k():
     """A longer run at k=500 on fresh data: every iteration bit-identical."""
     from oracle import oracle as O
