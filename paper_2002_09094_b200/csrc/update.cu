@@ -197,31 +197,20 @@ __global__ void keys_kernel(int64_t n_obj, const int64_t* __restrict__ row_ptr,
   }
 }
 
+// Sorted (cluster * D + term) keys, read from the key array (full sort) or
+// derived from the composite (cluster, term, object) keys of the label-delta
+// sort.
 template <class K>
-__global__ void head_kernel(int64_t nnz, const K* __restrict__ key, uint32_t* __restrict__ head) {
+struct ArrKey {
+  const K* p;
+  __device__ __forceinline__ K operator()(int64_t e) const { return p[e]; }
+};
+
+template <class K, class R>
+__global__ void head_kernel(int64_t nnz, R key, uint32_t* __restrict__ head) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
        e += (int64_t)gridDim.x * blockDim.x)
-    head[e] = (e == 0 || key[e] != key[e - 1]) ? 1u : 0u;
-}
-
-template <class K>
-__global__ void segstart_kernel(int64_t nnz, const K* __restrict__ key,
-                                const uint32_t* __restrict__ head,
-                                const uint32_t* __restrict__ segpos,
-                                uint32_t* __restrict__ seg_start, K* __restrict__ seg_key,
-                                uint32_t* __restrict__ n_seg) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    if (head[e]) {
-      seg_start[segpos[e]] = (uint32_t)e;
-      seg_key[segpos[e]] = key[e];
-    }
-    if (e == nnz - 1) {
-      const uint32_t ns = segpos[e] + head[e];
-      *n_seg = ns;
-      seg_start[ns] = (uint32_t)nnz;
-    }
-  }
+    head[e] = (e == 0 || key(e) != key(e - 1)) ? 1u : 0u;
 }
 
 // One thread per (cluster, term) run: sequential float64 sum in ascending
@@ -352,28 +341,64 @@ __device__ __forceinline__ int group_of(int64_t pos, const int32_t* glo, int ng)
   return lo;
 }
 
+template <class K, class R>
+__global__ void segstart_kernel(int64_t nnz, R key, const uint32_t* __restrict__ head,
+                                const uint32_t* __restrict__ segpos,
+                                uint32_t* __restrict__ seg_start, K* __restrict__ seg_key,
+                                uint32_t* __restrict__ n_seg) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (head[e]) {
+      seg_start[segpos[e]] = (uint32_t)e;
+      seg_key[segpos[e]] = key(e);
+    }
+    if (e == nnz - 1) {
+      const uint32_t ns = segpos[e] + head[e];
+      *n_seg = ns;
+      seg_start[ns] = (uint32_t)nnz;
+    }
+  }
+}
+
+// First run of every (cluster, leaf group), one thread per run: groups
+// after the previous run's group (same cluster; else from 0) up to this
+// run's start here, and a cluster's last run closes its remaining groups.
+// Groups holding no run thus point at the next run.  (A separate pass: done
+// at the run heads inside segstart it diverges and costs more.)
 template <class K>
 __global__ void __launch_bounds__(256) gstart_kernel(const uint32_t* __restrict__ n_seg_p,
                                                      const K* __restrict__ seg_key, int64_t dim,
                                                      const int32_t* __restrict__ plan,
                                                      int64_t nleaf, uint32_t* __restrict__ gstart) {
-  extern __shared__ int32_t glo[];  // group start positions
+  // glo[ng]: group start positions; tab[pos >> 8]: the group holding the
+  // bucket's first position (a group spans >= 256 positions when D > 128, so
+  // at most two more starts fall in one bucket)
+  extern __shared__ int32_t glo[];
   const int ng = (int)((nleaf + kLeafG - 1) / kLeafG);
+  const int nb = (int)(dim >> 8) + 1;
+  int32_t* tab = glo + ng;
   for (int g = threadIdx.x; g < ng; g += blockDim.x) glo[g] = plan[(int64_t)g * kLeafG];
   __syncthreads();
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) tab[b] = group_of((int64_t)b << 8, glo, ng);
+  __syncthreads();
+  auto gof = [&](int64_t pos) {
+    int g = tab[pos >> 8];
+    while (g + 1 < ng && glo[g + 1] <= pos) ++g;
+    return g;
+  };
   const int64_t n_seg = *n_seg_p;
   const int64_t stride = ng + 1;
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_seg;
        s += (int64_t)gridDim.x * blockDim.x) {
     const K key = seg_key[s];
     const int64_t c = (int64_t)(key / (K)dim);
-    const int g = group_of((int64_t)(key - (K)c * (K)dim), glo, ng);
+    const int g = gof((int64_t)(key - (K)c * (K)dim));
     uint32_t* gs = gstart + c * stride;
     int from = 0;
     if (s > 0) {
       const K pk = seg_key[s - 1];
       const int64_t pc = (int64_t)(pk / (K)dim);
-      if (pc == c) from = group_of((int64_t)(pk - (K)pc * (K)dim), glo, ng) + 1;
+      if (pc == c) from = gof((int64_t)(pk - (K)pc * (K)dim)) + 1;
     }
     for (int q = from; q <= g; ++q) gs[q] = (uint32_t)s;
     bool last = s + 1 == n_seg;
@@ -676,16 +701,15 @@ __global__ void keep_flags_kernel(int64_t nnz, const unsigned long long* __restr
 
 // composite (label, term, obj) -> the (label * dim + term) key of the classic path
 template <class K>
-__global__ void derive_keys_kernel(int64_t nnz, const unsigned long long* __restrict__ ck,
-                                   Bits bt, int64_t dim, K* __restrict__ key) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const unsigned long long c = ck[e];
-    const unsigned long long lab = c >> (bt.tb + bt.ob);
-    const unsigned long long t = (c >> bt.ob) & bt.tmask;
-    key[e] = (K)lab * (K)dim + (K)t;
+struct CompKey {
+  const unsigned long long* p;
+  Bits bt;
+  int64_t dim;
+  __device__ __forceinline__ K operator()(int64_t e) const {
+    const unsigned long long c = p[e];
+    return (K)(c >> (bt.tb + bt.ob)) * (K)dim + (K)((c >> bt.ob) & bt.tmask);
   }
-}
+};
 
 __global__ void set_hdr_kernel(DeltaHdr* hdr, DeltaHdr v) { *hdr = v; }
 
@@ -778,6 +802,24 @@ int delta_sort(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms, cons
   return IVFKM_OK;
 }
 
+// Run heads, their scan and the run starts / keys / leaf-group starts.
+template <class K, class R>
+int runs_impl(int64_t nnz, R rd, const UpdWs<K>& w, int64_t dim, int64_t nleaf, cudaStream_t st) {
+  const int T = 256;
+  head_kernel<K, R><<<grid_for(nnz, T), T, 0, st>>>(nnz, rd, w.head);
+  IVFKM_CHECK_LAUNCH();
+  size_t cb = w.cub_bytes;
+  IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.head, w.segpos, (int)nnz, st));
+  segstart_kernel<K, R><<<grid_for(nnz, T), T, 0, st>>>(nnz, rd, w.head, w.segpos, w.seg_start,
+                                                         w.seg_key, w.n_seg);
+  IVFKM_CHECK_LAUNCH();
+  const int ng = (int)((nleaf + kLeafG - 1) / kLeafG);
+  gstart_kernel<K><<<grid_for(nnz / 4 + 1, T), T, (size_t)(ng + (dim >> 8) + 1) * 4, st>>>(
+      w.n_seg, w.seg_key, dim, w.plan, nleaf, w.gstart);
+  IVFKM_CHECK_LAUNCH();
+  return IVFKM_OK;
+}
+
 template <class K>
 int update_count_impl(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
                       const double* val64, int64_t nnz, int64_t k, int64_t dim,
@@ -788,18 +830,23 @@ int update_count_impl(int64_t n_obj, const int64_t* row_ptr, const int32_t* term
   UpdWs<K> w = carve_upd<K>(ws, nnz, k, dim, &need);
   if (ws_bytes < need) return IVFKM_E_WORKSPACE;
   const int T = 256;
+  const NormPlan& P = norm_plan(dim);
+  const int64_t nleaf = P.nleaf, nint = P.nint;
+  const size_t nsmem = (size_t)kNormWarps * kLeafG * 128 * 8 + (size_t)(nleaf + nint) * 8 +
+                       (size_t)(nleaf + 1) * 4;
+  if (nsmem > 200 * 1024) return IVFKM_E_UNSUPPORTED;  // D beyond ~1M terms
+  // the plan lives in a process-lifetime cache, so an async copy is safe
+  IVFKM_TRY(cudaMemcpyAsync(w.plan, P.buf.data(), P.buf.size() * sizeof(int32_t),
+                            cudaMemcpyHostToDevice, st));
   if (nnz > 0) {
-    K* key;
     const double* sval;
     if (delta) {
       const unsigned long long* ck;
       int64_t moved = 0;
       IVFKM_TRY_RC(delta_sort(n_obj, row_ptr, terms, val64, nnz, k, dim, labels, *delta, &ck,
                               &sval, &moved, st));
-      derive_keys_kernel<K><<<grid_for(nnz, T), T, 0, st>>>(nnz, ck, comp_bits(n_obj, dim, k),
-                                                            dim, w.key_a);
-      IVFKM_CHECK_LAUNCH();
-      key = w.key_a;
+      IVFKM_TRY_RC(runs_impl<K>(nnz, CompKey<K>{ck, comp_bits(n_obj, dim, k), dim}, w, dim,
+                                nleaf, st));
     } else {
       keys_kernel<K><<<grid_for(n_obj, T / 32), T, 0, st>>>(n_obj, row_ptr, terms, val64, labels,
                                                             dim, w.key_a, w.val_a);
@@ -809,16 +856,9 @@ int update_count_impl(int64_t n_obj, const int64_t* row_ptr, const int32_t* term
       size_t cb = w.cub_bytes;
       IVFKM_TRY(cub::DeviceRadixSort::SortPairs(w.cub, cb, kb, vb, (int)nnz, 0, key_bits(k, dim),
                                                 st));
-      key = kb.Current();
       sval = vb.Current();
+      IVFKM_TRY_RC(runs_impl<K>(nnz, ArrKey<K>{kb.Current()}, w, dim, nleaf, st));
     }
-    head_kernel<K><<<grid_for(nnz, T), T, 0, st>>>(nnz, key, w.head);
-    IVFKM_CHECK_LAUNCH();
-    size_t cb = w.cub_bytes;
-    IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.head, w.segpos, (int)nnz, st));
-    segstart_kernel<K><<<grid_for(nnz, T), T, 0, st>>>(nnz, key, w.head, w.segpos, w.seg_start,
-                                                       w.seg_key, w.n_seg);
-    IVFKM_CHECK_LAUNCH();
     // the run count sizes the rest of the update (one 4-byte read-back)
     uint32_t n_seg = 0;
     IVFKM_TRY(cudaMemcpyAsync(&n_seg, w.n_seg, sizeof(n_seg), cudaMemcpyDeviceToHost, st));
@@ -831,27 +871,13 @@ int update_count_impl(int64_t n_obj, const int64_t* row_ptr, const int32_t* term
     segsum_long_kernel<K><<<kNumSM * 8, 256, 0, st>>>(w.seg_start, w.seg_key, sval, sizes, dim,
                                                       w.seg_w, w.head, w.segpos, w.n_seg + 1);
     IVFKM_CHECK_LAUNCH();
-    cb = w.cub_bytes;
+    size_t cb = w.cub_bytes;
     IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.head, w.nzpos, (int)n_seg + 1, st));
   } else {
     IVFKM_TRY(cudaMemsetAsync(w.n_seg, 0, sizeof(uint32_t), st));
   }
   clseg_kernel<K><<<grid_for(k + 1, T), T, 0, st>>>(k, dim, w.n_seg, w.seg_key, w.cl_seg);
   IVFKM_CHECK_LAUNCH();
-  const NormPlan& P = norm_plan(dim);
-  const int64_t nleaf = P.nleaf, nint = P.nint;
-  const size_t nsmem = (size_t)kNormWarps * kLeafG * 128 * 8 + (size_t)(nleaf + nint) * 8 +
-                       (size_t)(nleaf + 1) * 4;
-  if (nsmem > 200 * 1024) return IVFKM_E_UNSUPPORTED;  // D beyond ~1M terms
-  // the plan lives in a process-lifetime cache, so an async copy is safe
-  IVFKM_TRY(cudaMemcpyAsync(w.plan, P.buf.data(), P.buf.size() * sizeof(int32_t),
-                            cudaMemcpyHostToDevice, st));
-  const int ng = (int)((nleaf + kLeafG - 1) / kLeafG);
-  if (nnz > 0) {
-    gstart_kernel<K><<<grid_for(nnz / 4 + 1, T), T, (size_t)ng * 4, st>>>(w.n_seg, w.seg_key, dim,
-                                                                          w.plan, nleaf, w.gstart);
-    IVFKM_CHECK_LAUNCH();
-  }
   IVFKM_TRY(cudaFuncSetAttribute(norm_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)nsmem));
   norm_kernel<K><<<(int)std::min<int64_t>(k, kNumSM * 4), kNormWarps * 32, nsmem, st>>>(

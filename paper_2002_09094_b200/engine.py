@@ -146,7 +146,7 @@ class DeviceMeans:
 def update_launches(k: int, dim: int) -> int:
     """Kernels one update launches: keys, CUB onesweep radix sort (histogram,
     exclusive sum, one pass per 8 key bits), head, 3 CUB scans (init + sweep
-    each), segstart, segsum (short + long runs), clseg, group starts, norm,
+    each), segstart, group starts, segsum (short + long runs), clseg, norm,
     fill, retain."""
     bits = max(1, int(np.ceil(np.log2(max(2.0, float(k) * float(dim))))))
     return 18 + (bits + 7) // 8
@@ -154,8 +154,8 @@ def update_launches(k: int, dim: int) -> int:
 def delta_update_launches() -> int:
     """Extra kernels of the label-delta sort (changed, keep flags, 3 CUB
     selects, lengths, scan, keys, the changed entries' radix sort, merge,
-    derived keys, header) in place of keys + the full sort."""
-    return 24
+    header) in place of keys + the full sort."""
+    return 23
 
 
 def update_rows(lib, n_obj, nnz, row_ptr, terms, val64, labels0, sizes, prev: DeviceMeans, k,
