@@ -380,11 +380,12 @@ def ours_arm(args, rank, world):
         evs[i][0].record()
         lab = eng.assign(dm, prev, events=ev[i])
         evs[i][1].record()
-        st = eng.read_stats()
+        eng.stats_async()  # read once the update has synchronised
+        dm = eng.update(lab, dm)
+        st = eng.stats_ready()
         posts.append(st.postings)
         changed.append(st.changed)
         near.append(st.near_ties)
-        dm = eng.update(lab, dm)
         prev = lab
     end.record()
     torch.cuda.synchronize()

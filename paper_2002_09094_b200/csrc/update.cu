@@ -75,6 +75,7 @@ size_t cub_bytes_for(int64_t nnz, int64_t k) {
 struct NormPlan {
   int64_t nleaf = 0, nint = 0, nlevels = 0;
   std::vector<int32_t> buf;
+  int32_t* pinned = nullptr;  // page-locked copy of buf (a truly async upload)
 };
 
 int64_t norm_plan_ints_max(int64_t dim) { return 4 * (dim / 64 + 2) + 130; }
@@ -142,6 +143,11 @@ const NormPlan& norm_plan(int64_t D) {
   P.buf.push_back(run);
   for (size_t q = 0; q < order.size(); ++q) P.buf.push_back(ref(nodes[order[q]].l));
   for (size_t q = 0; q < order.size(); ++q) P.buf.push_back(ref(nodes[order[q]].r));
+  if (cudaMallocHost(reinterpret_cast<void**>(&P.pinned), P.buf.size() * sizeof(int32_t)) ==
+      cudaSuccess)
+    std::copy(P.buf.begin(), P.buf.end(), P.pinned);
+  else
+    P.pinned = nullptr;
   return cache.emplace(D, std::move(P)).first->second;
 }
 
@@ -836,8 +842,8 @@ int update_count_impl(int64_t n_obj, const int64_t* row_ptr, const int32_t* term
                        (size_t)(nleaf + 1) * 4;
   if (nsmem > 200 * 1024) return IVFKM_E_UNSUPPORTED;  // D beyond ~1M terms
   // the plan lives in a process-lifetime cache, so an async copy is safe
-  IVFKM_TRY(cudaMemcpyAsync(w.plan, P.buf.data(), P.buf.size() * sizeof(int32_t),
-                            cudaMemcpyHostToDevice, st));
+  IVFKM_TRY(cudaMemcpyAsync(w.plan, P.pinned ? P.pinned : P.buf.data(),
+                            P.buf.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   if (nnz > 0) {
     const double* sval;
     if (delta) {

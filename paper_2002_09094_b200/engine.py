@@ -159,11 +159,15 @@ def delta_update_launches() -> int:
 
 
 def update_rows(lib, n_obj, nnz, row_ptr, terms, val64, labels0, sizes, prev: DeviceMeans, k,
-                dim, ws, total_host=None, state=None) -> DeviceMeans:
+                dim, ws, total_host=None, state=None, deferred=False) -> DeviceMeans:
     """Bit-exact update (variants.py:254-307) of k means from n_obj device rows
     whose 0-based labels lie in [0, k): ivfkm_update_count (or, with a
     label-delta ``state``, ivfkm_update_count_delta), one 8-byte device->host
-    read of the new size, ivfkm_update_fill.  No BIVF."""
+    read of the new size, ivfkm_update_fill.  No BIVF.
+
+    ``deferred``: skip the size read; the mean arrays get a capacity bound
+    (new nonzeros <= runs <= nnz, plus retained means' previous postings) and
+    ``nnz`` stays -1 until build_bivf, whose plan returns the exact count."""
     dev = row_ptr.device
     new_ptr = torch.empty(k + 1, dtype=torch.int64, device=dev)
     if state is not None:
@@ -177,11 +181,14 @@ def update_rows(lib, n_obj, nnz, row_ptr, terms, val64, labels0, sizes, prev: De
                                     _p(labels0), _p(sizes), _p(prev.ptr), _p(new_ptr), _p(ws),
                                     ws.numel(), _stream())
         _lib.check(rc, "ivfkm_update_count")
-    if total_host is None:
-        total_host = torch.zeros(1, dtype=torch.int64)
-    total_host.copy_(new_ptr[k:], non_blocking=True)
-    torch.cuda.current_stream().synchronize()
-    total = int(total_host[0])
+    if deferred:
+        total = min(nnz + prev.nnz, k * dim)
+    else:
+        if total_host is None:
+            total_host = torch.zeros(1, dtype=torch.int64)
+        total_host.copy_(new_ptr[k:], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        total = int(total_host[0])
     t = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
     v = torch.empty(max(total, 1), dtype=torch.float64, device=dev)
     ret = torch.empty(k, dtype=torch.uint8, device=dev)
@@ -189,7 +196,10 @@ def update_rows(lib, n_obj, nnz, row_ptr, terms, val64, labels0, sizes, prev: De
                                _p(prev.vals), _p(new_ptr), _p(t), _p(v), _p(ret), total, _p(ws),
                                ws.numel(), _stream())
     _lib.check(rc, "ivfkm_update_fill")
-    return DeviceMeans(k, dim, new_ptr, t[:total], v[:total], ret)
+    out = DeviceMeans(k, dim, new_ptr, t[:total], v[:total], ret)
+    if deferred:
+        out.nnz = -1
+    return out
 
 
 class LloydEngine:
@@ -251,6 +261,9 @@ class LloydEngine:
                                       _p(dm.headers), C.c_void_p(totals.ctypes.data),
                                       _p(self.ws_bivf), self.ws_bivf.numel(), _stream())
         _lib.check(rc, "ivfkm_bivf_plan")
+        if dm.nnz < 0:  # deferred update: the plan counted the postings
+            dm.nnz = int(totals[1])
+            dm.terms, dm.vals = dm.terms[:dm.nnz], dm.vals[:dm.nnz]
         bits = self.screen_bits
         dm.pvs = torch.empty(max(int(totals[0]), 1),
                              dtype=torch.float16 if bits == 16 else torch.float32, device=dev)
@@ -321,8 +334,16 @@ class LloydEngine:
         self.launches += 2
 
     def read_stats(self) -> IterStats:
-        self.stats_host.copy_(self.stats, non_blocking=True)
+        self.stats_async()
         torch.cuda.current_stream().synchronize()
+        return self.stats_ready()
+
+    def stats_async(self) -> None:
+        """Queue the statistics' device->host copy (read with stats_ready after
+        any later synchronisation, e.g. the one inside update)."""
+        self.stats_host.copy_(self.stats, non_blocking=True)
+
+    def stats_ready(self) -> IterStats:
         raw = _lib.Stats.from_buffer_copy(self.stats_host.numpy().tobytes())
         return IterStats.from_raw(raw)
 
@@ -332,7 +353,7 @@ class LloydEngine:
         dd = self.dd
         out = update_rows(self.lib, dd.n, dd.nnz, dd.row_ptr, dd.terms, dd.val64, labels0,
                           self.sizes, dm, self.k, dd.dim, self.ws_update, self.total_host,
-                          self.upd_state)
+                          self.upd_state, deferred=True)
         self.launches += update_launches(self.k, dd.dim)
         if self.upd_state is not None:
             # minus keys + the full sort (histogram, exclusive sum, passes)
@@ -492,11 +513,12 @@ class StreamIteration:
             self.dm = self.eng.upload_means(self.means0)
         self.eng.dd = dd
         lab = self.eng.assign(self.dm, self.prev)
-        st = self.eng.read_stats()  # objective, changed, counters: the step's result
+        self.eng.stats_async()  # objective, changed, counters: the step's result
         self.labels_host.copy_(lab, non_blocking=True)
         self.dm = self.eng.update(lab, self.dm)
         self.prev = lab
         torch.cuda.current_stream().synchronize()
+        st = self.eng.stats_ready()
         self.last_h2d = self.hd.nbytes
         self.last_d2h = self.labels_host.numel() * 4 + C.sizeof(_lib.Stats)
         return self.labels_host.numpy() + 1, st
