@@ -73,6 +73,8 @@ int ivfkm_device_count(void);
  *   total                at headers[2*dim*nblk]: padded value count in use
  *   nc[t]                at headers[2*dim*nblk + 1 + t]: postings of term t
  *   perm[k], inv[k]      (int32) after nc: mean -> slot, slot -> mean
+ *   dpre[dim], off64[nh+1], then (8-byte aligned) {mask, off64} pairs for the
+ *                        exact rescoring (csrc/bivf.cuh has the full layout)
  * Values (val32 for the fp32 screen, val64 for the exact fp64 rescoring) are
  * term-major, slot ascending — the order of MeanSet.inverted
  * (means.py:169-179) — except that each 256-slot span is padded to a multiple

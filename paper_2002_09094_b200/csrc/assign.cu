@@ -1047,7 +1047,7 @@ BivfView exact_view(const uint32_t* headers, int64_t k, int64_t dim) {
   const int64_t nb = ivfkm_bivf_nblk(k);
   const int64_t nh = dim * nb;
   const uint32_t* nc = headers + 2 * nh + 1;
-  return BivfView{nb, headers, nc + dim + 2 * k + dim,
+  return BivfView{nb, reinterpret_cast<const uint2*>(headers + bivf_mo_word(k, dim, nb)),
                   reinterpret_cast<const int32_t*>(nc + dim)};
 }
 
@@ -1076,26 +1076,22 @@ __device__ double exact_score_warp(const ExactCtx& x, int64_t rb, int64_t re, in
   const uint32_t bit = 1u << (slot & 31);
   for (int64_t h0 = rb; h0 < re; h0 += 32 * kExactU) {
     int32_t t[kExactU];
-    uint32_t m[kExactU];
-    int64_t o[kExactU];
+    uint2 m[kExactU];
 #pragma unroll
     for (int u = 0; u < kExactU; ++u) {
       const int64_t h = h0 + 32 * u + lane;
       t[u] = h < re ? __ldg(x.terms + h) : -1;
     }
 #pragma unroll
-    for (int u = 0; u < kExactU; ++u) {
-      const int64_t q = (int64_t)t[u] * x.bv.nblk + sb;
-      m[u] = t[u] >= 0 ? __ldg(x.bv.masks + q) : 0u;
-      o[u] = t[u] >= 0 ? (int64_t)__ldg(x.bv.off64 + q) : 0;
-    }
+    for (int u = 0; u < kExactU; ++u)
+      m[u] = t[u] >= 0 ? __ldg(x.bv.mo + (int64_t)t[u] * x.bv.nblk + sb) : make_uint2(0u, 0u);
 #pragma unroll
     for (int u = 0; u < kExactU; ++u) {
       const int64_t h = h0 + 32 * u + lane;
       scratch[32 * u + lane] =
-          (m[u] & bit) ? __dmul_rn(__ldg(x.val64 + h),
-                                   __ldg(x.pv64 + o[u] + __popc(m[u] & (bit - 1u))))
-                       : 0.0;
+          (m[u].x & bit) ? __dmul_rn(__ldg(x.val64 + h),
+                                     __ldg(x.pv64 + m[u].y + __popc(m[u].x & (bit - 1u))))
+                         : 0.0;
     }
     __syncwarp();
     if (lane == 0) {

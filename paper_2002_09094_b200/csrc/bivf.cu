@@ -383,7 +383,7 @@ extern "C" void ivfkm_set_bivf_options(float dense_fill, int permute) {
 
 extern "C" int64_t ivfkm_bivf_headers_size(int64_t k, int64_t dim) {
   const int64_t nh = bivf_nh(dim, ivfkm_bivf_nblk(k));
-  return 2 * nh + 1 + dim + 2 * k + dim + nh + 1;
+  return bivf_mo_word(k, dim, ivfkm_bivf_nblk(k)) + 2 * nh;
 }
 
 extern "C" int64_t ivfkm_bivf_values_capacity(int64_t k, int64_t dim, int64_t nnz) {
@@ -445,7 +445,15 @@ int plan_count(int64_t k, int64_t dim, const uint32_t* headers, unsigned th, con
   return IVFKM_OK;
 }
 
-// Headers, part 2: offsets (total at offs[nh]), nc, dense prefixes.
+__global__ void bivf_mo_kernel(int64_t nh, const uint32_t* __restrict__ masks,
+                               const uint32_t* __restrict__ off64, uint2* __restrict__ mo) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nh;
+       i += (int64_t)gridDim.x * blockDim.x)
+    mo[i] = make_uint2(masks[i], off64[i]);
+}
+
+// Headers, part 2: offsets (total at offs[nh]), nc, dense prefixes, the
+// exact lookup's {mask, off64} pairs.
 int plan_layout(int64_t k, int64_t dim, uint32_t* headers, unsigned th, const BivfWs& w,
                 cudaStream_t st) {
   const int64_t nblk = ivfkm_bivf_nblk(k);
@@ -463,6 +471,9 @@ int plan_layout(int64_t k, int64_t dim, uint32_t* headers, unsigned th, const Bi
   IVFKM_CHECK_LAUNCH();
   bivf_nc_kernel<<<grid_for(dim, threads / 32), threads, 0, st>>>(dim, nblk, headers,
                                                                  headers + nh, nc, dpre);
+  IVFKM_CHECK_LAUNCH();
+  bivf_mo_kernel<<<grid_for(nh, threads), threads, 0, st>>>(
+      nh, headers, off64, reinterpret_cast<uint2*>(headers + bivf_mo_word(k, dim, nblk)));
   IVFKM_CHECK_LAUNCH();
   return IVFKM_OK;
 }

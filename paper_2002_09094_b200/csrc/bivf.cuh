@@ -20,6 +20,8 @@
 //   off64[t*nblk + b]        start of block b in the compact exact-value (fp64)
 //                            array: postings only, term-major, slot ascending;
 //   off64[dim*nblk]          their number
+//   mo   [t*nblk + b]        (uint2, at the next even word) {mask, off64}: the
+//                            exact lookup's two words in one 8-byte gather
 // Screen values: blocks are grouped in spans of 8 (256 slots); every span's
 // value segment is padded to a multiple of 8 values, so a span start is 16-B
 // aligned in both the fp32 and the fp16 screen arrays.
@@ -47,20 +49,25 @@ constexpr int kSpan = 8;
 // means.py:169-179), so block b of term t starts at off64[t*nblk + b].
 struct BivfView {
   int64_t nblk;
-  const uint32_t* masks;
-  const uint32_t* off64;
+  const uint2* mo;      // {mask, off64} per block
   const int32_t* perm;  // mean -> slot (nullptr: identity)
 };
 
 __host__ __device__ inline int64_t bivf_nh(int64_t dim, int64_t nblk) { return dim * nblk; }
 
+// Word offset of the mo array in the headers (8-byte aligned).
+__host__ __device__ inline int64_t bivf_mo_word(int64_t k, int64_t dim, int64_t nblk) {
+  const int64_t nh = bivf_nh(dim, nblk);
+  const int64_t w = 2 * nh + 1 + dim + 2 * k + dim + nh + 1;
+  return (w + 1) & ~(int64_t)1;
+}
+
 // Position of slot s's exact value for term t, or -1 when the slot lacks it.
 __device__ __forceinline__ int64_t bivf_find_slot(const BivfView& v, int64_t t, int64_t s) {
-  const int64_t b = s >> 5;
   const uint32_t bit = 1u << (s & 31);
-  const uint32_t m = __ldg(v.masks + t * v.nblk + b);
-  if (!(m & bit)) return -1;
-  return (int64_t)__ldg(v.off64 + t * v.nblk + b) + __popc(m & (bit - 1u));
+  const uint2 m = __ldg(v.mo + t * v.nblk + (s >> 5));
+  if (!(m.x & bit)) return -1;
+  return (int64_t)m.y + __popc(m.x & (bit - 1u));
 }
 
 // Position of mean c's exact value for term t, or -1.
