@@ -211,11 +211,11 @@ __device__ __forceinline__ int gather_values16(const MaskPack<RR>& mk, uint32_t 
 }
 
 // The screen's in-flight values of one (entry, span): fp32 values, or fp16 bits.
-template <int RR, bool HALF>
+template <int RR, bool HALF, bool F2 = false>
 struct SpanVals;
 
 template <int RR>
-struct SpanVals<RR, false> {
+struct SpanVals<RR, false, false> {
   float u[RR];
   bool has;
   __device__ __forceinline__ void gather(const MaskPack<RR>& mk, uint32_t o, uint32_t gb,
@@ -264,8 +264,10 @@ struct SpanVals<RR, false> {
   }
 };
 
-template <int RR>
-struct SpanVals<RR, true> {
+// F2: packed FFMA2 (faster in the 56-register small-CTA screen; the
+// 64-register instantiations lose more to register pairing than they gain)
+template <int RR, bool F2>
+struct SpanVals<RR, true, F2> {
   uint32_t w[RR];
   int code;
   __device__ __forceinline__ void gather(const MaskPack<RR>& mk, uint32_t o, uint32_t gb,
@@ -294,18 +296,41 @@ struct SpanVals<RR, true> {
   __device__ __forceinline__ void fma(const int* vbits, float (&acc)[RR]) const {
     if (code != 0) fma(__int_as_float(*vbits), acc);
   }
+  // packed fp32 FMA (FFMA2): two slots per instruction, each lane of the pair
+  // rounded exactly as fmaf
+  static __device__ __forceinline__ void fma2(float v, float a, float b, float& x, float& y) {
+    unsigned long long ab, xy;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(ab) : "f"(a), "f"(b));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(xy) : "f"(x), "f"(y));
+    unsigned long long vv;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(vv) : "f"(v));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(xy) : "l"(vv), "l"(ab));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(xy));
+  }
   __device__ __forceinline__ void fma(float v, float (&acc)[RR]) const {
     if (code == 2) {
 #pragma unroll
       for (int q = 0; q < RR / 2; ++q) {
         const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[q]));
-        acc[2 * q] = fmaf(v, f.x, acc[2 * q]);
-        acc[2 * q + 1] = fmaf(v, f.y, acc[2 * q + 1]);
+        if constexpr (F2) {
+          fma2(v, f.x, f.y, acc[2 * q], acc[2 * q + 1]);
+        } else {
+          acc[2 * q] = fmaf(v, f.x, acc[2 * q]);
+          acc[2 * q + 1] = fmaf(v, f.y, acc[2 * q + 1]);
+        }
       }
     } else if (code == 1) {
+      if constexpr (F2) {
 #pragma unroll
-      for (int r = 0; r < RR; ++r)
-        acc[r] = fmaf(v, __half2float(__ushort_as_half((unsigned short)w[r])), acc[r]);
+        for (int q = 0; q < RR / 2; ++q)
+          fma2(v, __half2float(__ushort_as_half((unsigned short)w[2 * q])),
+               __half2float(__ushort_as_half((unsigned short)w[2 * q + 1])), acc[2 * q],
+               acc[2 * q + 1]);
+      } else {
+#pragma unroll
+        for (int r = 0; r < RR; ++r)
+          acc[r] = fmaf(v, __half2float(__ushort_as_half((unsigned short)w[r])), acc[r]);
+      }
     }
   }
 };
@@ -580,7 +605,7 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
         {
           // dense-prefix entries: span gb>>3 starts 256*(gb>>3) values into the
           // term's run; kDepth entries' values in flight, then their FMAs
-          using SV = SpanVals<RR, HALF>;
+          using SV = SpanVals<RR, HALF, HALF && MAXREG == 56>;
           const uint32_t r0 = gb32 & (kSpan - 1);
           const char* pl =
               static_cast<const char*>(pv) + SV::lane_bytes(32u * (gb32 - r0), r0, lane);
@@ -621,7 +646,7 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
           MaskPack<RR> mk;
           uint32_t o;
           ld(nd, mk, o);
-          SpanVals<RR, HALF> A, B;
+          SpanVals<RR, HALF, HALF && MAXREG == 56> A, B;
           A.gather(mk, o, gb32, pv, lane, lanebit, lt);
           ld(nd + 1, mk, o);
           for (int e = nd; e < cn; e += 2) {
