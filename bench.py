@@ -352,7 +352,7 @@ def ours_arm(args, rank, world):
     t_gen = time.perf_counter() - t_gen
     k = c["k"]
     means0 = init_means(ds, k, c["seed"], representation="sparse_inverted")
-    hd = HostDataset(ds, pin=True)
+    hd = HostDataset(ds, pin=True, compact=True)  # 16-bit term gaps over PCIe
     dd = DeviceDataset(hd, dev)
     eng = LloydEngine(dd, k)
     dm = eng.upload_means(means0)

