@@ -75,7 +75,6 @@ size_t cub_bytes_for(int64_t nnz, int64_t k) {
 struct NormPlan {
   int64_t nleaf = 0, nint = 0, nlevels = 0;
   std::vector<int32_t> buf;
-  int32_t* pinned = nullptr;  // page-locked copy of buf (a truly async upload)
 };
 
 int64_t norm_plan_ints_max(int64_t dim) { return 4 * (dim / 64 + 2) + 130; }
@@ -143,11 +142,6 @@ const NormPlan& norm_plan(int64_t D) {
   P.buf.push_back(run);
   for (size_t q = 0; q < order.size(); ++q) P.buf.push_back(ref(nodes[order[q]].l));
   for (size_t q = 0; q < order.size(); ++q) P.buf.push_back(ref(nodes[order[q]].r));
-  if (cudaMallocHost(reinterpret_cast<void**>(&P.pinned), P.buf.size() * sizeof(int32_t)) ==
-      cudaSuccess)
-    std::copy(P.buf.begin(), P.buf.end(), P.pinned);
-  else
-    P.pinned = nullptr;
   return cache.emplace(D, std::move(P)).first->second;
 }
 
@@ -578,13 +572,14 @@ struct DeltaState {
   int32_t* clist;                // n_obj: changed objects
   int64_t* cptr;                 // n_obj+1: their entry offsets in B
   unsigned long long* counts;    // [0] changed objects, [1] their entries, [2] selected
+  int32_t* plan;                 // the norm's tree plan, uploaded once (hdr.pad = its dim)
   void* cub;
   size_t cub_bytes;
 };
 
 int64_t delta_cap(int64_t nnz) { return nnz / 4 + 1024; }
 
-DeltaState carve_delta(void* base, int64_t n_obj, int64_t nnz, size_t* total) {
+DeltaState carve_delta(void* base, int64_t n_obj, int64_t nnz, int64_t dim, size_t* total) {
   Carver c(base);
   DeltaState d;
   const size_t n = (size_t)(nnz > 0 ? nnz : 1), no = (size_t)(n_obj > 0 ? n_obj : 1);
@@ -602,6 +597,7 @@ DeltaState carve_delta(void* base, int64_t n_obj, int64_t nnz, size_t* total) {
   d.clist = c.take<int32_t>(no);
   d.cptr = c.take<int64_t>(no + 1);
   d.counts = c.take<unsigned long long>(4);
+  d.plan = c.take<int32_t>((size_t)norm_plan_ints_max(dim));
   size_t a = 0, b = 0, m = 0, sc = 0, so = 0;
   cub::DoubleBuffer<unsigned long long> kb(nullptr, nullptr);
   cub::DoubleBuffer<double> vb(nullptr, nullptr);
@@ -725,7 +721,7 @@ __global__ void set_hdr_kernel(DeltaHdr* hdr, DeltaHdr v) { *hdr = v; }
 int delta_sort(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms, const double* val64,
                int64_t nnz, int64_t k, int64_t dim, const int32_t* labels, DeltaState& d,
                const unsigned long long** sk, const double** sv, int64_t* moved,
-               cudaStream_t st) {
+               bool* plan_ok, cudaStream_t st) {
   const Bits bt = comp_bits(n_obj, dim, k);
   const int total_bits = bt.ob + bt.tb + bt.lb;
   const int T = 256;
@@ -743,6 +739,7 @@ int delta_sort(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms, cons
   bool full = !(h.magic == kDeltaMagic && h.valid == 1 && h.n_obj == n_obj && h.nnz == nnz &&
                 h.k == k && h.dim == dim && (h.cur == 0 || h.cur == 1));
   int cur = full ? 0 : (int)h.cur;
+  *plan_ok = !full && h.pad == dim;  // same layout, plan already uploaded
   if (!full && (int64_t)cnt[1] > delta_cap(nnz) - 1024) full = true;
   if (full) {
     comp_keys_kernel<<<grid_for(n_obj, T / 32), T, 0, st>>>(n_obj, row_ptr, terms, val64, labels,
@@ -801,7 +798,7 @@ int delta_sort(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms, cons
   // remember the labels S now holds
   IVFKM_TRY(cudaMemcpyAsync(d.labels, labels, sizeof(int32_t) * n_obj, cudaMemcpyDeviceToDevice,
                             st));
-  set_hdr_kernel<<<1, 1, 0, st>>>(d.hdr, DeltaHdr{kDeltaMagic, n_obj, nnz, k, dim, 1, cur, 0});
+  set_hdr_kernel<<<1, 1, 0, st>>>(d.hdr, DeltaHdr{kDeltaMagic, n_obj, nnz, k, dim, 1, cur, dim});
   IVFKM_CHECK_LAUNCH();
   *sk = d.key[cur];
   *sv = d.val[cur];
@@ -810,7 +807,8 @@ int delta_sort(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms, cons
 
 // Run heads, their scan and the run starts / keys / leaf-group starts.
 template <class K, class R>
-int runs_impl(int64_t nnz, R rd, const UpdWs<K>& w, int64_t dim, int64_t nleaf, cudaStream_t st) {
+int runs_impl(int64_t nnz, R rd, const UpdWs<K>& w, int64_t dim, int64_t nleaf,
+              const int32_t* plan, cudaStream_t st) {
   const int T = 256;
   head_kernel<K, R><<<grid_for(nnz, T), T, 0, st>>>(nnz, rd, w.head);
   IVFKM_CHECK_LAUNCH();
@@ -821,7 +819,7 @@ int runs_impl(int64_t nnz, R rd, const UpdWs<K>& w, int64_t dim, int64_t nleaf, 
   IVFKM_CHECK_LAUNCH();
   const int ng = (int)((nleaf + kLeafG - 1) / kLeafG);
   gstart_kernel<K><<<grid_for(nnz / 4 + 1, T), T, (size_t)(ng + (dim >> 8) + 1) * 4, st>>>(
-      w.n_seg, w.seg_key, dim, w.plan, nleaf, w.gstart);
+      w.n_seg, w.seg_key, dim, plan, nleaf, w.gstart);
   IVFKM_CHECK_LAUNCH();
   return IVFKM_OK;
 }
@@ -841,18 +839,28 @@ int update_count_impl(int64_t n_obj, const int64_t* row_ptr, const int32_t* term
   const size_t nsmem = (size_t)kNormWarps * kLeafG * 128 * 8 + (size_t)(nleaf + nint) * 8 +
                        (size_t)(nleaf + 1) * 4;
   if (nsmem > 200 * 1024) return IVFKM_E_UNSUPPORTED;  // D beyond ~1M terms
-  // the plan lives in a process-lifetime cache, so an async copy is safe
-  IVFKM_TRY(cudaMemcpyAsync(w.plan, P.pinned ? P.pinned : P.buf.data(),
-                            P.buf.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  // The plan lives in a process-lifetime cache.  It is uploaded from pageable
+  // memory (a small copy the driver stages itself; a page-locked async copy
+  // would queue behind a concurrent bulk upload on the copy engine), and
+  // kept in the label-delta state across calls when there is one.
+  const size_t plan_bytes = P.buf.size() * sizeof(int32_t);
+  const int32_t* plan = w.plan;
+  if (!(delta && nnz > 0))
+    IVFKM_TRY(cudaMemcpyAsync(w.plan, P.buf.data(), plan_bytes, cudaMemcpyHostToDevice, st));
   if (nnz > 0) {
     const double* sval;
     if (delta) {
       const unsigned long long* ck;
       int64_t moved = 0;
+      bool plan_ok = false;
       IVFKM_TRY_RC(delta_sort(n_obj, row_ptr, terms, val64, nnz, k, dim, labels, *delta, &ck,
-                              &sval, &moved, st));
+                              &sval, &moved, &plan_ok, st));
+      plan = delta->plan;
+      if (!plan_ok)
+        IVFKM_TRY(cudaMemcpyAsync(delta->plan, P.buf.data(), plan_bytes, cudaMemcpyHostToDevice,
+                                  st));
       IVFKM_TRY_RC(runs_impl<K>(nnz, CompKey<K>{ck, comp_bits(n_obj, dim, k), dim}, w, dim,
-                                nleaf, st));
+                                nleaf, plan, st));
     } else {
       keys_kernel<K><<<grid_for(n_obj, T / 32), T, 0, st>>>(n_obj, row_ptr, terms, val64, labels,
                                                             dim, w.key_a, w.val_a);
@@ -863,7 +871,7 @@ int update_count_impl(int64_t n_obj, const int64_t* row_ptr, const int32_t* term
       IVFKM_TRY(cub::DeviceRadixSort::SortPairs(w.cub, cb, kb, vb, (int)nnz, 0, key_bits(k, dim),
                                                 st));
       sval = vb.Current();
-      IVFKM_TRY_RC(runs_impl<K>(nnz, ArrKey<K>{kb.Current()}, w, dim, nleaf, st));
+      IVFKM_TRY_RC(runs_impl<K>(nnz, ArrKey<K>{kb.Current()}, w, dim, nleaf, plan, st));
     }
     // the run count sizes the rest of the update (one 4-byte read-back)
     uint32_t n_seg = 0;
@@ -887,7 +895,7 @@ int update_count_impl(int64_t n_obj, const int64_t* row_ptr, const int32_t* term
   IVFKM_TRY(cudaFuncSetAttribute(norm_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)nsmem));
   norm_kernel<K><<<(int)std::min<int64_t>(k, kNumSM * 4), kNormWarps * 32, nsmem, st>>>(
-      k, dim, nleaf, nint, P.nlevels, w.plan, sizes, prev_ptr, w.cl_seg, w.gstart, w.seg_key,
+      k, dim, nleaf, nint, P.nlevels, plan, sizes, prev_ptr, w.cl_seg, w.gstart, w.seg_key,
       w.seg_w, w.nzpos, w.nrm, w.counts);
   IVFKM_CHECK_LAUNCH();
   size_t cb = w.cub_bytes;
@@ -950,7 +958,7 @@ extern "C" size_t ivfkm_update_state_size(int64_t n_obj, int64_t nnz, int64_t k,
   const Bits bt = comp_bits(n_obj, dim, k);
   if (bt.ob + bt.tb + bt.lb > 64) return 0;
   size_t total = 0;
-  carve_delta(nullptr, n_obj, nnz, &total);
+  carve_delta(nullptr, n_obj, nnz, dim, &total);
   return total;
 }
 
@@ -966,7 +974,7 @@ extern "C" int ivfkm_update_count_delta(int64_t n_obj, int64_t nnz, const int64_
   const size_t need = ivfkm_update_state_size(n_obj, nnz, k, dim);
   if (need == 0) return IVFKM_E_UNSUPPORTED;
   if (state_bytes < need) return IVFKM_E_WORKSPACE;
-  DeltaState d = carve_delta(state, n_obj, nnz, nullptr);
+  DeltaState d = carve_delta(state, n_obj, nnz, dim, nullptr);
   cudaStream_t st = as_stream(stream_);
   if (use_k32(k, dim))
     return update_count_impl<uint32_t>(n_obj, row_ptr, terms, val64, nnz, k, dim, labels, sizes,
