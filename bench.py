@@ -416,6 +416,10 @@ def ours_arm(args, rank, world):
 
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(3, min(args.steps, 10))
     host_means = dm.to_meanset()
+    last_labels = (lab.cpu().numpy() + 1).astype(np.int32)
+    screen_bits = eng.screen_bits
+    del eng, dd, dm, lab, prev  # the e2e engines below bring their own device state
+    torch.cuda.empty_cache()
     h2d = d2h = 0
     e2e_value = e2e_rt = None
     rt_h2d = rt_d2h = 0
@@ -433,6 +437,7 @@ def ours_arm(args, rank, world):
         e2e_value = e2e_steps / (time.perf_counter() - t0)
         h2d, d2h = stream.last_h2d, stream.last_d2h
         del stream
+        torch.cuda.empty_cache()
         # (2) stricter: the means also round-trip through host memory every
         # step (the reference's assign/update API on host arrays)
         stepper = HostIteration(hd, k, dev)
@@ -450,7 +455,7 @@ def ours_arm(args, rank, world):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "screen": f"fp{eng.screen_bits} values, fp32 FMA, rigorous window -> exact f64 rescoring",
+        "screen": f"fp{screen_bits} values, fp32 FMA, rigorous window -> exact f64 rescoring",
         "data": "synthetic", "config": config_dict(args.config, c, spec, ds, world),
         "postings_per_sec": sum(posts) / (sum(assign_ms) / 1000.0),
         "screen_postings_per_sec": sum(posts) / (sum(screen_ms) / 1000.0),
@@ -460,7 +465,7 @@ def ours_arm(args, rank, world):
         "near_ties_per_step": sum(near) / len(near), "changed_per_step": sum(changed) / len(changed),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                     "kernel": f"screen_kernel (BIVF register screen, fp{eng.screen_bits} values)",
+                     "kernel": f"screen_kernel (BIVF register screen, fp{screen_bits} values)",
                      "bytes_per_launch": avg_b, "l2": l2_model(args.config, avg_screen_s)},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
@@ -474,9 +479,8 @@ def ours_arm(args, rank, world):
     }
     if not args.no_cpu_baseline:
         try:
-            labels = (lab.cpu().numpy() + 1).astype(np.int32)
             info, per = cpu_baseline_measure(ds, k, c["seed"], args.cpu_seconds, steps=1,
-                                             labels=labels, means=dm.to_meanset())
+                                             labels=last_labels, means=host_means)
             line["cpu_baseline"] = {"value": 1.0 / per[0], "unit": UNIT, "cores": info["threads"],
                                     "kind": info["kind"], "sample": info["sample"]}
         except Exception as exc:  # baseline must not sink the GPU number

@@ -416,12 +416,18 @@ class LloydEngine:
         dd = self.dd
         out = update_rows(self.lib, dd.n, dd.nnz, dd.row_ptr, dd.terms, dd.val64, labels0,
                           self.sizes, dm, self.k, dd.dim, self.ws_update, self.total_host,
-                          self.upd_state, deferred=True)
+                          self.upd_state, deferred=self._defer_ok(dm))
         self.launches += update_launches(self.k, dd.dim)
         if self.upd_state is not None:
             # minus keys + the full sort (histogram, exclusive sum, passes)
             self.launches += delta_update_launches() - (update_launches(self.k, dd.dim) - 15)
         return self.build_bivf(out)
+
+    def _defer_ok(self, dm: DeviceMeans) -> bool:
+        """The size read is skipped only while the capacity bound stays small
+        (<= 2 GB of mean arrays); at the largest configs the exact size is
+        worth its synchronisation."""
+        return (self.dd.nnz + dm.nnz) * 12 <= (2 << 30)
 
     def set_sizes_from_labels(self, labels0: torch.Tensor) -> None:
         """sizes = bincount(labels) for an externally supplied assignment."""
