@@ -532,7 +532,13 @@ int sorted_fill(int64_t k, int64_t dim, int major, int64_t nrows, const int64_t*
   cub::DoubleBuffer<K> kb(w.key_a, w.key_b);
   cub::DoubleBuffer<double> vb(w.val_a, w.val_b);
   size_t cb = w.cub_bytes;
-  IVFKM_TRY(cub::DeviceRadixSort::SortPairs(w.cub, cb, kb, vb, (int)nnz, 0, bits, st));
+  // The write is a scatter by computed position, so it needs locality, not
+  // order: sorting by the key's top 16 bits (a few terms per bucket) keeps
+  // its stores and header reads inside L2-resident windows — 2 radix passes
+  // instead of 4 (measured +0.8% per iteration at config 1 against the full
+  // sort; 1 pass of 8 bits gains less).
+  const int begin = bits > 16 ? bits - 16 : 0;
+  IVFKM_TRY(cub::DeviceRadixSort::SortPairs(w.cub, cb, kb, vb, (int)nnz, begin, bits, st));
   bivf_write_kernel<K><<<grid_for(nnz, threads), threads, 0, st>>>(
       nnz, dim, nblk, nslot, kb.Current(), vb.Current(), headers, off64, val32, val64, half);
   IVFKM_CHECK_LAUNCH();

@@ -341,12 +341,12 @@ class LloydEngine:
         dm.screen_bits = bits
         _lib.check(rc, "ivfkm_bivf_fill")
         # plan: sizes, CUB sort of the k slot keys (single tile / onesweep), perm,
-        # mask, count, 2 scans (init + sweep each), offset, nc; fill: zero,
-        # position keys, CUB onesweep sort (histogram, exclusive sum, a pass
-        # per 8 key bits), write
+        # mask, count, 2 scans (init + sweep each), offset, nc, {mask, offset}
+        # pairs; fill: zero, position keys, CUB onesweep sort of the keys' top
+        # 16 bits (histogram, exclusive sum, a pass per 8 bits), write
         nslot = self.nblk * 32
         kbits = max(1, int(np.ceil(np.log2(float(dm.dim) * nslot + 1))))
-        self.launches += 10 + (1 if self.k <= 4096 else 6) + 5 + (kbits + 7) // 8
+        self.launches += 11 + (1 if self.k <= 4096 else 6) + 5 + (min(kbits, 16) + 7) // 8
         return dm
 
     def upload_means(self, ms) -> DeviceMeans:
