@@ -299,3 +299,28 @@ def test_row_gap_encoding_round_trips():
             cur = exc[h] if gaps[h] == 0xFFFF else cur + int(gaps[h])
             out[h] = cur
     assert np.array_equal(out, terms0)
+
+
+def test_l2_model_closed_forms():
+    """l2model (reference cache.py restated for the B200 L2): the window at
+    z=1 is one scan, the window is monotone in z, z* is the last fitting
+    window, everything fitting leaves the compulsory misses only, and a
+    smaller cache misses more."""
+    import math
+
+    from paper_2002_09094_b200 import l2model as L
+
+    rng = np.random.default_rng(5)
+    no = rng.integers(0, 500, 300)
+    blocks = rng.integers(1, 40, 300).astype(float)
+    p = L.FreqProfile(no, blocks, 500)
+    assert L.expected_blocks_ivf_window(p, 1) == L.expected_blocks_ivf(p)
+    w = [L.expected_blocks_ivf_window(p, z) for z in (1, 2, 4, 8, 16)]
+    assert all(a <= b for a, b in zip(w, w[1:]))
+    c = L.CacheParams(cache_bytes=int(w[2] * 32 / 0.75) + 64, block_bytes=32, usable=0.75)
+    z = L.find_z_star(p, c)
+    assert L.expected_blocks_ivf_window(p, z) <= c.nb_llc < L.expected_blocks_ivf_window(p, z + 1)
+    big = L.CacheParams(cache_bytes=10**9)
+    assert math.isinf(L.find_z_star(p, big))
+    assert L.llcm_ivf(p, big) == blocks[no > 0].sum()
+    assert L.llcm_ivf(p, c) > L.llcm_ivf(p, big)
