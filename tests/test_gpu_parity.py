@@ -499,15 +499,17 @@ def test_dist_driver_single_rank_matches_engine():
         prev = lab
 
 
-def test_host_iteration_end_to_end_matches_oracle():
+@pytest.mark.parametrize("compact", [False, True])
+def test_host_iteration_end_to_end_matches_oracle(compact):
     """The e2e path (corpus + means uploaded from pinned host memory each step,
-    labels + means read back) equals the oracle's iteration bit for bit."""
+    labels + means read back; with compact, the term ids travel as 16-bit
+    gaps) equals the oracle's iteration bit for bit."""
     from oracle import oracle as O
     from paper_2002_09094_b200.engine import HostDataset, HostIteration
 
     P = _pkg()
     ds, om, means = _random_case(n=1800, dim=900, seed=14, k=60)
-    it = HostIteration(HostDataset(ds, pin=True), 60, "cuda")
+    it = HostIteration(HostDataset(ds, pin=True, compact=compact), 60, "cuda")
     m = om
     for _ in range(3):
         labels, means, st = it.step(means)
@@ -518,6 +520,26 @@ def test_host_iteration_end_to_end_matches_oracle():
         assert np.array_equal(means.values, m.values) and np.array_equal(means.term_ids, m.term_ids)
         P.MeanSet(means.k, means.dim, means.representation, means.indptr, means.term_ids,
                   means.values, means.retained)  # the trusted wrap passes full validation
+
+
+@pytest.mark.parametrize("compact", [False, True])
+def test_stream_iteration_matches_oracle(compact):
+    """bench.py's e2e leg (engine.StreamIteration: the corpus re-uploaded
+    every step on a copy stream, the next step's upload in flight, labels and
+    statistics read back, means on the device) follows the oracle's run."""
+    from oracle import oracle as O
+    from paper_2002_09094_b200.engine import HostDataset, StreamIteration
+
+    ds, om, means = _random_case(n=1800, dim=900, seed=15, k=50)
+    it = StreamIteration(HostDataset(ds, pin=True, compact=compact), 50, means, "cuda")
+    m = om
+    for _ in range(4):
+        labels, st = it.step()
+        ol, _, _, post = O.assign(ds, m)
+        assert np.array_equal(labels, ol) and st.postings == post
+        assert st.objective == O.objective(ds, ol, m)
+        m = O.update(ds, ol, m)
+    assert it.last_h2d == it.hd.nbytes
 
 
 @pytest.mark.parametrize("bits", [16, 32])
