@@ -19,6 +19,10 @@
 // scans give the new CSR offsets; the fill pass writes terms and values.
 #include <cub/cub.cuh>
 #include <cub/device/device_merge.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
+
+#include <iterator>
 
 #include <algorithm>
 #include <map>
@@ -805,18 +809,86 @@ int delta_sort(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms, cons
   return IVFKM_OK;
 }
 
+// Fused run detection: one CUB exclusive scan whose input is the head flag
+// computed from the sorted keys on the fly and whose output, instead of
+// being stored, writes the run start and key at every head (and the run
+// count at the last entry) — no flag array, no position array, no extra pass.
+template <class R>
+struct HeadFlag {
+  R key;
+  __device__ __forceinline__ uint32_t operator()(int64_t e) const {
+    return (e == 0 || key(e) != key(e - 1)) ? 1u : 0u;
+  }
+};
+
+template <class K, class R>
+struct RunStartOut {
+  R key;
+  uint32_t* seg_start;
+  K* seg_key;
+  uint32_t* n_seg;
+  int64_t nnz;
+  int64_t base = 0;
+  struct Ref {
+    R key;
+    uint32_t* seg_start;
+    K* seg_key;
+    uint32_t* n_seg;
+    int64_t nnz, e;
+    __device__ __forceinline__ void operator=(uint32_t pos) const {
+      const K k = key(e);
+      const bool head = e == 0 || k != key(e - 1);
+      if (head) {
+        seg_start[pos] = (uint32_t)e;
+        seg_key[pos] = k;
+      }
+      if (e == nnz - 1) {
+        const uint32_t ns = pos + (head ? 1u : 0u);
+        *n_seg = ns;
+        seg_start[ns] = (uint32_t)nnz;
+      }
+    }
+  };
+  using iterator_category = std::random_access_iterator_tag;
+  using value_type = uint32_t;
+  using difference_type = int64_t;
+  using pointer = void;
+  using reference = Ref;
+  __host__ __device__ RunStartOut operator+(int64_t d) const {
+    RunStartOut o = *this;
+    o.base += d;
+    return o;
+  }
+  __device__ __forceinline__ Ref operator[](int64_t i) const {
+    return Ref{key, seg_start, seg_key, n_seg, nnz, base + i};
+  }
+  __device__ __forceinline__ Ref operator*() const { return (*this)[0]; }
+};
+
 // Run heads, their scan and the run starts / keys / leaf-group starts.
 template <class K, class R>
 int runs_impl(int64_t nnz, R rd, const UpdWs<K>& w, int64_t dim, int64_t nleaf,
               const int32_t* plan, cudaStream_t st) {
   const int T = 256;
-  head_kernel<K, R><<<grid_for(nnz, T), T, 0, st>>>(nnz, rd, w.head);
-  IVFKM_CHECK_LAUNCH();
-  size_t cb = w.cub_bytes;
-  IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.head, w.segpos, (int)nnz, st));
-  segstart_kernel<K, R><<<grid_for(nnz, T), T, 0, st>>>(nnz, rd, w.head, w.segpos, w.seg_start,
-                                                         w.seg_key, w.n_seg);
-  IVFKM_CHECK_LAUNCH();
+  {
+    auto in = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0),
+                                              HeadFlag<R>{rd});
+    RunStartOut<K, R> out{rd, w.seg_start, w.seg_key, w.n_seg, nnz, 0};
+    size_t need = 0;
+    IVFKM_TRY(cub::DeviceScan::ExclusiveSum(nullptr, need, in, out, (int)nnz, st));
+    if (need <= w.cub_bytes) {
+      size_t cb = w.cub_bytes;
+      IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, in, out, (int)nnz, st));
+    } else {
+      head_kernel<K, R><<<grid_for(nnz, T), T, 0, st>>>(nnz, rd, w.head);
+      IVFKM_CHECK_LAUNCH();
+      size_t cb = w.cub_bytes;
+      IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.head, w.segpos, (int)nnz, st));
+      segstart_kernel<K, R><<<grid_for(nnz, T), T, 0, st>>>(
+          nnz, rd, w.head, w.segpos, w.seg_start, w.seg_key, w.n_seg);
+      IVFKM_CHECK_LAUNCH();
+    }
+  }
   const int ng = (int)((nleaf + kLeafG - 1) / kLeafG);
   gstart_kernel<K><<<grid_for(nnz / 4 + 1, T), T, (size_t)(ng + (dim >> 8) + 1) * 4, st>>>(
       w.n_seg, w.seg_key, dim, plan, nleaf, w.gstart);

@@ -208,11 +208,11 @@ class DeviceMeans:
 
 def update_launches(k: int, dim: int) -> int:
     """Kernels one update launches: keys, CUB onesweep radix sort (histogram,
-    exclusive sum, one pass per 8 key bits), head, 3 CUB scans (init + sweep
-    each), segstart, group starts, segsum (short + long runs), clseg, norm,
-    fill, retain."""
+    exclusive sum, one pass per 8 key bits), 3 CUB scans (init + sweep each;
+    the first also finds the runs), group starts, segsum (short + long runs),
+    clseg, norm, fill, retain."""
     bits = max(1, int(np.ceil(np.log2(max(2.0, float(k) * float(dim))))))
-    return 18 + (bits + 7) // 8
+    return 16 + (bits + 7) // 8
 
 def delta_update_launches() -> int:
     """Extra kernels of the label-delta sort (changed, keep flags, 3 CUB
@@ -420,7 +420,7 @@ class LloydEngine:
         self.launches += update_launches(self.k, dd.dim)
         if self.upd_state is not None:
             # minus keys + the full sort (histogram, exclusive sum, passes)
-            self.launches += delta_update_launches() - (update_launches(self.k, dd.dim) - 15)
+            self.launches += delta_update_launches() - (update_launches(self.k, dd.dim) - 13)
         return self.build_bivf(out)
 
     def _defer_ok(self, dm: DeviceMeans) -> bool:
