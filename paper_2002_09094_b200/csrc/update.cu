@@ -572,13 +572,21 @@ struct DeltaState {
   unsigned long long* bkey[2];   // changed entries (B), capacity nnz/4
   double* bval[2];
   uint8_t* oflag;                // n_obj: changed
-  uint8_t* eflag;                // nnz: entry kept in A
   int32_t* clist;                // n_obj: changed objects
   int64_t* cptr;                 // n_obj+1: their entry offsets in B
   unsigned long long* counts;    // [0] changed objects, [1] their entries, [2] selected
   int32_t* plan;                 // the norm's tree plan, uploaded once (hdr.pad = its dim)
   void* cub;
   size_t cub_bytes;
+};
+
+struct KeptFlag {
+  const unsigned long long* key;
+  const uint8_t* oflag;
+  unsigned long long omask;
+  __device__ __forceinline__ uint8_t operator()(int64_t e) const {
+    return oflag[key[e] & omask] ? 0 : 1;
+  }
 };
 
 int64_t delta_cap(int64_t nnz) { return nnz / 4 + 1024; }
@@ -597,7 +605,6 @@ DeltaState carve_delta(void* base, int64_t n_obj, int64_t nnz, int64_t dim, size
     d.bval[b] = c.take<double>(nb);
   }
   d.oflag = c.take<uint8_t>(no);
-  d.eflag = c.take<uint8_t>(n);
   d.clist = c.take<int32_t>(no);
   d.cptr = c.take<int64_t>(no + 1);
   d.counts = c.take<unsigned long long>(4);
@@ -606,8 +613,16 @@ DeltaState carve_delta(void* base, int64_t n_obj, int64_t nnz, int64_t dim, size
   cub::DoubleBuffer<unsigned long long> kb(nullptr, nullptr);
   cub::DoubleBuffer<double> vb(nullptr, nullptr);
   cub::DeviceRadixSort::SortPairs(nullptr, a, kb, vb, (int)n, 0, 64);
-  cub::DeviceSelect::Flagged(nullptr, b, (unsigned long long*)nullptr, (uint8_t*)nullptr,
-                             (unsigned long long*)nullptr, (unsigned long long*)nullptr, (int)n);
+  {
+    auto kept = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0),
+                                                KeptFlag{nullptr, nullptr, 0ull});
+    size_t b1 = 0, b2 = 0;
+    cub::DeviceSelect::Flagged(nullptr, b1, (unsigned long long*)nullptr, kept,
+                               (unsigned long long*)nullptr, (unsigned long long*)nullptr, (int)n);
+    cub::DeviceSelect::Flagged(nullptr, b2, (double*)nullptr, kept, (double*)nullptr,
+                               (unsigned long long*)nullptr, (int)n);
+    b = std::max(b1, b2);
+  }
   cub::DeviceMerge::MergePairs(nullptr, m, (unsigned long long*)nullptr, (double*)nullptr, (int)n,
                                (unsigned long long*)nullptr, (double*)nullptr, (int)nb,
                                (unsigned long long*)nullptr, (double*)nullptr);
@@ -697,14 +712,6 @@ __global__ void list_len_kernel(int64_t n_list, const int32_t* __restrict__ objs
     len[q] = row_ptr[objs[q] + 1] - row_ptr[objs[q]];
 }
 
-__global__ void keep_flags_kernel(int64_t nnz, const unsigned long long* __restrict__ key,
-                                  unsigned long long omask, const uint8_t* __restrict__ oflag,
-                                  uint8_t* __restrict__ eflag) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
-       e += (int64_t)gridDim.x * blockDim.x)
-    eflag[e] = oflag[key[e] & omask] ? 0 : 1;
-}
-
 // composite (label, term, obj) -> the (label * dim + term) key of the classic path
 template <class K>
 struct CompKey {
@@ -759,16 +766,18 @@ int delta_sort(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms, cons
   } else if (cnt[1] > 0) {
     const int oth = cur ^ 1;
     const int64_t nb = (int64_t)cnt[1], nc = (int64_t)cnt[0];
-    // A: the unchanged objects' entries, in order
-    keep_flags_kernel<<<grid_for(nnz, T), T, 0, st>>>(nnz, d.key[cur], bt.omask, d.oflag,
-                                                      d.eflag);
-    IVFKM_CHECK_LAUNCH();
+    // A: the unchanged objects' entries, in order (the kept flags computed
+    // from the keys inside both selects: no flag pass)
     size_t cb = d.cub_bytes;
-    IVFKM_TRY(cub::DeviceSelect::Flagged(d.cub, cb, d.key[cur], d.eflag, d.key[oth],
-                                         d.counts + 2, (int)nnz, st));
-    cb = d.cub_bytes;
-    IVFKM_TRY(cub::DeviceSelect::Flagged(d.cub, cb, d.val[cur], d.eflag, d.val[oth],
-                                         d.counts + 2, (int)nnz, st));
+    {
+      auto kept = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0),
+                                                  KeptFlag{d.key[cur], d.oflag, bt.omask});
+      IVFKM_TRY(cub::DeviceSelect::Flagged(d.cub, cb, d.key[cur], kept, d.key[oth],
+                                           d.counts + 2, (int)nnz, st));
+      cb = d.cub_bytes;
+      IVFKM_TRY(cub::DeviceSelect::Flagged(d.cub, cb, d.val[cur], kept, d.val[oth],
+                                           d.counts + 2, (int)nnz, st));
+    }
     // B: the changed objects' entries under their new labels, sorted
     {
       // list the changed objects (ascending ids)

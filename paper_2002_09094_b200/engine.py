@@ -215,10 +215,11 @@ def update_launches(k: int, dim: int) -> int:
     return 16 + (bits + 7) // 8
 
 def delta_update_launches() -> int:
-    """Extra kernels of the label-delta sort (changed, keep flags, 3 CUB
-    selects, lengths, scan, keys, the changed entries' radix sort, merge,
-    header) in place of keys + the full sort."""
-    return 23
+    """Extra kernels of the label-delta sort (changed, 3 CUB selects — the
+    kept keys and values with their flags computed from the keys, the movers
+    — lengths, scan, keys, the movers' radix sort, merge, header) in place
+    of keys + the full sort."""
+    return 22
 
 
 def update_rows(lib, n_obj, nnz, row_ptr, terms, val64, labels0, sizes, prev: DeviceMeans, k,
