@@ -760,7 +760,11 @@ int delta_sort(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms, cons
     cub::DoubleBuffer<unsigned long long> kb(d.key[0], d.key[1]);
     cub::DoubleBuffer<double> vb(d.val[0], d.val[1]);
     size_t cb = d.cub_bytes;
-    IVFKM_TRY(cub::DeviceRadixSort::SortPairs(d.cub, cb, kb, vb, (int)nnz, 0, total_bits, st));
+    // the entries are produced in object order and the radix sort is stable,
+    // so sorting the (label, term) bits alone leaves equal pairs in object
+    // order: the object bits need no passes
+    IVFKM_TRY(cub::DeviceRadixSort::SortPairs(d.cub, cb, kb, vb, (int)nnz, bt.ob, total_bits,
+                                              st));
     cur = kb.selector;
     *moved = nnz;
   } else if (cnt[1] > 0) {
@@ -798,7 +802,9 @@ int delta_sort(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms, cons
     cub::DoubleBuffer<unsigned long long> kb(d.bkey[0], d.bkey[1]);
     cub::DoubleBuffer<double> vb(d.bval[0], d.bval[1]);
     cb = d.cub_bytes;
-    IVFKM_TRY(cub::DeviceRadixSort::SortPairs(d.cub, cb, kb, vb, (int)nb, 0, total_bits, st));
+    // movers listed in ascending object order: (label, term) bits only, as above
+    IVFKM_TRY(cub::DeviceRadixSort::SortPairs(d.cub, cb, kb, vb, (int)nb, bt.ob, total_bits,
+                                              st));
     // merge A (oth) and B into cur (keys are unique: no ties to order)
     cb = d.cub_bytes;
     IVFKM_TRY(cub::DeviceMerge::MergePairs(d.cub, cb, d.key[oth], d.val[oth], (int)(nnz - nb),

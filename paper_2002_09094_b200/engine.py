@@ -214,12 +214,14 @@ def update_launches(k: int, dim: int) -> int:
     bits = max(1, int(np.ceil(np.log2(max(2.0, float(k) * float(dim))))))
     return 16 + (bits + 7) // 8
 
-def delta_update_launches() -> int:
-    """Extra kernels of the label-delta sort (changed, 3 CUB selects — the
-    kept keys and values with their flags computed from the keys, the movers
-    — lengths, scan, keys, the movers' radix sort, merge, header) in place
-    of keys + the full sort."""
-    return 22
+def delta_update_launches(k: int, dim: int) -> int:
+    """Kernels of the label-delta sort (changed, 3 CUB selects — the kept
+    keys and values with their flags computed from the keys, the movers —
+    lengths, scan, keys, the movers' radix sort over the (label, term) bits:
+    histogram, exclusive sum, a pass per 8 bits — merge (2), header), in
+    place of keys + the full sort."""
+    bits = int(np.ceil(np.log2(max(2, k)))) + int(np.ceil(np.log2(max(2, dim))))
+    return 16 + (bits + 7) // 8
 
 
 def update_rows(lib, n_obj, nnz, row_ptr, terms, val64, labels0, sizes, prev: DeviceMeans, k,
@@ -421,7 +423,8 @@ class LloydEngine:
         self.launches += update_launches(self.k, dd.dim)
         if self.upd_state is not None:
             # minus keys + the full sort (histogram, exclusive sum, passes)
-            self.launches += delta_update_launches() - (update_launches(self.k, dd.dim) - 13)
+            self.launches += (delta_update_launches(self.k, dd.dim)
+                              - (update_launches(self.k, dd.dim) - 13))
         return self.build_bivf(out)
 
     def _defer_ok(self, dm: DeviceMeans) -> bool:
