@@ -44,10 +44,11 @@ def main():
         prev = lab
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
-        for _ in range(a.steps):
+        for _ in range(a.steps):  # the bench's loop
             lab = eng.assign(dm, prev)
-            eng.read_stats()
+            eng.stats_async()
             dm = eng.update(lab, dm)
+            eng.stats_ready()
             prev = lab
         torch.cuda.synchronize()
     evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
