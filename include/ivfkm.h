@@ -112,6 +112,15 @@ int ivfkm_bivf_plan(int64_t k, int64_t dim, int major, int64_t nrows,
 /* fill: with a workspace of ivfkm_bivf_fill_workspace_size(k, dim, nnz)
  * bytes (nnz = input entries) the postings are sorted by position first, so
  * the writes stream; ws = NULL scatters them directly.                      */
+/* plan + fill in one call when val_screen / val64 / ws_fill are large enough
+ * (screen_cap, val64_cap elements); otherwise IVFKM_E_WORKSPACE with the plan
+ * done and totals set, and the caller runs ivfkm_bivf_fill.                 */
+int ivfkm_bivf_plan_fill(int64_t k, int64_t dim, int major, int64_t nrows, const int64_t* ptr,
+                         const int32_t* cols, const double* vals, uint32_t* headers,
+                         int64_t* totals /*[host] out, 2*/, void* val_screen,
+                         int64_t screen_cap, int screen_bits, double* val64, int64_t val64_cap,
+                         void* ws_plan, size_t ws_plan_bytes, void* ws_fill,
+                         size_t ws_fill_bytes, ivfkm_stream_t stream);
 size_t ivfkm_bivf_fill_workspace_size(int64_t k, int64_t dim, int64_t nnz);
 int ivfkm_bivf_fill(int64_t k, int64_t dim, int major, int64_t nrows,
                     const int64_t* ptr /*[dev]*/, const int32_t* cols /*[dev]*/,

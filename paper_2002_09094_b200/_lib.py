@@ -14,6 +14,7 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libivfkm.so"
 
 IVFKM_OBJ_LIMBS = 34
 IVFKM_MAXC = 32
+IVFKM_E_WORKSPACE = -4  # include/ivfkm.h
 
 _i64, _u64, _i32, _f64, _vp, _sz = C.c_int64, C.c_uint64, C.c_int32, C.c_double, C.c_void_p, C.c_size_t
 
@@ -80,6 +81,8 @@ SIGNATURES = {
                                     _vp, _i64, _vp, _sz, _vp]),
     "ivfkm_assign_ivf_host": (C.c_int, [_i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp,
                                         _vp]),
+    "ivfkm_bivf_plan_fill": (C.c_int, [_i64, _i64, C.c_int, _i64, _vp, _vp, _vp, _vp, _vp, _vp,
+                                       _i64, C.c_int, _vp, _i64, _vp, _sz, _vp, _sz, _vp]),
     "ivfkm_rows_decode": (C.c_int, [_i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp]),
     "ivfkm_uci_parse": (C.c_int, [_vp, _sz, C.c_int, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp,
                                   _vp, _vp, _vp]),

@@ -638,6 +638,27 @@ extern "C" int ivfkm_bivf_fill(int64_t k, int64_t dim, int major, int64_t nrows,
                    val64, as_stream(stream_), nnz, ws);
 }
 
+// plan, then (when the caller's buffers are large enough) fill, with no
+// host round trip in between; IVFKM_E_WORKSPACE leaves the plan done and the
+// fill to the caller (totals tell the sizes).
+extern "C" int ivfkm_bivf_plan_fill(int64_t k, int64_t dim, int major, int64_t nrows,
+                                    const int64_t* ptr, const int32_t* cols, const double* vals,
+                                    uint32_t* headers, int64_t* totals, void* val_screen,
+                                    int64_t screen_cap, int screen_bits, double* val64,
+                                    int64_t val64_cap, void* ws_plan, size_t ws_plan_bytes,
+                                    void* ws_fill, size_t ws_fill_bytes, ivfkm_stream_t stream_) {
+  if (screen_bits != 32 && screen_bits != 16) return IVFKM_E_ARG;
+  if (int rc = ivfkm_bivf_plan(k, dim, major, nrows, ptr, cols, headers, totals, ws_plan,
+                               ws_plan_bytes, stream_))
+    return rc;
+  const int64_t nnz = totals[1];
+  if (totals[0] > screen_cap || nnz > val64_cap || !ws_fill ||
+      ws_fill_bytes < ivfkm_bivf_fill_workspace_size(k, dim, nnz))
+    return IVFKM_E_WORKSPACE;
+  return fill_impl(k, dim, major, nrows, ptr, cols, vals, headers, val_screen, screen_bits,
+                   val64, as_stream(stream_), nnz, ws_fill);
+}
+
 extern "C" int ivfkm_bivf_build(int64_t k, int64_t dim, int major, int64_t nrows,
                                 const int64_t* ptr, const int32_t* cols, const double* vals,
                                 uint32_t* headers, void* val_screen, int screen_bits,

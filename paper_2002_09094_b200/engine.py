@@ -291,6 +291,11 @@ class LloydEngine:
         self.ws_bivf = torch.empty(int(self.lib.ivfkm_bivf_workspace_size(dim, self.k)),
                                    dtype=u8, device=dev)
         self.ws_fill = None  # sorted BIVF fill (grows with the means' size)
+        # BIVF value arrays, grown on demand and alternated between builds (the
+        # means of the previous build keep theirs)
+        self._bvbuf = [None, None]
+        self._bvpar = 0
+        self._totals = np.zeros(2, np.int64)
         # label-delta update sort: the previous iteration's sorted entries
         # (DESIGN.md §4); zero-filled = no state yet
         sbytes = int(self.lib.ivfkm_update_state_size(n, nnz, self.k, dim)) if delta_update else 0
@@ -321,28 +326,44 @@ class LloydEngine:
         dev = self.device
         dm.headers = torch.empty(int(self.lib.ivfkm_bivf_headers_size(self.k, dm.dim)),
                                  dtype=torch.int32, device=dev)
-        # plan (headers; the host learns the exact value count), then fill
-        totals = np.zeros(2, np.int64)  # (screen values, exact values)
-        rc = self.lib.ivfkm_bivf_plan(self.k, dm.dim, 0, self.k, _p(dm.ptr), _p(dm.terms),
-                                      _p(dm.headers), C.c_void_p(totals.ctypes.data),
-                                      _p(self.ws_bivf), self.ws_bivf.numel(), _stream())
-        _lib.check(rc, "ivfkm_bivf_plan")
-        if dm.nnz < 0:  # deferred update: the plan counted the postings
-            dm.nnz = int(totals[1])
-            dm.terms, dm.vals = dm.terms[:dm.nnz], dm.vals[:dm.nnz]
+        # plan (headers; the host learns the exact value counts), then fill —
+        # in the same call when this parity's value buffers are big enough
+        # (no host round trip between the two), else once more after growing
+        totals = self._totals  # (screen values, exact values)
         bits = self.screen_bits
-        dm.pvs = torch.empty(max(int(totals[0]), 1),
-                             dtype=torch.float16 if bits == 16 else torch.float32, device=dev)
-        dm.pv64 = torch.empty(max(int(totals[1]), 1), dtype=torch.float64, device=dev)
-        need = int(self.lib.ivfkm_bivf_fill_workspace_size(self.k, dm.dim, dm.nnz))
-        if self.ws_fill is None or self.ws_fill.numel() < need:
-            self.ws_fill = torch.empty(int(need * 1.25) + 4096, dtype=torch.uint8, device=dev)
-        rc = self.lib.ivfkm_bivf_fill(self.k, dm.dim, 0, self.k, _p(dm.ptr), _p(dm.terms),
-                                      _p(dm.vals), _p(dm.headers), _p(dm.pvs), bits,
-                                      _p(dm.pv64), dm.nnz, _p(self.ws_fill),
-                                      self.ws_fill.numel(), _stream())
+        vdt = torch.float16 if bits == 16 else torch.float32
+        buf = self._bvbuf[self._bvpar]
+        self._bvpar ^= 1  # the previous means keep their arrays
+        rc = self.lib.ivfkm_bivf_plan_fill(
+            self.k, dm.dim, 0, self.k, _p(dm.ptr), _p(dm.terms), _p(dm.vals), _p(dm.headers),
+            C.c_void_p(totals.ctypes.data), _p(buf["pvs"]) if buf else None,
+            buf["pvs"].numel() if buf else 0, bits, _p(buf["pv64"]) if buf else None,
+            buf["pv64"].numel() if buf else 0, _p(self.ws_bivf), self.ws_bivf.numel(),
+            _p(self.ws_fill), self.ws_fill.numel() if self.ws_fill is not None else 0, _stream())
+        filled = rc == 0
+        if rc != _lib.IVFKM_E_WORKSPACE:
+            _lib.check(rc, "ivfkm_bivf_plan_fill")
+        n_s, n_64 = int(totals[0]), int(totals[1])
+        if dm.nnz < 0:  # deferred update: the plan counted the postings
+            dm.nnz = n_64
+            dm.terms, dm.vals = dm.terms[:dm.nnz], dm.vals[:dm.nnz]
+        if not filled:
+            if buf is None or buf["pvs"].numel() < n_s or buf["pv64"].numel() < n_64:
+                buf = {"pvs": torch.empty(int(n_s * 1.25) + 1024, dtype=vdt, device=dev),
+                       "pv64": torch.empty(int(n_64 * 1.25) + 1024, dtype=torch.float64,
+                                           device=dev)}
+                self._bvbuf[self._bvpar ^ 1] = buf
+            need = int(self.lib.ivfkm_bivf_fill_workspace_size(self.k, dm.dim, dm.nnz))
+            if self.ws_fill is None or self.ws_fill.numel() < need:
+                self.ws_fill = torch.empty(int(need * 1.25) + 4096, dtype=torch.uint8, device=dev)
+            rc = self.lib.ivfkm_bivf_fill(self.k, dm.dim, 0, self.k, _p(dm.ptr), _p(dm.terms),
+                                          _p(dm.vals), _p(dm.headers), _p(buf["pvs"]), bits,
+                                          _p(buf["pv64"]), dm.nnz, _p(self.ws_fill),
+                                          self.ws_fill.numel(), _stream())
+            _lib.check(rc, "ivfkm_bivf_fill")
+        dm.pvs = buf["pvs"][:max(n_s, 1)]
+        dm.pv64 = buf["pv64"][:max(n_64, 1)]
         dm.screen_bits = bits
-        _lib.check(rc, "ivfkm_bivf_fill")
         # plan: sizes, CUB sort of the k slot keys (single tile / onesweep), perm,
         # mask, count, 2 scans (init + sweep each), offset, nc, {mask, offset}
         # pairs; fill: zero, position keys, CUB onesweep sort of the keys' top
