@@ -36,6 +36,9 @@
 #include <cuda_fp16.h>
 
 #include <cub/cub.cuh>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include <cfloat>
 #include <climits>
@@ -1473,7 +1476,22 @@ int launch_screen(const Plan& pl, const ScreenParams& p, cudaStream_t st) {
                                                           ? screen_kernel<RR, true, 56>
                                                           : screen_kernel<RR, true>)
                                                    : screen_kernel<RR, false>));
-  IVFKM_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+  {
+    // raise the kernel's dynamic shared-memory limit only when a launch needs
+    // more than it was given (per device): the call costs host time on every
+    // launch otherwise
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> limit;
+    std::lock_guard<std::mutex> g(mu);
+    int dev = 0;
+    IVFKM_TRY(cudaGetDevice(&dev));
+    size_t& cur = limit[std::make_pair(reinterpret_cast<const void*>(fn), dev)];
+    if (pl.smem > cur) {
+      IVFKM_TRY(
+          cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+      cur = pl.smem;
+    }
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(p.n_obj * pl.nsplit));
   cfg.blockDim = dim3(pl.warps * 32);
