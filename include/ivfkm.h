@@ -191,6 +191,21 @@ int ivfkm_assign_finish(int64_t n_obj, const int64_t* row_ptr, const int32_t* te
                         double* sims, unsigned long long* sizes, ivfkm_stats* stats,
                         int label_rule, void* ws, size_t ws_bytes, ivfkm_stream_t stream);
 
+/* finish, rescoring through the means' mean-major CSR (m_ptr[k+1], 0-based
+ * m_terms, m_vals — the same means as headers/pval64) instead of the BIVF:
+ * builds a rank directory in dir (k * ceil(dim/32) uint2: the mean's term
+ * bits per 32-term word + the rank of the word's first term in the mean's
+ * row) and rescores the objects grouped by their screen winner, so that
+ * concurrently resident warps read a few means' contiguous values.  Same
+ * results bit for bit.                                                      */
+int ivfkm_assign_finish_dir(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
+                            const double* val64, int64_t k, int64_t dim, const uint32_t* headers,
+                            const double* pval64, const int64_t* m_ptr, const int32_t* m_terms,
+                            const double* m_vals, void* dir /*[dev] k*ceil(dim/32)*8 B*/,
+                            const int32_t* prev_labels, int32_t* labels, double* sims,
+                            unsigned long long* sizes, ivfkm_stats* stats, int label_rule,
+                            void* ws, size_t ws_bytes, ivfkm_stream_t stream);
+
 /* Exact float64 similarity of every object to the mean its (0-based) label
  * names — the summand of objective_cosine (clustering.py:105-119) — written
  * to sims, with the exact sum accumulated into stats->obj_limbs (stats is

@@ -1085,6 +1085,12 @@ struct ExactCtx {
   const double* val64;
   BivfView bv;
   const double* pv64;
+  // optional rank directory of the means' CSR: dir[c*nw + w] = {bits of
+  // terms 32w..32w+31 in mean c, rank of the first within the mean's row}
+  const uint2* dir = nullptr;
+  const int64_t* m_ptr = nullptr;
+  const double* m_vals = nullptr;
+  int64_t nw = 0;
 };
 
 // Warp-cooperative: lanes look up kExactU*32 nonzeros at a time (every
@@ -1099,6 +1105,43 @@ constexpr int kExactU = 4;
 __device__ double exact_score_warp(const ExactCtx& x, int64_t rb, int64_t re, int c, int lane,
                                    double* scratch) {
   double acc = 0.0;
+  if (x.dir) {  // mean-major lookups through the rank directory
+    const uint2* drow = x.dir + (int64_t)c * x.nw;
+    const double* mv = x.m_vals + __ldg(x.m_ptr + c);
+    for (int64_t h0 = rb; h0 < re; h0 += 32 * kExactU) {
+      int32_t t[kExactU];
+      uint2 d[kExactU];
+#pragma unroll
+      for (int u = 0; u < kExactU; ++u) {
+        const int64_t h = h0 + 32 * u + lane;
+        t[u] = h < re ? __ldg(x.terms + h) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < kExactU; ++u) d[u] = t[u] >= 0 ? __ldg(drow + (t[u] >> 5)) : make_uint2(0u, 0u);
+#pragma unroll
+      for (int u = 0; u < kExactU; ++u) {
+        const int64_t h = h0 + 32 * u + lane;
+        const uint32_t b = t[u] >= 0 ? 1u << (t[u] & 31) : 0u;
+        scratch[32 * u + lane] =
+            (d[u].x & b) ? __dmul_rn(__ldg(x.val64 + h),
+                                     __ldg(mv + d[u].y + __popc(d[u].x & (b - 1u))))
+                         : 0.0;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const int n = re - h0 < 32 * kExactU ? (int)(re - h0) : 32 * kExactU;
+        int j = 0;
+        for (; j + 4 <= n; j += 4) {
+          const double2 u = reinterpret_cast<const double2*>(scratch)[j >> 1];
+          const double2 v = reinterpret_cast<const double2*>(scratch)[(j >> 1) + 1];
+          acc = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(acc, u.x), u.y), v.x), v.y);
+        }
+        for (; j < n; ++j) acc = __dadd_rn(acc, scratch[j]);
+      }
+      __syncwarp();
+    }
+    return __shfl_sync(kFull, acc, 0);
+  }
   const int64_t slot = x.bv.perm ? (int64_t)__ldg(x.bv.perm + c) : c;
   const int64_t sb = slot >> 5;
   const uint32_t bit = 1u << (slot & 31);
@@ -1147,6 +1190,99 @@ __device__ double exact_score_thread(const ExactCtx& x, int64_t rb, int64_t re, 
   return acc;
 }
 
+__global__ void winner_hist_kernel(int64_t n_obj, const int32_t* __restrict__ label32,
+                                   unsigned int* __restrict__ hist) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_obj;
+       i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&hist[label32[i]], 1u);
+}
+
+__global__ void winner_scatter_kernel(int64_t n_obj, const int32_t* __restrict__ label32,
+                                      unsigned int* __restrict__ cursor,
+                                      int32_t* __restrict__ order) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_obj;
+       i += (int64_t)gridDim.x * blockDim.x)
+    order[atomicAdd(&cursor[label32[i]], 1u)] = (int32_t)i;
+}
+
+// rank directory of a mean-major CSR (0-based terms ascending per row):
+// each warp takes a contiguous range of entries (one binary search for its
+// first mean, then advancing), 32 at a time; lanes sharing a (mean, word) OR
+// their bits together and the lowest of them publishes
+__global__ void rankdir_bits_kernel(int64_t k, int64_t nw, const int64_t* __restrict__ ptr,
+                                    const int32_t* __restrict__ terms, uint2* __restrict__ dir) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t nnz = ptr[k];
+  const int64_t per = ((nnz + nwarps - 1) / nwarps + 31) / 32 * 32;
+  const int64_t b0 = wid * per, b1 = b0 + per < nnz ? b0 + per : nnz;
+  if (b0 >= b1) return;
+  int64_t c;
+  {
+    int64_t lo = 0, hi = k;  // ptr[c] <= b0 < ptr[c+1]
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (__ldg(ptr + mid) <= b0) lo = mid; else hi = mid;
+    }
+    c = lo;
+  }
+  for (int64_t e0 = b0; e0 < b1; e0 += 32) {
+    const int64_t e = e0 + lane;
+    int64_t key = -1;
+    uint32_t bit = 0u;
+    if (e < b1) {
+      int64_t cl = c;
+      while (__ldg(ptr + cl + 1) <= e) ++cl;  // rows are long: rarely more than once
+      const int32_t t = terms[e];
+      key = cl * nw + (t >> 5);
+      bit = 1u << (t & 31);
+    }
+    // keys ascend across the lanes: a segmented OR towards each run's last
+    // lane (shuffles), which publishes — with an atomic only where the run
+    // may continue in a neighbouring chunk (first and last run)
+    const int64_t kn = __shfl_down_sync(kFull, key, 1);
+    uint32_t acc = bit;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, acc, off);
+      const int64_t ky = __shfl_up_sync(kFull, key, off);
+      if (lane >= off && ky == key) acc |= y;
+    }
+    const int64_t k0 = __shfl_sync(kFull, key, 0);
+    const bool tail = lane == 31 || kn < 0;  // the chunk's last valid run
+    if (key >= 0 && (tail || kn != key)) {
+      if (key == k0 || tail) atomicOr(&dir[key].x, acc);
+      else dir[key].x = acc;  // wholly inside this chunk
+    }
+    // the mean of the next chunk's first entry
+    const int64_t nx = e0 + 32;
+    if (nx < b1)
+      while (__ldg(ptr + c + 1) <= nx) ++c;
+  }
+}
+
+__global__ void rankdir_scan_kernel(int64_t k, int64_t nw, uint2* __restrict__ dir) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t c = blockIdx.x * wpb + (threadIdx.x >> 5); c < k; c += gridDim.x * wpb) {
+    uint2* row = dir + c * nw;
+    unsigned int carry = 0;
+    for (int64_t w0 = 0; w0 < nw; w0 += 32) {
+      const int64_t w = w0 + lane;
+      const unsigned int pc = w < nw ? __popc(row[w].x) : 0u;
+      unsigned int inc = pc;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const unsigned int y = __shfl_up_sync(kFull, inc, off);
+        if (lane >= off) inc += y;
+      }
+      if (w < nw) row[w].y = carry + inc - pc;
+      carry += __shfl_sync(kFull, inc, 31);
+    }
+  }
+}
+
 struct FinalParams {
   int64_t n_obj;
   ExactCtx x;
@@ -1159,6 +1295,7 @@ struct FinalParams {
   int32_t* ovf_list;
   unsigned int* ovf_len;
   int rule;  // 0: IVF argmax (_kernels.pyx:17-26); 1: IVFD (_kernels.pyx:178-207)
+  const int32_t* order = nullptr;  // objects grouped by screen winner, or nullptr
 };
 
 // IVFD keeps a label only when its similarity beats 0.0 (rho_max starts at
@@ -1173,7 +1310,8 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinalParams p) {
   const int lane = threadIdx.x & 31;
   double* scratch = s_scr[threadIdx.x >> 5];
   const int64_t wpb = blockDim.x >> 5;
-  for (int64_t i = blockIdx.x * wpb + (threadIdx.x >> 5); i < p.n_obj; i += gridDim.x * wpb) {
+  for (int64_t q = blockIdx.x * wpb + (threadIdx.x >> 5); q < p.n_obj; q += gridDim.x * wpb) {
+    const int64_t i = p.order ? (int64_t)p.order[q] : q;
     const int64_t rb = p.x.row_ptr[i], re = p.x.row_ptr[i + 1];
     const int slot = p.slot_of[i];
     if (slot < 0) {
@@ -1358,9 +1496,13 @@ struct AssignWs {
   int32_t* q_cid;
   int32_t* ovf_list;
   unsigned int* ovf_len;
+  unsigned int* cl_pos;  // k + 1: objects per screen winner, then their cursors
+  int32_t* fin_order;    // n: objects grouped by screen winner
+  void* cub;
+  size_t cub_bytes;
 };
 
-AssignWs carve_assign(void* base, int64_t n, size_t* total) {
+AssignWs carve_assign(void* base, int64_t n, int64_t k, size_t* total) {
   Carver c(base);
   AssignWs w;
   w.label32 = c.take<int32_t>(n);
@@ -1370,6 +1512,12 @@ AssignWs carve_assign(void* base, int64_t n, size_t* total) {
   w.q_cid = c.take<int32_t>((size_t)n * kMaxC);
   w.ovf_list = c.take<int32_t>(n);
   w.ovf_len = c.take<unsigned int>(4);
+  w.cl_pos = c.take<unsigned int>((size_t)k + 1);
+  w.fin_order = c.take<int32_t>(n);
+  w.cub_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, w.cub_bytes, (unsigned int*)nullptr,
+                                (unsigned int*)nullptr, (int)(k + 1));
+  w.cub = c.take_bytes(w.cub_bytes);
   if (total) *total = c.off;
   return w;
 }
@@ -1565,9 +1713,9 @@ extern "C" int ivfkm_row_order(int64_t n_obj, const int64_t* row_ptr, int32_t* o
   return IVFKM_OK;
 }
 
-extern "C" size_t ivfkm_assign_workspace_size(int64_t n_obj, int64_t /*k*/) {
+extern "C" size_t ivfkm_assign_workspace_size(int64_t n_obj, int64_t k) {
   size_t total = 0;
-  carve_assign(nullptr, n_obj, &total);
+  carve_assign(nullptr, n_obj, k, &total);
   return total;
 }
 
@@ -1646,8 +1794,27 @@ int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
 
 int finish_impl(const AssignArgs& a, const AssignWs& w, const int32_t* prev_labels,
                 int32_t* labels, double* sims, unsigned long long* sizes, int rule,
-                cudaStream_t st) {
+                cudaStream_t st, const int64_t* m_ptr = nullptr, const int32_t* m_terms = nullptr,
+                const double* m_vals = nullptr, uint2* dir = nullptr) {
   FinalParams fp;
+  const int T = 256;
+  const int64_t nw = (a.dim + 31) / 32;
+  if (dir) {
+    IVFKM_TRY(cudaMemsetAsync(dir, 0, sizeof(uint2) * a.k * nw, st));
+    rankdir_bits_kernel<<<kNumSM * 8, T, 0, st>>>(a.k, nw, m_ptr, m_terms, dir);
+    IVFKM_CHECK_LAUNCH();
+    rankdir_scan_kernel<<<grid_for(a.k, T / 32), T, 0, st>>>(a.k, nw, dir);
+    IVFKM_CHECK_LAUNCH();
+    IVFKM_TRY(cudaMemsetAsync(w.cl_pos, 0, sizeof(unsigned int) * (a.k + 1), st));
+    winner_hist_kernel<<<grid_for(a.n_obj, T), T, 0, st>>>(a.n_obj, w.label32, w.cl_pos);
+    IVFKM_CHECK_LAUNCH();
+    size_t cb = w.cub_bytes;
+    IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.cl_pos, w.cl_pos, (int)(a.k + 1), st));
+    winner_scatter_kernel<<<grid_for(a.n_obj, T), T, 0, st>>>(a.n_obj, w.label32, w.cl_pos,
+                                                             w.fin_order);
+    IVFKM_CHECK_LAUNCH();
+    fp.order = w.fin_order;
+  }
   fp.n_obj = a.n_obj;
   fp.rule = rule;
   fp.x.row_ptr = a.row_ptr;
@@ -1655,6 +1822,12 @@ int finish_impl(const AssignArgs& a, const AssignWs& w, const int32_t* prev_labe
   fp.x.val64 = a.val64;
   fp.x.bv = exact_view(a.headers, a.k, a.dim);
   fp.x.pv64 = a.pval64;
+  if (dir) {
+    fp.x.dir = dir;
+    fp.x.m_ptr = m_ptr;
+    fp.x.m_vals = m_vals;
+    fp.x.nw = nw;
+  }
   fp.label32 = w.label32;
   fp.slot_of = w.slot_of;
   fp.q_cnt = w.q_cnt;
@@ -1687,7 +1860,7 @@ extern "C" int ivfkm_assign_screen(int64_t n_obj, const int64_t* row_ptr, const 
   if (screen_bits == 16 && !(mu_max <= 32768.0)) return IVFKM_E_UNSUPPORTED;
   if (n_obj > INT32_MAX || k > INT32_MAX) return IVFKM_E_UNSUPPORTED;
   size_t need = 0;
-  AssignWs w = carve_assign(ws, n_obj, &need);
+  AssignWs w = carve_assign(ws, n_obj, k, &need);
   if (ws_bytes < need) return IVFKM_E_WORKSPACE;
   cudaStream_t st = as_stream(stream_);
   IVFKM_TRY(cudaMemsetAsync(stats, 0, sizeof(ivfkm_stats), st));
@@ -1708,7 +1881,7 @@ extern "C" int ivfkm_assign_finish(int64_t n_obj, const int64_t* row_ptr, const 
     return IVFKM_E_ARG;
   if (label_rule != 0 && label_rule != 1) return IVFKM_E_ARG;
   size_t need = 0;
-  AssignWs w = carve_assign(ws, n_obj, &need);
+  AssignWs w = carve_assign(ws, n_obj, k, &need);
   if (ws_bytes < need) return IVFKM_E_WORKSPACE;
   cudaStream_t st = as_stream(stream_);
   if (sizes) IVFKM_TRY(cudaMemsetAsync(sizes, 0, sizeof(unsigned long long) * k, st));
@@ -1716,6 +1889,30 @@ extern "C" int ivfkm_assign_finish(int64_t n_obj, const int64_t* row_ptr, const 
   AssignArgs a{n_obj,   row_ptr, terms, nullptr, val64, nullptr, k,      dim,
                headers, nullptr, 32,    pval64,  0.0,   stats,   nullptr};
   return finish_impl(a, w, prev_labels, labels, sims, sizes, label_rule, st);
+}
+
+extern "C" int ivfkm_assign_finish_dir(int64_t n_obj, const int64_t* row_ptr,
+                                       const int32_t* terms, const double* val64, int64_t k,
+                                       int64_t dim, const uint32_t* headers, const double* pval64,
+                                       const int64_t* m_ptr, const int32_t* m_terms,
+                                       const double* m_vals, void* dir, const int32_t* prev_labels,
+                                       int32_t* labels, double* sims, unsigned long long* sizes,
+                                       ivfkm_stats* stats, int label_rule, void* ws,
+                                       size_t ws_bytes, ivfkm_stream_t stream_) {
+  if (n_obj < 0 || k < 1 || dim < 1 || !row_ptr || !labels || !sims || !stats || !headers)
+    return IVFKM_E_ARG;
+  if (!m_ptr || !m_terms || !m_vals || !dir) return IVFKM_E_ARG;
+  if (label_rule != 0 && label_rule != 1) return IVFKM_E_ARG;
+  size_t need = 0;
+  AssignWs w = carve_assign(ws, n_obj, k, &need);
+  if (ws_bytes < need) return IVFKM_E_WORKSPACE;
+  cudaStream_t st = as_stream(stream_);
+  if (sizes) IVFKM_TRY(cudaMemsetAsync(sizes, 0, sizeof(unsigned long long) * k, st));
+  if (n_obj == 0) return IVFKM_OK;
+  AssignArgs a{n_obj,   row_ptr, terms, nullptr, val64, nullptr, k,      dim,
+               headers, nullptr, 32,    pval64,  0.0,   stats,   nullptr};
+  return finish_impl(a, w, prev_labels, labels, sims, sizes, label_rule, st, m_ptr, m_terms,
+                     m_vals, static_cast<uint2*>(dir));
 }
 
 extern "C" int ivfkm_assign(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,

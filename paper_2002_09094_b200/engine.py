@@ -293,6 +293,11 @@ class LloydEngine:
         self.ws_fill = None  # sorted BIVF fill (grows with the means' size)
         # BIVF value arrays, grown on demand and alternated between builds (the
         # means of the previous build keep theirs)
+        # rank directory of the means' CSR for the exact rescoring (one lookup
+        # word per 32 terms per mean), used while it stays L2-sized
+        nw = (dim + 31) // 32
+        self.rankdir = (torch.empty(self.k * nw * 2, dtype=torch.int32, device=dev)
+                        if self.k * nw * 8 <= (64 << 20) else None)
         self._bvbuf = [None, None]
         self._bvpar = 0
         self._totals = np.zeros(2, np.int64)
@@ -404,11 +409,21 @@ class LloydEngine:
         _lib.check(rc, "ivfkm_assign_screen")
         if events is not None:
             events[1].record()
-        rc = self.lib.ivfkm_assign_finish(dd.n, _p(dd.row_ptr), _p(dd.terms), _p(dd.val64),
-                                          self.k, dd.dim, _p(dm.headers), _p(dm.pv64), _p(prev),
-                                          _p(out), _p(self.sims), _p(self.sizes), _p(self.stats),
-                                          rule, _p(self.ws_assign), self.ws_assign.numel(), st)
-        _lib.check(rc, "ivfkm_assign_finish")
+        if self.rankdir is not None:
+            rc = self.lib.ivfkm_assign_finish_dir(
+                dd.n, _p(dd.row_ptr), _p(dd.terms), _p(dd.val64), self.k, dd.dim,
+                _p(dm.headers), _p(dm.pv64), _p(dm.ptr), _p(dm.terms), _p(dm.vals),
+                _p(self.rankdir), _p(prev), _p(out), _p(self.sims), _p(self.sizes),
+                _p(self.stats), rule, _p(self.ws_assign), self.ws_assign.numel(), st)
+            _lib.check(rc, "ivfkm_assign_finish_dir")
+            self.launches += 6  # directory bits + ranks, winner histogram, scan (2), grouping
+        else:
+            rc = self.lib.ivfkm_assign_finish(dd.n, _p(dd.row_ptr), _p(dd.terms), _p(dd.val64),
+                                              self.k, dd.dim, _p(dm.headers), _p(dm.pv64),
+                                              _p(prev), _p(out), _p(self.sims), _p(self.sizes),
+                                              _p(self.stats), rule, _p(self.ws_assign),
+                                              self.ws_assign.numel(), st)
+            _lib.check(rc, "ivfkm_assign_finish")
         self.launches += 4
         return out
 
