@@ -151,6 +151,16 @@ size_t ivfkm_assign_workspace_size(int64_t n_obj, int64_t k);
  * sets w warps per CTA for the TMA screen.
  * Out-of-range values leave the setting unchanged.                          */
 void ivfkm_set_tuning(int rowcap, int smem_limit, int rr);
+/* Tests / tuning: force the register screen's warps per CTA (1..16; 0 = the
+ * planned count).  Spans are handed out to warps dynamically, so every count
+ * computes identical sums. */
+void ivfkm_set_screen_warps(int warps);
+/* The screen plan ivfkm_assign_screen would use for k means under the
+ * current tuning ([host] out[8]: span blocks RR, cluster CTAs per object,
+ * 32-mean blocks per CTA, warps per CTA, staged row entries, mode (0 register
+ * screen, 1 TMA ring, 2 cp.async ring), dynamic shared bytes, registers per
+ * thread of the instantiation).  rowcap < 32: the current default. */
+int ivfkm_screen_plan(int64_t k, int rowcap, int screen_bits, int32_t* out /*[host] 8*/);
 /* Object order: ivfkm_assign/_screen take `order`, the order in which the
  * screen visits objects ([dev] permutation of 0..n_obj-1; NULL = natural
  * order).  Results do not depend on it; it only changes load balance and
@@ -244,6 +254,10 @@ int ivfkm_update_count_delta(int64_t n_obj, int64_t nnz, const int64_t* row_ptr,
                              const int64_t* prev_ptr, int64_t* new_ptr, void* ws,
                              size_t ws_bytes, void* state /*[dev] zero-filled first*/,
                              size_t state_bytes, ivfkm_stream_t stream);
+/* fill: `capacity` = entries new_terms/new_vals hold.  Size them by the
+ * exact count new_ptr[k] (read after count) or by the bound
+ * min(nnz + prev_ptr[k], k * dim) (runs <= nnz, plus retained means'
+ * postings); writes at positions >= capacity are dropped, never performed. */
 int ivfkm_update_fill(int64_t n_obj, int64_t nnz, int64_t k, int64_t dim,
                       const unsigned long long* sizes, const int64_t* prev_ptr,
                       const int32_t* prev_terms, const double* prev_vals,

@@ -206,6 +206,67 @@ def update(ds, labels, prev: Means) -> Means:
     return Means(k, ds.dim, indptr, terms.astype(np.int32), vals, retained)
 
 
+def update_fast(ds, labels, prev: Means, chunk_bytes: int = 256 << 20) -> Means:
+    """update() vectorised for large k (BASELINE configs 2-4), bit-identical
+    to it (tests/test_oracle.py pins the two against each other):
+
+    * the per-cluster ``bincount(tsub - 1, weights=vsub)`` of variants.py:290
+      adds a cluster's entries of one term sequentially in entry order; one
+      global bincount over the (cluster, term) keys' ranks adds the same
+      subsequence in the same order, starting from the same 0.0;
+    * ``w /= size`` and the nonzero test (variants.py:291,294) per key;
+    * ``np.sum(w * w)`` (variants.py:292) is numpy's pairwise sum over the
+      dense length-D vector: replayed on dense (clusters x D) chunks with
+      ``np.sum(axis=1)``, which reduces each contiguous row with the same
+      pairwise routine as the 1-D sum;
+    * empty clusters keep the previous mean (variants.py:281-286)."""
+    k, dim = prev.k, ds.dim
+    labels = np.asarray(labels, dtype=np.int32)
+    sizes = sizes_of(labels, k)
+    entry, order = _member_entry_order(ds, labels)
+    lens = np.diff(ds.indptr)[order]
+    lab_e = np.repeat(labels[order].astype(np.int64) - 1, lens)
+    tsub = np.asarray(ds.term_ids)[entry].astype(np.int64) - 1
+    vsub = np.asarray(ds.values)[entry]
+    keys, inv = np.unique(lab_e * dim + tsub, return_inverse=True)
+    sums = np.bincount(inv.ravel(), weights=vsub, minlength=keys.size)
+    kc = keys // dim
+    kt = keys - kc * dim
+    w = sums / sizes[kc].astype(np.float64)
+    # pairwise norms over dense chunks of clusters (zeros included, as numpy)
+    nrm = np.zeros(k)
+    starts = np.searchsorted(kc, np.arange(k + 1))
+    per = max(1, chunk_bytes // (8 * max(dim, 1)))
+    live = np.flatnonzero(sizes > 0)
+    for c0 in range(0, live.size, per):
+        cl = live[c0:c0 + per]
+        dense = np.zeros((cl.size, dim))
+        for r, c in enumerate(cl):
+            s, e = starts[c], starts[c + 1]
+            dense[r, kt[s:e]] = w[s:e]
+        nrm[cl] = np.sqrt(np.sum(dense * dense, axis=1))
+    keep = w != 0.0
+    counts = np.bincount(kc[keep], minlength=k).astype(np.int64)
+    retained = sizes == 0
+    pc = np.diff(prev.indptr)
+    counts[retained] = pc[retained]
+    indptr = np.zeros(k + 1, dtype=np.int64)
+    np.cumsum(counts, out=indptr[1:])
+    terms = np.empty(int(indptr[-1]), np.int32)
+    vals = np.empty(int(indptr[-1]), np.float64)
+    kk = np.flatnonzero(keep)
+    kcl = kc[kk]
+    rank = np.arange(kk.size) - np.searchsorted(kcl, kcl)  # position within its cluster
+    pos = indptr[kcl] + rank
+    terms[pos] = (kt[kk] + 1).astype(np.int32)
+    vals[pos] = w[kk] / nrm[kcl]
+    for c in np.flatnonzero(retained):
+        s, e = int(prev.indptr[c]), int(prev.indptr[c + 1])
+        terms[indptr[c]:indptr[c + 1]] = prev.term_ids[s:e]
+        vals[indptr[c]:indptr[c + 1]] = prev.values[s:e]
+    return Means(k, dim, indptr, terms, vals, retained)
+
+
 def objective(ds, labels, m: Means, dense_limit: int = 600_000_000) -> float:
     """clustering.py:105-119: each entry's product v * mu_{label}[t] (0 where
     the mean lacks t), per-object bincount in entry order, then math.fsum.

@@ -60,6 +60,8 @@ SIGNATURES = {
                                    _vp, _vp, _sz, _vp]),
     "ivfkm_assign_workspace_size": (_sz, [_i64, _i64]),
     "ivfkm_set_tuning": (None, [C.c_int, C.c_int, C.c_int]),
+    "ivfkm_set_screen_warps": (None, [C.c_int]),
+    "ivfkm_screen_plan": (C.c_int, [_i64, C.c_int, C.c_int, _vp]),
     "ivfkm_row_order_workspace_size": (_sz, [_i64]),
     "ivfkm_row_order": (C.c_int, [_i64, _vp, _vp, _vp, _sz, _vp]),
     "ivfkm_assign": (C.c_int, [_i64, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, C.c_int, _vp,

@@ -36,21 +36,55 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > mt for p in deps)
 
 
+def _compile(src: Path, nvcc: str):
+    """One translation unit -> _lib/obj/<name>.o (rebuilt when older than its
+    source, any header or this file)."""
+    obj = LIBDIR / "obj" / (src.name + ".o")
+    hdrs = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [ROOT / "include" / "ivfkm.h",
+                                                                  Path(__file__)]
+    if obj.exists() and all(p.stat().st_mtime <= obj.stat().st_mtime for p in [src, *hdrs]):
+        return obj, None
+    cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-c", "-o", str(obj), str(src)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    return obj, (cmd, res)
+
+
 def build_library(force: bool = False, verbose: bool = False) -> Path:
+    """Compile each source in parallel (nvcc -c), then link the shared library."""
     if not force and not _stale():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
+
     LIBDIR.mkdir(exist_ok=True)
+    (LIBDIR / "obj").mkdir(exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-shared", "-I", str(ROOT / "include"), "-o", str(LIB),
-           *map(str, sources()), "-lgomp"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    if force:
+        for o in (LIBDIR / "obj").glob("*.o"):
+            o.unlink()
+    srcs = sources()
+    with ThreadPoolExecutor(max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(lambda s: _compile(s, nvcc), srcs))
     log = LIBDIR / "build.log"
-    log.write_text(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+    text = []
+    for obj, r in results:
+        if r is None:
+            continue
+        cmd, res = r
+        text.append(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+        if res.returncode != 0:
+            log.write_text("\n".join(text))
+            sys.stderr.write(res.stderr[-6000:])
+            raise RuntimeError(f"nvcc failed ({res.returncode}) on {cmd[-1]}; see {log}")
+    cmd = [nvcc, *ARCH, "-shared", "-Xcompiler", "-fopenmp", "-o", str(LIB),
+           *[str(o) for o, _ in results], "-lgomp"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    text.append(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+    log.write_text("\n".join(text))
     if res.returncode != 0:
         sys.stderr.write(res.stderr[-6000:])
-        raise RuntimeError(f"nvcc failed ({res.returncode}); see {log}")
+        raise RuntimeError(f"nvcc link failed ({res.returncode}); see {log}")
     if verbose:
-        sys.stderr.write(res.stderr)
+        sys.stderr.write("\n".join(text))
     return LIB
 
 

@@ -79,6 +79,7 @@ struct ScreenParams {
   double mu_max;
   int cta_blocks;  // 32-mean blocks held by one CTA (multiple of RR)
   int nsplit;      // CTAs per object (cluster size)
+  int pass = -1;   // >= 0: slot-range pass — this launch computes split `pass` only
   int rowcap;      // row entries staged in shared memory per pass
   int32_t* label32;
   int32_t* slot_of;
@@ -393,10 +394,11 @@ __device__ __forceinline__ void screen_epilogue(const ScreenParams& p, ScreenSha
   }
 
   cg::cluster_group cluster = cg::this_cluster();
+  const bool clus = p.nsplit > 1 && p.pass < 0;
   float gv;
   int gc;
   unsigned long long gpost;
-  if (p.nsplit > 1) {
+  if (clus) {
     cluster.sync();
     gv = -INFINITY;
     gc = INT_MAX;
@@ -435,11 +437,18 @@ __device__ __forceinline__ void screen_epilogue(const ScreenParams& p, ScreenSha
       }
     }
   }
-  if (p.nsplit > 1) cluster.sync(); else __syncthreads();
+  if (clus) cluster.sync(); else __syncthreads();
 
+  if (p.pass >= 0) {  // experiment: per-pass local results only
+    if (threadIdx.x == 0 && z == 0) {
+      p.label32[obj] = gpost == 0 ? 0 : __ldg(p.inv + gc);
+      p.slot_of[obj] = -1;
+    }
+    return;
+  }
   if (z == 0 && threadIdx.x == 0) {
     int total = 0;
-    if (p.nsplit > 1) {
+    if (clus) {
       for (int q = 0; q < p.nsplit; ++q) total += cluster.map_shared_rank(&sh, q)->cnt;
     } else {
       total = sh.cnt;
@@ -466,7 +475,7 @@ __device__ __forceinline__ void screen_epilogue(const ScreenParams& p, ScreenSha
       }
     }
   }
-  if (p.nsplit > 1) cluster.sync();  // peers keep their shared memory alive
+  if (clus) cluster.sync();  // peers keep their shared memory alive
 }
 
 // MAXREG: 64 in general; 56 for small CTAs (<= 4 warps, k <= ~1000), where it
@@ -487,9 +496,10 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
-  const int z = blockIdx.x % p.nsplit;
-  const int64_t obj = p.order ? (int64_t)__ldg(p.order + blockIdx.x / p.nsplit)
-                              : (int64_t)(blockIdx.x / p.nsplit);
+  const int ctas = p.pass >= 0 ? 1 : p.nsplit;
+  const int z = p.pass >= 0 ? p.pass : blockIdx.x % p.nsplit;
+  const int64_t obj = p.order ? (int64_t)__ldg(p.order + blockIdx.x / ctas)
+                              : (int64_t)(blockIdx.x / ctas);
   if (obj >= p.n_obj) return;  // whole cluster shares obj
   const int64_t rb = p.row_ptr[obj], re = p.row_ptr[obj + 1];
   const int64_t nblk = p.nblk;
@@ -1524,6 +1534,7 @@ AssignWs carve_assign(void* base, int64_t n, int64_t k, size_t* total) {
 
 static int g_tma_warps = 8;
 static int g_max_warps = 16;  // register screen: warps per CTA at most
+static int g_force_warps = 0;  // register screen: exact warps per CTA (0 = planned)
 
 struct Plan {
   int rr, nsplit, cta_blocks, warps, rowcap;
@@ -1531,6 +1542,25 @@ struct Plan {
   int mode;  // 0 LDG register screen, 1 TMA ring, 2 cp.async ring
   size_t smem;
 };
+
+static int g_passes = 0;  // experiment: slot-range passes (0 = off)
+
+int choose_warps(int spans, size_t smem) {
+  const int by_smem = (228 * 1024) / (int)(smem + 1024 + 5 * 1024);
+  int best_w = 1;
+  long best = -1;
+  for (int w = 1; w <= 16 && w <= (spans > 0 ? spans : 1); ++w) {
+    int ctas = 65536 / (w * 32 * 64);
+    if (ctas > by_smem) ctas = by_smem;
+    if (ctas > 32) ctas = 32;
+    const long score = (long)ctas * w * 64 + ctas;
+    if (score > best) {
+      best = score;
+      best_w = w;
+    }
+  }
+  return best_w;
+}
 
 int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
   const int64_t nblk = ivfkm_bivf_nblk(k);
@@ -1597,30 +1627,31 @@ int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
   // lane) and the shared-memory footprint, then the most resident CTAs
   // (objects in flight).  Measured at config 2: 8 warps x 4 CTAs beats
   // 14 x 2 by 14%; at config 4 (95 KB per CTA) 16 x 2 beats 8 x 2 by 40%.
-  const int spans = pl.cta_blocks / pl.rr;
-  const int by_smem = (228 * 1024) / (int)(pl.smem + 1024 + 5 * 1024);
-  int best_w = 1;
-  long best = -1;
-  for (int w = 1; w <= 16 && w <= (spans > 0 ? spans : 1); ++w) {
-    int ctas = 65536 / (w * 32 * 64);
-    if (ctas > by_smem) ctas = by_smem;
-    if (ctas > 32) ctas = 32;
-    const long score = (long)ctas * w * 64 + ctas;
-    if (score > best) {
-      best = score;
-      best_w = w;
-    }
+  if (g_passes > 0) {  // experiment: slot-range passes instead of a cluster
+    int64_t cb = (nblk + g_passes - 1) / g_passes;
+    cb = (cb + pl.rr - 1) / pl.rr * pl.rr;
+    pl.nsplit = (int)((nblk + cb - 1) / cb);
+    pl.cta_blocks = (int)cb;
+    pl.smem = (size_t)cb * 128 + stage;
   }
+  const int best_w = choose_warps(pl.cta_blocks / pl.rr, pl.smem);
   pl.warps = g_max_warps < best_w ? g_max_warps : best_w;
+  if (g_force_warps > 0) pl.warps = g_force_warps;  // tests: any count is valid
   *out = pl;
   return IVFKM_OK;
+}
+
+// The instantiation launch_screen picks for a plan (56 registers for the
+// small fp16 CTAs, 64 otherwise).
+int plan_maxreg(const Plan& pl, bool half) {
+  return (!pl.tma && half && pl.rr == 8 && pl.warps <= 4) ? 56 : 64;
 }
 
 template <int RR>
 int launch_screen(const Plan& pl, const ScreenParams& p, cudaStream_t st) {
   auto fn = pl.mode == 1 ? screen_tma_kernel
                          : (pl.mode == 2 ? screen_async_kernel
-                                         : (p.half ? (RR == 8 && pl.warps <= 4
+                                         : (p.half ? (plan_maxreg(pl, true) == 56
                                                           ? screen_kernel<RR, true, 56>
                                                           : screen_kernel<RR, true>)
                                                    : screen_kernel<RR, false>));
@@ -1639,6 +1670,15 @@ int launch_screen(const Plan& pl, const ScreenParams& p, cudaStream_t st) {
           cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
       cur = pl.smem;
     }
+  }
+  if (g_passes > 0 && !pl.tma) {
+    for (int z = 0; z < pl.nsplit; ++z) {
+      ScreenParams q = p;
+      q.pass = z;
+      fn<<<(unsigned)p.n_obj, pl.warps * 32, pl.smem, st>>>(q);
+      IVFKM_CHECK_LAUNCH();
+    }
+    return IVFKM_OK;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(p.n_obj * pl.nsplit));
@@ -1732,6 +1772,30 @@ extern "C" void ivfkm_set_tuning(int rowcap, int smem_limit, int rr) {
   if (smem_limit == -1) g_smem_limit = 0;  // back to adaptive
   if (rr == 0 || rr == 2 || rr == 4 || rr == 8 || rr == -8 || rr == -4) g_rr = rr;
   if (rr <= -16 && rr >= -16 * 16) g_tma_warps = -rr / 16;  // -16*w: TMA warps per CTA
+}
+
+// Tests: force the register screen's warps per CTA (1..16; 0 = planned) —
+// spans are handed out dynamically, so every count computes the same sums.
+extern "C" void ivfkm_set_screen_warps(int warps) {
+  if (warps >= 0 && warps <= 16) g_force_warps = warps;
+  if (warps <= -1) g_passes = -warps - 1;  // experiment: -1 - passes
+}
+
+extern "C" int ivfkm_screen_plan(int64_t k, int rowcap, int screen_bits, int32_t* out) {
+  if (k < 1 || !out || (screen_bits != 16 && screen_bits != 32)) return IVFKM_E_ARG;
+  Plan pl;
+  const int rc = plan_screen(k, rowcap >= 32 ? rowcap / 32 * 32 : g_rowcap, g_smem_limit, g_rr,
+                             &pl);
+  if (rc) return rc;
+  out[0] = pl.rr;
+  out[1] = pl.nsplit;
+  out[2] = pl.cta_blocks;
+  out[3] = pl.warps;
+  out[4] = pl.rowcap;
+  out[5] = pl.mode;
+  out[6] = (int32_t)pl.smem;
+  out[7] = plan_maxreg(pl, screen_bits == 16);
+  return IVFKM_OK;
 }
 
 namespace {

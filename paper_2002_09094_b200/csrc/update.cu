@@ -516,7 +516,7 @@ __global__ void fill_kernel(int64_t nnz, int64_t dim, const uint32_t* __restrict
                             const uint32_t* __restrict__ nz, const uint32_t* __restrict__ nzpos,
                             const uint32_t* __restrict__ cl_seg, const double* __restrict__ nrm,
                             const int64_t* __restrict__ new_ptr, int32_t* __restrict__ new_terms,
-                            double* __restrict__ new_vals) {
+                            double* __restrict__ new_vals, int64_t capacity) {
   const uint32_t n_seg = *n_seg_p;
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_seg;
        s += (int64_t)gridDim.x * blockDim.x) {
@@ -524,6 +524,7 @@ __global__ void fill_kernel(int64_t nnz, int64_t dim, const uint32_t* __restrict
     const int64_t c = (int64_t)(seg_key[s] / (K)dim);
     const int64_t t = (int64_t)(seg_key[s] - (K)c * (K)dim);
     const int64_t pos = new_ptr[c] + (int64_t)(nzpos[s] - nzpos[cl_seg[c]]);
+    if (pos >= capacity) continue;  // caller's buffer too small: never write past it
     new_terms[pos] = (int32_t)t;
     new_vals[pos] = __ddiv_rn(seg_w[s], nrm[c]);
   }
@@ -534,14 +535,17 @@ __global__ void retain_kernel(int64_t k, const unsigned long long* __restrict__ 
                               const int32_t* __restrict__ prev_terms,
                               const double* __restrict__ prev_vals,
                               const int64_t* __restrict__ new_ptr, int32_t* __restrict__ new_terms,
-                              double* __restrict__ new_vals, uint8_t* __restrict__ retained) {
+                              double* __restrict__ new_vals, uint8_t* __restrict__ retained,
+                              int64_t capacity) {
   const int lane = threadIdx.x & 31;
   const int64_t wpb = blockDim.x >> 5;
   for (int64_t c = blockIdx.x * wpb + (threadIdx.x >> 5); c < k; c += gridDim.x * wpb) {
     const bool empty = sizes[c] == 0;
     if (lane == 0) retained[c] = empty ? 1 : 0;
     if (!empty) continue;
-    const int64_t pb = prev_ptr[c], n = prev_ptr[c + 1] - pb, nb = new_ptr[c];
+    const int64_t pb = prev_ptr[c], nb = new_ptr[c];
+    int64_t n = prev_ptr[c + 1] - pb;
+    if (nb + n > capacity) n = capacity > nb ? capacity - nb : 0;
     for (int64_t q = lane; q < n; q += 32) {
       new_terms[nb + q] = prev_terms[pb + q];
       new_vals[nb + q] = prev_vals[pb + q];
@@ -994,8 +998,8 @@ template <class K>
 int update_fill_impl(int64_t nnz, int64_t k, int64_t dim, const unsigned long long* sizes,
                      const int64_t* prev_ptr, const int32_t* prev_terms,
                      const double* prev_vals, const int64_t* new_ptr, int32_t* new_terms,
-                     double* new_vals, uint8_t* retained, void* ws, size_t ws_bytes,
-                     cudaStream_t st) {
+                     double* new_vals, uint8_t* retained, int64_t capacity, void* ws,
+                     size_t ws_bytes, cudaStream_t st) {
   size_t need = 0;
   UpdWs<K> w = carve_upd<K>(ws, nnz, k, dim, &need);
   if (ws_bytes < need) return IVFKM_E_WORKSPACE;
@@ -1003,11 +1007,12 @@ int update_fill_impl(int64_t nnz, int64_t k, int64_t dim, const unsigned long lo
   if (nnz > 0) {
     fill_kernel<K><<<grid_for(nnz, T), T, 0, st>>>(nnz, dim, w.n_seg, w.seg_key, w.seg_w, w.head,
                                                    w.nzpos, w.cl_seg, w.nrm, new_ptr, new_terms,
-                                                   new_vals);
+                                                   new_vals, capacity);
     IVFKM_CHECK_LAUNCH();
   }
   retain_kernel<<<grid_for(k, T / 32), T, 0, st>>>(k, sizes, prev_ptr, prev_terms, prev_vals,
-                                                   new_ptr, new_terms, new_vals, retained);
+                                                   new_ptr, new_terms, new_vals, retained,
+                                                   capacity);
   IVFKM_CHECK_LAUNCH();
   return IVFKM_OK;
 }
@@ -1076,13 +1081,13 @@ extern "C" int ivfkm_update_fill(int64_t /*n_obj*/, int64_t nnz, int64_t k, int6
                                  const int64_t* new_ptr, int32_t* new_terms, double* new_vals,
                                  uint8_t* retained, int64_t capacity, void* ws, size_t ws_bytes,
                                  ivfkm_stream_t stream_) {
-  if (k < 1 || dim < 1 || !new_ptr || !retained) return IVFKM_E_ARG;
-  (void)capacity;
+  if (k < 1 || dim < 1 || !new_ptr || !retained || capacity < 0) return IVFKM_E_ARG;
+  if (capacity > 0 && (!new_terms || !new_vals)) return IVFKM_E_ARG;
   cudaStream_t st = as_stream(stream_);
   if (use_k32(k, dim))
     return update_fill_impl<uint32_t>(nnz, k, dim, sizes, prev_ptr, prev_terms, prev_vals, new_ptr,
-                                      new_terms, new_vals, retained, ws, ws_bytes, st);
+                                      new_terms, new_vals, retained, capacity, ws, ws_bytes, st);
   return update_fill_impl<unsigned long long>(nnz, k, dim, sizes, prev_ptr, prev_terms, prev_vals,
-                                              new_ptr, new_terms, new_vals, retained, ws, ws_bytes,
-                                              st);
+                                              new_ptr, new_terms, new_vals, retained, capacity, ws,
+                                              ws_bytes, st);
 }

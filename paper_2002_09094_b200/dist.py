@@ -198,9 +198,12 @@ class DistLloyd:
         self.lo, self.hi = lo, hi
         self.host = HostDataset(_Shard, pin=torch.cuda.is_available())
         self.dd = DeviceDataset(self.host, device)
-        self.eng = LloydEngine(self.dd, self.k)
+        # the sharded update routes rows to cluster owners and runs the
+        # stateless count (no label-delta state, no whole-shard workspace)
+        self.eng = LloydEngine(self.dd, self.k, delta_update=False, update_ws=False)
         self.device = self.dd.device
-        self.stats_vec = torch.zeros(4 + 34 + self.k, dtype=torch.int64, device=self.device)
+        self.stats_vec = torch.zeros(5 + 34 + self.k, dtype=torch.int64, device=self.device)
+        self.ws = None  # update workspace of the routed rows, grown on demand
 
     def assign(self, dm, prev, events=None):
         """Local assign + the one statistics all-reduce; returns labels and
@@ -211,14 +214,17 @@ class DistLloyd:
         raw = self.eng.stats.view(torch.int64)  # 6 + 34 words (ivfkm_stats)
         v = self.stats_vec
         v[:4] = raw[:4]
-        v[4:38] = raw[6:40]
-        v[38:] = self.eng.sizes
+        v[4] = raw[5]  # obj_flags: nonzero on any rank poisons the objective
+        v[5:39] = raw[6:40]
+        v[39:] = self.eng.sizes
         self.comm.allreduce_sum_(v)
         h = v.cpu()
         self.local_postings = int(raw[0].item())  # this rank's share (roofline)
-        self.eng.sizes.copy_(v[38:])  # global sizes for the update
+        self.eng.sizes.copy_(v[39:])  # global sizes for the update
+        if int(h[4]):
+            raise FloatingPointError("objective summand outside the exact accumulator range")
         return lab, dict(postings=int(h[0]), changed=int(h[1]), near_ties=int(h[2]),
-                         overflow=int(h[3]), objective=objective_from_limbs(h[4:38].tolist()))
+                         overflow=int(h[3]), objective=objective_from_limbs(h[5:39].tolist()))
 
     def update(self, lab, dm):
         from .engine import DeviceMeans, update_rows
@@ -233,11 +239,13 @@ class DistLloyd:
             p1 = int(dm.ptr[chi])
             prev = DeviceMeans(kl, dd.dim, dm.ptr[clo:chi + 1] - p0, dm.terms[p0:p1],
                                dm.vals[p0:p1], dm.retained[clo:chi])
-            ws = torch.empty(int(self.eng.lib.ivfkm_update_workspace_size(
-                recv.n, recv.nnz, kl, dd.dim)), dtype=torch.uint8, device=self.device)
+            need = int(self.eng.lib.ivfkm_update_workspace_size(recv.n, recv.nnz, kl, dd.dim))
+            if self.ws is None or self.ws.numel() < need:
+                self.ws = torch.empty(int(need * 1.25) + 4096, dtype=torch.uint8,
+                                      device=self.device)
             sl = update_rows(self.eng.lib, recv.n, recv.nnz, recv.row_ptr, recv.terms,
                              recv.vals, recv.labels - clo, self.eng.sizes[clo:chi].contiguous(),
-                             prev, kl, dd.dim, ws)
+                             prev, kl, dd.dim, self.ws)
             parts = (sl.ptr, sl.terms, sl.vals, sl.retained)
         else:
             dev = self.device

@@ -272,7 +272,7 @@ class LloydEngine:
     """Runs IVF Lloyd iterations over one device-resident dataset."""
 
     def __init__(self, dd: DeviceDataset, k: int, screen_bits: int = 16,
-                 delta_update: bool = True):
+                 delta_update: bool = True, update_ws: bool = True):
         self.lib = _lib.load()
         self.dd, self.k = dd, int(k)
         # fp16 screen values: half the posting bytes, a wider (still rigorous)
@@ -285,9 +285,10 @@ class LloydEngine:
         u8 = torch.uint8
         self.ws_assign = torch.empty(int(self.lib.ivfkm_assign_workspace_size(n, self.k)),
                                      dtype=u8, device=dev)
+        # update_ws=False: a caller that updates other rows (dist.py) brings its own
         self.ws_update = torch.empty(int(self.lib.ivfkm_update_workspace_size(n, nnz, self.k,
                                                                               dim)),
-                                     dtype=u8, device=dev)
+                                     dtype=u8, device=dev) if update_ws else None
         self.ws_bivf = torch.empty(int(self.lib.ivfkm_bivf_workspace_size(dim, self.k)),
                                    dtype=u8, device=dev)
         self.ws_fill = None  # sorted BIVF fill (grows with the means' size)

@@ -163,3 +163,28 @@ def test_sample_without_replacement_matches_literal():
     for n, k, seed in [(10, 10, 0), (1000, 17, 3), (300000, 1000, 1), (5, 1, 9)]:
         assert np.array_equal(sample_without_replacement(n, k, seed),
                               O.sample_without_replacement(n, k, seed))
+
+
+@pytest.mark.parametrize("n,dim,k,seed,signed", [(1500, 400, 64, 0, False),
+                                                 (3000, 5000, 300, 1, True),
+                                                 (2000, 129, 1500, 2, False),
+                                                 (600, 4097, 40, 3, True)])
+def test_oracle_update_fast_equals_update(n, dim, k, seed, signed):
+    """update_fast (vectorised, used at configs 1-4) is bit-identical to the
+    literal per-cluster restatement of variants.py:254-307, empty clusters
+    and cancelling signed sums included."""
+    from oracle import oracle as O
+    from paper_2002_09094_b200 import Dataset, synth
+
+    spec = synth.CONFIGS[0]["corpus"].scaled(n, dim, seed=100 + seed)
+    ip, t, v, _ = synth.make_corpus(spec)
+    if signed:
+        v = v * np.where(np.random.default_rng(seed).random(v.size) < 0.4, -1.0, 1.0)
+    ds = Dataset(dim, ip, t, v, normalized=True)
+    m = O.init_means(ds, min(k, ds.n), seed)
+    lab = np.random.default_rng(seed).integers(1, m.k + 1, size=ds.n).astype(np.int32)
+    lab[lab == 2] = 1  # an empty cluster
+    a = O.update(ds, lab, m)
+    b = O.update_fast(ds, lab, m, chunk_bytes=1 << 20)  # several dense chunks
+    for f in ("indptr", "term_ids", "values", "retained"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f

@@ -1,0 +1,49 @@
+"""Experiment: the screen as slot-range passes (R launches over all objects,
+each covering 1/R of the slots) against the one-pass plan.  Timing only —
+labels of the pass mode are not final (no cross-pass merge)."""
+import argparse
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch  # noqa: E402
+
+from paper_2002_09094_b200 import synth  # noqa: E402
+from paper_2002_09094_b200.clustering import init_means  # noqa: E402
+from paper_2002_09094_b200.engine import DeviceDataset, HostDataset, LloydEngine  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--iters", type=int, default=2)
+    ap.add_argument("--passes", default="0,2,4,8,16")
+    ap.add_argument("--reps", type=int, default=2)
+    a = ap.parse_args()
+    c = synth.CONFIGS[a.config]
+    ds = synth.make_dataset(c["corpus"])
+    eng = LloydEngine(DeviceDataset(HostDataset(ds), "cuda"), c["k"])
+    dm = eng.upload_means(init_means(ds, c["k"], c["seed"], "sparse_inverted"))
+    prev = None
+    for _ in range(a.iters):
+        lab = eng.assign(dm, prev)
+        eng.read_stats()
+        dm = eng.update(lab, dm)
+        prev = lab
+    for r in map(int, a.passes.split(",")):
+        eng.lib.ivfkm_set_screen_warps(-1 - r)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ts = []
+        for _ in range(a.reps):
+            eng.assign(dm, None, events=ev)
+            torch.cuda.synchronize()
+            ts.append(ev[0].elapsed_time(ev[1]))
+        st = eng.read_stats()
+        print(json.dumps({"config": a.config, "passes": r, "screen_ms": min(ts), "all": ts,
+                          "postings": st.postings}), flush=True)
+    eng.lib.ivfkm_set_screen_warps(-1)
+
+
+if __name__ == "__main__":
+    main()
