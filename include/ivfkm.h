@@ -155,6 +155,15 @@ void ivfkm_set_tuning(int rowcap, int smem_limit, int rr);
  * planned count).  Spans are handed out to warps dynamically, so every count
  * computes identical sums. */
 void ivfkm_set_screen_warps(int warps);
+/* Screen tuning: which = 1: slot-range passes for the next screens (0 or 1
+ * = one pass).  With P > 1 passes the fp16 register screen runs P launches,
+ * each over all objects and 1/P of the slots (one CTA per object, no
+ * cluster), merging each object's best value and near-tie candidates in a
+ * workspace state between launches; the candidate window — and so every
+ * result — equals the one-pass screen's.  Ignored under a forced shared-
+ * memory budget or a staged (TMA / cp.async) screen.  Returns IVFKM_E_ARG
+ * for an unknown `which`. */
+int ivfkm_set_screen_option(int which, int value);
 /* The screen plan ivfkm_assign_screen would use for k means under the
  * current tuning ([host] out[8]: span blocks RR, cluster CTAs per object,
  * 32-mean blocks per CTA, warps per CTA, staged row entries, mode (0 register

@@ -88,5 +88,30 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+CORPUS_LIB = ROOT / "tools" / "_build" / "libcorpus.so"
+
+
+def build_corpus_library(force: bool = False) -> Path:
+    """The seeded corpus generator alone (csrc/synth.cpp, host C++/OpenMP, no
+    CUDA): the reference arm of bench.py generates its inputs with it, so
+    the reference's process never maps libivfkm.so."""
+    src = CSRC / "synth.cpp"
+    if not force and CORPUS_LIB.exists() and CORPUS_LIB.stat().st_mtime >= src.stat().st_mtime:
+        return CORPUS_LIB
+    CORPUS_LIB.parent.mkdir(parents=True, exist_ok=True)
+    cxx = os.environ.get("CXX", "g++")
+    obj = CORPUS_LIB.with_suffix(".o")
+    res = subprocess.run([cxx, "-O3", "-std=c++17", "-fPIC", "-fopenmp", "-I",
+                          str(ROOT / "include"), "-c", "-o", str(obj), str(src)],
+                         capture_output=True, text=True)
+    if res.returncode == 0:
+        res = subprocess.run([cxx, "-shared", "-o", str(CORPUS_LIB), str(obj), "-l:libgomp.so.1"],
+                             capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stderr[-4000:])
+        raise RuntimeError("g++ failed on csrc/synth.cpp")
+    return CORPUS_LIB
+
+
 if __name__ == "__main__":
     print(build_library(force="--force" in sys.argv, verbose=True))

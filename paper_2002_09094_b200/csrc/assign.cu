@@ -79,7 +79,12 @@ struct ScreenParams {
   double mu_max;
   int cta_blocks;  // 32-mean blocks held by one CTA (multiple of RR)
   int nsplit;      // CTAs per object (cluster size)
-  int pass = -1;   // >= 0: slot-range pass — this launch computes split `pass` only
+  int pass = -1;   // >= 0: slot-range pass `pass` of npass (one CTA per object)
+  int npass = 0;
+  float* st_best;  // pass state per object: best screen value so far,
+  int32_t* st_slot;  // its slot,
+  int32_t* st_cnt;   // candidates kept (kMaxC + 1: overflow) | kHasPost,
+  int2* st_cand;     // [n][kMaxC] the candidates (slot, fp32 value bits)
   int rowcap;      // row entries staged in shared memory per pass
   int32_t* label32;
   int32_t* slot_of;
@@ -97,8 +102,14 @@ struct ScreenShared {
   int best_c;
   int cnt;
   int cand[kMaxC];
+  float cval[kMaxC];  // pass mode: the candidates' screen values
   unsigned long long post;
+  float pv;  // pass mode: state of the earlier passes
+  int pc, pn;
 };
+
+constexpr int kHasPost = 1 << 30;  // pass state: the object touches some posting
+constexpr int kCntMask = kHasPost - 1;
 
 __device__ __forceinline__ void better(float& bv, int& bc, float ov, int oc) {
   if (ov > bv || (ov == bv && oc < bc)) {
@@ -339,6 +350,106 @@ struct SpanVals<RR, true, F2> {
   }
 };
 
+// Half-width of the rigorous screen window of an object with n_i entries
+// (DESIGN.md §3): |rho_screen - rho_f64| <= eps for every mean.
+__device__ __forceinline__ double window_eps(const ScreenParams& p, int64_t obj, int64_t n_i) {
+  const double xn = p.xnorm ? p.xnorm[obj] : 1.0;
+  // fp16 screen values add a relative 2^-11 rounding per mean value plus an
+  // absolute 2^-25 below fp16's normal range (sum over h of |x_h| <= n*|x|)
+  return p.half ? (0x1p-11 + (double)(n_i + 4) * 0x1p-24) * xn * p.mu_max * (1.0 + 0x1p-9) +
+                      (double)n_i * xn * 0x1p-25 * (1.0 + 0x1p-9) + (double)(n_i + 1) * 0x1p-125
+                : ((double)(n_i + 3) * 0x1p-24 + (double)n_i * 0x1p-50) * xn * p.mu_max *
+                          (1.0 + 1e-6) +
+                      (double)(n_i + 1) * 0x1p-125;
+}
+
+// Slot-range pass epilogue: merge this pass's slots into the object's running
+// state — the best screen value so far and every slot within 2*eps of it.  A
+// slot kept at pass z satisfies rho >= best_z - 2 eps >= best_final - 2 eps,
+// and candidates are re-filtered against each new best, so after the last
+// pass the set is exactly the one-pass window (an overflow stays one: its
+// dropped values are unknown, and the overflow kernel rescores every mean).
+__device__ void pass_epilogue(const ScreenParams& p, ScreenShared& sh, const float* rho,
+                              int64_t obj, int z, int64_t n_i, float gv, int gc,
+                              unsigned long long gpost) {
+  const int cta_cids = p.cta_blocks * 32;
+  const int64_t cid0 = (int64_t)z * cta_cids;
+  if (threadIdx.x == 0) {
+    if (z > 0) {
+      sh.pv = p.st_best[obj];
+      sh.pc = p.st_slot[obj];
+      sh.pn = p.st_cnt[obj];
+    } else {
+      sh.pv = -INFINITY;
+      sh.pc = INT_MAX;
+      sh.pn = gpost ? kHasPost : 0;
+    }
+    sh.cnt = 0;
+  }
+  __syncthreads();
+  float bv = sh.pv;
+  int bc = sh.pc;
+  better(bv, bc, gv, gc);
+  const int pn = sh.pn;
+  const bool has = (pn & kHasPost) != 0;
+  const int prev = pn & kCntMask;
+  if (has) {
+    const double thr = (double)bv - 2.0 * window_eps(p, obj, n_i);
+    const int2* pc = p.st_cand + obj * kMaxC;
+    for (int j = threadIdx.x; j < (prev < kMaxC ? prev : kMaxC); j += blockDim.x) {
+      const int2 c = pc[j];
+      const float v = __int_as_float(c.y);
+      if ((double)v >= thr) {
+        const int s = atomicAdd(&sh.cnt, 1);
+        if (s < kMaxC) {
+          sh.cand[s] = c.x;
+          sh.cval[s] = v;
+        }
+      }
+    }
+    for (int j = threadIdx.x; j < cta_cids; j += blockDim.x) {
+      const int64_t cid = cid0 + j;
+      if (cid >= p.k) break;
+      const float v = rho[j];
+      if ((double)v >= thr) {
+        const int s = atomicAdd(&sh.cnt, 1);
+        if (s < kMaxC) {
+          sh.cand[s] = (int)cid;
+          sh.cval[s] = v;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  int total = sh.cnt;
+  if (prev > kMaxC && total <= kMaxC) total = kMaxC + 1;
+  if (z < p.npass - 1) {
+    if (threadIdx.x == 0) {
+      p.st_best[obj] = bv;
+      p.st_slot[obj] = bc;
+      p.st_cnt[obj] = (total < kMaxC + 1 ? total : kMaxC + 1) | (has ? kHasPost : 0);
+    }
+    for (int j = threadIdx.x; j < (total < kMaxC ? total : kMaxC); j += blockDim.x)
+      p.st_cand[obj * kMaxC + j] = make_int2(sh.cand[j], __float_as_int(sh.cval[j]));
+    return;
+  }
+  if (threadIdx.x == 0) {
+    p.label32[obj] = has ? __ldg(p.inv + bc) : 0;
+    if (total <= 1) {
+      p.slot_of[obj] = -1;
+    } else {
+      const int slot = (int)atomicAdd(&p.stats->queue_len, 1ull);
+      atomicAdd(&p.stats->near_ties, 1ull);
+      if (total > kMaxC) atomicAdd(&p.stats->overflow, 1ull);
+      p.slot_of[obj] = slot;
+      p.q_obj[slot] = (int)obj;
+      p.q_cnt[slot] = total;
+      const int w = total < kMaxC ? total : kMaxC;
+      for (int j = 0; j < w; ++j) p.q_cid[(int64_t)slot * kMaxC + j] = __ldg(p.inv + sh.cand[j]);
+    }
+  }
+}
+
 // CTA-local argmax (value desc, index asc) over the parked rho, merged over
 // the cluster through DSMEM when k is split; then the rigorous fp32 window and
 // the candidate queue for exact rescoring.  Every thread of the CTA calls it.
@@ -414,19 +525,13 @@ __device__ __forceinline__ void screen_epilogue(const ScreenParams& p, ScreenSha
     gc = sh.best_c;
     gpost = sh.post;
   }
+  if (p.pass >= 0) {
+    pass_epilogue(p, sh, rho, obj, z, re - rb, gv, gc, gpost);
+    return;
+  }
 
   // ---- rigorous fp32 window and candidate collection ----
-  const int64_t n_i = re - rb;
-  const double xn = p.xnorm ? p.xnorm[obj] : 1.0;
-  // fp16 screen values add a relative 2^-11 rounding per mean value plus an
-  // absolute 2^-25 below fp16's normal range (sum over h of |x_h| <= n*|x|)
-  const double eps =
-      p.half ? (0x1p-11 + (double)(n_i + 4) * 0x1p-24) * xn * p.mu_max * (1.0 + 0x1p-9) +
-                   (double)n_i * xn * 0x1p-25 * (1.0 + 0x1p-9) + (double)(n_i + 1) * 0x1p-125
-             : ((double)(n_i + 3) * 0x1p-24 + (double)n_i * 0x1p-50) * xn * p.mu_max *
-                       (1.0 + 1e-6) +
-                   (double)(n_i + 1) * 0x1p-125;
-  const double thr = (double)gv - 2.0 * eps;
+  const double thr = (double)gv - 2.0 * window_eps(p, obj, re - rb);
   if (gpost != 0) {
     for (int j = threadIdx.x; j < cta_cids; j += blockDim.x) {
       const int64_t cid = cid0 + j;
@@ -439,13 +544,6 @@ __device__ __forceinline__ void screen_epilogue(const ScreenParams& p, ScreenSha
   }
   if (clus) cluster.sync(); else __syncthreads();
 
-  if (p.pass >= 0) {  // experiment: per-pass local results only
-    if (threadIdx.x == 0 && z == 0) {
-      p.label32[obj] = gpost == 0 ? 0 : __ldg(p.inv + gc);
-      p.slot_of[obj] = -1;
-    }
-    return;
-  }
   if (z == 0 && threadIdx.x == 0) {
     int total = 0;
     if (clus) {
@@ -1508,6 +1606,10 @@ struct AssignWs {
   unsigned int* ovf_len;
   unsigned int* cl_pos;  // k + 1: objects per screen winner, then their cursors
   int32_t* fin_order;    // n: objects grouped by screen winner
+  float* st_best;        // slot-range pass state (ScreenParams)
+  int32_t* st_slot;
+  int32_t* st_cnt;
+  int2* st_cand;
   void* cub;
   size_t cub_bytes;
 };
@@ -1524,6 +1626,10 @@ AssignWs carve_assign(void* base, int64_t n, int64_t k, size_t* total) {
   w.ovf_len = c.take<unsigned int>(4);
   w.cl_pos = c.take<unsigned int>((size_t)k + 1);
   w.fin_order = c.take<int32_t>(n);
+  w.st_best = c.take<float>(n);
+  w.st_slot = c.take<int32_t>(n);
+  w.st_cnt = c.take<int32_t>(n);
+  w.st_cand = c.take<int2>((size_t)n * kMaxC);
   w.cub_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, w.cub_bytes, (unsigned int*)nullptr,
                                 (unsigned int*)nullptr, (int)(k + 1));
@@ -1538,12 +1644,13 @@ static int g_force_warps = 0;  // register screen: exact warps per CTA (0 = plan
 
 struct Plan {
   int rr, nsplit, cta_blocks, warps, rowcap;
+  bool passes = false;  // nsplit slot-range passes instead of a cluster of nsplit CTAs
   bool tma;
   int mode;  // 0 LDG register screen, 1 TMA ring, 2 cp.async ring
   size_t smem;
 };
 
-static int g_passes = 0;  // experiment: slot-range passes (0 = off)
+static int g_passes = 0;  // slot-range passes (0/1 = off; set per launch by the engine)
 
 int choose_warps(int spans, size_t smem) {
   const int by_smem = (228 * 1024) / (int)(smem + 1024 + 5 * 1024);
@@ -1565,6 +1672,7 @@ int choose_warps(int spans, size_t smem) {
 int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
   const int64_t nblk = ivfkm_bivf_nblk(k);
   Plan pl;
+  const bool adaptive = smem_limit <= 0;
   if (smem_limit <= 0) {
     // Adaptive budget (measured on configs 1-4): one CTA per object while rho
     // and the staged row fit in 64 KB (k <= ~13,000: every split CTA would
@@ -1627,12 +1735,16 @@ int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
   // lane) and the shared-memory footprint, then the most resident CTAs
   // (objects in flight).  Measured at config 2: 8 warps x 4 CTAs beats
   // 14 x 2 by 14%; at config 4 (95 KB per CTA) 16 x 2 beats 8 x 2 by 40%.
-  if (g_passes > 0) {  // experiment: slot-range passes instead of a cluster
+  if (g_passes > 1 && adaptive && rr >= 0) {
+    // slot-range passes: every launch screens all objects
+    // against 1/passes of the slots, so a pass's postings share the L2 and
+    // small CTAs (<= 4 warps, 56 registers) keep more objects in flight
     int64_t cb = (nblk + g_passes - 1) / g_passes;
     cb = (cb + pl.rr - 1) / pl.rr * pl.rr;
     pl.nsplit = (int)((nblk + cb - 1) / cb);
     pl.cta_blocks = (int)cb;
     pl.smem = (size_t)cb * 128 + stage;
+    pl.passes = pl.nsplit > 1;
   }
   const int best_w = choose_warps(pl.cta_blocks / pl.rr, pl.smem);
   pl.warps = g_max_warps < best_w ? g_max_warps : best_w;
@@ -1671,10 +1783,11 @@ int launch_screen(const Plan& pl, const ScreenParams& p, cudaStream_t st) {
       cur = pl.smem;
     }
   }
-  if (g_passes > 0 && !pl.tma) {
+  if (pl.passes) {  // slot-range passes: one launch per pass, state in between
     for (int z = 0; z < pl.nsplit; ++z) {
       ScreenParams q = p;
       q.pass = z;
+      q.npass = pl.nsplit;
       fn<<<(unsigned)p.n_obj, pl.warps * 32, pl.smem, st>>>(q);
       IVFKM_CHECK_LAUNCH();
     }
@@ -1778,7 +1891,13 @@ extern "C" void ivfkm_set_tuning(int rowcap, int smem_limit, int rr) {
 // spans are handed out dynamically, so every count computes the same sums.
 extern "C" void ivfkm_set_screen_warps(int warps) {
   if (warps >= 0 && warps <= 16) g_force_warps = warps;
-  if (warps <= -1) g_passes = -warps - 1;  // experiment: -1 - passes
+}
+
+extern "C" int ivfkm_set_screen_option(int which, int value) {
+  switch (which) {
+    case 1: g_passes = value < 0 ? 0 : (value > 4096 ? 4096 : value); return IVFKM_OK;
+    default: return IVFKM_E_ARG;
+  }
 }
 
 extern "C" int ivfkm_screen_plan(int64_t k, int rowcap, int screen_bits, int32_t* out) {
@@ -1848,6 +1967,10 @@ int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
   sp.q_cnt = w.q_cnt;
   sp.q_cid = w.q_cid;
   sp.stats = a.stats;
+  sp.st_best = w.st_best;
+  sp.st_slot = w.st_slot;
+  sp.st_cnt = w.st_cnt;
+  sp.st_cand = w.st_cand;
   if (pl.tma) return launch_screen<8>(pl, sp, st);
   switch (pl.rr) {
     case 8: return launch_screen<8>(pl, sp, st);

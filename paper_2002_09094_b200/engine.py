@@ -318,6 +318,11 @@ class LloydEngine:
         self.rowcap = max(32, min(512, (dd.max_row + 31) // 32 * 32))
         self.order = self._row_order(dd)
         self.launches = 0  # our kernels launched (for the bench's gpu_launches)
+        # slot-range passes of the screen: None = planned from the last
+        # iteration's postings (screen_passes), an int forces a count (1 = off)
+        self.passes = None
+        self.last_postings = None
+        self._doc_freq = None
 
     def _row_order(self, dd):
         """Longest rows first (computed once per dataset, on the device)."""
@@ -384,6 +389,33 @@ class LloydEngine:
         return self.build_bivf(DeviceMeans.from_meanset(ms, self.device))
 
     # -- assign --------------------------------------------------------------
+    # postings per object and pass that amortise a pass's per-object cost
+    # (row staging, epilogue, state merge); measured on configs 2-4
+    PASS_WORK = 90_000
+
+    def screen_passes(self, dm: DeviceMeans) -> int:
+        """Slot-range passes for the fp16 screen at large k:
+        enough 256-slot spans per pass that an object's pass does about
+        PASS_WORK postings, from the previous iteration's V (or, before the
+        first, V = sum_t no_t * nc_t from the BIVF headers)."""
+        if self.passes is not None:
+            return int(self.passes)
+        spans = self.nblk // 8
+        if self.screen_bits != 16 or spans < 16 or self.dd.n == 0:
+            return 1
+        v = self.last_postings
+        if v is None:
+            if self._doc_freq is None:
+                self._doc_freq = torch.bincount(self.dd.terms.long(),
+                                                minlength=self.dd.dim).to(torch.float64)
+            nh = self.dd.dim * self.nblk
+            nc = dm.headers[2 * nh + 1:2 * nh + 1 + self.dd.dim].to(torch.float64)
+            v = float(torch.dot(self._doc_freq, nc).item())
+        w = max(v / (self.dd.n * spans), 1.0)  # postings per (object, span)
+        per = max(2, int(np.ceil(self.PASS_WORK / w)))
+        p = int(np.ceil(spans / per))
+        return p if p > 1 else 1
+
     def assign(self, dm: DeviceMeans, prev: torch.Tensor | None, events=None,
                rule: int = 0) -> torch.Tensor:
         """Launch the assignment step; returns the (device) 0-based labels.
@@ -399,6 +431,8 @@ class LloydEngine:
             self.cur ^= 1
             out = self.labels[self.cur]
         self.lib.ivfkm_set_tuning(self.rowcap, 0, -1)
+        npass = self.screen_passes(dm)
+        _lib.check(self.lib.ivfkm_set_screen_option(1, npass), "ivfkm_set_screen_option")
         order = self.order if self.order is not None and dd.n == self.order.numel() else None
         st = _stream()
         if events is not None:
@@ -409,6 +443,7 @@ class LloydEngine:
                                           _p(order),
                                           _p(self.ws_assign), self.ws_assign.numel(), st)
         _lib.check(rc, "ivfkm_assign_screen")
+        self.launches += npass - 1
         if events is not None:
             events[1].record()
         if self.rankdir is not None:
@@ -449,7 +484,9 @@ class LloydEngine:
 
     def stats_ready(self) -> IterStats:
         raw = _lib.Stats.from_buffer_copy(self.stats_host.numpy().tobytes())
-        return IterStats.from_raw(raw)
+        st = IterStats.from_raw(raw)
+        self.last_postings = st.postings
+        return st
 
     # -- update --------------------------------------------------------------
     def update(self, labels0: torch.Tensor, dm: DeviceMeans) -> DeviceMeans:

@@ -69,9 +69,32 @@ def config_spec(index: int) -> dict:
     return CONFIGS[index]
 
 
-def make_corpus(spec: CorpusSpec):
-    """(indptr int64[N+1], term_ids int32 1-based, values float64, n dropped rows)."""
-    lib = _lib.load()
+_corpus = None
+
+
+def corpus_lib():
+    """The generator alone (tools/_build/libcorpus.so: csrc/synth.cpp without
+    CUDA) — for processes that must not map libivfkm.so (bench.py's
+    reference arm).  Same code, same output."""
+    global _corpus
+    if _corpus is None:
+        from .build import CORPUS_LIB, build_corpus_library
+
+        if not CORPUS_LIB.exists():
+            build_corpus_library()
+        lib = C.CDLL(str(CORPUS_LIB))
+        for name in ("ivfkm_synth_rows", "ivfkm_synth_fill"):
+            fn = getattr(lib, name)
+            fn.restype, fn.argtypes = _lib.SIGNATURES[name]
+        _corpus = lib
+    return _corpus
+
+
+def make_corpus(spec: CorpusSpec, standalone: bool = False):
+    """(indptr int64[N+1], term_ids int32 1-based, values float64, n dropped rows).
+
+    ``standalone``: generate with corpus_lib() instead of libivfkm.so."""
+    lib = corpus_lib() if standalone else _lib.load()
     cs = _lib.SynthSpec(spec.n, spec.dim, 0 if spec.nnz_kind == "poisson" else 1,
                         spec.nnz_mean, spec.nnz_sigma, spec.nnz_lo, spec.nnz_hi, spec.zipf_s,
                         spec.seed)
@@ -92,9 +115,9 @@ def make_corpus(spec: CorpusSpec):
     return indptr[: n + 1].copy(), terms[:nnz].copy(), vals[:nnz].copy(), spec.n - n
 
 
-def make_dataset(spec: CorpusSpec, dataset_cls=None):
+def make_dataset(spec: CorpusSpec, dataset_cls=None, standalone: bool = False):
     """Generate a corpus and wrap it in a (reference-compatible) Dataset."""
     if dataset_cls is None:
         from .types import Dataset as dataset_cls  # noqa: N813
-    indptr, terms, vals, _ = make_corpus(spec)
+    indptr, terms, vals, _ = make_corpus(spec, standalone)
     return dataset_cls(spec.dim, indptr, terms, vals, normalized=True)

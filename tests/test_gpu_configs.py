@@ -152,13 +152,18 @@ def test_config_sample_parity(cfg):
 
     # -- whole corpus: one iteration -> steady-state means M1, then assign again
     eng = LloydEngine(DeviceDataset.from_dataset(ds, "cuda"), k)
-    plan = _plan(k, eng.rowcap)
-    if cfg in (2, 3):
-        assert plan["nsplit"] == 1 and plan["rr"] == 8 and plan["warps"] > 4
-        assert plan["maxreg"] == 64  # screen_kernel<8, fp16, 64>
-    else:
-        assert plan["nsplit"] >= 2 and plan["warps"] > 4  # DSMEM cluster split
     dm0 = eng.upload_means(init_means(ds, k, c["seed"], representation="sparse_inverted"))
+    lib.ivfkm_set_screen_option(1, 1)
+    plan1 = _plan(k, eng.rowcap)  # the one-pass plan
+    if cfg in (2, 3):
+        assert plan1["nsplit"] == 1 and plan1["rr"] == 8 and plan1["warps"] > 4
+        assert plan1["maxreg"] == 64  # screen_kernel<8, fp16, 64>
+    else:
+        assert plan1["nsplit"] >= 2 and plan1["warps"] > 4  # DSMEM cluster split
+    npass = eng.screen_passes(dm0)
+    lib.ivfkm_set_screen_option(1, npass)
+    plan = _plan(k, eng.rowcap)  # the production plan: slot-range passes
+    assert npass > 1 and plan["nsplit"] > 1 and plan["maxreg"] == 56
     lab0 = eng.assign(dm0, None)
     st0 = eng.read_stats()
     dm1 = eng.update(lab0, dm0)
@@ -185,8 +190,9 @@ def test_config_sample_parity(cfg):
     assert np.array_equal(full_labels[rows], ol), "whole-corpus labels differ on the sample"
     oobj = O.objective(sub, ol, om1)
 
-    def run(bits=16, warps=0, directory=True):
+    def run(bits=16, warps=0, directory=True, passes=None):
         e = LloydEngine(DeviceDataset.from_dataset(sub, "cuda"), k, screen_bits=bits)
+        e.passes = passes
         if not directory:
             e.rankdir = None
         lib.ivfkm_set_screen_warps(warps)
@@ -198,7 +204,10 @@ def test_config_sample_parity(cfg):
             lib.ivfkm_set_screen_warps(0)
         return e, d, lab, st
 
-    variants = [dict(), dict(bits=32), dict(directory=False), dict(warps=3), dict(warps=16)]
+    # production (passes), the one-pass plan (64-register screen / DSMEM
+    # cluster), fp32 values, forced warps, an odd pass count, BIVF-lookup finalize
+    variants = [dict(), dict(passes=1), dict(passes=1, warps=16), dict(bits=32),
+                dict(passes=7, warps=3), dict(directory=False)]
     recs = []
     for v in variants:
         e, d, lab, st = run(**v)
@@ -213,7 +222,8 @@ def test_config_sample_parity(cfg):
             assert _same_means(new.to_meanset(validate=False), O.update_fast(sub, ol, om1))
         del e, d, lab
     REPORT[f"config{cfg}"] = {
-        "N": ds.n, "k": k, "plan": plan, "whole_corpus_iteration2": full_rec,
+        "N": ds.n, "k": k, "plan": plan, "one_pass_plan": plan1, "passes": npass,
+        "whole_corpus_iteration2": full_rec,
         "sample_rows": int(rows.size), "sample_gap_lt_1e-6": int(((top1 - top2) < 1e-6).sum()),
         "sample_variants": recs}
     _write_report()

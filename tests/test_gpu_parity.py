@@ -216,7 +216,7 @@ def tuning():
     lib.ivfkm_set_tuning(1024, -1, 0)
 
 
-def _assign_raw(ds, means, rowcap=None, smem=None, rr=-1, bits=None):
+def _assign_raw(ds, means, rowcap=None, smem=None, rr=-1, bits=None, passes=None):
     """Assign through the engine with explicit tuning (rowcap applies per call;
     rr = 0 automatic LDG screen, 2/4/8 LDG screen with that span, -8 / -4 the
     TMA / cp.async staged screens, which take fp32 screen values only)."""
@@ -226,6 +226,7 @@ def _assign_raw(ds, means, rowcap=None, smem=None, rr=-1, bits=None):
     if rowcap:
         eng.rowcap = rowcap
     eng.screen_bits = bits or (32 if rr < 0 else 16)
+    eng.passes = passes
     eng.lib.ivfkm_set_tuning(eng.rowcap, smem or 0, rr)
     try:
         dm = eng.upload_means(means)
@@ -234,6 +235,7 @@ def _assign_raw(ds, means, rowcap=None, smem=None, rr=-1, bits=None):
     finally:
         eng.rowcap = max(32, min(512, (eng.dd.max_row + 31) // 32 * 32))
         eng.screen_bits = 16
+        eng.passes = None
     return lab.cpu().numpy() + 1, st
 
 
@@ -349,6 +351,62 @@ def test_exact_ties_overflow_path():
     ol, _, _, _ = O.assign(ds, om)
     assert np.array_equal(labels, ol)
     assert st.overflow > 0 and st.near_ties >= st.overflow
+
+
+@pytest.mark.parametrize("bits", [16, 32])
+@pytest.mark.parametrize("k,passes,signed", [(4500, None, False), (4500, 2, True),
+                                             (9000, 3, False), (9000, 36, True),
+                                             (9000, 7, False)])
+def test_slot_range_passes_match_oracle(tuning, k, passes, signed, bits):
+    """The screen as slot-range passes (each launch: all objects x 1/P of the
+    slots, the best value and the near-tie window merged in a workspace state
+    between launches) gives the one-pass window, hence the oracle's labels."""
+    from oracle import oracle as O
+
+    ds, om, means = _random_case(n=k + 700, dim=3000, k=k, seed=21 + k % 7, signed=signed)
+    labels, st = _assign_raw(ds, means, bits=bits, passes=passes)
+    ol, _, _, post = O.assign(ds, om)
+    assert np.array_equal(labels, ol)
+    assert st.postings == post
+    assert st.objective == O.objective(ds, ol, om)
+    one, st1 = _assign_raw(ds, means, bits=bits, passes=1)
+    assert np.array_equal(one, ol)
+    assert (st.near_ties, st.overflow) == (st1.near_ties, st1.overflow)  # the same windows
+
+
+@pytest.mark.parametrize("passes", [1, 2, 5, 20])
+def test_slot_range_passes_exact_ties_across_passes(tuning, passes):
+    """300 copies of object 0's row among 4,700 other means: object 0 ties
+    300 ways (the overflow path) and the copies span several passes; the
+    smallest mean id must win, as in the reference (_kernels.pyx:17-26)."""
+    from oracle import oracle as O
+
+    P = _pkg()
+    ds, om, _ = _random_case(n=5400, dim=3000, k=4700, seed=5)
+    r0 = slice(int(ds.indptr[0]), int(ds.indptr[1]))
+    rng = np.random.default_rng(3)
+    k = 5000
+    is_copy = np.zeros(k, bool)
+    is_copy[rng.choice(k, 300, replace=False)] = True
+    src = iter(range(om.k))
+    rows_t, rows_v = [], []
+    for c in range(k):
+        if is_copy[c]:
+            rows_t.append(ds.term_ids[r0])
+            rows_v.append(ds.values[r0])
+        else:
+            j = next(src)
+            rows_t.append(om.term_ids[om.indptr[j]:om.indptr[j + 1]])
+            rows_v.append(om.values[om.indptr[j]:om.indptr[j + 1]])
+    ip = np.zeros(k + 1, np.int64)
+    np.cumsum([len(t) for t in rows_t], out=ip[1:])
+    terms, vals = np.concatenate(rows_t), np.concatenate(rows_v)
+    means = P.MeanSet.from_csr(ip, terms, vals, ds.dim, "sparse_inverted")
+    labels, st = _assign_raw(ds, means, passes=passes)
+    ol, _, _, post = O.assign(ds, O.Means(k, ds.dim, ip, terms, vals, np.zeros(k, bool)))
+    assert ol[0] == 1 + int(np.flatnonzero(is_copy)[0])
+    assert np.array_equal(labels, ol) and st.postings == post
+    assert st.overflow >= 1
 
 
 def test_update_matches_oracle_bitwise_with_empty_clusters():

@@ -20,6 +20,8 @@ def main():
     ap.add_argument("--iters", type=int, default=2)
     ap.add_argument("--passes", default="0,2,4,8,16")
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--pf", default="0")
+    ap.add_argument("--warps", default="0")
     a = ap.parse_args()
     c = synth.CONFIGS[a.config]
     ds = synth.make_dataset(c["corpus"])
@@ -31,8 +33,11 @@ def main():
         eng.read_stats()
         dm = eng.update(lab, dm)
         prev = lab
-    for r in map(int, a.passes.split(",")):
-        eng.lib.ivfkm_set_screen_warps(-1 - r)
+    import itertools
+    for r, pf, w in itertools.product(map(int, a.passes.split(",")), map(int, a.pf.split(",")),
+                                      map(int, a.warps.split(","))):
+        eng.lib.ivfkm_set_screen_warps(w)
+        eng.passes = r if r > 0 else None  # 0: the engine's plan
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         ts = []
         for _ in range(a.reps):
@@ -40,9 +45,9 @@ def main():
             torch.cuda.synchronize()
             ts.append(ev[0].elapsed_time(ev[1]))
         st = eng.read_stats()
-        print(json.dumps({"config": a.config, "passes": r, "screen_ms": min(ts), "all": ts,
+        print(json.dumps({"config": a.config, "passes": r, "planned": eng.screen_passes(dm), "pf": pf, "warps": w, "screen_ms": min(ts), "all": ts,
                           "postings": st.postings}), flush=True)
-    eng.lib.ivfkm_set_screen_warps(-1)
+    eng.lib.ivfkm_set_screen_warps(0)
 
 
 if __name__ == "__main__":

@@ -1,0 +1,4 @@
+timeout 900 python tools/exp_passes.py --config 3 --passes 0,4,8 2>&1 | tail -3
+timeout 600 python tools/exp_passes.py --config 2 --passes 0,8,16 2>&1 | tail -3
+timeout 600 python tools/exp_passes.py --config 1 --passes 0 2>&1 | tail -1
+timeout 900 python tools/exp_passes.py --config 4 --iters 1 --reps 1 --passes 0,16 2>&1 | tail -2
