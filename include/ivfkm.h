@@ -298,6 +298,14 @@ int ivfkm_assign_ivfd_host(int64_t n, const int64_t* x_indptr, const int32_t* x_
  * (t[-1] = -1, so the first gap is t0 + 1); a gap >= 0xFFFF is stored as
  * 0xFFFF and its absolute 0-based id is exc_term[j] where exc_idx[j] = h
  * (exc_idx ascending).  Integer work, exact.                                  */
+/* Rows from the reference's arrays ([dev]): 1-based term ids -> 0-based
+ * terms0, values -> fp32 val32 (the screen's copy), and each row's L2 norm
+ * xnorm (the screen's error bound; any summation order — the bound carries
+ * a relative margin). In-place terms0 == terms1 is allowed. */
+int ivfkm_rows_prepare(int64_t n_obj, const int64_t* row_ptr /*[dev] n+1*/,
+                       const int32_t* terms1 /*[dev]*/, const double* val64 /*[dev]*/,
+                       int32_t* terms0 /*[dev]*/, float* val32 /*[dev]*/, double* xnorm /*[dev] n*/,
+                       ivfkm_stream_t stream);
 int ivfkm_rows_decode(int64_t n_obj, const int64_t* row_ptr /*[dev] n+1*/,
                       const uint16_t* gaps /*[dev] nnz*/, int64_t n_exc,
                       const int64_t* exc_idx /*[dev]*/, const int32_t* exc_term /*[dev]*/,

@@ -374,16 +374,9 @@ __device__ void pass_epilogue(const ScreenParams& p, ScreenShared& sh, const flo
                               unsigned long long gpost) {
   const int cta_cids = p.cta_blocks * 32;
   const int64_t cid0 = (int64_t)z * cta_cids;
+  // (sh.pv/pc/pn were loaded at the kernel's start, pass_state_prefetch)
   if (threadIdx.x == 0) {
-    if (z > 0) {
-      sh.pv = p.st_best[obj];
-      sh.pc = p.st_slot[obj];
-      sh.pn = p.st_cnt[obj];
-    } else {
-      sh.pv = -INFINITY;
-      sh.pc = INT_MAX;
-      sh.pn = gpost ? kHasPost : 0;
-    }
+    if (z == 0) sh.pn = gpost ? kHasPost : 0;
     sh.cnt = 0;
   }
   __syncthreads();
@@ -396,7 +389,8 @@ __device__ void pass_epilogue(const ScreenParams& p, ScreenShared& sh, const flo
   if (has) {
     const double thr = (double)bv - 2.0 * window_eps(p, obj, n_i);
     const int2* pc = p.st_cand + obj * kMaxC;
-    for (int j = threadIdx.x; j < (prev < kMaxC ? prev : kMaxC); j += blockDim.x) {
+    // after an overflow the stored candidates are incomplete: not read
+    for (int j = threadIdx.x; j < (prev <= kMaxC ? prev : 0); j += blockDim.x) {
       const int2 c = pc[j];
       const float v = __int_as_float(c.y);
       if ((double)v >= thr) {
@@ -421,15 +415,17 @@ __device__ void pass_epilogue(const ScreenParams& p, ScreenShared& sh, const flo
     }
   }
   __syncthreads();
-  int total = sh.cnt;
-  if (prev > kMaxC && total <= kMaxC) total = kMaxC + 1;
+  const int got = sh.cnt;
+  const int stored = got < kMaxC ? got : kMaxC;  // valid entries of sh.cand
+  int total = got;
+  if (prev > kMaxC && total <= kMaxC) total = kMaxC + 1;  // an overflow stays one
   if (z < p.npass - 1) {
     if (threadIdx.x == 0) {
       p.st_best[obj] = bv;
       p.st_slot[obj] = bc;
       p.st_cnt[obj] = (total < kMaxC + 1 ? total : kMaxC + 1) | (has ? kHasPost : 0);
     }
-    for (int j = threadIdx.x; j < (total < kMaxC ? total : kMaxC); j += blockDim.x)
+    for (int j = threadIdx.x; j < stored; j += blockDim.x)
       p.st_cand[obj * kMaxC + j] = make_int2(sh.cand[j], __float_as_int(sh.cval[j]));
     return;
   }
@@ -444,10 +440,18 @@ __device__ void pass_epilogue(const ScreenParams& p, ScreenShared& sh, const flo
       p.slot_of[obj] = slot;
       p.q_obj[slot] = (int)obj;
       p.q_cnt[slot] = total;
-      const int w = total < kMaxC ? total : kMaxC;
-      for (int j = 0; j < w; ++j) p.q_cid[(int64_t)slot * kMaxC + j] = __ldg(p.inv + sh.cand[j]);
+      for (int j = 0; j < stored; ++j)
+        p.q_cid[(int64_t)slot * kMaxC + j] = __ldg(p.inv + sh.cand[j]);
     }
   }
+}
+
+// Byte offset of a dense run's value index: 32-bit for fp16 values (indices
+// stay below 2^31, bivf.cu), 64-bit for fp32 ones (4 B x 2^30+ values pass 2^32).
+template <bool HALF>
+__device__ __forceinline__ size_t dense_off(int x) {
+  if constexpr (HALF) return (size_t)(2u * (uint32_t)x);
+  else return (size_t)4 * (uint32_t)x;
 }
 
 // CTA-local argmax (value desc, index asc) over the parked rho, merged over
@@ -613,6 +617,15 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
     s_base[0] = p.masks;
     s_base[1] = p.offs;
     s_base[2] = p.pv32;
+    if (p.pass > 0) {  // the earlier passes' state, read long before the epilogue
+      sh.pv = p.st_best[obj];
+      sh.pc = p.st_slot[obj];
+      sh.pn = p.st_cnt[obj];
+    } else {
+      sh.pv = -INFINITY;
+      sh.pc = INT_MAX;
+      sh.pn = 0;
+    }
   }
   __syncthreads();
   const uint32_t* __restrict__ masks = static_cast<const uint32_t*>(s_base[0]);
@@ -729,7 +742,7 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
 #pragma unroll
             for (int u = 0; u < kDepth; ++u) {
               en[u] = dl[2 * (e + u)];
-              q[u].load_dense(pl + SV::kElem * (uint32_t)en[u].x);
+              q[u].load_dense(pl + dense_off<HALF>(en[u].x));
             }
 #pragma unroll
             for (int u = 0; u < kDepth; ++u) q[u].fma(__int_as_float(en[u].y), acc);
@@ -737,7 +750,7 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
           for (; e < nd; ++e) {
             SV q;
             const int2 en = dl[2 * e];
-            q.load_dense(pl + SV::kElem * (uint32_t)en.x);
+            q.load_dense(pl + dense_off<HALF>(en.x));
             q.fma(__int_as_float(en.y), acc);
           }
         }

@@ -64,7 +64,45 @@ __global__ void __launch_bounds__(256) rows_decode_kernel(
   }
 }
 
+// One warp per row: the reference's 1-based term ids -> 0-based, the fp32
+// screen copy of the values, and the row norm (used only inside the screen's
+// error bound, which carries a relative margin far above the order-dependent
+// last bits of this sum).
+__global__ void __launch_bounds__(256) rows_prepare_kernel(
+    int64_t n_obj, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ terms1,
+    const double* __restrict__ val64, int32_t* __restrict__ terms0, float* __restrict__ val32,
+    double* __restrict__ xnorm) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t i = blockIdx.x * wpb + (threadIdx.x >> 5); i < n_obj; i += gridDim.x * wpb) {
+    const int64_t rb = row_ptr[i], re = row_ptr[i + 1];
+    double ss = 0.0;
+    for (int64_t h = rb + lane; h < re; h += 32) {
+      const double v = val64[h];
+      terms0[h] = terms1[h] - 1;
+      val32[h] = (float)v;
+      ss = fma(v, v, ss);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(kFull, ss, off);
+    if (lane == 0) xnorm[i] = sqrt(ss);
+  }
+}
+
 }  // namespace
+
+extern "C" int ivfkm_rows_prepare(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms1,
+                                  const double* val64, int32_t* terms0, float* val32,
+                                  double* xnorm, ivfkm_stream_t stream_) {
+  if (n_obj < 0 || (n_obj > 0 && (!row_ptr || !terms1 || !val64 || !terms0 || !val32 || !xnorm)))
+    return IVFKM_E_ARG;
+  if (n_obj == 0) return IVFKM_OK;
+  cudaStream_t st = as_stream(stream_);
+  rows_prepare_kernel<<<grid_for(n_obj, 8), 256, 0, st>>>(n_obj, row_ptr, terms1, val64, terms0,
+                                                          val32, xnorm);
+  IVFKM_CHECK_LAUNCH();
+  return IVFKM_OK;
+}
 
 extern "C" int ivfkm_rows_decode(int64_t n_obj, const int64_t* row_ptr, const uint16_t* gaps,
                                  int64_t n_exc, const int64_t* exc_idx, const int32_t* exc_term,

@@ -174,7 +174,28 @@ class DeviceDataset:
 
     @classmethod
     def from_dataset(cls, ds, device="cuda") -> "DeviceDataset":
-        return cls(HostDataset(ds, pin=False), device)
+        """Upload a reference Dataset's own arrays (no host-side conversion) and
+        derive the device layout there (ivfkm_rows_prepare)."""
+        self = cls.__new__(cls)
+        dev = torch.device(device)
+        ip = np.ascontiguousarray(ds.indptr, dtype=np.int64)
+        t1 = np.ascontiguousarray(ds.term_ids, dtype=np.int32)
+        v = np.ascontiguousarray(ds.values, dtype=np.float64)
+        self.n, self.dim, self.nnz = int(ip.size - 1), int(ds.dim), int(ip[-1])
+        self.max_row = int(np.diff(ip).max()) if self.n else 0
+        self.device = dev
+        with warnings.catch_warnings():  # read-only reference arrays: only read here
+            warnings.simplefilter("ignore", UserWarning)
+            self.row_ptr = torch.from_numpy(ip).to(dev)
+            self.terms = torch.from_numpy(t1).to(dev)  # 1-based; made 0-based in place below
+            self.val64 = torch.from_numpy(v).to(dev)
+        self.val32 = torch.empty(max(self.nnz, 1), dtype=torch.float32, device=dev)[:self.nnz]
+        self.xnorm = torch.empty(max(self.n, 1), dtype=torch.float64, device=dev)[:self.n]
+        self._pending = ()
+        _lib.check(_lib.load().ivfkm_rows_prepare(
+            self.n, _p(self.row_ptr), _p(self.terms), _p(self.val64), _p(self.terms),
+            _p(self.val32), _p(self.xnorm), _stream()), "ivfkm_rows_prepare")
+        return self
 
 
 class DeviceMeans:
@@ -391,26 +412,26 @@ class LloydEngine:
     # -- assign --------------------------------------------------------------
     # postings per object and pass that amortise a pass's per-object cost
     # (row staging, epilogue, state merge); measured on configs 2-4
-    PASS_WORK = 90_000
+    PASS_WORK = 95_000
 
     def screen_passes(self, dm: DeviceMeans) -> int:
         """Slot-range passes for the fp16 screen at large k:
         enough 256-slot spans per pass that an object's pass does about
-        PASS_WORK postings, from the previous iteration's V (or, before the
-        first, V = sum_t no_t * nc_t from the BIVF headers)."""
+        PASS_WORK postings, from this assign's V = sum_t no_t * nc_t (object
+        document frequencies against the BIVF's per-term posting counts; one
+        small reduction and read-back, only at k >= 4,096 where a screen
+        takes 100 ms and more)."""
         if self.passes is not None:
             return int(self.passes)
         spans = self.nblk // 8
         if self.screen_bits != 16 or spans < 16 or self.dd.n == 0:
             return 1
-        v = self.last_postings
-        if v is None:
-            if self._doc_freq is None:
-                self._doc_freq = torch.bincount(self.dd.terms.long(),
-                                                minlength=self.dd.dim).to(torch.float64)
-            nh = self.dd.dim * self.nblk
-            nc = dm.headers[2 * nh + 1:2 * nh + 1 + self.dd.dim].to(torch.float64)
-            v = float(torch.dot(self._doc_freq, nc).item())
+        if self._doc_freq is None or self._doc_freq[0] is not self.dd.terms:
+            self._doc_freq = (self.dd.terms, torch.bincount(
+                self.dd.terms.long(), minlength=self.dd.dim).to(torch.float64))
+        nh = self.dd.dim * self.nblk
+        nc = dm.headers[2 * nh + 1:2 * nh + 1 + self.dd.dim].to(torch.float64)
+        v = float(torch.dot(self._doc_freq[1], nc).item())
         w = max(v / (self.dd.n * spans), 1.0)  # postings per (object, span)
         per = max(2, int(np.ceil(self.PASS_WORK / w)))
         p = int(np.ceil(spans / per))

@@ -160,13 +160,13 @@ def test_config_sample_parity(cfg):
         assert plan1["maxreg"] == 64  # screen_kernel<8, fp16, 64>
     else:
         assert plan1["nsplit"] >= 2 and plan1["warps"] > 4  # DSMEM cluster split
-    npass = eng.screen_passes(dm0)
-    lib.ivfkm_set_screen_option(1, npass)
-    plan = _plan(k, eng.rowcap)  # the production plan: slot-range passes
-    assert npass > 1 and plan["nsplit"] > 1 and plan["maxreg"] == 56
     lab0 = eng.assign(dm0, None)
-    st0 = eng.read_stats()
+    eng.read_stats()
     dm1 = eng.update(lab0, dm0)
+    npass = eng.screen_passes(dm1)
+    lib.ivfkm_set_screen_option(1, npass)
+    plan = _plan(k, eng.rowcap)  # the production plan at steady state: slot-range passes
+    assert npass > 1 and plan["nsplit"] > 1 and plan["maxreg"] == 56
     lab1 = eng.assign(dm1, lab0)
     st1 = eng.read_stats()
     full_labels = lab1.cpu().numpy() + 1
