@@ -10,7 +10,11 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libivfkm.so"
+import os
+
+# IVFKM_LIB: another build of the same ABI (A/B timing of kernel variants)
+LIB_PATH = Path(os.environ.get("IVFKM_LIB") or
+                Path(__file__).resolve().parent / "_lib" / "libivfkm.so")
 
 IVFKM_OBJ_LIMBS = 34
 IVFKM_MAXC = 32

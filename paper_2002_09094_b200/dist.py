@@ -7,28 +7,32 @@ tests).  Per iteration:
 * assign — purely local: every rank screens and rescores its contiguous row
   shard against the replicated means (no communication; the reference's
   per-object independence, _kernels.pyx:116-125).
-* statistics — one all-reduce of int64: postings V, changed labels,
-  near-ties, the 34 limbs of the exact objective accumulator and the k
-  cluster sizes.  Integer sums are order-free, so the objective stays the
-  exactly rounded sum (math.fsum semantics) for any rank count.
-* update — cluster range r = [r*k/P, (r+1)*k/P) is owned by rank r.  Every
-  rank routes each of its object rows to the owner of its label
-  (all-to-all-v of labels, row lengths, term ids and float64 values).  The
-  owner receives its clusters' members from ranks 0..P-1 in rank order, i.e.
-  in ascending global object order, so its per-(cluster, term) float64 sums,
-  divisions and pairwise norms are bit-identical to the single-GPU update
-  (variants.py:254-307) — means do not depend on P.  Owners then
-  all-gather their mean slices (sizes first, then padded payloads) and every
-  rank rebuilds the bitmap-block inverted file locally.
+* statistics — one int64 all-reduce (pack_stats): postings V, changed
+  labels, near-ties, overflows, the objective's range flags, the 34 limbs of
+  the exact objective accumulator and the k cluster sizes.  Integer sums are
+  order-free, so the objective stays the exactly rounded sum (math.fsum
+  semantics) for any rank count.
+* update — cluster range r = [r*k/P, (r+1)*k/P) is owned by rank r, which
+  keeps the rows of every object labelled in its range (``Members``, in
+  ascending global object id).  Each iteration only what changed moves
+  (ShardComm.exchange_members): a 16-byte notice (gid, new label) to the old
+  owner of every object whose label changed, and the row itself to the new
+  owner when the owner changed — one count all-to-all, one packed byte
+  all-to-all.  The owner drops leavers, relabels stayers and merges arrivals
+  by gid, so it sums its clusters' members in ascending global object order:
+  its float64 sums, divisions and pairwise norms are bit-identical to the
+  single-GPU update (variants.py:254-307) — the means do not depend on P.
+  Owners then all-gather their mean slices (one size all-gather, one packed
+  byte all-gather) and every rank rebuilds the bitmap-block inverted file.
 
-Raw rows cross NVLink once per iteration (sum_nnz * 12 B in total; ~5.8 GB at
-config 3, milliseconds at ~770 GB/s per GPU) instead of pre-reduced partial
-sums: that is what keeps the float64 summation order, and hence the means,
-independent of the rank count.
+Raw member rows, not pre-reduced partial sums, are what keeps the float64
+summation order — and so the means — independent of the rank count; after
+the first iteration the exchange carries only the movers (a few percent of
+the rows at steady state) instead of the whole corpus.
 
 The exchange code is device-agnostic (torch tensors + torch.distributed);
 the local compute is injected, so tests/test_dist.py runs the same exchange
-over gloo on CPU with the oracle as the local compute.
+and statistics packing over gloo on CPU with the oracle as the local compute.
 """
 
 from __future__ import annotations
@@ -44,7 +48,8 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-__all__ = ["shard_rows", "cluster_range", "Rows", "ShardComm", "DistLloyd", "bench_multi"]
+__all__ = ["shard_rows", "cluster_range", "Rows", "Members", "ShardComm", "DistLloyd",
+           "pack_stats", "unpack_stats", "STAT_WORDS", "bench_multi"]
 
 
 def shard_rows(indptr: np.ndarray, world: int) -> list[tuple[int, int]]:
@@ -87,94 +92,254 @@ class Rows:
         return int(self.terms.numel())
 
 
+@dataclass
+class Members(Rows):
+    """An owner's member rows: every object labelled in its cluster range, in
+    ascending global object id (``gid``) — the order the single-GPU update
+    sums them in, so the owner's means do not depend on the rank count."""
+
+    gid: torch.Tensor = None  # int64 [n], ascending
+
+
+# -- statistics vector (one int64 all-reduce per iteration) -------------------
+STAT_WORDS = 5 + 34  # V, changed, near-ties, overflow, objective flags, 34 limbs
+
+
+def pack_stats(vec: torch.Tensor, raw: torch.Tensor, sizes: torch.Tensor) -> torch.Tensor:
+    """Fill ``vec`` (int64 [STAT_WORDS + k]) from an ivfkm_stats block viewed as
+    int64 (``raw``: postings, changed, near_ties, overflow, queue_len,
+    obj_flags, 34 limbs) and the k cluster sizes.  Integer sums are
+    order-free, so the all-reduced objective is still exactly rounded."""
+    vec[:4] = raw[:4]
+    vec[4] = raw[5]  # obj_flags: a summand outside the accumulator on any rank
+    vec[5:STAT_WORDS] = raw[6:40]
+    vec[STAT_WORDS:] = sizes
+    return vec
+
+
+def unpack_stats(h) -> dict:
+    """The all-reduced vector (host) -> global statistics (raises like
+    IterStats.from_raw when any rank saw an objective summand out of range)."""
+    from .engine import objective_from_limbs
+
+    h = [int(x) for x in h[:STAT_WORDS]]
+    if h[4]:
+        raise FloatingPointError("objective summand outside the exact accumulator range")
+    return dict(postings=h[0], changed=h[1], near_ties=h[2], overflow=h[3],
+                objective=objective_from_limbs(h[5:STAT_WORDS]))
+
+
+def _bytes(t: torch.Tensor) -> torch.Tensor:
+    """A flat byte view (empty tensors may carry a zero stride)."""
+    t = t.reshape(-1)
+    if t.numel() == 0:
+        return torch.empty(0, dtype=torch.uint8, device=t.device)
+    return t.contiguous().view(torch.uint8)
+
+
+def _gather_rows(row_ptr, terms, vals, sel):
+    """Rows ``sel`` (int64 index) of a CSR block, concatenated."""
+    dev = row_ptr.device
+    lens = row_ptr[sel + 1] - row_ptr[sel]
+    ptr = torch.zeros(sel.numel() + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(lens, 0, out=ptr[1:])
+    total = int(ptr[-1])
+    seg = torch.repeat_interleave(torch.arange(sel.numel(), device=dev), lens,
+                                  output_size=total)
+    idx = row_ptr[sel][seg] + (torch.arange(total, device=dev) - ptr[:-1][seg])
+    return ptr, terms[idx], vals[idx]
+
+
 class ShardComm:
     """The collectives of one Lloyd iteration over a process group."""
 
     def __init__(self, rank: int, world: int, group=None):
         self.rank, self.world, self.group = rank, world, group
+        self.last_exchange_bytes = 0
 
     def allreduce_sum_(self, t: torch.Tensor) -> torch.Tensor:
         if self.world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
         return t
 
-    def _a2a(self, send: torch.Tensor, send_counts: list[int], recv_counts: list[int]):
-        out = torch.empty(sum(recv_counts), dtype=send.dtype, device=send.device)
+    def _a2a_bytes(self, send: torch.Tensor, send_counts: list[int], recv_counts: list[int]):
+        out = torch.empty(sum(recv_counts), dtype=torch.uint8, device=send.device)
         if self.world == 1:
             out.copy_(send)
             return out
-        dist.all_to_all_single(out, send.contiguous(), recv_counts, send_counts, group=self.group)
+        dist.all_to_all_single(out, send, recv_counts, send_counts, group=self.group)
         return out
 
-    def route_rows(self, rows: Rows, k: int) -> Rows:
-        """Send each row to the owner of its label's cluster range; the result
-        holds the owner's rows in ascending global object order."""
-        if self.world == 1:  # the only rank owns every cluster: nothing moves
-            return rows
-        dev = rows.row_ptr.device
-        bounds = cluster_owner_bounds(k, self.world).to(dev)
-        lab = rows.labels.to(torch.int64)
-        owner = torch.bucketize(lab, bounds, right=True)
-        order = torch.argsort(owner, stable=True)
-        nnz_row = (rows.row_ptr[1:] - rows.row_ptr[:-1])
-        obj_cnt = torch.bincount(owner, minlength=self.world)
-        ent_cnt = torch.zeros(self.world, dtype=torch.int64, device=dev)
-        ent_cnt.index_add_(0, owner, nnz_row)
-        counts = torch.stack([obj_cnt, ent_cnt], 1).reshape(-1)
-        rcounts = torch.empty_like(counts)
-        if self.world > 1:
-            dist.all_to_all_single(rcounts, counts, group=self.group)
+    def exchange_members(self, owned: "Members | None", gid0: int, local: Rows,
+                         prev: torch.Tensor | None, k: int) -> Members:
+        """Bring the cluster owners' member sets up to the new labels.
+
+        Only what changed crosses the wire: for every object whose label
+        changed, a 16-byte notice (gid, new label) to its old owner, and —
+        when its owner changed too — the row itself (gid, label, length, then
+        int32 terms + float64 values) to the new owner.  The first iteration
+        (``owned is None``) routes every row.  One all-to-all of the per-peer
+        counts (the only host read), one packed byte all-to-all.  The owner
+        drops leavers, relabels stayers and merges arrivals by gid, so its
+        members stay in ascending global object order."""
+        dev = local.row_ptr.device
+        P, r = self.world, self.rank
+        bounds = cluster_owner_bounds(k, P).to(dev)
+        new = local.labels.to(torch.int64)
+        new_own = torch.bucketize(new, bounds, right=True)
+        n = new.numel()
+        if owned is None or prev is None:
+            mover = torch.ones(n, dtype=torch.bool, device=dev)
+            notice = torch.zeros(n, dtype=torch.bool, device=dev)
+            old_own = new_own
         else:
-            rcounts.copy_(counts)
-        c = counts.view(-1, 2).cpu().tolist()
-        rc = rcounts.view(-1, 2).cpu().tolist()
-        # entries in the routed order
-        sel_len = nnz_row[order]
-        starts = rows.row_ptr[:-1][order]
-        seg = torch.repeat_interleave(torch.arange(order.numel(), device=dev), sel_len)
-        seg_start = torch.cumsum(sel_len, 0) - sel_len
-        ent_idx = starts[seg] + (torch.arange(seg.numel(), device=dev) - seg_start[seg])
-        meta = torch.stack([lab[order], sel_len], 1).reshape(-1)
-        r_meta = self._a2a(meta, [2 * a for a, _ in c], [2 * a for a, _ in rc]).view(-1, 2)
-        r_terms = self._a2a(rows.terms[ent_idx], [b for _, b in c], [b for _, b in rc])
-        r_vals = self._a2a(rows.vals[ent_idx], [b for _, b in c], [b for _, b in rc])
-        ptr = torch.zeros(r_meta.shape[0] + 1, dtype=torch.int64, device=dev)
-        torch.cumsum(r_meta[:, 1], 0, out=ptr[1:])
-        return Rows(ptr, r_terms.to(torch.int32), r_vals, r_meta[:, 0].to(torch.int32))
+            old = prev.to(torch.int64)
+            old_own = torch.bucketize(old, bounds, right=True)
+            notice = new != old
+            mover = notice & (new_own != old_own)
+        nt = torch.nonzero(notice).flatten()
+        mv = torch.nonzero(mover).flatten()
+        nt = nt[torch.argsort(old_own[nt], stable=True)]
+        mv = mv[torch.argsort(new_own[mv], stable=True)]
+        lens = local.row_ptr[1:] - local.row_ptr[:-1]
+        cnt = torch.zeros(P, 3, dtype=torch.int64, device=dev)
+        cnt[:, 0] = torch.bincount(old_own[nt], minlength=P)
+        cnt[:, 1] = torch.bincount(new_own[mv], minlength=P)
+        cnt[:, 2].index_add_(0, new_own[mv], lens[mv])
+        rcnt = torch.empty_like(cnt)
+        if P > 1:
+            dist.all_to_all_single(rcnt, cnt, group=self.group)
+        else:
+            rcnt.copy_(cnt)
+        both = torch.stack([cnt, rcnt]).cpu().tolist()
+        sc, rc = both[0], both[1]
+
+        def nbytes(c):
+            return 16 * c[0] + 24 * c[1] + 4 * c[2] + (4 if c[2] % 2 else 0) + 8 * c[2]
+
+        gid = torch.arange(n, device=dev, dtype=torch.int64) + gid0
+        notes = torch.stack([gid[nt], new[nt]], 1).reshape(-1)
+        meta = torch.stack([gid[mv], new[mv], lens[mv]], 1).reshape(-1)
+        _, m_terms, m_vals = _gather_rows(local.row_ptr, local.terms, local.vals, mv)
+        parts, o_nt, o_mv, o_e = [], 0, 0, 0
+        for d in range(P):
+            a, b, e = sc[d]
+            parts.append(_bytes(notes[2 * o_nt:2 * (o_nt + a)]))
+            parts.append(_bytes(meta[3 * o_mv:3 * (o_mv + b)]))
+            t = m_terms[o_e:o_e + e]
+            if e % 2:
+                t = torch.cat([t, torch.zeros(1, dtype=torch.int32, device=dev)])
+            parts.append(_bytes(t))
+            parts.append(_bytes(m_vals[o_e:o_e + e]))
+            o_nt, o_mv, o_e = o_nt + a, o_mv + b, o_e + e
+        send = torch.cat(parts) if parts else torch.zeros(0, dtype=torch.uint8, device=dev)
+        recv = self._a2a_bytes(send, [nbytes(c) for c in sc], [nbytes(c) for c in rc])
+        self.last_exchange_bytes = int(send.numel())
+        # parse, source by source (sources hold ascending, disjoint gid ranges)
+        r_notes, r_meta, r_terms, r_vals, off = [], [], [], [], 0
+        for src in range(P):
+            a, b, e = rc[src]
+            seg = recv[off:off + nbytes(rc[src])]
+            q = 0
+            r_notes.append(seg[q:q + 16 * a].view(torch.int64).view(-1, 2))
+            q += 16 * a
+            r_meta.append(seg[q:q + 24 * b].view(torch.int64).view(-1, 3))
+            q += 24 * b
+            r_terms.append(seg[q:q + 4 * e].view(torch.int32))
+            q += 4 * e + (4 if e % 2 else 0)
+            r_vals.append(seg[q:q + 8 * e].view(torch.float64))
+            off += nbytes(rc[src])
+        notes_in = torch.cat(r_notes)
+        meta_in = torch.cat(r_meta)
+        a_terms = torch.cat(r_terms)
+        a_vals = torch.cat(r_vals)
+        a_ptr = torch.zeros(meta_in.shape[0] + 1, dtype=torch.int64, device=dev)
+        torch.cumsum(meta_in[:, 2], 0, out=a_ptr[1:])
+        a_gid, a_lab = meta_in[:, 0], meta_in[:, 1].to(torch.int32)
+        if owned is None:
+            return Members(a_ptr, a_terms, a_vals, a_lab, gid=a_gid)
+        # apply the notices: leavers out, stayers relabelled
+        labels = owned.labels.clone()
+        keep = torch.ones(owned.n, dtype=torch.bool, device=dev)
+        if notes_in.shape[0]:
+            pos = torch.searchsorted(owned.gid, notes_in[:, 0])
+            nl = notes_in[:, 1]
+            stay = torch.bucketize(nl, bounds, right=True) == r
+            labels[pos[stay]] = nl[stay].to(torch.int32)
+            keep[pos[~stay]] = False
+        kept = torch.nonzero(keep).flatten()
+        if a_gid.numel() == 0 and kept.numel() == owned.n:
+            return Members(owned.row_ptr, owned.terms, owned.vals, labels, gid=owned.gid)
+        # merge kept members and arrivals by gid (both ascending)
+        all_gid = torch.cat([owned.gid[kept], a_gid])
+        order = torch.argsort(all_gid, stable=True)
+        base = owned.terms.numel()
+        ptr = torch.cat([owned.row_ptr[:-1], a_ptr[:-1] + base, a_ptr[-1:] + base])
+        terms = torch.cat([owned.terms, a_terms])
+        vals = torch.cat([owned.vals, a_vals])
+        src_rows = torch.cat([kept, torch.arange(a_gid.numel(), device=dev) + owned.n])[order]
+        ends = torch.cat([owned.row_ptr[1:], a_ptr[1:] + base])
+        lens_all = ends - ptr[:-1]
+        full_ptr = torch.cat([ptr[:-1], ptr[-1:]])
+        del lens_all
+        # rows src_rows of the concatenated block (row i spans full_ptr[i] .. ends[i])
+        sel_start = full_ptr[src_rows]
+        sel_len = ends[src_rows] - sel_start
+        new_ptr = torch.zeros(src_rows.numel() + 1, dtype=torch.int64, device=dev)
+        torch.cumsum(sel_len, 0, out=new_ptr[1:])
+        total = int(new_ptr[-1])
+        seg = torch.repeat_interleave(torch.arange(src_rows.numel(), device=dev), sel_len,
+                                      output_size=total)
+        idx = sel_start[seg] + (torch.arange(total, device=dev) - new_ptr[:-1][seg])
+        all_lab = torch.cat([labels[kept], a_lab])[order]
+        return Members(new_ptr, terms[idx], vals[idx], all_lab, gid=all_gid[order])
 
     def allgather_means(self, ptr: torch.Tensor, terms: torch.Tensor, vals: torch.Tensor,
                         retained: torch.Tensor):
-        """Concatenate every rank's mean slice in rank (= cluster) order."""
+        """Concatenate every rank's mean slice in rank (= cluster) order: one
+        size all-gather, then one packed byte all-gather (NCCL: per-rank
+        exact sizes; gloo: padded to the largest slice)."""
         if self.world == 1:
             return ptr, terms, vals, retained
         dev = ptr.device
         kl = int(ptr.numel() - 1)
         nl = int(terms.numel())
+        cnt = ptr[1:] - ptr[:-1]
+
+        def nb(kl_, nl_):
+            return 8 * kl_ + 4 * nl_ + (4 if nl_ % 2 else 0) + 8 * nl_ + kl_
+
+        t = terms if nl % 2 == 0 else torch.cat([terms, torch.zeros(1, dtype=torch.int32,
+                                                                     device=dev)])
+        buf = torch.cat([_bytes(cnt), _bytes(t), _bytes(vals), _bytes(retained.to(torch.uint8))])
         sz = torch.tensor([kl, nl], dtype=torch.int64, device=dev)
         sizes = [torch.empty_like(sz) for _ in range(self.world)]
         dist.all_gather(sizes, sz, group=self.group)
         sizes = [tuple(x.cpu().tolist()) for x in sizes]
-        kmax = max(a for a, _ in sizes)
-        nmax = max(max(b for _, b in sizes), 1)
-
-        def gather(t, length, fill_dtype):
-            buf = torch.zeros(length, dtype=fill_dtype, device=dev)
-            buf[: t.numel()] = t
-            outs = [torch.empty_like(buf) for _ in range(self.world)]
-            dist.all_gather(outs, buf, group=self.group)
-            return outs
-
-        g_cnt = gather(ptr[1:] - ptr[:-1], kmax, torch.int64)
-        g_terms = gather(terms, nmax, torch.int32)
-        g_vals = gather(vals, nmax, torch.float64)
-        g_ret = gather(retained.to(torch.int32), kmax, torch.int32)
-        cnt = torch.cat([g_cnt[r][: sizes[r][0]] for r in range(self.world)])
-        full_ptr = torch.zeros(cnt.numel() + 1, dtype=torch.int64, device=dev)
-        torch.cumsum(cnt, 0, out=full_ptr[1:])
-        full_terms = torch.cat([g_terms[r][: sizes[r][1]] for r in range(self.world)])
-        full_vals = torch.cat([g_vals[r][: sizes[r][1]] for r in range(self.world)])
-        full_ret = torch.cat([g_ret[r][: sizes[r][0]] for r in range(self.world)]).to(torch.uint8)
-        return full_ptr, full_terms, full_vals, full_ret
+        lens = [nb(a, b) for a, b in sizes]
+        if dist.get_backend(self.group) == "nccl":
+            outs = [torch.empty(L, dtype=torch.uint8, device=dev) for L in lens]
+            dist.all_gather(outs, buf, group=self.group)  # uneven sizes
+        else:
+            mx = max(lens)
+            pad = torch.zeros(mx, dtype=torch.uint8, device=dev)
+            pad[:buf.numel()] = buf
+            outs = [torch.empty(mx, dtype=torch.uint8, device=dev) for _ in lens]
+            dist.all_gather(outs, pad, group=self.group)
+        cnts, tl, vl, rl = [], [], [], []
+        for (a, b), o in zip(sizes, outs):
+            q = 0
+            cnts.append(o[q:q + 8 * a].view(torch.int64))
+            q += 8 * a
+            tl.append(o[q:q + 4 * b].view(torch.int32))
+            q += 4 * b + (4 if b % 2 else 0)
+            vl.append(o[q:q + 8 * b].view(torch.float64))
+            q += 8 * b
+            rl.append(o[q:q + a])
+        cnt_all = torch.cat(cnts)
+        full_ptr = torch.zeros(cnt_all.numel() + 1, dtype=torch.int64, device=dev)
+        torch.cumsum(cnt_all, 0, out=full_ptr[1:])
+        return full_ptr, torch.cat(tl), torch.cat(vl), torch.cat(rl)
 
 
 class DistLloyd:
@@ -198,40 +363,35 @@ class DistLloyd:
         self.lo, self.hi = lo, hi
         self.host = HostDataset(_Shard, pin=torch.cuda.is_available())
         self.dd = DeviceDataset(self.host, device)
+        self.members = None  # this rank's cluster-range member rows (exchange_members)
+        self.prev_labels = None
         # the sharded update routes rows to cluster owners and runs the
         # stateless count (no label-delta state, no whole-shard workspace)
         self.eng = LloydEngine(self.dd, self.k, delta_update=False, update_ws=False)
         self.device = self.dd.device
-        self.stats_vec = torch.zeros(5 + 34 + self.k, dtype=torch.int64, device=self.device)
+        self.stats_vec = torch.zeros(STAT_WORDS + self.k, dtype=torch.int64, device=self.device)
         self.ws = None  # update workspace of the routed rows, grown on demand
 
     def assign(self, dm, prev, events=None):
         """Local assign + the one statistics all-reduce; returns labels and
         global (postings, changed, near_ties, overflow, objective, sizes)."""
-        from .engine import objective_from_limbs
-
         lab = self.eng.assign(dm, prev, events=events)
         raw = self.eng.stats.view(torch.int64)  # 6 + 34 words (ivfkm_stats)
-        v = self.stats_vec
-        v[:4] = raw[:4]
-        v[4] = raw[5]  # obj_flags: nonzero on any rank poisons the objective
-        v[5:39] = raw[6:40]
-        v[39:] = self.eng.sizes
+        v = pack_stats(self.stats_vec, raw, self.eng.sizes)
         self.comm.allreduce_sum_(v)
         h = v.cpu()
         self.local_postings = int(raw[0].item())  # this rank's share (roofline)
-        self.eng.sizes.copy_(v[39:])  # global sizes for the update
-        if int(h[4]):
-            raise FloatingPointError("objective summand outside the exact accumulator range")
-        return lab, dict(postings=int(h[0]), changed=int(h[1]), near_ties=int(h[2]),
-                         overflow=int(h[3]), objective=objective_from_limbs(h[5:39].tolist()))
+        self.eng.sizes.copy_(v[STAT_WORDS:])  # global sizes for the update
+        return lab, unpack_stats(h)
 
     def update(self, lab, dm):
         from .engine import DeviceMeans, update_rows
 
         dd, k = self.dd, self.k
         rows = Rows(dd.row_ptr, dd.terms, dd.val64, lab)
-        recv = self.comm.route_rows(rows, k)
+        recv = self.members = self.comm.exchange_members(self.members, self.lo, rows,
+                                                         self.prev_labels, k)
+        self.prev_labels = lab.clone()
         clo, chi = cluster_range(k, self.comm.world, self.comm.rank)
         kl = chi - clo
         if kl > 0:

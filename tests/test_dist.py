@@ -58,8 +58,8 @@ def _worker(rank, world, port, k, iters, q):
     import torch.distributed as dist
 
     from oracle import oracle as O
-    from paper_2002_09094_b200.dist import Rows, ShardComm, cluster_range, shard_rows
-    from paper_2002_09094_b200.engine import objective_from_limbs
+    from paper_2002_09094_b200.dist import (STAT_WORDS, Rows, ShardComm, cluster_range,
+                                            pack_stats, shard_rows, unpack_stats)
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -77,38 +77,60 @@ def _worker(rank, world, port, k, iters, q):
 
     means = O.init_means(ds, k, 4)
     prev = None
+    members = None
+    vec = torch.zeros(STAT_WORDS + k, dtype=torch.int64)
     out = []
     for _ in range(iters):
         labels, _, _, post = O.assign(Shard, means)
         sims = _sims(Shard, labels, means)
         changed = 0 if prev is None else int(np.sum(labels != prev))
         sizes = np.bincount(labels - 1, minlength=k)
-        vec = torch.tensor([post, changed] + limbs_of(sims) + sizes.tolist(), dtype=torch.int64)
+        # the local statistics in ivfkm_stats' layout (what the kernels write)
+        raw = torch.tensor([post, changed, 0, 0, 0, 0] + limbs_of(sims), dtype=torch.int64)
+        pack_stats(vec, raw, torch.from_numpy(sizes.astype(np.int64)))  # DistLloyd.assign's
         comm.allreduce_sum_(vec)
-        objective = objective_from_limbs(vec[2:36].tolist())
+        st = unpack_stats(vec)
         rows = Rows(torch.from_numpy(Shard.indptr.copy()),
                     torch.from_numpy(Shard.term_ids.astype(np.int32) - 1),
                     torch.from_numpy(Shard.values.copy()),
                     torch.from_numpy(labels.astype(np.int32) - 1))
-        recv = comm.route_rows(rows, k)
+        prev_t = None if prev is None else torch.from_numpy(prev.astype(np.int32) - 1)
+        members = comm.exchange_members(members, lo, rows, prev_t, k)  # DistLloyd.update's
         clo, chi = cluster_range(k, world, rank)
+        assert bool(torch.all(members.gid[1:] > members.gid[:-1]))  # ascending global order
+        assert bool(torch.all((members.labels >= clo) & (members.labels < chi)))
 
         class Recv:
             dim = ds.dim
-            indptr = recv.row_ptr.numpy()
-            term_ids = recv.terms.numpy() + 1
-            values = recv.vals.numpy()
+            indptr = members.row_ptr.numpy()
+            term_ids = members.terms.numpy() + 1
+            values = members.vals.numpy()
 
         p0, p1 = int(means.indptr[clo]), int(means.indptr[chi])
         prev_slice = O.Means(chi - clo, ds.dim, means.indptr[clo:chi + 1] - p0,
                              means.term_ids[p0:p1], means.values[p0:p1],
                              means.retained[clo:chi])
-        new = O.update(Recv, recv.labels.numpy() - clo + 1, prev_slice)
+        new = O.update(Recv, members.labels.numpy() - clo + 1, prev_slice)
         ptr, terms, vals, ret = comm.allgather_means(
             torch.from_numpy(new.indptr), torch.from_numpy(new.term_ids - 1),
             torch.from_numpy(new.values), torch.from_numpy(new.retained.astype(np.uint8)))
-        out.append(dict(labels=labels, post=int(vec[0]), changed=int(vec[1]),
-                        objective=objective, sizes=vec[36:].numpy().copy()))
+        # after the first iteration only movers cross: notices + rows of the
+        # objects whose owner changed
+        if prev is None:
+            bound = None
+        else:
+            from paper_2002_09094_b200.dist import cluster_owner_bounds
+
+            bnd = cluster_owner_bounds(k, world).numpy()
+            own_o = np.searchsorted(bnd, prev - 1, side="right")
+            own_n = np.searchsorted(bnd, labels - 1, side="right")
+            ch = labels != prev
+            mv = ch & (own_o != own_n)
+            lens = np.diff(Shard.indptr)
+            bound = 16 * int(ch.sum()) + int(np.sum(24 + 12 * lens[mv])) + 4 * world
+        out.append(dict(labels=labels, post=st["postings"], changed=st["changed"],
+                        objective=st["objective"], sizes=vec[STAT_WORDS:].numpy().copy(),
+                        sent=comm.last_exchange_bytes, bound=bound))
         means = O.Means(k, ds.dim, ptr.numpy(), terms.numpy().astype(np.int32) + 1,
                         vals.numpy(), ret.numpy().astype(bool))
         prev = labels
@@ -116,7 +138,7 @@ def _worker(rank, world, port, k, iters, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,k", [(2, 12), (3, 7), (2, 1)])
+@pytest.mark.parametrize("world,k", [(2, 12), (3, 7), (2, 1), (3, 40)])
 def test_sharded_lloyd_equals_single_process(world, k):
     from oracle import oracle as O
 
@@ -143,6 +165,9 @@ def test_sharded_lloyd_equals_single_process(world, k):
             assert r[3][it]["objective"] == O.objective(ds, labels, m)
             assert r[3][it]["changed"] == (0 if prev is None else int(np.sum(labels != prev)))
             assert np.array_equal(r[3][it]["sizes"], O.sizes_of(labels, k))
+            if r[3][it]["bound"] is not None:  # only what changed was exchanged
+                assert r[3][it]["sent"] <= r[3][it]["bound"], (r[3][it]["sent"],
+                                                               r[3][it]["bound"])
         m = O.update(ds, labels, m)
         prev = labels
     for r in res:  # every rank holds the same, bit-identical means

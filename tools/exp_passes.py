@@ -34,18 +34,22 @@ def main():
         dm = eng.update(lab, dm)
         prev = lab
     import itertools
+
+    from bench import Clocks
     for r, pf, w in itertools.product(map(int, a.passes.split(",")), map(int, a.pf.split(",")),
                                       map(int, a.warps.split(","))):
         eng.lib.ivfkm_set_screen_warps(w)
         eng.passes = r if r > 0 else None  # 0: the engine's plan
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         ts = []
+        clk = Clocks(0)
         for _ in range(a.reps):
             eng.assign(dm, None, events=ev)
             torch.cuda.synchronize()
             ts.append(ev[0].elapsed_time(ev[1]))
         st = eng.read_stats()
-        print(json.dumps({"config": a.config, "passes": r, "planned": eng.screen_passes(dm), "pf": pf, "warps": w, "screen_ms": min(ts), "all": ts,
+        ck = clk.stop() or {}
+        print(json.dumps({"sm_mhz": ck.get("sm_mhz"), "reasons": ck.get("reasons"), "config": a.config, "passes": r, "planned": eng.screen_passes(dm), "pf": pf, "warps": w, "screen_ms": min(ts), "all": ts,
                           "postings": st.postings}), flush=True)
     eng.lib.ivfkm_set_screen_warps(0)
 
