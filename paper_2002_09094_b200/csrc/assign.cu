@@ -371,7 +371,7 @@ __device__ __forceinline__ double window_eps(const ScreenParams& p, int64_t obj,
 // dropped values are unknown, and the overflow kernel rescores every mean).
 __device__ void pass_epilogue(const ScreenParams& p, ScreenShared& sh, const float* rho,
                               int64_t obj, int z, int64_t n_i, float gv, int gc,
-                              unsigned long long gpost, const float* smax, int span_slots) {
+                              unsigned long long gpost) {
   const int cta_cids = p.cta_blocks * 32;
   const int64_t cid0 = (int64_t)z * cta_cids;
   // (sh.pv/pc/pn were loaded at the kernel's start, pass_state_prefetch)
@@ -401,22 +401,15 @@ __device__ void pass_epilogue(const ScreenParams& p, ScreenShared& sh, const flo
         }
       }
     }
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    const int nsp = smax ? cta_cids / span_slots : 1;
-    const int len = smax ? span_slots : cta_cids;
-    for (int sp = smax ? warp : 0; sp < nsp; sp += smax ? nwarps : 1) {
-      if (smax && (double)smax[sp] < thr) continue;  // no slot of this span reaches it
-      for (int j = sp * len + (smax ? lane : (int)threadIdx.x); j < (sp + 1) * len;
-           j += smax ? 32 : (int)blockDim.x) {
-        const int64_t cid = cid0 + j;
-        if (cid >= p.k) break;
-        const float v = rho[j];
-        if ((double)v >= thr) {
-          const int s = atomicAdd(&sh.cnt, 1);
-          if (s < kMaxC) {
-            sh.cand[s] = (int)cid;
-            sh.cval[s] = v;
-          }
+    for (int j = threadIdx.x; j < cta_cids; j += blockDim.x) {
+      const int64_t cid = cid0 + j;
+      if (cid >= p.k) break;
+      const float v = rho[j];
+      if ((double)v >= thr) {
+        const int s = atomicAdd(&sh.cnt, 1);
+        if (s < kMaxC) {
+          sh.cand[s] = (int)cid;
+          sh.cval[s] = v;
         }
       }
     }
@@ -466,9 +459,7 @@ __device__ __forceinline__ size_t dense_off(int x) {
 // the candidate queue for exact rescoring.  Every thread of the CTA calls it.
 __device__ __forceinline__ void screen_epilogue(const ScreenParams& p, ScreenShared& sh,
                                                 const float* rho, int64_t obj, int z, int64_t rb,
-                                                int64_t re, unsigned long long post,
-                                                const float* smax = nullptr,
-                                                const int* sarg = nullptr, int span_slots = 0) {
+                                                int64_t re, unsigned long long post) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
@@ -477,18 +468,13 @@ __device__ __forceinline__ void screen_epilogue(const ScreenParams& p, ScreenSha
   float bv = -INFINITY;
   int bc = INT_MAX;
   const int64_t cid0 = blk0 * 32;
-  if (smax) {  // from the spans' maxima (value desc, slot asc)
-    for (int j = threadIdx.x; j < cta_cids / span_slots; j += blockDim.x)
-      better(bv, bc, smax[j], sarg[j]);
-  } else {
-    for (int j = threadIdx.x; j < cta_cids; j += blockDim.x) {
-      const int64_t cid = cid0 + j;
-      if (cid >= p.k) break;
-      const float v = rho[j];
-      if (v > bv) {
-        bv = v;
-        bc = (int)cid;
-      }
+  for (int j = threadIdx.x; j < cta_cids; j += blockDim.x) {
+    const int64_t cid = cid0 + j;
+    if (cid >= p.k) break;
+    const float v = rho[j];
+    if (v > bv) {
+      bv = v;
+      bc = (int)cid;
     }
   }
 #pragma unroll
@@ -544,33 +530,19 @@ __device__ __forceinline__ void screen_epilogue(const ScreenParams& p, ScreenSha
     gpost = sh.post;
   }
   if (p.pass >= 0) {
-    pass_epilogue(p, sh, rho, obj, z, re - rb, gv, gc, gpost, smax, span_slots);
+    pass_epilogue(p, sh, rho, obj, z, re - rb, gv, gc, gpost);
     return;
   }
 
   // ---- rigorous fp32 window and candidate collection ----
   const double thr = (double)gv - 2.0 * window_eps(p, obj, re - rb);
   if (gpost != 0) {
-    if (smax) {  // only spans whose maximum reaches the window hold candidates
-      const int nsp = cta_cids / span_slots;
-      for (int sp = warp; sp < nsp; sp += nwarps) {
-        if ((double)smax[sp] < thr) continue;
-        for (int j = sp * span_slots + lane; j < (sp + 1) * span_slots; j += 32) {
-          const int64_t cid = cid0 + j;
-          if (cid < p.k && (double)rho[j] >= thr) {
-            const int s = atomicAdd(&sh.cnt, 1);
-            if (s < kMaxC) sh.cand[s] = (int)cid;
-          }
-        }
-      }
-    } else {
-      for (int j = threadIdx.x; j < cta_cids; j += blockDim.x) {
-        const int64_t cid = cid0 + j;
-        if (cid >= p.k) break;
-        if ((double)rho[j] >= thr) {
-          const int s = atomicAdd(&sh.cnt, 1);
-          if (s < kMaxC) sh.cand[s] = (int)cid;
-        }
+    for (int j = threadIdx.x; j < cta_cids; j += blockDim.x) {
+      const int64_t cid = cid0 + j;
+      if (cid >= p.k) break;
+      if ((double)rho[j] >= thr) {
+        const int s = atomicAdd(&sh.cnt, 1);
+        if (s < kMaxC) sh.cand[s] = (int)cid;
       }
     }
   }
@@ -622,10 +594,6 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
   int4* s_ent = reinterpret_cast<int4*>(rho + cta_cids);
   uint16_t* s_pos = reinterpret_cast<uint16_t*>(s_ent + p.rowcap);
   uint8_t* s_lp = reinterpret_cast<uint8_t*>(s_pos + p.rowcap);
-  // per span: its best screen value and that slot (smallest on ties), from
-  // the finished registers — the epilogue's argmax and window read these
-  float* s_smax = reinterpret_cast<float*>(s_lp + ((p.rowcap + 15) & ~15));
-  int* s_sarg = reinterpret_cast<int*>(s_smax + p.cta_blocks / RR);
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -817,31 +785,12 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
       }
 #pragma unroll
       for (int r = 0; r < RR; ++r) rho[(sp * RR + r) * 32 + lane] = acc[r];
-      if (c0 + p.rowcap >= re) {  // the row's last piece: the span's sums are final
-        float bv = -INFINITY;
-        int bc = INT_MAX;
-#pragma unroll
-        for (int r = 0; r < RR; ++r) {
-          const int64_t slot = (gb + r) * 32 + lane;
-          if (slot < p.k && acc[r] > bv) {
-            bv = acc[r];
-            bc = (int)slot;
-          }
-        }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1)
-          better(bv, bc, __shfl_xor_sync(kFull, bv, off), __shfl_xor_sync(kFull, bc, off));
-        if (lane == 0) {
-          s_smax[sp] = bv;
-          s_sarg[sp] = bc;
-        }
-      }
     }
     c0 += p.rowcap;
   } while (c0 < re);
   __syncthreads();
 
-  screen_epilogue(p, sh, rho, obj, z, rb, re, post, s_smax, s_sarg, RR * 32);
+  screen_epilogue(p, sh, rho, obj, z, rb, re, post);
 }
 
 // ---------------------------------------------------------------------------
@@ -1780,13 +1729,12 @@ int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
   pl.mode = 0;
   pl.rr = rr > 0 ? rr : (nblk >= 32 ? 8 : 2);
   pl.rowcap = rowcap < kMaxChunks * 32 ? rowcap : kMaxChunks * 32;  // staging counts cap
-  // staged entries (16 + 2 + 1 bytes each, 16-B aligned) + the span maxima
-  const size_t stage = (size_t)pl.rowcap * kEntryBytes + 16;
+  const size_t stage = (size_t)pl.rowcap * kEntryBytes;
   pl.nsplit = 0;
   for (int s = 1; s <= kMaxSplit; ++s) {
     int64_t cb = (nblk + s - 1) / s;
     cb = (cb + pl.rr - 1) / pl.rr * pl.rr;
-    const size_t smem = (size_t)cb * 128 + stage + (size_t)(cb / pl.rr) * 8;
+    const size_t smem = (size_t)cb * 128 + stage;
     if (smem <= (size_t)smem_limit) {
       pl.nsplit = s;
       pl.cta_blocks = (int)cb;
@@ -1808,7 +1756,7 @@ int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
     cb = (cb + pl.rr - 1) / pl.rr * pl.rr;
     pl.nsplit = (int)((nblk + cb - 1) / cb);
     pl.cta_blocks = (int)cb;
-    pl.smem = (size_t)cb * 128 + stage + (size_t)(cb / pl.rr) * 8;
+    pl.smem = (size_t)cb * 128 + stage;
     pl.passes = pl.nsplit > 1;
   }
   const int best_w = choose_warps(pl.cta_blocks / pl.rr, pl.smem);

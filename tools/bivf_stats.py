@@ -68,6 +68,20 @@ def main():
         "sum_nc": int(nc.sum().item()),
         "sum_nc_in_prefix": int((cnt * inpre).sum().item()),
     }
+    # object blocking potential: dense-prefix bytes a tile of B consecutive
+    # objects (the screen's longest-first order) reads if each distinct term's
+    # spans are fetched once per tile, against once per object
+    terms = eng.dd.terms.long()
+    rows = torch.repeat_interleave(torch.arange(ds.n, device=terms.device),
+                                   eng.dd.row_ptr[1:] - eng.dd.row_ptr[:-1])
+    rank = torch.empty(ds.n, dtype=torch.int64, device=terms.device)
+    rank[eng.order.long()] = torch.arange(ds.n, device=terms.device)
+    single = float(dpre[terms].sum())
+    tiles = {}
+    for B in (2, 4, 8, 16):
+        key = torch.unique((rank[rows] // B) * D + terms)
+        tiles[B] = float(dpre[key % D].sum()) / max(single, 1.0)
+    out["dense_span_reads_tiled_fraction"] = tiles
     hist = torch.bincount(cnt[~inpre & (cnt > 0)].flatten(), minlength=257)[:40].tolist()
     out["masked_nonempty_span_fill_hist"] = hist
     print(json.dumps(out), flush=True)
