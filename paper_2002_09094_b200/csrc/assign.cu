@@ -729,12 +729,12 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
         {
           // dense-prefix entries: span gb>>3 starts 256*(gb>>3) values into the
           // term's run; kDepth entries' values in flight, then their FMAs
-          using SV = SpanVals<RR, HALF, HALF && MAXREG == 56>;
+          using SV = SpanVals<RR, HALF, HALF && MAXREG <= 56>;
           const uint32_t r0 = gb32 & (kSpan - 1);
           const char* pl =
               static_cast<const char*>(pv) + SV::lane_bytes(32u * (gb32 - r0), r0, lane);
           const int2* dl = reinterpret_cast<const int2*>(s_ent) + 1;  // {base, value}
-          constexpr int kDepth = HALF ? 8 : 2;
+          constexpr int kDepth = HALF ? (MAXREG < 56 ? 6 : 8) : 2;
           int e = 0;
           for (; e + kDepth <= nd; e += kDepth) {
             SV q[kDepth];
@@ -770,7 +770,7 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
           MaskPack<RR> mk;
           uint32_t o;
           ld(nd, mk, o);
-          SpanVals<RR, HALF, HALF && MAXREG == 56> A, B;
+          SpanVals<RR, HALF, HALF && MAXREG <= 56> A, B;
           A.gather(mk, o, gb32, pv, lane, lanebit, lt);
           ld(nd + 1, mk, o);
           for (int e = nd; e < cn; e += 2) {
@@ -1768,15 +1768,18 @@ int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
 
 // The instantiation launch_screen picks for a plan (56 registers for the
 // small fp16 CTAs, 64 otherwise).
+static int g_small_maxreg = 56;  // register cap of the small fp16 CTAs (56 or 48)
 int plan_maxreg(const Plan& pl, bool half) {
-  return (!pl.tma && half && pl.rr == 8 && pl.warps <= 4) ? 56 : 64;
+  return (!pl.tma && half && pl.rr == 8 && pl.warps <= 4) ? g_small_maxreg : 64;
 }
 
 template <int RR>
 int launch_screen(const Plan& pl, const ScreenParams& p, cudaStream_t st) {
   auto fn = pl.mode == 1 ? screen_tma_kernel
                          : (pl.mode == 2 ? screen_async_kernel
-                                         : (p.half ? (plan_maxreg(pl, true) == 56
+                                         : (p.half ? (plan_maxreg(pl, true) == 48
+                                                          ? screen_kernel<RR, true, 48>
+                                                          : plan_maxreg(pl, true) == 56
                                                           ? screen_kernel<RR, true, 56>
                                                           : screen_kernel<RR, true>)
                                                    : screen_kernel<RR, false>));
@@ -1909,6 +1912,10 @@ extern "C" void ivfkm_set_screen_warps(int warps) {
 extern "C" int ivfkm_set_screen_option(int which, int value) {
   switch (which) {
     case 1: g_passes = value < 0 ? 0 : (value > 4096 ? 4096 : value); return IVFKM_OK;
+    case 2:  // register cap of the small fp16 CTAs
+      if (value != 56 && value != 48) return IVFKM_E_ARG;
+      g_small_maxreg = value;
+      return IVFKM_OK;
     default: return IVFKM_E_ARG;
   }
 }

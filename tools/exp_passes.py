@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--pf", default="0")
     ap.add_argument("--warps", default="0")
+    ap.add_argument("--rowcap", default="0", help="0: the engine's")
+    ap.add_argument("--maxreg", default="56", help="small-CTA register cap: 56,48")
     a = ap.parse_args()
     c = synth.CONFIGS[a.config]
     ds = synth.make_dataset(c["corpus"])
@@ -36,9 +38,15 @@ def main():
     import itertools
 
     from bench import Clocks
-    for r, pf, w in itertools.product(map(int, a.passes.split(",")), map(int, a.pf.split(",")),
-                                      map(int, a.warps.split(","))):
+    rc0 = eng.rowcap
+    for r, pf, w, rc, mr in itertools.product(map(int, a.passes.split(",")),
+                                              map(int, a.pf.split(",")),
+                                              map(int, a.warps.split(",")),
+                                              map(int, a.rowcap.split(",")),
+                                              map(int, a.maxreg.split(","))):
         eng.lib.ivfkm_set_screen_warps(w)
+        eng.rowcap = rc or rc0
+        eng.lib.ivfkm_set_screen_option(2, mr)
         eng.passes = r if r > 0 else None  # 0: the engine's plan
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         ts = []
@@ -49,9 +57,11 @@ def main():
             ts.append(ev[0].elapsed_time(ev[1]))
         st = eng.read_stats()
         ck = clk.stop() or {}
-        print(json.dumps({"sm_mhz": ck.get("sm_mhz"), "reasons": ck.get("reasons"), "config": a.config, "passes": r, "planned": eng.screen_passes(dm), "pf": pf, "warps": w, "screen_ms": min(ts), "all": ts,
+        print(json.dumps({"sm_mhz": ck.get("sm_mhz"), "reasons": ck.get("reasons"), "config": a.config, "passes": r, "planned": eng.screen_passes(dm), "warps": w, "rowcap": eng.rowcap,
+                          "maxreg": mr, "screen_ms": min(ts), "all": ts,
                           "postings": st.postings}), flush=True)
     eng.lib.ivfkm_set_screen_warps(0)
+    eng.lib.ivfkm_set_screen_option(2, 56)
 
 
 if __name__ == "__main__":
