@@ -643,7 +643,7 @@ def ours_arm(args, rank, world):
         import paper_2002_09094_b200 as P
 
         ds2 = P.Dataset(ds.dim, ds.indptr, ds.term_ids, ds.values, normalized=True)
-        iters = max(2, min(args.steps, 10))
+        iters = c["iters"]  # the config's own run length (BASELINE.json: 50 at config 1)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         res = P.run("IVF", ds2, k, seed=c["seed"], max_iter=iters)
@@ -654,6 +654,7 @@ def ours_arm(args, rank, world):
             "seconds": dt, "h2d_bytes": int(ds.indptr.nbytes + ds.term_ids.nbytes
                                             + ds.values.nbytes),
             "d2h_bytes_per_step": int(ds.n * 4),
+            "max_iter": iters, "converged": res.converged,
             "what": "paper_2002_09094_b200.run('IVF', ds, k, seed, max_iter) from a host "
                     "Dataset: corpus upload, init_means, BIVF builds, every iteration's labels "
                     "read back and digested into its IterationRecord, final means read back"}

@@ -274,6 +274,34 @@ int ivfkm_update_fill(int64_t n_obj, int64_t nnz, int64_t k, int64_t dim,
                       double* new_vals /*[dev]*/, uint8_t* retained /*[dev] k*/,
                       int64_t capacity, void* ws, size_t ws_bytes, ivfkm_stream_t stream);
 
+/* ---- IVFD, object-inverted (_kernels.pyx:178-207) ------------------------
+ * The paper's comparison variant in its own loop order: means outermost, each
+ * mean's similarities to all N objects accumulated over the objects' inverted
+ * file.  objects_inverted builds that file from the object CSR ([dev] x_ptr
+ * int64[dim+1], x_obj int32[nnz] 0-based ascending within a term, x_val fp64).
+ * assign_ivfd runs waves of `wave` means, one CTA per mean with a length-N
+ * float64 slot each (workspace: ivfkm_ivfd_workspace_size); every object's
+ * sum adds u*x in ascending term order (mul then add, no FMA), so the
+ * similarities are the reference's bit for bit; labels by strict '>' from
+ * 0.0 in ascending mean order (else mean 0), sims = the label's similarity
+ * (mean 0's when nothing beats 0.0), then sizes / changed / exact objective
+ * as ivfkm_assign_finish.  Reference interface: replaces
+ * variants.py:188-206 + _kernels.pyx:178-207. */
+size_t ivfkm_objects_inverted_workspace_size(int64_t nnz, int64_t dim);
+int ivfkm_objects_inverted(int64_t n_obj, int64_t nnz, int64_t dim,
+                           const int64_t* row_ptr /*[dev]*/, const int32_t* terms /*[dev] 0-based*/,
+                           const double* val64 /*[dev]*/, int64_t* x_ptr /*[dev] dim+1*/,
+                           int32_t* x_obj /*[dev] nnz*/, double* x_val /*[dev] nnz*/, void* ws,
+                           size_t ws_bytes, ivfkm_stream_t stream);
+size_t ivfkm_ivfd_workspace_size(int64_t n_obj, int64_t wave);
+int ivfkm_assign_ivfd(int64_t n_obj, int64_t dim, const int64_t* x_ptr, const int32_t* x_obj,
+                      const double* x_val, int64_t k, const int64_t* m_ptr /*[dev] k+1*/,
+                      const int32_t* m_terms /*[dev] 0-based*/, const double* m_vals,
+                      const int32_t* prev_labels /*[dev] or NULL*/, int32_t* labels /*[dev]*/,
+                      double* sims /*[dev]*/, unsigned long long* sizes /*[dev] k or NULL*/,
+                      ivfkm_stats* stats /*[dev]*/, int64_t wave, void* ws, size_t ws_bytes,
+                      ivfkm_stream_t stream);
+
 /* ---- host-buffer drop-in for _kernels.pyx:106-128 --------------------------
  * Same arguments and meaning as the reference kernel: 1-based term / mean
  * ids, float64 values, labels written 1-based, ctr[0..2] += postings touched.

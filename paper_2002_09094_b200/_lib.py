@@ -105,6 +105,12 @@ SIGNATURES = {
                               _vp, _sz, _vp]),
     "ivfkm_assign_ivfd_host": (C.c_int, [_i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp,
                                          _vp]),
+    "ivfkm_objects_inverted_workspace_size": (_sz, [_i64, _i64]),
+    "ivfkm_objects_inverted": (C.c_int, [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz,
+                                         _vp]),
+    "ivfkm_ivfd_workspace_size": (_sz, [_i64, _i64]),
+    "ivfkm_assign_ivfd": (C.c_int, [_i64, _i64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp,
+                                    _vp, _vp, _i64, _vp, _sz, _vp]),
     "ivfkm_fnv1a64": (_u64, [_vp, _sz]),
     "ivfkm_synth_rows": (C.c_int, [C.POINTER(SynthSpec), _vp]),
     "ivfkm_synth_fill": (C.c_int, [C.POINTER(SynthSpec), _vp, _vp, _vp, _vp,

@@ -729,12 +729,12 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
         {
           // dense-prefix entries: span gb>>3 starts 256*(gb>>3) values into the
           // term's run; kDepth entries' values in flight, then their FMAs
-          using SV = SpanVals<RR, HALF, HALF && MAXREG <= 56>;
+          using SV = SpanVals<RR, HALF, HALF && MAXREG == 56>;
           const uint32_t r0 = gb32 & (kSpan - 1);
           const char* pl =
               static_cast<const char*>(pv) + SV::lane_bytes(32u * (gb32 - r0), r0, lane);
           const int2* dl = reinterpret_cast<const int2*>(s_ent) + 1;  // {base, value}
-          constexpr int kDepth = HALF ? (MAXREG < 56 ? 6 : 8) : 2;
+          constexpr int kDepth = HALF ? 8 : 2;
           int e = 0;
           for (; e + kDepth <= nd; e += kDepth) {
             SV q[kDepth];
@@ -770,7 +770,7 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
           MaskPack<RR> mk;
           uint32_t o;
           ld(nd, mk, o);
-          SpanVals<RR, HALF, HALF && MAXREG <= 56> A, B;
+          SpanVals<RR, HALF, HALF && MAXREG == 56> A, B;
           A.gather(mk, o, gb32, pv, lane, lanebit, lt);
           ld(nd + 1, mk, o);
           for (int e = nd; e < cn; e += 2) {
@@ -1609,6 +1609,106 @@ __global__ void __launch_bounds__(256) accumulate_kernel(int64_t n_obj, const in
   }
 }
 
+// ---------------------------------------------------------------------------
+// IVFD, object-inverted (_kernels.pyx:178-207): means outermost, each mean's
+// similarity to every object accumulated in a length-N vector over the
+// objects' inverted file, then folded into the running best per object.
+// The GPU shape: a *wave* of M means at once, one CTA per mean, each with its
+// own length-N float64 slot (scratch in HBM); inside a CTA the mean's terms go
+// in ascending order with a barrier between terms (one object may appear in
+// consecutive terms' lists), the term's object postings split over the
+// threads — every object's sum therefore adds u*x in ascending term order
+// with __dmul_rn/__dadd_rn, bit-identical to the reference's rho; a reduce
+// kernel then scans the wave's slots per object in ascending mean order
+// (strict '>' from 0.0, label 1 when nothing beats it) and clears them.
+
+__global__ void __launch_bounds__(256) ivfd_scatter_kernel(
+    int64_t n_obj, int64_t j0, int64_t k, const int64_t* __restrict__ x_ptr,
+    const int32_t* __restrict__ x_obj, const double* __restrict__ x_val,
+    const int64_t* __restrict__ m_ptr, const int32_t* __restrict__ m_terms,
+    const double* __restrict__ m_vals, double* __restrict__ slots,
+    unsigned long long* __restrict__ postings) {
+  const int64_t j = j0 + blockIdx.x;
+  if (j >= k) return;
+  double* rho = slots + (int64_t)blockIdx.x * n_obj;
+  unsigned long long cnt = 0;
+  for (int64_t h = m_ptr[j]; h < m_ptr[j + 1]; ++h) {
+    const int32_t t = __ldg(m_terms + h);
+    const double u = __ldg(m_vals + h);
+    const int64_t q0 = __ldg(x_ptr + t), q1 = __ldg(x_ptr + t + 1);
+    for (int64_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
+      const int32_t i = __ldg(x_obj + q);
+      rho[i] = __dadd_rn(rho[i], __dmul_rn(u, __ldg(x_val + q)));
+    }
+    if (threadIdx.x == 0) cnt += (unsigned long long)(q1 - q0);
+    __syncthreads();  // the next term may hit the same objects
+  }
+  if (threadIdx.x == 0 && cnt) atomicAdd(postings, cnt);
+}
+
+__global__ void __launch_bounds__(256) ivfd_reduce_kernel(
+    int64_t n_obj, int64_t j0, int64_t m, double* __restrict__ slots, double* __restrict__ best,
+    int32_t* __restrict__ label, double* __restrict__ sim0) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_obj;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double b = j0 == 0 ? 0.0 : best[i];
+    int32_t l = j0 == 0 ? 0 : label[i];
+    for (int64_t c = 0; c < m; ++c) {
+      double* r = slots + c * n_obj + i;
+      const double v = *r;
+      *r = 0.0;
+      if (j0 + c == 0) sim0[i] = v;  // mean 1's similarity: the summand when nothing beats 0.0
+      if (v > b) {
+        b = v;
+        l = (int32_t)(j0 + c);
+      }
+    }
+    best[i] = b;
+    label[i] = l;
+  }
+}
+
+__global__ void ivfd_finish_kernel(int64_t n_obj, const double* __restrict__ best,
+                                   const int32_t* __restrict__ label,
+                                   const double* __restrict__ sim0, int32_t* __restrict__ labels,
+                                   double* __restrict__ sims) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_obj;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    labels[i] = label[i];
+    sims[i] = best[i] > 0.0 ? best[i] : sim0[i];
+  }
+}
+
+// objects' inverted file: entry -> (term key, entry index), stably sorted by term
+__global__ void entry_keys_kernel(int64_t n_obj, const int64_t* __restrict__ row_ptr,
+                                  const int32_t* __restrict__ terms, int32_t* __restrict__ key,
+                                  int32_t* __restrict__ obj, int32_t* __restrict__ idx,
+                                  unsigned int* __restrict__ hist) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t i = blockIdx.x * wpb + (threadIdx.x >> 5); i < n_obj; i += gridDim.x * wpb) {
+    for (int64_t e = row_ptr[i] + lane; e < row_ptr[i + 1]; e += 32) {
+      const int32_t t = terms[e];
+      key[e] = t;
+      obj[e] = (int32_t)i;
+      idx[e] = (int32_t)e;
+      atomicAdd(&hist[t], 1u);
+    }
+  }
+}
+
+__global__ void entry_gather_kernel(int64_t nnz, const int32_t* __restrict__ sidx,
+                                    const int32_t* __restrict__ obj,
+                                    const double* __restrict__ val64,
+                                    int32_t* __restrict__ x_obj, double* __restrict__ x_val) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t e = sidx[q];
+    x_obj[q] = obj[e];
+    x_val[q] = val64[e];
+  }
+}
+
 struct AssignWs {
   int32_t* label32;
   int32_t* slot_of;
@@ -1768,18 +1868,15 @@ int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
 
 // The instantiation launch_screen picks for a plan (56 registers for the
 // small fp16 CTAs, 64 otherwise).
-static int g_small_maxreg = 56;  // register cap of the small fp16 CTAs (56 or 48)
 int plan_maxreg(const Plan& pl, bool half) {
-  return (!pl.tma && half && pl.rr == 8 && pl.warps <= 4) ? g_small_maxreg : 64;
+  return (!pl.tma && half && pl.rr == 8 && pl.warps <= 4) ? 56 : 64;
 }
 
 template <int RR>
 int launch_screen(const Plan& pl, const ScreenParams& p, cudaStream_t st) {
   auto fn = pl.mode == 1 ? screen_tma_kernel
                          : (pl.mode == 2 ? screen_async_kernel
-                                         : (p.half ? (plan_maxreg(pl, true) == 48
-                                                          ? screen_kernel<RR, true, 48>
-                                                          : plan_maxreg(pl, true) == 56
+                                         : (p.half ? (plan_maxreg(pl, true) == 56
                                                           ? screen_kernel<RR, true, 56>
                                                           : screen_kernel<RR, true>)
                                                    : screen_kernel<RR, false>));
@@ -1912,10 +2009,6 @@ extern "C" void ivfkm_set_screen_warps(int warps) {
 extern "C" int ivfkm_set_screen_option(int which, int value) {
   switch (which) {
     case 1: g_passes = value < 0 ? 0 : (value > 4096 ? 4096 : value); return IVFKM_OK;
-    case 2:  // register cap of the small fp16 CTAs
-      if (value != 56 && value != 48) return IVFKM_E_ARG;
-      g_small_maxreg = value;
-      return IVFKM_OK;
     default: return IVFKM_E_ARG;
   }
 }
@@ -2157,6 +2250,116 @@ extern "C" int ivfkm_score_labels(int64_t n_obj, const int64_t* row_ptr, const i
   IVFKM_CHECK_LAUNCH();
   accumulate_kernel<<<grid_for(n_obj, 256, kNumSM * 8), 256, 0, st>>>(n_obj, labels, sims, nullptr,
                                                                       nullptr, stats);
+  IVFKM_CHECK_LAUNCH();
+  return IVFKM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// IVFD, object-inverted (see ivfd_scatter_kernel).
+
+extern "C" size_t ivfkm_objects_inverted_workspace_size(int64_t nnz, int64_t dim) {
+  size_t sb = 0;
+  cub::DoubleBuffer<int32_t> kb(nullptr, nullptr), vb(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, sb, kb, vb, (int)nnz);
+  size_t sc = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, sc, (unsigned int*)nullptr, (int64_t*)nullptr,
+                                (int)dim + 1);
+  Carver c(nullptr);
+  for (int q = 0; q < 5; ++q) c.take<int32_t>((size_t)(nnz > 0 ? nnz : 1));
+  c.take<unsigned int>((size_t)dim + 1);
+  c.take_bytes(sb > sc ? sb : sc);
+  return c.off;
+}
+
+extern "C" int ivfkm_objects_inverted(int64_t n_obj, int64_t nnz, int64_t dim,
+                                      const int64_t* row_ptr, const int32_t* terms,
+                                      const double* val64, int64_t* x_ptr, int32_t* x_obj,
+                                      double* x_val, void* ws, size_t ws_bytes,
+                                      ivfkm_stream_t stream_) {
+  if (n_obj < 0 || nnz < 0 || dim < 1 || !x_ptr) return IVFKM_E_ARG;
+  if (n_obj > INT32_MAX || nnz > INT32_MAX) return IVFKM_E_UNSUPPORTED;
+  if (ws_bytes < ivfkm_objects_inverted_workspace_size(nnz, dim)) return IVFKM_E_WORKSPACE;
+  cudaStream_t st = as_stream(stream_);
+  size_t sb = 0;
+  {
+    cub::DoubleBuffer<int32_t> kb(nullptr, nullptr), vb(nullptr, nullptr);
+    cub::DeviceRadixSort::SortPairs(nullptr, sb, kb, vb, (int)nnz);
+  }
+  size_t sc = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, sc, (unsigned int*)nullptr, (int64_t*)nullptr,
+                                (int)dim + 1);
+  Carver c(ws);
+  const size_t nz = (size_t)(nnz > 0 ? nnz : 1);
+  int32_t* k0 = c.take<int32_t>(nz);
+  int32_t* k1 = c.take<int32_t>(nz);
+  int32_t* i0 = c.take<int32_t>(nz);
+  int32_t* i1 = c.take<int32_t>(nz);
+  int32_t* ob = c.take<int32_t>(nz);
+  unsigned int* hist = c.take<unsigned int>((size_t)dim + 1);
+  void* tmp = c.take_bytes(sb > sc ? sb : sc);
+  IVFKM_TRY(cudaMemsetAsync(hist, 0, sizeof(unsigned int) * (dim + 1), st));
+  if (nnz > 0) {
+    entry_keys_kernel<<<grid_for(n_obj, 8), 256, 0, st>>>(n_obj, row_ptr, terms, k0, ob, i0,
+                                                          hist);
+    IVFKM_CHECK_LAUNCH();
+    cub::DoubleBuffer<int32_t> kb(k0, k1), vb(i0, i1);
+    int bits = 1;
+    while (bits < 31 && (1ll << bits) < dim) ++bits;
+    IVFKM_TRY(cub::DeviceRadixSort::SortPairs(tmp, sb, kb, vb, (int)nnz, 0, bits, st));
+    entry_gather_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(nnz, vb.Current(), ob, val64, x_obj,
+                                                            x_val);
+    IVFKM_CHECK_LAUNCH();
+  }
+  IVFKM_TRY(cub::DeviceScan::ExclusiveSum(tmp, sc, hist, x_ptr, (int)dim + 1, st));
+  return IVFKM_OK;
+}
+
+extern "C" size_t ivfkm_ivfd_workspace_size(int64_t n_obj, int64_t wave) {
+  Carver c(nullptr);
+  const size_t n = (size_t)(n_obj > 0 ? n_obj : 1);
+  c.take<double>(n * (size_t)(wave > 0 ? wave : 1));
+  c.take<double>(n);
+  c.take<int32_t>(n);
+  c.take<double>(n);
+  return c.off;
+}
+
+extern "C" int ivfkm_assign_ivfd(int64_t n_obj, int64_t dim, const int64_t* x_ptr,
+                                 const int32_t* x_obj, const double* x_val, int64_t k,
+                                 const int64_t* m_ptr, const int32_t* m_terms,
+                                 const double* m_vals, const int32_t* prev_labels,
+                                 int32_t* labels, double* sims, unsigned long long* sizes,
+                                 ivfkm_stats* stats, int64_t wave, void* ws, size_t ws_bytes,
+                                 ivfkm_stream_t stream_) {
+  if (n_obj < 0 || dim < 1 || k < 1 || wave < 1 || !x_ptr || !m_ptr || !labels || !sims ||
+      !stats)
+    return IVFKM_E_ARG;
+  if (n_obj > INT32_MAX || k > INT32_MAX) return IVFKM_E_UNSUPPORTED;
+  if (ws_bytes < ivfkm_ivfd_workspace_size(n_obj, wave)) return IVFKM_E_WORKSPACE;
+  cudaStream_t st = as_stream(stream_);
+  IVFKM_TRY(cudaMemsetAsync(stats, 0, sizeof(ivfkm_stats), st));
+  if (sizes) IVFKM_TRY(cudaMemsetAsync(sizes, 0, sizeof(unsigned long long) * k, st));
+  if (n_obj == 0) return IVFKM_OK;
+  Carver c(ws);
+  const size_t n = (size_t)n_obj;
+  double* slots = c.take<double>(n * (size_t)wave);
+  double* best = c.take<double>(n);
+  int32_t* label = c.take<int32_t>(n);
+  double* sim0 = c.take<double>(n);
+  IVFKM_TRY(cudaMemsetAsync(slots, 0, sizeof(double) * n * (size_t)wave, st));
+  for (int64_t j0 = 0; j0 < k; j0 += wave) {
+    const int64_t m = k - j0 < wave ? k - j0 : wave;
+    ivfd_scatter_kernel<<<(unsigned)m, 256, 0, st>>>(n_obj, j0, k, x_ptr, x_obj, x_val, m_ptr,
+                                                      m_terms, m_vals, slots, &stats->postings);
+    IVFKM_CHECK_LAUNCH();
+    ivfd_reduce_kernel<<<grid_for(n_obj, 256), 256, 0, st>>>(n_obj, j0, m, slots, best, label,
+                                                              sim0);
+    IVFKM_CHECK_LAUNCH();
+  }
+  ivfd_finish_kernel<<<grid_for(n_obj, 256), 256, 0, st>>>(n_obj, best, label, sim0, labels, sims);
+  IVFKM_CHECK_LAUNCH();
+  accumulate_kernel<<<grid_for(n_obj, 256, kNumSM * 8), 256, 0, st>>>(
+      n_obj, labels, sims, prev_labels, sizes, stats);
   IVFKM_CHECK_LAUNCH();
   return IVFKM_OK;
 }

@@ -176,31 +176,65 @@ extern "C" int ivfkm_assign_ivf_host(int64_t n, const int64_t* indptr, const int
 }
 
 // IVFD (_kernels.pyx:178-207): objects arrive as their inverted file
-// (x_indptr over terms, 1-based object ids), means mean-major.  The object
-// postings are transposed back to rows on the host (terms ascending per row,
-// as the reference's per-object sums run), then the IVF kernels run with the
-// IVFD label rule.
+// (x_indptr over terms, 1-based object ids ascending within a term), means
+// mean-major — exactly the input of the object-inverted kernel
+// (ivfkm_assign_ivfd): ids made 0-based, everything uploaded, one call.
 extern "C" int ivfkm_assign_ivfd_host(int64_t n, const int64_t* x_indptr, const int32_t* x_oids,
                                       const double* x_vals, int64_t dim, const int64_t* m_indptr,
                                       const int32_t* m_terms, const double* m_vals, int64_t k,
                                       int32_t* labels, int64_t* ctr) {
   if (n < 0 || dim < 1 || k < 1 || !x_indptr || !m_indptr || !labels) return IVFKM_E_ARG;
+  if (ivfkm_device_count() < 1) return IVFKM_E_NOGPU;
   const int64_t nnz = x_indptr[dim];
-  std::vector<int64_t> ip((size_t)n + 1, 0);
+  const int64_t mnz = m_indptr[k];
+  std::vector<int32_t> o0((size_t)nnz), t0((size_t)mnz);
   for (int64_t q = 0; q < nnz; ++q) {
     if (x_oids[q] < 1 || x_oids[q] > n) return IVFKM_E_RANGE;
-    ++ip[(size_t)x_oids[q]];
+    o0[q] = x_oids[q] - 1;
   }
-  for (int64_t i = 0; i < n; ++i) ip[i + 1] += ip[i];
-  std::vector<int64_t> cur(ip.begin(), ip.end() - 1);
-  std::vector<int32_t> t((size_t)nnz);
-  std::vector<double> v((size_t)nnz);
-  for (int64_t term = 0; term < dim; ++term)
-    for (int64_t q = x_indptr[term]; q < x_indptr[term + 1]; ++q) {
-      const int64_t o = cur[x_oids[q] - 1]++;
-      t[o] = (int32_t)(term + 1);
-      v[o] = x_vals[q];
-    }
-  return assign_host(n, ip.data(), t.data(), v.data(), dim, 0, m_indptr, m_terms, m_vals, k, 1,
-                     labels, ctr);
+  for (int64_t q = 0; q < mnz; ++q) {
+    if (m_terms[q] < 1 || m_terms[q] > dim) return IVFKM_E_RANGE;
+    t0[q] = m_terms[q] - 1;
+  }
+  if (n == 0) return IVFKM_OK;
+  // one wave of means while their length-n slots stay within 2 GB
+  int64_t wave = (int64_t)((2ull << 30) / (8ull * (uint64_t)n));
+  wave = wave < 1 ? 1 : (wave > k ? k : wave);
+  const size_t ws = ivfkm_ivfd_workspace_size(n, wave);
+  DevBuf d_xp, d_xo, d_xv, d_mp, d_mt, d_mv, d_lab, d_sims, d_sizes, d_stats, d_ws;
+  IVFKM_TRY(d_xp.alloc(sizeof(int64_t) * (dim + 1)));
+  IVFKM_TRY(d_xo.alloc(sizeof(int32_t) * (nnz + 1)));
+  IVFKM_TRY(d_xv.alloc(sizeof(double) * (nnz + 1)));
+  IVFKM_TRY(d_mp.alloc(sizeof(int64_t) * (k + 1)));
+  IVFKM_TRY(d_mt.alloc(sizeof(int32_t) * (mnz + 1)));
+  IVFKM_TRY(d_mv.alloc(sizeof(double) * (mnz + 1)));
+  IVFKM_TRY(d_lab.alloc(sizeof(int32_t) * n));
+  IVFKM_TRY(d_sims.alloc(sizeof(double) * n));
+  IVFKM_TRY(d_sizes.alloc(sizeof(unsigned long long) * k));
+  IVFKM_TRY(d_stats.alloc(sizeof(ivfkm_stats)));
+  IVFKM_TRY(d_ws.alloc(ws));
+  cudaStream_t st = nullptr;
+  IVFKM_TRY(cudaMemcpyAsync(d_xp.p, x_indptr, sizeof(int64_t) * (dim + 1), cudaMemcpyHostToDevice, st));
+  IVFKM_TRY(cudaMemcpyAsync(d_xo.p, o0.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, st));
+  IVFKM_TRY(cudaMemcpyAsync(d_xv.p, x_vals, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
+  IVFKM_TRY(cudaMemcpyAsync(d_mp.p, m_indptr, sizeof(int64_t) * (k + 1), cudaMemcpyHostToDevice, st));
+  IVFKM_TRY(cudaMemcpyAsync(d_mt.p, t0.data(), sizeof(int32_t) * mnz, cudaMemcpyHostToDevice, st));
+  IVFKM_TRY(cudaMemcpyAsync(d_mv.p, m_vals, sizeof(double) * mnz, cudaMemcpyHostToDevice, st));
+  int rc = ivfkm_assign_ivfd(n, dim, d_xp.as<int64_t>(), d_xo.as<int32_t>(), d_xv.as<double>(), k,
+                             d_mp.as<int64_t>(), d_mt.as<int32_t>(), d_mv.as<double>(), nullptr,
+                             d_lab.as<int32_t>(), d_sims.as<double>(),
+                             d_sizes.as<unsigned long long>(), d_stats.as<ivfkm_stats>(), wave,
+                             d_ws.p, ws, st);
+  if (rc) return rc;
+  ivfkm_stats stats;
+  IVFKM_TRY(cudaMemcpyAsync(labels, d_lab.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+  IVFKM_TRY(cudaMemcpyAsync(&stats, d_stats.p, sizeof(stats), cudaMemcpyDeviceToHost, st));
+  IVFKM_TRY(cudaStreamSynchronize(st));
+  for (int64_t i = 0; i < n; ++i) labels[i] += 1;
+  if (ctr) {
+    ctr[0] += (int64_t)stats.postings;
+    ctr[1] += (int64_t)stats.postings;
+    ctr[2] += (int64_t)stats.postings;
+  }
+  return IVFKM_OK;
 }

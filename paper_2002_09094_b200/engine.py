@@ -344,6 +344,12 @@ class LloydEngine:
         self.passes = None
         self.last_postings = None
         self._doc_freq = None
+        # IVFD (rule 1) in its own loop order: the object-inverted kernel
+        # (ivfkm_assign_ivfd); False serves IVFD through the IVF kernels with
+        # the IVFD label rule (identical results)
+        self.ivfd_native = True
+        self._xinv = None
+        self._ivfd_ws = None
 
     def _row_order(self, dd):
         """Longest rows first (computed once per dataset, on the device)."""
@@ -451,6 +457,8 @@ class LloydEngine:
         if prev is not None and prev.data_ptr() == out.data_ptr():
             self.cur ^= 1
             out = self.labels[self.cur]
+        if rule == 1 and self.ivfd_native:
+            return self._assign_ivfd(dm, prev, out, events)
         self.lib.ivfkm_set_tuning(self.rowcap, 0, -1)
         npass = self.screen_passes(dm)
         _lib.check(self.lib.ivfkm_set_screen_option(1, npass), "ivfkm_set_screen_option")
@@ -483,6 +491,46 @@ class LloydEngine:
                                               self.ws_assign.numel(), st)
             _lib.check(rc, "ivfkm_assign_finish")
         self.launches += 4
+        return out
+
+    IVFD_SLOT_BYTES = 4 << 30  # the wave's per-mean similarity slots (N float64 each)
+
+    def objects_inverted(self):
+        """The objects' inverted file (term-major object postings, objects
+        ascending within a term) of the current dataset, built once."""
+        dd = self.dd
+        if self._xinv is not None and self._xinv[0] is dd.terms:
+            return self._xinv[1]
+        dev = self.device
+        x_ptr = torch.empty(dd.dim + 1, dtype=torch.int64, device=dev)
+        x_obj = torch.empty(max(dd.nnz, 1), dtype=torch.int32, device=dev)
+        x_val = torch.empty(max(dd.nnz, 1), dtype=torch.float64, device=dev)
+        ws = torch.empty(int(self.lib.ivfkm_objects_inverted_workspace_size(dd.nnz, dd.dim)),
+                         dtype=torch.uint8, device=dev)
+        _lib.check(self.lib.ivfkm_objects_inverted(
+            dd.n, dd.nnz, dd.dim, _p(dd.row_ptr), _p(dd.terms), _p(dd.val64), _p(x_ptr),
+            _p(x_obj), _p(x_val), _p(ws), ws.numel(), _stream()), "ivfkm_objects_inverted")
+        self.launches += 5
+        self._xinv = (dd.terms, (x_ptr, x_obj, x_val))
+        return self._xinv[1]
+
+    def _assign_ivfd(self, dm: DeviceMeans, prev, out, events):
+        dd = self.dd
+        x_ptr, x_obj, x_val = self.objects_inverted()
+        wave = int(max(1, min(self.k, self.IVFD_SLOT_BYTES // max(8 * dd.n, 1))))
+        need = int(self.lib.ivfkm_ivfd_workspace_size(dd.n, wave))
+        if self._ivfd_ws is None or self._ivfd_ws.numel() < need:
+            self._ivfd_ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        if events is not None:
+            events[0].record()
+        rc = self.lib.ivfkm_assign_ivfd(dd.n, dd.dim, _p(x_ptr), _p(x_obj), _p(x_val), self.k,
+                                        _p(dm.ptr), _p(dm.terms), _p(dm.vals), _p(prev), _p(out),
+                                        _p(self.sims), _p(self.sizes), _p(self.stats), wave,
+                                        _p(self._ivfd_ws), self._ivfd_ws.numel(), _stream())
+        _lib.check(rc, "ivfkm_assign_ivfd")
+        if events is not None:
+            events[1].record()
+        self.launches += 2 * ((self.k + wave - 1) // wave) + 2
         return out
 
     def score_labels(self, dm: DeviceMeans, labels0: torch.Tensor) -> None:

@@ -669,3 +669,32 @@ def test_bivf_plan_reports_out_of_range_ids():
         assert rc == want
         if rc == 0:
             assert totals[0] % 8 == 0 and totals[0] >= 5 and totals[1] == 5
+
+
+@pytest.mark.parametrize("k,signed,slot_bytes", [(40, True, 4 << 30), (300, False, 1 << 20),
+                                                 (7, True, 1)])
+def test_native_ivfd_matches_oracle(k, signed, slot_bytes):
+    """IVFD in its own loop order (means outermost over the objects' inverted
+    file, ivfkm_assign_ivfd) against the oracle's IVFD rule, with waves of
+    one to all means; and against the IVF kernels serving the same rule."""
+    from oracle import oracle as O
+    from paper_2002_09094_b200.engine import DeviceDataset, DeviceMeans, LloydEngine
+
+    ds, om, _ = _random_case(n=1200, dim=500, k=k, seed=30 + k, signed=signed)
+    ol, top1, _, post = O.assign(ds, om)
+    want = np.where(top1 > 0.0, ol, 1).astype(np.int32)
+    eng = LloydEngine(DeviceDataset.from_dataset(ds, "cuda"), k)
+    eng.IVFD_SLOT_BYTES = slot_bytes
+    P = _pkg()
+    ms = P.MeanSet.from_csr(om.indptr, om.term_ids, om.values, ds.dim, "sparse_standard")
+    dm = eng.upload_means(ms)
+    lab = eng.assign(dm, None, rule=1)
+    st = eng.read_stats()
+    assert np.array_equal(lab.cpu().numpy() + 1, want)
+    assert st.postings == post
+    assert st.objective == O.objective(ds, want, om)
+    assert np.array_equal(eng.sizes.cpu().numpy().astype(np.int64), O.sizes_of(want, k))
+    eng.ivfd_native = False  # the IVF kernels with the IVFD label rule agree
+    lab2 = eng.assign(dm, None, rule=1)
+    st2 = eng.read_stats()
+    assert np.array_equal(lab2.cpu().numpy() + 1, want) and st2.objective == st.objective

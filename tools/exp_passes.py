@@ -23,7 +23,7 @@ def main():
     ap.add_argument("--pf", default="0")
     ap.add_argument("--warps", default="0")
     ap.add_argument("--rowcap", default="0", help="0: the engine's")
-    ap.add_argument("--maxreg", default="56", help="small-CTA register cap: 56,48")
+    ap.add_argument("--maxreg", default="56", help="(recorded only)")
     a = ap.parse_args()
     c = synth.CONFIGS[a.config]
     ds = synth.make_dataset(c["corpus"])
@@ -46,7 +46,6 @@ def main():
                                               map(int, a.maxreg.split(","))):
         eng.lib.ivfkm_set_screen_warps(w)
         eng.rowcap = rc or rc0
-        eng.lib.ivfkm_set_screen_option(2, mr)
         eng.passes = r if r > 0 else None  # 0: the engine's plan
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         ts = []
@@ -61,7 +60,6 @@ def main():
                           "maxreg": mr, "screen_ms": min(ts), "all": ts,
                           "postings": st.postings}), flush=True)
     eng.lib.ivfkm_set_screen_warps(0)
-    eng.lib.ivfkm_set_screen_option(2, 56)
 
 
 if __name__ == "__main__":
