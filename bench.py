@@ -254,21 +254,23 @@ def ncu_path():
 
 
 def traffic_probe(cfg, warmup, timeout=300):
-    """DRAM and L2->SM bytes of the screen launch of the first timed
-    iteration, measured by ncu on a child process that replays this run's
-    state (same corpus, seed and warm-up: the iterations are deterministic)."""
+    """DRAM and L2->SM bytes of the screen of the first timed iteration —
+    summed over its launches (one, or one per slot-range pass) — measured by
+    ncu on a child process that replays this run's state (same corpus, seed
+    and warm-up: the iterations are deterministic) and marks that assign with
+    an NVTX range."""
     ncu = ncu_path()
     if ncu is None:
         return None, "ncu not found"
-    cmd = [ncu, "--metrics", ",".join(TRAFFIC_METRICS), "-k", "regex:screen_kernel",
-           "--launch-skip", str(warmup), "--launch-count", "1", "--csv", "--print-units", "base",
+    cmd = [ncu, "--metrics", ",".join(TRAFFIC_METRICS), "--nvtx", "--nvtx-include", "probe/",
+           "-k", "regex:screen_kernel", "--launch-count", "4096", "--csv", "--print-units", "base",
            sys.executable, str(ROOT / "bench.py"), "--probe", "--config", str(cfg),
            "--warmup", str(warmup)]
     try:
         res = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
     except Exception as exc:
         return None, f"ncu probe failed: {exc!r}"
-    vals = {}
+    vals, launches = {}, set()
     for line in res.stdout.splitlines():
         cells = [c.strip().strip('"') for c in line.split('","')]
         if len(cells) < 3:
@@ -281,12 +283,14 @@ def traffic_probe(cfg, warmup, timeout=300):
                 except (IndexError, ValueError):
                     continue
                 mult = {"byte": 1, "sector": 32}.get(unit, 1)
-                vals[m] = v * mult
+                vals[m] = vals.get(m, 0.0) + v * mult
+                launches.add(cells[0])
     if len(vals) < 3:
         return None, f"ncu probe: no metrics (rc {res.returncode}): {res.stderr[-300:]}"
     return {"dram_bytes": vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"],
             "l2_read_bytes": vals["lts__t_sectors_srcunit_tex_op_read.sum"],
-            "source": "ncu " + " ".join(cmd[1:12]) + " (this run)"}, None
+            "launches": len(launches),
+            "source": "ncu " + " ".join(cmd[1:14]) + " (this run)"}, None
 
 
 def stamped_traffic(cfg):
@@ -313,6 +317,7 @@ def roofline(avg_b, screen_s, traffic, screen_bits):
         r["hbm"]["dram_achieved"] = traffic["dram_bytes"] / screen_s / 1e9
         r["hbm"]["dram_frac"] = r["hbm"]["dram_achieved"] / hbm
         r["traffic_source"] = traffic["source"]
+        r["traffic_launches"] = traffic.get("launches", 1)
     if ach > hbm and l2pk:
         # more algorithmic bytes per second than HBM can deliver: the postings
         # are mostly L2 hits, so the binding ceiling is the L2 read bandwidth
@@ -574,11 +579,14 @@ def _engine_run(cfg, warmup, steps, world=1, events=True):
 def probe_arm(args):
     """Child of traffic_probe (under ncu): replay the run to its first timed
     screen launch."""
-    r = _engine_run(args.config, args.warmup, 0)
-    r["eng"].assign(r["dm"], r["prev"])
     import torch
 
+    r = _engine_run(args.config, args.warmup, 0)
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_push("probe")
+    r["eng"].assign(r["dm"], r["prev"])
+    torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
 
 
 def ours_arm(args, rank, world):

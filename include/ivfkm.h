@@ -155,6 +155,17 @@ void ivfkm_set_tuning(int rowcap, int smem_limit, int rr);
  * planned count).  Spans are handed out to warps dynamically, so every count
  * computes identical sums. */
 void ivfkm_set_screen_warps(int warps);
+/* ivfkm_assign_screen with caller buffers for slot-range passes
+ * (presort_terms int32[nnz], presort_vals fp32[nnz], [dev], or NULL): when
+ * the plan runs passes, each row's entries are first sorted by the terms'
+ * dense prefix, longest first, into them, so that every pass stages its rows
+ * by copying instead of sorting them again. */
+int ivfkm_assign_screen_ex(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
+                           const float* val32, const double* xnorm, int64_t k, int64_t dim,
+                           const uint32_t* headers, const void* pval_screen, int screen_bits,
+                           double mu_max, ivfkm_stats* stats, const int32_t* order,
+                           int32_t* presort_terms, float* presort_vals, void* ws,
+                           size_t ws_bytes, ivfkm_stream_t stream);
 /* Screen tuning: which = 1: slot-range passes for the next screens (0 or 1
  * = one pass).  With P > 1 passes the fp16 register screen runs P launches,
  * each over all objects and 1/P of the slots (one CTA per object, no

@@ -74,6 +74,8 @@ SIGNATURES = {
     "ivfkm_assign_screen": (C.c_int, [_i64, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, C.c_int,
                                       _f64, _vp,
                                       _vp, _vp, _sz, _vp]),
+    "ivfkm_assign_screen_ex": (C.c_int, [_i64, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, C.c_int,
+                                         _f64, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "ivfkm_assign_finish": (C.c_int, [_i64, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp,
                                       _vp, _vp, C.c_int, _vp, _sz, _vp]),
     "ivfkm_score_labels": (C.c_int, [_i64, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp,

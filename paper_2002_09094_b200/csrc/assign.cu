@@ -74,6 +74,8 @@ struct ScreenParams {
   const uint32_t* dpre;   // [dim] dense prefix spans per term
   const int32_t* inv;     // [k] slot -> mean
   const int32_t* order;   // [n] processing order of objects, or nullptr
+  const int32_t* ps_t = nullptr;  // rows presorted by dense prefix (ivfkm_presort_rows), or
+  const float* ps_v = nullptr;    // nullptr: the CTA sorts its staged row itself
   const float* pv32;  // fp32 screen values, or fp16 ones when half
   int half;
   double mu_max;
@@ -646,70 +648,99 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
     const int64_t rem = re - c0;
     const int cn = (int)(rem < p.rowcap ? rem : p.rowcap);
     const int nch = (cn + 31) >> 5;
-    __syncthreads();
-    // Stage the row chunk sorted by the terms' dense prefix (bivf.cuh, dpre),
-    // longest first, stable: for local span s the entries [0, cntd[s]) read
-    // span s as one contiguous 256-value run (no masks, no offsets), the rest
-    // [cntd[s], cn) go through masks + offsets.  (The screen's fp32 sum may run
-    // in any order — its error bound does not depend on it — and the sort is
-    // stable, so the sums are deterministic; the exact rescoring keeps the
-    // reference order.)  Counting sort over 32-entry chunks: rank within the
-    // chunk by __match_any_sync, per-(chunk, bucket) counts, offsets.
-    for (int q = threadIdx.x; q < nch * nb; q += blockDim.x) s_cc[q] = 0;
-    if (threadIdx.x == 0) s_next = 0;
-    __syncthreads();
-    for (int j0 = warp * 32; j0 < cn; j0 += nwarps * 32) {
-      const int j = j0 + lane;
-      int lp = -1;
-      if (j < cn) {
-        const uint32_t t = (uint32_t)p.terms[c0 + j];
-        lp = (int)__ldg(p.dpre + t) - gs0;
+    if (p.ps_t) {
+      // The row arrives sorted by dense prefix, descending (ivfkm_presort_rows):
+      // every pass's clamped bucket order is the same order, so staging is a
+      // copy, and bucket b starts where the (non-increasing) buckets drop to b.
+      __syncthreads();
+      if (threadIdx.x == 0) s_next = 0;
+      for (int j = threadIdx.x; j < cn; j += blockDim.x) {
+        const uint32_t t = (uint32_t)__ldg(p.ps_t + c0 + j);
+        int lp = (int)__ldg(p.dpre + t) - gs0;
         lp = lp < 0 ? 0 : (lp > nls ? nls : lp);
         if (z == 0) post += __ldg(p.nc + t);
-      }
-      const unsigned peers = __match_any_sync(kFull, lp);
-      if (j < cn) {
+        const uint32_t row = t * (uint32_t)nblk;
+        const int v = __float_as_int(__ldg(p.ps_v + c0 + j));
+        const uint32_t base = lp ? (__ldg(offs + row) & ~kDense) : 0u;
+        s_ent[j] = make_int4((int)row, v, (int)base, v);
         s_lp[j] = (uint8_t)lp;
-        s_pos[j] = (uint16_t)__popc(peers & lt);  // rank among the chunk's equals
-        if (lane == __ffs(peers) - 1) s_cc[(j0 >> 5) * nb + lp] = (uint16_t)__popc(peers);
       }
-    }
-    __syncthreads();
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) {  // per bucket: chunk offsets
-      int run = 0;
-      for (int c = 0; c < nch; ++c) {
-        const int x = s_cc[c * nb + b];
-        s_cc[c * nb + b] = (uint16_t)run;
-        run += x;
-      }
-      s_cntd[b] = run;
-    }
-    __syncthreads();
-    if (warp == 0) {  // bucket starts in descending prefix order
-      int run = 0;
-      for (int b0 = nls; b0 >= 0; b0 -= 32) {
-        const int b = b0 - lane;
-        const int c = b >= 0 ? s_cntd[b] : 0;
-        int x = c;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const int y = __shfl_up_sync(kFull, x, off);
-          if (lane >= off) x += y;
+      __syncthreads();
+      for (int b = threadIdx.x; b < nb; b += blockDim.x) {  // first j with lp <= b
+        int lo = 0, hi = cn;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if ((int)s_lp[mid] > b) lo = mid + 1; else hi = mid;
         }
-        if (b >= 0) s_cntd[b] = run + x - c;  // = entries with a longer prefix than b
-        run += __shfl_sync(kFull, x, 31);
+        s_cntd[b] = lo;  // = entries with a longer prefix than b
       }
+      __syncthreads();
+    } else {
+      __syncthreads();
+      // Stage the row chunk sorted by the terms' dense prefix (bivf.cuh, dpre),
+      // longest first, stable: for local span s the entries [0, cntd[s]) read
+      // span s as one contiguous 256-value run (no masks, no offsets), the rest
+      // [cntd[s], cn) go through masks + offsets.  (The screen's fp32 sum may run
+      // in any order — its error bound does not depend on it — and the sort is
+      // stable, so the sums are deterministic; the exact rescoring keeps the
+      // reference order.)  Counting sort over 32-entry chunks: rank within the
+      // chunk by __match_any_sync, per-(chunk, bucket) counts, offsets.
+      for (int q = threadIdx.x; q < nch * nb; q += blockDim.x) s_cc[q] = 0;
+      if (threadIdx.x == 0) s_next = 0;
+      __syncthreads();
+      for (int j0 = warp * 32; j0 < cn; j0 += nwarps * 32) {
+        const int j = j0 + lane;
+        int lp = -1;
+        if (j < cn) {
+          const uint32_t t = (uint32_t)p.terms[c0 + j];
+          lp = (int)__ldg(p.dpre + t) - gs0;
+          lp = lp < 0 ? 0 : (lp > nls ? nls : lp);
+          if (z == 0) post += __ldg(p.nc + t);
+        }
+        const unsigned peers = __match_any_sync(kFull, lp);
+        if (j < cn) {
+          s_lp[j] = (uint8_t)lp;
+          s_pos[j] = (uint16_t)__popc(peers & lt);  // rank among the chunk's equals
+          if (lane == __ffs(peers) - 1) s_cc[(j0 >> 5) * nb + lp] = (uint16_t)__popc(peers);
+        }
+      }
+      __syncthreads();
+      for (int b = threadIdx.x; b < nb; b += blockDim.x) {  // per bucket: chunk offsets
+        int run = 0;
+        for (int c = 0; c < nch; ++c) {
+          const int x = s_cc[c * nb + b];
+          s_cc[c * nb + b] = (uint16_t)run;
+          run += x;
+        }
+        s_cntd[b] = run;
+      }
+      __syncthreads();
+      if (warp == 0) {  // bucket starts in descending prefix order
+        int run = 0;
+        for (int b0 = nls; b0 >= 0; b0 -= 32) {
+          const int b = b0 - lane;
+          const int c = b >= 0 ? s_cntd[b] : 0;
+          int x = c;
+  #pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const int y = __shfl_up_sync(kFull, x, off);
+            if (lane >= off) x += y;
+          }
+          if (b >= 0) s_cntd[b] = run + x - c;  // = entries with a longer prefix than b
+          run += __shfl_sync(kFull, x, 31);
+        }
+      }
+      __syncthreads();
+      for (int j = threadIdx.x; j < cn; j += blockDim.x) {
+        const int lp = s_lp[j];
+        const uint32_t row = (uint32_t)p.terms[c0 + j] * (uint32_t)nblk;
+        const int v = __float_as_int(p.val32[c0 + j]);
+        const uint32_t base = lp ? (__ldg(offs + row) & ~kDense) : 0u;
+        s_ent[s_cntd[lp] + s_cc[(j >> 5) * nb + lp] + s_pos[j]] =
+            make_int4((int)row, v, (int)base, v);
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    for (int j = threadIdx.x; j < cn; j += blockDim.x) {
-      const int lp = s_lp[j];
-      const uint32_t row = (uint32_t)p.terms[c0 + j] * (uint32_t)nblk;
-      const int v = __float_as_int(p.val32[c0 + j]);
-      const uint32_t base = lp ? (__ldg(offs + row) & ~kDense) : 0u;
-      s_ent[s_cntd[lp] + s_cc[(j >> 5) * nb + lp] + s_pos[j]] =
-          make_int4((int)row, v, (int)base, v);
-    }
-    __syncthreads();
     const bool first = (c0 == rb);
     for (;;) {  // spans handed out dynamically: dense low spans and sparse high
                 // ones cost very differently
@@ -1709,6 +1740,73 @@ __global__ void entry_gather_kernel(int64_t nnz, const int32_t* __restrict__ sid
   }
 }
 
+// Each row's entries stably sorted by the terms' dense prefix, longest first
+// (for the slot-range passes: every pass's clamped bucket order is this order,
+// so the screen stages a pass by copying).  One warp per row: a counting sort
+// over the prefix lengths 0..nsp, ranks within 32-entry chunks by
+// __match_any_sync.
+constexpr int kPresortBuckets = 256;
+__global__ void __launch_bounds__(256) presort_rows_kernel(
+    int64_t n_obj, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ terms,
+    const float* __restrict__ val32, const uint32_t* __restrict__ dpre, int nsp,
+    int32_t* __restrict__ ps_t, float* __restrict__ ps_v) {
+  __shared__ int s_cnt[8][kPresortBuckets];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  int* cnt = s_cnt[w];
+  const int nbk = nsp + 1;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t i = blockIdx.x * wpb + w; i < n_obj; i += gridDim.x * wpb) {
+    const int64_t rb = row_ptr[i], re = row_ptr[i + 1];
+    for (int b = lane; b < nbk; b += 32) cnt[b] = 0;
+    __syncwarp();
+    for (int64_t h0 = rb; h0 < re; h0 += 32) {
+      const int64_t h = h0 + lane;
+      int key = -1;
+      if (h < re) {
+        const int d = (int)__ldg(dpre + terms[h]);
+        key = nsp - (d < nsp ? d : nsp);
+      }
+      const unsigned peers = __match_any_sync(kFull, key);
+      if (h < re && lane == __ffs(peers) - 1) cnt[key] += __popc(peers);
+      __syncwarp();
+    }
+    int carry = 0;  // exclusive scan of the bucket counts
+    for (int b0 = 0; b0 < nbk; b0 += 32) {
+      const int b = b0 + lane;
+      const int c = b < nbk ? cnt[b] : 0;
+      int x = c;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(kFull, x, off);
+        if (lane >= off) x += y;
+      }
+      if (b < nbk) cnt[b] = carry + x - c;
+      carry += __shfl_sync(kFull, x, 31);
+    }
+    __syncwarp();
+    for (int64_t h0 = rb; h0 < re; h0 += 32) {
+      const int64_t h = h0 + lane;
+      int key = -1;
+      int32_t t = 0;
+      if (h < re) {
+        t = terms[h];
+        const int d = (int)__ldg(dpre + t);
+        key = nsp - (d < nsp ? d : nsp);
+      }
+      const unsigned peers = __match_any_sync(kFull, key);
+      if (h < re) {
+        const int64_t pos = rb + cnt[key] + __popc(peers & lt);
+        ps_t[pos] = t;
+        ps_v[pos] = val32[h];
+      }
+      __syncwarp();
+      if (h < re && lane == __ffs(peers) - 1) cnt[key] += __popc(peers);
+      __syncwarp();
+    }
+  }
+}
+
 struct AssignWs {
   int32_t* label32;
   int32_t* slot_of;
@@ -2047,6 +2145,8 @@ struct AssignArgs {
   double mu_max;
   ivfkm_stats* stats;
   const int32_t* order;
+  const int32_t* ps_t = nullptr;  // presorted rows (pass mode), see ivfkm_assign_screen_ex
+  float* ps_v = nullptr;
 };
 
 int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
@@ -2080,6 +2180,15 @@ int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
   sp.q_cnt = w.q_cnt;
   sp.q_cid = w.q_cid;
   sp.stats = a.stats;
+  if (pl.passes && a.ps_t && (pl.cta_blocks / pl.rr) > 0 &&
+      ivfkm_bivf_nblk(a.k) / kSpan < kPresortBuckets) {
+    const int nsp = (int)(ivfkm_bivf_nblk(a.k) / kSpan);
+    presort_rows_kernel<<<grid_for(a.n_obj, 8), 256, 0, st>>>(
+        a.n_obj, a.row_ptr, a.terms, a.val32, sp.dpre, nsp, const_cast<int32_t*>(a.ps_t), a.ps_v);
+    IVFKM_CHECK_LAUNCH();
+    sp.ps_t = a.ps_t;
+    sp.ps_v = a.ps_v;
+  }
   sp.st_best = w.st_best;
   sp.st_slot = w.st_slot;
   sp.st_cnt = w.st_cnt;
@@ -2148,12 +2257,34 @@ int finish_impl(const AssignArgs& a, const AssignWs& w, const int32_t* prev_labe
 
 }  // namespace
 
+extern "C" int ivfkm_assign_screen_ex(int64_t n_obj, const int64_t* row_ptr,
+                                      const int32_t* terms, const float* val32,
+                                      const double* xnorm, int64_t k, int64_t dim,
+                                      const uint32_t* headers, const void* pval_screen,
+                                      int screen_bits, double mu_max, ivfkm_stats* stats,
+                                      const int32_t* order, int32_t* presort_terms,
+                                      float* presort_vals, void* ws, size_t ws_bytes,
+                                      ivfkm_stream_t stream_);
+
 extern "C" int ivfkm_assign_screen(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
                                    const float* val32, const double* xnorm, int64_t k,
                                    int64_t dim, const uint32_t* headers, const void* pval_screen,
                                    int screen_bits, double mu_max, ivfkm_stats* stats,
                                    const int32_t* order, void* ws, size_t ws_bytes,
                                    ivfkm_stream_t stream_) {
+  return ivfkm_assign_screen_ex(n_obj, row_ptr, terms, val32, xnorm, k, dim, headers,
+                                pval_screen, screen_bits, mu_max, stats, order, nullptr, nullptr,
+                                ws, ws_bytes, stream_);
+}
+
+extern "C" int ivfkm_assign_screen_ex(int64_t n_obj, const int64_t* row_ptr,
+                                      const int32_t* terms, const float* val32,
+                                      const double* xnorm, int64_t k, int64_t dim,
+                                      const uint32_t* headers, const void* pval_screen,
+                                      int screen_bits, double mu_max, ivfkm_stats* stats,
+                                      const int32_t* order, int32_t* presort_terms,
+                                      float* presort_vals, void* ws, size_t ws_bytes,
+                                      ivfkm_stream_t stream_) {
   if (n_obj < 0 || k < 1 || dim < 1 || !row_ptr || !stats || !headers) return IVFKM_E_ARG;
   if (screen_bits != 32 && screen_bits != 16) return IVFKM_E_ARG;
   // fp16 holds mean values up to 65504; unit-norm means are far inside
@@ -2168,6 +2299,8 @@ extern "C" int ivfkm_assign_screen(int64_t n_obj, const int64_t* row_ptr, const 
   if (n_obj == 0) return IVFKM_OK;
   AssignArgs a{n_obj,   row_ptr,     terms,       val32,   nullptr, xnorm, k, dim,
                headers, pval_screen, screen_bits, nullptr, mu_max,  stats, order};
+  a.ps_t = presort_terms;
+  a.ps_v = presort_vals;
   return screen_impl(a, w, st);
 }
 

@@ -348,6 +348,9 @@ class LloydEngine:
         # (ivfkm_assign_ivfd); False serves IVFD through the IVF kernels with
         # the IVFD label rule (identical results)
         self.ivfd_native = True
+        # slot-range passes stage presorted rows (ivfkm_assign_screen_ex)
+        self.presort = True
+        self._presort = None
         self._xinv = None
         self._ivfd_ws = None
 
@@ -466,12 +469,15 @@ class LloydEngine:
         st = _stream()
         if events is not None:
             events[0].record()
-        rc = self.lib.ivfkm_assign_screen(dd.n, _p(dd.row_ptr), _p(dd.terms), _p(dd.val32),
-                                          _p(dd.xnorm), self.k, dd.dim, _p(dm.headers),
-                                          _p(dm.pvs), dm.screen_bits, _MU_MAX, _p(self.stats),
-                                          _p(order),
-                                          _p(self.ws_assign), self.ws_assign.numel(), st)
-        _lib.check(rc, "ivfkm_assign_screen")
+        ps = self._presort_buffers() if npass > 1 and self.presort else (None, None)
+        rc = self.lib.ivfkm_assign_screen_ex(dd.n, _p(dd.row_ptr), _p(dd.terms), _p(dd.val32),
+                                             _p(dd.xnorm), self.k, dd.dim, _p(dm.headers),
+                                             _p(dm.pvs), dm.screen_bits, _MU_MAX, _p(self.stats),
+                                             _p(order), _p(ps[0]), _p(ps[1]),
+                                             _p(self.ws_assign), self.ws_assign.numel(), st)
+        _lib.check(rc, "ivfkm_assign_screen_ex")
+        if ps[0] is not None:
+            self.launches += 1
         self.launches += npass - 1
         if events is not None:
             events[1].record()
@@ -492,6 +498,14 @@ class LloydEngine:
             _lib.check(rc, "ivfkm_assign_finish")
         self.launches += 4
         return out
+
+    def _presort_buffers(self):
+        dd = self.dd
+        if self._presort is None or self._presort[0] is not dd.terms:
+            self._presort = (dd.terms, torch.empty(max(dd.nnz, 1), dtype=torch.int32,
+                                                   device=self.device),
+                             torch.empty(max(dd.nnz, 1), dtype=torch.float32, device=self.device))
+        return self._presort[1], self._presort[2]
 
     IVFD_SLOT_BYTES = 4 << 30  # the wave's per-mean similarity slots (N float64 each)
 

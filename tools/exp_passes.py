@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--warps", default="0")
     ap.add_argument("--rowcap", default="0", help="0: the engine's")
     ap.add_argument("--maxreg", default="56", help="(recorded only)")
+    ap.add_argument("--presort", default="1", help="pass mode stages presorted rows: 1,0")
     a = ap.parse_args()
     c = synth.CONFIGS[a.config]
     ds = synth.make_dataset(c["corpus"])
@@ -39,11 +40,13 @@ def main():
 
     from bench import Clocks
     rc0 = eng.rowcap
-    for r, pf, w, rc, mr in itertools.product(map(int, a.passes.split(",")),
-                                              map(int, a.pf.split(",")),
-                                              map(int, a.warps.split(",")),
-                                              map(int, a.rowcap.split(",")),
-                                              map(int, a.maxreg.split(","))):
+    for r, pf, w, rc, mr, ps in itertools.product(map(int, a.passes.split(",")),
+                                                  map(int, a.pf.split(",")),
+                                                  map(int, a.warps.split(",")),
+                                                  map(int, a.rowcap.split(",")),
+                                                  map(int, a.maxreg.split(",")),
+                                                  map(int, a.presort.split(","))):
+        eng.presort = bool(ps)
         eng.lib.ivfkm_set_screen_warps(w)
         eng.rowcap = rc or rc0
         eng.passes = r if r > 0 else None  # 0: the engine's plan
@@ -57,7 +60,7 @@ def main():
         st = eng.read_stats()
         ck = clk.stop() or {}
         print(json.dumps({"sm_mhz": ck.get("sm_mhz"), "reasons": ck.get("reasons"), "config": a.config, "passes": r, "planned": eng.screen_passes(dm), "warps": w, "rowcap": eng.rowcap,
-                          "maxreg": mr, "screen_ms": min(ts), "all": ts,
+                          "maxreg": mr, "presort": ps, "screen_ms": min(ts), "all": ts,
                           "postings": st.postings}), flush=True)
     eng.lib.ivfkm_set_screen_warps(0)
 
