@@ -2210,7 +2210,7 @@ int finish_impl(const AssignArgs& a, const AssignWs& w, const int32_t* prev_labe
   const int64_t nw = (a.dim + 31) / 32;
   if (dir) {
     IVFKM_TRY(cudaMemsetAsync(dir, 0, sizeof(uint2) * a.k * nw, st));
-    rankdir_bits_kernel<<<kNumSM * 8, T, 0, st>>>(a.k, nw, m_ptr, m_terms, dir);
+    rankdir_bits_kernel<<<num_sms() * 8, T, 0, st>>>(a.k, nw, m_ptr, m_terms, dir);
     IVFKM_CHECK_LAUNCH();
     rankdir_scan_kernel<<<grid_for(a.k, T / 32), T, 0, st>>>(a.k, nw, dir);
     IVFKM_CHECK_LAUNCH();
@@ -2247,9 +2247,9 @@ int finish_impl(const AssignArgs& a, const AssignWs& w, const int32_t* prev_labe
   fp.ovf_len = w.ovf_len;
   finalize_kernel<<<grid_for(a.n_obj, 8), 256, 0, st>>>(fp);
   IVFKM_CHECK_LAUNCH();
-  overflow_kernel<<<kNumSM, 1024, 0, st>>>(fp, a.k);
+  overflow_kernel<<<num_sms(), 1024, 0, st>>>(fp, a.k);
   IVFKM_CHECK_LAUNCH();
-  accumulate_kernel<<<grid_for(a.n_obj, 256, kNumSM * 8), 256, 0, st>>>(
+  accumulate_kernel<<<grid_for(a.n_obj, 256, num_sms() * 8), 256, 0, st>>>(
       a.n_obj, labels, sims, prev_labels, sizes, a.stats);
   IVFKM_CHECK_LAUNCH();
   return IVFKM_OK;
@@ -2381,7 +2381,7 @@ extern "C" int ivfkm_score_labels(int64_t n_obj, const int64_t* row_ptr, const i
   x.pv64 = pval64;
   score_labels_kernel<<<grid_for(n_obj, 8), 256, 0, st>>>(n_obj, x, labels, sims);
   IVFKM_CHECK_LAUNCH();
-  accumulate_kernel<<<grid_for(n_obj, 256, kNumSM * 8), 256, 0, st>>>(n_obj, labels, sims, nullptr,
+  accumulate_kernel<<<grid_for(n_obj, 256, num_sms() * 8), 256, 0, st>>>(n_obj, labels, sims, nullptr,
                                                                       nullptr, stats);
   IVFKM_CHECK_LAUNCH();
   return IVFKM_OK;
@@ -2491,7 +2491,7 @@ extern "C" int ivfkm_assign_ivfd(int64_t n_obj, int64_t dim, const int64_t* x_pt
   }
   ivfd_finish_kernel<<<grid_for(n_obj, 256), 256, 0, st>>>(n_obj, best, label, sim0, labels, sims);
   IVFKM_CHECK_LAUNCH();
-  accumulate_kernel<<<grid_for(n_obj, 256, kNumSM * 8), 256, 0, st>>>(
+  accumulate_kernel<<<grid_for(n_obj, 256, num_sms() * 8), 256, 0, st>>>(
       n_obj, labels, sims, prev_labels, sizes, stats);
   IVFKM_CHECK_LAUNCH();
   return IVFKM_OK;

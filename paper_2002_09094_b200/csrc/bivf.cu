@@ -413,7 +413,7 @@ int plan_masks(int64_t k, int64_t dim, int major, int64_t nrows, const int64_t* 
       bivf_ids_kernel<<<grid_for(k, threads), threads, 0, st>>>(k, w.id_a);
       IVFKM_CHECK_LAUNCH();
     }
-    bivf_sizes_kernel<<<major == 0 ? grid_for(k, threads) : kNumSM * 8, threads, 0, st>>>(
+    bivf_sizes_kernel<<<major == 0 ? grid_for(k, threads) : num_sms() * 8, threads, 0, st>>>(
         major, nrows, ptr, cols, k, w.key_a, w.id_a);
     IVFKM_CHECK_LAUNCH();
     cub::DoubleBuffer<unsigned int> kb(w.key_a, w.key_b);
@@ -427,7 +427,7 @@ int plan_masks(int64_t k, int64_t dim, int major, int64_t nrows, const int64_t* 
   IVFKM_CHECK_LAUNCH();
   IVFKM_TRY(cudaMemsetAsync(headers, 0, sizeof(uint32_t) * nh, st));
   IVFKM_TRY(cudaMemsetAsync(w.err, 0, sizeof(unsigned int), st));
-  bivf_mask_kernel<<<kNumSM * 8, threads, 0, st>>>(major, nrows, ptr, cols, k, dim, nblk, perm,
+  bivf_mask_kernel<<<num_sms() * 8, threads, 0, st>>>(major, nrows, ptr, cols, k, dim, nblk, perm,
                                                    headers, w.err);
   IVFKM_CHECK_LAUNCH();
   return IVFKM_OK;
@@ -523,7 +523,7 @@ int sorted_fill(int64_t k, int64_t dim, int major, int64_t nrows, const int64_t*
   const unsigned int* off64 = headers + 2 * nh + 1 + dim + 2 * k + dim;
   FillWs<K> w = carve_fill<K>(ws, nnz, nullptr);
   const int threads = 256;
-  bivf_poskey_kernel<K><<<kNumSM * 8, threads, 0, st>>>(major, nrows, ptr, cols, vals, k, dim,
+  bivf_poskey_kernel<K><<<num_sms() * 8, threads, 0, st>>>(major, nrows, ptr, cols, vals, k, dim,
                                                         nslot, perm, w.key_a, w.val_a);
   IVFKM_CHECK_LAUNCH();
   int bits = 1;  // keys lie in [0, dim * nslot] (the sentinel included)
@@ -554,7 +554,7 @@ int fill_impl(int64_t k, int64_t dim, int major, int64_t nrows, const int64_t* p
   const int32_t* perm = reinterpret_cast<const int32_t*>(headers + 2 * nh + 1 + dim);
   float* val32 = static_cast<float*>(val_screen);  // or fp16 values (screen_bits 16)
   const int threads = 256;
-  bivf_zero_kernel<<<kNumSM * 16, threads, 0, st>>>(headers + 2 * nh, val32, screen_bits == 16);
+  bivf_zero_kernel<<<num_sms() * 16, threads, 0, st>>>(headers + 2 * nh, val32, screen_bits == 16);
   IVFKM_CHECK_LAUNCH();
   if (ws && nnz > 0 && nnz < (int64_t)INT32_MAX) {
     return fill_k32(k, dim)
@@ -563,7 +563,7 @@ int fill_impl(int64_t k, int64_t dim, int major, int64_t nrows, const int64_t* p
                : sorted_fill<unsigned long long>(k, dim, major, nrows, ptr, cols, vals, headers,
                                                  val32, screen_bits == 16, val64, nnz, ws, st);
   }
-  bivf_scatter_kernel<<<kNumSM * 8, threads, 0, st>>>(major, nrows, ptr, cols, vals, k, dim,
+  bivf_scatter_kernel<<<num_sms() * 8, threads, 0, st>>>(major, nrows, ptr, cols, vals, k, dim,
                                                       nblk, headers, perm, val32, val64,
                                                       screen_bits == 16);
   IVFKM_CHECK_LAUNCH();

@@ -23,7 +23,21 @@
 namespace ivfkm {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kNumSM = 148;  // B200; grids are sized as multiples of this
+
+// SMs of the current device (148 on a B200), queried once per device; grids
+// are sized as multiples of it.
+inline int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (!cache[dev]) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1)
+      n = 148;
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
 
 inline cudaStream_t as_stream(ivfkm_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
@@ -43,7 +57,8 @@ struct Carver {
   void* take_bytes(size_t bytes, size_t align = 256) { return take<char>(bytes, align); }
 };
 
-inline int grid_for(int64_t items, int per_block, int max_blocks = kNumSM * 32) {
+inline int grid_for(int64_t items, int per_block, int max_blocks = 0) {
+  if (max_blocks <= 0) max_blocks = num_sms() * 32;
   int64_t g = (items + per_block - 1) / per_block;
   if (g < 1) g = 1;
   if (g > max_blocks) g = max_blocks;

@@ -973,7 +973,7 @@ int update_count_impl(int64_t n_obj, const int64_t* row_ptr, const int32_t* term
     segsum_kernel<K><<<grid_for((int64_t)n_seg + 1, T), T, 0, st>>>(
         n_seg, w.seg_start, w.seg_key, sval, sizes, dim, w.seg_w, w.head, w.segpos, w.n_seg + 1);
     IVFKM_CHECK_LAUNCH();
-    segsum_long_kernel<K><<<kNumSM * 8, 256, 0, st>>>(w.seg_start, w.seg_key, sval, sizes, dim,
+    segsum_long_kernel<K><<<num_sms() * 8, 256, 0, st>>>(w.seg_start, w.seg_key, sval, sizes, dim,
                                                       w.seg_w, w.head, w.segpos, w.n_seg + 1);
     IVFKM_CHECK_LAUNCH();
     size_t cb = w.cub_bytes;
@@ -985,7 +985,7 @@ int update_count_impl(int64_t n_obj, const int64_t* row_ptr, const int32_t* term
   IVFKM_CHECK_LAUNCH();
   IVFKM_TRY(cudaFuncSetAttribute(norm_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)nsmem));
-  norm_kernel<K><<<(int)std::min<int64_t>(k, kNumSM * 4), kNormWarps * 32, nsmem, st>>>(
+  norm_kernel<K><<<(int)std::min<int64_t>(k, num_sms() * 4), kNormWarps * 32, nsmem, st>>>(
       k, dim, nleaf, nint, P.nlevels, plan, sizes, prev_ptr, w.cl_seg, w.gstart, w.seg_key,
       w.seg_w, w.nzpos, w.nrm, w.counts);
   IVFKM_CHECK_LAUNCH();
