@@ -137,17 +137,17 @@ def _bytes(t: torch.Tensor) -> torch.Tensor:
     return t.contiguous().view(torch.uint8)
 
 
-def _gather_rows(row_ptr, terms, vals, sel):
-    """Rows ``sel`` (int64 index) of a CSR block, concatenated."""
+def _gather_entries(row_ptr, terms, vals, sel, total: int):
+    """The entries of rows ``sel`` (int64 index) of a CSR block, concatenated;
+    ``total`` = their count (known on the host: no device read)."""
     dev = row_ptr.device
     lens = row_ptr[sel + 1] - row_ptr[sel]
     ptr = torch.zeros(sel.numel() + 1, dtype=torch.int64, device=dev)
     torch.cumsum(lens, 0, out=ptr[1:])
-    total = int(ptr[-1])
     seg = torch.repeat_interleave(torch.arange(sel.numel(), device=dev), lens,
                                   output_size=total)
     idx = row_ptr[sel][seg] + (torch.arange(total, device=dev) - ptr[:-1][seg])
-    return ptr, terms[idx], vals[idx]
+    return terms[idx], vals[idx]
 
 
 class ShardComm:
@@ -170,60 +170,90 @@ class ShardComm:
         dist.all_to_all_single(out, send, recv_counts, send_counts, group=self.group)
         return out
 
-    def exchange_members(self, owned: "Members | None", gid0: int, local: Rows,
-                         prev: torch.Tensor | None, k: int) -> Members:
-        """Bring the cluster owners' member sets up to the new labels.
-
-        Only what changed crosses the wire: for every object whose label
-        changed, a 16-byte notice (gid, new label) to its old owner, and —
-        when its owner changed too — the row itself (gid, label, length, then
-        int32 terms + float64 values) to the new owner.  The first iteration
-        (``owned is None``) routes every row.  One all-to-all of the per-peer
-        counts (the only host read), one packed byte all-to-all.  The owner
-        drops leavers, relabels stayers and merges arrivals by gid, so its
-        members stay in ascending global object order."""
+    def plan_exchange(self, local: Rows, prev: torch.Tensor | None, k: int,
+                      first: bool) -> dict:
+        """The device side of exchange_members, with no host read: which
+        local objects send a notice (label changed) or their row (owner
+        changed), grouped by destination, and per destination the counts
+        [notices, rows, row entries, leavers, leaver entries] — all-to-all'ed
+        so every rank also holds what it will receive.  The caller reads
+        ``counts``/``rcounts`` together with the iteration's statistics (one
+        host read per iteration) and passes them to exchange_members."""
         dev = local.row_ptr.device
-        P, r = self.world, self.rank
+        P = self.world
         bounds = cluster_owner_bounds(k, P).to(dev)
         new = local.labels.to(torch.int64)
         new_own = torch.bucketize(new, bounds, right=True)
         n = new.numel()
-        if owned is None or prev is None:
-            mover = torch.ones(n, dtype=torch.bool, device=dev)
+        if first or prev is None:
+            old_own = torch.full_like(new_own, P)  # nobody owns anything yet
             notice = torch.zeros(n, dtype=torch.bool, device=dev)
-            old_own = new_own
+            mover = torch.ones(n, dtype=torch.bool, device=dev)
         else:
-            old = prev.to(torch.int64)
-            old_own = torch.bucketize(old, bounds, right=True)
-            notice = new != old
+            old_own = torch.bucketize(prev.to(torch.int64), bounds, right=True)
+            notice = new != prev.to(torch.int64)
             mover = notice & (new_own != old_own)
-        nt = torch.nonzero(notice).flatten()
-        mv = torch.nonzero(mover).flatten()
-        nt = nt[torch.argsort(old_own[nt], stable=True)]
-        mv = mv[torch.argsort(new_own[mv], stable=True)]
         lens = local.row_ptr[1:] - local.row_ptr[:-1]
-        cnt = torch.zeros(P, 3, dtype=torch.int64, device=dev)
-        cnt[:, 0] = torch.bincount(old_own[nt], minlength=P)
-        cnt[:, 1] = torch.bincount(new_own[mv], minlength=P)
-        cnt[:, 2].index_add_(0, new_own[mv], lens[mv])
+        key_n = torch.where(notice, old_own, P)
+        key_m = torch.where(mover, new_own, P)
+        key_l = torch.where(mover & (old_own < P), old_own, P)  # leavers, by old owner
+        cnt = torch.zeros(P + 1, 5, dtype=torch.int64, device=dev)
+        one = torch.ones(n, dtype=torch.int64, device=dev)
+        cnt[:, 0].index_add_(0, key_n, one)
+        cnt[:, 1].index_add_(0, key_m, one)
+        cnt[:, 2].index_add_(0, key_m, lens)
+        cnt[:, 3].index_add_(0, key_l, one)
+        cnt[:, 4].index_add_(0, key_l, lens)
+        cnt = cnt[:P].contiguous()
         rcnt = torch.empty_like(cnt)
         if P > 1:
             dist.all_to_all_single(rcnt, cnt, group=self.group)
         else:
             rcnt.copy_(cnt)
-        both = torch.stack([cnt, rcnt]).cpu().tolist()
-        sc, rc = both[0], both[1]
+        return dict(order_n=torch.argsort(key_n, stable=True),
+                    order_m=torch.argsort(key_m, stable=True), new=new, lens=lens,
+                    counts=cnt, rcounts=rcnt, k=k, first=first or prev is None)
+
+    def exchange_members(self, owned: "Members | None", gid0: int, local: Rows,
+                         prev: torch.Tensor | None, k: int, plan: dict | None = None,
+                         host_counts=None) -> Members:
+        """Bring the cluster owners' member sets up to the new labels.
+
+        Only what changed crosses the wire: for every object whose label
+        changed, a 16-byte notice (gid, new label) to its old owner, and —
+        when its owner changed too — the row itself (gid, label, length, then
+        int32 terms + float64 values) to the new owner; the first iteration
+        (``owned is None``) routes every row.  One packed byte all-to-all.
+        The owner drops leavers, relabels stayers and merges arrivals by gid,
+        so its members stay in ascending global object order.  With ``plan``
+        and its ``host_counts`` (plan_exchange; read by the caller together
+        with the iteration's statistics) nothing here reads the device: every
+        size comes from those counts."""
+        dev = local.row_ptr.device
+        P, r = self.world, self.rank
+        if plan is None:
+            plan = self.plan_exchange(local, prev, k, owned is None)
+        if host_counts is None:
+            host_counts = torch.stack([plan["counts"], plan["rcounts"]]).cpu().tolist()
+        sc, rc = host_counts
+        bounds = cluster_owner_bounds(k, P).to(dev)
+        n_nt = sum(c[0] for c in sc)
+        n_mv = sum(c[1] for c in sc)
+        e_mv = sum(c[2] for c in sc)
+        nt = plan["order_n"][:n_nt]
+        mv = plan["order_m"][:n_mv]
+        new, lens = plan["new"], plan["lens"]
 
         def nbytes(c):
             return 16 * c[0] + 24 * c[1] + 4 * c[2] + (4 if c[2] % 2 else 0) + 8 * c[2]
 
-        gid = torch.arange(n, device=dev, dtype=torch.int64) + gid0
+        gid = torch.arange(new.numel(), device=dev, dtype=torch.int64) + gid0
         notes = torch.stack([gid[nt], new[nt]], 1).reshape(-1)
         meta = torch.stack([gid[mv], new[mv], lens[mv]], 1).reshape(-1)
-        _, m_terms, m_vals = _gather_rows(local.row_ptr, local.terms, local.vals, mv)
+        m_terms, m_vals = _gather_entries(local.row_ptr, local.terms, local.vals, mv, e_mv)
         parts, o_nt, o_mv, o_e = [], 0, 0, 0
         for d in range(P):
-            a, b, e = sc[d]
+            a, b, e = sc[d][0], sc[d][1], sc[d][2]
             parts.append(_bytes(notes[2 * o_nt:2 * (o_nt + a)]))
             parts.append(_bytes(meta[3 * o_mv:3 * (o_mv + b)]))
             t = m_terms[o_e:o_e + e]
@@ -238,7 +268,7 @@ class ShardComm:
         # parse, source by source (sources hold ascending, disjoint gid ranges)
         r_notes, r_meta, r_terms, r_vals, off = [], [], [], [], 0
         for src in range(P):
-            a, b, e = rc[src]
+            a, b, e = rc[src][0], rc[src][1], rc[src][2]
             seg = recv[off:off + nbytes(rc[src])]
             q = 0
             r_notes.append(seg[q:q + 16 * a].view(torch.int64).view(-1, 2))
@@ -253,46 +283,44 @@ class ShardComm:
         meta_in = torch.cat(r_meta)
         a_terms = torch.cat(r_terms)
         a_vals = torch.cat(r_vals)
-        a_ptr = torch.zeros(meta_in.shape[0] + 1, dtype=torch.int64, device=dev)
+        n_arr = sum(c[1] for c in rc)
+        e_arr = sum(c[2] for c in rc)
+        a_ptr = torch.zeros(n_arr + 1, dtype=torch.int64, device=dev)
         torch.cumsum(meta_in[:, 2], 0, out=a_ptr[1:])
         a_gid, a_lab = meta_in[:, 0], meta_in[:, 1].to(torch.int32)
         if owned is None:
             return Members(a_ptr, a_terms, a_vals, a_lab, gid=a_gid)
-        # apply the notices: leavers out, stayers relabelled
+        # the notices: leavers out, stayers relabelled (no data-dependent shapes)
         labels = owned.labels.clone()
         keep = torch.ones(owned.n, dtype=torch.bool, device=dev)
         if notes_in.shape[0]:
             pos = torch.searchsorted(owned.gid, notes_in[:, 0])
             nl = notes_in[:, 1]
             stay = torch.bucketize(nl, bounds, right=True) == r
-            labels[pos[stay]] = nl[stay].to(torch.int32)
-            keep[pos[~stay]] = False
-        kept = torch.nonzero(keep).flatten()
-        if a_gid.numel() == 0 and kept.numel() == owned.n:
+            labels[pos] = torch.where(stay, nl.to(torch.int32), labels[pos])
+            keep[pos] = stay
+        n_left = sum(c[3] for c in rc)
+        e_left = sum(c[4] for c in rc)
+        if n_arr == 0 and n_left == 0:
             return Members(owned.row_ptr, owned.terms, owned.vals, labels, gid=owned.gid)
+        kept = torch.argsort((~keep).to(torch.int8), stable=True)[:owned.n - n_left]
         # merge kept members and arrivals by gid (both ascending)
         all_gid = torch.cat([owned.gid[kept], a_gid])
         order = torch.argsort(all_gid, stable=True)
         base = owned.terms.numel()
-        ptr = torch.cat([owned.row_ptr[:-1], a_ptr[:-1] + base, a_ptr[-1:] + base])
-        terms = torch.cat([owned.terms, a_terms])
-        vals = torch.cat([owned.vals, a_vals])
-        src_rows = torch.cat([kept, torch.arange(a_gid.numel(), device=dev) + owned.n])[order]
-        ends = torch.cat([owned.row_ptr[1:], a_ptr[1:] + base])
-        lens_all = ends - ptr[:-1]
-        full_ptr = torch.cat([ptr[:-1], ptr[-1:]])
-        del lens_all
-        # rows src_rows of the concatenated block (row i spans full_ptr[i] .. ends[i])
-        sel_start = full_ptr[src_rows]
-        sel_len = ends[src_rows] - sel_start
-        new_ptr = torch.zeros(src_rows.numel() + 1, dtype=torch.int64, device=dev)
-        torch.cumsum(sel_len, 0, out=new_ptr[1:])
-        total = int(new_ptr[-1])
-        seg = torch.repeat_interleave(torch.arange(src_rows.numel(), device=dev), sel_len,
+        starts = torch.cat([owned.row_ptr[kept], a_ptr[:-1] + base])[order]
+        lens_all = torch.cat([owned.row_ptr[kept + 1] - owned.row_ptr[kept],
+                              a_ptr[1:] - a_ptr[:-1]])[order]
+        total = owned.nnz - e_left + e_arr
+        new_ptr = torch.zeros(all_gid.numel() + 1, dtype=torch.int64, device=dev)
+        torch.cumsum(lens_all, 0, out=new_ptr[1:])
+        seg = torch.repeat_interleave(torch.arange(all_gid.numel(), device=dev), lens_all,
                                       output_size=total)
-        idx = sel_start[seg] + (torch.arange(total, device=dev) - new_ptr[:-1][seg])
+        idx = starts[seg] + (torch.arange(total, device=dev) - new_ptr[:-1][seg])
+        terms = torch.cat([owned.terms, a_terms])[idx]
+        vals = torch.cat([owned.vals, a_vals])[idx]
         all_lab = torch.cat([labels[kept], a_lab])[order]
-        return Members(new_ptr, terms[idx], vals[idx], all_lab, gid=all_gid[order])
+        return Members(new_ptr, terms, vals, all_lab, gid=all_gid[order])
 
     def allgather_means(self, ptr: torch.Tensor, terms: torch.Tensor, vals: torch.Tensor,
                         retained: torch.Tensor):
@@ -365,6 +393,7 @@ class DistLloyd:
         self.dd = DeviceDataset(self.host, device)
         self.members = None  # this rank's cluster-range member rows (exchange_members)
         self.prev_labels = None
+        self._plan = None    # (labels, exchange plan, host counts) from assign
         # the sharded update routes rows to cluster owners and runs the
         # stateless count (no label-delta state, no whole-shard workspace)
         self.eng = LloydEngine(self.dd, self.k, delta_update=False, update_ws=False)
@@ -377,20 +406,33 @@ class DistLloyd:
         global (postings, changed, near_ties, overflow, objective, sizes)."""
         lab = self.eng.assign(dm, prev, events=events)
         raw = self.eng.stats.view(torch.int64)  # 6 + 34 words (ivfkm_stats)
+        # the update's exchange plan rides on the statistics' host read: one
+        # device->host read per iteration for both
+        dd = self.dd
+        plan = self.comm.plan_exchange(Rows(dd.row_ptr, dd.terms, dd.val64, lab),
+                                       self.prev_labels, self.k, self.members is None)
         v = pack_stats(self.stats_vec, raw, self.eng.sizes)
         self.comm.allreduce_sum_(v)
-        h = v.cpu()
-        self.local_postings = int(raw[0].item())  # this rank's share (roofline)
+        h = torch.cat([v, raw[:1], plan["counts"].reshape(-1), plan["rcounts"].reshape(-1)]).cpu()
+        nv = v.numel()
+        self.local_postings = int(h[nv])  # this rank's share (roofline)
+        P = self.comm.world
+        c = h[nv + 1:].view(2, P, 5).tolist()
+        self._plan = (lab, plan, c)
         self.eng.sizes.copy_(v[STAT_WORDS:])  # global sizes for the update
-        return lab, unpack_stats(h)
+        return lab, unpack_stats(h[:nv])
 
     def update(self, lab, dm):
         from .engine import DeviceMeans, update_rows
 
         dd, k = self.dd, self.k
         rows = Rows(dd.row_ptr, dd.terms, dd.val64, lab)
+        plan = host = None
+        if self._plan is not None and self._plan[0] is lab:
+            _, plan, host = self._plan
         recv = self.members = self.comm.exchange_members(self.members, self.lo, rows,
-                                                         self.prev_labels, k)
+                                                         self.prev_labels, k, plan, host)
+        self._plan = None
         self.prev_labels = lab.clone()
         clo, chi = cluster_range(k, self.comm.world, self.comm.rank)
         kl = chi - clo

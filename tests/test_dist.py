@@ -87,15 +87,19 @@ def _worker(rank, world, port, k, iters, q):
         sizes = np.bincount(labels - 1, minlength=k)
         # the local statistics in ivfkm_stats' layout (what the kernels write)
         raw = torch.tensor([post, changed, 0, 0, 0, 0] + limbs_of(sims), dtype=torch.int64)
-        pack_stats(vec, raw, torch.from_numpy(sizes.astype(np.int64)))  # DistLloyd.assign's
-        comm.allreduce_sum_(vec)
-        st = unpack_stats(vec)
         rows = Rows(torch.from_numpy(Shard.indptr.copy()),
                     torch.from_numpy(Shard.term_ids.astype(np.int32) - 1),
                     torch.from_numpy(Shard.values.copy()),
                     torch.from_numpy(labels.astype(np.int32) - 1))
         prev_t = None if prev is None else torch.from_numpy(prev.astype(np.int32) - 1)
-        members = comm.exchange_members(members, lo, rows, prev_t, k)  # DistLloyd.update's
+        # DistLloyd.assign: the exchange plan rides on the statistics' one host read
+        plan = comm.plan_exchange(rows, prev_t, k, members is None)
+        pack_stats(vec, raw, torch.from_numpy(sizes.astype(np.int64)))
+        comm.allreduce_sum_(vec)
+        h = torch.cat([vec, plan["counts"].reshape(-1), plan["rcounts"].reshape(-1)])
+        st = unpack_stats(h[:vec.numel()])
+        host = h[vec.numel():].view(2, world, 5).tolist()
+        members = comm.exchange_members(members, lo, rows, prev_t, k, plan, host)
         clo, chi = cluster_range(k, world, rank)
         assert bool(torch.all(members.gid[1:] > members.gid[:-1]))  # ascending global order
         assert bool(torch.all((members.labels >= clo) & (members.labels < chi)))
