@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--rowcap", default="0", help="0: the engine's")
     ap.add_argument("--maxreg", default="56", help="(recorded only)")
     ap.add_argument("--presort", default="1", help="pass mode stages presorted rows: 1,0")
+    ap.add_argument("--tma", default="0", help="dense segments by TMA ring: 0,1")
     a = ap.parse_args()
     c = synth.CONFIGS[a.config]
     ds = synth.make_dataset(c["corpus"])
@@ -40,13 +41,16 @@ def main():
 
     from bench import Clocks
     rc0 = eng.rowcap
-    for r, pf, w, rc, mr, ps in itertools.product(map(int, a.passes.split(",")),
-                                                  map(int, a.pf.split(",")),
-                                                  map(int, a.warps.split(",")),
-                                                  map(int, a.rowcap.split(",")),
-                                                  map(int, a.maxreg.split(",")),
-                                                  map(int, a.presort.split(","))):
+    base = None
+    for r, pf, w, rc, mr, ps, tm in itertools.product(map(int, a.passes.split(",")),
+                                                      map(int, a.pf.split(",")),
+                                                      map(int, a.warps.split(",")),
+                                                      map(int, a.rowcap.split(",")),
+                                                      map(int, a.maxreg.split(",")),
+                                                      map(int, a.presort.split(",")),
+                                                      map(int, a.tma.split(","))):
         eng.presort = bool(ps)
+        eng.lib.ivfkm_set_screen_option(3, tm)
         eng.lib.ivfkm_set_screen_warps(w)
         eng.rowcap = rc or rc0
         eng.passes = r if r > 0 else None  # 0: the engine's plan
@@ -54,15 +58,20 @@ def main():
         ts = []
         clk = Clocks(0)
         for _ in range(a.reps):
-            eng.assign(dm, None, events=ev)
+            lab = eng.assign(dm, None, events=ev)
             torch.cuda.synchronize()
             ts.append(ev[0].elapsed_time(ev[1]))
+        lab = lab.clone()
+        if base is None:
+            base = lab
+        ok = bool(torch.equal(lab, base))
         st = eng.read_stats()
         ck = clk.stop() or {}
         print(json.dumps({"sm_mhz": ck.get("sm_mhz"), "reasons": ck.get("reasons"), "config": a.config, "passes": r, "planned": eng.screen_passes(dm), "warps": w, "rowcap": eng.rowcap,
-                          "maxreg": mr, "presort": ps, "screen_ms": min(ts), "all": ts,
+                          "maxreg": mr, "presort": ps, "tma": tm, "labels_ok": ok, "screen_ms": min(ts), "all": ts,
                           "postings": st.postings}), flush=True)
     eng.lib.ivfkm_set_screen_warps(0)
+    eng.lib.ivfkm_set_screen_option(3, 0)
 
 
 if __name__ == "__main__":
