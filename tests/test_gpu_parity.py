@@ -698,3 +698,70 @@ def test_native_ivfd_matches_oracle(k, signed, slot_bytes):
     lab2 = eng.assign(dm, None, rule=1)
     st2 = eng.read_stats()
     assert np.array_equal(lab2.cpu().numpy() + 1, want) and st2.objective == st.objective
+
+
+@pytest.mark.parametrize("presort", [True, False])
+@pytest.mark.parametrize("rowcap,passes", [(64, 3), (32, 7)])
+def test_slot_range_passes_multipiece_rows(tuning, presort, rowcap, passes):
+    """Pass mode on rows longer than the staging piece: each piece of a
+    presorted row is still sorted by dense prefix; both staging paths."""
+    from oracle import oracle as O
+    from paper_2002_09094_b200.variants import engine_for
+
+    ds, om, means = _random_case(n=5200, dim=3000, k=4600, seed=44, signed=True)
+    assert int(np.diff(ds.indptr).max()) > 2 * rowcap
+    eng = engine_for(ds, means.k)
+    eng.presort = presort
+    try:
+        labels, st = _assign_raw(ds, means, rowcap=rowcap, passes=passes)
+    finally:
+        eng.presort = True
+    ol, _, _, post = O.assign(ds, om)
+    assert np.array_equal(labels, ol) and st.postings == post
+    assert st.objective == O.objective(ds, ol, om)
+
+
+def test_update_fill_never_writes_past_capacity():
+    """ivfkm_update_fill with a caller buffer smaller than the new means: the
+    entries up to the capacity are the exact ones, nothing is written past it
+    (guard bytes), and a full-size buffer still gives the oracle's means."""
+    import torch
+
+    from oracle import oracle as O
+    from paper_2002_09094_b200 import _lib
+    from paper_2002_09094_b200.engine import _p, _stream
+
+    ds, om, means = _random_case(seed=12, k=60, n=2000)
+    lib = _lib.load()
+    dev = torch.device("cuda")
+    labels = np.random.default_rng(1).integers(1, 51, size=ds.n).astype(np.int32)  # 51..60 empty
+    ref = O.update(ds, labels, om)
+    n, nnz, k, dim = ds.n, int(ds.indptr[-1]), om.k, ds.dim
+    t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)  # noqa: E731
+    row_ptr, terms, val64 = t(ds.indptr, np.int64), t(ds.term_ids - 1, np.int32), t(ds.values, np.float64)
+    lab0 = t(labels - 1, np.int32)
+    sizes = t(O.sizes_of(labels, k), np.int64)
+    pptr, pterms, pvals = t(om.indptr, np.int64), t(om.term_ids - 1, np.int32), t(om.values, np.float64)
+    new_ptr = torch.empty(k + 1, dtype=torch.int64, device=dev)
+    ws = torch.empty(int(lib.ivfkm_update_workspace_size(n, nnz, k, dim)), dtype=torch.uint8,
+                     device=dev)
+    _lib.check(lib.ivfkm_update_count(n, nnz, _p(row_ptr), _p(terms), _p(val64), k, dim, _p(lab0),
+                                      _p(sizes), _p(pptr), _p(new_ptr), _p(ws), ws.numel(),
+                                      _stream()), "count")
+    total = int(new_ptr[-1].item())
+    assert total == ref.term_ids.size
+    for cap in (total // 2, total):
+        guard = 512
+        tb = torch.full((cap + guard,), -7, dtype=torch.int32, device=dev)
+        vb = torch.full((cap + guard,), -7.0, dtype=torch.float64, device=dev)
+        ret = torch.empty(k, dtype=torch.uint8, device=dev)
+        _lib.check(lib.ivfkm_update_fill(n, nnz, k, dim, _p(sizes), _p(pptr), _p(pterms),
+                                         _p(pvals), _p(new_ptr), _p(tb), _p(vb), _p(ret), cap,
+                                         _p(ws), ws.numel(), _stream()), "fill")
+        torch.cuda.synchronize()
+        assert bool((tb[cap:] == -7).all()) and bool((vb[cap:] == -7.0).all())
+        assert np.array_equal(tb[:cap].cpu().numpy() + 1, ref.term_ids[:cap])
+        assert np.array_equal(vb[:cap].cpu().numpy(), ref.values[:cap])
+    assert lib.ivfkm_update_fill(n, nnz, k, dim, _p(sizes), _p(pptr), _p(pterms), _p(pvals),
+                                 _p(new_ptr), _p(tb), _p(vb), _p(ret), -1, _p(ws), ws.numel(),
+                                 _stream()) == -1  # IVFKM_E_ARG
