@@ -708,7 +708,7 @@ def test_slot_range_passes_multipiece_rows(tuning, presort, rowcap, passes):
     from oracle import oracle as O
     from paper_2002_09094_b200.variants import engine_for
 
-    ds, om, means = _random_case(n=5200, dim=3000, k=4600, seed=44, signed=True)
+    ds, om, means = _random_case(n=5200, dim=6000, k=4600, seed=44, signed=True, corpus=1)
     assert int(np.diff(ds.indptr).max()) > 2 * rowcap
     eng = engine_for(ds, means.k)
     eng.presort = presort
