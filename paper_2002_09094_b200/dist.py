@@ -294,7 +294,7 @@ class ShardComm:
         labels = owned.labels.clone()
         keep = torch.ones(owned.n, dtype=torch.bool, device=dev)
         if notes_in.shape[0]:
-            pos = torch.searchsorted(owned.gid, notes_in[:, 0])
+            pos = torch.searchsorted(owned.gid, notes_in[:, 0].contiguous())
             nl = notes_in[:, 1]
             stay = torch.bucketize(nl, bounds, right=True) == r
             labels[pos] = torch.where(stay, nl.to(torch.int32), labels[pos])
@@ -515,11 +515,11 @@ def bench_multi(args, rank: int, world: int) -> None:
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     screen_s = sum(a.elapsed_time(b) for a, b in ev) / len(ev) / 1000.0
     # roofline of the screen on the slowest rank: its own shard's bytes / time
-    from bench import algorithmic_bytes, measured_peak_hbm
+    from bench import algorithmic_bytes, roofline
 
     mine = algorithmic_bytes(sum(local_posts) / len(local_posts), run.dd.nnz, run.dd.n,
                              run.eng.screen_bits // 8)
-    rl = torch.tensor([mine / screen_s / 1e9, screen_s], dtype=torch.float64, device=dev)
+    rl = torch.tensor([mine / screen_s / 1e9], dtype=torch.float64, device=dev)
     slow = rl.clone()
     dist.all_reduce(slow, op=dist.ReduceOp.MIN)  # lowest achieved GB/s over ranks
     # ---- end to end: host buffers in and out every step
@@ -551,7 +551,11 @@ def bench_multi(args, rank: int, world: int) -> None:
     dist.barrier()
     if rank == 0:
         t = float(ms.item())
-        peak, peak_kind = measured_peak_hbm()
+        # the slowest rank's screen: its algorithmic bytes over its time
+        rf = roofline(float(slow[0].item()) * screen_s * 1e9, screen_s, None,
+                      run.eng.screen_bits)
+        rf["per"] = "slowest rank's screen over its shard"
+
         print(json.dumps({
             "metric": "Lloyd iterations/sec and assign-step postings/sec (% roofline), 1/2/4/8 B200",
             "value": args.steps / (t / 1000.0), "unit": "iter/s", "n_gpus": world,
@@ -564,10 +568,7 @@ def bench_multi(args, rank: int, world: int) -> None:
                        "parallelism": f"objects sharded over {world} GPUs, means replicated",
                        "l2": "inputs larger than L2"},
             "postings_per_sec": sum(posts) / (t / 1000.0),
-            "roofline": {"bound": "hbm", "achieved": float(slow[0].item()), "peak": peak,
-                         "unit": "GB/s", "frac": float(slow[0].item()) / peak, "traffic": None,
-                         "peak_source": peak_kind, "per": "slowest rank's screen over its shard",
-                         "kernel": f"screen_kernel (BIVF register screen, fp{run.eng.screen_bits} values)"},
+            "roofline": rf,
             "gpu_launches": launches * world,
             "clocks": clocks,
             "e2e": {"value": e2e_steps / float(e2e_t.item()), "unit": "iter/s",
