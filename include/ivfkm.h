@@ -147,8 +147,7 @@ size_t ivfkm_assign_workspace_size(int64_t n_obj, int64_t k);
  * CTA in bytes (min 1 KB; -1 = adaptive default: rho is split over a
  * thread-block cluster once it passes ~24 KB; a smaller budget forces the thread-block
  * cluster split), rr = 32-mean blocks per warp span of the register screen
- * (2, 4 or 8; 0 = automatic) or -8 for the TMA-pipelined screen; rr = -16*w
- * sets w warps per CTA for the TMA screen.
+ * (2, 4 or 8; 0 = automatic).
  * Out-of-range values leave the setting unchanged.                          */
 void ivfkm_set_tuning(int rowcap, int smem_limit, int rr);
 /* Tests / tuning: force the register screen's warps per CTA (1..16; 0 = the
@@ -172,13 +171,13 @@ int ivfkm_assign_screen_ex(int64_t n_obj, const int64_t* row_ptr, const int32_t*
  * cluster), merging each object's best value and near-tie candidates in a
  * workspace state between launches; the candidate window — and so every
  * result — equals the one-pass screen's.  Ignored under a forced shared-
- * memory budget or a staged (TMA / cp.async) screen.  Returns IVFKM_E_ARG
+ * memory budget.  Returns IVFKM_E_ARG
  * for an unknown `which`. */
 int ivfkm_set_screen_option(int which, int value);
 /* The screen plan ivfkm_assign_screen would use for k means under the
  * current tuning ([host] out[8]: span blocks RR, cluster CTAs per object,
  * 32-mean blocks per CTA, warps per CTA, staged row entries, mode (0 register
- * screen, 1 TMA ring, 2 cp.async ring), dynamic shared bytes, registers per
+ * screen — the only one since round 2), dynamic shared bytes, registers per
  * thread of the instantiation).  rowcap < 32: the current default. */
 int ivfkm_screen_plan(int64_t k, int rowcap, int screen_bits, int32_t* out /*[host] 8*/);
 /* Object order: ivfkm_assign/_screen take `order`, the order in which the

@@ -825,401 +825,6 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
 }
 
 // ---------------------------------------------------------------------------
-// TMA-pipelined screen.  Same ownership and arithmetic as screen_kernel<8>
-// (lane = mean within a 32-mean block, 8 blocks per warp span, fp32 FMAs in
-// row order), but the posting data of each (object nonzero, span) — the 32-B
-// mask row and the span's contiguous, 16-B-padded value segment — is fetched
-// by cp.async.bulk (TMA) into a per-warp ring of kStages shared-memory stages
-// completed on mbarriers, kStages entries ahead of the FMAs.  Latency is hidden
-// by the copy engine instead of registers, no LSU instruction is spent per
-// posting load, and spans a term does not populate are skipped outright.
-
-constexpr int kStages = 4;
-constexpr int kStageBytes = 32 + 4 * 256;  // masks + the largest span segment
-
-__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-      " selp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-__host__ __device__ inline size_t tma_warp_bytes(int rowcap) {
-  return ((size_t)16 * rowcap + 15) / 16 * 16 + 8 * kStages + (size_t)kStages * kStageBytes;
-}
-
-__global__ void __launch_bounds__(512) screen_tma_kernel(ScreenParams p) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ ScreenShared sh;
-  constexpr int RR = kSpan;
-  float* rho = reinterpret_cast<float*>(smem);
-  const int cta_cids = p.cta_blocks * 32;
-  int32_t* s_term = reinterpret_cast<int32_t*>(rho + cta_cids);
-  float* s_val = reinterpret_cast<float*>(s_term + p.rowcap);
-
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int nwarps = blockDim.x >> 5;
-  const int z = blockIdx.x % p.nsplit;
-  const int64_t obj = p.order ? (int64_t)__ldg(p.order + blockIdx.x / p.nsplit)
-                              : (int64_t)(blockIdx.x / p.nsplit);
-  if (obj >= p.n_obj) return;  // whole cluster shares obj
-  const int64_t rb = p.row_ptr[obj], re = p.row_ptr[obj + 1];
-  const int64_t nblk = p.nblk;
-  const int64_t blk0 = (int64_t)z * p.cta_blocks;
-  const int nspans = p.cta_blocks / RR;
-  const unsigned lanebit = 1u << lane;
-  const unsigned lt = lanebit - 1u;
-
-  // per-warp region: active list, mbarriers, stage ring
-  unsigned char* wbase = reinterpret_cast<unsigned char*>(s_val + p.rowcap);
-  wbase = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(wbase) + 127) & ~(uintptr_t)127);
-  wbase += (size_t)warp * tma_warp_bytes(p.rowcap);
-  uint32_t* act_row = reinterpret_cast<uint32_t*>(wbase);
-  uint32_t* act_os = act_row + p.rowcap;
-  uint32_t* act_nv = act_os + p.rowcap;
-  float* act_v = reinterpret_cast<float*>(act_nv + p.rowcap);
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(wbase + ((size_t)16 * p.rowcap + 15) / 16 * 16);
-  unsigned char* ring = reinterpret_cast<unsigned char*>(mbar + kStages);
-
-  __shared__ const void* s_base[4];
-  if (threadIdx.x == 0) {
-    s_base[0] = p.masks;
-    s_base[1] = p.offs;
-    s_base[2] = p.pv32;
-    s_base[3] = p.nc;
-  }
-  if (lane == 0) {
-#pragma unroll
-    for (int q = 0; q < kStages; ++q) mbar_init(&mbar[q], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  const uint32_t* __restrict__ masks = static_cast<const uint32_t*>(s_base[0]);
-  const uint32_t* __restrict__ offs = static_cast<const uint32_t*>(s_base[1]);
-  const float* __restrict__ pv = static_cast<const float*>(s_base[2]);
-  const uint32_t* __restrict__ ncp = static_cast<const uint32_t*>(s_base[3]);
-  unsigned long long post = 0;
-  uint32_t used = 0;  // stage uses so far (ring position and mbarrier parity)
-
-  int64_t c0 = rb;
-  do {
-    const int64_t rem = re - c0;
-    const int cn = (int)(rem < p.rowcap ? rem : p.rowcap);
-    __syncthreads();
-    for (int j = threadIdx.x; j < cn; j += blockDim.x) {
-      const int32_t t = p.terms[c0 + j];
-      s_term[j] = t;
-      s_val[j] = p.val32[c0 + j];
-      if (z == 0) post += __ldg(ncp + t);
-    }
-    __syncthreads();
-    const bool first = (c0 == rb);
-    for (int sp = warp; sp < nspans; sp += nwarps) {
-      const int64_t gb = blk0 + (int64_t)sp * RR;
-      float acc[RR];
-#pragma unroll
-      for (int r = 0; r < RR; ++r) acc[r] = first ? 0.f : rho[(sp * RR + r) * 32 + lane];
-      if (gb < nblk) {
-        const uint32_t nb32 = (uint32_t)nblk, gb32 = (uint32_t)gb;
-        // ---- active list: entries whose term populates this span
-        int n_act = 0;
-        for (int j0 = 0; j0 < cn; j0 += 128) {
-          uint32_t os[4], oe[4], row[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int e = j0 + 32 * q + lane;
-            os[q] = 0u;
-            oe[q] = 0u;
-            row[q] = 0u;
-            if (e < cn) {
-              row[q] = (uint32_t)s_term[e] * nb32 + gb32;
-              os[q] = __ldg(offs + row[q]);
-              oe[q] = __ldg(offs + row[q] + RR);
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int e = j0 + 32 * q + lane;
-            const uint32_t start = os[q] & ~kDense;
-            const uint32_t nv = (oe[q] & ~kDense) - start;
-            const bool on = e < cn && nv != 0u;
-            const unsigned bal = __ballot_sync(kFull, on);
-            if (on) {
-              const int at = n_act + __popc(bal & lt);
-              act_row[at] = row[q];
-              act_os[at] = os[q];
-              act_nv[at] = nv;
-              act_v[at] = s_val[e];
-            }
-            n_act += __popc(bal);
-          }
-        }
-        __syncwarp();
-        // ---- pipeline: kStages bulk copies in flight ahead of the FMAs
-        auto issue = [&](int i) {
-          const uint32_t st = (used + (uint32_t)i) % kStages;
-          unsigned char* dst = ring + (size_t)st * kStageBytes;
-          const uint32_t nv = act_nv[i];
-          mbar_expect_tx(&mbar[st], 32u + 4u * nv);
-          bulk_g2s(dst, masks + act_row[i], 32u, &mbar[st]);
-          bulk_g2s(dst + 32, pv + (act_os[i] & ~kDense), 4u * nv, &mbar[st]);
-        };
-        if (lane == 0)
-          for (int i = 0; i < n_act && i < kStages; ++i) issue(i);
-        for (int i = 0; i < n_act; ++i) {
-          const uint32_t g = used + (uint32_t)i;
-          const uint32_t st = g % kStages;
-          while (!mbar_try_wait(&mbar[st], (g / kStages) & 1u)) {
-          }
-          const unsigned char* src = ring + (size_t)st * kStageBytes;
-          const float v = act_v[i];
-          float u[RR];
-          if (act_os[i] & kDense) {
-            const float4 a = reinterpret_cast<const float4*>(src + 32)[lane];
-            const float4 b = reinterpret_cast<const float4*>(src + 32)[32 + lane];
-            u[0] = a.x; u[1] = a.y; u[2] = a.z; u[3] = a.w;
-            u[4] = b.x; u[5] = b.y; u[6] = b.z; u[7] = b.w;
-          } else {
-            const uint4 ma = reinterpret_cast<const uint4*>(src)[0];
-            const uint4 mb = reinterpret_cast<const uint4*>(src)[1];
-            const uint32_t m[RR] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
-            const float* vals = reinterpret_cast<const float*>(src + 32);
-            uint32_t o = 0;
-#pragma unroll
-            for (int r = 0; r < RR; ++r) {
-              u[r] = 0.f;
-              if (m[r] & lanebit) u[r] = vals[o + (uint32_t)__popc(m[r] & lt)];
-              o += (uint32_t)__popc(m[r]);
-            }
-          }
-          // fma(v, 0, acc) == acc exactly: absent postings cost no rounding
-#pragma unroll
-          for (int r = 0; r < RR; ++r) acc[r] = fmaf(v, u[r], acc[r]);
-          __syncwarp();  // every lane is done with this stage
-          if (lane == 0 && i + kStages < n_act) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(i + kStages);
-          }
-        }
-        used += (uint32_t)n_act;
-        __syncwarp();
-      }
-#pragma unroll
-      for (int r = 0; r < RR; ++r) rho[(sp * RR + r) * 32 + lane] = acc[r];
-    }
-    c0 += p.rowcap;
-  } while (c0 < re);
-  __syncthreads();
-  screen_epilogue(p, sh, rho, obj, z, rb, re, post);
-}
-
-// ---------------------------------------------------------------------------
-// cp.async-pipelined screen.  Same ownership and arithmetic as
-// screen_kernel<8>, but each (object nonzero, span) segment — the span's
-// contiguous, 16-B-padded values and, for a sparse span, its 32-B mask row —
-// is copied global -> shared with 16-B cp.async (LDGSTS) into a per-warp ring
-// of kAsyncStages stages, kAsyncStages-1 entries ahead of the FMAs.  The
-// segment bounds come from a per-span prepass (all lanes load offsets for the
-// whole staged row at once), so only one dependent global latency remains
-// per row chunk, and the in-flight data occupies shared memory, not registers.
-
-constexpr int kAsyncStages = 6;
-constexpr int kAsyncStageBytes = 32 + 4 * 256;
-
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-__host__ __device__ inline size_t async_warp_bytes(int rowcap) {
-  return (size_t)8 * rowcap + (size_t)kAsyncStages * kAsyncStageBytes;
-}
-
-__global__ void __launch_bounds__(512) screen_async_kernel(ScreenParams p) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ ScreenShared sh;
-  constexpr int RR = kSpan;
-  float* rho = reinterpret_cast<float*>(smem);
-  const int cta_cids = p.cta_blocks * 32;
-  int32_t* s_term = reinterpret_cast<int32_t*>(rho + cta_cids);
-  float* s_val = reinterpret_cast<float*>(s_term + p.rowcap);
-
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int nwarps = blockDim.x >> 5;
-  const int z = blockIdx.x % p.nsplit;
-  const int64_t obj = p.order ? (int64_t)__ldg(p.order + blockIdx.x / p.nsplit)
-                              : (int64_t)(blockIdx.x / p.nsplit);
-  if (obj >= p.n_obj) return;
-  const int64_t rb = p.row_ptr[obj], re = p.row_ptr[obj + 1];
-  const int64_t nblk = p.nblk;
-  const int64_t blk0 = (int64_t)z * p.cta_blocks;
-  const int nspans = p.cta_blocks / RR;
-  const unsigned lanebit = 1u << lane;
-  const unsigned lt = lanebit - 1u;
-
-  unsigned char* wbase = reinterpret_cast<unsigned char*>(s_val + p.rowcap);
-  wbase = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(wbase) + 127) &
-                                           ~(uintptr_t)127);
-  wbase += (size_t)warp * async_warp_bytes(p.rowcap);
-  unsigned char* ring = wbase;  // kAsyncStages stages, 16-B aligned
-  uint32_t* m_os = reinterpret_cast<uint32_t*>(wbase + (size_t)kAsyncStages * kAsyncStageBytes);
-  uint32_t* m_nv = m_os + p.rowcap;
-
-  __shared__ const void* s_base[4];
-  if (threadIdx.x == 0) {
-    s_base[0] = p.masks;
-    s_base[1] = p.offs;
-    s_base[2] = p.pv32;
-    s_base[3] = p.nc;
-  }
-  __syncthreads();
-  const uint32_t* __restrict__ masks = static_cast<const uint32_t*>(s_base[0]);
-  const uint32_t* __restrict__ offs = static_cast<const uint32_t*>(s_base[1]);
-  const float* __restrict__ pv = static_cast<const float*>(s_base[2]);
-  const uint32_t* __restrict__ ncp = static_cast<const uint32_t*>(s_base[3]);
-  unsigned long long post = 0;
-
-  int64_t c0 = rb;
-  do {
-    const int64_t rem = re - c0;
-    const int cn = (int)(rem < p.rowcap ? rem : p.rowcap);
-    __syncthreads();
-    for (int j = threadIdx.x; j < cn; j += blockDim.x) {
-      const int32_t t = p.terms[c0 + j];
-      s_term[j] = t;
-      s_val[j] = p.val32[c0 + j];
-      if (z == 0) post += __ldg(ncp + t);
-    }
-    __syncthreads();
-    const bool first = (c0 == rb);
-    for (int sp = warp; sp < nspans; sp += nwarps) {
-      const int64_t gb = blk0 + (int64_t)sp * RR;
-      float acc[RR];
-#pragma unroll
-      for (int r = 0; r < RR; ++r) acc[r] = first ? 0.f : rho[(sp * RR + r) * 32 + lane];
-      if (gb < nblk) {
-        const uint32_t nb32 = (uint32_t)nblk, gb32 = (uint32_t)gb;
-        // ---- prepass: segment bounds of every staged entry for this span
-        for (int j0 = 0; j0 < cn; j0 += 128) {
-          uint32_t os[4], oe[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int e = j0 + 32 * q + lane;
-            os[q] = 0u;
-            oe[q] = 0u;
-            if (e < cn) {
-              const uint32_t row = (uint32_t)s_term[e] * nb32 + gb32;
-              os[q] = __ldg(offs + row);
-              oe[q] = __ldg(offs + row + RR);
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int e = j0 + 32 * q + lane;
-            if (e < cn) {
-              m_os[e] = os[q];
-              m_nv[e] = (oe[q] & ~kDense) - (os[q] & ~kDense);
-            }
-          }
-        }
-        __syncwarp();
-        auto issue = [&](int e) {
-          if (e < cn) {
-            unsigned char* dst = ring + (size_t)(e % kAsyncStages) * kAsyncStageBytes;
-            const uint32_t os = m_os[e];
-            const uint32_t nv = m_nv[e];
-            if (nv) {
-              if (!(os & kDense) && lane < 2)
-                cp_async16(dst + 16 * lane,
-                           masks + (uint32_t)s_term[e] * nb32 + gb32 + 4u * (uint32_t)lane);
-              const float* src = pv + (os & ~kDense);
-              for (uint32_t q = (uint32_t)lane; 4u * q < nv; q += 32u)
-                cp_async16(dst + 32 + 16 * q, src + 4u * q);
-            }
-          }
-          cp_async_commit();
-        };
-#pragma unroll
-        for (int e = 0; e < kAsyncStages - 1; ++e) issue(e);
-        for (int e = 0; e < cn; ++e) {
-          issue(e + kAsyncStages - 1);
-          cp_async_wait<kAsyncStages - 1>();
-          __syncwarp();
-          const uint32_t os = m_os[e];
-          const uint32_t nv = m_nv[e];
-          if (nv) {
-            const unsigned char* src = ring + (size_t)(e % kAsyncStages) * kAsyncStageBytes;
-            const float v = s_val[e];
-            float u[RR];
-            if (os & kDense) {
-              const float4 a = reinterpret_cast<const float4*>(src + 32)[lane];
-              const float4 b = reinterpret_cast<const float4*>(src + 32)[32 + lane];
-              u[0] = a.x; u[1] = a.y; u[2] = a.z; u[3] = a.w;
-              u[4] = b.x; u[5] = b.y; u[6] = b.z; u[7] = b.w;
-            } else {
-              const uint4 ma = reinterpret_cast<const uint4*>(src)[0];
-              const uint4 mb = reinterpret_cast<const uint4*>(src)[1];
-              const uint32_t m[RR] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
-              const float* vals = reinterpret_cast<const float*>(src + 32);
-              uint32_t o = 0;
-#pragma unroll
-              for (int r = 0; r < RR; ++r) {
-                u[r] = 0.f;
-                if (m[r] & lanebit) u[r] = vals[o + (uint32_t)__popc(m[r] & lt)];
-                o += (uint32_t)__popc(m[r]);
-              }
-            }
-#pragma unroll
-            for (int r = 0; r < RR; ++r) acc[r] = fmaf(v, u[r], acc[r]);
-          }
-          __syncwarp();  // the stage is re-filled by issue(e + kAsyncStages)
-        }
-        cp_async_wait<0>();
-        __syncwarp();
-      }
-#pragma unroll
-      for (int r = 0; r < RR; ++r) rho[(sp * RR + r) * 32 + lane] = acc[r];
-    }
-    c0 += p.rowcap;
-  } while (c0 < re);
-  __syncthreads();
-  screen_epilogue(p, sh, rho, obj, z, rb, re, post);
-}
-
-// ---------------------------------------------------------------------------
 // exact float64 similarity of object rows to one mean, in the reference order
 
 // headers -> the exact-value lookup view (bivf.cuh: masks, perm, off64)
@@ -1849,15 +1454,14 @@ AssignWs carve_assign(void* base, int64_t n, int64_t k, size_t* total) {
   return w;
 }
 
-static int g_tma_warps = 8;
 static int g_max_warps = 16;  // register screen: warps per CTA at most
 static int g_force_warps = 0;  // register screen: exact warps per CTA (0 = planned)
 
 struct Plan {
   int rr, nsplit, cta_blocks, warps, rowcap;
   bool passes = false;  // nsplit slot-range passes instead of a cluster of nsplit CTAs
-  bool tma;
-  int mode;  // 0 LDG register screen, 1 TMA ring, 2 cp.async ring
+  bool tma = false;  // (staged screens removed in round 2; the plan query reports 0)
+  int mode = 0;
   size_t smem;
 };
 
@@ -1890,38 +1494,12 @@ int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
     // stage the whole row again); beyond, split rho over a thread-block
     // cluster at about half of it per CTA, between 24 KB and 100 KB.
     const int64_t rho = nblk * 128;
-    const int64_t stg = (int64_t)rowcap * (rr < 0 ? 8 : kEntryBytes);
+    const int64_t stg = (int64_t)rowcap * kEntryBytes;
     int64_t b = rho / 2 + (stg > 8 * 1024 ? stg : 8 * 1024);
     if (b < 24 * 1024) b = 24 * 1024;
     if (b > 100 * 1024) b = 100 * 1024;
-    if (rho + stg <= (rr < 0 ? 24 : 64) * 1024) b = kSmemLimit - 2048;
+    if (rho + stg <= 64 * 1024) b = kSmemLimit - 2048;
     smem_limit = (int)b;
-  }
-  if (rr == -8 || rr == -4) {  // TMA (-8) / cp.async (-4) pipelined screens, 8-block spans
-    pl.tma = true;
-    pl.mode = rr == -8 ? 1 : 2;
-    pl.rr = kSpan;
-    pl.rowcap = rowcap < 256 ? rowcap : 256;
-    const int64_t spans_total = nblk / kSpan;
-    for (int s = 1; s <= kMaxSplit; ++s) {
-      int64_t cb = (nblk + s - 1) / s;
-      cb = (cb + kSpan - 1) / kSpan * kSpan;
-      const int spans = (int)(cb / kSpan);
-      const int warps = spans < g_tma_warps ? spans : g_tma_warps;
-      const size_t smem = (size_t)cb * 128 + (size_t)pl.rowcap * 8 + 128 +
-                          (size_t)warps * (pl.mode == 1 ? tma_warp_bytes(pl.rowcap)
-                                                        : async_warp_bytes(pl.rowcap));
-      if (smem <= (size_t)smem_limit) {
-        pl.nsplit = s;
-        pl.cta_blocks = (int)cb;
-        pl.warps = warps;
-        pl.smem = smem;
-        *out = pl;
-        (void)spans_total;
-        return IVFKM_OK;
-      }
-    }
-    return IVFKM_E_UNSUPPORTED;
   }
   pl.tma = false;
   pl.mode = 0;
@@ -1972,12 +1550,9 @@ int plan_maxreg(const Plan& pl, bool half) {
 
 template <int RR>
 int launch_screen(const Plan& pl, const ScreenParams& p, cudaStream_t st) {
-  auto fn = pl.mode == 1 ? screen_tma_kernel
-                         : (pl.mode == 2 ? screen_async_kernel
-                                         : (p.half ? (plan_maxreg(pl, true) == 56
-                                                          ? screen_kernel<RR, true, 56>
-                                                          : screen_kernel<RR, true>)
-                                                   : screen_kernel<RR, false>));
+  auto fn = p.half ? (plan_maxreg(pl, true) == 56 ? screen_kernel<RR, true, 56>
+                                                   : screen_kernel<RR, true>)
+                    : screen_kernel<RR, false>;
   {
     // raise the kernel's dynamic shared-memory limit only when a launch needs
     // more than it was given (per device): the call costs host time on every
@@ -2094,8 +1669,7 @@ extern "C" void ivfkm_set_tuning(int rowcap, int smem_limit, int rr) {
   if (rowcap >= 32 && rowcap <= 8192) g_rowcap = rowcap / 32 * 32;
   if (smem_limit >= 1024 && smem_limit <= kSmemLimit - 2048) g_smem_limit = smem_limit;
   if (smem_limit == -1) g_smem_limit = 0;  // back to adaptive
-  if (rr == 0 || rr == 2 || rr == 4 || rr == 8 || rr == -8 || rr == -4) g_rr = rr;
-  if (rr <= -16 && rr >= -16 * 16) g_tma_warps = -rr / 16;  // -16*w: TMA warps per CTA
+  if (rr == 0 || rr == 2 || rr == 4 || rr == 8) g_rr = rr;
 }
 
 // Tests: force the register screen's warps per CTA (1..16; 0 = planned) —
@@ -2153,7 +1727,6 @@ int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
   Plan pl;
   int rc = plan_screen(a.k, g_rowcap, g_smem_limit, g_rr, &pl);
   if (rc) return rc;
-  if (pl.tma && a.screen_bits != 32) return IVFKM_E_UNSUPPORTED;  // staged screens: fp32 only
   ScreenParams sp;
   sp.n_obj = a.n_obj;
   sp.row_ptr = a.row_ptr;
@@ -2193,7 +1766,6 @@ int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
   sp.st_slot = w.st_slot;
   sp.st_cnt = w.st_cnt;
   sp.st_cand = w.st_cand;
-  if (pl.tma) return launch_screen<8>(pl, sp, st);
   switch (pl.rr) {
     case 8: return launch_screen<8>(pl, sp, st);
     case 4: return launch_screen<4>(pl, sp, st);

@@ -218,8 +218,8 @@ def tuning():
 
 def _assign_raw(ds, means, rowcap=None, smem=None, rr=-1, bits=None, passes=None):
     """Assign through the engine with explicit tuning (rowcap applies per call;
-    rr = 0 automatic LDG screen, 2/4/8 LDG screen with that span, -8 / -4 the
-    TMA / cp.async staged screens, which take fp32 screen values only)."""
+    rr = 0 automatic register screen, 2/4/8 register screen with that span,
+    -1 = leave the tuning; fp32 screen values unless ``bits`` says otherwise)."""
     from paper_2002_09094_b200.variants import engine_for
 
     eng = engine_for(ds, means.k)
@@ -256,7 +256,7 @@ def _random_case(n=1500, dim=400, k=64, seed=0, signed=False, corpus=0):
     return ds, om, means
 
 
-SCREENS = [(0, 16), (0, 32), (-8, 32), (-4, 32), (2, 16), (2, 32)]
+SCREENS = [(0, 16), (0, 32), (2, 16), (2, 32), (4, 16), (8, 32)]
 
 
 @pytest.mark.parametrize("rr,bits", SCREENS)
@@ -286,19 +286,22 @@ def test_multipass_rows(tuning, rowcap, corpus, rr, bits):
     assert np.array_equal(labels, ol) and st.postings == post
 
 
-@pytest.mark.parametrize("k,smem,rr", [(1000, 25 * 1024, -8), (1500, 12 * 1024, -8),
-                                       (1000, 25 * 1024, -4), (1500, 12 * 1024, -4),
-                                       (1000, 3 * 1024, 0), (1500, 2560, 0)])
+@pytest.mark.parametrize("k,smem,rr", [(1000, 3 * 1024, 0), (1500, 2560, 0),
+                                       (3000, 5 * 1024, 0), (6000, 9 * 1024, 0),
+                                       (2000, 4 * 1024, 4), (2000, 4 * 1024, 8)])
 @pytest.mark.parametrize("bits", [16, 32])
 def test_cluster_split_dsmem(tuning, k, smem, rr, bits):
     """Force the thread-block-cluster split (rho spread over 2-8 CTAs' shared
     memory, argmax and candidate window merged over DSMEM)."""
     from oracle import oracle as O
 
-    ds, om, means = _random_case(seed=6, k=k, n=2500)
-    if rr < 0 and bits == 16:
-        pytest.skip("the staged screens take fp32 screen values only")
-    labels, st = _assign_raw(ds, means, rowcap=64, smem=smem, rr=rr, bits=bits)
+    from paper_2002_09094_b200 import _lib
+
+    ds, om, means = _random_case(seed=6, k=k, n=max(2500, k + 500))
+    labels, st = _assign_raw(ds, means, rowcap=64, smem=smem, rr=rr, bits=bits, passes=1)
+    out = np.zeros(8, np.int32)
+    _lib.load().ivfkm_screen_plan(k, 64, bits, out.ctypes.data)
+    assert out[1] >= 2  # the cluster split ran (2-8 CTAs per object)
     ol, _, _, post = O.assign(ds, om)
     assert np.array_equal(labels, ol) and st.postings == post
     assert st.objective == O.objective(ds, ol, om)
