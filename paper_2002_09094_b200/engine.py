@@ -125,6 +125,36 @@ class HostDataset:
         return sum(t.numel() * t.element_size() for t in self._arrays())
 
 
+def _upload(a: np.ndarray, dev, chunk: int = 64 << 20) -> torch.Tensor:
+    """Host array -> device through two pinned staging buffers (chunked,
+    asynchronous, double-buffered): pageable copies run at a fraction of the
+    PCIe bandwidth."""
+    a = np.ascontiguousarray(a)
+    out = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, device=dev)
+    nbytes = a.nbytes
+    if nbytes <= chunk or not torch.cuda.is_available():
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", UserWarning)
+            out.copy_(torch.from_numpy(a))
+        return out
+    src = a.reshape(-1).view(np.uint8)
+    dst = out.view(-1).view(torch.uint8)
+    stage = [torch.empty(chunk, dtype=torch.uint8).pin_memory() for _ in range(2)]
+    done = [None, None]
+    st = torch.cuda.current_stream()
+    for i, off in enumerate(range(0, nbytes, chunk)):
+        b = i & 1
+        if done[b] is not None:
+            done[b].synchronize()  # the copy out of this staging buffer has finished
+        n = min(chunk, nbytes - off)
+        stage[b][:n].numpy()[:] = src[off:off + n]
+        dst[off:off + n].copy_(stage[b][:n], non_blocking=True)
+        done[b] = torch.cuda.Event()
+        done[b].record(st)
+    st.synchronize()
+    return out
+
+
 class DeviceDataset:
     """Objects on the device: int64 row_ptr, 0-based int32 terms, fp32 values
     (screening) and fp64 values (rescoring, update), fp64 row norms."""
@@ -184,11 +214,9 @@ class DeviceDataset:
         self.n, self.dim, self.nnz = int(ip.size - 1), int(ds.dim), int(ip[-1])
         self.max_row = int(np.diff(ip).max()) if self.n else 0
         self.device = dev
-        with warnings.catch_warnings():  # read-only reference arrays: only read here
-            warnings.simplefilter("ignore", UserWarning)
-            self.row_ptr = torch.from_numpy(ip).to(dev)
-            self.terms = torch.from_numpy(t1).to(dev)  # 1-based; made 0-based in place below
-            self.val64 = torch.from_numpy(v).to(dev)
+        self.row_ptr = _upload(ip, dev)
+        self.terms = _upload(t1, dev)  # 1-based; made 0-based in place below
+        self.val64 = _upload(v, dev)
         self.val32 = torch.empty(max(self.nnz, 1), dtype=torch.float32, device=dev)[:self.nnz]
         self.xnorm = torch.empty(max(self.n, 1), dtype=torch.float64, device=dev)[:self.n]
         self._pending = ()
