@@ -130,7 +130,9 @@ def _upload(a: np.ndarray, dev, chunk: int = 64 << 20) -> torch.Tensor:
     asynchronous, double-buffered): pageable copies run at a fraction of the
     PCIe bandwidth."""
     a = np.ascontiguousarray(a)
-    out = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, device=dev)
+    with warnings.catch_warnings():  # read-only reference arrays: only read here
+        warnings.simplefilter("ignore", UserWarning)
+        out = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, device=dev)
     nbytes = a.nbytes
     if nbytes <= chunk or not torch.cuda.is_available():
         with warnings.catch_warnings():
