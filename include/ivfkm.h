@@ -158,13 +158,16 @@ void ivfkm_set_screen_warps(int warps);
  * (presort_terms int32[nnz], presort_vals fp32[nnz], [dev], or NULL): when
  * the plan runs passes, each row's entries are first sorted by the terms'
  * dense prefix, longest first, into them, so that every pass stages its rows
- * by copying instead of sorting them again. */
+ * by copying instead of sorting them again.  slot8 (ivfkm_bivf_slots, fp16
+ * screens): the sparse spans are read through their slot bytes instead of
+ * the block masks. */
 int ivfkm_assign_screen_ex(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
                            const float* val32, const double* xnorm, int64_t k, int64_t dim,
                            const uint32_t* headers, const void* pval_screen, int screen_bits,
                            double mu_max, ivfkm_stats* stats, const int32_t* order,
-                           int32_t* presort_terms, float* presort_vals, void* ws,
-                           size_t ws_bytes, ivfkm_stream_t stream);
+                           int32_t* presort_terms, float* presort_vals,
+                           const uint8_t* slot8 /*[dev] or NULL*/, void* ws, size_t ws_bytes,
+                           ivfkm_stream_t stream);
 /* Screen tuning: which = 1: slot-range passes for the next screens (0 or 1
  * = one pass).  With P > 1 passes the fp16 register screen runs P launches,
  * each over all objects and 1/P of the slots (one CTA per object, no
@@ -283,6 +286,14 @@ int ivfkm_update_fill(int64_t n_obj, int64_t nnz, int64_t k, int64_t dim,
                       const int64_t* new_ptr, int32_t* new_terms /*[dev]*/,
                       double* new_vals /*[dev]*/, uint8_t* retained /*[dev] k*/,
                       int64_t capacity, void* ws, size_t ws_bytes, ivfkm_stream_t stream);
+
+/* Slot bytes of the BIVF's sparse spans ([dev] slot8: one byte per screen
+ * value position — ivfkm_bivf_values_capacity() of them — written only at
+ * the positions of sparse-span postings: the posting's slot within its
+ * 256-slot span).  Call after the fill; read by ivfkm_assign_screen_ex. */
+int ivfkm_bivf_slots(int64_t k, int64_t dim, int major, int64_t nrows, const int64_t* ptr,
+                     const int32_t* cols, const uint32_t* headers, uint8_t* slot8,
+                     ivfkm_stream_t stream);
 
 /* ---- IVFD, object-inverted (_kernels.pyx:178-207) ------------------------
  * The paper's comparison variant in its own loop order: means outermost, each

@@ -74,6 +74,7 @@ struct ScreenParams {
   const uint32_t* dpre;   // [dim] dense prefix spans per term
   const int32_t* inv;     // [k] slot -> mean
   const int32_t* order;   // [n] processing order of objects, or nullptr
+  const uint8_t* slot8 = nullptr;  // sparse spans' slot bytes (ivfkm_bivf_slots), or nullptr
   const int32_t* ps_t = nullptr;  // rows presorted by dense prefix (ivfkm_presort_rows), or
   const float* ps_v = nullptr;    // nullptr: the CTA sorts its staged row itself
   const float* pv32;  // fp32 screen values, or fp16 ones when half
@@ -358,7 +359,9 @@ __device__ __forceinline__ double window_eps(const ScreenParams& p, int64_t obj,
   const double xn = p.xnorm ? p.xnorm[obj] : 1.0;
   // fp16 screen values add a relative 2^-11 rounding per mean value plus an
   // absolute 2^-25 below fp16's normal range (sum over h of |x_h| <= n*|x|)
-  return p.half ? (0x1p-11 + (double)(n_i + 4) * 0x1p-24) * xn * p.mu_max * (1.0 + 0x1p-9) +
+  // (n_i + 5): the sparse spans' products are summed apart and folded in
+  // with one more rounding (screen_kernel)
+  return p.half ? (0x1p-11 + (double)(n_i + 5) * 0x1p-24) * xn * p.mu_max * (1.0 + 0x1p-9) +
                       (double)n_i * xn * 0x1p-25 * (1.0 + 0x1p-9) + (double)(n_i + 1) * 0x1p-125
                 : ((double)(n_i + 3) * 0x1p-24 + (double)n_i * 0x1p-50) * xn * p.mu_max *
                           (1.0 + 1e-6) +
@@ -596,6 +599,8 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
   int4* s_ent = reinterpret_cast<int4*>(rho + cta_cids);
   uint16_t* s_pos = reinterpret_cast<uint16_t*>(s_ent + p.rowcap);
   uint8_t* s_lp = reinterpret_cast<uint8_t*>(s_pos + p.rowcap);
+  // slot-byte sparse path: a 256-slot scratch per warp (zero between spans)
+  float* s_scr = reinterpret_cast<float*>(s_lp + ((p.rowcap + 15) & ~15));
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -615,6 +620,9 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
   // otherwise re-load kernel parameters from the constant bank inside every
   // predicated gather (one extra LDC per posting block).
   __shared__ const void* s_base[3];
+  if (HALF && RR == 8 && p.slot8) {
+    for (int q = threadIdx.x; q < (int)(blockDim.x >> 5) * 256; q += blockDim.x) s_scr[q] = 0.f;
+  }
   if (threadIdx.x == 0) {
     s_base[0] = p.masks;
     s_base[1] = p.offs;
@@ -797,7 +805,86 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
             o = 0u;
           }
         };
-        if (nd < cn) {
+        if constexpr (HALF && RR == 8) {
+          if (p.slot8 && nd < cn) {
+            // Sparse spans (< dense_fill*256 postings): the span's values are
+            // contiguous at its offset and their slots are in slot8 — a lane
+            // per posting, products summed into the warp's slot scratch in
+            // entry order (deterministic: one entry's slots are distinct),
+            // folded into the registers once per span.  Dense spans beyond
+            // the prefix: one 16-B load per lane as in the dense loop.
+            float* scr = s_scr + warp * 256;
+            float2* stg = reinterpret_cast<float2*>(s_scr + (blockDim.x >> 5) * 256) + warp * 32;
+            const unsigned short* p16 = static_cast<const unsigned short*>(pv);
+            bool any = false;
+            // four entries at a time, eight lanes each (a sparse span holds
+            // fewer than dense_fill*256 postings — 4 by default — padded to a
+            // multiple of 8 values)
+            const int g = lane >> 3, gi = lane & 7;
+            for (int e0 = nd; e0 < cn; e0 += 4) {
+              const int e = e0 + g;
+              uint32_t o0 = 0u, cnt = 0u;
+              float v = 0.f;
+              bool dense = false;
+              if (e < cn) {
+                const uint32_t row = (uint32_t)s_ent[e].x + gb32;
+                o0 = __ldg(offs + row);
+                v = __int_as_float(s_ent[e].y);
+                dense = (o0 & kDense) != 0u;
+                if (!dense) cnt = (__ldg(offs + row + kSpan) & ~kDense) - o0;
+              }
+              // dense spans beyond the prefix (rare): whole-warp 16-B loads, in entry order
+              unsigned dm = __ballot_sync(kFull, dense && gi == 0);
+              while (dm) {
+                const int src = __ffs(dm) - 1;
+                dm &= dm - 1u;
+                const uint32_t od = __shfl_sync(kFull, o0, src) & ~kDense;
+                const float vd = __shfl_sync(kFull, v, src);
+                SpanVals<RR, HALF, HALF && MAXREG == 56> q;
+                q.load_dense(static_cast<const char*>(pv) + 2u * (od + 8u * (uint32_t)lane));
+                q.fma(vd, acc);
+              }
+              // sparse postings: a lane each, eight per entry and round (one
+              // round under the default dense_fill); equal slots of different
+              // entries are added by the lowest lane, in lane order
+              const uint32_t rounds = (__reduce_max_sync(kFull, dense ? 0u : cnt) + 7u) >> 3;
+              for (uint32_t j = 0; j < rounds; ++j) {
+                const uint32_t pi = (uint32_t)gi + 8u * j;
+                int sl = 256 + lane;  // distinct sentinel: nothing to add
+                float u = 0.f;
+                if (!dense && pi < cnt) {
+                  const unsigned short hv = __ldg(p16 + o0 + pi);
+                  if (hv & 0x7fffu) {  // padding (and an fp16 underflow) is +-0
+                    sl = __ldg(p.slot8 + o0 + pi);
+                    u = __half2float(__ushort_as_half(hv));
+                  }
+                }
+                any = any || __any_sync(kFull, sl < 256);
+                stg[lane] = make_float2(v, u);
+                const unsigned peers = __match_any_sync(kFull, sl);
+                __syncwarp();
+                if (sl < 256 && lane == __ffs(peers) - 1) {
+                  float acc_s = scr[sl];
+                  for (unsigned pm = peers; pm; pm &= pm - 1u) {
+                    const float2 vu = stg[__ffs(pm) - 1];
+                    acc_s = fmaf(vu.x, vu.y, acc_s);
+                  }
+                  scr[sl] = acc_s;
+                }
+                __syncwarp();
+              }
+            }
+            if (any) {
+#pragma unroll
+              for (int r = 0; r < RR; ++r) {
+                acc[r] += scr[32 * r + lane];
+                scr[32 * r + lane] = 0.f;
+              }
+              __syncwarp();
+            }
+          }
+        }
+        if (nd < cn && !(HALF && RR == 8 && p.slot8)) {
           MaskPack<RR> mk;
           uint32_t o;
           ld(nd, mk, o);
@@ -1484,7 +1571,8 @@ int choose_warps(int spans, size_t smem) {
   return best_w;
 }
 
-int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
+int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out,
+                bool sparse_scratch = false) {
   const int64_t nblk = ivfkm_bivf_nblk(k);
   Plan pl;
   const bool adaptive = smem_limit <= 0;
@@ -1538,6 +1626,10 @@ int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out) {
   const int best_w = choose_warps(pl.cta_blocks / pl.rr, pl.smem);
   pl.warps = g_max_warps < best_w ? g_max_warps : best_w;
   if (g_force_warps > 0) pl.warps = g_force_warps;  // tests: any count is valid
+  // the sparse-span path's slot scratch (1 KB per warp) after the 16-B
+  // aligned stage (fp16 8-block spans only)
+  if (sparse_scratch && pl.rr == 8)
+    pl.smem += 16 + (size_t)pl.warps * (256 * sizeof(float) + 32 * sizeof(float2));
   *out = pl;
   return IVFKM_OK;
 }
@@ -1721,11 +1813,13 @@ struct AssignArgs {
   const int32_t* order;
   const int32_t* ps_t = nullptr;  // presorted rows (pass mode), see ivfkm_assign_screen_ex
   float* ps_v = nullptr;
+  const uint8_t* slot8 = nullptr;  // sparse spans' slot bytes (ivfkm_bivf_slots)
 };
 
 int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
   Plan pl;
-  int rc = plan_screen(a.k, g_rowcap, g_smem_limit, g_rr, &pl);
+  int rc = plan_screen(a.k, g_rowcap, g_smem_limit, g_rr, &pl,
+                       a.slot8 != nullptr && a.screen_bits == 16);
   if (rc) return rc;
   ScreenParams sp;
   sp.n_obj = a.n_obj;
@@ -1762,6 +1856,7 @@ int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
     sp.ps_t = a.ps_t;
     sp.ps_v = a.ps_v;
   }
+  if (a.screen_bits == 16 && pl.rr == 8) sp.slot8 = a.slot8;
   sp.st_best = w.st_best;
   sp.st_slot = w.st_slot;
   sp.st_cnt = w.st_cnt;
@@ -1835,8 +1930,8 @@ extern "C" int ivfkm_assign_screen_ex(int64_t n_obj, const int64_t* row_ptr,
                                       const uint32_t* headers, const void* pval_screen,
                                       int screen_bits, double mu_max, ivfkm_stats* stats,
                                       const int32_t* order, int32_t* presort_terms,
-                                      float* presort_vals, void* ws, size_t ws_bytes,
-                                      ivfkm_stream_t stream_);
+                                      float* presort_vals, const uint8_t* slot8, void* ws,
+                                      size_t ws_bytes, ivfkm_stream_t stream_);
 
 extern "C" int ivfkm_assign_screen(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
                                    const float* val32, const double* xnorm, int64_t k,
@@ -1846,7 +1941,7 @@ extern "C" int ivfkm_assign_screen(int64_t n_obj, const int64_t* row_ptr, const 
                                    ivfkm_stream_t stream_) {
   return ivfkm_assign_screen_ex(n_obj, row_ptr, terms, val32, xnorm, k, dim, headers,
                                 pval_screen, screen_bits, mu_max, stats, order, nullptr, nullptr,
-                                ws, ws_bytes, stream_);
+                                nullptr, ws, ws_bytes, stream_);
 }
 
 extern "C" int ivfkm_assign_screen_ex(int64_t n_obj, const int64_t* row_ptr,
@@ -1855,8 +1950,8 @@ extern "C" int ivfkm_assign_screen_ex(int64_t n_obj, const int64_t* row_ptr,
                                       const uint32_t* headers, const void* pval_screen,
                                       int screen_bits, double mu_max, ivfkm_stats* stats,
                                       const int32_t* order, int32_t* presort_terms,
-                                      float* presort_vals, void* ws, size_t ws_bytes,
-                                      ivfkm_stream_t stream_) {
+                                      float* presort_vals, const uint8_t* slot8, void* ws,
+                                      size_t ws_bytes, ivfkm_stream_t stream_) {
   if (n_obj < 0 || k < 1 || dim < 1 || !row_ptr || !stats || !headers) return IVFKM_E_ARG;
   if (screen_bits != 32 && screen_bits != 16) return IVFKM_E_ARG;
   // fp16 holds mean values up to 65504; unit-norm means are far inside
@@ -1873,6 +1968,7 @@ extern "C" int ivfkm_assign_screen_ex(int64_t n_obj, const int64_t* row_ptr,
                headers, pval_screen, screen_bits, nullptr, mu_max,  stats, order};
   a.ps_t = presort_terms;
   a.ps_v = presort_vals;
+  a.slot8 = slot8;
   return screen_impl(a, w, st);
 }
 

@@ -659,6 +659,47 @@ extern "C" int ivfkm_bivf_plan_fill(int64_t k, int64_t dim, int major, int64_t n
                    val64, as_stream(stream_), nnz, ws_fill);
 }
 
+namespace {
+// Slot bytes of the sparse spans: for a posting stored in a sparse span at
+// screen position o + below, its slot within the span (0..255) at the same
+// position of `slot8` — the screen's sparse path then needs neither masks
+// nor popcounts.  Dense spans' positions are left untouched (never read).
+__global__ void bivf_slot_kernel(int major, int64_t nrows, const int64_t* __restrict__ ptr,
+                                 const int32_t* __restrict__ cols, int64_t k, int64_t dim,
+                                 int64_t nblk, const unsigned int* __restrict__ hdr,
+                                 const int32_t* __restrict__ perm, uint8_t* __restrict__ slot8) {
+  const int64_t nh = bivf_nh(dim, nblk);
+  for_each_entry(nrows, ptr, [&](int64_t r, int64_t q) {
+    const int64_t col = cols[q];
+    const int64_t c = major == 0 ? r : col;
+    const int64_t t = major == 0 ? col : r;
+    if (c < 0 || c >= k || t < 0 || t >= dim) return;
+    const int64_t sl = perm[c];
+    const int64_t b = sl >> 5;
+    const uint32_t j = (uint32_t)(sl & 31);
+    const uint32_t o = hdr[nh + t * nblk + b];
+    if (o & kDense) return;
+    const uint32_t m = hdr[t * nblk + b];
+    slot8[(int64_t)o + __popc(m & ((1u << j) - 1u))] = (uint8_t)(sl & 255);
+  });
+}
+}  // namespace
+
+extern "C" int ivfkm_bivf_slots(int64_t k, int64_t dim, int major, int64_t nrows,
+                                const int64_t* ptr, const int32_t* cols, const uint32_t* headers,
+                                uint8_t* slot8, ivfkm_stream_t stream_) {
+  if (int rc = check_build_args(k, dim, major, nrows, ptr, headers)) return rc;
+  if (!slot8) return IVFKM_E_ARG;
+  const int64_t nblk = ivfkm_bivf_nblk(k);
+  const int64_t nh = bivf_nh(dim, nblk);
+  const int32_t* perm = reinterpret_cast<const int32_t*>(headers + 2 * nh + 1 + dim);
+  cudaStream_t st = as_stream(stream_);
+  bivf_slot_kernel<<<num_sms() * 8, 256, 0, st>>>(major, nrows, ptr, cols, k, dim, nblk, headers,
+                                                  perm, slot8);
+  IVFKM_CHECK_LAUNCH();
+  return IVFKM_OK;
+}
+
 extern "C" int ivfkm_bivf_build(int64_t k, int64_t dim, int major, int64_t nrows,
                                 const int64_t* ptr, const int32_t* cols, const double* vals,
                                 uint32_t* headers, void* val_screen, int screen_bits,

@@ -236,6 +236,7 @@ class DeviceMeans:
         self.ptr, self.terms, self.vals, self.retained = ptr, terms, vals, retained
         self.nnz = int(terms.numel())
         self.headers = self.pvs = self.pv64 = None
+        self.slot8 = None  # sparse spans' slot bytes (ivfkm_bivf_slots), or None
         self.screen_bits = 32  # precision of pvs (the screen's values), set by build_bivf
 
     @classmethod
@@ -381,6 +382,10 @@ class LloydEngine:
         # slot-range passes stage presorted rows (ivfkm_assign_screen_ex)
         self.presort = True
         self._presort = None
+        # sparse spans read through their slot bytes (ivfkm_bivf_slots): None =
+        # at large k (>= 16 spans), where they are a sixth of the screen's pairs
+        self.sparse_slots = None
+        self._slotbuf = [None, None]
         self._xinv = None
         self._ivfd_ws = None
 
@@ -436,6 +441,19 @@ class LloydEngine:
         dm.pvs = buf["pvs"][:max(n_s, 1)]
         dm.pv64 = buf["pv64"][:max(n_64, 1)]
         dm.screen_bits = bits
+        dm.slot8 = None
+        use_slots = self.sparse_slots if self.sparse_slots is not None else self.nblk // 8 >= 16
+        if use_slots and bits == 16:
+            par = self._bvpar ^ 1  # the value buffers' parity of this build
+            sb = self._slotbuf[par]
+            if sb is None or sb.numel() < n_s:
+                sb = torch.empty(int(n_s * 1.25) + 1024, dtype=torch.uint8, device=dev)
+                self._slotbuf[par] = sb
+            _lib.check(self.lib.ivfkm_bivf_slots(self.k, dm.dim, 0, self.k, _p(dm.ptr),
+                                                 _p(dm.terms), _p(dm.headers), _p(sb), _stream()),
+                       "ivfkm_bivf_slots")
+            dm.slot8 = sb
+            self.launches += 1
         # plan: sizes, CUB sort of the k slot keys (single tile / onesweep), perm,
         # mask, count, 2 scans (init + sweep each), offset, nc, {mask, offset}
         # pairs; fill: zero, position keys, CUB onesweep sort of the keys' top
@@ -504,6 +522,7 @@ class LloydEngine:
                                              _p(dd.xnorm), self.k, dd.dim, _p(dm.headers),
                                              _p(dm.pvs), dm.screen_bits, _MU_MAX, _p(self.stats),
                                              _p(order), _p(ps[0]), _p(ps[1]),
+                                             _p(dm.slot8 if dm.screen_bits == 16 else None),
                                              _p(self.ws_assign), self.ws_assign.numel(), st)
         _lib.check(rc, "ivfkm_assign_screen_ex")
         if ps[0] is not None:

@@ -216,7 +216,7 @@ def tuning():
     lib.ivfkm_set_tuning(1024, -1, 0)
 
 
-def _assign_raw(ds, means, rowcap=None, smem=None, rr=-1, bits=None, passes=None):
+def _assign_raw(ds, means, rowcap=None, smem=None, rr=-1, bits=None, passes=None, slots=None):
     """Assign through the engine with explicit tuning (rowcap applies per call;
     rr = 0 automatic register screen, 2/4/8 register screen with that span,
     -1 = leave the tuning; fp32 screen values unless ``bits`` says otherwise)."""
@@ -227,6 +227,7 @@ def _assign_raw(ds, means, rowcap=None, smem=None, rr=-1, bits=None, passes=None
         eng.rowcap = rowcap
     eng.screen_bits = bits or (32 if rr < 0 else 16)
     eng.passes = passes
+    eng.sparse_slots = slots
     eng.lib.ivfkm_set_tuning(eng.rowcap, smem or 0, rr)
     try:
         dm = eng.upload_means(means)
@@ -236,6 +237,7 @@ def _assign_raw(ds, means, rowcap=None, smem=None, rr=-1, bits=None, passes=None
         eng.rowcap = max(32, min(512, (eng.dd.max_row + 31) // 32 * 32))
         eng.screen_bits = 16
         eng.passes = None
+        eng.sparse_slots = None
     return lab.cpu().numpy() + 1, st
 
 
@@ -642,7 +644,7 @@ def test_bivf_build_stays_within_capacity(bits, fill):
         assert total <= cap
         assert bool((vs[cap * esz:] == 0x5A).all()) and bool((v64[cap * 8:] == 0x5A).all())
     finally:
-        lib.ivfkm_set_bivf_options(0.25, 1)
+        lib.ivfkm_set_bivf_options(1.0 / 64.0, 1)  # the default
 
 
 def test_bivf_plan_reports_out_of_range_ids():
@@ -768,3 +770,33 @@ def test_update_fill_never_writes_past_capacity():
     assert lib.ivfkm_update_fill(n, nnz, k, dim, _p(sizes), _p(pptr), _p(pterms), _p(pvals),
                                  _p(new_ptr), _p(tb), _p(vb), _p(ret), -1, _p(ws), ws.numel(),
                                  _stream()) == -1  # IVFKM_E_ARG
+
+
+@pytest.mark.parametrize("slots", [True, False])
+@pytest.mark.parametrize("seed,k,signed,passes", [(0, 300, False, 1), (1, 1000, True, 1),
+                                                  (2, 5000, True, None), (3, 5000, False, 4),
+                                                  (4, 2500, True, 1)])
+def test_sparse_span_slot_path_matches_oracle(tuning, slots, seed, k, signed, passes):
+    """The sparse spans read through the BIVF's slot bytes (ivfkm_bivf_slots:
+    products summed per slot in a warp scratch, folded once per span) against
+    the block-mask path and the oracle; one pass, passes, cluster split."""
+    from oracle import oracle as O
+
+    ds, om, means = _random_case(n=k + 800, dim=2500, k=k, seed=60 + seed, signed=signed)
+    labels, st = _assign_raw(ds, means, bits=16, passes=passes, slots=slots)
+    ol, _, _, post = O.assign(ds, om)
+    assert np.array_equal(labels, ol) and st.postings == post
+    assert st.objective == O.objective(ds, ol, om)
+    if seed == 1:  # sparse spans of up to 63 postings (dense_fill 1/4): several rounds
+        from paper_2002_09094_b200 import _lib
+
+        _lib.load().ivfkm_set_bivf_options(0.25, 1)
+        try:
+            labels, st = _assign_raw(ds, means, bits=16, passes=passes, slots=slots)
+        finally:
+            _lib.load().ivfkm_set_bivf_options(1.0 / 64.0, 1)
+        assert np.array_equal(labels, ol) and st.objective == O.objective(ds, ol, om)
+    if seed == 4:  # and under a forced thread-block-cluster split
+        labels, st = _assign_raw(ds, means, bits=16, passes=1, slots=slots, rowcap=64,
+                                 smem=6 * 1024, rr=8)
+        assert np.array_equal(labels, ol) and st.objective == O.objective(ds, ol, om)

@@ -102,7 +102,7 @@ def main():
             print(json.dumps(rec), flush=True)
     eng.lib.ivfkm_set_tuning(1024, 0, 0)
     eng.lib.ivfkm_set_tuning(1024, 0, -128)
-    eng.lib.ivfkm_set_bivf_options(0.25, 1)
+    eng.lib.ivfkm_set_bivf_options(1.0 / 64.0, 1)  # the default
 
 
 if __name__ == "__main__":
