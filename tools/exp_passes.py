@@ -26,7 +26,8 @@ def main():
     ap.add_argument("--maxreg", default="56", help="(recorded only)")
     ap.add_argument("--presort", default="1", help="pass mode stages presorted rows: 1,0")
     ap.add_argument("--tma", default="0", help="(removed variant)")
-    ap.add_argument("--hot", default="0", help="L1-kept hot terms: 0,16,64")
+    ap.add_argument("--hot", default="0", help="(removed variant)")
+    ap.add_argument("--fill", default="0.015625", help="BIVF dense_fill values to sweep")
     a = ap.parse_args()
     c = synth.CONFIGS[a.config]
     ds = synth.make_dataset(c["corpus"])
@@ -43,7 +44,8 @@ def main():
     from bench import Clocks
     rc0 = eng.rowcap
     base = None
-    for r, pf, w, rc, mr, ps, tm, hot in itertools.product(map(int, a.passes.split(",")),
+    last_fill = None
+    for fill, r, pf, w, rc, mr, ps, tm, hot in itertools.product(map(float, a.fill.split(",")),map(int, a.passes.split(",")),
                                                       map(int, a.pf.split(",")),
                                                       map(int, a.warps.split(",")),
                                                       map(int, a.rowcap.split(",")),
@@ -52,6 +54,10 @@ def main():
                                                       map(int, a.tma.split(",")),
                                                       map(int, a.hot.split(","))):
         eng.presort = bool(ps)
+        if fill != last_fill:
+            eng.lib.ivfkm_set_bivf_options(fill, 1)
+            dm = eng.build_bivf(dm)
+            last_fill = fill
         eng.lib.ivfkm_set_screen_warps(w)
         eng.rowcap = rc or rc0
         eng.passes = r if r > 0 else None  # 0: the engine's plan
@@ -69,9 +75,10 @@ def main():
         st = eng.read_stats()
         ck = clk.stop() or {}
         print(json.dumps({"sm_mhz": ck.get("sm_mhz"), "reasons": ck.get("reasons"), "config": a.config, "passes": r, "planned": eng.screen_passes(dm), "warps": w, "rowcap": eng.rowcap,
-                          "maxreg": mr, "presort": ps, "hot": hot, "labels_ok": ok, "screen_ms": min(ts), "all": ts,
+                          "maxreg": mr, "presort": ps, "fill": fill, "labels_ok": ok, "screen_ms": min(ts), "all": ts,
                           "postings": st.postings}), flush=True)
     eng.lib.ivfkm_set_screen_warps(0)
+    eng.lib.ivfkm_set_bivf_options(1.0 / 64.0, 1)
 
 
 if __name__ == "__main__":
