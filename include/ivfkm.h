@@ -276,6 +276,11 @@ int ivfkm_update_count_delta(int64_t n_obj, int64_t nnz, const int64_t* row_ptr,
                              const int64_t* prev_ptr, int64_t* new_ptr, void* ws,
                              size_t ws_bytes, void* state /*[dev] zero-filled first*/,
                              size_t state_bytes, ivfkm_stream_t stream);
+/* Update tuning: which = 1: the label-delta sort's merge (0 = one fused
+ * merge with deletions, the default; 1 = two stable CUB selects + a CUB
+ * merge).  Both give the same sorted state.  IVFKM_E_ARG for an unknown
+ * `which`. */
+int ivfkm_set_update_option(int which, int value);
 /* fill: `capacity` = entries new_terms/new_vals hold.  Size them by the
  * exact count new_ptr[k] (read after count) or by the bound
  * min(nnz + prev_ptr[k], k * dim) (runs <= nnz, plus retained means'

@@ -66,6 +66,7 @@ SIGNATURES = {
     "ivfkm_set_tuning": (None, [C.c_int, C.c_int, C.c_int]),
     "ivfkm_set_screen_warps": (None, [C.c_int]),
     "ivfkm_set_screen_option": (C.c_int, [C.c_int, C.c_int]),
+    "ivfkm_set_update_option": (C.c_int, [C.c_int, C.c_int]),
     "ivfkm_screen_plan": (C.c_int, [_i64, C.c_int, C.c_int, _vp]),
     "ivfkm_row_order_workspace_size": (_sz, [_i64]),
     "ivfkm_row_order": (C.c_int, [_i64, _vp, _vp, _vp, _sz, _vp]),

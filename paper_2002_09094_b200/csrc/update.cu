@@ -576,10 +576,13 @@ struct DeltaState {
   unsigned long long* bkey[2];   // changed entries (B), capacity nnz/4
   double* bval[2];
   uint8_t* oflag;                // n_obj: changed
+  uint32_t* obits;               // n_obj bits: changed (the merge's lookups stay in L1)
   int32_t* clist;                // n_obj: changed objects
   int64_t* cptr;                 // n_obj+1: their entry offsets in B
   unsigned long long* counts;    // [0] changed objects, [1] their entries, [2] selected
   int32_t* plan;                 // the norm's tree plan, uploaded once (hdr.pad = its dim)
+  int64_t* tcnt;                 // merge with deletions: kept entries per tile, scanned
+  int64_t* tb;                   // B entries below each tile's first key
   void* cub;
   size_t cub_bytes;
 };
@@ -595,6 +598,10 @@ struct KeptFlag {
 
 int64_t delta_cap(int64_t nnz) { return nnz / 4 + 1024; }
 
+// 0: one fused merge with deletions (mdel_*_kernel); 1: round 1's two CUB
+// stable selects + CUB merge (A/B and tests; ivfkm_set_update_option)
+int g_delta_cub_merge = 0;
+
 DeltaState carve_delta(void* base, int64_t n_obj, int64_t nnz, int64_t dim, size_t* total) {
   Carver c(base);
   DeltaState d;
@@ -609,11 +616,14 @@ DeltaState carve_delta(void* base, int64_t n_obj, int64_t nnz, int64_t dim, size
     d.bval[b] = c.take<double>(nb);
   }
   d.oflag = c.take<uint8_t>(no);
+  d.obits = c.take<uint32_t>(no / 32 + 1);
   d.clist = c.take<int32_t>(no);
   d.cptr = c.take<int64_t>(no + 1);
   d.counts = c.take<unsigned long long>(4);
   d.plan = c.take<int32_t>((size_t)norm_plan_ints_max(dim));
-  size_t a = 0, b = 0, m = 0, sc = 0, so = 0;
+  d.tcnt = c.take<int64_t>((size_t)n / 2048 + 2);
+  d.tb = c.take<int64_t>((size_t)n / 2048 + 2);
+  size_t a = 0, b = 0, m = 0, sc = 0, so = 0, st = 0;
   cub::DoubleBuffer<unsigned long long> kb(nullptr, nullptr);
   cub::DoubleBuffer<double> vb(nullptr, nullptr);
   cub::DeviceRadixSort::SortPairs(nullptr, a, kb, vb, (int)n, 0, 64);
@@ -633,7 +643,9 @@ DeltaState carve_delta(void* base, int64_t n_obj, int64_t nnz, int64_t dim, size
   cub::DeviceScan::ExclusiveSum(nullptr, sc, (int64_t*)nullptr, (int64_t*)nullptr, (int)no + 1);
   cub::DeviceSelect::Flagged(nullptr, so, (int32_t*)nullptr, (uint8_t*)nullptr,
                              (int32_t*)nullptr, (unsigned long long*)nullptr, (int)no);
-  d.cub_bytes = std::max(std::max(a, b), std::max(std::max(m, sc), so));
+  cub::DeviceScan::ExclusiveSum(nullptr, st, (int64_t*)nullptr, (int64_t*)nullptr,
+                                (int)(n / 2048 + 2));
+  d.cub_bytes = std::max(std::max(std::max(a, b), st), std::max(std::max(m, sc), so));
   d.cub = c.take_bytes(d.cub_bytes);
   if (total) *total = c.off;
   return d;
@@ -686,17 +698,24 @@ __global__ void comp_keys_kernel(int64_t n_obj, const int64_t* __restrict__ row_
 
 __global__ void changed_kernel(int64_t n_obj, const int32_t* __restrict__ labels,
                                const int32_t* __restrict__ old, const int64_t* __restrict__ row_ptr,
-                               uint8_t* __restrict__ oflag, int64_t* __restrict__ len,
-                               unsigned long long* __restrict__ counts) {
+                               uint8_t* __restrict__ oflag, uint32_t* __restrict__ obits,
+                               int64_t* __restrict__ len, unsigned long long* __restrict__ counts) {
   unsigned long long co = 0, ce = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_obj;
+  // whole warps walk 32 consecutive objects (the ballot is one mask word)
+  const int64_t n32 = (n_obj + 31) & ~31ll;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n32;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const bool ch = labels[i] != old[i];
-    oflag[i] = ch ? 1 : 0;
-    const int64_t l = ch ? row_ptr[i + 1] - row_ptr[i] : 0;
-    len[i] = l;
-    co += ch;
-    ce += (unsigned long long)l;
+    const bool in = i < n_obj;
+    const bool ch = in && labels[i] != old[i];
+    const unsigned m = __ballot_sync(0xffffffffu, ch);
+    if ((threadIdx.x & 31) == 0) obits[i >> 5] = m;
+    if (in) {
+      oflag[i] = ch ? 1 : 0;
+      const int64_t l = ch ? row_ptr[i + 1] - row_ptr[i] : 0;
+      len[i] = l;
+      co += ch;
+      ce += (unsigned long long)l;
+    }
   }
   for (int off = 16; off > 0; off >>= 1) {
     co += __shfl_xor_sync(0xffffffffu, co, off);
@@ -730,6 +749,227 @@ struct CompKey {
 
 __global__ void set_hdr_kernel(DeltaHdr* hdr, DeltaHdr v) { *hdr = v; }
 
+// Merge with deletions: O = merge(S minus the changed objects' entries, B),
+// every output position computed directly (keys are unique, so the order is
+// the full sort's).  S is cut into tiles of kMTile entries; tile t's output
+// starts after the kept entries of the tiles before it (scan of the tile
+// counts) and the B entries below its first key (tb[t], a binary search).
+// Inside a tile every B entry finds its insertion point L among the tile's
+// keys (binary search in shared memory) and bumps a count at L; one block
+// scan over (kept flag, B count) pairs packed in 16-bit halves then places
+// both: a kept entry at i after the kept entries and the B entries inserted
+// at or before i, a B entry after the kept entries below L and the B entries
+// before it.  A tile holding more than kMBCap B entries (movers piled into
+// one region) places its kept entries by binary searches in global B
+// instead.  Keys and values are read once into registers, the changed
+// objects are one bit each (an L1-resident mask where the objects are a few
+// hundred thousand): one read of S's keys for the tile counts, one read of
+// keys + values and one write — where two stable selects and a merge path
+// read and wrote S twice.
+constexpr int kMT = 256, kMPer = 8, kMTile = kMT * kMPer, kMBPer = 4, kMBCap = kMT * kMBPer;
+
+int64_t mdel_tiles(int64_t n) { return (n + kMTile - 1) / kMTile; }
+
+__device__ __forceinline__ bool mdel_kept(const uint32_t* __restrict__ obits,
+                                          unsigned long long k, unsigned long long omask) {
+  const unsigned long long o = k & omask;
+  return !((__ldg(obits + (o >> 5)) >> (o & 31)) & 1u);
+}
+
+__global__ void __launch_bounds__(kMT) mdel_count_kernel(
+    int64_t n, const unsigned long long* __restrict__ key, const uint32_t* __restrict__ obits,
+    unsigned long long omask, int64_t* __restrict__ tcnt) {
+  __shared__ int wsum[kMT / 32];
+  const int64_t t = blockIdx.x, i0 = t * kMTile;
+  const int len = (int)min((int64_t)kMTile, n - i0);
+  unsigned long long kk[kMPer];
+#pragma unroll
+  for (int r = 0; r < kMPer; ++r) {
+    const int i = r * kMT + threadIdx.x;
+    kk[r] = i < len ? __ldcs(key + i0 + i) : 0ull;
+  }
+  int c = 0;
+#pragma unroll
+  for (int r = 0; r < kMPer; ++r)
+    if (r * kMT + (int)threadIdx.x < len) c += mdel_kept(obits, kk[r], omask) ? 1 : 0;
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+#pragma unroll
+    for (int w = 0; w < kMT / 32; ++w) s += wsum[w];
+    tcnt[t] = s;
+    if (t == gridDim.x - 1) tcnt[t + 1] = 0;
+  }
+}
+
+// tb[t] = B entries below tile t's first key (one thread per tile: the
+// binary searches' dependent loads overlap across tiles instead of holding
+// a counting CTA each)
+__global__ void mdel_tb_kernel(int64_t n, int64_t nt, const unsigned long long* __restrict__ key,
+                               const unsigned long long* __restrict__ bkey, int64_t nb,
+                               int64_t* __restrict__ tb) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t > nt) return;
+  int64_t lo = 0;
+  if (t == nt) {
+    lo = nb;
+  } else if (t > 0) {
+    const unsigned long long k0 = key[t * kMTile];
+    int64_t hi = nb;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (bkey[mid] < k0) lo = mid + 1;
+      else hi = mid;
+    }
+  }
+  tb[t] = lo;
+}
+
+__global__ void __launch_bounds__(kMT, 4) mdel_merge_kernel(
+    int64_t n, const unsigned long long* __restrict__ key, const double* __restrict__ val,
+    const uint32_t* __restrict__ obits, unsigned long long omask,
+    const unsigned long long* __restrict__ bkey, const double* __restrict__ bval,
+    const int64_t* __restrict__ tpre, const int64_t* __restrict__ tb,
+    unsigned long long* __restrict__ okey, double* __restrict__ oval) {
+  __shared__ unsigned long long sk[kMTile];
+  // per position: kept flag (low half) + B entries inserted there (high
+  // half), scanned in place to the exclusive prefix; [kMTile] = the totals
+  __shared__ __align__(16) uint32_t sv[kMTile + 1];
+  __shared__ uint32_t wsum[kMT / 32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t t = blockIdx.x, i0 = t * kMTile;
+  const int len = (int)min((int64_t)kMTile, n - i0);
+  const int64_t jb = tb[t], je = tb[t + 1];
+  const int nbt = (int)(je - jb);
+  const bool fits = nbt <= kMBCap;
+  unsigned long long kk[kMPer];
+  double vv[kMPer];
+#pragma unroll
+  for (int r = 0; r < kMPer; ++r) {
+    const int i = r * kMT + tid;
+    kk[r] = i < len ? __ldcs(key + i0 + i) : ~0ull;
+    vv[r] = i < len ? __ldcs(val + i0 + i) : 0.0;
+  }
+  unsigned long long bk[kMBPer];
+  if (fits) {
+#pragma unroll
+    for (int r = 0; r < kMBPer; ++r) {
+      const int j = r * kMT + tid;
+      bk[r] = j < nbt ? __ldcs(bkey + jb + j) : 0ull;
+    }
+  }
+  unsigned kept = 0;
+#pragma unroll
+  for (int r = 0; r < kMPer; ++r) {
+    const int i = r * kMT + tid;
+    const bool f = i < len && mdel_kept(obits, kk[r], omask);
+    kept |= (f ? 1u : 0u) << r;
+    sk[i] = kk[r];
+    sv[i] = f ? 1u : 0u;
+  }
+  __syncthreads();
+  int bl[kMBPer];
+  if (fits) {
+#pragma unroll
+    for (int r = 0; r < kMBPer; ++r) {
+      const int j = r * kMT + tid;
+      int lo = 0;
+      if (j < nbt) {
+        int hi = len;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (sk[mid] < bk[r]) lo = mid + 1;
+          else hi = mid;
+        }
+        if (lo < kMTile) atomicAdd(&sv[lo], 1u << 16);
+      }
+      bl[r] = lo;
+    }
+    __syncthreads();
+  }
+  // blocked exclusive scan: thread tid owns [tid*kMPer, tid*kMPer + kMPer)
+  uint4 a = *reinterpret_cast<const uint4*>(sv + tid * kMPer);
+  uint4 b = *reinterpret_cast<const uint4*>(sv + tid * kMPer + 4);
+  uint32_t e[kMPer] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  uint32_t c = 0;
+#pragma unroll
+  for (int q = 0; q < kMPer; ++q) c += e[q];
+  uint32_t inc = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) wsum[wid] = inc;
+  __syncthreads();
+  uint32_t run = 0, total = 0;
+#pragma unroll
+  for (int w = 0; w < kMT / 32; ++w) {
+    run += w < wid ? wsum[w] : 0u;
+    total += wsum[w];
+  }
+  run += inc - c;
+#pragma unroll
+  for (int q = 0; q < kMPer; ++q) {
+    const uint32_t x = e[q];
+    e[q] = run;
+    run += x;
+  }
+  *reinterpret_cast<uint4*>(sv + tid * kMPer) = make_uint4(e[0], e[1], e[2], e[3]);
+  *reinterpret_cast<uint4*>(sv + tid * kMPer + 4) = make_uint4(e[4], e[5], e[6], e[7]);
+  if (tid == 0) sv[kMTile] = total;
+  __syncthreads();
+  const int64_t base = tpre[t];
+  // kept entries (striped: near-contiguous writes)
+#pragma unroll
+  for (int r = 0; r < kMPer; ++r) {
+    if (!((kept >> r) & 1u)) continue;
+    const int i = r * kMT + tid;
+    int64_t nbelow;  // this tile's B entries below the key
+    if (fits) {
+      nbelow = (int64_t)(sv[i + 1] >> 16);  // inserted at positions <= i
+    } else {
+      int64_t lo = 0, hi = nbt;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (bkey[jb + mid] < kk[r]) lo = mid + 1;
+        else hi = mid;
+      }
+      nbelow = lo;
+    }
+    const int64_t pos = base + jb + (int64_t)(sv[i] & 0xffffu) + nbelow;
+    __stcs(okey + pos, kk[r]);
+    __stcs(oval + pos, vv[r]);
+  }
+  // this tile's B entries
+  if (fits) {
+#pragma unroll
+    for (int r = 0; r < kMBPer; ++r) {
+      const int j = r * kMT + tid;
+      if (j < nbt) {
+        const int64_t pos = base + (int64_t)(sv[bl[r]] & 0xffffu) + jb + j;
+        __stcs(okey + pos, bk[r]);
+        __stcs(oval + pos, __ldcs(bval + jb + j));
+      }
+    }
+  } else {
+    for (int j = tid; j < nbt; j += kMT) {
+      const unsigned long long k = bkey[jb + j];
+      int lo = 0, hi = len;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (sk[mid] < k) lo = mid + 1;
+        else hi = mid;
+      }
+      const int64_t pos = base + (int64_t)(sv[lo] & 0xffffu) + jb + j;
+      okey[pos] = k;
+      oval[pos] = bval[jb + j];
+    }
+  }
+}
+
 // Sorted (key, value) for this update: the composite-key state S brought up to
 // the current labels (incrementally when few objects moved); returns the S
 // buffers through *sk / *sv.
@@ -746,7 +986,7 @@ int delta_sort(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms, cons
   unsigned long long cnt[2] = {0, 0};
   IVFKM_TRY(cudaMemsetAsync(d.counts, 0, sizeof(unsigned long long) * 4, st));
   changed_kernel<<<grid_for(n_obj, T), T, 0, st>>>(n_obj, labels, d.labels, row_ptr, d.oflag,
-                                                  d.cptr, d.counts);
+                                                  d.obits, d.cptr, d.counts);
   IVFKM_CHECK_LAUNCH();
   IVFKM_TRY(cudaMemcpyAsync(&h, d.hdr, sizeof(h), cudaMemcpyDeviceToHost, st));
   IVFKM_TRY(cudaMemcpyAsync(cnt, d.counts, sizeof(cnt), cudaMemcpyDeviceToHost, st));
@@ -774,18 +1014,7 @@ int delta_sort(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms, cons
   } else if (cnt[1] > 0) {
     const int oth = cur ^ 1;
     const int64_t nb = (int64_t)cnt[1], nc = (int64_t)cnt[0];
-    // A: the unchanged objects' entries, in order (the kept flags computed
-    // from the keys inside both selects: no flag pass)
     size_t cb = d.cub_bytes;
-    {
-      auto kept = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0),
-                                                  KeptFlag{d.key[cur], d.oflag, bt.omask});
-      IVFKM_TRY(cub::DeviceSelect::Flagged(d.cub, cb, d.key[cur], kept, d.key[oth],
-                                           d.counts + 2, (int)nnz, st));
-      cb = d.cub_bytes;
-      IVFKM_TRY(cub::DeviceSelect::Flagged(d.cub, cb, d.val[cur], kept, d.val[oth],
-                                           d.counts + 2, (int)nnz, st));
-    }
     // B: the changed objects' entries under their new labels, sorted
     {
       // list the changed objects (ascending ids)
@@ -809,11 +1038,38 @@ int delta_sort(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms, cons
     // movers listed in ascending object order: (label, term) bits only, as above
     IVFKM_TRY(cub::DeviceRadixSort::SortPairs(d.cub, cb, kb, vb, (int)nb, bt.ob, total_bits,
                                               st));
-    // merge A (oth) and B into cur (keys are unique: no ties to order)
-    cb = d.cub_bytes;
-    IVFKM_TRY(cub::DeviceMerge::MergePairs(d.cub, cb, d.key[oth], d.val[oth], (int)(nnz - nb),
-                                           kb.Current(), vb.Current(), (int)nb, d.key[cur],
-                                           d.val[cur], ::cuda::std::less<>{}, st));
+    if (g_delta_cub_merge) {
+      // A: the unchanged objects' entries, in order (the kept flags computed
+      // from the keys inside both selects: no flag pass); merge A (oth) and
+      // B into cur (keys are unique: no ties to order)
+      auto kept = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0),
+                                                  KeptFlag{d.key[cur], d.oflag, bt.omask});
+      cb = d.cub_bytes;
+      IVFKM_TRY(cub::DeviceSelect::Flagged(d.cub, cb, d.key[cur], kept, d.key[oth],
+                                           d.counts + 2, (int)nnz, st));
+      cb = d.cub_bytes;
+      IVFKM_TRY(cub::DeviceSelect::Flagged(d.cub, cb, d.val[cur], kept, d.val[oth],
+                                           d.counts + 2, (int)nnz, st));
+      cb = d.cub_bytes;
+      IVFKM_TRY(cub::DeviceMerge::MergePairs(d.cub, cb, d.key[oth], d.val[oth], (int)(nnz - nb),
+                                             kb.Current(), vb.Current(), (int)nb, d.key[cur],
+                                             d.val[cur], ::cuda::std::less<>{}, st));
+    } else {
+      // one fused merge with deletions, S (cur) -> oth
+      const int64_t nt = mdel_tiles(nnz);
+      mdel_tb_kernel<<<grid_for(nt + 1, T), T, 0, st>>>(nnz, nt, d.key[cur], kb.Current(), nb,
+                                                         d.tb);
+      IVFKM_CHECK_LAUNCH();
+      mdel_count_kernel<<<(unsigned)nt, kMT, 0, st>>>(nnz, d.key[cur], d.obits, bt.omask, d.tcnt);
+      IVFKM_CHECK_LAUNCH();
+      cb = d.cub_bytes;
+      IVFKM_TRY(cub::DeviceScan::ExclusiveSum(d.cub, cb, d.tcnt, d.tcnt, (int)nt + 1, st));
+      mdel_merge_kernel<<<(unsigned)nt, kMT, 0, st>>>(nnz, d.key[cur], d.val[cur], d.obits,
+                                                      bt.omask, kb.Current(), vb.Current(),
+                                                      d.tcnt, d.tb, d.key[oth], d.val[oth]);
+      IVFKM_CHECK_LAUNCH();
+      cur = oth;
+    }
     *moved = nb;
   } else {
     *moved = 0;
@@ -1043,6 +1299,13 @@ extern "C" int ivfkm_update_count(int64_t n_obj, int64_t nnz, const int64_t* row
                                        prev_ptr, new_ptr, ws, ws_bytes, nullptr, st);
   return update_count_impl<unsigned long long>(n_obj, row_ptr, terms, val64, nnz, k, dim, labels,
                                                sizes, prev_ptr, new_ptr, ws, ws_bytes, nullptr, st);
+}
+
+extern "C" int ivfkm_set_update_option(int which, int value) {
+  switch (which) {
+    case 1: g_delta_cub_merge = value ? 1 : 0; return IVFKM_OK;
+    default: return IVFKM_E_ARG;
+  }
 }
 
 extern "C" size_t ivfkm_update_state_size(int64_t n_obj, int64_t nnz, int64_t k, int64_t dim) {

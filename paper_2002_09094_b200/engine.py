@@ -18,7 +18,9 @@ stream only; all compute on the path is in libivfkm.so.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import warnings
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
 import numpy as np
@@ -125,10 +127,31 @@ class HostDataset:
         return sum(t.numel() * t.element_size() for t in self._arrays())
 
 
+# host threads that fill / drain the pinned staging buffers (one thread's
+# memcpy runs at a fraction of the PCIe bandwidth); numpy copies release the GIL
+UPLOAD_THREADS = max(1, min(8, os.cpu_count() or 1))
+_POOL: ThreadPoolExecutor | None = None
+
+
+def _pcopy(dst: np.ndarray, src: np.ndarray) -> None:
+    """dst[:] = src over UPLOAD_THREADS host threads (1-D byte views)."""
+    global _POOL
+    n, th = dst.size, UPLOAD_THREADS
+    if th <= 1 or n < (4 << 20):
+        dst[:] = src
+        return
+    if _POOL is None or _POOL._max_workers < th:
+        _POOL = ThreadPoolExecutor(max(th, 8))
+    step = -(-n // th)
+    futs = [_POOL.submit(np.copyto, dst[i:i + step], src[i:i + step]) for i in range(0, n, step)]
+    for f in futs:
+        f.result()
+
+
 def _upload(a: np.ndarray, dev, chunk: int = 64 << 20) -> torch.Tensor:
     """Host array -> device through two pinned staging buffers (chunked,
-    asynchronous, double-buffered): pageable copies run at a fraction of the
-    PCIe bandwidth."""
+    asynchronous, double-buffered, each stage filled by several host
+    threads): pageable copies run at a fraction of the PCIe bandwidth."""
     a = np.ascontiguousarray(a)
     with warnings.catch_warnings():  # read-only reference arrays: only read here
         warnings.simplefilter("ignore", UserWarning)
@@ -149,11 +172,38 @@ def _upload(a: np.ndarray, dev, chunk: int = 64 << 20) -> torch.Tensor:
         if done[b] is not None:
             done[b].synchronize()  # the copy out of this staging buffer has finished
         n = min(chunk, nbytes - off)
-        stage[b][:n].numpy()[:] = src[off:off + n]
+        _pcopy(stage[b][:n].numpy(), src[off:off + n])
         dst[off:off + n].copy_(stage[b][:n], non_blocking=True)
         done[b] = torch.cuda.Event()
         done[b].record(st)
     st.synchronize()
+    return out
+
+
+def _download(t: torch.Tensor, chunk: int = 64 << 20) -> np.ndarray:
+    """Device tensor -> new host array through two pinned staging buffers:
+    the copy of chunk i+1 runs while host threads drain chunk i."""
+    t = t.contiguous().reshape(-1)
+    if t.numel() * t.element_size() <= chunk or not t.is_cuda:
+        return t.cpu().numpy()
+    out = np.empty(t.numel(), dtype=torch.empty(0, dtype=t.dtype).numpy().dtype)
+    nbytes = out.nbytes
+    src = t.view(torch.uint8)
+    dst = out.view(np.uint8)
+    stage = [torch.empty(chunk, dtype=torch.uint8).pin_memory() for _ in range(2)]
+    st = torch.cuda.current_stream()
+    pending = []
+    for i, off in enumerate(range(0, nbytes + chunk, chunk)):
+        if off < nbytes:
+            n = min(chunk, nbytes - off)
+            stage[i & 1][:n].copy_(src[off:off + n], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(st)
+            pending.append((i & 1, off, n, ev))
+        if pending and (len(pending) == 2 or off >= nbytes):
+            b, o, n, ev = pending.pop(0)
+            ev.synchronize()
+            _pcopy(dst[o:o + n], stage[b][:n].numpy())
     return out
 
 
@@ -250,8 +300,9 @@ class DeviceMeans:
 
     def to_meanset(self, representation: str = "sparse_inverted", validate: bool = True) -> MeanSet:
         ptr = self.ptr.cpu().numpy()
-        terms = (self.terms + 1).cpu().numpy()
-        vals = self.vals.cpu().numpy()
+        terms = _download(self.terms)
+        terms += 1
+        vals = _download(self.vals)
         ret = self.retained.cpu().numpy().astype(bool)
         if not validate:
             return MeanSet.trusted(self.k, self.dim, representation, ptr, terms, vals, ret)

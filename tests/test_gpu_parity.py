@@ -430,25 +430,44 @@ def test_update_matches_oracle_bitwise_with_empty_clusters():
     assert np.array_equal(up.retained, ref.retained) and up.retained[40:].all()
 
 
-def test_update_label_delta_sort_matches_oracle_bitwise():
+@pytest.mark.parametrize("cub_merge", [0, 1])
+def test_update_label_delta_sort_matches_oracle_bitwise(cub_merge):
     """The engine's label-delta update sort (kept entries + merged movers,
     full re-sort past a quarter of the entries, nothing moved, a label set
-    with empty clusters) against the oracle on every step, and against the
-    stateless sort."""
+    with empty clusters, movers piled into one cluster — one merge tile's
+    movers beyond its shared-memory stage) against the oracle on every step,
+    and against the stateless sort; with the fused merge with deletions
+    (default) and with the CUB selects + merge."""
     from oracle import oracle as O
-    from paper_2002_09094_b200.engine import DeviceMeans, update_rows
+    from paper_2002_09094_b200 import _lib
     from paper_2002_09094_b200.variants import engine_for
 
     P = _pkg()
     ds, om, means = _random_case(seed=12, k=60, n=2500)
     rng = np.random.default_rng(12)
     labels = rng.integers(1, 61, size=ds.n).astype(np.int32)
-    steps = [0.0, 0.02, 0.0, 0.001, 0.6, 0.05, 0.3, 0.01, 1.0]
+    steps = [0.0, 0.02, 0.0, 0.001, 0.6, 0.05, 0.3, 0.01, 0.15, 0.004, 1.0]
     eng = engine_for(ds, 60)
     assert eng.upd_state is not None
+    lib = _lib.load()
+    _lib.check(lib.ivfkm_set_update_option(1, cub_merge), "ivfkm_set_update_option")
+    try:
+        _delta_steps(P, O, ds, om, means, rng, labels, steps)
+    finally:
+        lib.ivfkm_set_update_option(1, 0)
+
+
+def _delta_steps(P, O, ds, om, means, rng, labels, steps):
+    from paper_2002_09094_b200.engine import DeviceMeans, update_rows
+    from paper_2002_09094_b200.variants import engine_for
+
+    eng = engine_for(ds, 60)
     for i, frac in enumerate(steps):
         moved = rng.random(ds.n) < frac
-        labels = np.where(moved, rng.integers(1, 61, size=ds.n), labels).astype(np.int32)
+        if i == 8:  # movers piled into cluster 2
+            labels = np.where(moved, 2, labels).astype(np.int32)
+        else:
+            labels = np.where(moved, rng.integers(1, 61, size=ds.n), labels).astype(np.int32)
         if i == 5:
             labels = np.where(labels > 50, 1 + labels % 7, labels).astype(np.int32)
         asg = P.Assignment.from_labels(labels, 60)

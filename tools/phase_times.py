@@ -20,7 +20,12 @@ def main():
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--update-option", type=int, nargs=2, action="append", default=[],
+                    metavar=("WHICH", "VALUE"), help="ivfkm_set_update_option before the run")
     a = ap.parse_args()
+    from paper_2002_09094_b200 import _lib
+    for w, v in a.update_option:
+        _lib.check(_lib.load().ivfkm_set_update_option(w, v), "ivfkm_set_update_option")
     c = synth.CONFIGS[a.config]
     ds = synth.make_dataset(c["corpus"])
     eng = E.LloydEngine(E.DeviceDataset(E.HostDataset(ds), "cuda"), c["k"])
@@ -65,7 +70,8 @@ def main():
         rows.append(r)
         prev = lab
     avg = {k: sum(r[k] for r in rows) / len(rows) for k in rows[0]}
-    print(json.dumps({"config": a.config, "ms": avg}), flush=True)
+    print(json.dumps({"config": a.config, "update_option": a.update_option, "ms": avg}),
+          flush=True)
 
 
 if __name__ == "__main__":
