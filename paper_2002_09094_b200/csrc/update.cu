@@ -223,33 +223,79 @@ __global__ void head_kernel(int64_t nnz, R key, uint32_t* __restrict__ head) {
 // longer than kLongRun (the hot terms: hundreds of members each) go to a
 // list summed a warp per run (segsum_long_kernel), so no thread walks a
 // long run four loads at a time (split measured best at 64 of 28-128).
+// The same pass writes the run tables the norm reads: the first run of
+// every cluster (cl_seg) and of every (cluster, leaf group) (gstart) — at
+// the runs where the cluster or the group changes, groups and clusters
+// holding no run pointing at the next run.
 constexpr uint32_t kLongRun = 64;
 
+__device__ __forceinline__ int group_of(int64_t pos, const int32_t* glo, int ng);
+
 template <class K>
-__global__ void segsum_kernel(int64_t n_seg, const uint32_t* __restrict__ seg_start,
-                              const K* __restrict__ seg_key, const double* __restrict__ sval,
-                              const unsigned long long* __restrict__ sizes, int64_t dim,
-                              double* __restrict__ seg_w, uint32_t* __restrict__ nz,
-                              uint32_t* __restrict__ long_list, uint32_t* __restrict__ n_long) {
+__global__ void __launch_bounds__(256) segsum_kernel(
+    int64_t n_seg, const uint32_t* __restrict__ seg_start, const K* __restrict__ seg_key,
+    const double* __restrict__ sval, const unsigned long long* __restrict__ sizes, int64_t k,
+    int64_t dim, const int32_t* __restrict__ plan, int64_t nleaf, double* __restrict__ seg_w,
+    uint32_t* __restrict__ nz, uint32_t* __restrict__ long_list, uint32_t* __restrict__ n_long,
+    uint32_t* __restrict__ cl_seg, uint32_t* __restrict__ gstart) {
+  // glo[ng]: group start positions; tab[pos >> 8]: the group holding the
+  // bucket's first position (a group spans >= 256 positions when D > 128, so
+  // at most two more starts fall in one bucket)
+  extern __shared__ int32_t glo[];
+  const int ng = (int)((nleaf + kLeafG - 1) / kLeafG);
+  const int nb = (int)(dim >> 8) + 1;
+  int32_t* tab = glo + ng;
+  for (int g = threadIdx.x; g < ng; g += blockDim.x) glo[g] = plan[(int64_t)g * kLeafG];
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) tab[b] = group_of((int64_t)b << 8, glo, ng);
+  __syncthreads();
+  auto gof = [&](int64_t pos) {
+    int g = tab[pos >> 8];
+    while (g + 1 < ng && glo[g + 1] <= pos) ++g;
+    return g;
+  };
+  const int64_t stride = ng + 1;
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s <= n_seg;
        s += (int64_t)gridDim.x * blockDim.x) {
     if (s == n_seg) {
       nz[s] = 0u;
       continue;
     }
-    double acc = 0.0;
     uint32_t e = seg_start[s];
     const uint32_t end = seg_start[s + 1];
+    const K key = seg_key[s];
+    const int64_t c = (int64_t)(key / (K)dim);
+    // run tables
+    {
+      const int g = gof((int64_t)(key - (K)c * (K)dim));
+      uint32_t* gs = gstart + c * stride;
+      int from = 0;
+      int64_t pc = -1;
+      if (s > 0) {
+        const K pk = seg_key[s - 1];
+        pc = (int64_t)(pk / (K)dim);
+        if (pc == c) from = gof((int64_t)(pk - (K)pc * (K)dim)) + 1;
+      }
+      for (int q = from; q <= g; ++q) gs[q] = (uint32_t)s;
+      for (int64_t q = pc + 1; q <= c; ++q) cl_seg[q] = (uint32_t)s;
+      int64_t nc = k;  // the next run's cluster
+      if (s + 1 < n_seg) nc = (int64_t)(seg_key[s + 1] / (K)dim);
+      if (nc != c) {
+        for (int q = g + 1; q <= ng; ++q) gs[q] = (uint32_t)(s + 1);
+        if (s + 1 == n_seg)
+          for (int64_t q = c + 1; q <= k; ++q) cl_seg[q] = (uint32_t)n_seg;
+      }
+    }
     if (end - e > kLongRun) {
       long_list[atomicAdd(n_long, 1u)] = (uint32_t)s;
       continue;
     }
+    double acc = 0.0;
     for (; e + 4 <= end; e += 4) {  // four loads in flight, adds in order
       const double a = sval[e], b = sval[e + 1], c2 = sval[e + 2], d = sval[e + 3];
       acc = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(acc, a), b), c2), d);
     }
     for (; e < end; ++e) acc = __dadd_rn(acc, sval[e]);
-    const int64_t c = (int64_t)(seg_key[s] / (K)dim);
     const double w = __ddiv_rn(acc, (double)sizes[c]);
     seg_w[s] = w;
     nz[s] = (w != 0.0) ? 1u : 0u;
@@ -361,54 +407,6 @@ __global__ void segstart_kernel(int64_t nnz, R key, const uint32_t* __restrict__
       *n_seg = ns;
       seg_start[ns] = (uint32_t)nnz;
     }
-  }
-}
-
-// First run of every (cluster, leaf group), one thread per run: groups
-// after the previous run's group (same cluster; else from 0) up to this
-// run's start here, and a cluster's last run closes its remaining groups.
-// Groups holding no run thus point at the next run.  (A separate pass: done
-// at the run heads inside segstart it diverges and costs more.)
-template <class K>
-__global__ void __launch_bounds__(256) gstart_kernel(const uint32_t* __restrict__ n_seg_p,
-                                                     const K* __restrict__ seg_key, int64_t dim,
-                                                     const int32_t* __restrict__ plan,
-                                                     int64_t nleaf, uint32_t* __restrict__ gstart) {
-  // glo[ng]: group start positions; tab[pos >> 8]: the group holding the
-  // bucket's first position (a group spans >= 256 positions when D > 128, so
-  // at most two more starts fall in one bucket)
-  extern __shared__ int32_t glo[];
-  const int ng = (int)((nleaf + kLeafG - 1) / kLeafG);
-  const int nb = (int)(dim >> 8) + 1;
-  int32_t* tab = glo + ng;
-  for (int g = threadIdx.x; g < ng; g += blockDim.x) glo[g] = plan[(int64_t)g * kLeafG];
-  __syncthreads();
-  for (int b = threadIdx.x; b < nb; b += blockDim.x) tab[b] = group_of((int64_t)b << 8, glo, ng);
-  __syncthreads();
-  auto gof = [&](int64_t pos) {
-    int g = tab[pos >> 8];
-    while (g + 1 < ng && glo[g + 1] <= pos) ++g;
-    return g;
-  };
-  const int64_t n_seg = *n_seg_p;
-  const int64_t stride = ng + 1;
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_seg;
-       s += (int64_t)gridDim.x * blockDim.x) {
-    const K key = seg_key[s];
-    const int64_t c = (int64_t)(key / (K)dim);
-    const int g = gof((int64_t)(key - (K)c * (K)dim));
-    uint32_t* gs = gstart + c * stride;
-    int from = 0;
-    if (s > 0) {
-      const K pk = seg_key[s - 1];
-      const int64_t pc = (int64_t)(pk / (K)dim);
-      if (pc == c) from = gof((int64_t)(pk - (K)pc * (K)dim)) + 1;
-    }
-    for (int q = from; q <= g; ++q) gs[q] = (uint32_t)s;
-    bool last = s + 1 == n_seg;
-    if (!last) last = (int64_t)(seg_key[s + 1] / (K)dim) != c;
-    if (last)
-      for (int q = g + 1; q <= ng; ++q) gs[q] = (uint32_t)(s + 1);
   }
 }
 
@@ -1164,10 +1162,6 @@ int runs_impl(int64_t nnz, R rd, const UpdWs<K>& w, int64_t dim, int64_t nleaf,
       IVFKM_CHECK_LAUNCH();
     }
   }
-  const int ng = (int)((nleaf + kLeafG - 1) / kLeafG);
-  gstart_kernel<K><<<grid_for(nnz / 4 + 1, T), T, (size_t)(ng + (dim >> 8) + 1) * 4, st>>>(
-      w.n_seg, w.seg_key, dim, plan, nleaf, w.gstart);
-  IVFKM_CHECK_LAUNCH();
   return IVFKM_OK;
 }
 
@@ -1226,9 +1220,13 @@ int update_count_impl(int64_t n_obj, const int64_t* row_ptr, const int32_t* term
     IVFKM_TRY(cudaStreamSynchronize(st));
     IVFKM_TRY(cudaMemsetAsync(w.n_seg + 1, 0, sizeof(uint32_t), st));
     // segpos is free again: it holds the long-run list
-    segsum_kernel<K><<<grid_for((int64_t)n_seg + 1, T), T, 0, st>>>(
-        n_seg, w.seg_start, w.seg_key, sval, sizes, dim, w.seg_w, w.head, w.segpos, w.n_seg + 1);
-    IVFKM_CHECK_LAUNCH();
+    {
+      const int ng = (int)((nleaf + kLeafG - 1) / kLeafG);
+      segsum_kernel<K><<<grid_for((int64_t)n_seg + 1, T), T, (size_t)(ng + (dim >> 8) + 1) * 4,
+                         st>>>(n_seg, w.seg_start, w.seg_key, sval, sizes, k, dim, plan, nleaf,
+                               w.seg_w, w.head, w.segpos, w.n_seg + 1, w.cl_seg, w.gstart);
+      IVFKM_CHECK_LAUNCH();
+    }
     segsum_long_kernel<K><<<num_sms() * 8, 256, 0, st>>>(w.seg_start, w.seg_key, sval, sizes, dim,
                                                       w.seg_w, w.head, w.segpos, w.n_seg + 1);
     IVFKM_CHECK_LAUNCH();
@@ -1236,9 +1234,9 @@ int update_count_impl(int64_t n_obj, const int64_t* row_ptr, const int32_t* term
     IVFKM_TRY(cub::DeviceScan::ExclusiveSum(w.cub, cb, w.head, w.nzpos, (int)n_seg + 1, st));
   } else {
     IVFKM_TRY(cudaMemsetAsync(w.n_seg, 0, sizeof(uint32_t), st));
+    clseg_kernel<K><<<grid_for(k + 1, T), T, 0, st>>>(k, dim, w.n_seg, w.seg_key, w.cl_seg);
+    IVFKM_CHECK_LAUNCH();
   }
-  clseg_kernel<K><<<grid_for(k + 1, T), T, 0, st>>>(k, dim, w.n_seg, w.seg_key, w.cl_seg);
-  IVFKM_CHECK_LAUNCH();
   IVFKM_TRY(cudaFuncSetAttribute(norm_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)nsmem));
   norm_kernel<K><<<(int)std::min<int64_t>(k, num_sms() * 4), kNormWarps * 32, nsmem, st>>>(
