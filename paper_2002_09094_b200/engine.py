@@ -309,22 +309,29 @@ class DeviceMeans:
         return MeanSet(self.k, self.dim, representation, ptr, terms, vals, ret)
 
 
+# kernels every update launches after its sort: the run scan (init + sweep),
+# run sums (+ the cluster and leaf-group run tables), long runs, the nonzero
+# scan (2), norm, the counts scan (2), fill, retain
+_UPDATE_COMMON = 11
+
+
 def update_launches(k: int, dim: int) -> int:
-    """Kernels one update launches: keys, CUB onesweep radix sort (histogram,
-    exclusive sum, one pass per 8 key bits), 3 CUB scans (init + sweep each;
-    the first also finds the runs), group starts, segsum (short + long runs),
-    clseg, norm, fill, retain."""
+    """Kernels one stateless update launches: keys, CUB onesweep radix sort
+    (histogram, exclusive sum, one pass per 8 key bits), then the common
+    kernels."""
     bits = max(1, int(np.ceil(np.log2(max(2.0, float(k) * float(dim))))))
-    return 16 + (bits + 7) // 8
+    return 3 + (bits + 7) // 8 + _UPDATE_COMMON
+
 
 def delta_update_launches(k: int, dim: int) -> int:
-    """Kernels of the label-delta sort (changed, 3 CUB selects — the kept
-    keys and values with their flags computed from the keys, the movers —
-    lengths, scan, keys, the movers' radix sort over the (label, term) bits:
-    histogram, exclusive sum, a pass per 8 bits — merge (2), header), in
-    place of keys + the full sort."""
+    """Kernels of an update through the label-delta sort when few objects
+    moved: changed flags, the movers' list (CUB select: 2), their lengths and
+    offsets (scan: 2), their keys, their radix sort over the (label, term)
+    bits (histogram, exclusive sum, a pass per 8 bits), the merge with
+    deletions (tile searches, tile counts, their scan (2), merge), header;
+    then the common kernels."""
     bits = int(np.ceil(np.log2(max(2, k)))) + int(np.ceil(np.log2(max(2, dim))))
-    return 16 + (bits + 7) // 8
+    return 15 + (bits + 7) // 8 + _UPDATE_COMMON
 
 
 def update_rows(lib, n_obj, nnz, row_ptr, terms, val64, labels0, sizes, prev: DeviceMeans, k,
@@ -678,11 +685,8 @@ class LloydEngine:
         out = update_rows(self.lib, dd.n, dd.nnz, dd.row_ptr, dd.terms, dd.val64, labels0,
                           self.sizes, dm, self.k, dd.dim, self.ws_update, self.total_host,
                           self.upd_state, deferred=self._defer_ok(dm))
-        self.launches += update_launches(self.k, dd.dim)
-        if self.upd_state is not None:
-            # minus keys + the full sort (histogram, exclusive sum, passes)
-            self.launches += (delta_update_launches(self.k, dd.dim)
-                              - (update_launches(self.k, dd.dim) - 13))
+        self.launches += (delta_update_launches(self.k, dd.dim) if self.upd_state is not None
+                          else update_launches(self.k, dd.dim))
         return self.build_bivf(out)
 
     def _defer_ok(self, dm: DeviceMeans) -> bool:
