@@ -229,7 +229,9 @@ int ivfkm_assign_finish(int64_t n_obj, const int64_t* row_ptr, const int32_t* te
  * bits per 32-term word + the rank of the word's first term in the mean's
  * row) and rescores the objects grouped by their screen winner, so that
  * concurrently resident warps read a few means' contiguous values.  Same
- * results bit for bit.                                                      */
+ * results bit for bit.  m_terms == NULL: dir already holds these means'
+ * directory (ivfkm_rankdir_build — the directory depends on the means only,
+ * so it can be built on another stream while the screen runs).              */
 int ivfkm_assign_finish_dir(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
                             const double* val64, int64_t k, int64_t dim, const uint32_t* headers,
                             const double* pval64, const int64_t* m_ptr, const int32_t* m_terms,
@@ -237,6 +239,12 @@ int ivfkm_assign_finish_dir(int64_t n_obj, const int64_t* row_ptr, const int32_t
                             const int32_t* prev_labels, int32_t* labels, double* sims,
                             unsigned long long* sizes, ivfkm_stats* stats, int label_rule,
                             void* ws, size_t ws_bytes, ivfkm_stream_t stream);
+
+/* The rank directory ivfkm_assign_finish_dir rescoring reads, alone: dir
+ * (k * ceil(dim/32) * 8 bytes) from the means' CSR structure (m_ptr[k+1],
+ * 0-based m_terms ascending per mean; entries past m_ptr[k] are not read).  */
+int ivfkm_rankdir_build(int64_t k, int64_t dim, const int64_t* m_ptr, const int32_t* m_terms,
+                        void* dir /*[dev]*/, ivfkm_stream_t stream);
 
 /* Exact float64 similarity of every object to the mean its (0-based) label
  * names — the summand of objective_cosine (clustering.py:105-119) — written

@@ -1868,6 +1868,19 @@ int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
   }
 }
 
+// Rank directory of the means' mean-major CSR (ivfkm.h, ivfkm_assign_finish_dir).
+int rankdir_build(int64_t k, int64_t dim, const int64_t* m_ptr, const int32_t* m_terms, uint2* dir,
+                  cudaStream_t st) {
+  const int T = 256;
+  const int64_t nw = (dim + 31) / 32;
+  IVFKM_TRY(cudaMemsetAsync(dir, 0, sizeof(uint2) * k * nw, st));
+  rankdir_bits_kernel<<<num_sms() * 8, T, 0, st>>>(k, nw, m_ptr, m_terms, dir);
+  IVFKM_CHECK_LAUNCH();
+  rankdir_scan_kernel<<<grid_for(k, T / 32), T, 0, st>>>(k, nw, dir);
+  IVFKM_CHECK_LAUNCH();
+  return IVFKM_OK;
+}
+
 int finish_impl(const AssignArgs& a, const AssignWs& w, const int32_t* prev_labels,
                 int32_t* labels, double* sims, unsigned long long* sizes, int rule,
                 cudaStream_t st, const int64_t* m_ptr = nullptr, const int32_t* m_terms = nullptr,
@@ -1876,11 +1889,11 @@ int finish_impl(const AssignArgs& a, const AssignWs& w, const int32_t* prev_labe
   const int T = 256;
   const int64_t nw = (a.dim + 31) / 32;
   if (dir) {
-    IVFKM_TRY(cudaMemsetAsync(dir, 0, sizeof(uint2) * a.k * nw, st));
-    rankdir_bits_kernel<<<num_sms() * 8, T, 0, st>>>(a.k, nw, m_ptr, m_terms, dir);
-    IVFKM_CHECK_LAUNCH();
-    rankdir_scan_kernel<<<grid_for(a.k, T / 32), T, 0, st>>>(a.k, nw, dir);
-    IVFKM_CHECK_LAUNCH();
+    // m_terms == nullptr: the caller built the directory for these means
+    // already (ivfkm_rankdir_build, e.g. on another stream during the screen)
+    if (m_terms) {
+      if (int rc = rankdir_build(a.k, a.dim, m_ptr, m_terms, dir, st)) return rc;
+    }
     IVFKM_TRY(cudaMemsetAsync(w.cl_pos, 0, sizeof(unsigned int) * (a.k + 1), st));
     winner_hist_kernel<<<grid_for(a.n_obj, T), T, 0, st>>>(a.n_obj, w.label32, w.cl_pos);
     IVFKM_CHECK_LAUNCH();
@@ -2002,7 +2015,7 @@ extern "C" int ivfkm_assign_finish_dir(int64_t n_obj, const int64_t* row_ptr,
                                        size_t ws_bytes, ivfkm_stream_t stream_) {
   if (n_obj < 0 || k < 1 || dim < 1 || !row_ptr || !labels || !sims || !stats || !headers)
     return IVFKM_E_ARG;
-  if (!m_ptr || !m_terms || !m_vals || !dir) return IVFKM_E_ARG;
+  if (!m_ptr || !m_vals || !dir) return IVFKM_E_ARG;  // m_terms NULL: dir is prebuilt
   if (label_rule != 0 && label_rule != 1) return IVFKM_E_ARG;
   size_t need = 0;
   AssignWs w = carve_assign(ws, n_obj, k, &need);
@@ -2014,6 +2027,12 @@ extern "C" int ivfkm_assign_finish_dir(int64_t n_obj, const int64_t* row_ptr,
                headers, nullptr, 32,    pval64,  0.0,   stats,   nullptr};
   return finish_impl(a, w, prev_labels, labels, sims, sizes, label_rule, st, m_ptr, m_terms,
                      m_vals, static_cast<uint2*>(dir));
+}
+
+extern "C" int ivfkm_rankdir_build(int64_t k, int64_t dim, const int64_t* m_ptr,
+                                   const int32_t* m_terms, void* dir, ivfkm_stream_t stream_) {
+  if (k < 1 || dim < 1 || !m_ptr || !m_terms || !dir) return IVFKM_E_ARG;
+  return rankdir_build(k, dim, m_ptr, m_terms, static_cast<uint2*>(dir), as_stream(stream_));
 }
 
 extern "C" int ivfkm_assign(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,

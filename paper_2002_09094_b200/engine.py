@@ -287,6 +287,7 @@ class DeviceMeans:
         self.nnz = int(terms.numel())
         self.headers = self.pvs = self.pv64 = None
         self.slot8 = None  # sparse spans' slot bytes (ivfkm_bivf_slots), or None
+        self.dir_ready = None  # event: the engine's rank directory holds these means'
         self.screen_bits = 32  # precision of pvs (the screen's values), set by build_bivf
 
     @classmethod
@@ -408,6 +409,10 @@ class LloydEngine:
         nw = (dim + 31) // 32
         self.rankdir = (torch.empty(self.k * nw * 2, dtype=torch.int32, device=dev)
                         if self.k * nw * 8 <= (512 << 20) else None)
+        # the directory depends on the means only: it is built on a side
+        # stream as soon as the means exist, under the BIVF build and the screen
+        self.side = torch.cuda.Stream(device=dev) if self.rankdir is not None and \
+            torch.cuda.is_available() else None
         # BIVF value arrays, grown on demand and alternated between builds (the
         # means of the previous build keep theirs)
         self._bvbuf = [None, None]
@@ -457,8 +462,29 @@ class LloydEngine:
         return order
 
     # -- means ---------------------------------------------------------------
+    def _rankdir_async(self, dm: DeviceMeans) -> None:
+        """Build the rank directory of dm's CSR (ivfkm_rankdir_build) on the
+        side stream; assign waits for dm.dir_ready before the rescoring.  The
+        one directory buffer is free by then: this runs after the previous
+        means' finalize in the current stream's order."""
+        dm.dir_ready = None
+        if self.side is None or self.rankdir is None:
+            return
+        cur = torch.cuda.current_stream()
+        self.side.wait_stream(cur)
+        with torch.cuda.stream(self.side):
+            _lib.check(self.lib.ivfkm_rankdir_build(self.k, dm.dim, _p(dm.ptr), _p(dm.terms),
+                                                    _p(self.rankdir), _stream()),
+                       "ivfkm_rankdir_build")
+            dm.dir_ready = torch.cuda.Event()
+            dm.dir_ready.record(self.side)
+        dm.ptr.record_stream(self.side)
+        dm.terms.record_stream(self.side)
+        self._dir_of = dm
+
     def build_bivf(self, dm: DeviceMeans) -> DeviceMeans:
         dev = self.device
+        self._rankdir_async(dm)
         dm.headers = torch.empty(int(self.lib.ivfkm_bivf_headers_size(self.k, dm.dim)),
                                  dtype=torch.int32, device=dev)
         # plan (headers; the host learns the exact value counts), then fill —
@@ -589,11 +615,20 @@ class LloydEngine:
         if events is not None:
             events[1].record()
         if self.rankdir is not None:
+            # the directory built on the side stream for these very means, or
+            # (another engine's means, a rebuilt buffer) built here
+            pre = dm.dir_ready is not None and getattr(self, "_dir_of", None) is dm
+            if pre:
+                torch.cuda.current_stream().wait_event(dm.dir_ready)
+            elif self.side is not None:  # the buffer may still be written for other means
+                torch.cuda.current_stream().wait_stream(self.side)
             rc = self.lib.ivfkm_assign_finish_dir(
                 dd.n, _p(dd.row_ptr), _p(dd.terms), _p(dd.val64), self.k, dd.dim,
-                _p(dm.headers), _p(dm.pv64), _p(dm.ptr), _p(dm.terms), _p(dm.vals),
-                _p(self.rankdir), _p(prev), _p(out), _p(self.sims), _p(self.sizes),
+                _p(dm.headers), _p(dm.pv64), _p(dm.ptr), None if pre else _p(dm.terms),
+                _p(dm.vals), _p(self.rankdir), _p(prev), _p(out), _p(self.sims), _p(self.sizes),
                 _p(self.stats), rule, _p(self.ws_assign), self.ws_assign.numel(), st)
+            if not pre:
+                self._dir_of = None  # the buffer now holds dm's directory, unmarked
             _lib.check(rc, "ivfkm_assign_finish_dir")
             self.launches += 6  # directory bits + ranks, winner histogram, scan (2), grouping
         else:
