@@ -155,10 +155,11 @@ void ivfkm_set_tuning(int rowcap, int smem_limit, int rr);
  * computes identical sums. */
 void ivfkm_set_screen_warps(int warps);
 /* ivfkm_assign_screen with caller buffers for slot-range passes
- * (presort_terms int32[nnz], presort_vals fp32[nnz], [dev], or NULL): when
- * the plan runs passes, each row's entries are first sorted by the terms'
- * dense prefix, longest first, into them, so that every pass stages its rows
- * by copying instead of sorting them again.  slot8 (ivfkm_bivf_slots, fp16
+ * (presort_terms int32[2*nnz], presort_vals fp32[2*nnz], [dev], 8-byte
+ * aligned, or NULL): when the plan runs passes, each row's entries are first
+ * sorted by the terms' dense prefix, longest first, into them — per entry
+ * {term, dense prefix} and {dense-run start, value} — so that every pass
+ * stages its rows by copying, with no per-term lookups.  slot8 (ivfkm_bivf_slots, fp16
  * screens): the sparse spans are read through their slot bytes instead of
  * the block masks. */
 int ivfkm_assign_screen_ex(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,

@@ -75,8 +75,11 @@ struct ScreenParams {
   const int32_t* inv;     // [k] slot -> mean
   const int32_t* order;   // [n] processing order of objects, or nullptr
   const uint8_t* slot8 = nullptr;  // sparse spans' slot bytes (ivfkm_bivf_slots), or nullptr
-  const int32_t* ps_t = nullptr;  // rows presorted by dense prefix (ivfkm_presort_rows), or
-  const float* ps_v = nullptr;    // nullptr: the CTA sorts its staged row itself
+  // rows presorted by dense prefix (presort_rows_kernel), per entry {term,
+  // dense prefix} and {dense-run start, fp32 value bits}; or nullptr: the CTA
+  // sorts its staged row itself
+  const int2* ps_t = nullptr;
+  const int2* ps_v = nullptr;
   const float* pv32;  // fp32 screen values, or fp16 ones when half
   int half;
   double mu_max;
@@ -662,15 +665,16 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
       // copy, and bucket b starts where the (non-increasing) buckets drop to b.
       __syncthreads();
       if (threadIdx.x == 0) s_next = 0;
+      // (the entry's dense prefix and run start were looked up once, by the
+      // presort: no dependent gathers between the row's load and its spans)
       for (int j = threadIdx.x; j < cn; j += blockDim.x) {
-        const uint32_t t = (uint32_t)__ldg(p.ps_t + c0 + j);
-        int lp = (int)__ldg(p.dpre + t) - gs0;
+        const int2 td = __ldg(p.ps_t + c0 + j);
+        const int2 bv = __ldg(p.ps_v + c0 + j);
+        int lp = td.y - gs0;
         lp = lp < 0 ? 0 : (lp > nls ? nls : lp);
-        if (z == 0) post += __ldg(p.nc + t);
-        const uint32_t row = t * (uint32_t)nblk;
-        const int v = __float_as_int(__ldg(p.ps_v + c0 + j));
-        const uint32_t base = lp ? (__ldg(offs + row) & ~kDense) : 0u;
-        s_ent[j] = make_int4((int)row, v, (int)base, v);
+        if (z == 0) post += __ldg(p.nc + td.x);
+        const uint32_t row = (uint32_t)td.x * (uint32_t)nblk;
+        s_ent[j] = make_int4((int)row, bv.y, lp ? bv.x : 0, bv.y);
         s_lp[j] = (uint8_t)lp;
       }
       __syncthreads();
@@ -1440,8 +1444,9 @@ __global__ void entry_gather_kernel(int64_t nnz, const int32_t* __restrict__ sid
 constexpr int kPresortBuckets = 256;
 __global__ void __launch_bounds__(256) presort_rows_kernel(
     int64_t n_obj, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ terms,
-    const float* __restrict__ val32, const uint32_t* __restrict__ dpre, int nsp,
-    int32_t* __restrict__ ps_t, float* __restrict__ ps_v) {
+    const float* __restrict__ val32, const uint32_t* __restrict__ dpre,
+    const uint32_t* __restrict__ offs, uint32_t nblk, int nsp, int2* __restrict__ ps_t,
+    int2* __restrict__ ps_v) {
   __shared__ int s_cnt[8][kPresortBuckets];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
@@ -1481,16 +1486,19 @@ __global__ void __launch_bounds__(256) presort_rows_kernel(
       const int64_t h = h0 + lane;
       int key = -1;
       int32_t t = 0;
+      int d = 0;
       if (h < re) {
         t = terms[h];
-        const int d = (int)__ldg(dpre + t);
+        d = (int)__ldg(dpre + t);
         key = nsp - (d < nsp ? d : nsp);
       }
       const unsigned peers = __match_any_sync(kFull, key);
       if (h < re) {
         const int64_t pos = rb + cnt[key] + __popc(peers & lt);
-        ps_t[pos] = t;
-        ps_v[pos] = val32[h];
+        // the start of the term's dense run (bivf.cuh), read when d > 0
+        const uint32_t base = d ? (__ldg(offs + (uint32_t)t * nblk) & ~kDense) : 0u;
+        ps_t[pos] = make_int2(t, d);
+        ps_v[pos] = make_int2((int)base, __float_as_int(val32[h]));
       }
       __syncwarp();
       if (h < re && lane == __ffs(peers) - 1) cnt[key] += __popc(peers);
@@ -1811,7 +1819,7 @@ struct AssignArgs {
   double mu_max;
   ivfkm_stats* stats;
   const int32_t* order;
-  const int32_t* ps_t = nullptr;  // presorted rows (pass mode), see ivfkm_assign_screen_ex
+  int32_t* ps_t = nullptr;  // presorted rows (pass mode), see ivfkm_assign_screen_ex
   float* ps_v = nullptr;
   const uint8_t* slot8 = nullptr;  // sparse spans' slot bytes (ivfkm_bivf_slots)
 };
@@ -1850,11 +1858,13 @@ int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
   if (pl.passes && a.ps_t && (pl.cta_blocks / pl.rr) > 0 &&
       ivfkm_bivf_nblk(a.k) / kSpan < kPresortBuckets) {
     const int nsp = (int)(ivfkm_bivf_nblk(a.k) / kSpan);
+    int2* pt = reinterpret_cast<int2*>(a.ps_t);
+    int2* pvv = reinterpret_cast<int2*>(a.ps_v);
     presort_rows_kernel<<<grid_for(a.n_obj, 8), 256, 0, st>>>(
-        a.n_obj, a.row_ptr, a.terms, a.val32, sp.dpre, nsp, const_cast<int32_t*>(a.ps_t), a.ps_v);
+        a.n_obj, a.row_ptr, a.terms, a.val32, sp.dpre, sp.offs, (uint32_t)sp.nblk, nsp, pt, pvv);
     IVFKM_CHECK_LAUNCH();
-    sp.ps_t = a.ps_t;
-    sp.ps_v = a.ps_v;
+    sp.ps_t = pt;
+    sp.ps_v = pvv;
   }
   if (a.screen_bits == 16 && pl.rr == 8) sp.slot8 = a.slot8;
   sp.st_best = w.st_best;

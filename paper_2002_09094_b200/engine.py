@@ -644,9 +644,11 @@ class LloydEngine:
     def _presort_buffers(self):
         dd = self.dd
         if self._presort is None or self._presort[0] is not dd.terms:
-            self._presort = (dd.terms, torch.empty(max(dd.nnz, 1), dtype=torch.int32,
+            # per entry {term, dense prefix} and {dense-run start, value}
+            self._presort = (dd.terms, torch.empty(2 * max(dd.nnz, 1), dtype=torch.int32,
                                                    device=self.device),
-                             torch.empty(max(dd.nnz, 1), dtype=torch.float32, device=self.device))
+                             torch.empty(2 * max(dd.nnz, 1), dtype=torch.float32,
+                                         device=self.device))
         return self._presort[1], self._presort[2]
 
     IVFD_SLOT_BYTES = 4 << 30  # the wave's per-mean similarity slots (N float64 each)
