@@ -301,10 +301,14 @@ int ivfkm_update_fill(int64_t n_obj, int64_t nnz, int64_t k, int64_t dim,
                       double* new_vals /*[dev]*/, uint8_t* retained /*[dev] k*/,
                       int64_t capacity, void* ws, size_t ws_bytes, ivfkm_stream_t stream);
 
-/* Slot bytes of the BIVF's sparse spans ([dev] slot8: one byte per screen
- * value position — ivfkm_bivf_values_capacity() of them — written only at
- * the positions of sparse-span postings: the posting's slot within its
- * 256-slot span).  Call after the fill; read by ivfkm_assign_screen_ex. */
+/* Slot bytes of the BIVF's sparse spans ([dev] slot8, 16-byte aligned,
+ * ivfkm_bivf_slots_size(k, dim, number of screen values) bytes: a table of
+ * the spans' value offsets per term — dim * (spans + 1) words, so that a
+ * sparse span's start and end are two adjacent words — then one byte per
+ * screen value position, written only at the positions of sparse-span
+ * postings: the posting's slot within its 256-slot span).  Call after the
+ * fill; read by ivfkm_assign_screen_ex. */
+size_t ivfkm_bivf_slots_size(int64_t k, int64_t dim, int64_t n_values);
 int ivfkm_bivf_slots(int64_t k, int64_t dim, int major, int64_t nrows, const int64_t* ptr,
                      const int32_t* cols, const uint32_t* headers, uint8_t* slot8,
                      ivfkm_stream_t stream);

@@ -98,6 +98,7 @@ SIGNATURES = {
                                           _vp, _vp, _vp, _vp, _vp, _vp, _vp, C.c_int, _vp, _sz,
                                           _vp]),
     "ivfkm_rankdir_build": (C.c_int, [_i64, _i64, _vp, _vp, _vp, _vp]),
+    "ivfkm_bivf_slots_size": (_sz, [_i64, _i64, _i64]),
     "ivfkm_rows_decode": (C.c_int, [_i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp]),
     "ivfkm_rows_prepare": (C.c_int, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "ivfkm_uci_parse": (C.c_int, [_vp, _sz, C.c_int, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp,

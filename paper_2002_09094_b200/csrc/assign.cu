@@ -75,6 +75,8 @@ struct ScreenParams {
   const int32_t* inv;     // [k] slot -> mean
   const int32_t* order;   // [n] processing order of objects, or nullptr
   const uint8_t* slot8 = nullptr;  // sparse spans' slot bytes (ivfkm_bivf_slots), or nullptr
+  const uint32_t* soff = nullptr;  // with slot8: compact span offsets [dim][nsp1] (bivf.cuh)
+  int nsp1 = 0;                    // spans per term + 1
   // rows presorted by dense prefix (presort_rows_kernel), per entry {term,
   // dense prefix} and {dense-run start, fp32 value bits}; or nullptr: the CTA
   // sorts its staged row itself
@@ -454,6 +456,11 @@ __device__ void pass_epilogue(const ScreenParams& p, ScreenShared& sh, const flo
   }
 }
 
+// Two adjacent words at any 4-byte alignment.
+__device__ __forceinline__ uint2 ldg_u2(const uint32_t* at) {
+  return make_uint2(__ldg(at), __ldg(at + 1));
+}
+
 // Byte offset of a dense run's value index: 32-bit for fp16 values (indices
 // stay below 2^31, bivf.cu), 64-bit for fp32 ones (4 B x 2^30+ values pass 2^32).
 template <bool HALF>
@@ -641,6 +648,7 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
     }
   }
   __syncthreads();
+  const bool sparse8 = HALF && RR == 8 && p.slot8 != nullptr;
   const uint32_t* __restrict__ masks = static_cast<const uint32_t*>(s_base[0]);
   const uint32_t* __restrict__ offs = static_cast<const uint32_t*>(s_base[1]);
   const void* pv = s_base[2];
@@ -673,7 +681,9 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
         int lp = td.y - gs0;
         lp = lp < 0 ? 0 : (lp > nls ? nls : lp);
         if (z == 0) post += __ldg(p.nc + td.x);
-        const uint32_t row = (uint32_t)td.x * (uint32_t)nblk;
+        // staged row word: the term's row of the block headers, or — when the
+        // sparse spans go through slot bytes — of the span offsets table
+        const uint32_t row = (uint32_t)td.x * (sparse8 ? (uint32_t)p.nsp1 : (uint32_t)nblk);
         s_ent[j] = make_int4((int)row, bv.y, lp ? bv.x : 0, bv.y);
         s_lp[j] = (uint8_t)lp;
       }
@@ -745,11 +755,12 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
       __syncthreads();
       for (int j = threadIdx.x; j < cn; j += blockDim.x) {
         const int lp = s_lp[j];
-        const uint32_t row = (uint32_t)p.terms[c0 + j] * (uint32_t)nblk;
+        const uint32_t t = (uint32_t)p.terms[c0 + j];
+        const uint32_t row = t * (uint32_t)nblk;
         const int v = __float_as_int(p.val32[c0 + j]);
         const uint32_t base = lp ? (__ldg(offs + row) & ~kDense) : 0u;
         s_ent[s_cntd[lp] + s_cc[(j >> 5) * nb + lp] + s_pos[j]] =
-            make_int4((int)row, v, (int)base, v);
+            make_int4((int)(sparse8 ? t * (uint32_t)p.nsp1 : row), v, (int)base, v);
       }
       __syncthreads();
     }
@@ -831,11 +842,12 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
               float v = 0.f;
               bool dense = false;
               if (e < cn) {
-                const uint32_t row = (uint32_t)s_ent[e].x + gb32;
-                o0 = __ldg(offs + row);
+                // the span's start and end: adjacent words of the span offsets
+                const uint2 oo = ldg_u2(p.soff + (uint32_t)s_ent[e].x + (gb32 >> 3));
+                o0 = oo.x;
                 v = __int_as_float(s_ent[e].y);
                 dense = (o0 & kDense) != 0u;
-                if (!dense) cnt = (__ldg(offs + row + kSpan) & ~kDense) - o0;
+                if (!dense) cnt = (oo.y & ~kDense) - o0;
               }
               // dense spans beyond the prefix (rare): whole-warp 16-B loads, in entry order
               unsigned dm = __ballot_sync(kFull, dense && gi == 0);
@@ -1866,7 +1878,12 @@ int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
     sp.ps_t = pt;
     sp.ps_v = pvv;
   }
-  if (a.screen_bits == 16 && pl.rr == 8) sp.slot8 = a.slot8;
+  if (a.screen_bits == 16 && pl.rr == 8 && a.slot8) {
+    // [span offsets][slot bytes] (bivf.cuh, bivf_soff_bytes)
+    sp.soff = reinterpret_cast<const uint32_t*>(a.slot8);
+    sp.slot8 = a.slot8 + bivf_soff_bytes(a.dim, sp.nblk);
+    sp.nsp1 = (int)(sp.nblk / kSpan + 1);
+  }
   sp.st_best = w.st_best;
   sp.st_slot = w.st_slot;
   sp.st_cnt = w.st_cnt;

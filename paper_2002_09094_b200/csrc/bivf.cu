@@ -683,7 +683,23 @@ __global__ void bivf_slot_kernel(int major, int64_t nrows, const int64_t* __rest
     slot8[(int64_t)o + __popc(m & ((1u << j) - 1u))] = (uint8_t)(sl & 255);
   });
 }
+// Compact span offsets (bivf.cuh, bivf_soff_bytes).
+__global__ void bivf_soff_kernel(int64_t dim, int64_t nblk, const unsigned int* __restrict__ offs,
+                                 unsigned int* __restrict__ soff) {
+  const int64_t nsp1 = nblk / kSpan + 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < dim * nsp1;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / nsp1, sp = i - t * nsp1;
+    // sp == nsp1 - 1: the next term's first block (the total after the last term)
+    soff[i] = offs[t * nblk + sp * kSpan];
+  }
+}
 }  // namespace
+
+extern "C" size_t ivfkm_bivf_slots_size(int64_t k, int64_t dim, int64_t n_values) {
+  if (k < 1 || dim < 1 || n_values < 0) return 0;
+  return bivf_soff_bytes(dim, ivfkm_bivf_nblk(k)) + (size_t)n_values;
+}
 
 extern "C" int ivfkm_bivf_slots(int64_t k, int64_t dim, int major, int64_t nrows,
                                 const int64_t* ptr, const int32_t* cols, const uint32_t* headers,
@@ -694,8 +710,11 @@ extern "C" int ivfkm_bivf_slots(int64_t k, int64_t dim, int major, int64_t nrows
   const int64_t nh = bivf_nh(dim, nblk);
   const int32_t* perm = reinterpret_cast<const int32_t*>(headers + 2 * nh + 1 + dim);
   cudaStream_t st = as_stream(stream_);
+  bivf_soff_kernel<<<grid_for(dim * (nblk / kSpan + 1), 256, num_sms() * 16), 256, 0, st>>>(
+      dim, nblk, headers + nh, reinterpret_cast<unsigned int*>(slot8));
+  IVFKM_CHECK_LAUNCH();
   bivf_slot_kernel<<<num_sms() * 8, 256, 0, st>>>(major, nrows, ptr, cols, k, dim, nblk, headers,
-                                                  perm, slot8);
+                                                  perm, slot8 + bivf_soff_bytes(dim, nblk));
   IVFKM_CHECK_LAUNCH();
   return IVFKM_OK;
 }

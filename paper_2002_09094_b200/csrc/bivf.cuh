@@ -62,6 +62,16 @@ __host__ __device__ inline int64_t bivf_mo_word(int64_t k, int64_t dim, int64_t 
   return (w + 1) & ~(int64_t)1;
 }
 
+// The slot-byte buffer of the sparse path (ivfkm_bivf_slots) starts with the
+// compact span offsets soff[t*(nsp+1) + s] = offs[t*nblk + 8*s] (s = nsp: the
+// end of the term's last span): the screen's sparse path reads a span's start
+// and end from two adjacent words of a table of dim*(nsp+1) words (23 MB at
+// config 3, 133 MB at config 4) instead of two words 32 bytes apart in the
+// (term x block) offsets (0.45 / 5.3 GB).  The slot bytes follow, 16-B aligned.
+__host__ __device__ inline size_t bivf_soff_bytes(int64_t dim, int64_t nblk) {
+  return ((size_t)dim * (size_t)(nblk / kSpan + 1) * 4 + 15) & ~(size_t)15;
+}
+
 // Position of slot s's exact value for term t, or -1 when the slot lacks it.
 __device__ __forceinline__ int64_t bivf_find_slot(const BivfView& v, int64_t t, int64_t s) {
   const uint32_t bit = 1u << (s & 31);

@@ -530,14 +530,15 @@ class LloydEngine:
         if use_slots and bits == 16:
             par = self._bvpar ^ 1  # the value buffers' parity of this build
             sb = self._slotbuf[par]
-            if sb is None or sb.numel() < n_s:
-                sb = torch.empty(int(n_s * 1.25) + 1024, dtype=torch.uint8, device=dev)
+            need = int(self.lib.ivfkm_bivf_slots_size(self.k, dm.dim, n_s))
+            if sb is None or sb.numel() < need:
+                sb = torch.empty(need + n_s // 4 + 1024, dtype=torch.uint8, device=dev)
                 self._slotbuf[par] = sb
             _lib.check(self.lib.ivfkm_bivf_slots(self.k, dm.dim, 0, self.k, _p(dm.ptr),
                                                  _p(dm.terms), _p(dm.headers), _p(sb), _stream()),
                        "ivfkm_bivf_slots")
             dm.slot8 = sb
-            self.launches += 1
+            self.launches += 2  # span offsets, slot bytes
         # plan: sizes, CUB sort of the k slot keys (single tile / onesweep), perm,
         # mask, count, 2 scans (init + sweep each), offset, nc, {mask, offset}
         # pairs; fill: zero, position keys, CUB onesweep sort of the keys' top
@@ -574,7 +575,10 @@ class LloydEngine:
         nc = dm.headers[2 * nh + 1:2 * nh + 1 + self.dd.dim].to(torch.float64)
         v = float(torch.dot(self._doc_freq[1], nc).item())
         w = max(v / (self.dd.n * spans), 1.0)  # postings per (object, span)
-        per = max(2, int(np.ceil(self.PASS_WORK / w)))
+        # whole spans per warp: a pass's CTAs run four warps, and 5 or 11 spans
+        # leave some of them idle (config 4: 8 spans per pass 5.77 s, 11: 5.94 s,
+        # 12: 6.21 s; config 2: 4 spans 115 ms, 5: 168 ms, 3: 139 ms)
+        per = max(4, int(self.PASS_WORK / w) // 4 * 4)
         p = int(np.ceil(spans / per))
         return p if p > 1 else 1
 
