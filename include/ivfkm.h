@@ -161,14 +161,21 @@ void ivfkm_set_screen_warps(int warps);
  * {term, dense prefix} and {dense-run start, value} — so that every pass
  * stages its rows by copying, with no per-term lookups.  slot8 (ivfkm_bivf_slots, fp16
  * screens): the sparse spans are read through their slot bytes instead of
- * the block masks. */
+ * the block masks.  doc_freq (ivfkm_doc_freq of these rows, [dev] uint32[dim],
+ * or NULL): the postings counter is then sum_t doc_freq[t] * nc[t] — one pass
+ * over the terms — instead of a posting-count gather per object entry. */
 int ivfkm_assign_screen_ex(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
                            const float* val32, const double* xnorm, int64_t k, int64_t dim,
                            const uint32_t* headers, const void* pval_screen, int screen_bits,
                            double mu_max, ivfkm_stats* stats, const int32_t* order,
                            int32_t* presort_terms, float* presort_vals,
-                           const uint8_t* slot8 /*[dev] or NULL*/, void* ws, size_t ws_bytes,
+                           const uint8_t* slot8 /*[dev] or NULL*/,
+                           const uint32_t* doc_freq /*[dev] or NULL*/, void* ws, size_t ws_bytes,
                            ivfkm_stream_t stream);
+/* Objects per term of a corpus (0-based terms [dev] int32[nnz]) -> doc_freq
+ * [dev] uint32[dim] (the reference's Dataset.doc_freq, data.py:200-211). */
+int ivfkm_doc_freq(int64_t nnz, const int32_t* terms, int64_t dim, uint32_t* doc_freq,
+                   ivfkm_stream_t stream);
 /* Screen tuning: which = 1: slot-range passes for the next screens (0 or 1
  * = one pass).  With P > 1 passes the fp16 register screen runs P launches,
  * each over all objects and 1/P of the slots (one CTA per object, no

@@ -76,7 +76,8 @@ SIGNATURES = {
                                       _f64, _vp,
                                       _vp, _vp, _sz, _vp]),
     "ivfkm_assign_screen_ex": (C.c_int, [_i64, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, C.c_int,
-                                         _f64, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+                                         _f64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "ivfkm_doc_freq": (C.c_int, [_i64, _vp, _i64, _vp, _vp]),
     "ivfkm_bivf_slots": (C.c_int, [_i64, _i64, C.c_int, _i64, _vp, _vp, _vp, _vp, _vp]),
     "ivfkm_assign_finish": (C.c_int, [_i64, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp,
                                       _vp, _vp, C.c_int, _vp, _sz, _vp]),

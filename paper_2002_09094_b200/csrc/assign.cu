@@ -72,6 +72,8 @@ struct ScreenParams {
   const uint32_t* offs;   // [dim][nblk] (+1: total)
   const uint32_t* nc;     // [dim] postings per term
   const uint32_t* dpre;   // [dim] dense prefix spans per term
+  const uint2* tinfo;     // [dim] {dense-run start, dense prefix} (bivf.cuh)
+  int count_post = 1;     // 0: the postings counter comes from doc_freq . nc (screen_impl)
   const int32_t* inv;     // [k] slot -> mean
   const int32_t* order;   // [n] processing order of objects, or nullptr
   const uint8_t* slot8 = nullptr;  // sparse spans' slot bytes (ivfkm_bivf_slots), or nullptr
@@ -519,7 +521,7 @@ __device__ __forceinline__ void screen_epilogue(const ScreenParams& p, ScreenSha
       sh.best_c = c;
       sh.post = q;
       sh.cnt = 0;
-      if (q) atomicAdd(&p.stats->postings, q);
+      if (q && p.count_post) atomicAdd(&p.stats->postings, q);
     }
   }
 
@@ -678,9 +680,10 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
       for (int j = threadIdx.x; j < cn; j += blockDim.x) {
         const int2 td = __ldg(p.ps_t + c0 + j);
         const int2 bv = __ldg(p.ps_v + c0 + j);
-        int lp = td.y - gs0;
+        int lp = (td.y & 0x7fffffff) - gs0;
         lp = lp < 0 ? 0 : (lp > nls ? nls : lp);
-        if (z == 0) post += __ldg(p.nc + td.x);
+        // the postings counter, or (counted from doc_freq) whether any exist
+        if (z == 0) post += p.count_post ? __ldg(p.nc + td.x) : ((uint32_t)td.y >> 31);
         // staged row word: the term's row of the block headers, or — when the
         // sparse spans go through slot bytes — of the span offsets table
         const uint32_t row = (uint32_t)td.x * (sparse8 ? (uint32_t)p.nsp1 : (uint32_t)nblk);
@@ -715,9 +718,10 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
         int lp = -1;
         if (j < cn) {
           const uint32_t t = (uint32_t)p.terms[c0 + j];
-          lp = (int)__ldg(p.dpre + t) - gs0;
+          const uint32_t dy = __ldg(p.tinfo + t).y;
+          lp = (int)(dy & 0x7fffffffu) - gs0;
           lp = lp < 0 ? 0 : (lp > nls ? nls : lp);
-          if (z == 0) post += __ldg(p.nc + t);
+          if (z == 0) post += p.count_post ? __ldg(p.nc + t) : (dy >> 31);
         }
         const unsigned peers = __match_any_sync(kFull, lp);
         if (j < cn) {
@@ -758,7 +762,7 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
         const uint32_t t = (uint32_t)p.terms[c0 + j];
         const uint32_t row = t * (uint32_t)nblk;
         const int v = __float_as_int(p.val32[c0 + j]);
-        const uint32_t base = lp ? (__ldg(offs + row) & ~kDense) : 0u;
+        const uint32_t base = lp ? __ldg(p.tinfo + t).x : 0u;  // (same sector as the prefix)
         s_ent[s_cntd[lp] + s_cc[(j >> 5) * nb + lp] + s_pos[j]] =
             make_int4((int)(sparse8 ? t * (uint32_t)p.nsp1 : row), v, (int)base, v);
       }
@@ -1448,6 +1452,18 @@ __global__ void entry_gather_kernel(int64_t nnz, const int32_t* __restrict__ sid
   }
 }
 
+// The assign's posting volume from the objects' document frequencies.
+__global__ void postings_dot_kernel(int64_t dim, const uint32_t* __restrict__ df,
+                                    const uint32_t* __restrict__ nc, ivfkm_stats* stats) {
+  unsigned long long s = 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < dim;
+       t += (int64_t)gridDim.x * blockDim.x)
+    s += (unsigned long long)df[t] * (unsigned long long)nc[t];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(&stats->postings, s);
+}
+
 // Each row's entries stably sorted by the terms' dense prefix, longest first
 // (for the slot-range passes: every pass's clamped bucket order is this order,
 // so the screen stages a pass by copying).  One warp per row: a counting sort
@@ -1457,7 +1473,7 @@ constexpr int kPresortBuckets = 256;
 __global__ void __launch_bounds__(256) presort_rows_kernel(
     int64_t n_obj, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ terms,
     const float* __restrict__ val32, const uint32_t* __restrict__ dpre,
-    const uint32_t* __restrict__ offs, uint32_t nblk, int nsp, int2* __restrict__ ps_t,
+    const uint2* __restrict__ tinfo, int nsp, int2* __restrict__ ps_t,
     int2* __restrict__ ps_v) {
   __shared__ int s_cnt[8][kPresortBuckets];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1507,10 +1523,10 @@ __global__ void __launch_bounds__(256) presort_rows_kernel(
       const unsigned peers = __match_any_sync(kFull, key);
       if (h < re) {
         const int64_t pos = rb + cnt[key] + __popc(peers & lt);
-        // the start of the term's dense run (bivf.cuh), read when d > 0
-        const uint32_t base = d ? (__ldg(offs + (uint32_t)t * nblk) & ~kDense) : 0u;
-        ps_t[pos] = make_int2(t, d);
-        ps_v[pos] = make_int2((int)base, __float_as_int(val32[h]));
+        // {the start of the term's dense run, dense prefix | has-postings bit}
+        const uint2 ti = __ldg(tinfo + t);
+        ps_t[pos] = make_int2(t, (int)ti.y);
+        ps_v[pos] = make_int2((int)ti.x, __float_as_int(val32[h]));
       }
       __syncwarp();
       if (h < re && lane == __ffs(peers) - 1) cnt[key] += __popc(peers);
@@ -1834,6 +1850,7 @@ struct AssignArgs {
   int32_t* ps_t = nullptr;  // presorted rows (pass mode), see ivfkm_assign_screen_ex
   float* ps_v = nullptr;
   const uint8_t* slot8 = nullptr;  // sparse spans' slot bytes (ivfkm_bivf_slots)
+  const uint32_t* doc_freq = nullptr;  // objects per term, or nullptr: the screen counts
 };
 
 int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
@@ -1854,6 +1871,15 @@ int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
   sp.nc = a.headers + 2 * a.dim * sp.nblk + 1;
   sp.inv = reinterpret_cast<const int32_t*>(sp.nc + a.dim) + a.k;
   sp.dpre = reinterpret_cast<const uint32_t*>(sp.inv + a.k);
+  sp.tinfo = reinterpret_cast<const uint2*>(a.headers + bivf_tinfo_word(a.k, a.dim, sp.nblk));
+  if (a.doc_freq) {
+    // V = sum_t no_t * nc_t (counters.py:71-81 regrouped by term): one pass
+    // over the D terms instead of a posting-count gather per object entry
+    sp.count_post = 0;
+    postings_dot_kernel<<<grid_for(a.dim, 256, num_sms() * 4), 256, 0, st>>>(a.dim, a.doc_freq,
+                                                                            sp.nc, a.stats);
+    IVFKM_CHECK_LAUNCH();
+  }
   sp.order = a.order;
   sp.pv32 = static_cast<const float*>(a.pval_screen);
   sp.half = a.screen_bits == 16;
@@ -1873,7 +1899,7 @@ int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
     int2* pt = reinterpret_cast<int2*>(a.ps_t);
     int2* pvv = reinterpret_cast<int2*>(a.ps_v);
     presort_rows_kernel<<<grid_for(a.n_obj, 8), 256, 0, st>>>(
-        a.n_obj, a.row_ptr, a.terms, a.val32, sp.dpre, sp.offs, (uint32_t)sp.nblk, nsp, pt, pvv);
+        a.n_obj, a.row_ptr, a.terms, a.val32, sp.dpre, sp.tinfo, nsp, pt, pvv);
     IVFKM_CHECK_LAUNCH();
     sp.ps_t = pt;
     sp.ps_v = pvv;
@@ -1970,8 +1996,9 @@ extern "C" int ivfkm_assign_screen_ex(int64_t n_obj, const int64_t* row_ptr,
                                       const uint32_t* headers, const void* pval_screen,
                                       int screen_bits, double mu_max, ivfkm_stats* stats,
                                       const int32_t* order, int32_t* presort_terms,
-                                      float* presort_vals, const uint8_t* slot8, void* ws,
-                                      size_t ws_bytes, ivfkm_stream_t stream_);
+                                      float* presort_vals, const uint8_t* slot8,
+                                      const uint32_t* doc_freq, void* ws, size_t ws_bytes,
+                                      ivfkm_stream_t stream_);
 
 extern "C" int ivfkm_assign_screen(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,
                                    const float* val32, const double* xnorm, int64_t k,
@@ -1981,7 +2008,7 @@ extern "C" int ivfkm_assign_screen(int64_t n_obj, const int64_t* row_ptr, const 
                                    ivfkm_stream_t stream_) {
   return ivfkm_assign_screen_ex(n_obj, row_ptr, terms, val32, xnorm, k, dim, headers,
                                 pval_screen, screen_bits, mu_max, stats, order, nullptr, nullptr,
-                                nullptr, ws, ws_bytes, stream_);
+                                nullptr, nullptr, ws, ws_bytes, stream_);
 }
 
 extern "C" int ivfkm_assign_screen_ex(int64_t n_obj, const int64_t* row_ptr,
@@ -1990,8 +2017,9 @@ extern "C" int ivfkm_assign_screen_ex(int64_t n_obj, const int64_t* row_ptr,
                                       const uint32_t* headers, const void* pval_screen,
                                       int screen_bits, double mu_max, ivfkm_stats* stats,
                                       const int32_t* order, int32_t* presort_terms,
-                                      float* presort_vals, const uint8_t* slot8, void* ws,
-                                      size_t ws_bytes, ivfkm_stream_t stream_) {
+                                      float* presort_vals, const uint8_t* slot8,
+                                      const uint32_t* doc_freq, void* ws, size_t ws_bytes,
+                                      ivfkm_stream_t stream_) {
   if (n_obj < 0 || k < 1 || dim < 1 || !row_ptr || !stats || !headers) return IVFKM_E_ARG;
   if (screen_bits != 32 && screen_bits != 16) return IVFKM_E_ARG;
   // fp16 holds mean values up to 65504; unit-norm means are far inside
@@ -2009,7 +2037,32 @@ extern "C" int ivfkm_assign_screen_ex(int64_t n_obj, const int64_t* row_ptr,
   a.ps_t = presort_terms;
   a.ps_v = presort_vals;
   a.slot8 = slot8;
+  a.doc_freq = doc_freq;
   return screen_impl(a, w, st);
+}
+
+// Objects per term (the document frequencies no_p of data.py:200-211) as the
+// screen's posting counter reads them.
+namespace {
+__global__ void doc_freq_kernel(int64_t nnz, const int32_t* __restrict__ terms, int64_t dim,
+                                unsigned int* __restrict__ df) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t t = terms[e];
+    if (t >= 0 && t < dim) atomicAdd(&df[t], 1u);
+  }
+}
+}  // namespace
+
+extern "C" int ivfkm_doc_freq(int64_t nnz, const int32_t* terms, int64_t dim, uint32_t* doc_freq,
+                              ivfkm_stream_t stream_) {
+  if (nnz < 0 || dim < 1 || !doc_freq || (nnz > 0 && !terms)) return IVFKM_E_ARG;
+  cudaStream_t st = as_stream(stream_);
+  IVFKM_TRY(cudaMemsetAsync(doc_freq, 0, sizeof(uint32_t) * dim, st));
+  if (nnz == 0) return IVFKM_OK;
+  doc_freq_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(nnz, terms, dim, doc_freq);
+  IVFKM_CHECK_LAUNCH();
+  return IVFKM_OK;
 }
 
 extern "C" int ivfkm_assign_finish(int64_t n_obj, const int64_t* row_ptr, const int32_t* terms,

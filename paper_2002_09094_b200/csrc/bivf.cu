@@ -342,7 +342,8 @@ __global__ void bivf_perm_kernel(int64_t k, const int32_t* __restrict__ sorted,
 // One warp per term: postings (nc) and the dense prefix (dpre, bivf.cuh).
 __global__ void bivf_nc_kernel(int64_t dim, int64_t nblk, const unsigned int* __restrict__ masks,
                                const unsigned int* __restrict__ offs,
-                               unsigned int* __restrict__ nc, unsigned int* __restrict__ dpre) {
+                               unsigned int* __restrict__ nc, unsigned int* __restrict__ dpre,
+                               uint2* __restrict__ tinfo) {
   const int lane = threadIdx.x & 31;
   const int64_t wpb = blockDim.x >> 5;
   const int64_t nspan = nblk / kSpan;
@@ -364,6 +365,8 @@ __global__ void bivf_nc_kernel(int64_t dim, int64_t nblk, const unsigned int* __
     if (lane == 0) {
       nc[t] = c;
       dpre[t] = (unsigned)pre;
+      // bit 31: the term has postings (an object touching none keeps label 0)
+      tinfo[t] = make_uint2(offs[t * nblk] & ~kDense, (unsigned)pre | (c ? 0x80000000u : 0u));
     }
   }
 }
@@ -383,7 +386,8 @@ extern "C" void ivfkm_set_bivf_options(float dense_fill, int permute) {
 
 extern "C" int64_t ivfkm_bivf_headers_size(int64_t k, int64_t dim) {
   const int64_t nh = bivf_nh(dim, ivfkm_bivf_nblk(k));
-  return bivf_mo_word(k, dim, ivfkm_bivf_nblk(k)) + 2 * nh;
+  (void)nh;
+  return bivf_tinfo_word(k, dim, ivfkm_bivf_nblk(k)) + 2 * dim;
 }
 
 extern "C" int64_t ivfkm_bivf_values_capacity(int64_t k, int64_t dim, int64_t nnz) {
@@ -469,8 +473,9 @@ int plan_layout(int64_t k, int64_t dim, uint32_t* headers, unsigned th, const Bi
   bivf_offset_kernel<<<grid_for(nh / kSpan + 1, threads), threads, 0, st>>>(nh, w.off, th,
                                                                            headers);
   IVFKM_CHECK_LAUNCH();
-  bivf_nc_kernel<<<grid_for(dim, threads / 32), threads, 0, st>>>(dim, nblk, headers,
-                                                                 headers + nh, nc, dpre);
+  bivf_nc_kernel<<<grid_for(dim, threads / 32), threads, 0, st>>>(
+      dim, nblk, headers, headers + nh, nc, dpre,
+      reinterpret_cast<uint2*>(headers + bivf_tinfo_word(k, dim, nblk)));
   IVFKM_CHECK_LAUNCH();
   bivf_mo_kernel<<<grid_for(nh, threads), threads, 0, st>>>(
       nh, headers, off64, reinterpret_cast<uint2*>(headers + bivf_mo_word(k, dim, nblk)));

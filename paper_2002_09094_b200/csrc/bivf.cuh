@@ -22,6 +22,9 @@
 //   off64[dim*nblk]          their number
 //   mo   [t*nblk + b]        (uint2, at the next even word) {mask, off64}: the
 //                            exact lookup's two words in one 8-byte gather
+//   tinfo[t]                 (uint2) {offs[t*nblk] & ~kDense, dpre[t] | bit 31
+//                            when nc[t] > 0}: the screen's per-entry staging
+//                            lookup in one gather
 // Screen values: blocks are grouped in spans of 8 (256 slots); every span's
 // value segment is padded to a multiple of 8 values, so a span start is 16-B
 // aligned in both the fp32 and the fp16 screen arrays.
@@ -60,6 +63,12 @@ __host__ __device__ inline int64_t bivf_mo_word(int64_t k, int64_t dim, int64_t 
   const int64_t nh = bivf_nh(dim, nblk);
   const int64_t w = 2 * nh + 1 + dim + 2 * k + dim + nh + 1;
   return (w + 1) & ~(int64_t)1;
+}
+
+// Word offset of tinfo (after mo): per term {start of its dense-prefix run,
+// dense prefix} — the screen's staging reads both with one 8-byte gather.
+__host__ __device__ inline int64_t bivf_tinfo_word(int64_t k, int64_t dim, int64_t nblk) {
+  return bivf_mo_word(k, dim, nblk) + 2 * bivf_nh(dim, nblk);
 }
 
 // The slot-byte buffer of the sparse path (ivfkm_bivf_slots) starts with the

@@ -438,6 +438,11 @@ class LloydEngine:
         self.passes = None
         self.last_postings = None
         self._doc_freq = None
+        # postings counted from the rows' document frequencies (one pass over
+        # the terms per assign); False: in the screen, per object entry — for
+        # callers whose rows change every step (the streamed end-to-end paths)
+        self.df_counter = True
+        self._pass_df = None
         # IVFD (rule 1) in its own loop order: the object-inverted kernel
         # (ivfkm_assign_ivfd); False serves IVFD through the IVF kernels with
         # the IVFD label rule (identical results)
@@ -568,12 +573,12 @@ class LloydEngine:
         spans = self.nblk // 8
         if self.screen_bits != 16 or spans < 16 or self.dd.n == 0:
             return 1
-        if self._doc_freq is None or self._doc_freq[0] is not self.dd.terms:
-            self._doc_freq = (self.dd.terms, torch.bincount(
-                self.dd.terms.long(), minlength=self.dd.dim).to(torch.float64))
         nh = self.dd.dim * self.nblk
         nc = dm.headers[2 * nh + 1:2 * nh + 1 + self.dd.dim].to(torch.float64)
-        v = float(torch.dot(self._doc_freq[1], nc).item())
+        if self._pass_df is None or self._pass_df[0] is not self.dd.terms:
+            self._pass_df = (self.dd.terms, torch.bincount(
+                self.dd.terms.long(), minlength=self.dd.dim).to(torch.float64))
+        v = float(torch.dot(self._pass_df[1], nc).item())
         w = max(v / (self.dd.n * spans), 1.0)  # postings per (object, span)
         # whole spans per warp: a pass's CTAs run four warps, and 5 or 11 spans
         # leave some of them idle (config 4: 8 spans per pass 5.77 s, 11: 5.94 s,
@@ -581,6 +586,20 @@ class LloydEngine:
         per = max(4, int(self.PASS_WORK / w) // 4 * 4)
         p = int(np.ceil(spans / per))
         return p if p > 1 else 1
+
+    def doc_freq(self) -> torch.Tensor:
+        """Objects per term of the current rows (ivfkm_doc_freq; uint32 held as
+        int32), computed once per corpus: the screen's posting counter is
+        sum_t doc_freq[t] * nc[t] instead of a gather per object entry."""
+        dd = self.dd
+        if not self.df_counter:
+            return None
+        if self._doc_freq is None or self._doc_freq[0] is not dd.terms:
+            df = torch.empty(dd.dim, dtype=torch.int32, device=self.device)
+            _lib.check(self.lib.ivfkm_doc_freq(dd.nnz, _p(dd.terms), dd.dim, _p(df), _stream()),
+                       "ivfkm_doc_freq")
+            self._doc_freq = (dd.terms, df)
+        return self._doc_freq[1]
 
     def assign(self, dm: DeviceMeans, prev: torch.Tensor | None, events=None,
                rule: int = 0) -> torch.Tensor:
@@ -611,10 +630,12 @@ class LloydEngine:
                                              _p(dm.pvs), dm.screen_bits, _MU_MAX, _p(self.stats),
                                              _p(order), _p(ps[0]), _p(ps[1]),
                                              _p(dm.slot8 if dm.screen_bits == 16 else None),
-                                             _p(self.ws_assign), self.ws_assign.numel(), st)
+                                             _p(self.doc_freq()), _p(self.ws_assign),
+                                             self.ws_assign.numel(), st)
         _lib.check(rc, "ivfkm_assign_screen_ex")
         if ps[0] is not None:
             self.launches += 1
+        self.launches += 1  # the postings counter from the document frequencies
         self.launches += npass - 1
         if events is not None:
             events[1].record()
@@ -820,6 +841,7 @@ class HostIteration:
             self.next_dd, self.next_ready = self._upload()
         if self.eng is None:  # after the wait: the engine reads the rows on this stream
             self.eng = LloydEngine(dd, self.k)
+            self.eng.df_counter = False  # new rows every step
         self.eng.dd = dd
         dm = self.eng.build_bivf(DeviceMeans(self.k, ms.dim, ptr, terms, vals, ret))
         lab = self.eng.assign(dm, None)
@@ -888,6 +910,7 @@ class StreamIteration:
         self.next_dd, self.next_ready = self._upload()  # the next step's corpus, in flight
         if self.eng is None:
             self.eng = LloydEngine(dd, self.k)
+            self.eng.df_counter = False  # new rows every step
             self.dm = self.eng.upload_means(self.means0)
         self.eng.dd = dd
         lab = self.eng.assign(self.dm, self.prev)
