@@ -819,3 +819,57 @@ def test_sparse_span_slot_path_matches_oracle(tuning, slots, seed, k, signed, pa
         labels, st = _assign_raw(ds, means, bits=16, passes=1, slots=slots, rowcap=64,
                                  smem=6 * 1024, rr=8)
         assert np.array_equal(labels, ol) and st.objective == O.objective(ds, ol, om)
+
+
+@pytest.mark.parametrize("passes", [None, 3])
+def test_postings_counter_from_doc_freq_equals_in_screen_count(tuning, passes):
+    """The two postings counters — sum_t doc_freq[t] * nc[t] (ivfkm_doc_freq,
+    one pass over the terms) and the screen's per-entry count — agree with
+    counters.py:71-81, and objects whose terms hold no posting keep label 1
+    either way (the has-postings bit of tinfo / the presorted rows)."""
+    from paper_2002_09094_b200.variants import engine_for
+
+    k = 4500 if passes else 200
+    ds, om, means = _random_case(n=6000 if passes else 1200, dim=900, k=k, seed=11)
+    # rows 0..39 keep only terms no mean holds: build means from rows >= 40
+    P = _pkg()
+    ip, t, v = np.asarray(ds.indptr), np.asarray(ds.term_ids), np.asarray(ds.values)
+    dim2 = ds.dim + 50
+    t2 = t.copy()
+    for i in range(40):  # move the row onto fresh terms (still ascending, unit norm)
+        n_i = ip[i + 1] - ip[i]
+        t2[ip[i]:ip[i + 1]] = ds.dim + 1 + np.arange(n_i) % 50
+        t2[ip[i]:ip[i + 1]].sort()
+    keep = np.ones(t2.size, bool)
+    for i in range(40):  # drop duplicate ids the wrap-around made
+        seg = t2[ip[i]:ip[i + 1]]
+        keep[ip[i]:ip[i + 1]] = np.concatenate([[True], seg[1:] != seg[:-1]])
+    rows = np.repeat(np.arange(ds.n), np.diff(ip))[keep]
+    t2, v2 = t2[keep], v[keep].copy()
+    ip2 = np.concatenate([[0], np.cumsum(np.bincount(rows, minlength=ds.n))])
+    nrm = np.sqrt(np.bincount(rows, weights=v2 * v2, minlength=ds.n))
+    v2 /= nrm[rows]
+    ds2 = P.Dataset(dim2, ip2, t2.astype(np.int32), v2, normalized=True)
+    means2 = P.MeanSet.from_csr(np.asarray(means.indptr), np.asarray(means.term_ids),
+                                np.asarray(means.values), dim2, "sparse_inverted")
+    eng = engine_for(ds2, means2.k)
+    eng.passes = passes
+    try:
+        got = []
+        for counter in (True, False):
+            eng.df_counter = counter
+            dm = eng.upload_means(means2)
+            lab = eng.assign(dm, None)
+            st = eng.read_stats()
+            got.append((lab.cpu().numpy() + 1, st.postings, st.objective))
+    finally:
+        eng.df_counter = True
+        eng.passes = None
+    assert np.array_equal(got[0][0], got[1][0])
+    assert got[0][1] == got[1][1] and got[0][2] == got[1][2]
+    assert (got[0][0][:40] == 1).all()  # no overlap with any mean: cluster one
+    # V against the definition: sum over object entries of the term's postings
+    nc = np.bincount(np.asarray(means2.term_ids), minlength=dim2 + 1)
+    assert got[0][1] == int(nc[t2].sum())
+    df = eng.doc_freq().cpu().numpy().astype(np.int64)
+    assert np.array_equal(df, np.bincount(t2 - 1, minlength=dim2))
