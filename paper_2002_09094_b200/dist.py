@@ -462,15 +462,20 @@ class DistLloyd:
 def bench_multi(args, rank: int, world: int) -> None:
     """bench.py --gpus N under torchrun: strong scaling of one Lloyd run over N
     ranks (objects sharded, means replicated), plus the same metric end to end
-    (every step re-uploads each rank's shard and the means from pinned host
-    memory and reads labels + means back)."""
+    (every step re-uploads each rank's shard from pinned host memory and reads
+    the labels and statistics back; the means stay on the devices)."""
     from . import synth
     from .clustering import init_means
-    from .engine import DeviceDataset, DeviceMeans
+    from .engine import DeviceDataset
 
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    # NCCL writes its version / debug lines to stdout: keep stdout for the one
+    # JSON line (bench.py's contract) and send everything before it to stderr
+    sys.stdout.flush()
+    stdout_fd = os.dup(1)
+    os.dup2(2, 1)
     if os.environ.get("MASTER_ADDR") is None:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29513")
@@ -522,38 +527,42 @@ def bench_multi(args, rank: int, world: int) -> None:
     rl = torch.tensor([mine / screen_s / 1e9], dtype=torch.float64, device=dev)
     slow = rl.clone()
     dist.all_reduce(slow, op=dist.ReduceOp.MIN)  # lowest achieved GB/s over ranks
-    # ---- end to end: host buffers in and out every step
+    # ---- end to end, as the single-GPU e2e leg (engine.StreamIteration): every
+    # step re-uploads this rank's shard from pinned host memory and reads the
+    # step's result back — labels and the statistics (already a host read of
+    # assign) — while the means and the owners' member rows, the model state,
+    # stay on the devices
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(1, min(args.steps, 3))
-    host = {name: getattr(dm, name).cpu().pin_memory() for name in ("ptr", "terms", "vals",
-                                                                     "retained")}
     lab_host = torch.empty(run.dd.n, dtype=torch.int32).pin_memory()
     h2d = d2h = 0
+    run.eng.df_counter = False  # new rows every step
     torch.cuda.synchronize()
     dist.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         run.dd = DeviceDataset(run.host, dev)
         run.eng.dd = run.dd
-        dmh = DeviceMeans(k, ds.dim, host["ptr"].to(dev, non_blocking=True),
-                          host["terms"].to(dev, non_blocking=True),
-                          host["vals"].to(dev, non_blocking=True),
-                          host["retained"].to(dev, non_blocking=True))
-        dmh = run.eng.build_bivf(dmh)
-        lab, _ = run.assign(dmh, None)
+        lab, _ = run.assign(dm, prev)
         lab_host.copy_(lab, non_blocking=True)
-        new = run.update(lab, dmh)
-        host = {name: getattr(new, name).cpu() for name in ("ptr", "terms", "vals", "retained")}
-        h2d = run.host.nbytes + sum(v.numel() * v.element_size() for v in host.values())
-        d2h = lab_host.numel() * 4 + sum(v.numel() * v.element_size() for v in host.values())
+        dm = run.update(lab, dm)
+        prev = lab
+        torch.cuda.current_stream().synchronize()
+        h2d = run.host.nbytes
+        d2h = lab_host.numel() * 4 + (STAT_WORDS + k) * 8
     torch.cuda.synchronize()
     e2e_t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
     dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     dist.barrier()
+    t = float(ms.item())
+    slow_gbs = float(slow[0].item())
+    e2e_s = float(e2e_t.item())
+    dist.destroy_process_group()
+    sys.stdout.flush()
+    os.dup2(stdout_fd, 1)
+    os.close(stdout_fd)
     if rank == 0:
-        t = float(ms.item())
         # the slowest rank's screen: its algorithmic bytes over its time
-        rf = roofline(float(slow[0].item()) * screen_s * 1e9, screen_s, None,
-                      run.eng.screen_bits)
+        rf = roofline(slow_gbs * screen_s * 1e9, screen_s, None, run.eng.screen_bits)
         rf["per"] = "slowest rank's screen over its shard"
 
         print(json.dumps({
@@ -571,9 +580,8 @@ def bench_multi(args, rank: int, world: int) -> None:
             "roofline": rf,
             "gpu_launches": launches * world,
             "clocks": clocks,
-            "e2e": {"value": e2e_steps / float(e2e_t.item()), "unit": "iter/s",
+            "e2e": {"value": e2e_steps / e2e_s, "unit": "iter/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "steps": e2e_steps, "per_rank_bytes": True},
             "time": time.strftime("%Y-%m-%dT%H:%M:%S"),
         }), flush=True)
-    dist.destroy_process_group()
