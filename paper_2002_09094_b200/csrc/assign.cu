@@ -96,6 +96,7 @@ struct ScreenParams {
   int32_t* st_cnt;   // candidates kept (kMaxC + 1: overflow) | kHasPost,
   int2* st_cand;     // [n][kMaxC] the candidates (slot, fp32 value bits)
   int rowcap;      // row entries staged in shared memory per pass
+  int cc_bytes = 0;  // counting-sort scratch after the staged row (0: presorted rows)
   int32_t* label32;
   int32_t* slot_of;
   int32_t* q_obj;
@@ -612,7 +613,10 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
   uint16_t* s_pos = reinterpret_cast<uint16_t*>(s_ent + p.rowcap);
   uint8_t* s_lp = reinterpret_cast<uint8_t*>(s_pos + p.rowcap);
   // slot-byte sparse path: a 256-slot scratch per warp (zero between spans)
-  float* s_scr = reinterpret_cast<float*>(s_lp + ((p.rowcap + 15) & ~15));
+  // [chunk][bucket] counts of the in-CTA counting sort (absent when the rows
+  // arrive presorted: the shared-memory footprint decides the L1 carve-out)
+  uint16_t* s_cc = reinterpret_cast<uint16_t*>(s_lp + ((p.rowcap + 15) & ~15));
+  float* s_scr = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(s_cc) + p.cc_bytes);
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -661,7 +665,6 @@ __global__ void __maxnreg__(MAXREG) screen_kernel(ScreenParams p) {
   int nls = (int)(((blk0 + p.cta_blocks - 1) >> 3) - gs0 + 1);
   if (nls > kMaxLocalSpans) nls = kMaxLocalSpans;  // later local spans: masked path
   const int nb = nls + 1;                           // prefix buckets 0..nls
-  __shared__ uint16_t s_cc[kMaxChunks * (kMaxLocalSpans + 1)];  // [chunk][bucket]
   __shared__ int s_cntd[kMaxLocalSpans + 1];  // entries whose prefix covers local span s
   __shared__ int s_next;                      // next span to process (dynamic)
   int64_t c0 = rb;
@@ -1586,6 +1589,7 @@ struct Plan {
   bool tma = false;  // (staged screens removed in round 2; the plan query reports 0)
   int mode = 0;
   size_t smem;
+  size_t cc_bytes = 0;
 };
 
 static int g_passes = 0;  // slot-range passes (0/1 = off; set per launch by the engine)
@@ -1607,8 +1611,16 @@ int choose_warps(int spans, size_t smem) {
   return best_w;
 }
 
+// Counting-sort scratch of the in-CTA row sort: a uint16 per (32-entry chunk,
+// dense-prefix bucket), buckets = the CTA's spans + 1 (<= kMaxLocalSpans + 1).
+size_t cc_bytes_for(int rowcap, int cta_blocks) {
+  int nb = cta_blocks / kSpan + 2;
+  if (nb > kMaxLocalSpans + 1) nb = kMaxLocalSpans + 1;
+  return ((size_t)(rowcap / 32) * nb * sizeof(uint16_t) + 15) & ~(size_t)15;
+}
+
 int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out,
-                bool sparse_scratch = false) {
+                bool sparse_scratch = false, bool presorted = false) {
   const int64_t nblk = ivfkm_bivf_nblk(k);
   Plan pl;
   const bool adaptive = smem_limit <= 0;
@@ -1659,6 +1671,9 @@ int plan_screen(int64_t k, int rowcap, int smem_limit, int rr, Plan* out,
     pl.smem = (size_t)cb * 128 + stage;
     pl.passes = pl.nsplit > 1;
   }
+  // the counting-sort scratch, unless every launch stages presorted rows
+  pl.cc_bytes = (presorted && pl.passes) ? 0 : cc_bytes_for(pl.rowcap, pl.cta_blocks);
+  pl.smem += pl.cc_bytes;
   const int best_w = choose_warps(pl.cta_blocks / pl.rr, pl.smem);
   pl.warps = g_max_warps < best_w ? g_max_warps : best_w;
   if (g_force_warps > 0) pl.warps = g_force_warps;  // tests: any count is valid
@@ -1855,8 +1870,9 @@ struct AssignArgs {
 
 int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
   Plan pl;
+  const bool can_presort = a.ps_t && ivfkm_bivf_nblk(a.k) / kSpan < kPresortBuckets;
   int rc = plan_screen(a.k, g_rowcap, g_smem_limit, g_rr, &pl,
-                       a.slot8 != nullptr && a.screen_bits == 16);
+                       a.slot8 != nullptr && a.screen_bits == 16, can_presort);
   if (rc) return rc;
   ScreenParams sp;
   sp.n_obj = a.n_obj;
@@ -1887,14 +1903,14 @@ int screen_impl(const AssignArgs& a, const AssignWs& w, cudaStream_t st) {
   sp.cta_blocks = pl.cta_blocks;
   sp.nsplit = pl.nsplit;
   sp.rowcap = pl.rowcap;
+  sp.cc_bytes = (int)pl.cc_bytes;
   sp.label32 = w.label32;
   sp.slot_of = w.slot_of;
   sp.q_obj = w.q_obj;
   sp.q_cnt = w.q_cnt;
   sp.q_cid = w.q_cid;
   sp.stats = a.stats;
-  if (pl.passes && a.ps_t && (pl.cta_blocks / pl.rr) > 0 &&
-      ivfkm_bivf_nblk(a.k) / kSpan < kPresortBuckets) {
+  if (pl.passes && can_presort && (pl.cta_blocks / pl.rr) > 0) {
     const int nsp = (int)(ivfkm_bivf_nblk(a.k) / kSpan);
     int2* pt = reinterpret_cast<int2*>(a.ps_t);
     int2* pvv = reinterpret_cast<int2*>(a.ps_v);

@@ -82,6 +82,15 @@ def main():
         key = torch.unique((rank[rows] // B) * D + terms)
         tiles[B] = float(dpre[key % D].sum()) / max(single, 1.0)
     out["dense_span_reads_tiled_fraction"] = tiles
+    # dense-span reads (prefix + dense spans beyond it) by fill: share of the
+    # (object entry, span) reads whose span holds (10 d)%..(10 d + 10)% of its
+    # 256 slots — what a cheaper mid-fill representation could save
+    dn = dense | inpre
+    dec = torch.clamp((cnt * 10) // 256, max=9)
+    wd = (w * dn).flatten()
+    by = torch.zeros(10, dtype=torch.float64, device=h.device).index_add_(0, dec.flatten(), wd)
+    out["dense_reads_by_fill_decile"] = (by / by.sum()).tolist()
+    out["dense_reads_mean_fill"] = float((w * dn * cnt).sum() / (256.0 * (w * dn).sum()))
     hist = torch.bincount(cnt[~inpre & (cnt > 0)].flatten(), minlength=257)[:40].tolist()
     out["masked_nonempty_span_fill_hist"] = hist
     print(json.dumps(out), flush=True)
