@@ -1831,8 +1831,11 @@ extern "C" int ivfkm_set_screen_option(int which, int value) {
 extern "C" int ivfkm_screen_plan(int64_t k, int rowcap, int screen_bits, int32_t* out) {
   if (k < 1 || !out || (screen_bits != 16 && screen_bits != 32)) return IVFKM_E_ARG;
   Plan pl;
+  // as the engine launches it: slot bytes for the fp16 screen's sparse spans
+  // from 16 spans up, presorted rows under slot-range passes
+  const bool slots = screen_bits == 16 && ivfkm_bivf_nblk(k) / kSpan >= 16;
   const int rc = plan_screen(k, rowcap >= 32 ? rowcap / 32 * 32 : g_rowcap, g_smem_limit, g_rr,
-                             &pl);
+                             &pl, slots, /*presorted=*/true);
   if (rc) return rc;
   out[0] = pl.rr;
   out[1] = pl.nsplit;

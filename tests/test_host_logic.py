@@ -332,3 +332,28 @@ def test_l2_model_closed_forms():
     assert math.isinf(L.find_z_star(p, big))
     assert L.llcm_ivf(p, big) == blocks[no > 0].sum()
     assert L.llcm_ivf(p, c) > L.llcm_ivf(p, big)
+
+
+@pytest.mark.parametrize("k,passes,rowcap", [(1000, 1, 512), (10000, 10, 512), (10000, 5, 128),
+                                             (60000, 30, 128)])
+def test_screen_plan_keeps_nine_ctas_under_the_196k_carveout(k, passes, rowcap):
+    """The screen's loads allocate L1 lines while in flight, and the L1 is what
+    the shared-memory carve-out leaves of 256 KB: nine CTAs (the register
+    limit at 56 registers x 128 threads) must fit the 196 KB carve-out, or
+    the driver moves to 228 KB and the screen loses a quarter of its speed
+    (DESIGN.md section 4a).  Plans of BASELINE configs 1-4 (host-side query)."""
+    from paper_2002_09094_b200 import _lib
+
+    lib = _lib.load()
+    out = np.zeros(8, np.int32)
+    lib.ivfkm_set_tuning(rowcap, -1, 0)
+    lib.ivfkm_set_screen_option(1, passes)
+    try:
+        _lib.check(lib.ivfkm_screen_plan(k, rowcap, 16, out.ctypes.data), "plan")
+    finally:
+        lib.ivfkm_set_screen_option(1, 0)
+        lib.ivfkm_set_tuning(1024, -1, 0)
+    warps, dyn, maxreg = int(out[3]), int(out[6]), int(out[7])
+    assert warps <= 4 and maxreg == 56
+    static_and_reserved = 1200 + 1024  # ScreenShared, counters; 1 KB per CTA for the driver
+    assert 9 * (dyn + static_and_reserved) <= 196 * 1024, (dyn, warps)
