@@ -413,6 +413,7 @@ class LloydEngine:
         # stream as soon as the means exist, under the BIVF build and the screen
         self.side = torch.cuda.Stream(device=dev) if self.rankdir is not None and \
             torch.cuda.is_available() else None
+        self._dir_of = None  # the means whose directory the buffer holds (side-stream build)
         # BIVF value arrays, grown on demand and alternated between builds (the
         # means of the previous build keep theirs)
         self._bvbuf = [None, None]
@@ -642,7 +643,7 @@ class LloydEngine:
         if self.rankdir is not None:
             # the directory built on the side stream for these very means, or
             # (another engine's means, a rebuilt buffer) built here
-            pre = dm.dir_ready is not None and getattr(self, "_dir_of", None) is dm
+            pre = dm.dir_ready is not None and self._dir_of is dm
             if pre:
                 torch.cuda.current_stream().wait_event(dm.dir_ready)
             elif self.side is not None:  # the buffer may still be written for other means
